@@ -1,0 +1,342 @@
+"""bench.py — GF(2^e) bitsliced-Karatsuba matmul on B200: effective GF(2) Tbit-op/s.
+
+Default workload (BASELINE.json config 3): F_256 (e=8, f=0x11d), C = A.B with A, B
+16384 x 16384 per GPU, entries from the reference generator (seeds A=1, B=2), sliced planes
+resident in HBM.  One step = one ``karatsuba_mul`` (mzd_slice_mul): operand combinations +
+the fused tcgen05 product/combine/fold kernel.  Metric: K(e) * 2*m*k*n GF(2) bit-ops per
+second (K(8) = 27).  Multi-GPU (torchrun): each rank owns a 16384-row block of
+C (weak scaling, no data-path collective); B is generated on rank 0 and broadcast once with
+NCCL before timing.  ``--config 5`` runs the 65536^3 case sharded by C row-blocks instead.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3|1|2|4|5]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+K_OF_E = {2: 3, 3: 6, 4: 9, 5: 15, 6: 18, 7: 24, 8: 27, 9: 39, 10: 45}
+DEFAULT_F = {2: 0x7, 3: 0xB, 4: 0x13, 5: 0x25, 6: 0x43, 7: 0x83, 8: 0x11D, 9: 0x211, 10: 0x409}
+
+
+def workload(config: int, e_override: int | None, world: int):
+    """(name, e, m_per_rank, k, n, accumulate, scaling)"""
+    if config == 1:
+        return ("F4 C=A.B 1024^3 (BASELINE config 1)", 2, 1024, 1024, 1024, False, "weak")
+    if config == 2:
+        return ("F16 C=A.B 4096^3 (BASELINE config 2)", 4, 4096, 4096, 4096, False, "weak")
+    if config == 3:
+        return ("F256 C=A.B 16384^3 per GPU (BASELINE config 3)", 8, 16384, 16384, 16384, False, "weak")
+    if config == 4:
+        e = e_override or 8
+        return (f"F(2^{e}) C+=A.B 65536x256.256x65536 (BASELINE config 4)", e, 65536, 256, 65536, True, "weak")
+    if config == 5:
+        if 65536 % world:
+            raise SystemExit("config 5 needs world size dividing 65536")
+        return ("F256 C=A.B 65536^3 sharded by C row-blocks (BASELINE config 5)", 8, 65536 // world, 65536,
+                65536, False, "strong")
+    raise SystemExit(f"unknown config {config}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p, "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def cpu_sample(e: int, k: int, n: int, rows: int, threads: int = 0):
+    """Oracle ("port") karatsuba on C rows [0, rows) — a bounded slice of the same workload."""
+    import oracle
+
+    f = DEFAULT_F[e]
+    a = oracle.sliced_random(e, rows, k, 1)
+    b = oracle.sliced_random(e, k, n, 2)
+    t0 = time.perf_counter()
+    oracle.karatsuba(e, f, a, b, rows, k, n, nthreads=threads)
+    dt = time.perf_counter() - t0
+    ops = K_OF_E[e] * 2.0 * rows * k * n
+    return ops / dt / 1e12, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+
+    name, e, m, k, n, acc, scaling = workload(args.config, args.e, 1)
+    rows = args.cpu_rows or (256 if k * n >= 16384 * 16384 else min(m, 1024))
+    cores = oracle.max_threads()
+    vals = []
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_sample(e, k, n, min(rows, 64))
+    for _ in range(args.steps):
+        v, dt = cpu_sample(e, k, n, rows)
+        vals.append((v, dt))
+    v = statistics.median(x[0] for x in vals)
+    dt = statistics.median(x[1] for x in vals)
+    sample = (f"rows 0..{rows - 1} of C ({rows}x{k}x{n}, e={e}) through oracle.karatsuba "
+              f"(C port of the reference poly_mul._kara + M4RM), {cores} threads")
+    line = {
+        "metric": "effective GF(2) Tbit-op/s (K(e)*2mkn / time)", "value": round(v, 4), "unit": "Tbit-op/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u64 (GF(2) bit-planes)",
+        "data": "synthetic (reference splitmix64 generator, seeds A=1 B=2)", "impl": "reference",
+        "config": {"workload": name, "e": e, "m": m, "k": k, "n": n, "f": hex(DEFAULT_F[e])},
+        "cpu_baseline": {"value": round(v, 4), "unit": "Tbit-op/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": round(v, 4), "unit": "Tbit-op/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1111_6900_b200 as g
+    from paper_1111_6900_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    name, e, m, k, n, acc, scaling = workload(args.config, args.e, world)
+    ctx = g.field_new(e)
+    K = g.count_products(e)
+    ops_rank = K * 2.0 * m * k * n
+    backend = args.backend
+
+    # ---- inputs resident in HBM: A row-block (rank's rows of the global matrix), B broadcast ----
+    row0 = rank * m
+    A = g.SlicedMatrix.random(ctx, m, k, 1, row0=row0, gcols=k)
+    if rank == 0 or world == 1:
+        B = g.SlicedMatrix.random(ctx, k, n, 2)
+    else:
+        B = g.SlicedMatrix(ctx, k, n, torch.empty((e, k, g.words_for(n)), dtype=torch.int64, device=dev))
+    if world > 1:
+        dist.broadcast(B.planes, src=0)  # the one collective: B over NVLink (NCCL)
+    C = (g.SlicedMatrix.random(ctx, m, n, 3, row0=row0, gcols=n) if acc
+         else g.SlicedMatrix(ctx, m, n, torch.empty((e, m, g.words_for(n)), dtype=torch.int64, device=dev)))
+    torch.cuda.synchronize()
+
+    def step():
+        if acc:
+            g.addmul(C, A, B, backend=backend)
+        else:
+            g.karatsuba_mul(A, B, backend=backend)
+        return _lib.last_launch_count()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: device events, barrier + sync on both sides, max over ranks ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    _lib.profile_enable(True)
+    _lib.profile_read()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(st)
+    launches = 0
+    for _ in range(args.steps):
+        launches += step()
+    ev1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    prod_ms, prod_launches = _lib.profile_read()
+    _lib.profile_enable(False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms, prod_ms / max(prod_launches, 1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, prod_ms_max = float(t[0]), float(t[1])
+    value = world * ops_rank / (ms_max * 1e-3) / 1e12
+
+    # ---- e2e through the public packed API with host buffers (pinned), per step:
+    #      H2D of A, B packed; karatsuba_mul_packed (slice -> product -> cling); D2H of C packed ----
+    e2e = None
+    if not args.no_e2e:
+        Ap = g.PackedMatrix.random(ctx, m, k, 1) if world == 1 else g.cling(A)
+        Bp = g.cling(B)
+        hA = torch.empty(Ap.storage.words.shape, dtype=torch.int64, pin_memory=True)
+        hB = torch.empty(Bp.storage.words.shape, dtype=torch.int64, pin_memory=True)
+        hA.copy_(Ap.storage.words)
+        hB.copy_(Bp.storage.words)
+        wpc = g.words_for(n * g.pack_width(e))
+        hC = torch.empty((m, wpc), dtype=torch.int64, pin_memory=True)
+        dA = g.PackedMatrix(ctx, m, k, g.BitMatrix(m, k * g.pack_width(e), torch.empty_like(Ap.storage.words)))
+        dB = g.PackedMatrix(ctx, k, n, g.BitMatrix(k, n * g.pack_width(e), torch.empty_like(Bp.storage.words)))
+        del Ap, Bp
+
+        def e2e_step():
+            dA.storage.words.copy_(hA, non_blocking=True)
+            dB.storage.words.copy_(hB, non_blocking=True)
+            Cp = g.karatsuba_mul_packed(dA, dB, backend=backend)
+            hC.copy_(Cp.storage.words, non_blocking=True)
+
+        for _ in range(max(1, args.warmup // 2)):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(st)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(world * ops_rank / (float(te[0]) * 1e-3) / 1e12, 4), "unit": "Tbit-op/s",
+               "h2d_bytes_per_step": int(hA.numel() * 8 + hB.numel() * 8),
+               "d2h_bytes_per_step": int(hC.numel() * 8), "ms_per_step": round(float(te[0]), 3),
+               "path": "karatsuba_mul_packed (slice K1 + combos K3 + product K4/K5 + cling K2) with pinned host I/O"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    pk, pk_kind = peaks()
+    int8_peak = 2.0 * pk["bf16_tflops"]  # sm_100: dense int8 tensor rate = 2x dense bf16
+    achieved = ops_rank / (prod_ms_max * 1e-3) / 1e12  # GF(2) bit-ops == int8 tensor ops (1 MAC = 2 ops)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"config{args.config}")
+        except (OSError, ValueError):
+            traffic = None
+    line = {
+        "metric": "effective GF(2) Tbit-op/s (K(e)*2mkn / time)", "value": round(value, 4), "unit": "Tbit-op/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8 (0/1 bytes on tcgen05 kind::i8, s32 acc)",
+        "data": "synthetic (reference splitmix64 generator, seeds A=1 B=2 C0=3)",
+        "config": {"workload": name, "e": e, "f": hex(ctx.f), "m_per_gpu": m, "k": k, "n": n,
+                   "gf2_products": K, "backend": backend or "tc", "parallelism": f"C row-blocks x{world}",
+                   "l2": "inputs larger than L2 (A planes + combos >> 126 MB)"},
+        "time_s": round(ms_max / 1e3, 6),
+        "gpu_launches": launches,
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(int8_peak, 1),
+                     "unit": "TFLOP/s", "frac": round(achieved / int8_peak, 4), "traffic": traffic,
+                     "kernel": _lib.last_product_kernel(), "kernel_ms": round(prod_ms_max, 4),
+                     "peak_basis": f"int8 dense = 2 x {pk_kind} bf16 {pk['bf16_tflops']} TF/s (MEASURED_PEAKS.json)",
+                     "ops_per_launch": ops_rank},
+        "clocks": clocks,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline:
+        import oracle
+
+        rows = args.cpu_rows or (256 if k * n >= 16384 * 16384 else min(m, 1024))
+        v, dt = cpu_sample(e, k, n, rows)
+        line["cpu_baseline"] = {"value": round(v, 4), "unit": "Tbit-op/s", "cores": oracle.max_threads(),
+                                "kind": "port",
+                                "sample": f"rows 0..{rows - 1} of C ({rows}x{k}x{n}, e={e}) via oracle.karatsuba, "
+                                          f"{dt:.2f} s"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--e", type=int, default=None, help="field degree for config 4")
+    ap.add_argument("--backend", default=None, choices=[None, "tc", "m4rm"])
+    ap.add_argument("--cpu-rows", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

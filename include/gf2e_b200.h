@@ -1,0 +1,156 @@
+/*
+ * gf2e_b200.h — C ABI of libgf2e_b200.so, the B200 (sm_100a) implementation of the
+ * GF(2^e) bitsliced-Karatsuba hot path of the M4RIE paper (arxiv 1111.6900), reference
+ * package gf2elin (/root/reference/pkg/src/gf2elin).
+ *
+ * Plain pointers and sizes only.  Every pointer argument named *_dev is a CUDA device
+ * pointer; `stream` is a cudaStream_t passed as void*.  All calls are stream-ordered and
+ * asynchronous (no hidden host synchronisation); they return 0 on success and a nonzero
+ * GF2E_E* status otherwise, with a thread-local message in gf2e_last_error().
+ *
+ * Layouts (identical to the reference, mat_gf2.py:3-7 and mat_packed.py:1-13):
+ *   plane  (BitMatrix / mzd_t)   : rows x ld uint64 words, entry (i, j) = bit j%64 of word
+ *                                  [i*ld + j/64]; bits past ncols are zero.
+ *   plane stack (SlicedMatrix /  : e planes, plane t at base + t*pstride words.
+ *                mzd_slice_t)
+ *   packed (PackedMatrix / mzed_t): rows x ldp words, element (i, j) in bits
+ *                                  [j*w, j*w+e) of the packed row, w = gf2e_pack_width(e),
+ *                                  pad bits zero.
+ *
+ * Each entry point names the reference interface it replaces (file:line in gf2elin).
+ */
+#ifndef GF2E_B200_H
+#define GF2E_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define GF2E_OK 0
+#define GF2E_EINVAL 1   /* invalid argument (maps to ValueError in the Python shim) */
+#define GF2E_ECUDA 2    /* CUDA runtime / launch error (RuntimeError)            */
+#define GF2E_ENOMEM 3   /* workspace too small                                   */
+#define GF2E_ENODEV 4   /* no sm_100 device                                      */
+
+/* gf2e_slice_mul flags */
+#define GF2E_ACCUMULATE 1u   /* C ^= A*B (addmul) instead of C = A*B              */
+#define GF2E_BACKEND_TC 0u   /* K4 on tcgen05 kind::i8 tensor cores (default)     */
+#define GF2E_BACKEND_M4RM 2u /* K4 as M4RM Gray tables in shared memory (INT pipe) */
+
+/* Last error message of the calling thread ("" if none). */
+const char *gf2e_last_error(void);
+
+/* Library version string. */
+const char *gf2e_version(void);
+
+/* mat_packed.pack_width (mat_packed.py:26-33): smallest divisor of 64 >= e; -1 if e out of 2..10. */
+int gf2e_pack_width(int e);
+
+/*
+ * Karatsuba schedule for GF(2^e) mod f — the symbolic replay of _kara + reduce_mod_f
+ * (poly_mul.py:166-242).  Replaces count_products (poly_mul.py:262-272) and the
+ * MulCounters bookkeeping (poly_mul.py:32-43).
+ *   n_products       <- K(e) (3, 6, 9, 15, 18, 24, 27, 39, 45 for the default f)
+ *   subsets[t]       <- bitmask of input planes XOR-ed into operand t (t < K(e), cap 64)
+ *   outmap[j]        <- bitmask over products folded into output plane j (j < e)
+ *   counters[3]      <- gf2_matmul_count, additions, peak_live_products
+ * Any output pointer may be NULL.  Fails (GF2E_EINVAL) if e is outside 2..10 or f is not
+ * an irreducible polynomial of degree e (gf2e.py:125-137).
+ */
+int gf2e_schedule(int e, uint32_t f, int *n_products, uint64_t *subsets, uint64_t *outmap,
+                  int64_t *counters);
+
+/*
+ * K7 generator: counter-mode splitmix64 (rng.py:20-35) exactly as
+ * PackedMatrix.random (mat_packed.py:253-265), for the window of rows
+ * [row0, row0+rows) and columns [col0, col0+cols) of a matrix with gcols columns
+ * (element (i, j) uses stream index (row0+i)*gcols + col0 + j).
+ * gf2e_random_packed writes packed words; gf2e_random_sliced writes e planes
+ * (= slice_packed of the same matrix).
+ */
+int gf2e_random_packed(int e, int64_t rows, int64_t cols, uint64_t seed, int64_t row0,
+                       int64_t col0, int64_t gcols, uint64_t *out_dev, int64_t ldp, void *stream);
+int gf2e_random_sliced(int e, int64_t rows, int64_t cols, uint64_t seed, int64_t row0,
+                       int64_t col0, int64_t gcols, uint64_t *planes_dev, int64_t ld,
+                       int64_t pstride, void *stream);
+
+/* BitMatrix.random (mat_gf2.py:194-206): words[i, w] = word_stream(seed)[i*ld_ref + w]
+ * with ld_ref = ceil(ncols/64), tail bits past ncols cleared. */
+int gf2e_random_words(int64_t rows, int64_t ncols, uint64_t seed, uint64_t *out_dev, int64_t ld,
+                      void *stream);
+
+/* K1 slice_packed (mat_sliced.py:97-101): packed -> e planes (mzed -> mzd_slice). */
+int gf2e_slice(int e, int64_t rows, int64_t cols, const uint64_t *packed_dev, int64_t ldp,
+               uint64_t *planes_dev, int64_t ld, int64_t pstride, void *stream);
+
+/* K2 cling (mat_sliced.py:104-106): e planes -> packed, pad bits zero (mzd_slice -> mzed). */
+int gf2e_cling(int e, int64_t rows, int64_t cols, const uint64_t *planes_dev, int64_t ld,
+               int64_t pstride, uint64_t *packed_dev, int64_t ldp, void *stream);
+
+/* Plane / packed addition X ^= Y over rows x nwords words (BitMatrix.iadd mat_gf2.py:161-164,
+ * PackedMatrix.iadd mat_packed.py:180-190, SlicedMatrix.add mat_sliced.py:69-72). */
+int gf2e_xor(uint64_t *x_dev, int64_t ldx, const uint64_t *y_dev, int64_t ldy, int64_t rows,
+             int64_t nwords, void *stream);
+
+/*
+ * reduce_mod_f (poly_mul.py:223-242) on device: 2e-1 planes (plane d at base + d*pstride)
+ * folded in place so planes 0..e-1 hold the reduced result.
+ */
+int gf2e_reduce_mod_f(int e, uint32_t f, uint64_t *planes_dev, int64_t rows, int64_t nwords,
+                      int64_t ld, int64_t pstride, void *stream);
+
+/*
+ * Workspace bytes needed by gf2e_slice_mul / gf2e_plane_mul for this shape.
+ * (Operand combinations of the Karatsuba schedule in the tensor-core layout.)
+ */
+int64_t gf2e_slice_mul_workspace(int e, uint32_t f, int64_t m, int64_t k, int64_t n,
+                                 uint32_t flags);
+int64_t gf2e_plane_mul_workspace(int64_t m, int64_t k, int64_t n, uint32_t flags);
+
+/*
+ * ★ The hot path: mzd_slice_mul / mzd_slice_addmul.
+ * Replaces karatsuba_mul (poly_mul.py:245-259) and the addmul pattern
+ * X.xor_window(0, 0, karatsuba_mul(A, B)) (ple_echelon.py:130-136,259).
+ *   A: e planes m x k (lda words/row, plane stride pa)
+ *   B: e planes k x n (ldb, pb)
+ *   C: e planes m x n (ldc, pc); C = A*B, or C ^= A*B with GF2E_ACCUMULATE.
+ * C must not overlap A or B.  workspace: >= gf2e_slice_mul_workspace(...) bytes of device
+ * memory (256-byte aligned).
+ */
+int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, int64_t pa,
+                   const uint64_t *B_dev, int64_t ldb, int64_t pb, uint64_t *C_dev, int64_t ldc,
+                   int64_t pc, int64_t m, int64_t k, int64_t n, uint32_t flags, void *workspace,
+                   int64_t workspace_bytes, void *stream);
+
+/*
+ * GF(2) plane product mzd_mul / mzd_addmul (mat_gf2.mul, mat_gf2.py:425-455):
+ * C = A*B or C ^= A*B (GF2E_ACCUMULATE).  A m x k, B k x n, C m x n.
+ */
+int gf2e_plane_mul(const uint64_t *A_dev, int64_t lda, const uint64_t *B_dev, int64_t ldb,
+                   uint64_t *C_dev, int64_t ldc, int64_t m, int64_t k, int64_t n, uint32_t flags,
+                   void *workspace, int64_t workspace_bytes, void *stream);
+
+/*
+ * Instrumentation: number of kernels the last successful call on this thread launched,
+ * and the name of the product kernel it used.
+ */
+int gf2e_last_launch_count(void);
+const char *gf2e_last_product_kernel(void);
+
+/*
+ * Live kernel timing for bench.py: while enabled, every product-kernel launch is bracketed
+ * by CUDA events recorded on the launching stream.  gf2e_profile_read synchronises those
+ * events and returns the summed duration (ms) and the number of launches, then clears.
+ */
+int gf2e_profile_enable(int on);
+int gf2e_profile_read(double *total_ms, int *launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GF2E_B200_H */

@@ -1,0 +1,65 @@
+"""Device plumbing: CUDA device/stream handles and the workspace cache.
+
+PyTorch is used only for device memory and streams; all arithmetic runs in
+libgf2e_b200.so.  There is no CPU path: without an sm_100 GPU every call raises.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1111_6900_b200 needs a CUDA (sm_100) device; there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: torch.Tensor) -> int:
+    return t.data_ptr() if t.numel() else 0
+
+
+def empty_words(shape, device=None) -> torch.Tensor:
+    return torch.empty(shape, dtype=torch.int64, device=device or require_cuda())
+
+
+def zeros_words(shape, device=None) -> torch.Tensor:
+    return torch.zeros(shape, dtype=torch.int64, device=device or require_cuda())
+
+
+def to_device_words(arr: np.ndarray, device=None) -> torch.Tensor:
+    a = np.ascontiguousarray(arr, dtype=np.uint64)
+    return torch.from_numpy(a.view(np.int64)).to(device or require_cuda())
+
+
+def to_host_words(t: torch.Tensor) -> np.ndarray:
+    return t.detach().contiguous().cpu().numpy().view(np.uint64)
+
+
+class _Workspace(threading.local):
+    """Per-thread, per-(device, stream) scratch buffer that only grows."""
+
+    def __init__(self):
+        self.bufs: dict[tuple[int, int], torch.Tensor] = {}
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        dev = require_cuda()
+        key = (dev.index, stream_handle())
+        buf = self.bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+            self.bufs[key] = buf
+        return buf
+
+    def clear(self) -> None:
+        self.bufs.clear()
+
+
+workspace = _Workspace()

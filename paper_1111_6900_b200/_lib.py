@@ -1,0 +1,107 @@
+"""ctypes binding of libgf2e_b200.so (the C ABI declared in include/gf2e_b200.h).
+
+There is no CPU fallback: if the shared library is missing, or there is no sm_100 GPU,
+every device entry point raises.  Status codes map to the reference's exception types:
+GF2E_EINVAL -> ValueError (poly_mul.py:248-253, gf2e.py:126-137), everything else ->
+RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgf2e_b200.so")
+
+GF2E_OK, GF2E_EINVAL, GF2E_ECUDA, GF2E_ENOMEM, GF2E_ENODEV = 0, 1, 2, 3, 4
+ACCUMULATE = 1
+BACKEND_TC = 0
+BACKEND_M4RM = 2
+
+_I64 = ctypes.c_int64
+_U64 = ctypes.c_uint64
+_P = ctypes.c_void_p
+_INT = ctypes.c_int
+_U32 = ctypes.c_uint32
+
+# name -> (restype, argtypes); mirrors include/gf2e_b200.h one for one
+SIGNATURES = {
+    "gf2e_last_error": (ctypes.c_char_p, []),
+    "gf2e_version": (ctypes.c_char_p, []),
+    "gf2e_pack_width": (_INT, [_INT]),
+    "gf2e_schedule": (_INT, [_INT, _U32, ctypes.POINTER(_INT), ctypes.POINTER(_U64), ctypes.POINTER(_U64),
+                             ctypes.POINTER(_I64)]),
+    "gf2e_random_packed": (_INT, [_INT, _I64, _I64, _U64, _I64, _I64, _I64, _P, _I64, _P]),
+    "gf2e_random_sliced": (_INT, [_INT, _I64, _I64, _U64, _I64, _I64, _I64, _P, _I64, _I64, _P]),
+    "gf2e_random_words": (_INT, [_I64, _I64, _U64, _P, _I64, _P]),
+    "gf2e_slice": (_INT, [_INT, _I64, _I64, _P, _I64, _P, _I64, _I64, _P]),
+    "gf2e_cling": (_INT, [_INT, _I64, _I64, _P, _I64, _I64, _P, _I64, _P]),
+    "gf2e_xor": (_INT, [_P, _I64, _P, _I64, _I64, _I64, _P]),
+    "gf2e_reduce_mod_f": (_INT, [_INT, _U32, _P, _I64, _I64, _I64, _I64, _P]),
+    "gf2e_slice_mul_workspace": (_I64, [_INT, _U32, _I64, _I64, _I64, _U32]),
+    "gf2e_plane_mul_workspace": (_I64, [_I64, _I64, _I64, _U32]),
+    "gf2e_slice_mul": (_INT, [_INT, _U32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64,
+                              _U32, _P, _I64, _P]),
+    "gf2e_plane_mul": (_INT, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _U32, _P, _I64, _P]),
+    "gf2e_last_launch_count": (_INT, []),
+    "gf2e_last_product_kernel": (ctypes.c_char_p, []),
+    "gf2e_profile_enable": (_INT, [_INT]),
+    "gf2e_profile_read": (_INT, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_INT)]),
+}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the in-tree shared library (built by __graft_entry__.build / csrc/Makefile)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"libgf2e_b200.so not found at {LIB_PATH}; build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    return load().gf2e_last_error().decode()
+
+
+def check(rc: int, what: str) -> None:
+    if rc == GF2E_OK:
+        return
+    msg = last_error()
+    if rc == GF2E_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(f"{what}: {msg} (status {rc})")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def last_launch_count() -> int:
+    return int(load().gf2e_last_launch_count())
+
+
+def profile_enable(on: bool) -> None:
+    load().gf2e_profile_enable(1 if on else 0)
+
+
+def profile_read() -> tuple[float, int]:
+    """(summed product-kernel ms, launches) since the last read; synchronises the events."""
+    ms = ctypes.c_double()
+    n = ctypes.c_int()
+    check(load().gf2e_profile_read(ctypes.byref(ms), ctypes.byref(n)), "gf2e_profile_read")
+    return ms.value, n.value
+
+
+def last_product_kernel() -> str:
+    return load().gf2e_last_product_kernel().decode()

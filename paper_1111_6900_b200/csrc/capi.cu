@@ -1,0 +1,507 @@
+// capi.cu — the extern "C" boundary of libgf2e_b200.so (declared in include/gf2e_b200.h):
+// argument validation with the reference's error semantics, the native Karatsuba
+// schedule, workspace carving, and the launch sequence of the hot path.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gf2e_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace gf2e;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+thread_local const char *g_kernel = "";
+
+// live product-kernel timing (gf2e_profile_*)
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_events;
+
+struct ProfScope {
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    explicit ProfScope(cudaStream_t s) : st(s) {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        if (!g_prof_on) return;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, st);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        cudaEventRecord(b, st);
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        g_prof_events.emplace_back(a, b);
+    }
+};
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    return fail(GF2E_ECUDA, "CUDA error in %s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(expr, what)                               \
+    do {                                             \
+        cudaError_t _e = (expr);                     \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+        ++g_launches;                                \
+    } while (0)
+
+// ---- field checks (gf2e.py:44-71, 125-137) ---------------------------------------------
+int poly_degree(uint64_t p) { return p ? 63 - __builtin_clzll(p) : -1; }
+uint64_t poly_mod(uint64_t a, uint64_t m) {
+    int dm = poly_degree(m);
+    while (poly_degree(a) >= dm) a ^= m << (poly_degree(a) - dm);
+    return a;
+}
+bool is_irreducible(uint64_t f) {
+    int d = poly_degree(f);
+    if (d < 1) return false;
+    if (d == 1) return true;
+    if ((f & 1) == 0) return false;
+    for (uint64_t g = 2; g < (1ULL << (d / 2 + 1)); ++g)
+        if (poly_degree(g) >= 1 && poly_mod(f, g) == 0) return false;
+    return true;
+}
+
+int check_field(int e, uint32_t f) {
+    if (e < 2 || e > 10) return fail(GF2E_EINVAL, "extension degree must be in 2..10, got %d", e);
+    if (poly_degree(f) != e)
+        return fail(GF2E_EINVAL, "modulus 0x%x has degree %d, expected %d", f, poly_degree(f), e);
+    if (!is_irreducible(f)) return fail(GF2E_EINVAL, "modulus 0x%x is not irreducible over GF(2)", f);
+    return GF2E_OK;
+}
+
+// ---- Karatsuba schedule: symbolic replay of poly_mul.py:128-242 -------------------------
+struct Schedule {
+    std::vector<uint64_t> subsets;  // per product: bitmask of input planes
+    std::vector<uint64_t> outmap;   // per output plane: bitmask of products
+    int64_t counters[3];            // gf2_matmul_count, additions, peak_live_products
+};
+
+struct Replay {
+    std::vector<uint64_t> subsets;
+    int64_t additions = 0, live = 0, peak = 0;
+    void grab(int64_t k) {
+        live += k;
+        if (live > peak) peak = live;
+    }
+    uint64_t base(uint64_t a) {  // poly_mul.py:146-150
+        subsets.push_back(a);
+        grab(1);
+        return 1ULL << (subsets.size() - 1);
+    }
+    std::vector<uint64_t> add_lists(std::vector<uint64_t> xs, std::vector<uint64_t> ys) {  // 153-163
+        if (xs.size() < ys.size()) std::swap(xs, ys);
+        for (size_t i = 0; i < ys.size(); ++i) xs[i] ^= ys[i];
+        additions += (int64_t)ys.size();
+        return xs;
+    }
+    std::vector<uint64_t> kara(const std::vector<uint64_t> &a) {  // 166-220 (a == b symbolically)
+        const size_t ka = a.size();
+        if (ka == 1) return {base(a[0])};
+        if (ka == 3) {
+            uint64_t d0 = base(a[0]), d1 = base(a[1]), d2 = base(a[2]);
+            uint64_t d01 = base(a[0] ^ a[1]), d02 = base(a[0] ^ a[2]), d12 = base(a[1] ^ a[2]);
+            additions += 6 + 7;
+            live -= 6;
+            grab(5);
+            return {d0, d01 ^ d0 ^ d1, d02 ^ d0 ^ d1 ^ d2, d12 ^ d1 ^ d2, d2};
+        }
+        const size_t h = (ka + 1) / 2;
+        std::vector<uint64_t> alo(a.begin(), a.begin() + h), ahi(a.begin() + h, a.end());
+        std::vector<uint64_t> lo = kara(alo), hi = kara(ahi);
+        std::vector<uint64_t> mid = kara(add_lists(alo, ahi));
+        add_lists(alo, ahi);  // the B-side _add_lists of poly_mul.py:201 (counted, same subsets)
+        for (size_t i = 0; i < lo.size(); ++i) mid[i] ^= lo[i];
+        for (size_t i = 0; i < hi.size(); ++i) mid[i] ^= hi[i];
+        additions += (int64_t)(lo.size() + hi.size());
+        std::vector<uint64_t> out(2 * ka - 1, 0);
+        for (size_t i = 0; i < lo.size(); ++i) out[i] ^= lo[i];
+        for (size_t i = 0; i < mid.size(); ++i) out[h + i] ^= mid[i];
+        for (size_t i = 0; i < hi.size(); ++i) out[2 * h + i] ^= hi[i];
+        additions += (int64_t)(lo.size() + mid.size() + hi.size());
+        live -= (int64_t)(lo.size() + hi.size() + mid.size());
+        grab((int64_t)out.size());
+        return out;
+    }
+};
+
+std::mutex g_sched_mu;
+std::map<std::pair<int, uint32_t>, Schedule> g_sched_cache;
+
+const Schedule &get_schedule(int e, uint32_t f) {
+    std::lock_guard<std::mutex> lk(g_sched_mu);
+    auto key = std::make_pair(e, f);
+    auto it = g_sched_cache.find(key);
+    if (it != g_sched_cache.end()) return it->second;
+    Replay r;
+    std::vector<uint64_t> planes(e);
+    for (int i = 0; i < e; ++i) planes[i] = 1ULL << i;
+    std::vector<uint64_t> gamma = r.kara(planes);
+    Schedule s;
+    s.subsets = r.subsets;
+    s.counters[0] = (int64_t)r.subsets.size();
+    s.counters[2] = r.peak;
+    // reduce_mod_f (poly_mul.py:223-242) on symbols
+    std::vector<uint64_t> work(2 * e - 1);
+    for (int d = 0; d < 2 * e - 1; ++d) work[d] = 1ULL << d;
+    int64_t adds = r.additions;
+    for (int d = 2 * e - 2; d >= e; --d)
+        for (int k = 0; k < e; ++k)
+            if ((f >> k) & 1u) {
+                work[d - e + k] ^= work[d];
+                ++adds;
+            }
+    s.counters[1] = adds;
+    s.outmap.assign(e, 0);
+    for (int j = 0; j < e; ++j)
+        for (int d = 0; d < 2 * e - 1; ++d)
+            if ((work[j] >> d) & 1ULL) s.outmap[j] ^= gamma[d];
+    return g_sched_cache.emplace(key, s).first->second;
+}
+
+Sched to_kernel_sched(int e, const Schedule &S) {
+    Sched k;
+    memset(&k, 0, sizeof(k));
+    k.e = e;
+    k.nout = e;
+    k.nprod = (int)S.subsets.size();
+    for (int t = 0; t < k.nprod; ++t) {
+        k.subset[t] = (uint16_t)S.subsets[t];
+        uint16_t m = 0;
+        for (int j = 0; j < e; ++j)
+            if ((S.outmap[j] >> t) & 1ULL) m |= (uint16_t)(1u << j);
+        k.outmask[t] = m;
+    }
+    return k;
+}
+
+Sched plane_sched() {
+    Sched k;
+    memset(&k, 0, sizeof(k));
+    k.e = 1;
+    k.nout = 1;
+    k.nprod = 1;
+    k.subset[0] = 1;
+    k.outmask[0] = 1;
+    return k;
+}
+
+// ---- device check ---------------------------------------------------------------------
+int check_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(GF2E_ENODEV, "no CUDA device: %s", cudaGetErrorString(e));
+    int major = 0;
+    e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e != cudaSuccess) return fail(GF2E_ENODEV, "cannot query device: %s", cudaGetErrorString(e));
+    if (major != 10) return fail(GF2E_ENODEV, "libgf2e_b200 needs an sm_100 (B200) device, found sm_%d", major * 10);
+    return GF2E_OK;
+}
+
+int check_mat(const void *p, int64_t rows, int64_t cols_words, int64_t ld, const char *name) {
+    if (rows < 0 || cols_words < 0) return fail(GF2E_EINVAL, "matrix dimensions must be non-negative");
+    if (rows > 0 && cols_words > 0) {
+        if (!p) return fail(GF2E_EINVAL, "%s is NULL", name);
+        if (ld < cols_words) return fail(GF2E_EINVAL, "%s: row stride %lld < %lld words", name, (long long)ld,
+                                         (long long)cols_words);
+    }
+    return GF2E_OK;
+}
+
+// ---- workspace layout -----------------------------------------------------------------
+struct Layout {
+    int64_t m_pad, n_pad, k_pad, kwords;
+    int64_t a_pstride, b_pstride;  // words
+    int64_t a_bytes, b_bytes, total;
+};
+
+int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
+
+Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags) {
+    Layout L;
+    if (flags & GF2E_BACKEND_M4RM) {
+        L.m_pad = round_up(m, kM4BM);
+        L.n_pad = round_up(n, kM4BN);
+        L.k_pad = round_up(k, kM4KPAD);
+        L.kwords = L.k_pad / 64;
+        L.a_pstride = L.m_pad * L.kwords;
+        L.b_pstride = L.k_pad * (L.n_pad / 64);
+    } else {
+        L.m_pad = round_up(m, kTcBM);
+        L.n_pad = round_up(n, kTcBN);
+        L.k_pad = round_up(k, kTcBK);
+        L.kwords = L.k_pad / 64;
+        L.a_pstride = L.m_pad * L.kwords;
+        L.b_pstride = L.n_pad * L.kwords;
+    }
+    L.a_bytes = align256((int64_t)nprod * L.a_pstride * 8);
+    L.b_bytes = align256((int64_t)nprod * L.b_pstride * 8);
+    L.total = L.a_bytes + L.b_bytes;
+    return L;
+}
+
+// The shared launch sequence: K3 combos -> fused K4/K5 product.
+int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, const uint64_t *B, int64_t ldb,
+                int64_t pb, uint64_t *C, int64_t ldc, int64_t pc, int64_t m, int64_t k, int64_t n, uint32_t flags,
+                void *ws, int64_t ws_bytes, cudaStream_t st) {
+    g_launches = 0;
+    const bool acc = (flags & GF2E_ACCUMULATE) != 0;
+    const int64_t nw = words_for(n);
+    if (m == 0 || n == 0) return GF2E_OK;
+    if (k == 0) {  // empty inner dimension: product is zero (mat_gf2.py:352-354)
+        if (!acc)
+            for (int j = 0; j < ks.nout; ++j)
+                CK(cudaMemset2DAsync(C + j * pc, ldc * 8, 0, nw * 8, m, st), "cudaMemset2DAsync");
+        return GF2E_OK;
+    }
+    Layout L = layout_for(ks.nprod, m, k, n, flags);
+    if (ws_bytes < L.total)
+        return fail(GF2E_ENOMEM, "workspace too small: %lld < %lld bytes", (long long)ws_bytes, (long long)L.total);
+    if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255))
+        return fail(GF2E_EINVAL, "workspace must be a 256-byte aligned device pointer");
+    uint64_t *Ac = static_cast<uint64_t *>(ws);
+    uint64_t *Bx = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + L.a_bytes);
+    CK(launch_combos_rows(ks, A, lda, pa, m, k, Ac, L.kwords, L.a_pstride, L.m_pad, L.kwords, st), "combos(A)");
+    if (flags & GF2E_BACKEND_M4RM) {
+        const int64_t nwp = L.n_pad / 64;
+        CK(launch_combos_rows(ks, B, ldb, pb, k, n, Bx, nwp, L.b_pstride, L.k_pad, nwp, st), "combos(B)");
+        if (!acc)
+            for (int j = 0; j < ks.nout; ++j)
+                CK(cudaMemset2DAsync(C + j * pc, ldc * 8, 0, nw * 8, m, st), "cudaMemset2DAsync");
+        M4rmArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, nwp, L.k_pad, m, n, L.m_pad, L.n_pad, C, ldc, pc};
+        ProfScope prof(st);
+        CK(launch_product_m4rm(ks, a, st), "product_m4rm");
+        g_kernel = "k_product_m4rm";
+    } else {
+        CK(launch_combos_bt(ks, B, ldb, pb, k, n, Bx, L.kwords, L.b_pstride, L.kwords, L.n_pad / 64, st),
+           "combos(B^T)");
+        TcArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, m, n, L.m_pad, L.n_pad, C, ldc, pc, acc ? 1 : 0};
+        ProfScope prof(st);
+        CK(launch_product_tc(ks, a, st), "product_tc");
+        g_kernel = "k_product_tc";
+    }
+    return GF2E_OK;
+}
+
+int check_flags(uint32_t flags) {
+    if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM)) return fail(GF2E_EINVAL, "unknown flags 0x%x", flags);
+    return GF2E_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *gf2e_last_error(void) { return g_err.c_str(); }
+const char *gf2e_version(void) { return "gf2e_b200 0.1 (sm_100a; tcgen05 kind::i8 + M4RM)"; }
+int gf2e_last_launch_count(void) { return g_launches; }
+const char *gf2e_last_product_kernel(void) { return g_kernel; }
+
+int gf2e_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = on != 0;
+    return GF2E_OK;
+}
+
+int gf2e_profile_read(double *total_ms, int *launches) {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        evs.swap(g_prof_events);
+    }
+    double tot = 0;
+    int rc = GF2E_OK;
+    for (auto &p : evs) {
+        float ms = 0;
+        cudaError_t e = cudaEventSynchronize(p.second);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, p.first, p.second);
+        if (e != cudaSuccess) rc = cuda_fail(e, "gf2e_profile_read");
+        tot += ms;
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = (int)evs.size();
+    return rc;
+}
+
+int gf2e_pack_width(int e) {
+    if (e < 2 || e > 10) return -1;
+    for (int w : {1, 2, 4, 8, 16, 32, 64})
+        if (w >= e) return w;
+    return -1;
+}
+
+int gf2e_schedule(int e, uint32_t f, int *n_products, uint64_t *subsets, uint64_t *outmap, int64_t *counters) {
+    g_err.clear();
+    int rc = check_field(e, f);
+    if (rc) return rc;
+    const Schedule &S = get_schedule(e, f);
+    if (n_products) *n_products = (int)S.subsets.size();
+    if (subsets)
+        for (size_t t = 0; t < S.subsets.size(); ++t) subsets[t] = S.subsets[t];
+    if (outmap)
+        for (int j = 0; j < e; ++j) outmap[j] = S.outmap[j];
+    if (counters)
+        for (int i = 0; i < 3; ++i) counters[i] = S.counters[i];
+    return GF2E_OK;
+}
+
+int gf2e_random_packed(int e, int64_t rows, int64_t cols, uint64_t seed, int64_t row0, int64_t col0, int64_t gcols,
+                       uint64_t *out, int64_t ldp, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    int w = gf2e_pack_width(e);
+    if (w < 0) return fail(GF2E_EINVAL, "extension degree must be in 2..10, got %d", e);
+    if (int rc = check_mat(out, rows, words_for(cols * w), ldp, "packed")) return rc;
+    if (rows == 0 || ldp == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    CK(launch_random_packed(e, w, rows, cols, seed, row0, col0, gcols, out, ldp, (cudaStream_t)stream),
+       "random_packed");
+    return GF2E_OK;
+}
+
+int gf2e_random_sliced(int e, int64_t rows, int64_t cols, uint64_t seed, int64_t row0, int64_t col0, int64_t gcols,
+                       uint64_t *planes, int64_t ld, int64_t pstride, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (e < 2 || e > 10) return fail(GF2E_EINVAL, "extension degree must be in 2..10, got %d", e);
+    if (int rc = check_mat(planes, rows, words_for(cols), ld, "planes")) return rc;
+    if (rows == 0 || ld == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    CK(launch_random_sliced(e, rows, cols, seed, row0, col0, gcols, planes, ld, pstride, (cudaStream_t)stream),
+       "random_sliced");
+    return GF2E_OK;
+}
+
+int gf2e_random_words(int64_t rows, int64_t ncols, uint64_t seed, uint64_t *out, int64_t ld, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (int rc = check_mat(out, rows, words_for(ncols), ld, "words")) return rc;
+    if (rows == 0 || ncols == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    CK(launch_random_words(rows, ncols, seed, out, ld, (cudaStream_t)stream), "random_words");
+    return GF2E_OK;
+}
+
+int gf2e_slice(int e, int64_t rows, int64_t cols, const uint64_t *packed, int64_t ldp, uint64_t *planes, int64_t ld,
+               int64_t pstride, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    int w = gf2e_pack_width(e);
+    if (w < 0) return fail(GF2E_EINVAL, "extension degree must be in 2..10, got %d", e);
+    if (int rc = check_mat(packed, rows, words_for(cols * w), ldp, "packed")) return rc;
+    if (int rc = check_mat(planes, rows, words_for(cols), ld, "planes")) return rc;
+    if (rows == 0 || ld == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    CK(launch_slice(e, w, rows, cols, packed, ldp, planes, ld, pstride, (cudaStream_t)stream), "slice");
+    return GF2E_OK;
+}
+
+int gf2e_cling(int e, int64_t rows, int64_t cols, const uint64_t *planes, int64_t ld, int64_t pstride,
+               uint64_t *packed, int64_t ldp, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    int w = gf2e_pack_width(e);
+    if (w < 0) return fail(GF2E_EINVAL, "extension degree must be in 2..10, got %d", e);
+    if (int rc = check_mat(packed, rows, words_for(cols * w), ldp, "packed")) return rc;
+    if (int rc = check_mat(planes, rows, words_for(cols), ld, "planes")) return rc;
+    if (rows == 0 || ldp == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    CK(launch_cling(e, w, rows, cols, planes, ld, pstride, packed, ldp, (cudaStream_t)stream), "cling");
+    return GF2E_OK;
+}
+
+int gf2e_xor(uint64_t *x, int64_t ldx, const uint64_t *y, int64_t ldy, int64_t rows, int64_t nwords, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (int rc = check_mat(x, rows, nwords, ldx, "x")) return rc;
+    if (int rc = check_mat(y, rows, nwords, ldy, "y")) return rc;
+    if (rows == 0 || nwords == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    CK(launch_xor(x, ldx, y, ldy, rows, nwords, (cudaStream_t)stream), "xor");
+    return GF2E_OK;
+}
+
+int gf2e_reduce_mod_f(int e, uint32_t f, uint64_t *planes, int64_t rows, int64_t nwords, int64_t ld, int64_t pstride,
+                      void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (int rc = check_field(e, f)) return rc;
+    if (int rc = check_mat(planes, rows, nwords, ld, "planes")) return rc;
+    if (rows == 0 || nwords == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    CK(launch_reduce(e, f, planes, rows, nwords, ld, pstride, (cudaStream_t)stream), "reduce_mod_f");
+    return GF2E_OK;
+}
+
+int64_t gf2e_slice_mul_workspace(int e, uint32_t f, int64_t m, int64_t k, int64_t n, uint32_t flags) {
+    g_err.clear();
+    if (check_field(e, f) || check_flags(flags)) return -1;
+    if (m < 0 || k < 0 || n < 0) return fail(GF2E_EINVAL, "matrix dimensions must be non-negative"), -1;
+    if (m == 0 || k == 0 || n == 0) return 0;
+    const Schedule &S = get_schedule(e, f);
+    return layout_for((int)S.subsets.size(), m, k, n, flags).total;
+}
+
+int64_t gf2e_plane_mul_workspace(int64_t m, int64_t k, int64_t n, uint32_t flags) {
+    g_err.clear();
+    if (check_flags(flags)) return -1;
+    if (m < 0 || k < 0 || n < 0) return fail(GF2E_EINVAL, "matrix dimensions must be non-negative"), -1;
+    if (m == 0 || k == 0 || n == 0) return 0;
+    return layout_for(1, m, k, n, flags).total;
+}
+
+int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa, const uint64_t *B, int64_t ldb,
+                   int64_t pb, uint64_t *C, int64_t ldc, int64_t pc, int64_t m, int64_t k, int64_t n, uint32_t flags,
+                   void *ws, int64_t ws_bytes, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (int rc = check_field(e, f)) return rc;
+    if (int rc = check_flags(flags)) return rc;
+    if (int rc = check_mat(A, m, words_for(k), lda, "A")) return rc;
+    if (int rc = check_mat(B, k, words_for(n), ldb, "B")) return rc;
+    if (int rc = check_mat(C, m, words_for(n), ldc, "C")) return rc;
+    if (m == 0 || n == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    Sched ks = to_kernel_sched(e, get_schedule(e, f));
+    return run_product(ks, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, flags, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int gf2e_plane_mul(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, uint64_t *C, int64_t ldc, int64_t m,
+                   int64_t k, int64_t n, uint32_t flags, void *ws, int64_t ws_bytes, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (int rc = check_flags(flags)) return rc;
+    if (int rc = check_mat(A, m, words_for(k), lda, "A")) return rc;
+    if (int rc = check_mat(B, k, words_for(n), ldb, "B")) return rc;
+    if (int rc = check_mat(C, m, words_for(n), ldc, "C")) return rc;
+    if (m == 0 || n == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    return run_product(plane_sched(), A, lda, 0, B, ldb, 0, C, ldc, 0, m, k, n, flags, ws, ws_bytes,
+                       (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,379 @@
+// convert.cu — HBM-bound kernels of the hot path (sm_100a):
+//   K7 generator (rng.py:20-35, mat_packed.py:253-265), K1 slice (mat_sliced.py:97-101),
+//   K2 cling (mat_sliced.py:104-106), plane XOR (mat_gf2.py:161-164), reduce_mod_f
+//   (poly_mul.py:223-242), and K3 operand combinations of the Karatsuba schedule
+//   (poly_mul.py:153-163,184-186,200-201) in the layouts the product kernels read.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gf2e {
+
+namespace {
+
+__host__ __device__ constexpr uint64_t rep(uint64_t pattern, int period) {
+    uint64_t r = 0;
+    for (int i = 0; i < 64; i += period) r |= pattern << i;
+    return r;
+}
+
+// Bit 0 of every W-bit slot of x, packed into the low 64/W bits (a PEXT by constant mask).
+template <int W>
+__device__ __forceinline__ uint64_t gather_slots(uint64_t x) {
+    x &= rep(1, W);
+#pragma unroll
+    for (int k = 1; (W << (k - 1)) < 64; ++k)
+        x = (x | (x >> ((W - 1) << (k - 1)))) & rep((1ULL << (1 << k)) - 1, W << k);
+    return x;
+}
+
+// Inverse of gather_slots: low 64/W bits of x to bit 0 of each W-bit slot (a PDEP).
+template <int W>
+__device__ __forceinline__ uint64_t spread_slots(uint64_t x) {
+    constexpr int P = 64 / W;
+    constexpr int K = (P == 32) ? 5 : (P == 16) ? 4 : (P == 8) ? 3 : (P == 4) ? 2 : 1;
+    x &= (P == 64) ? ~0ULL : ((1ULL << P) - 1);
+#pragma unroll
+    for (int k = K; k >= 1; --k)
+        x = (x | (x << ((W - 1) << (k - 1)))) & rep((1ULL << (1 << (k - 1))) - 1, W << (k - 1));
+    return x;
+}
+
+__device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
+
+// ---- K7 generators -------------------------------------------------------------------
+
+__global__ void k_random_packed(int e, int w, int64_t rows, int64_t cols, uint64_t seed, int64_t row0,
+                                int64_t col0, int64_t gcols, uint64_t *__restrict__ out, int64_t ldp) {
+    const int per = 64 / w;
+    const uint64_t mask = (1ULL << e) - 1;
+    const int64_t total = rows * ldp;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        int64_t r = idx / ldp, pw = idx - r * ldp;
+        int64_t j0 = pw * per;
+        uint64_t base = (uint64_t)(row0 + r) * (uint64_t)gcols + (uint64_t)col0;
+        uint64_t v = 0;
+        for (int s = 0; s < per; ++s) {
+            int64_t j = j0 + s;
+            if (j < cols) v |= (splitmix(seed, base + (uint64_t)j) & mask) << (s * w);
+        }
+        out[idx] = v;
+    }
+}
+
+__global__ void k_random_sliced(int e, int64_t rows, int64_t cols, uint64_t seed, int64_t row0,
+                                int64_t col0, int64_t gcols, uint64_t *__restrict__ planes, int64_t ld,
+                                int64_t pstride) {
+    const int64_t total = rows * ld;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        int64_t r = idx / ld, wi = idx - r * ld;
+        uint64_t base = (uint64_t)(row0 + r) * (uint64_t)gcols + (uint64_t)col0;
+        uint64_t acc[kMaxE];
+#pragma unroll
+        for (int t = 0; t < kMaxE; ++t) acc[t] = 0;
+        int64_t j0 = wi * 64;
+        int nvalid = (int)(cols - j0 < 64 ? (cols - j0 < 0 ? 0 : cols - j0) : 64);
+        for (int s = 0; s < nvalid; ++s) {
+            uint64_t v = splitmix(seed, base + (uint64_t)(j0 + s));
+#pragma unroll
+            for (int t = 0; t < kMaxE; ++t) acc[t] |= ((v >> t) & 1ULL) << s;
+        }
+#pragma unroll
+        for (int t = 0; t < kMaxE; ++t)
+            if (t < e) planes[t * pstride + idx] = acc[t];
+    }
+}
+
+// mat_gf2.py:194-206: one splitmix64 word per storage word, tail bits cleared.
+__global__ void k_random_words(int64_t rows, int64_t ncols, uint64_t seed, uint64_t *__restrict__ out,
+                               int64_t ld) {
+    const int64_t nw = words_for(ncols);
+    const uint64_t tm = tail_mask(ncols);
+    const int64_t total = rows * nw;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        int64_t r = idx / nw, w = idx - r * nw;
+        uint64_t v = splitmix(seed, (uint64_t)idx);
+        out[r * ld + w] = (w == nw - 1) ? (v & tm) : v;
+    }
+}
+
+// ---- K1 / K2 ----------------------------------------------------------------------
+
+template <int W>
+__global__ void k_slice(int e, int64_t rows, int64_t cols, const uint64_t *__restrict__ packed, int64_t ldp,
+                        uint64_t *__restrict__ planes, int64_t ld, int64_t pstride) {
+    constexpr int P = 64 / W;
+    const int64_t nw = words_for(cols);
+    const int64_t pwords = words_for(cols * W);
+    const int64_t total = rows * ld;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        int64_t r = idx / ld, wi = idx - r * ld;
+        uint64_t acc[kMaxE];
+#pragma unroll
+        for (int t = 0; t < kMaxE; ++t) acc[t] = 0;
+        if (wi < nw) {
+            const uint64_t *src = packed + r * ldp + wi * W;
+#pragma unroll
+            for (int q = 0; q < W; ++q) {
+                uint64_t x = (wi * W + q < pwords) ? src[q] : 0;
+#pragma unroll
+                for (int t = 0; t < kMaxE; ++t)
+                    if (t < e) acc[t] |= gather_slots<W>(x >> t) << (q * P);
+            }
+            if (wi == nw - 1) {
+                uint64_t tm = tail_mask(cols);
+#pragma unroll
+                for (int t = 0; t < kMaxE; ++t) acc[t] &= tm;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < kMaxE; ++t)
+            if (t < e) planes[t * pstride + idx] = acc[t];
+    }
+}
+
+template <int W>
+__global__ void k_cling(int e, int64_t rows, int64_t cols, const uint64_t *__restrict__ planes, int64_t ld,
+                        int64_t pstride, uint64_t *__restrict__ packed, int64_t ldp) {
+    constexpr int P = 64 / W;
+    const int64_t total = rows * ldp;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        int64_t r = idx / ldp, pw = idx - r * ldp;
+        int64_t j0 = pw * P;
+        uint64_t v = 0;
+        if (j0 < cols) {
+            int64_t wi = pw / W;
+            int sh = (int)(pw % W) * P;
+#pragma unroll
+            for (int t = 0; t < kMaxE; ++t)
+                if (t < e) v |= spread_slots<W>(planes[t * pstride + r * ld + wi] >> sh) << t;
+            int64_t nvalid = cols - j0;
+            if (nvalid < P) v &= (1ULL << (nvalid * W)) - 1;
+        }
+        packed[idx] = v;
+    }
+}
+
+__global__ void k_xor(uint64_t *__restrict__ x, int64_t ldx, const uint64_t *__restrict__ y, int64_t ldy,
+                      int64_t rows, int64_t nwords) {
+    const int64_t total = rows * nwords;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        int64_t r = idx / nwords, w = idx - r * nwords;
+        x[r * ldx + w] ^= y[r * ldy + w];
+    }
+}
+
+// poly_mul.py:223-242: for d = 2e-2 .. e, plane d folds into planes d-e+k for set low bits k of f.
+__global__ void k_reduce(int e, uint32_t f, uint64_t *__restrict__ planes, int64_t rows, int64_t nwords,
+                         int64_t ld, int64_t pstride) {
+    const int64_t total = rows * nwords;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        int64_t r = idx / nwords, w = idx - r * nwords;
+        int64_t off = r * ld + w;
+        uint64_t x[2 * kMaxE - 1];
+#pragma unroll
+        for (int d = 0; d < 2 * kMaxE - 1; ++d) x[d] = d < 2 * e - 1 ? planes[d * pstride + off] : 0;
+#pragma unroll
+        for (int d = 2 * kMaxE - 2; d >= 1; --d) {
+            if (d > 2 * e - 2 || d < e) continue;
+#pragma unroll
+            for (int k = 0; k < kMaxE; ++k)
+                if (k < e && ((f >> k) & 1u) && d - e + k >= 0) x[d - e + k] ^= x[d];
+        }
+#pragma unroll
+        for (int d = 0; d < kMaxE; ++d)
+            if (d < e) planes[d * pstride + off] = x[d];
+    }
+}
+
+// ---- K3 operand combinations --------------------------------------------------------
+
+// out[t] = XOR_{i in S_t} X_i on a zero-padded (rows_pad x words_pad) grid, natural bit order.
+__global__ void k_combos_rows(Sched s, const uint64_t *__restrict__ X, int64_t ldx, int64_t px, int64_t rows,
+                              int64_t ncols, uint64_t *__restrict__ out, int64_t ldo, int64_t po,
+                              int64_t rows_pad, int64_t words_pad) {
+    const int64_t nw = words_for(ncols);
+    const uint64_t tm = tail_mask(ncols);
+    const int64_t total = rows_pad * words_pad;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        int64_t r = idx / words_pad, w = idx - r * words_pad;
+        uint64_t x[kMaxE];
+        bool valid = r < rows && w < nw;
+#pragma unroll
+        for (int i = 0; i < kMaxE; ++i) {
+            uint64_t v = (i < s.e && valid) ? X[i * px + r * ldx + w] : 0;
+            x[i] = (w == nw - 1) ? (v & tm) : v;
+        }
+        for (int t = 0; t < s.nprod; ++t) {
+            uint32_t sub = s.subset[t];
+            uint64_t acc = 0;
+#pragma unroll
+            for (int i = 0; i < kMaxE; ++i) acc ^= x[i] & (0ULL - (uint64_t)((sub >> i) & 1u));
+            out[t * po + r * ldo + w] = acc;
+        }
+    }
+}
+
+// 64x64 bit-matrix transpose held as two words per lane (rows lane and lane+32).
+__device__ __forceinline__ void transpose64(uint64_t &xa, uint64_t &xb, int lane) {
+    uint64_t t = ((xa >> 32) ^ xb) & 0x00000000FFFFFFFFULL;
+    xb ^= t;
+    xa ^= t << 32;
+    const uint64_t masks[5] = {0x0000FFFF0000FFFFULL, 0x00FF00FF00FF00FFULL, 0x0F0F0F0F0F0F0F0FULL,
+                               0x3333333333333333ULL, 0x5555555555555555ULL};
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int j = 16 >> s;
+        const uint64_t m = masks[s];
+        uint64_t oa = __shfl_xor_sync(0xffffffffu, xa, j);
+        uint64_t ob = __shfl_xor_sync(0xffffffffu, xb, j);
+        if ((lane & j) == 0) {
+            xa ^= (((xa >> j) ^ oa) & m) << j;
+            xb ^= (((xb >> j) ^ ob) & m) << j;
+        } else {
+            xa ^= ((oa >> j) ^ xa) & m;
+            xb ^= ((ob >> j) ^ xb) & m;
+        }
+    }
+}
+
+// Bt[t] = (XOR_{i in S_t} B_i)^T: row n holds the k-bits of column n of B, with the bit
+// order reversed inside every byte (k-bit 8q+i at position 8q+7-i) — the layout the
+// tensor-core producer expands with one AND per output word (product_tc.cu).
+// One warp per 64x64 block; zero padded to n_pad rows x k_pad bits.
+__global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb, int64_t pb, int64_t k,
+                            int64_t n, uint64_t *__restrict__ out, int64_t ldo, int64_t po, int64_t kblocks,
+                            int64_t nblocks) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = gtid() >> 5;
+    const int64_t nwarps = gstride() >> 5;
+    const int64_t nw = words_for(n);
+    for (int64_t blk = warp; blk < kblocks * nblocks; blk += nwarps) {
+        int64_t kb = blk % kblocks, nb = blk / kblocks;
+        int64_t r0 = kb * 64 + (lane ^ 7), r1 = r0 + 32;
+        uint64_t tm = (nb == nw - 1) ? tail_mask(n) : ~0ULL;
+        uint64_t a[kMaxE], b[kMaxE];
+#pragma unroll
+        for (int i = 0; i < kMaxE; ++i) {
+            a[i] = (i < s.e && nb < nw && r0 < k) ? (B[i * pb + r0 * ldb + nb] & tm) : 0;
+            b[i] = (i < s.e && nb < nw && r1 < k) ? (B[i * pb + r1 * ldb + nb] & tm) : 0;
+        }
+        for (int t = 0; t < s.nprod; ++t) {
+            uint32_t sub = s.subset[t];
+            uint64_t xa = 0, xb = 0;
+#pragma unroll
+            for (int i = 0; i < kMaxE; ++i) {
+                uint64_t sel = 0ULL - (uint64_t)((sub >> i) & 1u);
+                xa ^= a[i] & sel;
+                xb ^= b[i] & sel;
+            }
+            transpose64(xa, xb, lane);
+            uint64_t *o = out + t * po + (nb * 64 + lane) * ldo + kb;
+            o[0] = xa;
+            o[32 * ldo] = xb;
+        }
+    }
+}
+
+inline int grid_for(int64_t total, int threads) {
+    int64_t g = (total + threads - 1) / threads;
+    if (g > 148 * 64) g = 148 * 64;
+    return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+// ---- host launchers -------------------------------------------------------------------
+
+cudaError_t launch_random_packed(int e, int w, int64_t rows, int64_t cols, uint64_t seed, int64_t row0,
+                                 int64_t col0, int64_t gcols, uint64_t *out, int64_t ldp, cudaStream_t st) {
+    int64_t total = rows * ldp;
+    if (total == 0) return cudaSuccess;
+    k_random_packed<<<grid_for(total, 256), 256, 0, st>>>(e, w, rows, cols, seed, row0, col0, gcols, out, ldp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_random_sliced(int e, int64_t rows, int64_t cols, uint64_t seed, int64_t row0, int64_t col0,
+                                 int64_t gcols, uint64_t *planes, int64_t ld, int64_t pstride, cudaStream_t st) {
+    int64_t total = rows * ld;
+    if (total == 0) return cudaSuccess;
+    k_random_sliced<<<grid_for(total, 256), 256, 0, st>>>(e, rows, cols, seed, row0, col0, gcols, planes, ld,
+                                                          pstride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_random_words(int64_t rows, int64_t ncols, uint64_t seed, uint64_t *out, int64_t ld,
+                                cudaStream_t st) {
+    int64_t total = rows * words_for(ncols);
+    if (total == 0) return cudaSuccess;
+    k_random_words<<<grid_for(total, 256), 256, 0, st>>>(rows, ncols, seed, out, ld);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_slice(int e, int w, int64_t rows, int64_t cols, const uint64_t *packed, int64_t ldp,
+                         uint64_t *planes, int64_t ld, int64_t pstride, cudaStream_t st) {
+    int64_t total = rows * ld;
+    if (total == 0) return cudaSuccess;
+    int g = grid_for(total, 256);
+    switch (w) {
+        case 2: k_slice<2><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
+        case 4: k_slice<4><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
+        case 8: k_slice<8><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
+        case 16: k_slice<16><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cling(int e, int w, int64_t rows, int64_t cols, const uint64_t *planes, int64_t ld,
+                         int64_t pstride, uint64_t *packed, int64_t ldp, cudaStream_t st) {
+    int64_t total = rows * ldp;
+    if (total == 0) return cudaSuccess;
+    int g = grid_for(total, 256);
+    switch (w) {
+        case 2: k_cling<2><<<g, 256, 0, st>>>(e, rows, cols, planes, ld, pstride, packed, ldp); break;
+        case 4: k_cling<4><<<g, 256, 0, st>>>(e, rows, cols, planes, ld, pstride, packed, ldp); break;
+        case 8: k_cling<8><<<g, 256, 0, st>>>(e, rows, cols, planes, ld, pstride, packed, ldp); break;
+        case 16: k_cling<16><<<g, 256, 0, st>>>(e, rows, cols, planes, ld, pstride, packed, ldp); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xor(uint64_t *x, int64_t ldx, const uint64_t *y, int64_t ldy, int64_t rows, int64_t nwords,
+                       cudaStream_t st) {
+    int64_t total = rows * nwords;
+    if (total == 0) return cudaSuccess;
+    k_xor<<<grid_for(total, 256), 256, 0, st>>>(x, ldx, y, ldy, rows, nwords);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(int e, uint32_t f, uint64_t *planes, int64_t rows, int64_t nwords, int64_t ld,
+                          int64_t pstride, cudaStream_t st) {
+    int64_t total = rows * nwords;
+    if (total == 0) return cudaSuccess;
+    k_reduce<<<grid_for(total, 256), 256, 0, st>>>(e, f, planes, rows, nwords, ld, pstride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, int64_t px, int64_t rows,
+                               int64_t ncols, uint64_t *out, int64_t ldo, int64_t po, int64_t rows_pad,
+                               int64_t words_pad, cudaStream_t st) {
+    int64_t total = rows_pad * words_pad;
+    if (total == 0) return cudaSuccess;
+    k_combos_rows<<<grid_for(total, 256), 256, 0, st>>>(s, X, ldx, px, rows, ncols, out, ldo, po, rows_pad,
+                                                        words_pad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int64_t pb, int64_t k, int64_t n,
+                             uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks,
+                             cudaStream_t st) {
+    int64_t warps = kblocks * nblocks;
+    if (warps == 0) return cudaSuccess;
+    int g = grid_for(warps * 32, 256);
+    k_combos_bt<<<g, 256, 0, st>>>(s, B, ldb, pb, k, n, out, ldo, po, kblocks, nblocks);
+    return cudaGetLastError();
+}
+
+}  // namespace gf2e

@@ -1,0 +1,189 @@
+"""★ The hot path: GF(2^e) matrix multiply(-accumulate) via bitsliced Karatsuba on the B200.
+
+Drop-in for the Karatsuba half of ``gf2elin.poly_mul`` (``poly_mul.py:32-43,128-278``):
+``MulCounters``, ``karatsuba_mul``, ``reduce_mod_f``, ``count_products``,
+``karatsuba_mul_packed`` keep their names, arguments, return types and errors; ``addmul``
+/ ``addmul_packed`` add the C += A*B form the reference writes inline
+(``ple_echelon.py:130-136,259``).  M4RIE names are aliases (``mzd_slice_mul`` ...).
+
+One call = one ``gf2e_slice_mul`` into libgf2e_b200.so: operand combinations (K3), then the
+fused tensor-core product + Karatsuba combine + mod-f fold (+ addmul XOR) kernel (K4/K5).
+Counters are replayed from the native schedule (``gf2e_schedule``) and equal the
+reference's ``MulCounters`` exactly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+from . import _device, _lib
+from .gf2e import FieldCtx, field_new
+from .mat_gf2 import BitMatrix, words_for
+from .mat_packed import PackedMatrix
+from .mat_sliced import SlicedMatrix, cling, slice_packed
+
+_BACKENDS = {"tc": _lib.BACKEND_TC, "m4rm": _lib.BACKEND_M4RM}
+DEFAULT_BACKEND = os.environ.get("GF2E_BACKEND", "tc")
+
+
+def _resolve_backend(backend: str | None) -> int:
+    b = DEFAULT_BACKEND if backend is None else backend
+    if b not in _BACKENDS:
+        raise ValueError(f"unknown backend {b!r}; expected one of {sorted(_BACKENDS)}")
+    return _BACKENDS[b]
+
+
+@dataclass
+class MulCounters:
+    """Operation counts accumulated over one multiplication call (poly_mul.py:32-43)."""
+
+    gf2_matmul_count: int = 0
+    additions: int = 0
+    peak_live_products: int = 0
+
+    def reset(self) -> None:
+        self.gf2_matmul_count = 0
+        self.additions = 0
+        self.peak_live_products = 0
+
+
+@dataclass(frozen=True)
+class Schedule:
+    """The Karatsuba schedule for (e, f) as computed natively by the library."""
+
+    e: int
+    f: int
+    subsets: tuple[int, ...]   # operand t = XOR of input planes in subsets[t]
+    outmap: tuple[int, ...]    # output plane j = XOR of products in outmap[j] (M = R_f . Gamma)
+    counters: tuple[int, int, int]
+
+    @property
+    def n_products(self) -> int:
+        return len(self.subsets)
+
+
+_SCHED_CACHE: dict[tuple[int, int], Schedule] = {}
+
+
+def schedule(e: int, f: int | None = None) -> Schedule:
+    """Native schedule (no GPU needed): symbolic replay of poly_mul.py:166-242 in C++."""
+    ctx = field_new(e, f)
+    key = (ctx.e, ctx.f)
+    s = _SCHED_CACHE.get(key)
+    if s is None:
+        n = ctypes.c_int()
+        subsets = (ctypes.c_uint64 * 64)()
+        outmap = (ctypes.c_uint64 * 10)()
+        cnt = (ctypes.c_int64 * 3)()
+        _lib.check(_lib.load().gf2e_schedule(ctx.e, ctx.f, ctypes.byref(n), subsets, outmap, cnt), "gf2e_schedule")
+        s = Schedule(ctx.e, ctx.f, tuple(int(subsets[t]) for t in range(n.value)),
+                     tuple(int(outmap[j]) for j in range(ctx.e)), (int(cnt[0]), int(cnt[1]), int(cnt[2])))
+        _SCHED_CACHE[key] = s
+    return s
+
+
+def _bump(counters: MulCounters | None, ctx: FieldCtx) -> None:
+    if counters is None:
+        return
+    g, adds, peak = schedule(ctx.e, ctx.f).counters
+    counters.gf2_matmul_count += g
+    counters.additions += adds
+    if peak > counters.peak_live_products:
+        counters.peak_live_products = peak
+
+
+def _check_operands(A: SlicedMatrix, B: SlicedMatrix) -> None:
+    if A.ctx != B.ctx:
+        raise ValueError(f"field mismatch: {A.ctx} vs {B.ctx}")
+    if A.ncols != B.nrows:
+        raise ValueError(f"inner dimensions differ: {A.nrows}x{A.ncols} times {B.nrows}x{B.ncols}")
+
+
+def _slice_mul(A: SlicedMatrix, B: SlicedMatrix, C: SlicedMatrix, accumulate: bool, backend: str | None) -> None:
+    ctx = A.ctx
+    m, k, n = A.nrows, A.ncols, B.ncols
+    flags = _resolve_backend(backend) | (_lib.ACCUMULATE if accumulate else 0)
+    L = _lib.load()
+    ws_bytes = int(L.gf2e_slice_mul_workspace(ctx.e, ctx.f, m, k, n, flags))
+    if ws_bytes < 0:
+        _lib.check(_lib.GF2E_EINVAL, "gf2e_slice_mul_workspace")
+    ws = _device.workspace.get(ws_bytes)
+    lda, ldb, ldc = A.planes.shape[2], B.planes.shape[2], C.planes.shape[2]
+    _lib.call("gf2e_slice_mul", ctx.e, ctx.f, _device.ptr(A.planes), lda, m * lda, _device.ptr(B.planes), ldb,
+              k * ldb, _device.ptr(C.planes), ldc, m * ldc, m, k, n, flags, ws.data_ptr(), ws.numel(),
+              _device.stream_handle())
+
+
+def karatsuba_mul(A: SlicedMatrix, B: SlicedMatrix, counters: MulCounters | None = None,
+                  backend: str | None = None) -> SlicedMatrix:
+    """GF(2^e) product via slice-polynomial Karatsuba plus reduction (poly_mul.py:245-259)."""
+    _check_operands(A, B)
+    C = SlicedMatrix(A.ctx, A.nrows, B.ncols, _device.empty_words((A.ctx.e, A.nrows, words_for(B.ncols))))
+    _slice_mul(A, B, C, False, backend)
+    _bump(counters, A.ctx)
+    return C
+
+
+def addmul(C: SlicedMatrix, A: SlicedMatrix, B: SlicedMatrix, counters: MulCounters | None = None,
+           backend: str | None = None) -> SlicedMatrix:
+    """C ^= A*B in place (mzd_slice_addmul) — the reference's ``X ^= karatsuba_mul(A, B)``."""
+    _check_operands(A, B)
+    if C.ctx != A.ctx:
+        raise ValueError(f"field mismatch: {C.ctx} vs {A.ctx}")
+    if C.shape != (A.nrows, B.ncols):
+        raise ValueError(f"dimension mismatch: {C.shape} vs {(A.nrows, B.ncols)}")
+    _slice_mul(A, B, C, True, backend)
+    _bump(counters, A.ctx)
+    return C
+
+
+def reduce_mod_f(slices: list[BitMatrix], ctx: FieldCtx, counters: MulCounters | None = None) -> list[BitMatrix]:
+    """Fold a degree-(2e-2) slice polynomial to degree < e (poly_mul.py:223-242), on device."""
+    e = ctx.e
+    if len(slices) != 2 * e - 1:
+        raise ValueError(f"expected {2 * e - 1} coefficient slices, got {len(slices)}")
+    m, n = slices[0].shape
+    work = _device.empty_words((2 * e - 1, m, words_for(n)))
+    for d, s in enumerate(slices):
+        work[d].copy_(s.words)
+    nw = words_for(n)
+    if m and nw:
+        _lib.call("gf2e_reduce_mod_f", e, ctx.f, _device.ptr(work), m, nw, nw, m * nw, _device.stream_handle())
+    if counters is not None:
+        counters.additions += sum(1 for _ in range(2 * e - 2, e - 1, -1) for k in range(e) if (ctx.f >> k) & 1)
+    return [BitMatrix(m, n, work[j].clone()) for j in range(e)]
+
+
+def count_products(e: int, f: int | None = None) -> int:
+    """GF(2) products per Karatsuba multiplication (poly_mul.py:262-272); host-only."""
+    return schedule(e, f).n_products
+
+
+def karatsuba_mul_packed(A: PackedMatrix, B: PackedMatrix, counters: MulCounters | None = None,
+                         backend: str | None = None) -> PackedMatrix:
+    """Slice, multiply, cling back (poly_mul.py:275-278): K1 -> K3/K4/K5 -> K2."""
+    return cling(karatsuba_mul(slice_packed(A), slice_packed(B), counters, backend))
+
+
+def addmul_packed(C: PackedMatrix, A: PackedMatrix, B: PackedMatrix, counters: MulCounters | None = None,
+                  backend: str | None = None) -> PackedMatrix:
+    """C ^= A*B on packed matrices (mzed_addmul), through the sliced path; C updated in place."""
+    if A.ctx != B.ctx or C.ctx != A.ctx:
+        raise ValueError(f"field mismatch: {A.ctx} vs {B.ctx}")
+    if A.ncols != B.nrows:
+        raise ValueError(f"inner dimensions differ: {A.nrows}x{A.ncols} times {B.nrows}x{B.ncols}")
+    if C.shape != (A.nrows, B.ncols):
+        raise ValueError(f"dimension mismatch: {C.shape} vs {(A.nrows, B.ncols)}")
+    Cs = slice_packed(C)
+    addmul(Cs, slice_packed(A), slice_packed(B), counters, backend)
+    cling(Cs, out=C)
+    return C
+
+
+# M4RIE vocabulary (BASELINE.json north star)
+mzd_slice_mul = karatsuba_mul
+mzd_slice_addmul = addmul
+mzed_mul = karatsuba_mul_packed
+mzed_addmul = addmul_packed

@@ -1,0 +1,142 @@
+"""Generate tests/golden/golden.npz by running the REFERENCE package itself.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+The fixtures pin the CPU oracle (oracle/) and, through it, the CUDA library.  Everything
+is produced by the reference's own public functions:
+    rng.word_stream                       (rng.py:20-28)
+    PackedMatrix.random / storage.words   (mat_packed.py:253-265)
+    slice_packed / cling                  (mat_sliced.py:97-106)
+    karatsuba_mul + MulCounters           (poly_mul.py:245-259, 32-43)
+    karatsuba_mul_packed                  (poly_mul.py:275-278)
+    reduce_mod_f                          (poly_mul.py:223-242)
+    count_products                        (poly_mul.py:262-272)
+    mat_gf2.mul (strategy m4rm / cubic)   (mat_gf2.py:425-455)
+    FieldCtx.mul_table                    (gf2e.py:91-106)
+Seeds follow SURVEY §8d: A = 1, B = 2, C0 = 3.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+from gf2elin import gf2e, mat_gf2, mat_packed, mat_sliced, poly_mul, rng  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
+
+# (m, k, n) shapes: word boundaries 63/64/65/127/128/129, empty dims
+SHAPES_ALL_E = [(37, 70, 65), (1, 1, 1)]
+SHAPES_EDGE = [(63, 64, 65), (64, 64, 64), (33, 127, 70), (129, 64, 1), (5, 0, 7), (0, 3, 4),
+               (65, 129, 128)]
+CUSTOM_F = {4: 0b11001, 8: 0x11B, 10: 0b10000001111}  # x^4+x^3+1, AES x^8+x^4+x^3+x+1, x^10+x^3+x^2+x+1
+
+
+def add_case(store, tag, e, f, m, k, n):
+    ctx = gf2e.field_new(e, f)
+    A = mat_packed.PackedMatrix.random(ctx, m, k, 1)
+    B = mat_packed.PackedMatrix.random(ctx, k, n, 2)
+    C0 = mat_packed.PackedMatrix.random(ctx, m, n, 3)
+    SA, SB, SC0 = (mat_sliced.slice_packed(X) for X in (A, B, C0))
+    cnt = poly_mul.MulCounters()
+    SC = poly_mul.karatsuba_mul(SA, SB, cnt)
+    PC = poly_mul.karatsuba_mul_packed(A, B)
+    assert mat_sliced.cling(SC) == PC
+    # addmul, written the way the reference library does it (ple_echelon.py:259 xor_window)
+    X = C0.copy()
+    X.xor_window(0, 0, PC)
+    store[f"{tag}/meta"] = np.array([e, ctx.f, m, k, n], dtype=np.int64)
+    store[f"{tag}/A_packed"] = A.storage.words.copy()
+    store[f"{tag}/B_packed"] = B.storage.words.copy()
+    store[f"{tag}/C0_packed"] = C0.storage.words.copy()
+    store[f"{tag}/A_planes"] = np.stack([s.words for s in SA.slices]) if e else None
+    store[f"{tag}/B_planes"] = np.stack([s.words for s in SB.slices])
+    store[f"{tag}/C0_planes"] = np.stack([s.words for s in SC0.slices])
+    store[f"{tag}/C_planes"] = np.stack([s.words for s in SC.slices])
+    store[f"{tag}/C_packed"] = PC.storage.words.copy()
+    store[f"{tag}/addmul_packed"] = X.storage.words.copy()
+    store[f"{tag}/counters"] = np.array([cnt.gf2_matmul_count, cnt.additions, cnt.peak_live_products],
+                                        dtype=np.int64)
+
+
+def main():
+    store: dict[str, np.ndarray] = {}
+    tags = []
+    for e in range(2, 11):
+        for (m, k, n) in SHAPES_ALL_E:
+            tag = f"kara/e{e}/{m}x{k}x{n}"
+            add_case(store, tag, e, None, m, k, n)
+            tags.append(tag)
+    for e in (2, 8):
+        for (m, k, n) in SHAPES_EDGE:
+            tag = f"kara/e{e}/{m}x{k}x{n}"
+            add_case(store, tag, e, None, m, k, n)
+            tags.append(tag)
+    for e, f in CUSTOM_F.items():
+        tag = f"kara/e{e}f{f:x}/40x33x71"
+        add_case(store, tag, e, f, 40, 33, 71)
+        tags.append(tag)
+    # a medium case for the device tiling (several 128-row / 256-col tiles, ragged edges)
+    tag = "kara/e4/300x520x270"
+    add_case(store, tag, 4, None, 300, 520, 270)
+    tags.append(tag)
+    store["kara_tags"] = np.array(tags)
+
+    # count_products (poly_mul.py:262-272)
+    store["count_products"] = np.array([poly_mul.count_products(e) for e in range(2, 11)], dtype=np.int64)
+    store["default_polys"] = np.array([gf2e.DEFAULT_POLYS[e] for e in range(2, 11)], dtype=np.int64)
+
+    # rng word stream (rng.py:20-28)
+    for seed in (0, 1, 2, 3, 2**64 - 1):
+        store[f"rng/{seed}"] = rng.word_stream(seed, 16)
+
+    # GF(2) plane products (mat_gf2.py:425-455); k in {0, 1, 255, 256, 257}
+    g2 = []
+    for (m, k, n) in [(64, 0, 64), (70, 1, 65), (33, 255, 129), (65, 256, 127), (128, 257, 64),
+                      (1, 300, 1), (200, 64, 200)]:
+        A = mat_gf2.BitMatrix.random(m, k, 11)
+        B = mat_gf2.BitMatrix.random(k, n, 12)
+        C = mat_gf2.mul(A, B, strategy="m4rm")
+        assert C == mat_gf2.mul(A, B, strategy="cubic")
+        tag = f"gf2/{m}x{k}x{n}"
+        store[f"{tag}/A"] = A.words.copy()
+        store[f"{tag}/B"] = B.words.copy()
+        store[f"{tag}/C"] = C.words.copy()
+        store[f"{tag}/meta"] = np.array([m, k, n], dtype=np.int64)
+        g2.append(tag)
+    store["gf2_tags"] = np.array(g2)
+
+    # Fig. 1: GF(8) [[5,2],[3,1]]
+    ctx8 = gf2e.field_new(3)
+    P = mat_packed.PackedMatrix.from_array(ctx8, np.array([[5, 2], [3, 1]]))
+    S = mat_sliced.slice_packed(P)
+    store["fig1/packed"] = P.storage.words.copy()
+    store["fig1/planes"] = np.stack([s.words for s in S.slices])
+
+    # reduce_mod_f GF(4) known answer: (C0, C1, C2) -> (C0^C2, C1^C2)
+    ctx4 = gf2e.field_new(2)
+    Cs = [mat_gf2.BitMatrix.random(5, 70, 20 + i) for i in range(3)]
+    R = poly_mul.reduce_mod_f(Cs, ctx4)
+    store["reduce/e2/in"] = np.stack([c.words for c in Cs])
+    store["reduce/e2/out"] = np.stack([r.words for r in R])
+    ctx8f = gf2e.field_new(8)
+    Cs = [mat_gf2.BitMatrix.random(3, 65, 40 + i) for i in range(15)]
+    R = poly_mul.reduce_mod_f(Cs, ctx8f)
+    store["reduce/e8/in"] = np.stack([c.words for c in Cs])
+    store["reduce/e8/out"] = np.stack([r.words for r in R])
+
+    # field tables for e = 2..4 (GF(4) mul(2,2)=3 etc.)
+    for e in (2, 3, 4):
+        store[f"field/e{e}/mul"] = gf2e.field_new(e).mul_table.copy()
+
+    np.savez_compressed(OUT, **store)
+    print(f"wrote {OUT}: {len(store)} arrays, {os.path.getsize(OUT)} bytes")
+
+
+if __name__ == "__main__":
+    main()

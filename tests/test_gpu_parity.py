@@ -1,0 +1,246 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle and the reference fixtures.
+Bit-exact everywhere: this path is integer/bitwise only."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+BACKENDS = ["tc", "m4rm"]
+
+
+@pytest.fixture(scope="module")
+def g():
+    import torch
+
+    import paper_1111_6900_b200 as g
+
+    torch.cuda.set_device(0)
+    return g
+
+
+def _tags(golden, key):
+    return [str(t) for t in golden[key]]
+
+
+def _sync():
+    import torch
+
+    torch.cuda.synchronize()
+
+
+# ---- K7 / K1 / K2 ----------------------------------------------------------------------
+
+def test_generators_and_conversions_golden(g, golden):
+    for tag in _tags(golden, "kara_tags"):
+        e, f, m, k, n = (int(x) for x in golden[f"{tag}/meta"])
+        ctx = g.field_new(e, f)
+        A = g.PackedMatrix.random(ctx, m, k, 1)
+        assert np.array_equal(A.to_numpy(), golden[f"{tag}/A_packed"]), tag
+        SA = g.slice_packed(A)
+        assert np.array_equal(SA.to_numpy(), golden[f"{tag}/A_planes"]), tag
+        assert np.array_equal(g.SlicedMatrix.random(ctx, m, k, 1).to_numpy(), golden[f"{tag}/A_planes"]), tag
+        assert np.array_equal(g.cling(SA).to_numpy(), golden[f"{tag}/A_packed"]), tag
+
+
+@pytest.mark.parametrize("e", range(2, 11))
+@pytest.mark.parametrize("shape", [(1, 1), (63, 64), (65, 127), (128, 129), (7, 1000), (129, 65)])
+def test_slice_cling_roundtrip(g, e, shape):
+    m, n = shape
+    ctx = g.field_new(e)
+    A = g.PackedMatrix.random(ctx, m, n, 5 + e)
+    S = g.slice_packed(A)
+    ref = oracle.slice_words(e, m, n, oracle.packed_random(e, m, n, 5 + e))
+    assert np.array_equal(S.to_numpy(), ref)
+    assert g.cling(S) == A
+
+
+def test_slice_drops_pad_bits(g):
+    # mat_packed.py:118-121: only bits 0..e-1 of a slot are read
+    ctx = g.field_new(5)
+    A = g.PackedMatrix.random(ctx, 9, 33, 1)
+    words = A.to_numpy()
+    pad = np.full(words.shape, 0xE0E0E0E0E0E0E0E0, dtype=np.uint64)  # bits 5..7 of every 8-bit slot
+    pad[:, -1] = np.uint64(0xE0)  # 33 slots: the last word holds one slot
+    B = g.PackedMatrix.from_numpy(ctx, words | pad, 33)
+    assert g.slice_packed(B) == g.slice_packed(A)
+
+
+def test_random_words_golden(g, golden):
+    for tag in _tags(golden, "gf2_tags"):
+        m, k, n = (int(x) for x in golden[f"{tag}/meta"])
+        assert np.array_equal(g.BitMatrix.random(m, k, 11).to_numpy(), golden[f"{tag}/A"]), tag
+
+
+# ---- the hot path ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_karatsuba_golden(g, golden, backend):
+    for tag in _tags(golden, "kara_tags"):
+        e, f, m, k, n = (int(x) for x in golden[f"{tag}/meta"])
+        ctx = g.field_new(e, f)
+        SA = g.SlicedMatrix.from_numpy(ctx, golden[f"{tag}/A_planes"], k)
+        SB = g.SlicedMatrix.from_numpy(ctx, golden[f"{tag}/B_planes"], n)
+        cnt = g.MulCounters()
+        SC = g.karatsuba_mul(SA, SB, cnt, backend=backend)
+        assert np.array_equal(SC.to_numpy(), golden[f"{tag}/C_planes"]), (tag, backend)
+        assert [cnt.gf2_matmul_count, cnt.additions, cnt.peak_live_products] == list(golden[f"{tag}/counters"])
+        A = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/A_packed"], k)
+        B = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/B_packed"], n)
+        assert np.array_equal(g.karatsuba_mul_packed(A, B, backend=backend).to_numpy(),
+                              golden[f"{tag}/C_packed"]), (tag, backend)
+        C0 = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/C0_packed"], n)
+        g.addmul_packed(C0, A, B, backend=backend)
+        assert np.array_equal(C0.to_numpy(), golden[f"{tag}/addmul_packed"]), (tag, backend)
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_gf2_plane_products_golden(g, golden, backend):
+    for tag in _tags(golden, "gf2_tags"):
+        m, k, n = (int(x) for x in golden[f"{tag}/meta"])
+        A = g.BitMatrix.from_numpy(golden[f"{tag}/A"], k)
+        B = g.BitMatrix.from_numpy(golden[f"{tag}/B"], n)
+        C = g.mul(A, B, backend=backend)
+        assert np.array_equal(C.to_numpy(), golden[f"{tag}/C"]), (tag, backend)
+        D = g.BitMatrix.random(m, n, 99)
+        d0 = D.to_numpy()
+        g.gf2_addmul(D, A, B, backend=backend)
+        assert np.array_equal(D.to_numpy(), d0 ^ golden[f"{tag}/C"]), (tag, backend)
+
+
+def test_reduce_mod_f_golden(g, golden):
+    for e, key in ((2, "reduce/e2"), (8, "reduce/e8")):
+        ctx = g.field_new(e)
+        cin = golden[f"{key}/in"]
+        n = {2: 70, 8: 65}[e]
+        slices = [g.BitMatrix.from_numpy(cin[d], n) for d in range(2 * e - 1)]
+        cnt = g.MulCounters()
+        out = g.reduce_mod_f(slices, ctx, cnt)
+        assert np.array_equal(np.stack([o.to_numpy() for o in out]), golden[f"{key}/out"])
+        assert cnt.additions == sum(1 for _ in range(e - 1) for k in range(e) if (ctx.f >> k) & 1)
+        with pytest.raises(ValueError, match="coefficient slices"):
+            g.reduce_mod_f(slices[:-1], ctx)
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+@pytest.mark.parametrize("e", range(2, 11))
+def test_word_boundary_shapes(g, e, backend):
+    # SPEC.md:146 word boundaries, empty and ragged dimensions, all e
+    ctx = g.field_new(e)
+    for (m, k, n) in [(63, 65, 129), (64, 64, 64), (129, 1, 257), (5, 0, 7), (0, 3, 4), (3, 4, 0),
+                      (130, 300, 70), (1, 129, 1)]:
+        SA = g.SlicedMatrix.random(ctx, m, k, 1)
+        SB = g.SlicedMatrix.random(ctx, k, n, 2)
+        C = g.karatsuba_mul(SA, SB, backend=backend)
+        ref, _ = oracle.karatsuba(e, ctx.f, oracle.sliced_random(e, m, k, 1), oracle.sliced_random(e, k, n, 2),
+                                  m, k, n)
+        assert np.array_equal(C.to_numpy(), ref), (m, k, n, backend)
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_errors_match_reference(g, backend):
+    A = g.SlicedMatrix.random(g.field_new(4), 5, 6, 1)
+    B = g.SlicedMatrix.random(g.field_new(4), 7, 5, 2)
+    with pytest.raises(ValueError, match="inner dimensions differ"):
+        g.karatsuba_mul(A, B, backend=backend)
+    B8 = g.SlicedMatrix.random(g.field_new(8), 6, 5, 2)
+    with pytest.raises(ValueError, match="field mismatch"):
+        g.karatsuba_mul(A, B8, backend=backend)
+    with pytest.raises(ValueError, match="unknown multiplication strategy"):
+        g.mul(A.slices[0], g.BitMatrix.random(6, 3, 1), strategy="bogus")
+
+
+def test_config1_full(g):
+    # BASELINE config 1: F_4, 1024^3, bit-exact vs the oracle restatement of the reference
+    e, m = 2, 1024
+    ctx = g.field_new(e)
+    A = g.PackedMatrix.random(ctx, m, m, 1)
+    B = g.PackedMatrix.random(ctx, m, m, 2)
+    C = g.karatsuba_mul_packed(A, B)
+    ref, _ = oracle.karatsuba(e, ctx.f, oracle.sliced_random(e, m, m, 1), oracle.sliced_random(e, m, m, 2), m, m, m)
+    assert np.array_equal(C.to_numpy(), oracle.cling_words(e, m, m, ref))
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_config2_full(g, backend):
+    # BASELINE config 2: F_16, 4096^3, packed -> sliced -> product -> packed
+    e, m = 4, 4096
+    ctx = g.field_new(e)
+    A = g.PackedMatrix.random(ctx, m, m, 1)
+    B = g.PackedMatrix.random(ctx, m, m, 2)
+    C = g.karatsuba_mul_packed(A, B, backend=backend)
+    ref, _ = oracle.karatsuba(e, ctx.f, oracle.sliced_random(e, m, m, 1), oracle.sliced_random(e, m, m, 2), m, m, m)
+    assert np.array_equal(C.to_numpy(), oracle.cling_words(e, m, m, ref))
+
+
+def _sampled_blocks(g, e, m, k, n, accumulate, rows, col_block, backend="tc"):
+    """C[R, S] = A[R, :] . B[:, S] (^ C0[R, S]) via the windowed generator."""
+    ctx = g.field_new(e)
+    SA = g.SlicedMatrix.random(ctx, m, k, 1)
+    SB = g.SlicedMatrix.random(ctx, k, n, 2)
+    if accumulate:
+        C = g.SlicedMatrix.random(ctx, m, n, 3)
+        g.addmul(C, SA, SB, backend=backend)
+    else:
+        C = g.karatsuba_mul(SA, SB, backend=backend)
+    _sync()
+    c0, c1 = col_block
+    got = C.planes[:, rows, c0 // 64:c1 // 64]
+    got = got.cpu().numpy().view(np.uint64)
+    for i, r in enumerate(rows):
+        a = oracle.sliced_random(e, 1, k, 1, row0=r, gcols=k)
+        b = oracle.sliced_random(e, k, c1 - c0, 2, col0=c0, gcols=n)
+        ref, _ = oracle.karatsuba(e, ctx.f, a, b, 1, k, c1 - c0)
+        if accumulate:
+            ref ^= oracle.sliced_random(e, 1, c1 - c0, 3, row0=r, col0=c0, gcols=n)
+        assert np.array_equal(got[:, i:i + 1, :], ref), (r, col_block)
+
+
+@pytest.mark.slow
+def test_config3_sampled_blocks(g):
+    # BASELINE config 3: F_256, 16384^3 on one GPU; sampled rows x 256-column blocks
+    rows = [0, 1, 127, 128, 8191, 16383]
+    _sampled_blocks(g, 8, 16384, 16384, 16384, False, rows, (16128, 16384))
+    _sampled_blocks(g, 8, 16384, 16384, 16384, False, [5, 9000], (0, 256))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("e", [2, 5, 8, 10])
+def test_config4_sampled_blocks(g, e):
+    # BASELINE config 4: C += A.B, A 65536x256, B 256x65536, C pre-filled (seed 3)
+    _sampled_blocks(g, e, 65536, 256, 65536, True, [0, 77, 32768, 65535], (65536 - 512, 65536))
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_linearity_and_addmul_consistency(g, backend):
+    # size-independent properties: (A1 + A2).B = A1.B + A2.B ; addmul == C0 + mul
+    e, m, k, n = 7, 700, 900, 600
+    ctx = g.field_new(e)
+    A1 = g.SlicedMatrix.random(ctx, m, k, 11)
+    A2 = g.SlicedMatrix.random(ctx, m, k, 12)
+    B = g.SlicedMatrix.random(ctx, k, n, 13)
+    lhs = g.karatsuba_mul(A1 ^ A2, B, backend=backend)
+    rhs = g.karatsuba_mul(A1, B, backend=backend) ^ g.karatsuba_mul(A2, B, backend=backend)
+    assert lhs == rhs
+    C0 = g.SlicedMatrix.random(ctx, m, n, 14)
+    D = C0.copy()
+    g.addmul(D, A1, B, backend=backend)
+    assert D == (C0 ^ g.karatsuba_mul(A1, B, backend=backend))
+
+
+def test_backends_agree_large(g):
+    e, m, k, n = 8, 2048, 2048, 2048
+    ctx = g.field_new(e)
+    A = g.SlicedMatrix.random(ctx, m, k, 1)
+    B = g.SlicedMatrix.random(ctx, k, n, 2)
+    assert g.karatsuba_mul(A, B, backend="tc") == g.karatsuba_mul(A, B, backend="m4rm")
+
+
+def test_native_code_used(g):
+    ctx = g.field_new(8)
+    A = g.SlicedMatrix.random(ctx, 256, 256, 1)
+    g.karatsuba_mul(A, A)
+    assert g._lib.last_product_kernel() == "k_product_tc"
+    assert g._lib.last_launch_count() == 3  # combos(A), combos(B^T), fused product
