@@ -40,6 +40,7 @@ extern "C" {
 #define GF2E_ACCUMULATE 1u   /* C ^= A*B (addmul) instead of C = A*B              */
 #define GF2E_BACKEND_TC 0u   /* K4 on tcgen05 kind::i8 tensor cores (default)     */
 #define GF2E_BACKEND_M4RM 2u /* K4 as M4RM Gray tables in shared memory (INT pipe) */
+#define GF2E_TC_1CTA 4u      /* tensor-core K4 on single CTAs (cta_group::1) instead of CTA pairs */
 
 /* Last error message of the calling thread ("" if none). */
 const char *gf2e_last_error(void);
@@ -147,6 +148,13 @@ const char *gf2e_last_product_kernel(void);
  * events and returns the summed duration (ms) and the number of launches, then clears.
  */
 int gf2e_profile_enable(int on);
+/*
+ * Pure-MMA microbenchmark (no operand production, no epilogue): tcgen05.mma kind::i8 with
+ * cta_group 1 (M=128,N=256,K=32) or 2 (M=256,N=256,K=32) on every SM for `iters` x 4
+ * instructions.  Returns the measured dense int8 tensor rate (ops/s, 2 per MAC) in *tops
+ * (units of 1e12) and the launch time in *ms.  The roofline denominator of bench.py.
+ */
+int gf2e_mma_peak(int cta_group, int iters, double *tops, double *ms, void *stream);
 int gf2e_profile_read(double *total_ms, int *launches);
 
 #ifdef __cplusplus

@@ -18,6 +18,7 @@ GF2E_OK, GF2E_EINVAL, GF2E_ECUDA, GF2E_ENOMEM, GF2E_ENODEV = 0, 1, 2, 3, 4
 ACCUMULATE = 1
 BACKEND_TC = 0
 BACKEND_M4RM = 2
+TC_1CTA = 4
 
 _I64 = ctypes.c_int64
 _U64 = ctypes.c_uint64
@@ -48,6 +49,7 @@ SIGNATURES = {
     "gf2e_last_product_kernel": (ctypes.c_char_p, []),
     "gf2e_profile_enable": (_INT, [_INT]),
     "gf2e_profile_read": (_INT, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_INT)]),
+    "gf2e_mma_peak": (_INT, [_INT, _INT, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
 }
 
 _lib = None
@@ -101,6 +103,17 @@ def profile_read() -> tuple[float, int]:
     n = ctypes.c_int()
     check(load().gf2e_profile_read(ctypes.byref(ms), ctypes.byref(n)), "gf2e_profile_read")
     return ms.value, n.value
+
+
+def mma_peak(cta_group: int = 1, iters: int = 20000) -> tuple[float, float]:
+    """Measured dense kind::i8 tensor rate (TOPS) and launch ms (gf2e_mma_peak)."""
+    import torch
+
+    tops = ctypes.c_double()
+    ms = ctypes.c_double()
+    check(load().gf2e_mma_peak(cta_group, iters, ctypes.byref(tops), ctypes.byref(ms),
+                               torch.cuda.current_stream().cuda_stream), "gf2e_mma_peak")
+    return tops.value, ms.value
 
 
 def last_product_kernel() -> str:

@@ -249,7 +249,7 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags) {
         L.a_pstride = L.m_pad * L.kwords;
         L.b_pstride = L.k_pad * (L.n_pad / 64);
     } else {
-        L.m_pad = round_up(m, kTcBM);
+        L.m_pad = round_up(m, 2 * kTcBM);  // CTA-pair tiles are 256 rows
         L.n_pad = round_up(n, kTcBN);
         L.k_pad = round_up(k, kTcBK);
         L.kwords = L.k_pad / 64;
@@ -299,14 +299,19 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
            "combos(B^T)");
         TcArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, m, n, L.m_pad, L.n_pad, C, ldc, pc, acc ? 1 : 0};
         ProfScope prof(st);
-        CK(launch_product_tc(ks, a, st), "product_tc");
-        g_kernel = "k_product_tc";
+        if (flags & GF2E_TC_1CTA) {
+            CK(launch_product_tc(ks, a, st), "product_tc");
+            g_kernel = "k_product_tc";
+        } else {
+            CK(launch_product_tc2(ks, a, st), "product_tc2");
+            g_kernel = "k_product_tc2";
+        }
     }
     return GF2E_OK;
 }
 
 int check_flags(uint32_t flags) {
-    if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM)) return fail(GF2E_EINVAL, "unknown flags 0x%x", flags);
+    if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM | GF2E_TC_1CTA)) return fail(GF2E_EINVAL, "unknown flags 0x%x", flags);
     return GF2E_OK;
 }
 
@@ -345,6 +350,24 @@ int gf2e_profile_read(double *total_ms, int *launches) {
     if (total_ms) *total_ms = tot;
     if (launches) *launches = (int)evs.size();
     return rc;
+}
+
+int gf2e_mma_peak(int cta_group, int iters, double *tops, double *ms, void *stream) {
+    g_err.clear();
+    if (cta_group != 1 && cta_group != 2) return fail(GF2E_EINVAL, "cta_group must be 1 or 2");
+    if (iters < 1) return fail(GF2E_EINVAL, "iters must be >= 1");
+    if (int rc = check_device()) return rc;
+    int dev = 0, nsms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsms, cudaDevAttrMultiProcessorCount, dev);
+    float t = 0;
+    cudaError_t e = run_mma_peak(cta_group, iters, nsms, (cudaStream_t)stream, &t);
+    if (e != cudaSuccess) return cuda_fail(e, "mma_peak");
+    const int sms_used = cta_group == 2 ? (nsms & ~1) : nsms;
+    const double ops = (double)sms_used * iters * 4.0 * 2.0 * 128.0 * 256.0 * 32.0;
+    if (ms) *ms = t;
+    if (tops) *tops = ops / (t * 1e-3) / 1e12;
+    return GF2E_OK;
 }
 
 int gf2e_pack_width(int e) {

@@ -43,6 +43,8 @@ struct TcArgs {
 };
 constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 128;  // tile rows, tile cols, k-bits per stage
 cudaError_t launch_product_tc(const Sched &s, const TcArgs &a, cudaStream_t st);
+// CTA-pair variant (product_tc2.cu): m_pad must be a multiple of 256.
+cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, cudaStream_t st);
 
 // INT-pipe M4RM product (product_m4rm.cu).  Operands: Ac as above, Bc [nprod][k_pad][n_pad/64].
 struct M4rmArgs {
@@ -59,5 +61,7 @@ struct M4rmArgs {
 };
 constexpr int kM4BM = 512, kM4BN = 1024, kM4KPAD = 64;
 cudaError_t launch_product_m4rm(const Sched &s, const M4rmArgs &a, cudaStream_t st);
+
+cudaError_t run_mma_peak(int cta_group, int iters, int nsms, cudaStream_t st, float *ms);
 
 }  // namespace gf2e

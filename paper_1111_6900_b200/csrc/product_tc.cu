@@ -26,9 +26,11 @@
 //              (2 x 256 columns) to the epilogue.
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_common.cuh"
 
 namespace gf2e {
 namespace {
+using namespace tc;
 
 constexpr int BM = kTcBM, BN = kTcBN, BK = kTcBK;
 constexpr int S = 3;  // expanded operand stages
@@ -51,45 +53,6 @@ struct __align__(8) Bars {
     uint16_t outmask[kMaxProducts];
 };
 constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + (int)sizeof(Bars) + 1024;
-
-// byte offset of 16-byte chunk c of row r in a K-major SWIZZLE_128B tile (8-row atoms of 1 KiB)
-__device__ __forceinline__ uint32_t swz(int r, int c) {
-    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
-}
-
-template <bool kReversed>
-__device__ __forceinline__ void expand_row(uint8_t *tile, int r, uint4 w4) {
-    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        uint32_t o[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = w[q] & (kReversed ? (0x80808080u >> i) : (0x01010101u << i));
-        *reinterpret_cast<uint4 *>(tile + swz(r, 2 * q)) = make_uint4(o[0], o[1], o[2], o[3]);
-        *reinterpret_cast<uint4 *>(tile + swz(r, 2 * q + 1)) = make_uint4(o[4], o[5], o[6], o[7]);
-    }
-}
-
-// 32 parity bits (bit 7 of each s32 accumulator) packed into one word with 3 PRMT per 4
-// values plus one shift+LOP3 per 4 values.  Result bit 8b+g = parity of v[4g+b]; the
-// producers load B^T rows in the matching order (b_row_perm) so this is column n0+8b+g.
-__device__ __forceinline__ uint32_t parity_word(const uint32_t (&v)[32]) {
-    uint32_t r = 0;
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        const uint32_t lo = __byte_perm(v[4 * g], v[4 * g + 1], 0x0040);
-        const uint32_t hi = __byte_perm(v[4 * g + 2], v[4 * g + 3], 0x0040);
-        const uint32_t z = __byte_perm(lo, hi, 0x5410);  // bytes: v[4g].b0 .. v[4g+3].b0
-        r |= (z >> (7 - g)) & (0x01010101u << g);
-    }
-    return r;
-}
-
-// TMEM column j (= B smem row j) of every 32-column group holds tile column b_row_perm(j).
-__host__ __device__ __forceinline__ int b_row_perm(int j) {
-    const int g = (j & 31) >> 2, b = j & 3;
-    return (j & ~31) | (8 * b + g);
-}
 
 template <int E>
 __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc(const Sched s, const TcArgs a) {

@@ -1,0 +1,306 @@
+// product_tc2.cu — the fused Karatsuba product kernel on CTA PAIRS (tcgen05 cta_group::2).
+//
+// Same contract and arithmetic as product_tc.cu (reference: karatsuba_mul poly_mul.py:245-259,
+// _kara 166-220, mat_gf2.mul mat_gf2.py:425-455, reduce_mod_f poly_mul.py:223-242), but each
+// cluster of 2 CTAs owns a 256 x 256 tile of C and issues M=256 N=256 K=32 MMAs:
+//   CTA r (r = cluster rank) expands A rows [128r, 128r+128) and B^T rows [128r, 128r+128)
+//   of the tile, so per SM the producers write 32 KiB of 0/1 bytes per 128-bit k-stage
+//   instead of 48 KiB and the tensor core reads 32 KiB instead of 48 KiB — shared-memory
+//   bandwidth, not the tensor pipe, bounds the 1-CTA kernel (profiles/r01).
+//   The leader (rank 0) issues the MMAs; accumulators land in each CTA's own TMEM (its 128
+//   rows x 256 columns, double buffered), so the epilogue is unchanged per CTA.
+// Synchronisation across the pair:
+//   full[s]   (leader)   <- 4 producer warps x 2 CTAs (remote arrive, release.cluster)
+//   empty[s]  (each CTA) <- tcgen05.commit multicast to both CTAs
+//   tfull[b]  (each CTA) <- tcgen05.commit multicast to both CTAs
+//   tempty[b] (leader)   <- 8 epilogue warps x 2 CTAs (remote arrive)
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace gf2e {
+namespace {
+using namespace tc;
+
+constexpr int BM = 128;    // rows per CTA (tile = 2 x BM)
+constexpr int BNH = 128;   // B^T rows per CTA (tile N = 2 x BNH = 256)
+constexpr int BN = 256;
+constexpr int BK = kTcBK;  // 128 k-bits per stage
+constexpr int S = 5;       // expanded operand stages
+constexpr int D = 8;       // bit-tile staging depth
+constexpr int NPW = 4;     // producer warps
+constexpr int NEW = 8;     // epilogue warps
+constexpr int MMA_WARP = NPW + NEW;
+constexpr int NTHREADS = (NPW + NEW + 1) * 32;
+constexpr int A_BYTES = BM * BK;   // 16 KiB
+constexpr int B_BYTES = BNH * BK;  // 16 KiB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BITS_A = BM * (BK / 8);
+constexpr int BITS_BYTES = (BM + BNH) * (BK / 8);  // 4 KiB
+constexpr int TMEM_COLS = 512;
+constexpr uint32_t IDESC = idesc_i8(2 * BM, BN);
+
+struct __align__(8) Bars {
+    uint64_t full[S], empty[S], tfull[2], tempty[2];
+    uint32_t tmem_base;
+    uint16_t outmask[kMaxProducts];
+};
+constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + (int)sizeof(Bars) + 1024;
+
+template <int E>
+__global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, const TcArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *stages = smem;
+    uint8_t *bits = smem + S * STAGE_BYTES;
+    Bars *bars = reinterpret_cast<Bars *>(bits + D * BITS_BYTES);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+    const int64_t tiles_n = a.n_pad / BN;
+    const int64_t ntiles = (a.m_pad / (2 * BM)) * tiles_n;
+    const int64_t my_tiles = ntiles > cluster ? (ntiles - cluster + nclusters - 1) / nclusters : 0;
+    const int nks = (int)(a.kwords / (BK / 64));
+    const int64_t per_tile = (int64_t)s.nprod * nks;
+    const int64_t total = my_tiles * per_tile;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&bars->full[i], 2 * NPW);
+            mbar_init(&bars->empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->tfull[i], 1);
+            mbar_init(&bars->tempty[i], 2 * NEW);
+        }
+        mbar_fence_init();
+    }
+    if (threadIdx.x < kMaxProducts) bars->outmask[threadIdx.x] = s.outmask[threadIdx.x];
+    if (warp == MMA_WARP) tmem_alloc2(&bars->tmem_base, TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+
+    if (warp < NPW) {
+        // ===================== producers (both CTAs) =====================
+        const int p = threadIdx.x;  // A row and B^T row of this CTA's half
+        const int64_t offA = (int64_t)(rank * BM + p) * a.kwords;
+        const int64_t offB = (int64_t)b_row_perm((int)rank * BNH + p) * a.kwords;
+        const uint32_t bits_s = smem_u32(bits);
+        const uint32_t full_leader = mapa(smem_u32(&bars->full[0]), 0);
+        int64_t i_tile = cluster;
+        int i_t = 0, i_ks = 0, i_slot = 0;
+        const uint64_t *Ab = nullptr, *Bb = nullptr;
+        auto set_base = [&]() {
+            const int64_t m0 = (i_tile / tiles_n) * (2 * BM), n0 = (i_tile % tiles_n) * BN;
+            Ab = a.Ac + m0 * a.kwords + offA;
+            Bb = a.Bt + n0 * a.kwords + offB;
+        };
+        set_base();
+        auto issue = [&]() {
+            const uint32_t slot = bits_s + (uint32_t)(i_slot * BITS_BYTES);
+            const int64_t koff = i_ks * (BK / 64);
+            cp_async16(slot + p * 16, Ab + i_t * a.a_pstride + koff);
+            cp_async16(slot + BITS_A + p * 16, Bb + i_t * a.b_pstride + koff);
+            if (++i_slot == D) i_slot = 0;
+            if (++i_ks == nks) {
+                i_ks = 0;
+                if (++i_t == s.nprod) {
+                    i_t = 0;
+                    i_tile += nclusters;
+                    if (i_tile < ntiles) set_base();
+                }
+            }
+        };
+        for (int i = 0; i < D - 1; ++i) {
+            if (i < total) issue();
+            cp_async_commit();
+        }
+        int c_slot = 0, st = 0;
+        uint32_t phase = 0;
+        for (int64_t it = 0; it < total; ++it) {
+            if (it + D - 1 < total) issue();
+            cp_async_commit();
+            cp_async_wait<D - 1>();
+            const uint8_t *slot = bits + c_slot * BITS_BYTES;
+            const uint4 wa = *reinterpret_cast<const uint4 *>(slot + p * 16);
+            const uint4 wb = *reinterpret_cast<const uint4 *>(slot + BITS_A + p * 16);
+            mbar_wait(&bars->empty[st], phase ^ 1);
+            uint8_t *sa = stages + st * STAGE_BYTES;
+            expand_row<false>(sa, p, wa);
+            expand_row<true>(sa + A_BYTES, p, wb);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(full_leader + (uint32_t)(st * 8));
+            if (++c_slot == D) c_slot = 0;
+            if (++st == S) {
+                st = 0;
+                phase ^= 1;
+            }
+        }
+        cp_async_wait<0>();
+    } else if (warp < MMA_WARP) {
+        // ===================== epilogue (both CTAs) =====================
+        const int ew = warp - NPW;
+        const int q = warp & 3;  // TMEM lane quarter (hardware: warp id % 4)
+        const int h = ew >> 2;   // column half
+        const int row_local = (int)rank * BM + q * 32 + lane;
+        const int64_t nw = words_for(a.n);
+        const uint32_t tempty_leader = mapa(smem_u32(&bars->tempty[0]), 0);
+        int64_t gp = 0;
+        for (int64_t ti = 0; ti < my_tiles; ++ti) {
+            const int64_t tile = cluster + ti * nclusters;
+            const int64_t m0 = (tile / tiles_n) * (2 * BM), n0 = (tile % tiles_n) * BN;
+            uint32_t acc[E][4];
+#pragma unroll
+            for (int j = 0; j < E; ++j)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[j][c] = 0;
+            for (int t = 0; t < s.nprod; ++t, ++gp) {
+                const int buf = (int)(gp & 1);
+                mbar_wait(&bars->tfull[buf], (uint32_t)((gp >> 1) & 1));
+                tc_fence_after();
+                const uint32_t mask = bars->outmask[t];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + c * 32), v);
+                    tmem_wait_ld();
+                    const uint32_t pw = parity_word(v);
+#pragma unroll
+                    for (int j = 0; j < E; ++j) acc[j][c] ^= pw & (0u - ((mask >> j) & 1u));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+            }
+            const int64_t row = m0 + row_local;
+            if (row < a.m) {
+                const int64_t w0 = (n0 >> 6) + 2 * h;
+                const bool v0 = w0 < nw, v1 = w0 + 1 < nw;
+#pragma unroll
+                for (int j0 = 0; j0 < E; j0 += 4) {  // C0 loads of up to 4 planes in flight per batch
+                    uint64_t old[4][2];
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const int j = j0 + jj;
+                        if (j < E) {
+                            const uint64_t *crow = a.C + j * a.c_pstride + row * a.ldc + w0;
+                            old[jj][0] = (a.accumulate && v0) ? crow[0] : 0;
+                            old[jj][1] = (a.accumulate && v1) ? crow[1] : 0;
+                        }
+                    }
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const int j = j0 + jj;
+                        if (j < E) {
+                            uint64_t *crow = a.C + j * a.c_pstride + row * a.ldc + w0;
+                            const uint64_t x0 = ((uint64_t)acc[j][0] | ((uint64_t)acc[j][1] << 32)) ^ old[jj][0];
+                            const uint64_t x1 = ((uint64_t)acc[j][2] | ((uint64_t)acc[j][3] << 32)) ^ old[jj][1];
+                            if (v0 && v1 && !(reinterpret_cast<uintptr_t>(crow) & 15)) {
+                                *reinterpret_cast<ulonglong2 *>(crow) = make_ulonglong2(x0, x1);
+                            } else {
+                                if (v0) crow[0] = x0;
+                                if (v1) crow[1] = x1;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    } else if (rank == 0) {
+        // ===================== MMA issuer (leader CTA, one thread) =====================
+        if (lane == 0) {
+            int64_t gp = 0;
+            int st = 0;
+            uint32_t phase = 0;
+            const uint32_t st0 = smem_u32(stages);
+            for (int64_t ti = 0; ti < my_tiles; ++ti) {
+                for (int t = 0; t < s.nprod; ++t, ++gp) {
+                    const int buf = (int)(gp & 1);
+                    mbar_wait_cluster(&bars->tempty[buf], (uint32_t)((gp >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t dt = tmem + (uint32_t)(buf * BN);
+                    for (int ks = 0; ks < nks; ++ks) {
+                        mbar_wait_cluster(&bars->full[st], phase);
+                        tc_fence_after();
+                        const uint32_t sa = st0 + (uint32_t)(st * STAGE_BYTES);
+                        const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+                        for (int kk = 0; kk < BK / 32; ++kk)
+                            mma2_i8(dt, umma_desc_sw128(sa + kk * 32), umma_desc_sw128(sb + kk * 32), IDESC,
+                                    (ks | kk) != 0);
+                        mma2_commit_both(&bars->empty[st]);
+                        if (++st == S) {
+                            st = 0;
+                            phase ^= 1;
+                        }
+                    }
+                    mma2_commit_both(&bars->tfull[buf]);
+                }
+            }
+        }
+        __syncwarp();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // all MMAs of the pair retired (every epilogue saw its last tfull)
+    if (warp == MMA_WARP) {
+        tc_fence_after();
+        tmem_dealloc2(tmem, TMEM_COLS);
+    }
+}
+
+int g_num_sms2 = 0;
+
+template <int E>
+cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
+    cudaError_t err = cudaFuncSetAttribute(k_product_tc2<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    const int64_t tiles = (a.m_pad / (2 * BM)) * (a.n_pad / BN);
+    if (tiles == 0) return cudaSuccess;
+    if (g_num_sms2 == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms2, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms2 <= 1) g_num_sms2 = 148;
+    }
+    const int64_t clusters = tiles < g_num_sms2 / 2 ? tiles : g_num_sms2 / 2;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(2 * clusters));
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_product_tc2<E>, s, a);
+}
+
+}  // namespace
+
+cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, cudaStream_t st) {
+    switch (s.nout) {
+        case 1: return launch_e<1>(s, a, st);
+        case 2: return launch_e<2>(s, a, st);
+        case 3: return launch_e<3>(s, a, st);
+        case 4: return launch_e<4>(s, a, st);
+        case 5: return launch_e<5>(s, a, st);
+        case 6: return launch_e<6>(s, a, st);
+        case 7: return launch_e<7>(s, a, st);
+        case 8: return launch_e<8>(s, a, st);
+        case 9: return launch_e<9>(s, a, st);
+        case 10: return launch_e<10>(s, a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace gf2e

@@ -1,0 +1,108 @@
+// tc_common.cuh — device helpers shared by the tcgen05 product kernels (product_tc*.cu):
+// operand expansion into the UMMA K-major SWIZZLE_128B layout, the bit-7 parity packer of
+// the epilogue, and cluster (2-SM) PTX wrappers.
+#pragma once
+#include "common.cuh"
+
+namespace gf2e {
+namespace tc {
+
+// byte offset of 16-byte chunk c of row r in a K-major SWIZZLE_128B tile (8-row atoms of 1 KiB)
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+
+template <bool kReversed>
+__device__ __forceinline__ void expand_row(uint8_t *tile, int r, uint4 w4) {
+    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = w[q] & (kReversed ? (0x80808080u >> i) : (0x01010101u << i));
+        *reinterpret_cast<uint4 *>(tile + swz(r, 2 * q)) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4 *>(tile + swz(r, 2 * q + 1)) = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+}
+
+// 32 parity bits (bit 7 of each s32 accumulator) packed into one word with 3 PRMT per 4
+// values plus one shift+LOP3 per 4 values.  Result bit 8b+g = parity of v[4g+b]; the
+// producers load B^T rows in the matching order (b_row_perm) so this is column n0+8b+g.
+__device__ __forceinline__ uint32_t parity_word(const uint32_t (&v)[32]) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        const uint32_t lo = __byte_perm(v[4 * g], v[4 * g + 1], 0x0040);
+        const uint32_t hi = __byte_perm(v[4 * g + 2], v[4 * g + 3], 0x0040);
+        const uint32_t z = __byte_perm(lo, hi, 0x5410);  // bytes: v[4g].b0 .. v[4g+3].b0
+        r |= (z >> (7 - g)) & (0x01010101u << g);
+    }
+    return r;
+}
+
+// TMEM column j (= B smem row j) of every 32-column group holds tile column b_row_perm(j).
+__host__ __device__ __forceinline__ int b_row_perm(int j) {
+    const int g = (j & 31) >> 2, b = j & 3;
+    return (j & ~31) | (8 * b + g);
+}
+
+
+// ---- cluster (CTA pair) helpers ----------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem offset in CTA `rank` of this cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra.uni DONEC_%=;\n\t"
+        "bra.uni WAITC_%=;\n"
+        "DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t *dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// D[tmem, both CTAs] (+)= A[smem, both CTAs: 2 x 128 rows] . B[smem, both CTAs: 2 x N/2 rows]^T
+__device__ __forceinline__ void mma2_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive on the barrier at this smem offset in both CTAs of the pair once all prior MMAs finish
+__device__ __forceinline__ void mma2_commit_both(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+}  // namespace tc
+}  // namespace gf2e

@@ -75,7 +75,8 @@ def test_workspace_sizes():
     assert ws == 27 * 2 * 16384 * 16384 // 8
     assert L.gf2e_slice_mul_workspace(8, 0x11D, 0, 5, 5, 0) == 0
     assert L.gf2e_slice_mul_workspace(8, 0x11D, 5, 5, 5, 1 << 7) == -1  # bad flag
-    assert L.gf2e_plane_mul_workspace(100, 1, 300, 0) == (128 * 128 + 512 * 128) // 8
+    # m padded to the 256-row CTA-pair tile, n to 256 columns, k to 128-bit stages
+    assert L.gf2e_plane_mul_workspace(100, 1, 300, 0) == (256 * 128 + 512 * 128) // 8
 
 
 def test_invalid_arguments_fail_before_device():

@@ -8,7 +8,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-BACKENDS = ["tc", "m4rm"]
+BACKENDS = ["tc", "tc1", "m4rm"]
 
 
 @pytest.fixture(scope="module")
@@ -242,5 +242,5 @@ def test_native_code_used(g):
     ctx = g.field_new(8)
     A = g.SlicedMatrix.random(ctx, 256, 256, 1)
     g.karatsuba_mul(A, A)
-    assert g._lib.last_product_kernel() == "k_product_tc"
+    assert g._lib.last_product_kernel() == "k_product_tc2"
     assert g._lib.last_launch_count() == 3  # combos(A), combos(B^T), fused product
