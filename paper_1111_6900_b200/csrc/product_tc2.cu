@@ -10,7 +10,7 @@
 //   The leader (rank 0) issues the MMAs; accumulators land in each CTA's own TMEM (its 128
 //   rows x 256 columns, double buffered), so the epilogue is unchanged per CTA.
 // Synchronisation across the pair:
-//   full[s]   (leader)   <- 4 producer warps x 2 CTAs (remote arrive, release.cluster)
+//   full[s]   (leader)   <- 4 producer warps x 2 CTAs (remote arrive after fence.proxy.async)
 //   empty[s]  (each CTA) <- tcgen05.commit multicast to both CTAs
 //   tfull[b]  (each CTA) <- tcgen05.commit multicast to both CTAs
 //   tempty[b] (leader)   <- 8 epilogue warps x 2 CTAs (remote arrive)
@@ -221,11 +221,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             for (int64_t ti = 0; ti < my_tiles; ++ti) {
                 for (int t = 0; t < s.nprod; ++t, ++gp) {
                     const int buf = (int)(gp & 1);
-                    mbar_wait_cluster(&bars->tempty[buf], (uint32_t)((gp >> 1) & 1) ^ 1);
+                    mbar_wait(&bars->tempty[buf], (uint32_t)((gp >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t dt = tmem + (uint32_t)(buf * BN);
                     for (int ks = 0; ks < nks; ++ks) {
-                        mbar_wait_cluster(&bars->full[st], phase);
+                        mbar_wait(&bars->full[st], phase);
                         tc_fence_after();
                         const uint32_t sa = st0 + (uint32_t)(st * STAGE_BYTES);
                         const uint32_t sb = sa + A_BYTES;

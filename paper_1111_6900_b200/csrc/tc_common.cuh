@@ -62,8 +62,13 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
     return r;
 }
+// Remote arrive on the pair leader's barrier.  Relaxed on purpose: release.cluster compiles
+// to MEMBAR.ALL.GPU, which would drain this thread's in-flight cp.async prefetches every
+// stage.  Producers order their st.shared before it with fence.proxy.async.shared::cta
+// (MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC.S); the epilogue's TMEM reads are complete after
+// tcgen05.wait::ld.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
     asm volatile(
