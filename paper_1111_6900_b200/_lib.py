@@ -18,7 +18,6 @@ GF2E_OK, GF2E_EINVAL, GF2E_ECUDA, GF2E_ENOMEM, GF2E_ENODEV = 0, 1, 2, 3, 4
 ACCUMULATE = 1
 BACKEND_TC = 0
 BACKEND_M4RM = 2
-TC_1CTA = 4
 
 _I64 = ctypes.c_int64
 _U64 = ctypes.c_uint64

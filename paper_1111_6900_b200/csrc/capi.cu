@@ -283,10 +283,11 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
         return fail(GF2E_EINVAL, "workspace must be a 256-byte aligned device pointer");
     uint64_t *Ac = static_cast<uint64_t *>(ws);
     uint64_t *Bx = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + L.a_bytes);
-    CK(launch_combos_rows(ks, A, lda, pa, m, k, Ac, L.kwords, L.a_pstride, L.m_pad, L.kwords, st), "combos(A)");
-    if (flags & GF2E_BACKEND_M4RM) {
+    const bool tc = !(flags & GF2E_BACKEND_M4RM);
+    CK(launch_combos_rows(ks, A, lda, pa, m, k, Ac, L.kwords, L.a_pstride, L.m_pad, L.kwords, tc, st), "combos(A)");
+    if (!tc) {
         const int64_t nwp = L.n_pad / 64;
-        CK(launch_combos_rows(ks, B, ldb, pb, k, n, Bx, nwp, L.b_pstride, L.k_pad, nwp, st), "combos(B)");
+        CK(launch_combos_rows(ks, B, ldb, pb, k, n, Bx, nwp, L.b_pstride, L.k_pad, nwp, false, st), "combos(B)");
         if (!acc)
             for (int j = 0; j < ks.nout; ++j)
                 CK(cudaMemset2DAsync(C + j * pc, ldc * 8, 0, nw * 8, m, st), "cudaMemset2DAsync");
@@ -299,19 +300,14 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
            "combos(B^T)");
         TcArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, m, n, L.m_pad, L.n_pad, C, ldc, pc, acc ? 1 : 0};
         ProfScope prof(st);
-        if (flags & GF2E_TC_1CTA) {
-            CK(launch_product_tc(ks, a, st), "product_tc");
-            g_kernel = "k_product_tc";
-        } else {
-            CK(launch_product_tc2(ks, a, st), "product_tc2");
-            g_kernel = "k_product_tc2";
-        }
+        CK(launch_product_tc2(ks, a, st), "product_tc2");
+        g_kernel = "k_product_tc2";
     }
     return GF2E_OK;
 }
 
 int check_flags(uint32_t flags) {
-    if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM | GF2E_TC_1CTA)) return fail(GF2E_EINVAL, "unknown flags 0x%x", flags);
+    if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM)) return fail(GF2E_EINVAL, "unknown flags 0x%x", flags);
     return GF2E_OK;
 }
 

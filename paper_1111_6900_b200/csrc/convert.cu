@@ -189,9 +189,11 @@ __global__ void k_reduce(int e, uint32_t f, uint64_t *__restrict__ planes, int64
 // ---- K3 operand combinations --------------------------------------------------------
 
 // out[t] = XOR_{i in S_t} X_i on a zero-padded (rows_pad x words_pad) grid, natural bit order.
+// tiled: write the stage-tiled layout of the tensor-core kernel (tc_tile_word) instead of
+// row-major rows of ldo words.
 __global__ void k_combos_rows(Sched s, const uint64_t *__restrict__ X, int64_t ldx, int64_t px, int64_t rows,
                               int64_t ncols, uint64_t *__restrict__ out, int64_t ldo, int64_t po,
-                              int64_t rows_pad, int64_t words_pad) {
+                              int64_t rows_pad, int64_t words_pad, int tiled) {
     const int64_t nw = words_for(ncols);
     const uint64_t tm = tail_mask(ncols);
     const int64_t total = rows_pad * words_pad;
@@ -209,7 +211,7 @@ __global__ void k_combos_rows(Sched s, const uint64_t *__restrict__ X, int64_t l
             uint64_t acc = 0;
 #pragma unroll
             for (int i = 0; i < kMaxE; ++i) acc ^= x[i] & (0ULL - (uint64_t)((sub >> i) & 1u));
-            out[t * po + r * ldo + w] = acc;
+            out[t * po + (tiled ? tc_tile_word(r, w, words_pad) : r * ldo + w)] = acc;
         }
     }
 }
@@ -239,8 +241,9 @@ __device__ __forceinline__ void transpose64(uint64_t &xa, uint64_t &xb, int lane
 
 // Bt[t] = (XOR_{i in S_t} B_i)^T: row n holds the k-bits of column n of B, with the bit
 // order reversed inside every byte (k-bit 8q+i at position 8q+7-i) — the layout the
-// tensor-core producer expands with one AND per output word (product_tc.cu).
-// One warp per 64x64 block; zero padded to n_pad rows x k_pad bits.
+// tensor-core producer expands with one AND per output word (product_tc2.cu) — stored
+// stage-tiled with the rows of every 32-row group in tc_b_row_inv order (the epilogue's
+// parity packer emits columns in b_row_perm order).  One warp per 64x64 block.
 __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb, int64_t pb, int64_t k,
                             int64_t n, uint64_t *__restrict__ out, int64_t ldo, int64_t po, int64_t kblocks,
                             int64_t nblocks) {
@@ -268,9 +271,9 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
                 xb ^= b[i] & sel;
             }
             transpose64(xa, xb, lane);
-            uint64_t *o = out + t * po + (nb * 64 + lane) * ldo + kb;
-            o[0] = xa;
-            o[32 * ldo] = xb;
+            const int64_t n0 = nb * 64 + lane;
+            out[t * po + tc_tile_word(tc_b_row_inv(n0), kb, ldo)] = xa;
+            out[t * po + tc_tile_word(tc_b_row_inv(n0 + 32), kb, ldo)] = xb;
         }
     }
 }
@@ -358,11 +361,11 @@ cudaError_t launch_reduce(int e, uint32_t f, uint64_t *planes, int64_t rows, int
 
 cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, int64_t px, int64_t rows,
                                int64_t ncols, uint64_t *out, int64_t ldo, int64_t po, int64_t rows_pad,
-                               int64_t words_pad, cudaStream_t st) {
+                               int64_t words_pad, bool tiled, cudaStream_t st) {
     int64_t total = rows_pad * words_pad;
     if (total == 0) return cudaSuccess;
     k_combos_rows<<<grid_for(total, 256), 256, 0, st>>>(s, X, ldx, px, rows, ncols, out, ldo, po, rows_pad,
-                                                        words_pad);
+                                                        words_pad, tiled ? 1 : 0);
     return cudaGetLastError();
 }
 

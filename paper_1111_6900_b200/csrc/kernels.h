@@ -21,15 +21,27 @@ cudaError_t launch_xor(uint64_t *x, int64_t ldx, const uint64_t *y, int64_t ldy,
                        cudaStream_t st);
 cudaError_t launch_reduce(int e, uint32_t f, uint64_t *planes, int64_t rows, int64_t nwords, int64_t ld,
                           int64_t pstride, cudaStream_t st);
+// Stage-tiled operand layout of the tensor-core kernel: a plane of rows_pad x kwords words
+// is a sequence of tiles (row block rb = r/128, k-stage ks = w/2), each 128 rows x 2 words
+// (2 KiB) contiguous, so one bulk copy moves one stage of one operand half.
+__host__ __device__ __forceinline__ int64_t tc_tile_word(int64_t r, int64_t w, int64_t kwords) {
+    return (((r >> 7) * (kwords >> 1) + (w >> 1)) * 128 + (r & 127)) * 2 + (w & 1);
+}
+// Row order inside each 32-row group of B^T tiles: tile row j holds column b_row_perm(j)
+// (tc_common.cuh), i.e. column o sits at tile row 4*(o%8) + o/8.
+__host__ __device__ __forceinline__ int64_t tc_b_row_inv(int64_t n) {
+    const int64_t o = n & 31;
+    return (n & ~int64_t(31)) | (4 * (o & 7) + (o >> 3));
+}
 cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, int64_t px, int64_t rows,
                                int64_t ncols, uint64_t *out, int64_t ldo, int64_t po, int64_t rows_pad,
-                               int64_t words_pad, cudaStream_t st);
+                               int64_t words_pad, bool tiled, cudaStream_t st);
 cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int64_t pb, int64_t k, int64_t n,
                              uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks,
                              cudaStream_t st);
 
-// Tensor-core product (product_tc.cu).  Operands: Ac [nprod][m_pad][k_pad/64] natural bit
-// order, Bt [nprod][n_pad][k_pad/64] transposed with bits reversed in each byte.
+// Tensor-core product.  Operands: Ac [nprod] x (m_pad x k_pad bits) natural bit order,
+// Bt [nprod] x (n_pad x k_pad bits) = B^T with bits reversed in each byte.
 struct TcArgs {
     const uint64_t *Ac;
     const uint64_t *Bt;
@@ -42,8 +54,8 @@ struct TcArgs {
     int accumulate;
 };
 constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 128;  // tile rows, tile cols, k-bits per stage
-cudaError_t launch_product_tc(const Sched &s, const TcArgs &a, cudaStream_t st);
-// CTA-pair variant (product_tc2.cu): m_pad must be a multiple of 256.
+// CTA-pair tcgen05 kernel (product_tc2.cu): m_pad multiple of 256, n_pad of 256, k_pad of
+// 128; Ac / Bt in the stage-tiled layout (tc_tile_word), Bt rows in tc_b_row_inv order.
 cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, cudaStream_t st);
 
 // INT-pipe M4RM product (product_m4rm.cu).  Operands: Ac as above, Bc [nprod][k_pad][n_pad/64].

@@ -28,10 +28,11 @@ constexpr int BN = 256;
 constexpr int BK = kTcBK;  // 128 k-bits per stage
 constexpr int S = 5;       // expanded operand stages
 constexpr int D = 8;       // bit-tile staging depth
-constexpr int NPW = 4;     // producer warps
+constexpr int NPW = 4;     // expander warps
 constexpr int NEW = 8;     // epilogue warps
 constexpr int MMA_WARP = NPW + NEW;
-constexpr int NTHREADS = (NPW + NEW + 1) * 32;
+constexpr int LOAD_WARP = MMA_WARP + 1;
+constexpr int NTHREADS = (NPW + NEW + 2) * 32;
 constexpr int A_BYTES = BM * BK;   // 16 KiB
 constexpr int B_BYTES = BNH * BK;  // 16 KiB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -41,7 +42,7 @@ constexpr int TMEM_COLS = 512;
 constexpr uint32_t IDESC = idesc_i8(2 * BM, BN);
 
 struct __align__(8) Bars {
-    uint64_t full[S], empty[S], tfull[2], tempty[2];
+    uint64_t full[S], empty[S], tfull[2], tempty[2], bfull[D], bempty[D];
     uint32_t tmem_base;
     uint16_t outmask[kMaxProducts];
 };
@@ -74,6 +75,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             mbar_init(&bars->tfull[i], 1);
             mbar_init(&bars->tempty[i], 2 * NEW);
         }
+        for (int i = 0; i < D; ++i) {
+            mbar_init(&bars->bfull[i], 1);
+            mbar_init(&bars->bempty[i], NPW);
+        }
         mbar_fence_init();
     }
     if (threadIdx.x < kMaxProducts) bars->outmask[threadIdx.x] = s.outmask[threadIdx.x];
@@ -85,49 +90,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     const uint32_t tmem = bars->tmem_base;
 
     if (warp < NPW) {
-        // ===================== producers (both CTAs) =====================
+        // ===================== expanders (both CTAs) =====================
+        // bit tiles arrive by bulk copy (loader warp); these warps keep no global loads in
+        // flight, so the per-stage fence.proxy.async (MEMBAR.ALL.CTA) only drains their STS.
         const int p = threadIdx.x;  // A row and B^T row of this CTA's half
-        const int64_t offA = (int64_t)(rank * BM + p) * a.kwords;
-        const int64_t offB = (int64_t)b_row_perm((int)rank * BNH + p) * a.kwords;
-        const uint32_t bits_s = smem_u32(bits);
         const uint32_t full_leader = mapa(smem_u32(&bars->full[0]), 0);
-        int64_t i_tile = cluster;
-        int i_t = 0, i_ks = 0, i_slot = 0;
-        const uint64_t *Ab = nullptr, *Bb = nullptr;
-        auto set_base = [&]() {
-            const int64_t m0 = (i_tile / tiles_n) * (2 * BM), n0 = (i_tile % tiles_n) * BN;
-            Ab = a.Ac + m0 * a.kwords + offA;
-            Bb = a.Bt + n0 * a.kwords + offB;
-        };
-        set_base();
-        auto issue = [&]() {
-            const uint32_t slot = bits_s + (uint32_t)(i_slot * BITS_BYTES);
-            const int64_t koff = i_ks * (BK / 64);
-            cp_async16(slot + p * 16, Ab + i_t * a.a_pstride + koff);
-            cp_async16(slot + BITS_A + p * 16, Bb + i_t * a.b_pstride + koff);
-            if (++i_slot == D) i_slot = 0;
-            if (++i_ks == nks) {
-                i_ks = 0;
-                if (++i_t == s.nprod) {
-                    i_t = 0;
-                    i_tile += nclusters;
-                    if (i_tile < ntiles) set_base();
-                }
-            }
-        };
-        for (int i = 0; i < D - 1; ++i) {
-            if (i < total) issue();
-            cp_async_commit();
-        }
-        int c_slot = 0, st = 0;
-        uint32_t phase = 0;
+        int slot = 0, st = 0;
+        uint32_t bph = 0, phase = 0;
         for (int64_t it = 0; it < total; ++it) {
-            if (it + D - 1 < total) issue();
-            cp_async_commit();
-            cp_async_wait<D - 1>();
-            const uint8_t *slot = bits + c_slot * BITS_BYTES;
-            const uint4 wa = *reinterpret_cast<const uint4 *>(slot + p * 16);
-            const uint4 wb = *reinterpret_cast<const uint4 *>(slot + BITS_A + p * 16);
+            mbar_wait(&bars->bfull[slot], bph);
+            const uint8_t *bs = bits + slot * BITS_BYTES;
+            const uint4 wa = *reinterpret_cast<const uint4 *>(bs + p * 16);
+            const uint4 wb = *reinterpret_cast<const uint4 *>(bs + BITS_A + p * 16);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->bempty[slot]);
+            if (++slot == D) {
+                slot = 0;
+                bph ^= 1;
+            }
             mbar_wait(&bars->empty[st], phase ^ 1);
             uint8_t *sa = stages + st * STAGE_BYTES;
             expand_row<false>(sa, p, wa);
@@ -135,13 +115,40 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(full_leader + (uint32_t)(st * 8));
-            if (++c_slot == D) c_slot = 0;
             if (++st == S) {
                 st = 0;
                 phase ^= 1;
             }
         }
-        cp_async_wait<0>();
+    } else if (warp == LOAD_WARP) {
+        // ===================== bit-tile loader (both CTAs, one thread) =====================
+        if (lane == 0) {
+            const int64_t KS = a.kwords >> 1;  // k-stages per row block
+            const uint32_t bits_s = smem_u32(bits);
+            int slot = 0;
+            uint32_t bph = 0;
+            for (int64_t ti = 0; ti < my_tiles; ++ti) {
+                const int64_t tile = cluster + ti * nclusters;
+                const int64_t rbA = (tile / tiles_n) * 2 + rank;  // 128-row block of A
+                const int64_t rbB = (tile % tiles_n) * 2 + rank;  // 128-row block of B^T
+                for (int t = 0; t < s.nprod; ++t) {
+                    const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * 256;
+                    const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * 256;
+                    for (int ks = 0; ks < nks; ++ks) {
+                        mbar_wait(&bars->bempty[slot], bph ^ 1);
+                        mbar_arrive_expect_tx(&bars->bfull[slot], BITS_BYTES);
+                        const uint32_t dst = bits_s + (uint32_t)(slot * BITS_BYTES);
+                        bulk_g2s(dst, Ab + ks * 256, BITS_A, &bars->bfull[slot]);
+                        bulk_g2s(dst + BITS_A, Bb + ks * 256, BITS_BYTES - BITS_A, &bars->bfull[slot]);
+                        if (++slot == D) {
+                            slot = 0;
+                            bph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
     } else if (warp < MMA_WARP) {
         // ===================== epilogue (both CTAs) =====================
         const int ew = warp - NPW;

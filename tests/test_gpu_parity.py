@@ -8,7 +8,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-BACKENDS = ["tc", "tc1", "m4rm"]
+BACKENDS = ["tc", "m4rm"]
 
 
 @pytest.fixture(scope="module")
