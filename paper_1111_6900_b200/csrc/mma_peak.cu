@@ -25,7 +25,8 @@ __device__ __forceinline__ void cluster_sync() {
 template <int CG>
 __global__ void __launch_bounds__(PK_THREADS, 1) k_mma_peak(int iters) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // keep the shared state space visible to the compiler (STS/LDS, not generic ST/LD)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 48 * 1024);
     uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + 48 * 1024 + 16);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -51,7 +51,8 @@ constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + (int)sizeof(Bars) 
 template <int E>
 __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, const TcArgs a) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // keep the shared state space visible to the compiler (STS/LDS, not generic ST/LD)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *stages = smem;
     uint8_t *bits = smem + S * STAGE_BYTES;
     Bars *bars = reinterpret_cast<Bars *>(bits + D * BITS_BYTES);
@@ -102,19 +103,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             const uint8_t *bs = bits + slot * BITS_BYTES;
             const uint4 wa = *reinterpret_cast<const uint4 *>(bs + p * 16);
             const uint4 wb = *reinterpret_cast<const uint4 *>(bs + BITS_A + p * 16);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->bempty[slot]);
-            if (++slot == D) {
-                slot = 0;
-                bph ^= 1;
-            }
             mbar_wait(&bars->empty[st], phase ^ 1);
             uint8_t *sa = stages + st * STAGE_BYTES;
             expand_row<false>(sa, p, wa);
             expand_row<true>(sa + A_BYTES, p, wb);
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(full_leader + (uint32_t)(st * 8));
+            if (lane == 0) {
+                mbar_arrive_cluster(full_leader + (uint32_t)(st * 8));
+                // the bit tile was consumed by the expansion above (data dependence), so the
+                // loader may overwrite the slot: no read-before-overwrite race on bits
+                mbar_arrive(&bars->bempty[slot]);
+            }
+            if (++slot == D) {
+                slot = 0;
+                bph ^= 1;
+            }
             if (++st == S) {
                 st = 0;
                 phase ^= 1;
