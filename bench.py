@@ -185,8 +185,9 @@ def run_ours(args):
         B = g.SlicedMatrix.random(ctx, k, n, 2)
     else:
         B = g.SlicedMatrix(ctx, k, n, torch.empty((e, k, g.words_for(n)), dtype=torch.int64, device=dev))
-    if world > 1:
-        dist.broadcast(B.planes, src=0)  # the one collective: B over NVLink (NCCL)
+    from paper_1111_6900_b200 import dist as gdist
+
+    gdist.broadcast_planes(B.planes, src=0)  # the one collective: B over NVLink (NCCL)
     C = (g.SlicedMatrix.random(ctx, m, n, 3, row0=row0, gcols=n) if acc
          else g.SlicedMatrix(ctx, m, n, torch.empty((e, m, g.words_for(n)), dtype=torch.int64, device=dev)))
     torch.cuda.synchronize()
