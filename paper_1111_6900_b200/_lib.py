@@ -12,7 +12,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgf2e_b200.so")
+LIB_PATH = os.environ.get("GF2E_LIB_PATH") or os.path.join(_HERE, "libgf2e_b200.so")  # env: dev A/B builds
 
 GF2E_OK, GF2E_EINVAL, GF2E_ECUDA, GF2E_ENOMEM, GF2E_ENODEV = 0, 1, 2, 3, 4
 ACCUMULATE = 1

@@ -28,8 +28,18 @@ constexpr int BN = 256;
 constexpr int BK = kTcBK;  // 128 k-bits per stage
 constexpr int S = 5;       // expanded operand stages
 constexpr int D = 8;       // bit-tile staging depth
-constexpr int NPW = 4;     // expander warps
-constexpr int NEW = 8;     // epilogue warps
+#ifndef GF2E_NPW
+#define GF2E_NPW 4
+#endif
+#ifndef GF2E_GROUP_M
+#define GF2E_GROUP_M 8
+#endif
+#ifndef GF2E_EPI_X16
+#define GF2E_EPI_X16 1
+#endif
+constexpr int NPW = GF2E_NPW;  // expander warps (8: 0-3 expand A rows, 4-7 B^T rows; 4: both)
+constexpr int NEW = 8;         // epilogue warps
+constexpr int GROUP_M = GF2E_GROUP_M;  // tile rasterisation: row-tiles per column sweep (L2 reuse)
 constexpr int MMA_WARP = NPW + NEW;
 constexpr int LOAD_WARP = MMA_WARP + 1;
 constexpr int NTHREADS = (NPW + NEW + 2) * 32;
@@ -48,6 +58,19 @@ struct __align__(8) Bars {
 };
 constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + (int)sizeof(Bars) + 1024;
 
+// tile index -> (row-tile, column-tile): sweep GROUP_M row-tiles down each column before
+// moving right, so the ~74 CTA pairs in flight share a few A row-blocks and B^T column-blocks
+// in L2 (row-major order re-read all of B^T from DRAM once per wave).
+__device__ __forceinline__ void tile_coords(int64_t tile, int64_t tiles_m, int64_t tiles_n, int64_t &tm,
+                                            int64_t &tn) {
+    const int64_t per_group = (int64_t)GROUP_M * tiles_n;
+    const int64_t g = tile / per_group, r = tile - g * per_group;
+    const int64_t first = g * GROUP_M;
+    const int64_t gsize = tiles_m - first < GROUP_M ? tiles_m - first : GROUP_M;
+    tm = first + r % gsize;
+    tn = r / gsize;
+}
+
 template <int E>
 __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, const TcArgs a) {
     extern __shared__ uint8_t smem_raw[];
@@ -61,7 +84,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     const uint32_t rank = cluster_ctarank();
     const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
     const int64_t tiles_n = a.n_pad / BN;
-    const int64_t ntiles = (a.m_pad / (2 * BM)) * tiles_n;
+    const int64_t tiles_m = a.m_pad / (2 * BM);
+    const int64_t ntiles = tiles_m * tiles_n;
     const int64_t my_tiles = ntiles > cluster ? (ntiles - cluster + nclusters - 1) / nclusters : 0;
     const int nks = (int)(a.kwords / (BK / 64));
     const int64_t per_tile = (int64_t)s.nprod * nks;
@@ -94,19 +118,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
         // ===================== expanders (both CTAs) =====================
         // bit tiles arrive by bulk copy (loader warp); these warps keep no global loads in
         // flight, so the per-stage fence.proxy.async (MEMBAR.ALL.CTA) only drains their STS.
-        const int p = threadIdx.x;  // A row and B^T row of this CTA's half
+        // Two warps per SMSP: one warp's fence / LDS latency overlaps another's expansion.
+        const bool isB = NPW == 8 && warp >= 4;
+        const int p = threadIdx.x & 127;  // row of this CTA's A half (isB: of its B^T half)
+        const uint32_t src_off = (isB ? BITS_A : 0) + p * 16;
+        const uint32_t dst_off = isB ? A_BYTES : 0;
         const uint32_t full_leader = mapa(smem_u32(&bars->full[0]), 0);
         int slot = 0, st = 0;
         uint32_t bph = 0, phase = 0;
         for (int64_t it = 0; it < total; ++it) {
             mbar_wait(&bars->bfull[slot], bph);
-            const uint8_t *bs = bits + slot * BITS_BYTES;
-            const uint4 wa = *reinterpret_cast<const uint4 *>(bs + p * 16);
-            const uint4 wb = *reinterpret_cast<const uint4 *>(bs + BITS_A + p * 16);
+            const uint4 w = *reinterpret_cast<const uint4 *>(bits + slot * BITS_BYTES + src_off);
+            uint4 wb2;
+            if (NPW == 4) wb2 = *reinterpret_cast<const uint4 *>(bits + slot * BITS_BYTES + BITS_A + p * 16);
             mbar_wait(&bars->empty[st], phase ^ 1);
-            uint8_t *sa = stages + st * STAGE_BYTES;
-            expand_row<false>(sa, p, wa);
-            expand_row<true>(sa + A_BYTES, p, wb);
+            uint8_t *tile = stages + st * STAGE_BYTES + dst_off;
+            if (isB)
+                expand_row<true>(tile, p, w);
+            else
+                expand_row<false>(tile, p, w);
+            if (NPW == 4) expand_row<true>(stages + st * STAGE_BYTES + A_BYTES, p, wb2);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -133,8 +164,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             uint32_t bph = 0;
             for (int64_t ti = 0; ti < my_tiles; ++ti) {
                 const int64_t tile = cluster + ti * nclusters;
-                const int64_t rbA = (tile / tiles_n) * 2 + rank;  // 128-row block of A
-                const int64_t rbB = (tile % tiles_n) * 2 + rank;  // 128-row block of B^T
+                int64_t tm, tn;
+                tile_coords(tile, tiles_m, tiles_n, tm, tn);
+                const int64_t rbA = tm * 2 + rank;  // 128-row block of A
+                const int64_t rbB = tn * 2 + rank;  // 128-row block of B^T
                 for (int t = 0; t < s.nprod; ++t) {
                     const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * 256;
                     const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * 256;
@@ -164,7 +197,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
         int64_t gp = 0;
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             const int64_t tile = cluster + ti * nclusters;
-            const int64_t m0 = (tile / tiles_n) * (2 * BM), n0 = (tile % tiles_n) * BN;
+            int64_t tm, tn;
+            tile_coords(tile, tiles_m, tiles_n, tm, tn);
+            const int64_t m0 = tm * (2 * BM), n0 = tn * BN;
             uint32_t acc[E][4];
 #pragma unroll
             for (int j = 0; j < E; ++j)
@@ -177,10 +212,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                 const uint32_t mask = bars->outmask[t];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + c * 32);
+#if GF2E_EPI_X16
+                    uint32_t v[16];
+                    tmem_ld16(ta, v);
+                    tmem_wait_ld();
+                    uint32_t pw = parity_half(v, 0);
+                    tmem_ld16(ta + 16, v);
+                    tmem_wait_ld();
+                    pw |= parity_half(v, 4);
+#else
                     uint32_t v[32];
-                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + c * 32), v);
+                    tmem_ld32(ta, v);
                     tmem_wait_ld();
                     const uint32_t pw = parity_word(v);
+#endif
 #pragma unroll
                     for (int j = 0; j < E; ++j) acc[j][c] ^= pw & (0u - ((mask >> j) & 1u));
                 }

@@ -40,6 +40,20 @@ __device__ __forceinline__ uint32_t parity_word(const uint32_t (&v)[32]) {
     return r;
 }
 
+// Half of parity_word: 16 accumulators = groups g0 .. g0+3 of a 32-column chunk.
+__device__ __forceinline__ uint32_t parity_half(const uint32_t (&v)[16], int g0) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int gg = 0; gg < 4; ++gg) {
+        const int g = g0 + gg;
+        const uint32_t lo = __byte_perm(v[4 * gg], v[4 * gg + 1], 0x0040);
+        const uint32_t hi = __byte_perm(v[4 * gg + 2], v[4 * gg + 3], 0x0040);
+        const uint32_t z = __byte_perm(lo, hi, 0x5410);
+        r |= (z >> (7 - g)) & (0x01010101u << g);
+    }
+    return r;
+}
+
 // TMEM column j (= B smem row j) of every 32-column group holds tile column b_row_perm(j).
 __host__ __device__ __forceinline__ int b_row_perm(int j) {
     const int g = (j & 31) >> 2, b = j & 3;
