@@ -35,7 +35,7 @@ constexpr int D = 8;       // bit-tile staging depth
 #define GF2E_GROUP_M 8
 #endif
 #ifndef GF2E_EPI_X16
-#define GF2E_EPI_X16 1
+#define GF2E_EPI_X16 2  // 2: pack::16b + sign-PRMT parity, 1: two x16 loads, 0: one x32 load
 #endif
 constexpr int NPW = GF2E_NPW;  // expander warps (8: 0-3 expand A rows, 4-7 B^T rows; 4: both)
 constexpr int NEW = 8;         // epilogue warps
@@ -213,7 +213,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + c * 32);
-#if GF2E_EPI_X16
+#if GF2E_EPI_X16 == 2
+                    uint32_t v[16];
+                    tmem_ld32_pack16(ta, v);
+                    tmem_wait_ld();
+                    const uint32_t pw = parity_word_packed(v);
+#elif GF2E_EPI_X16
                     uint32_t v[16];
                     tmem_ld16(ta, v);
                     tmem_wait_ld();

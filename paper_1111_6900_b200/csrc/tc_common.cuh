@@ -40,6 +40,21 @@ __device__ __forceinline__ uint32_t parity_word(const uint32_t (&v)[32]) {
     return r;
 }
 
+// parity_word from pack::16b registers (v[i] = column 2i | column 2i+1 << 16): PRMT with
+// sign-replicating selectors turns the bit-7 of 4 columns into 4 byte masks (0x00 / 0xFF) in
+// one instruction, and one LOP3 merges them: 16 ALU ops per 32 columns, same bit order as
+// parity_word (bit 8b+g = column 4g+b).
+__device__ __forceinline__ uint32_t parity_word_packed(const uint32_t (&v)[16]) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        uint32_t w;  // byte b = sign-replicated bit 7 of column 4g+b (prmt selector msb = replicate)
+        asm("prmt.b32 %0, %1, %2, 0xECA8;" : "=r"(w) : "r"(v[2 * g]), "r"(v[2 * g + 1]));
+        r |= w & (0x01010101u << g);
+    }
+    return r;
+}
+
 // Half of parity_word: 16 accumulators = groups g0 .. g0+3 of a 32-column chunk.
 __device__ __forceinline__ uint32_t parity_half(const uint32_t (&v)[16], int g0) {
     uint32_t r = 0;
