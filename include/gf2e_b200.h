@@ -127,6 +127,21 @@ int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, int64_
                    int64_t workspace_bytes, void *stream);
 
 /*
+ * mzed_mul / mzed_addmul with HOST buffers — the end-to-end entry a numpy-based caller
+ * (e.g. gf2elin itself) binds: karatsuba_mul_packed (poly_mul.py:275-278)
+ * and C ^= A*B on packed matrices, with A (m x k), B (k x n), C (m x n) in host memory in
+ * the reference PackedMatrix.storage.words layout (row stride in words; pinned memory gives
+ * full copy/compute overlap).  Synchronous.  B is uploaded, sliced and combined once; rows of
+ * A (and C0) then stream through in chunks of `chunk_rows` (<= 0: 4096) with H2D, the
+ * kernels and D2H of consecutive chunks overlapped on three internal streams.  Device memory
+ * comes from the stream-ordered pool.  *device_ms (optional) = CUDA-event time from the first
+ * H2D to the last D2H.
+ */
+int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_host, int64_t lda, const uint64_t *B_host,
+                       int64_t ldb, uint64_t *C_host, int64_t ldc, int64_t m, int64_t k, int64_t n,
+                       uint32_t flags, int64_t chunk_rows, double *device_ms);
+
+/*
  * GF(2) plane product mzd_mul / mzd_addmul (mat_gf2.mul, mat_gf2.py:425-455):
  * C = A*B or C ^= A*B (GF2E_ACCUMULATE).  A m x k, B k x n, C m x n.
  */

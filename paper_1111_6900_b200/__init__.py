@@ -19,6 +19,8 @@ from .poly_mul import (
     count_products,
     karatsuba_mul,
     karatsuba_mul_packed,
+    karatsuba_mul_packed_host,
+    mzed_mul_host,
     mzd_slice_addmul,
     mzd_slice_mul,
     mzed_addmul,
@@ -32,7 +34,7 @@ __all__ = [
     "BitMatrix", "RowOpCounters", "mul", "gf2_addmul", "mzd_mul", "mzd_addmul", "words_for",
     "PackedMatrix", "pack_width",
     "SlicedMatrix", "slice_packed", "cling", "mzed_slice", "mzed_cling",
-    "MulCounters", "Schedule", "schedule", "karatsuba_mul", "karatsuba_mul_packed", "addmul", "addmul_packed",
+    "MulCounters", "Schedule", "schedule", "karatsuba_mul", "karatsuba_mul_packed", "karatsuba_mul_packed_host", "mzed_mul_host", "addmul", "addmul_packed",
     "reduce_mod_f", "count_products", "mzd_slice_mul", "mzd_slice_addmul", "mzed_mul", "mzed_addmul",
 ]
 

@@ -43,6 +43,8 @@ SIGNATURES = {
     "gf2e_plane_mul_workspace": (_I64, [_I64, _I64, _I64, _U32]),
     "gf2e_slice_mul": (_INT, [_INT, _U32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64,
                               _U32, _P, _I64, _P]),
+    "gf2e_mzed_mul_host": (_INT, [_INT, _U32, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _U32, _I64,
+                                  ctypes.POINTER(ctypes.c_double)]),
     "gf2e_plane_mul": (_INT, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _U32, _P, _I64, _P]),
     "gf2e_last_launch_count": (_INT, []),
     "gf2e_last_product_kernel": (ctypes.c_char_p, []),

@@ -306,6 +306,36 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
     return GF2E_OK;
 }
 
+
+// ---- host-buffer packed multiply (e2e entry) ----------------------------------------------
+struct HostPlan {
+    cudaStream_t sc = nullptr, sh = nullptr, sd = nullptr;
+    std::vector<void *> allocs;
+    ~HostPlan() {
+        if (sh) cudaStreamSynchronize(sh);  // error paths: no copy may outlive its buffers
+        if (sd) cudaStreamSynchronize(sd);
+        for (void *p : allocs) cudaFreeAsync(p, sc);
+        if (sc) cudaStreamSynchronize(sc);
+        if (sc) cudaStreamDestroy(sc);
+        if (sh) cudaStreamDestroy(sh);
+        if (sd) cudaStreamDestroy(sd);
+    }
+    template <typename T>
+    cudaError_t alloc(T **p, int64_t bytes) {
+        void *q = nullptr;
+        cudaError_t e = cudaMallocAsync(&q, (size_t)(bytes > 256 ? bytes : 256), sc);
+        if (e == cudaSuccess) allocs.push_back(q);
+        *p = static_cast<T *>(q);
+        return e;
+    }
+};
+
+#define CKH(expr, what)                                    \
+    do {                                                   \
+        cudaError_t _e = (expr);                           \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
 int check_flags(uint32_t flags) {
     if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM)) return fail(GF2E_EINVAL, "unknown flags 0x%x", flags);
     return GF2E_OK;
@@ -507,6 +537,124 @@ int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa
     if (int rc = check_device()) return rc;
     Sched ks = to_kernel_sched(e, get_schedule(e, f));
     return run_product(ks, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, flags, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, const uint64_t *B_h, int64_t ldb,
+                       uint64_t *C_h, int64_t ldc, int64_t m, int64_t k, int64_t n, uint32_t flags,
+                       int64_t chunk_rows, double *device_ms) {
+    g_err.clear();
+    g_launches = 0;
+    if (device_ms) *device_ms = 0;
+    if (int rc = check_field(e, f)) return rc;
+    if (flags & ~GF2E_ACCUMULATE) return fail(GF2E_EINVAL, "gf2e_mzed_mul_host: unsupported flags 0x%x", flags);
+    const bool acc = (flags & GF2E_ACCUMULATE) != 0;
+    const int w = gf2e_pack_width(e);
+    const int64_t wa = words_for(k * w), wb = words_for(n * w), nwk = words_for(k), nwn = words_for(n);
+    if (int rc = check_mat(A_h, m, wa, lda, "A")) return rc;
+    if (int rc = check_mat(B_h, k, wb, ldb, "B")) return rc;
+    if (int rc = check_mat(C_h, m, wb, ldc, "C")) return rc;
+    if (m == 0 || n == 0) return GF2E_OK;
+    if (k == 0) {  // product is zero
+        if (!acc)
+            for (int64_t i = 0; i < m; ++i) memset(C_h + i * ldc, 0, (size_t)wb * 8);
+        return GF2E_OK;
+    }
+    if (int rc = check_device()) return rc;
+    Sched ks = to_kernel_sched(e, get_schedule(e, f));
+    int64_t chunk = chunk_rows > 0 ? round_up(chunk_rows, 2 * kTcBM) : 4096;
+    if (chunk > round_up(m, 2 * kTcBM)) chunk = round_up(m, 2 * kTcBM);
+    const int64_t nchunks = (m + chunk - 1) / chunk;
+    const int nslots = nchunks > 1 ? 2 : 1;
+
+    HostPlan P;
+    CKH(cudaStreamCreateWithFlags(&P.sc, cudaStreamNonBlocking), "stream");
+    CKH(cudaStreamCreateWithFlags(&P.sh, cudaStreamNonBlocking), "stream");
+    CKH(cudaStreamCreateWithFlags(&P.sd, cudaStreamNonBlocking), "stream");
+    Layout LB = layout_for(ks.nprod, chunk, k, n, 0);  // Ac sized for one chunk, Bt for all of B
+    uint64_t *dBp, *dBs, *dAc, *dBt, *dAp[2], *dAs[2], *dCs[2], *dCp[2];
+    CKH(P.alloc(&dBp, k * wb * 8), "cudaMallocAsync");
+    CKH(P.alloc(&dBs, (int64_t)e * k * nwn * 8), "cudaMallocAsync");
+    CKH(P.alloc(&dAc, LB.a_bytes), "cudaMallocAsync");
+    CKH(P.alloc(&dBt, LB.b_bytes), "cudaMallocAsync");
+    for (int sl = 0; sl < nslots; ++sl) {
+        CKH(P.alloc(&dAp[sl], chunk * wa * 8), "cudaMallocAsync");
+        CKH(P.alloc(&dAs[sl], (int64_t)e * chunk * nwk * 8), "cudaMallocAsync");
+        CKH(P.alloc(&dCs[sl], (int64_t)e * chunk * nwn * 8), "cudaMallocAsync");
+        CKH(P.alloc(&dCp[sl], chunk * wb * 8), "cudaMallocAsync");
+    }
+    cudaEvent_t ev_alloc, ev_t0, ev_t1, ev_b, in_ready[2], out_ready[2], d2h_done[2];
+    cudaEvent_t *all[] = {&ev_alloc, &ev_t0, &ev_t1, &ev_b, &in_ready[0], &in_ready[1], &out_ready[0],
+                          &out_ready[1], &d2h_done[0], &d2h_done[1]};
+    for (cudaEvent_t *ev : all) CKH(cudaEventCreate(ev), "cudaEventCreate");
+    struct EvGuard {
+        cudaEvent_t **evs;
+        int n;
+        ~EvGuard() {
+            for (int i = 0; i < n; ++i) cudaEventDestroy(*evs[i]);
+        }
+    } guard{all, 10};
+    CKH(cudaEventRecord(ev_alloc, P.sc), "cudaEventRecord");
+    CKH(cudaStreamWaitEvent(P.sh, ev_alloc, 0), "cudaStreamWaitEvent");
+    CKH(cudaStreamWaitEvent(P.sd, ev_alloc, 0), "cudaStreamWaitEvent");
+
+    CKH(cudaEventRecord(ev_t0, P.sh), "cudaEventRecord");
+    // B once: H2D, slice, transposed operand combinations
+    CKH(cudaMemcpy2DAsync(dBp, wb * 8, B_h, ldb * 8, wb * 8, k, cudaMemcpyHostToDevice, P.sh), "H2D(B)");
+    CKH(cudaEventRecord(ev_b, P.sh), "cudaEventRecord");
+    auto h2d_chunk = [&](int64_t i) -> int {
+        const int sl = (int)(i % nslots);
+        const int64_t r0 = i * chunk, rows = (m - r0) < chunk ? (m - r0) : chunk;
+        if (i >= nslots) {  // slot reuse: chunk i-2 fully consumed (its cling and its D2H)
+            CKH(cudaStreamWaitEvent(P.sh, out_ready[sl], 0), "cudaStreamWaitEvent");
+            CKH(cudaStreamWaitEvent(P.sh, d2h_done[sl], 0), "cudaStreamWaitEvent");
+        }
+        CKH(cudaMemcpy2DAsync(dAp[sl], wa * 8, A_h + r0 * lda, lda * 8, wa * 8, rows, cudaMemcpyHostToDevice, P.sh),
+            "H2D(A)");
+        if (acc)
+            CKH(cudaMemcpy2DAsync(dCp[sl], wb * 8, C_h + r0 * ldc, ldc * 8, wb * 8, rows, cudaMemcpyHostToDevice,
+                                  P.sh),
+                "H2D(C0)");
+        CKH(cudaEventRecord(in_ready[sl], P.sh), "cudaEventRecord");
+        return GF2E_OK;
+    };
+    if (int rc = h2d_chunk(0)) return rc;
+    CKH(cudaStreamWaitEvent(P.sc, ev_b, 0), "cudaStreamWaitEvent");
+    CK(launch_slice(e, w, k, n, dBp, wb, dBs, nwn, k * nwn, P.sc), "slice(B)");
+    CK(launch_combos_bt(ks, dBs, nwn, k * nwn, k, n, dBt, LB.kwords, LB.b_pstride, LB.kwords, LB.n_pad / 64, P.sc),
+       "combos(B^T)");
+    for (int64_t i = 0; i < nchunks; ++i) {
+        const int sl = (int)(i % nslots);
+        const int64_t r0 = i * chunk, rows = (m - r0) < chunk ? (m - r0) : chunk;
+        if (i + 1 < nchunks)
+            if (int rc = h2d_chunk(i + 1)) return rc;  // overlaps this chunk's kernels
+        CKH(cudaStreamWaitEvent(P.sc, in_ready[sl], 0), "cudaStreamWaitEvent");
+        CK(launch_slice(e, w, rows, k, dAp[sl], wa, dAs[sl], nwk, rows * nwk, P.sc), "slice(A)");
+        if (acc) CK(launch_slice(e, w, rows, n, dCp[sl], wb, dCs[sl], nwn, rows * nwn, P.sc), "slice(C0)");
+        Layout L = layout_for(ks.nprod, rows, k, n, 0);
+        CK(launch_combos_rows(ks, dAs[sl], nwk, rows * nwk, rows, k, dAc, L.kwords, L.a_pstride, L.m_pad, L.kwords,
+                              true, P.sc),
+           "combos(A)");
+        TcArgs ta{dAc, dBt, L.a_pstride, LB.b_pstride, L.kwords, rows, n, L.m_pad, LB.n_pad, dCs[sl], nwn, rows * nwn,
+                  acc ? 1 : 0};
+        {
+            ProfScope prof(P.sc);
+            CK(launch_product_tc2(ks, ta, P.sc), "product_tc2");
+        }
+        CK(launch_cling(e, w, rows, n, dCs[sl], nwn, rows * nwn, dCp[sl], wb, P.sc), "cling(C)");
+        CKH(cudaEventRecord(out_ready[sl], P.sc), "cudaEventRecord");
+        CKH(cudaStreamWaitEvent(P.sd, out_ready[sl], 0), "cudaStreamWaitEvent");
+        CKH(cudaMemcpy2DAsync(C_h + r0 * ldc, ldc * 8, dCp[sl], wb * 8, wb * 8, rows, cudaMemcpyDeviceToHost, P.sd),
+            "D2H(C)");
+        CKH(cudaEventRecord(d2h_done[sl], P.sd), "cudaEventRecord");
+    }
+    CKH(cudaStreamWaitEvent(P.sh, d2h_done[(nchunks - 1) % nslots], 0), "cudaStreamWaitEvent");
+    CKH(cudaEventRecord(ev_t1, P.sh), "cudaEventRecord");
+    CKH(cudaEventSynchronize(ev_t1), "cudaEventSynchronize");
+    float ms = 0;
+    CKH(cudaEventElapsedTime(&ms, ev_t0, ev_t1), "cudaEventElapsedTime");
+    if (device_ms) *device_ms = ms;
+    g_kernel = "k_product_tc2";
+    return GF2E_OK;
 }
 
 int gf2e_plane_mul(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, uint64_t *C, int64_t ldc, int64_t m,

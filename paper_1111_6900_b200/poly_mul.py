@@ -182,8 +182,42 @@ def addmul_packed(C: PackedMatrix, A: PackedMatrix, B: PackedMatrix, counters: M
     return C
 
 
+def karatsuba_mul_packed_host(ctx: FieldCtx, A_words, k: int, B_words, n: int, C_words=None,
+                              chunk_rows: int = 0, counters: MulCounters | None = None, out=None):
+    """mzed_mul / mzed_addmul on HOST packed words (reference ``PackedMatrix.storage.words``):
+    returns (C words, device ms).  With ``C_words`` the product is XOR-ed into it in place.
+    One synchronous ``gf2e_mzed_mul_host`` call: B uploaded and prepared once, rows of A
+    streamed in chunks with copies overlapping the kernels (use pinned arrays for overlap).
+    ``out``: optional preallocated (pinned) result array for C = A*B."""
+    import numpy as np
+
+    A = np.ascontiguousarray(A_words, dtype=np.uint64)
+    B = np.ascontiguousarray(B_words, dtype=np.uint64)
+    m = A.shape[0]
+    if B.shape[0] != k:
+        raise ValueError(f"inner dimensions differ: {m}x{k} times {B.shape[0]}x{n}")
+    acc = C_words is not None
+    if acc:
+        C = C_words
+        if C.dtype != np.uint64 or not C.flags.c_contiguous:
+            raise ValueError("C_words must be a C-contiguous uint64 array")
+    elif out is not None:
+        C = out
+        if C.dtype != np.uint64 or not C.flags.c_contiguous or C.shape[0] != m:
+            raise ValueError("out must be a C-contiguous uint64 array with one row per row of A")
+    else:
+        C = np.empty((m, B.shape[1]), dtype=np.uint64)
+    ms = ctypes.c_double()
+    _lib.call("gf2e_mzed_mul_host", ctx.e, ctx.f, A.ctypes.data, A.shape[1] if A.ndim == 2 else 0, B.ctypes.data,
+              B.shape[1], C.ctypes.data, C.shape[1], m, k, n, _lib.ACCUMULATE if acc else 0, chunk_rows,
+              ctypes.byref(ms))
+    _bump(counters, ctx)
+    return C, ms.value
+
+
 # M4RIE vocabulary (BASELINE.json north star)
 mzd_slice_mul = karatsuba_mul
 mzd_slice_addmul = addmul
 mzed_mul = karatsuba_mul_packed
 mzed_addmul = addmul_packed
+mzed_mul_host = karatsuba_mul_packed_host

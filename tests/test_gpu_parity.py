@@ -244,3 +244,19 @@ def test_native_code_used(g):
     g.karatsuba_mul(A, A)
     assert g._lib.last_product_kernel() == "k_product_tc2"
     assert g._lib.last_launch_count() == 3  # combos(A), combos(B^T), fused product
+
+
+@pytest.mark.parametrize("acc", [False, True])
+@pytest.mark.parametrize("e,m,k,n,chunk", [(8, 1000, 700, 600, 256), (4, 4096, 4096, 4096, 0), (2, 300, 0, 65, 0),
+                                           (10, 513, 129, 257, 512), (3, 1, 1, 1, 0)])
+def test_host_buffer_api(g, e, m, k, n, chunk, acc):
+    # gf2e_mzed_mul_host: packed host words in, packed host words out, chunked + overlapped
+    ctx = g.field_new(e)
+    A = oracle.packed_random(e, m, k, 1)
+    B = oracle.packed_random(e, k, n, 2)
+    C0 = oracle.packed_random(e, m, n, 3) if acc else None
+    C, ms = g.karatsuba_mul_packed_host(ctx, A, k, B, n, C_words=None if C0 is None else C0.copy(), chunk_rows=chunk)
+    ref, _ = oracle.karatsuba(e, ctx.f, oracle.sliced_random(e, m, k, 1), oracle.sliced_random(e, k, n, 2), m, k, n,
+                              C0=None if C0 is None else oracle.slice_words(e, m, n, C0))
+    assert np.array_equal(C, oracle.cling_words(e, m, n, ref))
+    assert ms >= 0
