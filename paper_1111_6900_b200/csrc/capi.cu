@@ -561,7 +561,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     }
     if (int rc = check_device()) return rc;
     Sched ks = to_kernel_sched(e, get_schedule(e, f));
-    int64_t chunk = chunk_rows > 0 ? round_up(chunk_rows, 2 * kTcBM) : 4096;
+    int64_t chunk = chunk_rows > 0 ? round_up(chunk_rows, 2 * kTcBM) : 2048;
     if (chunk > round_up(m, 2 * kTcBM)) chunk = round_up(m, 2 * kTcBM);
     const int64_t nchunks = (m + chunk - 1) / chunk;
     const int nslots = nchunks > 1 ? 2 : 1;

@@ -216,6 +216,46 @@ __global__ void k_combos_rows(Sched s, const uint64_t *__restrict__ X, int64_t l
     }
 }
 
+// Stage-tiled A'_t (tensor-core layout): thread = (row r, pair of k-stages); reads 32 B of each
+// input plane row (one sector), writes 16 B to each of two tiles; a warp's writes are 32
+// consecutive tile rows = 512 contiguous bytes.
+__global__ void k_combos_tiled(Sched s, const uint64_t *__restrict__ X, int64_t ldx, int64_t px, int64_t rows,
+                               int64_t ncols, uint64_t *__restrict__ out, int64_t po, int64_t rows_pad,
+                               int64_t kwords) {
+    const int64_t nw = words_for(ncols);
+    const uint64_t tm = tail_mask(ncols);
+    const int64_t KS = kwords >> 1, KP = (KS + 1) >> 1;  // k-stages, stage pairs
+    const int64_t total = rows_pad * KP;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        const int64_t rb = idx / (KP * 128), rem = idx - rb * KP * 128;
+        const int64_t kp = rem >> 7, r = rb * 128 + (rem & 127);
+        const int64_t w0 = kp * 4;
+        uint64_t x[kMaxE][4];
+#pragma unroll
+        for (int i = 0; i < kMaxE; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t w = w0 + q;
+                uint64_t v = (i < s.e && r < rows && w < nw) ? X[i * px + r * ldx + w] : 0;
+                x[i][q] = (w == nw - 1) ? (v & tm) : v;
+            }
+        const bool two = 2 * kp + 1 < KS;
+        for (int t = 0; t < s.nprod; ++t) {
+            const uint32_t sub = s.subset[t];
+            uint64_t a[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int i = 0; i < kMaxE; ++i) {
+                const uint64_t sel = 0ULL - (uint64_t)((sub >> i) & 1u);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) a[q] ^= x[i][q] & sel;
+            }
+            uint64_t *o = out + t * po;
+            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(r, w0, kwords)) = make_ulonglong2(a[0], a[1]);
+            if (two) *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(r, w0 + 2, kwords)) = make_ulonglong2(a[2], a[3]);
+        }
+    }
+}
+
 // 64x64 bit-matrix transpose held as two words per lane (rows lane and lane+32).
 __device__ __forceinline__ void transpose64(uint64_t &xa, uint64_t &xb, int lane) {
     uint64_t t = ((xa >> 32) ^ xb) & 0x00000000FFFFFFFFULL;
@@ -247,33 +287,44 @@ __device__ __forceinline__ void transpose64(uint64_t &xa, uint64_t &xb, int lane
 __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb, int64_t pb, int64_t k,
                             int64_t n, uint64_t *__restrict__ out, int64_t ldo, int64_t po, int64_t kblocks,
                             int64_t nblocks) {
+    // one warp per (k-stage = 2 x 64 k-rows, 64-column block): two 64x64 transposes, then each
+    // lane writes whole 16-byte tile rows (both words of its stage)
     const int lane = threadIdx.x & 31;
     const int64_t warp = gtid() >> 5;
     const int64_t nwarps = gstride() >> 5;
     const int64_t nw = words_for(n);
-    for (int64_t blk = warp; blk < kblocks * nblocks; blk += nwarps) {
-        int64_t kb = blk % kblocks, nb = blk / kblocks;
-        int64_t r0 = kb * 64 + (lane ^ 7), r1 = r0 + 32;
-        uint64_t tm = (nb == nw - 1) ? tail_mask(n) : ~0ULL;
-        uint64_t a[kMaxE], b[kMaxE];
+    const int64_t kstages = kblocks >> 1;
+    for (int64_t blk = warp; blk < kstages * nblocks; blk += nwarps) {
+        const int64_t ks = blk % kstages, nb = blk / kstages;
+        const uint64_t tm = (nb == nw - 1) ? tail_mask(n) : ~0ULL;
+        uint64_t a[2][kMaxE], b[2][kMaxE];
 #pragma unroll
-        for (int i = 0; i < kMaxE; ++i) {
-            a[i] = (i < s.e && nb < nw && r0 < k) ? (B[i * pb + r0 * ldb + nb] & tm) : 0;
-            b[i] = (i < s.e && nb < nw && r1 < k) ? (B[i * pb + r1 * ldb + nb] & tm) : 0;
-        }
-        for (int t = 0; t < s.nprod; ++t) {
-            uint32_t sub = s.subset[t];
-            uint64_t xa = 0, xb = 0;
+        for (int h = 0; h < 2; ++h) {
+            const int64_t r0 = (2 * ks + h) * 64 + (lane ^ 7), r1 = r0 + 32;
 #pragma unroll
             for (int i = 0; i < kMaxE; ++i) {
-                uint64_t sel = 0ULL - (uint64_t)((sub >> i) & 1u);
-                xa ^= a[i] & sel;
-                xb ^= b[i] & sel;
+                a[h][i] = (i < s.e && nb < nw && r0 < k) ? (B[i * pb + r0 * ldb + nb] & tm) : 0;
+                b[h][i] = (i < s.e && nb < nw && r1 < k) ? (B[i * pb + r1 * ldb + nb] & tm) : 0;
             }
-            transpose64(xa, xb, lane);
-            const int64_t n0 = nb * 64 + lane;
-            out[t * po + tc_tile_word(tc_b_row_inv(n0), kb, ldo)] = xa;
-            out[t * po + tc_tile_word(tc_b_row_inv(n0 + 32), kb, ldo)] = xb;
+        }
+        const int64_t ra = tc_b_row_inv(nb * 64 + lane), rb = tc_b_row_inv(nb * 64 + lane + 32);
+        for (int t = 0; t < s.nprod; ++t) {
+            const uint32_t sub = s.subset[t];
+            uint64_t xa[2] = {0, 0}, xb[2] = {0, 0};
+#pragma unroll
+            for (int i = 0; i < kMaxE; ++i) {
+                const uint64_t sel = 0ULL - (uint64_t)((sub >> i) & 1u);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    xa[h] ^= a[h][i] & sel;
+                    xb[h] ^= b[h][i] & sel;
+                }
+            }
+            transpose64(xa[0], xb[0], lane);
+            transpose64(xa[1], xb[1], lane);
+            uint64_t *o = out + t * po;
+            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(ra, 2 * ks, ldo)) = make_ulonglong2(xa[0], xa[1]);
+            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(rb, 2 * ks, ldo)) = make_ulonglong2(xb[0], xb[1]);
         }
     }
 }
@@ -362,6 +413,12 @@ cudaError_t launch_reduce(int e, uint32_t f, uint64_t *planes, int64_t rows, int
 cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, int64_t px, int64_t rows,
                                int64_t ncols, uint64_t *out, int64_t ldo, int64_t po, int64_t rows_pad,
                                int64_t words_pad, bool tiled, cudaStream_t st) {
+    if (tiled) {
+        const int64_t tot = rows_pad * (((words_pad >> 1) + 1) >> 1);
+        if (tot == 0) return cudaSuccess;
+        k_combos_tiled<<<grid_for(tot, 256), 256, 0, st>>>(s, X, ldx, px, rows, ncols, out, po, rows_pad, words_pad);
+        return cudaGetLastError();
+    }
     int64_t total = rows_pad * words_pad;
     if (total == 0) return cudaSuccess;
     k_combos_rows<<<grid_for(total, 256), 256, 0, st>>>(s, X, ldx, px, rows, ncols, out, ldo, po, rows_pad,
@@ -372,7 +429,7 @@ cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, i
 cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int64_t pb, int64_t k, int64_t n,
                              uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks,
                              cudaStream_t st) {
-    int64_t warps = kblocks * nblocks;
+    int64_t warps = (kblocks >> 1) * nblocks;  // kblocks is even (k_pad is a multiple of 128)
     if (warps == 0) return cudaSuccess;
     int g = grid_for(warps * 32, 256);
     k_combos_bt<<<g, 256, 0, st>>>(s, B, ldb, pb, k, n, out, ldo, po, kblocks, nblocks);
