@@ -260,3 +260,15 @@ def test_host_buffer_api(g, e, m, k, n, chunk, acc):
                               C0=None if C0 is None else oracle.slice_words(e, m, n, C0))
     assert np.array_equal(C, oracle.cling_words(e, m, n, ref))
     assert ms >= 0
+
+
+@pytest.mark.slow
+def test_config5_sampled_blocks(g):
+    # BASELINE config 5: F_256, 65536^3 on one GPU (the per-GPU problem of the 1-GPU point of the
+    # scaling run); sampled rows x 256-column blocks against the oracle
+    import torch
+
+    free, _ = torch.cuda.mem_get_info()
+    if free < 60 * 2**30:
+        pytest.skip("needs ~60 GiB of free HBM")
+    _sampled_blocks(g, 8, 65536, 65536, 65536, False, [0, 255, 40000, 65535], (65536 - 256, 65536))
