@@ -40,8 +40,16 @@ constexpr int D = 8;       // bit-tile staging depth
 constexpr int NPW = GF2E_NPW;  // expander warps (8: 0-3 expand A rows, 4-7 B^T rows; 4: both)
 constexpr int NEW = 8;         // epilogue warps
 constexpr int GROUP_M = GF2E_GROUP_M;  // tile rasterisation: row-tiles per column sweep (L2 reuse)
-constexpr int MMA_WARP = NPW + NEW;
+#ifndef GF2E_EXP_HIGH
+#define GF2E_EXP_HIGH 0
+#endif
+// Warp roles.  The issue arbiter favours higher warp ids, and the expanders are the critical
+// role, so (GF2E_EXP_HIGH) they take the highest ids: epilogue 0-7, MMA 8, loader 9,
+// expanders 10-13 (one per SMSP either way: warp id % 4 covers 0..3).
+constexpr int EPI_W0 = GF2E_EXP_HIGH ? 0 : NPW;
+constexpr int MMA_WARP = GF2E_EXP_HIGH ? NEW : NPW + NEW;
 constexpr int LOAD_WARP = MMA_WARP + 1;
+constexpr int EXP_W0 = GF2E_EXP_HIGH ? NEW + 2 : 0;
 constexpr int NTHREADS = (NPW + NEW + 2) * 32;
 constexpr int A_BYTES = BM * BK;   // 16 KiB
 constexpr int B_BYTES = BNH * BK;  // 16 KiB
@@ -114,13 +122,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
 
-    if (warp < NPW) {
+    if (warp >= EXP_W0 && warp < EXP_W0 + NPW) {
         // ===================== expanders (both CTAs) =====================
         // bit tiles arrive by bulk copy (loader warp); these warps keep no global loads in
         // flight, so the per-stage fence.proxy.async (MEMBAR.ALL.CTA) only drains their STS.
         // Two warps per SMSP: one warp's fence / LDS latency overlaps another's expansion.
-        const bool isB = NPW == 8 && warp >= 4;
-        const int p = threadIdx.x & 127;  // row of this CTA's A half (isB: of its B^T half)
+        const bool isB = NPW == 8 && warp - EXP_W0 >= 4;
+        const int p = (threadIdx.x - EXP_W0 * 32) & 127;  // row of this CTA's A half (isB: B^T half)
         const uint32_t src_off = (isB ? BITS_A : 0) + p * 16;
         const uint32_t dst_off = isB ? A_BYTES : 0;
         const uint32_t full_leader = mapa(smem_u32(&bars->full[0]), 0);
@@ -186,9 +194,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             }
         }
         __syncwarp();
-    } else if (warp < MMA_WARP) {
+    } else if (warp >= EPI_W0 && warp < EPI_W0 + NEW) {
         // ===================== epilogue (both CTAs) =====================
-        const int ew = warp - NPW;
+        const int ew = warp - EPI_W0;
         const int q = warp & 3;  // TMEM lane quarter (hardware: warp id % 4)
         const int h = ew >> 2;   // column half
         const int row_local = (int)rank * BM + q * 32 + lane;
@@ -273,7 +281,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                 }
             }
         }
-    } else if (rank == 0) {
+    } else if (warp == MMA_WARP && rank == 0) {
         // ===================== MMA issuer (leader CTA, one thread) =====================
         if (lane == 0) {
             int64_t gp = 0;
