@@ -35,6 +35,7 @@ extern "C" {
 #define GF2E_ECUDA 2    /* CUDA runtime / launch error (RuntimeError)            */
 #define GF2E_ENOMEM 3   /* workspace too small                                   */
 #define GF2E_ENODEV 4   /* no sm_100 device                                      */
+#define GF2E_ESINGULAR 5 /* zero diagonal entry in a triangular solve (SingularMatrixError) */
 
 /* gf2e_slice_mul flags */
 #define GF2E_ACCUMULATE 1u   /* C ^= A*B (addmul) instead of C = A*B              */
@@ -148,6 +149,30 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_host, int64_t lda, c
 int gf2e_plane_mul(const uint64_t *A_dev, int64_t lda, const uint64_t *B_dev, int64_t ldb,
                    uint64_t *C_dev, int64_t ldc, int64_t m, int64_t k, int64_t n, uint32_t flags,
                    void *workspace, int64_t workspace_bytes, void *stream);
+
+/*
+ * Triangular solve T X = B in place (X overwrites B), T m x m upper (upper != 0) or lower
+ * triangular over GF(2^e), both as plane stacks: the consumer of the hot path in the
+ * reference's recursive PLE/TRSM (trsm_upper_left / trsm_lower_left[_unit],
+ * ple_echelon.py:138-217).  Blocked recursion with 128-row-aligned splits; every off-diagonal
+ * update B_i ^= T_ij X_j is a gf2e_slice_mul(GF2E_ACCUMULATE) on plane views; diagonal blocks
+ * are inverted on device (k_tri_inverse) and applied with gf2e_slice_mul.  unit_diag: the
+ * stored diagonal is ignored and taken as 1 (lower only, as the reference).  Returns
+ * GF2E_ESINGULAR (B untouched) if a diagonal entry is zero; *bad_row (optional) receives the
+ * smallest such row.  Synchronises the stream once (singularity check).
+ */
+int64_t gf2e_trsm_workspace(int e, uint32_t f, int64_t m, int64_t n);
+int gf2e_trsm(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T_dev, int64_t ldt, int64_t pt,
+              uint64_t *B_dev, int64_t ldb, int64_t pb, int64_t m, int64_t n, void *workspace,
+              int64_t workspace_bytes, void *stream, int64_t *bad_row);
+
+/* mul_by_x (mat_sliced.py:109-122): out planes = alpha * in planes (alpha = class of x). */
+int gf2e_mul_by_x(int e, uint32_t f, const uint64_t *in_dev, int64_t ld, int64_t pin, uint64_t *out_dev,
+                  int64_t pout, int64_t rows, int64_t cols, void *stream);
+
+/* PackedMatrix.scalar_mul (mat_packed.py:192-199): out = c * in, packed words. */
+int gf2e_scalar_mul(int e, uint32_t f, uint32_t c, const uint64_t *in_dev, int64_t ldi, uint64_t *out_dev,
+                    int64_t ldo, int64_t rows, int64_t cols, void *stream);
 
 /*
  * Instrumentation: number of kernels the last successful call on this thread launched,

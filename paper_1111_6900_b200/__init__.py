@@ -10,7 +10,8 @@ from . import _lib
 from .gf2e import DEFAULT_POLYS, FieldCtx, field_new, is_irreducible, is_primitive
 from .mat_gf2 import BitMatrix, RowOpCounters, addmul as gf2_addmul, mul, mzd_addmul, mzd_mul, words_for
 from .mat_packed import PackedMatrix, pack_width
-from .mat_sliced import SlicedMatrix, cling, mzed_cling, mzed_slice, slice_packed
+from .mat_sliced import SlicedMatrix, cling, mul_by_x, mzed_cling, mzed_slice, slice_packed
+from .ple_echelon import SingularMatrixError, trsm_lower_left, trsm_lower_left_unit, trsm_sliced, trsm_upper_left
 from .poly_mul import (
     MulCounters,
     Schedule,
@@ -33,7 +34,8 @@ __all__ = [
     "DEFAULT_POLYS", "FieldCtx", "field_new", "is_irreducible", "is_primitive",
     "BitMatrix", "RowOpCounters", "mul", "gf2_addmul", "mzd_mul", "mzd_addmul", "words_for",
     "PackedMatrix", "pack_width",
-    "SlicedMatrix", "slice_packed", "cling", "mzed_slice", "mzed_cling",
+    "SlicedMatrix", "slice_packed", "cling", "mzed_slice", "mzed_cling", "mul_by_x",
+    "SingularMatrixError", "trsm_upper_left", "trsm_lower_left", "trsm_lower_left_unit", "trsm_sliced",
     "MulCounters", "Schedule", "schedule", "karatsuba_mul", "karatsuba_mul_packed", "karatsuba_mul_packed_host", "mzed_mul_host", "addmul", "addmul_packed",
     "reduce_mod_f", "count_products", "mzd_slice_mul", "mzd_slice_addmul", "mzed_mul", "mzed_addmul",
 ]

@@ -14,7 +14,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GF2E_LIB_PATH") or os.path.join(_HERE, "libgf2e_b200.so")  # env: dev A/B builds
 
-GF2E_OK, GF2E_EINVAL, GF2E_ECUDA, GF2E_ENOMEM, GF2E_ENODEV = 0, 1, 2, 3, 4
+GF2E_OK, GF2E_EINVAL, GF2E_ECUDA, GF2E_ENOMEM, GF2E_ENODEV, GF2E_ESINGULAR = 0, 1, 2, 3, 4, 5
 ACCUMULATE = 1
 BACKEND_TC = 0
 BACKEND_M4RM = 2
@@ -45,6 +45,11 @@ SIGNATURES = {
                               _U32, _P, _I64, _P]),
     "gf2e_mzed_mul_host": (_INT, [_INT, _U32, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _U32, _I64,
                                   ctypes.POINTER(ctypes.c_double)]),
+    "gf2e_trsm_workspace": (_I64, [_INT, _U32, _I64, _I64]),
+    "gf2e_trsm": (_INT, [_INT, _U32, _INT, _INT, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _P,
+                         ctypes.POINTER(_I64)]),
+    "gf2e_mul_by_x": (_INT, [_INT, _U32, _P, _I64, _I64, _P, _I64, _I64, _I64, _P]),
+    "gf2e_scalar_mul": (_INT, [_INT, _U32, _U32, _P, _I64, _P, _I64, _I64, _I64, _P]),
     "gf2e_plane_mul": (_INT, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _U32, _P, _I64, _P]),
     "gf2e_last_launch_count": (_INT, []),
     "gf2e_last_product_kernel": (ctypes.c_char_p, []),

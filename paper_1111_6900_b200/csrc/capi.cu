@@ -266,7 +266,6 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags) {
 int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, const uint64_t *B, int64_t ldb,
                 int64_t pb, uint64_t *C, int64_t ldc, int64_t pc, int64_t m, int64_t k, int64_t n, uint32_t flags,
                 void *ws, int64_t ws_bytes, cudaStream_t st) {
-    g_launches = 0;
     const bool acc = (flags & GF2E_ACCUMULATE) != 0;
     const int64_t nw = words_for(n);
     if (m == 0 || n == 0) return GF2E_OK;
@@ -335,6 +334,89 @@ struct HostPlan {
         cudaError_t _e = (expr);                           \
         if (_e != cudaSuccess) return cuda_fail(_e, what); \
     } while (0)
+
+
+// ---- blocked TRSM over plane views (consumer of run_product) ------------------------------
+uint32_t gf_mul_host(uint32_t a, uint32_t b, int e, uint32_t f) {
+    uint32_t acc = 0;
+    for (int i = 0; i < e; ++i)
+        if ((b >> i) & 1u) acc ^= a << i;
+    for (int d = 2 * e - 2; d >= e; --d)
+        if ((acc >> d) & 1u) acc ^= f << (d - e);
+    return acc;
+}
+
+// smallest element of multiplicative order 2^e - 1 (f irreducible => one exists)
+uint32_t primitive_element(int e, uint32_t f) {
+    const uint32_t q1 = (1u << e) - 1;
+    for (uint32_t g = 2; g <= q1; ++g) {
+        uint32_t v = g, ord = 1;
+        while (v != 1 && ord <= q1) {
+            v = gf_mul_host(v, g, e, f);
+            ++ord;
+        }
+        if (ord == q1) return g;
+    }
+    return 2;
+}
+
+struct TrsmLayout {
+    int64_t nblk, inv_bytes, tmp_bytes, mul_bytes, total;
+};
+
+TrsmLayout trsm_layout(int nprod, int e, int64_t m, int64_t n) {
+    TrsmLayout T;
+    T.nblk = (m + kTrsmBlock - 1) / kTrsmBlock;
+    T.inv_bytes = align256(T.nblk * e * kTrsmBlock * (kTrsmBlock / 64) * 8);
+    T.tmp_bytes = align256((int64_t)e * kTrsmBlock * words_for(n) * 8);
+    T.mul_bytes = layout_for(nprod, m, m, n, 0).total;  // bounds every update and block product
+    T.total = T.inv_bytes + T.tmp_bytes + 256 + T.mul_bytes;
+    return T;
+}
+
+struct TrsmCtx {
+    Sched ks;
+    bool upper;
+    const uint64_t *T;
+    int64_t ldt, pt;
+    uint64_t *B;
+    int64_t ldb, pb, n;
+    uint64_t *inv, *tmp;
+    void *mulws;
+    int64_t mulws_bytes;
+    int e;
+    cudaStream_t st;
+};
+
+int trsm_rec(TrsmCtx &c, int64_t i0, int64_t i1) {
+    const int64_t rows = i1 - i0;
+    const int64_t nw = words_for(c.n);
+    if (rows <= kTrsmBlock) {  // X = inv(T_blk) . B_blk  (tensor-core product), then copy back
+        const uint64_t *Ib = c.inv + (i0 / kTrsmBlock) * c.e * kTrsmBlock * (kTrsmBlock / 64);
+        if (int rc = run_product(c.ks, Ib, kTrsmBlock / 64, kTrsmBlock * (kTrsmBlock / 64), c.B + i0 * c.ldb, c.ldb,
+                                 c.pb, c.tmp, nw, kTrsmBlock * nw, rows, rows, c.n, 0, c.mulws, c.mulws_bytes, c.st))
+            return rc;
+        for (int t = 0; t < c.e; ++t)
+            CKH(cudaMemcpy2DAsync(c.B + t * c.pb + i0 * c.ldb, c.ldb * 8, c.tmp + t * kTrsmBlock * nw, nw * 8, nw * 8,
+                                  rows, cudaMemcpyDeviceToDevice, c.st),
+                "trsm copy");
+        return GF2E_OK;
+    }
+    const int64_t h = i0 + round_up(rows / 2, kTrsmBlock);  // aligned split: plane views stay word aligned
+    auto update = [&](int64_t r0, int64_t r1, int64_t k0, int64_t k1) {  // B[r0:r1] ^= T[r0:r1, k0:k1] X[k0:k1]
+        return run_product(c.ks, c.T + r0 * c.ldt + k0 / 64, c.ldt, c.pt, c.B + k0 * c.ldb, c.ldb, c.pb,
+                           c.B + r0 * c.ldb, c.ldb, c.pb, r1 - r0, k1 - k0, c.n, GF2E_ACCUMULATE, c.mulws,
+                           c.mulws_bytes, c.st);
+    };
+    if (c.upper) {  // ple_echelon.py:201-217 order: bottom block, update top, top block
+        if (int rc = trsm_rec(c, h, i1)) return rc;
+        if (int rc = update(i0, h, h, i1)) return rc;
+        return trsm_rec(c, i0, h);
+    }
+    if (int rc = trsm_rec(c, i0, h)) return rc;  // ple_echelon.py:159-175
+    if (int rc = update(h, i1, i0, h)) return rc;
+    return trsm_rec(c, h, i1);
+}
 
 int check_flags(uint32_t flags) {
     if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM)) return fail(GF2E_EINVAL, "unknown flags 0x%x", flags);
@@ -654,6 +736,82 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     CKH(cudaEventElapsedTime(&ms, ev_t0, ev_t1), "cudaEventElapsedTime");
     if (device_ms) *device_ms = ms;
     g_kernel = "k_product_tc2";
+    return GF2E_OK;
+}
+
+int64_t gf2e_trsm_workspace(int e, uint32_t f, int64_t m, int64_t n) {
+    g_err.clear();
+    if (check_field(e, f)) return -1;
+    if (m < 0 || n < 0) return fail(GF2E_EINVAL, "matrix dimensions must be non-negative"), -1;
+    if (m == 0 || n == 0) return 0;
+    return trsm_layout((int)get_schedule(e, f).subsets.size(), e, m, n).total;
+}
+
+int gf2e_trsm(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, int64_t ldt, int64_t pt, uint64_t *B,
+              int64_t ldb, int64_t pb, int64_t m, int64_t n, void *ws, int64_t ws_bytes, void *stream,
+              int64_t *bad_row) {
+    g_err.clear();
+    g_launches = 0;
+    if (bad_row) *bad_row = -1;
+    if (int rc = check_field(e, f)) return rc;
+    if (unit_diag && upper) return fail(GF2E_EINVAL, "unit_diag is only defined for lower triangular solves");
+    if (int rc = check_mat(T, m, words_for(m), ldt, "T")) return rc;
+    if (int rc = check_mat(B, m, words_for(n), ldb, "B")) return rc;
+    if (m == 0 || n == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    const Schedule &S = get_schedule(e, f);
+    TrsmLayout L = trsm_layout((int)S.subsets.size(), e, m, n);
+    if (ws_bytes < L.total)
+        return fail(GF2E_ENOMEM, "workspace too small: %lld < %lld bytes", (long long)ws_bytes, (long long)L.total);
+    if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255))
+        return fail(GF2E_EINVAL, "workspace must be a 256-byte aligned device pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    char *w = static_cast<char *>(ws);
+    uint64_t *inv = reinterpret_cast<uint64_t *>(w);
+    uint64_t *tmp = reinterpret_cast<uint64_t *>(w + L.inv_bytes);
+    int *flag = reinterpret_cast<int *>(w + L.inv_bytes + L.tmp_bytes);
+    void *mulws = w + L.inv_bytes + L.tmp_bytes + 256;
+    const int big = 0x7fffffff;
+    CKH(cudaMemcpyAsync(flag, &big, sizeof(int), cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    CK(launch_tri_inverse(e, f, primitive_element(e, f), T, ldt, pt, m, upper != 0, unit_diag != 0, inv, flag, st),
+       "tri_inverse");
+    int bad = big;
+    CKH(cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (bad != big) {
+        if (bad_row) *bad_row = bad;
+        return fail(GF2E_ESINGULAR, "zero diagonal entry at index %d", bad);
+    }
+    TrsmCtx c{to_kernel_sched(e, S), upper != 0, T, ldt, pt, B, ldb, pb, n, inv, tmp, mulws, L.mul_bytes, e, st};
+    return trsm_rec(c, 0, m);
+}
+
+int gf2e_mul_by_x(int e, uint32_t f, const uint64_t *in, int64_t ld, int64_t pin, uint64_t *out, int64_t pout,
+                  int64_t rows, int64_t cols, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (int rc = check_field(e, f)) return rc;
+    if (int rc = check_mat(in, rows, words_for(cols), ld, "in")) return rc;
+    if (int rc = check_mat(out, rows, words_for(cols), ld, "out")) return rc;
+    if (rows == 0 || cols == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    CK(launch_mul_by_x(e, f, in, ld, pin, out, pout, rows, words_for(cols), (cudaStream_t)stream), "mul_by_x");
+    return GF2E_OK;
+}
+
+int gf2e_scalar_mul(int e, uint32_t f, uint32_t c, const uint64_t *in, int64_t ldi, uint64_t *out, int64_t ldo,
+                    int64_t rows, int64_t cols, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (int rc = check_field(e, f)) return rc;
+    if (c >= (1u << e)) return fail(GF2E_EINVAL, "scalar %u out of range for GF(2^%d)", c, e);
+    const int w = gf2e_pack_width(e);
+    if (int rc = check_mat(in, rows, words_for(cols * w), ldi, "in")) return rc;
+    if (int rc = check_mat(out, rows, words_for(cols * w), ldo, "out")) return rc;
+    if (rows == 0 || cols == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    CK(launch_scalar_mul(e, f, c, w, in, ldi, out, ldo, rows, words_for(cols * w), (cudaStream_t)stream),
+       "scalar_mul");
     return GF2E_OK;
 }
 

@@ -162,3 +162,15 @@ class PackedMatrix:
 
     def is_zero(self) -> bool:
         return self.storage.is_zero()
+
+    def scalar_mul(self, c: int) -> "PackedMatrix":
+        """Every entry multiplied by the scalar c (mat_packed.py:192-199), on device."""
+        if not 0 <= c < self.ctx.order:
+            raise ValueError(f"scalar {c} out of range for GF(2^{self.ctx.e})")
+        ld = self.storage.words.shape[1]
+        out = PackedMatrix(self.ctx, self.nrows, self.ncols,
+                           BitMatrix(self.nrows, self.ncols * self.w, _device.empty_words((self.nrows, ld))))
+        if self.nrows and ld:
+            _lib.call("gf2e_scalar_mul", self.ctx.e, self.ctx.f, c, _device.ptr(self.storage.words), ld,
+                      _device.ptr(out.storage.words), ld, self.nrows, self.ncols, _device.stream_handle())
+        return out

@@ -151,5 +151,15 @@ def cling(S: SlicedMatrix, out: PackedMatrix | None = None) -> PackedMatrix:
     return out
 
 
+def mul_by_x(S: SlicedMatrix) -> SlicedMatrix:
+    """Every entry times alpha (the class of x), reduced mod f (mat_sliced.py:109-122), on device."""
+    out = SlicedMatrix(S.ctx, S.nrows, S.ncols, _device.empty_words(tuple(S.planes.shape)))
+    nw = S.planes.shape[2]
+    if S.nrows and nw:
+        _lib.call("gf2e_mul_by_x", S.ctx.e, S.ctx.f, _device.ptr(S.planes), nw, S.nrows * nw,
+                  _device.ptr(out.planes), S.nrows * nw, S.nrows, S.ncols, _device.stream_handle())
+    return out
+
+
 mzed_slice = slice_packed
 mzed_cling = cling

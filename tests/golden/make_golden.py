@@ -26,7 +26,7 @@ import sys
 import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
-from gf2elin import gf2e, mat_gf2, mat_packed, mat_sliced, poly_mul, rng  # noqa: E402
+from gf2elin import gf2e, mat_gf2, mat_packed, mat_sliced, ple_echelon, poly_mul, rng  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
 
@@ -133,6 +133,48 @@ def main():
     # field tables for e = 2..4 (GF(4) mul(2,2)=3 etc.)
     for e in (2, 3, 4):
         store[f"field/e{e}/mul"] = gf2e.field_new(e).mul_table.copy()
+
+    # triangular solves (ple_echelon.py:138-217): U X = B, L X = B (unit / non-unit)
+    tr = []
+    for e, m, n, seed in [(2, 70, 130, 5), (8, 300, 90, 6), (5, 257, 64, 7), (10, 130, 300, 8), (3, 1, 5, 9)]:
+        ctx = gf2e.field_new(e)
+        R = mat_packed.PackedMatrix.random(ctx, m, m, seed).to_array()
+        diag = (rng.element_stream(seed + 100, m, e) % (ctx.order - 1)) + 1  # nonzero diagonal
+        upper = np.triu(R, 1)
+        lower = np.tril(R, -1)
+        np.fill_diagonal(upper, diag)
+        np.fill_diagonal(lower, diag)
+        B = mat_packed.PackedMatrix.random(ctx, m, n, seed + 1)
+        U = mat_packed.PackedMatrix.from_array(ctx, upper)
+        L = mat_packed.PackedMatrix.from_array(ctx, lower)
+        XU, XL, XLu = B.copy(), B.copy(), B.copy()
+        ple_echelon.trsm_upper_left(U, XU)
+        ple_echelon.trsm_lower_left(L, XL)
+        ple_echelon.trsm_lower_left_unit(L, XLu)
+        tag = f"trsm/e{e}/{m}x{n}"
+        store[f"{tag}/meta"] = np.array([e, ctx.f, m, n], dtype=np.int64)
+        store[f"{tag}/U"] = U.storage.words.copy()
+        store[f"{tag}/L"] = L.storage.words.copy()
+        store[f"{tag}/B"] = B.storage.words.copy()
+        store[f"{tag}/XU"] = XU.storage.words.copy()
+        store[f"{tag}/XL"] = XL.storage.words.copy()
+        store[f"{tag}/XLu"] = XLu.storage.words.copy()
+        tr.append(tag)
+    store["trsm_tags"] = np.array(tr)
+
+    # sliced mul_by_x (mat_sliced.py:109-122) and packed scalar_mul (mat_packed.py:192-199)
+    sc = []
+    for e in range(2, 11):
+        ctx = gf2e.field_new(e)
+        A = mat_packed.PackedMatrix.random(ctx, 37, 70, 40 + e)
+        tag = f"scal/e{e}"
+        store[f"{tag}/A"] = A.storage.words.copy()
+        store[f"{tag}/xA"] = np.stack([s.words for s in mat_sliced.mul_by_x(mat_sliced.slice_packed(A)).slices])
+        cs = [0, 1, 2, ctx.order - 1, (5 * e) % ctx.order]
+        store[f"{tag}/c"] = np.array(cs, dtype=np.int64)
+        store[f"{tag}/cA"] = np.stack([A.scalar_mul(c).storage.words for c in cs])
+        sc.append(tag)
+    store["scal_tags"] = np.array(sc)
 
     np.savez_compressed(OUT, **store)
     print(f"wrote {OUT}: {len(store)} arrays, {os.path.getsize(OUT)} bytes")
