@@ -1,0 +1,88 @@
+"""Per-kernel measurements beside bench.py's headline: HBM-bound conversions against the
+measured HBM roofline, and the TRSM consumer's throughput.  Prints one JSON line per op.
+
+    python tools/bench_ops.py [--e 8] [--m 16384] [--n 16384]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1111_6900_b200 as g  # noqa: E402
+
+
+def timed(fn, reps=5, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--e", type=int, default=8)
+    ap.add_argument("--m", type=int, default=16384)
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--trsm-m", type=int, default=8192)
+    a = ap.parse_args()
+    try:
+        hbm = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                          "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except (OSError, ValueError, KeyError):
+        hbm = 6650.0
+    e, m, n = a.e, a.m, a.n
+    ctx = g.field_new(e)
+    w = g.pack_width(e)
+    P = g.PackedMatrix.random(ctx, m, n, 1)
+    S = g.slice_packed(P)
+    packed_b = m * g.words_for(n * w) * 8
+    planes_b = e * m * g.words_for(n) * 8
+
+    def line(op, ms, bytes_, extra=None):
+        gbs = bytes_ / (ms * 1e-3) / 1e9
+        d = {"op": op, "e": e, "shape": [m, n], "ms": round(ms, 4), "bytes": bytes_, "GB/s": round(gbs, 1),
+             "hbm_peak_GB/s": hbm, "frac": round(gbs / hbm, 3)}
+        d.update(extra or {})
+        print(json.dumps(d), flush=True)
+
+    line("slice (K1)", timed(lambda: g.slice_packed(P, out=S)), packed_b + planes_b)
+    line("cling (K2)", timed(lambda: g.cling(S, out=P)), packed_b + planes_b)
+    line("mul_by_x", timed(lambda: g.mul_by_x(S)), 2 * planes_b)
+    line("scalar_mul", timed(lambda: P.scalar_mul(3)), 2 * packed_b)
+    line("random_sliced (K7)", timed(lambda: g.SlicedMatrix.random(ctx, m, n, 5)), planes_b,
+         {"note": "ALU-bound generator (2 64-bit multiplies per element)"})
+
+    # TRSM consumer: U X = B, m x m upper triangular, n right-hand sides
+    tm = a.trsm_m
+    R = g.PackedMatrix.random(ctx, tm, tm, 7).to_array()
+    up = np.triu(R, 1)
+    np.fill_diagonal(up, (np.arange(tm) % (ctx.order - 1)) + 1)
+    Us = g.slice_packed(g.PackedMatrix.from_array(ctx, up))
+    B0 = g.SlicedMatrix.random(ctx, tm, n, 8)
+    X = B0.copy()
+
+    def solve():
+        X.planes.copy_(B0.planes)
+        g.trsm_sliced(Us, X, upper=True)
+
+    ms = timed(solve, reps=3, warm=1)
+    K = g.count_products(e)
+    ops = K * tm * tm * n  # ~K(e) * 2 * (m^2/2) * n GF(2) bit-ops for the triangular product
+    print(json.dumps({"op": "trsm_upper (sliced)", "e": e, "m": tm, "n": n, "ms": round(ms, 3),
+                      "eff_Tbit-op/s": round(ops / (ms * 1e-3) / 1e12, 1),
+                      "note": "K(e)*m^2*n GF(2) bit-ops; updates via addmul, 128-row diagonal blocks inverted on device"}),
+          flush=True)
+
+
+if __name__ == "__main__":
+    main()
