@@ -154,6 +154,107 @@ __global__ void k_cling(int e, int64_t rows, int64_t cols, const uint64_t *__res
     }
 }
 
+// ---- w = 8 (e = 5..8) fast paths: 8x8 bit-matrix transposes + byte gathers ---------------
+// transpose of the 8x8 bit matrix held in a word (byte i = row i, bit j = column j):
+// afterwards byte j bit i = old byte i bit j  (three delta swaps)
+__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {
+    uint64_t t;
+    t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAULL;
+    x = x ^ t ^ (t << 7);
+    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCULL;
+    x = x ^ t ^ (t << 14);
+    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ULL;
+    x = x ^ t ^ (t << 28);
+    return x;
+}
+
+// byte b of each of 8 words, packed into one word (byte q = byte b of v[q])
+__device__ __forceinline__ uint64_t gather_byte(const uint64_t (&v)[8], int b) {
+    const uint32_t sel = (uint32_t)(b & 3) | ((uint32_t)((b & 3) + 4) << 4);  // bytes b, 4+b of (a,c)
+    uint32_t h[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) h[q] = b < 4 ? (uint32_t)v[q] : (uint32_t)(v[q] >> 32);
+    const uint32_t p01 = __byte_perm(h[0], h[1], sel), p23 = __byte_perm(h[2], h[3], sel);
+    const uint32_t p45 = __byte_perm(h[4], h[5], sel), p67 = __byte_perm(h[6], h[7], sel);
+    const uint32_t lo = __byte_perm(p01, p23, 0x5410), hi = __byte_perm(p45, p67, 0x5410);
+    return (uint64_t)lo | ((uint64_t)hi << 32);
+}
+
+// K1, w = 8: thread = one 64-bit plane word position (64 elements = 8 packed words)
+__global__ void k_slice_w8(int e, int64_t rows, int64_t cols, const uint64_t *__restrict__ packed, int64_t ldp,
+                           uint64_t *__restrict__ planes, int64_t ld, int64_t pstride) {
+    const int64_t nw = words_for(cols);
+    const int64_t pwords = words_for(cols * 8);
+    const uint64_t tm = tail_mask(cols);
+    const int64_t total = rows * ld;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        const int64_t r = idx / ld, wi = idx - r * ld;
+        uint64_t v[8];
+        if (wi < nw) {
+            const uint64_t *src = packed + r * ldp + wi * 8;
+            if (wi * 8 + 8 <= pwords && !(reinterpret_cast<uintptr_t>(src) & 15)) {
+#pragma unroll
+                for (int q = 0; q < 8; q += 2) {
+                    const ulonglong2 p = *reinterpret_cast<const ulonglong2 *>(src + q);
+                    v[q] = p.x;
+                    v[q + 1] = p.y;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = (wi * 8 + q < pwords) ? src[q] : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = transpose8x8(v[q]);  // byte t of v[q] = bit t of elements 8q..8q+7
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = 0;
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            if (t < e) {
+                uint64_t p = gather_byte(v, t);
+                if (wi == nw - 1) p &= tm;
+                planes[t * pstride + idx] = p;
+            }
+        }
+    }
+}
+
+// K2, w = 8: thread = one plane word position -> 8 packed words (pad bits 0)
+__global__ void k_cling_w8(int e, int64_t rows, int64_t cols, const uint64_t *__restrict__ planes, int64_t ld,
+                           int64_t pstride, uint64_t *__restrict__ packed, int64_t ldp) {
+    const int64_t nw = words_for(cols);
+    const int64_t pwords = words_for(cols * 8);
+    const int64_t total = rows * nw;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        const int64_t r = idx / nw, wi = idx - r * nw;
+        uint64_t pl[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) pl[t] = t < e ? planes[t * pstride + r * ld + wi] : 0;
+        if (wi == nw - 1) {
+            const uint64_t tmk = tail_mask(cols);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) pl[t] &= tmk;
+        }
+        uint64_t out[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) out[q] = transpose8x8(gather_byte(pl, q));  // byte s bit t = plane t elem 8q+s
+        uint64_t *dst = packed + r * ldp + wi * 8;
+        if (wi * 8 + 8 <= pwords && !(reinterpret_cast<uintptr_t>(dst) & 15)) {
+#pragma unroll
+            for (int q = 0; q < 8; q += 2)
+                *reinterpret_cast<ulonglong2 *>(dst + q) = make_ulonglong2(out[q], out[q + 1]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (wi * 8 + q < pwords) dst[q] = out[q];
+        }
+        // words of the packed row beyond the last element-carrying word (ldp > pwords) are padding
+        if (wi == nw - 1)
+            for (int64_t q = pwords; q < ldp; ++q) packed[r * ldp + q] = 0;
+    }
+}
+
 __global__ void k_xor(uint64_t *__restrict__ x, int64_t ldx, const uint64_t *__restrict__ y, int64_t ldy,
                       int64_t rows, int64_t nwords) {
     const int64_t total = rows * nwords;
@@ -372,7 +473,7 @@ cudaError_t launch_slice(int e, int w, int64_t rows, int64_t cols, const uint64_
     switch (w) {
         case 2: k_slice<2><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
         case 4: k_slice<4><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
-        case 8: k_slice<8><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
+        case 8: k_slice_w8<<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
         case 16: k_slice<16><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
         default: return cudaErrorInvalidValue;
     }
@@ -387,7 +488,12 @@ cudaError_t launch_cling(int e, int w, int64_t rows, int64_t cols, const uint64_
     switch (w) {
         case 2: k_cling<2><<<g, 256, 0, st>>>(e, rows, cols, planes, ld, pstride, packed, ldp); break;
         case 4: k_cling<4><<<g, 256, 0, st>>>(e, rows, cols, planes, ld, pstride, packed, ldp); break;
-        case 8: k_cling<8><<<g, 256, 0, st>>>(e, rows, cols, planes, ld, pstride, packed, ldp); break;
+        case 8: {
+            const int64_t tw = rows * words_for(cols);
+            if (tw == 0) return cudaMemset2DAsync(packed, ldp * 8, 0, ldp * 8, rows, st);
+            k_cling_w8<<<grid_for(tw, 256), 256, 0, st>>>(e, rows, cols, planes, ld, pstride, packed, ldp);
+            break;
+        }
         case 16: k_cling<16><<<g, 256, 0, st>>>(e, rows, cols, planes, ld, pstride, packed, ldp); break;
         default: return cudaErrorInvalidValue;
     }
