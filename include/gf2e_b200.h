@@ -194,6 +194,14 @@ int gf2e_profile_enable(int on);
  * (units of 1e12) and the launch time in *ms.  The roofline denominator of bench.py.
  */
 int gf2e_mma_peak(int cta_group, int iters, double *tops, double *ms, void *stream);
+/*
+ * Development probe (not on the product path): block-scaled FP4 tcgen05 MMA (kind::mxf4,
+ * M=128 N=256 K=64, all scales 1.0) on fixed operand images a_dev [128][128 B], b_dev
+ * [256][128 B] (two e2m1 elements per byte), iters x 4 MMAs per SM; out_dev [128][256]
+ * receives CTA 0's raw fp32 accumulator.  mode bit 0: accumulator starts at 65536.0f.
+ */
+int gf2e_dev_fp4_probe(int iters, int mode, const uint8_t *a_dev, const uint8_t *b_dev, uint32_t *out_dev,
+                       double *tops, void *stream);
 int gf2e_profile_read(double *total_ms, int *launches);
 
 #ifdef __cplusplus

@@ -55,6 +55,7 @@ SIGNATURES = {
     "gf2e_last_product_kernel": (ctypes.c_char_p, []),
     "gf2e_profile_enable": (_INT, [_INT]),
     "gf2e_profile_read": (_INT, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_INT)]),
+    "gf2e_dev_fp4_probe": (_INT, [_INT, _INT, _P, _P, _P, ctypes.POINTER(ctypes.c_double), _P]),
     "gf2e_mma_peak": (_INT, [_INT, _INT, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
 }
 

@@ -478,6 +478,21 @@ int gf2e_mma_peak(int cta_group, int iters, double *tops, double *ms, void *stre
     return GF2E_OK;
 }
 
+int gf2e_dev_fp4_probe(int iters, int mode, const uint8_t *a_dev, const uint8_t *b_dev, uint32_t *out_dev,
+                       double *tops, void *stream) {
+    g_err.clear();
+    if (iters < 1 || !a_dev || !b_dev || !out_dev) return fail(GF2E_EINVAL, "bad probe arguments");
+    if (int rc = check_device()) return rc;
+    int dev = 0, nsms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsms, cudaDevAttrMultiProcessorCount, dev);
+    float ms = 0;
+    cudaError_t e = run_fp4_probe(iters, mode, a_dev, b_dev, out_dev, nsms, (cudaStream_t)stream, &ms);
+    if (e != cudaSuccess) return cuda_fail(e, "fp4_probe");
+    if (tops) *tops = (double)nsms * iters * 4.0 * 2.0 * 128.0 * 256.0 * 64.0 / (ms * 1e-3) / 1e12;
+    return GF2E_OK;
+}
+
 int gf2e_pack_width(int e) {
     if (e < 2 || e > 10) return -1;
     for (int w : {1, 2, 4, 8, 16, 32, 64})

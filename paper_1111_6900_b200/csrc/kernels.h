@@ -84,6 +84,8 @@ cudaError_t launch_mul_by_x(int e, uint32_t f, const uint64_t *in, int64_t ld, i
 cudaError_t launch_scalar_mul(int e, uint32_t f, uint32_t c, int w, const uint64_t *in, int64_t ldi, uint64_t *out,
                               int64_t ldo, int64_t rows, int64_t nwords, cudaStream_t st);
 
+cudaError_t run_fp4_probe(int iters, int mode, const uint8_t *a_img, const uint8_t *b_img, uint32_t *out, int nctas,
+                          cudaStream_t st, float *ms);
 cudaError_t run_mma_peak(int cta_group, int iters, int nsms, cudaStream_t st, float *ms);
 
 }  // namespace gf2e
