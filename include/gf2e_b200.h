@@ -41,6 +41,8 @@ extern "C" {
 #define GF2E_ACCUMULATE 1u   /* C ^= A*B (addmul) instead of C = A*B              */
 #define GF2E_BACKEND_TC 0u   /* K4 on tcgen05 kind::i8 tensor cores (default)     */
 #define GF2E_BACKEND_M4RM 2u /* K4 as M4RM Gray tables in shared memory (INT pipe) */
+#define GF2E_TC_INT8 4u      /* tensor-core K4 forced to kind::i8                          */
+#define GF2E_TC_FP4 8u       /* tensor-core K4 forced to kind::mxf4 (default for k >= 2048)  */
 
 /* Last error message of the calling thread ("" if none). */
 const char *gf2e_last_error(void);

@@ -18,6 +18,8 @@ GF2E_OK, GF2E_EINVAL, GF2E_ECUDA, GF2E_ENOMEM, GF2E_ENODEV, GF2E_ESINGULAR = 0, 
 ACCUMULATE = 1
 BACKEND_TC = 0
 BACKEND_M4RM = 2
+TC_INT8 = 4
+TC_FP4 = 8
 
 _I64 = ctypes.c_int64
 _U64 = ctypes.c_uint64

@@ -239,6 +239,15 @@ struct Layout {
 
 int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 
+// Tensor-core form: fp4 (kind::mxf4, 2x the int8 rate) unless forced to int8; int8 for short
+// inner dimensions, where the single fp4 accumulator's per-product hand-off would dominate.
+constexpr int64_t kFp4MinK = 2048;
+bool use_fp4(uint32_t flags, int64_t k) {
+    if (flags & GF2E_TC_FP4) return true;
+    if (flags & GF2E_TC_INT8) return false;
+    return k >= kFp4MinK;
+}
+
 Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags) {
     Layout L;
     if (flags & GF2E_BACKEND_M4RM) {
@@ -251,7 +260,7 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags) {
     } else {
         L.m_pad = round_up(m, 2 * kTcBM);  // CTA-pair tiles are 256 rows
         L.n_pad = round_up(n, kTcBN);
-        L.k_pad = round_up(k, kTcBK);
+        L.k_pad = round_up(k, use_fp4(flags, k) ? kTcBKFp4 : kTcBK);
         L.kwords = L.k_pad / 64;
         L.a_pstride = L.m_pad * L.kwords;
         L.b_pstride = L.n_pad * L.kwords;
@@ -283,10 +292,13 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
     uint64_t *Ac = static_cast<uint64_t *>(ws);
     uint64_t *Bx = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + L.a_bytes);
     const bool tc = !(flags & GF2E_BACKEND_M4RM);
-    CK(launch_combos_rows(ks, A, lda, pa, m, k, Ac, L.kwords, L.a_pstride, L.m_pad, L.kwords, tc, st), "combos(A)");
+    const bool fp4 = tc && use_fp4(flags, k);
+    CK(launch_combos_rows(ks, A, lda, pa, m, k, Ac, L.kwords, L.a_pstride, L.m_pad, L.kwords, tc ? (fp4 ? 4 : 2) : 0,
+                          st),
+       "combos(A)");
     if (!tc) {
         const int64_t nwp = L.n_pad / 64;
-        CK(launch_combos_rows(ks, B, ldb, pb, k, n, Bx, nwp, L.b_pstride, L.k_pad, nwp, false, st), "combos(B)");
+        CK(launch_combos_rows(ks, B, ldb, pb, k, n, Bx, nwp, L.b_pstride, L.k_pad, nwp, 0, st), "combos(B)");
         if (!acc)
             for (int j = 0; j < ks.nout; ++j)
                 CK(cudaMemset2DAsync(C + j * pc, ldc * 8, 0, nw * 8, m, st), "cudaMemset2DAsync");
@@ -295,12 +307,12 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
         CK(launch_product_m4rm(ks, a, st), "product_m4rm");
         g_kernel = "k_product_m4rm";
     } else {
-        CK(launch_combos_bt(ks, B, ldb, pb, k, n, Bx, L.kwords, L.b_pstride, L.kwords, L.n_pad / 64, st),
+        CK(launch_combos_bt(ks, B, ldb, pb, k, n, Bx, L.kwords, L.b_pstride, L.kwords, L.n_pad / 64, fp4, st),
            "combos(B^T)");
         TcArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, m, n, L.m_pad, L.n_pad, C, ldc, pc, acc ? 1 : 0};
         ProfScope prof(st);
-        CK(launch_product_tc2(ks, a, st), "product_tc2");
-        g_kernel = "k_product_tc2";
+        CK(launch_product_tc2(ks, a, fp4, st), "product_tc2");
+        g_kernel = fp4 ? "k_product_tc2<fp4>" : "k_product_tc2<i8>";
     }
     return GF2E_OK;
 }
@@ -419,7 +431,9 @@ int trsm_rec(TrsmCtx &c, int64_t i0, int64_t i1) {
 }
 
 int check_flags(uint32_t flags) {
-    if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM)) return fail(GF2E_EINVAL, "unknown flags 0x%x", flags);
+    if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM | GF2E_TC_INT8 | GF2E_TC_FP4))
+        return fail(GF2E_EINVAL, "unknown flags 0x%x", flags);
+    if ((flags & GF2E_TC_INT8) && (flags & GF2E_TC_FP4)) return fail(GF2E_EINVAL, "conflicting flags 0x%x", flags);
     return GF2E_OK;
 }
 
@@ -717,7 +731,9 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     if (int rc = h2d_chunk(0)) return rc;
     CKH(cudaStreamWaitEvent(P.sc, ev_b, 0), "cudaStreamWaitEvent");
     CK(launch_slice(e, w, k, n, dBp, wb, dBs, nwn, k * nwn, P.sc), "slice(B)");
-    CK(launch_combos_bt(ks, dBs, nwn, k * nwn, k, n, dBt, LB.kwords, LB.b_pstride, LB.kwords, LB.n_pad / 64, P.sc),
+    const bool fp4 = use_fp4(0, k);
+    CK(launch_combos_bt(ks, dBs, nwn, k * nwn, k, n, dBt, LB.kwords, LB.b_pstride, LB.kwords, LB.n_pad / 64, fp4,
+                        P.sc),
        "combos(B^T)");
     for (int64_t i = 0; i < nchunks; ++i) {
         const int sl = (int)(i % nslots);
@@ -729,13 +745,13 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         if (acc) CK(launch_slice(e, w, rows, n, dCp[sl], wb, dCs[sl], nwn, rows * nwn, P.sc), "slice(C0)");
         Layout L = layout_for(ks.nprod, rows, k, n, 0);
         CK(launch_combos_rows(ks, dAs[sl], nwk, rows * nwk, rows, k, dAc, L.kwords, L.a_pstride, L.m_pad, L.kwords,
-                              true, P.sc),
+                              fp4 ? 4 : 2, P.sc),
            "combos(A)");
         TcArgs ta{dAc, dBt, L.a_pstride, LB.b_pstride, L.kwords, rows, n, L.m_pad, LB.n_pad, dCs[sl], nwn, rows * nwn,
                   acc ? 1 : 0};
         {
             ProfScope prof(P.sc);
-            CK(launch_product_tc2(ks, ta, P.sc), "product_tc2");
+            CK(launch_product_tc2(ks, ta, fp4, P.sc), "product_tc2");
         }
         CK(launch_cling(e, w, rows, n, dCs[sl], nwn, rows * nwn, dCp[sl], wb, P.sc), "cling(C)");
         CKH(cudaEventRecord(out_ready[sl], P.sc), "cudaEventRecord");
@@ -750,7 +766,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     float ms = 0;
     CKH(cudaEventElapsedTime(&ms, ev_t0, ev_t1), "cudaEventElapsedTime");
     if (device_ms) *device_ms = ms;
-    g_kernel = "k_product_tc2";
+    g_kernel = fp4 ? "k_product_tc2<fp4>" : "k_product_tc2<i8>";
     return GF2E_OK;
 }
 

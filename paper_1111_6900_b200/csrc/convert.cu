@@ -289,12 +289,11 @@ __global__ void k_reduce(int e, uint32_t f, uint64_t *__restrict__ planes, int64
 
 // ---- K3 operand combinations --------------------------------------------------------
 
-// out[t] = XOR_{i in S_t} X_i on a zero-padded (rows_pad x words_pad) grid, natural bit order.
-// tiled: write the stage-tiled layout of the tensor-core kernel (tc_tile_word) instead of
-// row-major rows of ldo words.
+// out[t] = XOR_{i in S_t} X_i on a zero-padded (rows_pad x words_pad) grid, natural bit order,
+// row-major rows of ldo words (the M4RM operands; the tensor-core ones use k_combos_tiled).
 __global__ void k_combos_rows(Sched s, const uint64_t *__restrict__ X, int64_t ldx, int64_t px, int64_t rows,
                               int64_t ncols, uint64_t *__restrict__ out, int64_t ldo, int64_t po,
-                              int64_t rows_pad, int64_t words_pad, int tiled) {
+                              int64_t rows_pad, int64_t words_pad) {
     const int64_t nw = words_for(ncols);
     const uint64_t tm = tail_mask(ncols);
     const int64_t total = rows_pad * words_pad;
@@ -312,7 +311,7 @@ __global__ void k_combos_rows(Sched s, const uint64_t *__restrict__ X, int64_t l
             uint64_t acc = 0;
 #pragma unroll
             for (int i = 0; i < kMaxE; ++i) acc ^= x[i] & (0ULL - (uint64_t)((sub >> i) & 1u));
-            out[t * po + (tiled ? tc_tile_word(r, w, words_pad) : r * ldo + w)] = acc;
+            out[t * po + r * ldo + w] = acc;
         }
     }
 }
@@ -322,10 +321,10 @@ __global__ void k_combos_rows(Sched s, const uint64_t *__restrict__ X, int64_t l
 // consecutive tile rows = 512 contiguous bytes.
 __global__ void k_combos_tiled(Sched s, const uint64_t *__restrict__ X, int64_t ldx, int64_t px, int64_t rows,
                                int64_t ncols, uint64_t *__restrict__ out, int64_t po, int64_t rows_pad,
-                               int64_t kwords) {
+                               int64_t kwords, int kw) {
     const int64_t nw = words_for(ncols);
     const uint64_t tm = tail_mask(ncols);
-    const int64_t KS = kwords >> 1, KP = (KS + 1) >> 1;  // k-stages, stage pairs
+    const int64_t KP = (kwords + 3) >> 2;  // groups of 4 words (2 int8 stages / 1 fp4 stage)
     const int64_t total = rows_pad * KP;
     for (int64_t idx = gtid(); idx < total; idx += gstride()) {
         const int64_t rb = idx / (KP * 128), rem = idx - rb * KP * 128;
@@ -340,7 +339,7 @@ __global__ void k_combos_tiled(Sched s, const uint64_t *__restrict__ X, int64_t 
                 uint64_t v = (i < s.e && r < rows && w < nw) ? X[i * px + r * ldx + w] : 0;
                 x[i][q] = (w == nw - 1) ? (v & tm) : v;
             }
-        const bool two = 2 * kp + 1 < KS;
+        const bool two = w0 + 2 < kwords;
         for (int t = 0; t < s.nprod; ++t) {
             const uint32_t sub = s.subset[t];
             uint64_t a[4] = {0, 0, 0, 0};
@@ -351,8 +350,9 @@ __global__ void k_combos_tiled(Sched s, const uint64_t *__restrict__ X, int64_t 
                 for (int q = 0; q < 4; ++q) a[q] ^= x[i][q] & sel;
             }
             uint64_t *o = out + t * po;
-            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(r, w0, kwords)) = make_ulonglong2(a[0], a[1]);
-            if (two) *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(r, w0 + 2, kwords)) = make_ulonglong2(a[2], a[3]);
+            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(r, w0, kwords, kw)) = make_ulonglong2(a[0], a[1]);
+            if (two)
+                *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(r, w0 + 2, kwords, kw)) = make_ulonglong2(a[2], a[3]);
         }
     }
 }
@@ -387,9 +387,11 @@ __device__ __forceinline__ void transpose64(uint64_t &xa, uint64_t &xb, int lane
 // parity packer emits columns in b_row_perm order).  One warp per 64x64 block.
 __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb, int64_t pb, int64_t k,
                             int64_t n, uint64_t *__restrict__ out, int64_t ldo, int64_t po, int64_t kblocks,
-                            int64_t nblocks) {
-    // one warp per (k-stage = 2 x 64 k-rows, 64-column block): two 64x64 transposes, then each
-    // lane writes whole 16-byte tile rows (both words of its stage)
+                            int64_t nblocks, int fp4) {
+    // one warp per (2 x 64 k-rows, 64-column block): two 64x64 transposes, then each lane
+    // writes 16-byte pieces of tile rows.  Input row r of a 64-block lands at bit sigma(r):
+    // int8 reverses bits inside bytes (r ^ 7), fp4 swaps bits 0 and 2 of every nibble.
+    const int kw = fp4 ? 4 : 2;
     const int lane = threadIdx.x & 31;
     const int64_t warp = gtid() >> 5;
     const int64_t nwarps = gstride() >> 5;
@@ -401,7 +403,8 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
         uint64_t a[2][kMaxE], b[2][kMaxE];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int64_t r0 = (2 * ks + h) * 64 + (lane ^ 7), r1 = r0 + 32;
+            const int sl = fp4 ? (lane ^ ((~lane & 1) << 1)) : (lane ^ 7);
+            const int64_t r0 = (2 * ks + h) * 64 + sl, r1 = r0 + 32;
 #pragma unroll
             for (int i = 0; i < kMaxE; ++i) {
                 a[h][i] = (i < s.e && nb < nw && r0 < k) ? (B[i * pb + r0 * ldb + nb] & tm) : 0;
@@ -424,8 +427,8 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
             transpose64(xa[0], xb[0], lane);
             transpose64(xa[1], xb[1], lane);
             uint64_t *o = out + t * po;
-            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(ra, 2 * ks, ldo)) = make_ulonglong2(xa[0], xa[1]);
-            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(rb, 2 * ks, ldo)) = make_ulonglong2(xb[0], xb[1]);
+            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(ra, 2 * ks, ldo, kw)) = make_ulonglong2(xa[0], xa[1]);
+            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(rb, 2 * ks, ldo, kw)) = make_ulonglong2(xb[0], xb[1]);
         }
     }
 }
@@ -518,27 +521,28 @@ cudaError_t launch_reduce(int e, uint32_t f, uint64_t *planes, int64_t rows, int
 
 cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, int64_t px, int64_t rows,
                                int64_t ncols, uint64_t *out, int64_t ldo, int64_t po, int64_t rows_pad,
-                               int64_t words_pad, bool tiled, cudaStream_t st) {
-    if (tiled) {
-        const int64_t tot = rows_pad * (((words_pad >> 1) + 1) >> 1);
+                               int64_t words_pad, int tiled_kw, cudaStream_t st) {
+    if (tiled_kw) {
+        const int64_t tot = rows_pad * ((words_pad + 3) >> 2);
         if (tot == 0) return cudaSuccess;
-        k_combos_tiled<<<grid_for(tot, 256), 256, 0, st>>>(s, X, ldx, px, rows, ncols, out, po, rows_pad, words_pad);
+        k_combos_tiled<<<grid_for(tot, 256), 256, 0, st>>>(s, X, ldx, px, rows, ncols, out, po, rows_pad, words_pad,
+                                                           tiled_kw);
         return cudaGetLastError();
     }
     int64_t total = rows_pad * words_pad;
     if (total == 0) return cudaSuccess;
     k_combos_rows<<<grid_for(total, 256), 256, 0, st>>>(s, X, ldx, px, rows, ncols, out, ldo, po, rows_pad,
-                                                        words_pad, tiled ? 1 : 0);
+                                                        words_pad);
     return cudaGetLastError();
 }
 
 cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int64_t pb, int64_t k, int64_t n,
-                             uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks,
+                             uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks, bool fp4,
                              cudaStream_t st) {
     int64_t warps = (kblocks >> 1) * nblocks;  // kblocks is even (k_pad is a multiple of 128)
     if (warps == 0) return cudaSuccess;
     int g = grid_for(warps * 32, 256);
-    k_combos_bt<<<g, 256, 0, st>>>(s, B, ldb, pb, k, n, out, ldo, po, kblocks, nblocks);
+    k_combos_bt<<<g, 256, 0, st>>>(s, B, ldb, pb, k, n, out, ldo, po, kblocks, nblocks, fp4 ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -22,10 +22,11 @@ cudaError_t launch_xor(uint64_t *x, int64_t ldx, const uint64_t *y, int64_t ldy,
 cudaError_t launch_reduce(int e, uint32_t f, uint64_t *planes, int64_t rows, int64_t nwords, int64_t ld,
                           int64_t pstride, cudaStream_t st);
 // Stage-tiled operand layout of the tensor-core kernel: a plane of rows_pad x kwords words
-// is a sequence of tiles (row block rb = r/128, k-stage ks = w/2), each 128 rows x 2 words
-// (2 KiB) contiguous, so one bulk copy moves one stage of one operand half.
-__host__ __device__ __forceinline__ int64_t tc_tile_word(int64_t r, int64_t w, int64_t kwords) {
-    return (((r >> 7) * (kwords >> 1) + (w >> 1)) * 128 + (r & 127)) * 2 + (w & 1);
+// is a sequence of tiles (row block rb = r/128, k-stage ks = w/KW), each 128 rows x KW words
+// contiguous (KW = 2: 128-bit int8 stages, 2 KiB; KW = 4: 256-bit fp4 stages, 4 KiB), so one
+// bulk copy moves one stage of one operand half.
+__host__ __device__ __forceinline__ int64_t tc_tile_word(int64_t r, int64_t w, int64_t kwords, int kw) {
+    return (((r >> 7) * (kwords / kw) + (w / kw)) * 128 + (r & 127)) * kw + (w % kw);
 }
 // Row order inside each 32-row group of B^T tiles: tile row j holds column b_row_perm(j)
 // (tc_common.cuh), i.e. column o sits at tile row 4*(o%8) + o/8.
@@ -33,11 +34,14 @@ __host__ __device__ __forceinline__ int64_t tc_b_row_inv(int64_t n) {
     const int64_t o = n & 31;
     return (n & ~int64_t(31)) | (4 * (o & 7) + (o >> 3));
 }
+// tiled_kw: 0 = row-major rows of ldo words; 2 / 4 = stage-tiled (tc_tile_word) with KW words
 cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, int64_t px, int64_t rows,
                                int64_t ncols, uint64_t *out, int64_t ldo, int64_t po, int64_t rows_pad,
-                               int64_t words_pad, bool tiled, cudaStream_t st);
+                               int64_t words_pad, int tiled_kw, cudaStream_t st);
+// B^T combinations, stage-tiled; fp4: KW = 4 and bits 0/2 of every nibble swapped, else
+// KW = 2 and bits reversed inside every byte
 cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int64_t pb, int64_t k, int64_t n,
-                             uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks,
+                             uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks, bool fp4,
                              cudaStream_t st);
 
 // Tensor-core product.  Operands: Ac [nprod] x (m_pad x k_pad bits) natural bit order,
@@ -55,8 +59,10 @@ struct TcArgs {
 };
 constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 128;  // tile rows, tile cols, k-bits per stage
 // CTA-pair tcgen05 kernel (product_tc2.cu): m_pad multiple of 256, n_pad of 256, k_pad of
-// 128; Ac / Bt in the stage-tiled layout (tc_tile_word), Bt rows in tc_b_row_inv order.
-cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, cudaStream_t st);
+// 128 (int8) / 256 (fp4); Ac / Bt stage-tiled (tc_tile_word, KW 2 / 4), Bt rows in
+// tc_b_row_inv order.
+constexpr int kTcBKFp4 = 256;
+cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, bool fp4, cudaStream_t st);
 
 // INT-pipe M4RM product (product_m4rm.cu).  Operands: Ac as above, Bc [nprod][k_pad][n_pad/64].
 struct M4rmArgs {

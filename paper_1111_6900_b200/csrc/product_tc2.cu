@@ -1,16 +1,42 @@
 // product_tc2.cu — the fused Karatsuba product kernel on CTA PAIRS (tcgen05 cta_group::2).
 //
-// Same contract and arithmetic as product_tc.cu (reference: karatsuba_mul poly_mul.py:245-259,
-// _kara 166-220, mat_gf2.mul mat_gf2.py:425-455, reduce_mod_f poly_mul.py:223-242), but each
-// cluster of 2 CTAs owns a 256 x 256 tile of C and issues M=256 N=256 K=32 MMAs:
-//   CTA r (r = cluster rank) expands A rows [128r, 128r+128) and B^T rows [128r, 128r+128)
-//   of the tile, so per SM the producers write 32 KiB of 0/1 bytes per 128-bit k-stage
-//   instead of 48 KiB and the tensor core reads 32 KiB instead of 48 KiB — shared-memory
-//   bandwidth, not the tensor pipe, bounds the 1-CTA kernel (profiles/r01).
-//   The leader (rank 0) issues the MMAs; accumulators land in each CTA's own TMEM (its 128
-//   rows x 256 columns, double buffered), so the epilogue is unchanged per CTA.
+// Reference: karatsuba_mul (poly_mul.py:245-259) -> _kara (166-220) -> mat_gf2.mul
+// (mat_gf2.py:425-455) per product, then reduce_mod_f (poly_mul.py:223-242) and, for addmul,
+// xor_window (mat_gf2.py:270-277).  Here C_j (^)= XOR_{t : M[j,t]} A'_t . B'_t with
+// M = R_f . Gamma (the schedule, capi.cu), evaluated tile by tile; no product plane is ever
+// materialised.  Each cluster of 2 CTAs owns a 256 x 256 tile of C and issues M=256 N=256
+// MMAs: CTA r (cluster rank) expands A rows [128r, 128r+128) and B^T rows [128r, 128r+128)
+// of the tile; the leader issues the MMAs; accumulators land in each CTA's own TMEM.
+//
+// Two tensor-core forms of the same GF(2) product (template parameter FP4):
+//
+//  int8 (kind::i8, K=32 per MMA, 128 k-bits per stage).  Bits -> bytes with ONE AND per
+//    32-bit output word: A byte = a*2^i (w & 0x01010101<<i), B^T (bits reversed inside each
+//    byte) byte = b*2^(7-i) (w & 0x80808080>>i); both hold k-bit 32q+8j+i in the same slot, so
+//    every byte product is a*b*2^7 and the s32 accumulator is 128*count (mod 2^32): the GF(2)
+//    result is bit 7.  Two TMEM accumulators (2 x 256 columns) double-buffer the epilogue.
+//
+//  fp4 (kind::mxf4 block-scaled e2m1, K=64 per MMA, 256 k-bits per stage, all scale factors
+//    1.0 = E8M0 0x7F in TMEM).  Bits -> nibbles: A nibble i of k-bit 4j+i holds 0.5, 1, 2, 1
+//    (w & 0x11111111<<i for i<3, (w>>2) & 0x22222222 for i=3); B^T is stored with bits 0 and 2
+//    of every nibble swapped so its nibbles hold 2, 1, 0.5, 1 — every product is exactly 1.0.
+//    fp32 accumulation of 0/1 products is exact (probe: tools/fp4_probe.py, to 2^24); the
+//    accumulator starts at 65536.0f, so for counts < 2^16 the pattern is 0x47800000 + (count<<7)
+//    and the parity is again bit 7.  K is processed in chunks of <= 32768 bits (count < 2^16);
+//    one 256-column accumulator (the other 256 TMEM columns hold the scale factors); the
+//    epilogue re-initialises it to 65536.0f after each read-out.  2x the int8 rate, half the
+//    expanded bytes per k-bit.
+//
+// Warp roles (448 threads per CTA, 1 CTA / SM):
+//   warps 0-3   expanders: expand this CTA's A and B^T rows of each stage into the UMMA
+//               K-major SWIZZLE_128B layout, fence.proxy.async, arrive on the leader's full[s]
+//   warps 4-11  epilogue: tcgen05.ld pack::16b, parity via sign-replicating PRMT, fold into
+//               E register-resident output planes (the columns of M), store the tile once
+//   warp 12     MMA issuer (leader CTA, one thread)
+//   warp 13     loader: cp.async.bulk of the stage-tiled bit tiles into a ring (mbarrier tx)
 // Synchronisation across the pair:
-//   full[s]   (leader)   <- 4 producer warps x 2 CTAs (remote arrive after fence.proxy.async)
+//   full[s]   (leader)   <- 4 expander warps x 2 CTAs (relaxed remote arrive after the fence;
+//                           release.cluster would compile to MEMBAR.ALL.GPU)
 //   empty[s]  (each CTA) <- tcgen05.commit multicast to both CTAs
 //   tfull[b]  (each CTA) <- tcgen05.commit multicast to both CTAs
 //   tempty[b] (leader)   <- 8 epilogue warps x 2 CTAs (remote arrive)
@@ -22,49 +48,41 @@ namespace gf2e {
 namespace {
 using namespace tc;
 
-constexpr int BM = 128;    // rows per CTA (tile = 2 x BM)
-constexpr int BNH = 128;   // B^T rows per CTA (tile N = 2 x BNH = 256)
+constexpr int BM = 128;   // rows per CTA (tile = 2 x BM)
+constexpr int BNH = 128;  // B^T rows per CTA (tile N = 2 x BNH)
 constexpr int BN = 256;
-constexpr int BK = kTcBK;  // 128 k-bits per stage
-constexpr int S = 5;       // expanded operand stages
-constexpr int D = 8;       // bit-tile staging depth
-#ifndef GF2E_NPW
-#define GF2E_NPW 4
-#endif
-#ifndef GF2E_GROUP_M
-#define GF2E_GROUP_M 8
-#endif
-#ifndef GF2E_EPI_X16
-#define GF2E_EPI_X16 2  // 2: pack::16b + sign-PRMT parity, 1: two x16 loads, 0: one x32 load
-#endif
-constexpr int NPW = GF2E_NPW;  // expander warps (8: 0-3 expand A rows, 4-7 B^T rows; 4: both)
-constexpr int NEW = 8;         // epilogue warps
-constexpr int GROUP_M = GF2E_GROUP_M;  // tile rasterisation: row-tiles per column sweep (L2 reuse)
-#ifndef GF2E_EXP_HIGH
-#define GF2E_EXP_HIGH 0
-#endif
-// Warp roles.  The issue arbiter favours higher warp ids, and the expanders are the critical
-// role, so (GF2E_EXP_HIGH) they take the highest ids: epilogue 0-7, MMA 8, loader 9,
-// expanders 10-13 (one per SMSP either way: warp id % 4 covers 0..3).
-constexpr int EPI_W0 = GF2E_EXP_HIGH ? 0 : NPW;
-constexpr int MMA_WARP = GF2E_EXP_HIGH ? NEW : NPW + NEW;
+constexpr int S = 5;        // expanded operand stages (32 KiB each: one 128-byte swizzle row per operand row)
+constexpr int NPW = 4;      // expander warps
+constexpr int NEW = 8;      // epilogue warps
+constexpr int GROUP_M = 8;  // tile rasterisation: row-tiles per column sweep (L2 reuse)
+constexpr int EPI_W0 = NPW;
+constexpr int MMA_WARP = NPW + NEW;
 constexpr int LOAD_WARP = MMA_WARP + 1;
-constexpr int EXP_W0 = GF2E_EXP_HIGH ? NEW + 2 : 0;
 constexpr int NTHREADS = (NPW + NEW + 2) * 32;
-constexpr int A_BYTES = BM * BK;   // 16 KiB
-constexpr int B_BYTES = BNH * BK;  // 16 KiB
+constexpr int A_BYTES = BM * 128;
+constexpr int B_BYTES = BNH * 128;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int BITS_A = BM * (BK / 8);
-constexpr int BITS_BYTES = (BM + BNH) * (BK / 8);  // 4 KiB
 constexpr int TMEM_COLS = 512;
-constexpr uint32_t IDESC = idesc_i8(2 * BM, BN);
+constexpr uint32_t FP4_ACC_INIT = 0x47800000u;  // 65536.0f
+constexpr int FP4_CHUNK_STAGES = 32768 / 256;   // k-bits per accumulation chunk / bits per stage
+
+template <bool FP4>
+struct Cfg {
+    static constexpr int BK = FP4 ? 256 : 128;  // k-bits per stage (= one 128-byte row of operand)
+    static constexpr int KW = BK / 64;          // bit words per tile row per stage
+    static constexpr int D = FP4 ? 6 : 8;       // bit-tile ring depth
+    static constexpr int BITS_A = BM * (BK / 8);
+    static constexpr int BITS_BYTES = (BM + BNH) * (BK / 8);
+    static constexpr int NBUF = FP4 ? 1 : 2;    // TMEM accumulators
+    static constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + 512 + 1024;
+};
 
 struct __align__(8) Bars {
-    uint64_t full[S], empty[S], tfull[2], tempty[2], bfull[D], bempty[D];
+    uint64_t full[S], empty[S], tfull[2], tempty[2], bfull[8], bempty[8];
     uint32_t tmem_base;
     uint16_t outmask[kMaxProducts];
 };
-constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + (int)sizeof(Bars) + 1024;
+static_assert(sizeof(Bars) <= 512, "barrier block");
 
 // tile index -> (row-tile, column-tile): sweep GROUP_M row-tiles down each column before
 // moving right, so the ~74 CTA pairs in flight share a few A row-blocks and B^T column-blocks
@@ -79,14 +97,53 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t tiles_m, int64
     tn = r / gsize;
 }
 
-template <int E>
+// fp4 expansion of one 256-bit row of a stage into its 128-byte swizzle row: u32 word q of
+// the row gives chunk q (four u32 = 32 nibbles; nibble j of word i <-> k-bit 32q + 4j + i)
+template <bool kB>
+__device__ __forceinline__ void expand_row_fp4(uint8_t *tile, int r, uint4 lo, uint4 hi) {
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t x = w[q];
+        const uint32_t o3 = (x >> 2) & 0x22222222u;
+        const uint4 o = kB ? make_uint4(x & 0x44444444u, x & 0x22222222u, x & 0x11111111u, o3)
+                           : make_uint4(x & 0x11111111u, x & 0x22222222u, x & 0x44444444u, o3);
+        *reinterpret_cast<uint4 *>(tile + swz(r, q)) = o;
+    }
+}
+
+__device__ __forceinline__ void tmem_st32_const(uint32_t taddr, uint32_t v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+            taddr),
+        "r"(v)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// block-scaled instruction descriptor: e2m1 x e2m1, E8M0 scales, K-major, K=64
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+    return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma2_mxf4(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t sfa,
+                                          uint32_t sfb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.eq.u32 p, 1, 1;\n\t"  // always accumulate: D starts at 65536.0f
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+
+template <int E, bool FP4>
 __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, const TcArgs a) {
+    using C = Cfg<FP4>;
     extern __shared__ uint8_t smem_raw[];
     // keep the shared state space visible to the compiler (STS/LDS, not generic ST/LD)
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *stages = smem;
     uint8_t *bits = smem + S * STAGE_BYTES;
-    Bars *bars = reinterpret_cast<Bars *>(bits + D * BITS_BYTES);
+    Bars *bars = reinterpret_cast<Bars *>(bits + C::D * C::BITS_BYTES);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -95,9 +152,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     const int64_t tiles_m = a.m_pad / (2 * BM);
     const int64_t ntiles = tiles_m * tiles_n;
     const int64_t my_tiles = ntiles > cluster ? (ntiles - cluster + nclusters - 1) / nclusters : 0;
-    const int nks = (int)(a.kwords / (BK / 64));
-    const int64_t per_tile = (int64_t)s.nprod * nks;
-    const int64_t total = my_tiles * per_tile;
+    const int nks = (int)(a.kwords / C::KW);
+    // accumulation chunks per product: int8 wraps harmlessly mod 2^32; fp4 keeps count < 2^16
+    const int chunk = FP4 ? FP4_CHUNK_STAGES : nks;
+    const int nchunks = (nks + chunk - 1) / chunk;
+    const int64_t total = my_tiles * (int64_t)s.nprod * nks;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -108,7 +167,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             mbar_init(&bars->tfull[i], 1);
             mbar_init(&bars->tempty[i], 2 * NEW);
         }
-        for (int i = 0; i < D; ++i) {
+        for (int i = 0; i < C::D; ++i) {
             mbar_init(&bars->bfull[i], 1);
             mbar_init(&bars->bempty[i], NPW);
         }
@@ -118,34 +177,46 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     if (warp == MMA_WARP) tmem_alloc2(&bars->tmem_base, TMEM_COLS);
     tc_fence_before();
     __syncthreads();
-    cluster_sync();  // barriers of both CTAs initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
+    if (FP4 && warp >= EPI_W0 && warp < EPI_W0 + 4) {
+        // scale factors (columns 256..511: every byte E8M0 1.0) and the first accumulator init
+        const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+        for (int c = 256; c < 512; c += 32) tmem_st32_const(tmem + lb + c, 0x7F7F7F7Fu);
+        for (int c = 0; c < 256; c += 32) tmem_st32_const(tmem + lb + c, FP4_ACC_INIT);
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // barriers and TMEM of both CTAs ready before any remote arrive / MMA
+    tc_fence_after();
 
-    if (warp >= EXP_W0 && warp < EXP_W0 + NPW) {
+    if (warp < NPW) {
         // ===================== expanders (both CTAs) =====================
         // bit tiles arrive by bulk copy (loader warp); these warps keep no global loads in
         // flight, so the per-stage fence.proxy.async (MEMBAR.ALL.CTA) only drains their STS.
-        // Two warps per SMSP: one warp's fence / LDS latency overlaps another's expansion.
-        const bool isB = NPW == 8 && warp - EXP_W0 >= 4;
-        const int p = (threadIdx.x - EXP_W0 * 32) & 127;  // row of this CTA's A half (isB: B^T half)
-        const uint32_t src_off = (isB ? BITS_A : 0) + p * 16;
-        const uint32_t dst_off = isB ? A_BYTES : 0;
+        const int p = threadIdx.x;  // A row and B^T row of this CTA's half
         const uint32_t full_leader = mapa(smem_u32(&bars->full[0]), 0);
         int slot = 0, st = 0;
         uint32_t bph = 0, phase = 0;
         for (int64_t it = 0; it < total; ++it) {
             mbar_wait(&bars->bfull[slot], bph);
-            const uint4 w = *reinterpret_cast<const uint4 *>(bits + slot * BITS_BYTES + src_off);
-            uint4 wb2;
-            if (NPW == 4) wb2 = *reinterpret_cast<const uint4 *>(bits + slot * BITS_BYTES + BITS_A + p * 16);
+            const uint8_t *bs = bits + slot * C::BITS_BYTES;
             mbar_wait(&bars->empty[st], phase ^ 1);
-            uint8_t *tile = stages + st * STAGE_BYTES + dst_off;
-            if (isB)
-                expand_row<true>(tile, p, w);
-            else
-                expand_row<false>(tile, p, w);
-            if (NPW == 4) expand_row<true>(stages + st * STAGE_BYTES + A_BYTES, p, wb2);
+            uint8_t *sa = stages + st * STAGE_BYTES;
+            if constexpr (FP4) {
+                const uint4 a0 = *reinterpret_cast<const uint4 *>(bs + p * 32);
+                const uint4 a1 = *reinterpret_cast<const uint4 *>(bs + p * 32 + 16);
+                const uint4 b0 = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + p * 32);
+                const uint4 b1 = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + p * 32 + 16);
+                expand_row_fp4<false>(sa, p, a0, a1);
+                expand_row_fp4<true>(sa + A_BYTES, p, b0, b1);
+            } else {
+                const uint4 wa = *reinterpret_cast<const uint4 *>(bs + p * 16);
+                const uint4 wb = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + p * 16);
+                expand_row<false>(sa, p, wa);
+                expand_row<true>(sa + A_BYTES, p, wb);
+            }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -154,7 +225,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                 // loader may overwrite the slot: no read-before-overwrite race on bits
                 mbar_arrive(&bars->bempty[slot]);
             }
-            if (++slot == D) {
+            if (++slot == C::D) {
                 slot = 0;
                 bph ^= 1;
             }
@@ -166,7 +237,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     } else if (warp == LOAD_WARP) {
         // ===================== bit-tile loader (both CTAs, one thread) =====================
         if (lane == 0) {
-            const int64_t KS = a.kwords >> 1;  // k-stages per row block
+            const int64_t KS = a.kwords / C::KW;  // k-stages per row block
+            const int64_t tile_words = 128 * C::KW;
             const uint32_t bits_s = smem_u32(bits);
             int slot = 0;
             uint32_t bph = 0;
@@ -177,15 +249,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                 const int64_t rbA = tm * 2 + rank;  // 128-row block of A
                 const int64_t rbB = tn * 2 + rank;  // 128-row block of B^T
                 for (int t = 0; t < s.nprod; ++t) {
-                    const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * 256;
-                    const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * 256;
+                    const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * tile_words;
+                    const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * tile_words;
                     for (int ks = 0; ks < nks; ++ks) {
                         mbar_wait(&bars->bempty[slot], bph ^ 1);
-                        mbar_arrive_expect_tx(&bars->bfull[slot], BITS_BYTES);
-                        const uint32_t dst = bits_s + (uint32_t)(slot * BITS_BYTES);
-                        bulk_g2s(dst, Ab + ks * 256, BITS_A, &bars->bfull[slot]);
-                        bulk_g2s(dst + BITS_A, Bb + ks * 256, BITS_BYTES - BITS_A, &bars->bfull[slot]);
-                        if (++slot == D) {
+                        mbar_arrive_expect_tx(&bars->bfull[slot], C::BITS_BYTES);
+                        const uint32_t dst = bits_s + (uint32_t)(slot * C::BITS_BYTES);
+                        bulk_g2s(dst, Ab + ks * tile_words, C::BITS_A, &bars->bfull[slot]);
+                        bulk_g2s(dst + C::BITS_A, Bb + ks * tile_words, C::BITS_BYTES - C::BITS_A,
+                                 &bars->bfull[slot]);
+                        if (++slot == C::D) {
                             slot = 0;
                             bph ^= 1;
                         }
@@ -194,7 +267,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             }
         }
         __syncwarp();
-    } else if (warp >= EPI_W0 && warp < EPI_W0 + NEW) {
+    } else if (warp < MMA_WARP) {
         // ===================== epilogue (both CTAs) =====================
         const int ew = warp - EPI_W0;
         const int q = warp & 3;  // TMEM lane quarter (hardware: warp id % 4)
@@ -202,7 +275,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
         const int row_local = (int)rank * BM + q * 32 + lane;
         const int64_t nw = words_for(a.n);
         const uint32_t tempty_leader = mapa(smem_u32(&bars->tempty[0]), 0);
-        int64_t gp = 0;
+        int64_t gp = 0;  // accumulator hand-offs seen (products x chunks)
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             const int64_t tile = cluster + ti * nclusters;
             int64_t tm, tn;
@@ -213,39 +286,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             for (int j = 0; j < E; ++j)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) acc[j][c] = 0;
-            for (int t = 0; t < s.nprod; ++t, ++gp) {
-                const int buf = (int)(gp & 1);
-                mbar_wait(&bars->tfull[buf], (uint32_t)((gp >> 1) & 1));
-                tc_fence_after();
+            for (int t = 0; t < s.nprod; ++t) {
                 const uint32_t mask = bars->outmask[t];
+                for (int ch = 0; ch < nchunks; ++ch, ++gp) {
+                    const int buf = (int)(gp % C::NBUF);
+                    mbar_wait(&bars->tfull[buf], (uint32_t)((gp / C::NBUF) & 1));
+                    tc_fence_after();
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + c * 32);
-#if GF2E_EPI_X16 == 2
-                    uint32_t v[16];
-                    tmem_ld32_pack16(ta, v);
-                    tmem_wait_ld();
-                    const uint32_t pw = parity_word_packed(v);
-#elif GF2E_EPI_X16
-                    uint32_t v[16];
-                    tmem_ld16(ta, v);
-                    tmem_wait_ld();
-                    uint32_t pw = parity_half(v, 0);
-                    tmem_ld16(ta + 16, v);
-                    tmem_wait_ld();
-                    pw |= parity_half(v, 4);
-#else
-                    uint32_t v[32];
-                    tmem_ld32(ta, v);
-                    tmem_wait_ld();
-                    const uint32_t pw = parity_word(v);
-#endif
+                    for (int c = 0; c < 4; ++c) {
+                        const uint32_t ta =
+                            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + c * 32);
+                        uint32_t v[16];
+                        tmem_ld32_pack16(ta, v);
+                        tmem_wait_ld();
+                        const uint32_t pw = parity_word_packed(v);
 #pragma unroll
-                    for (int j = 0; j < E; ++j) acc[j][c] ^= pw & (0u - ((mask >> j) & 1u));
+                        for (int j = 0; j < E; ++j) acc[j][c] ^= pw & (0u - ((mask >> j) & 1u));
+                        if (FP4) tmem_st32_const(ta, FP4_ACC_INIT);
+                    }
+                    if (FP4) tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
             }
             const int64_t row = m0 + row_local;
             if (row < a.m) {
@@ -288,28 +351,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             int st = 0;
             uint32_t phase = 0;
             const uint32_t st0 = smem_u32(stages);
+            const uint32_t idesc = FP4 ? idesc_mxf4(2 * BM, BN) : idesc_i8(2 * BM, BN);
             for (int64_t ti = 0; ti < my_tiles; ++ti) {
-                for (int t = 0; t < s.nprod; ++t, ++gp) {
-                    const int buf = (int)(gp & 1);
-                    mbar_wait(&bars->tempty[buf], (uint32_t)((gp >> 1) & 1) ^ 1);
-                    tc_fence_after();
-                    const uint32_t dt = tmem + (uint32_t)(buf * BN);
-                    for (int ks = 0; ks < nks; ++ks) {
-                        mbar_wait(&bars->full[st], phase);
+                for (int t = 0; t < s.nprod; ++t) {
+                    for (int ch = 0; ch < nchunks; ++ch, ++gp) {
+                        const int buf = (int)(gp % C::NBUF);
+                        mbar_wait(&bars->tempty[buf], (uint32_t)((gp / C::NBUF) & 1) ^ 1);
                         tc_fence_after();
-                        const uint32_t sa = st0 + (uint32_t)(st * STAGE_BYTES);
-                        const uint32_t sb = sa + A_BYTES;
+                        const uint32_t dt = tmem + (uint32_t)(buf * BN);
+                        const int ks1 = (ch + 1) * chunk < nks ? (ch + 1) * chunk : nks;
+                        for (int ks = ch * chunk; ks < ks1; ++ks) {
+                            mbar_wait(&bars->full[st], phase);
+                            tc_fence_after();
+                            const uint32_t sa = st0 + (uint32_t)(st * STAGE_BYTES);
+                            const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-                        for (int kk = 0; kk < BK / 32; ++kk)
-                            mma2_i8(dt, umma_desc_sw128(sa + kk * 32), umma_desc_sw128(sb + kk * 32), IDESC,
-                                    (ks | kk) != 0);
-                        mma2_commit_both(&bars->empty[st]);
-                        if (++st == S) {
-                            st = 0;
-                            phase ^= 1;
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const uint64_t ad = umma_desc_sw128(sa + kk * 32), bd = umma_desc_sw128(sb + kk * 32);
+                                if constexpr (FP4)
+                                    mma2_mxf4(dt, ad, bd, idesc, tmem + 256, tmem + 384);
+                                else
+                                    mma2_i8(dt, ad, bd, idesc, (ks != ch * chunk) | kk);
+                            }
+                            mma2_commit_both(&bars->empty[st]);
+                            if (++st == S) {
+                                st = 0;
+                                phase ^= 1;
+                            }
                         }
+                        mma2_commit_both(&bars->tfull[buf]);
                     }
-                    mma2_commit_both(&bars->tfull[buf]);
                 }
             }
         }
@@ -327,9 +398,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
 
 int g_num_sms2 = 0;
 
-template <int E>
+template <int E, bool FP4>
 cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
-    cudaError_t err = cudaFuncSetAttribute(k_product_tc2<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    const int smem = Cfg<FP4>::SMEM_BYTES;
+    cudaError_t err = cudaFuncSetAttribute(k_product_tc2<E, FP4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
     const int64_t tiles = (a.m_pad / (2 * BM)) * (a.n_pad / BN);
     if (tiles == 0) return cudaSuccess;
@@ -348,29 +420,34 @@ cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3((unsigned)(2 * clusters));
     cfg.blockDim = dim3(NTHREADS);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_product_tc2<E>, s, a);
+    return cudaLaunchKernelEx(&cfg, k_product_tc2<E, FP4>, s, a);
+}
+
+template <bool FP4>
+cudaError_t launch_any(const Sched &s, const TcArgs &a, cudaStream_t st) {
+    switch (s.nout) {
+        case 1: return launch_e<1, FP4>(s, a, st);
+        case 2: return launch_e<2, FP4>(s, a, st);
+        case 3: return launch_e<3, FP4>(s, a, st);
+        case 4: return launch_e<4, FP4>(s, a, st);
+        case 5: return launch_e<5, FP4>(s, a, st);
+        case 6: return launch_e<6, FP4>(s, a, st);
+        case 7: return launch_e<7, FP4>(s, a, st);
+        case 8: return launch_e<8, FP4>(s, a, st);
+        case 9: return launch_e<9, FP4>(s, a, st);
+        case 10: return launch_e<10, FP4>(s, a, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace
 
-cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, cudaStream_t st) {
-    switch (s.nout) {
-        case 1: return launch_e<1>(s, a, st);
-        case 2: return launch_e<2>(s, a, st);
-        case 3: return launch_e<3>(s, a, st);
-        case 4: return launch_e<4>(s, a, st);
-        case 5: return launch_e<5>(s, a, st);
-        case 6: return launch_e<6>(s, a, st);
-        case 7: return launch_e<7>(s, a, st);
-        case 8: return launch_e<8>(s, a, st);
-        case 9: return launch_e<9>(s, a, st);
-        case 10: return launch_e<10>(s, a, st);
-        default: return cudaErrorInvalidValue;
-    }
+cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, bool fp4, cudaStream_t st) {
+    return fp4 ? launch_any<true>(s, a, st) : launch_any<false>(s, a, st);
 }
 
 }  // namespace gf2e

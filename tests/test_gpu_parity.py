@@ -8,7 +8,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-BACKENDS = ["tc", "m4rm"]
+BACKENDS = ["tc_i8", "tc_fp4", "m4rm"]
 
 
 @pytest.fixture(scope="module")
@@ -242,8 +242,11 @@ def test_native_code_used(g):
     ctx = g.field_new(8)
     A = g.SlicedMatrix.random(ctx, 256, 256, 1)
     g.karatsuba_mul(A, A)
-    assert g._lib.last_product_kernel() == "k_product_tc2"
+    assert g._lib.last_product_kernel() == "k_product_tc2<i8>"  # k < 2048: int8 form
     assert g._lib.last_launch_count() == 3  # combos(A), combos(B^T), fused product
+    B = g.SlicedMatrix.random(ctx, 4096, 256, 2)
+    g.karatsuba_mul(g.SlicedMatrix.random(ctx, 256, 4096, 1), B)
+    assert g._lib.last_product_kernel() == "k_product_tc2<fp4>"
 
 
 @pytest.mark.parametrize("acc", [False, True])
