@@ -223,6 +223,7 @@ def run_ours(args):
         dist.barrier()
     clocks = sampler.stop()
     prod_ms, prod_launches = _lib.profile_read()
+    kernel_name = _lib.last_product_kernel()
     _lib.profile_enable(False)
     ms = ev0.elapsed_time(ev1) / args.steps
     t = torch.tensor([ms, prod_ms / max(prod_launches, 1)], dtype=torch.float64, device=dev)
@@ -277,10 +278,18 @@ def run_ours(args):
         return 0
 
     pk, pk_kind = peaks()
-    # Denominator: the dense kind::i8 tcgen05 rate measured on THIS GPU right now by a pure-MMA
-    # loop on every SM (gf2e_mma_peak; best of 2 launches).  MEASURED_PEAKS.json holds only bf16,
-    # whose cuBLAS figure x2 understates the int8 pipe, so it is reported alongside, not used.
-    int8_peak = max(_lib.mma_peak(2, 20000)[0], _lib.mma_peak(1, 20000)[0])
+    # Denominator: the dense tensor rate of the form the kernel ran (kind::i8 or kind::mxf4),
+    # measured on THIS GPU right now by a pure-MMA loop on every SM.  MEASURED_PEAKS.json holds
+    # only bf16 (its cuBLAS figure x2 understates the int8 pipe), reported alongside.
+    fp4_form = "fp4" in kernel_name
+    if fp4_form:
+        tc_peak = max(_lib.mma_peak_fp4(20000), _lib.mma_peak_fp4(20000))
+        peak_basis = ("measured live: pure tcgen05.mma kind::mxf4 (e2m1, scale 1.0) loop on all SMs; "
+                      f"for reference 4 x {pk_kind} cuBLAS bf16 = {4 * pk['bf16_tflops']:.1f}")
+    else:
+        tc_peak = max(_lib.mma_peak(2, 20000)[0], _lib.mma_peak(1, 20000)[0])
+        peak_basis = ("measured live: pure tcgen05.mma kind::i8 loop on all SMs (gf2e_mma_peak); "
+                      f"for reference 2 x {pk_kind} cuBLAS bf16 = {2 * pk['bf16_tflops']:.1f}")
     achieved = ops_rank / (prod_ms_max * 1e-3) / 1e12  # GF(2) bit-ops == int8 tensor ops (1 MAC = 2 ops)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -292,18 +301,17 @@ def run_ours(args):
     line = {
         "metric": "effective GF(2) Tbit-op/s (K(e)*2mkn / time)", "value": round(value, 4), "unit": "Tbit-op/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
-        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8 (0/1 bytes on tcgen05 kind::i8, s32 acc)",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "e2m1 0/1 (kind::mxf4, exact fp32 acc)" if fp4_form else "u8 0/1 (kind::i8, s32 acc)",
         "data": "synthetic (reference splitmix64 generator, seeds A=1 B=2 C0=3)",
         "config": {"workload": name, "e": e, "f": hex(ctx.f), "m_per_gpu": m, "k": k, "n": n,
                    "gf2_products": K, "backend": backend or "tc", "parallelism": f"C row-blocks x{world}",
                    "l2": "inputs larger than L2 (A planes + combos >> 126 MB)"},
         "time_s": round(ms_max / 1e3, 6),
         "gpu_launches": launches,
-        "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(int8_peak, 1),
-                     "unit": "TFLOP/s", "frac": round(achieved / int8_peak, 4), "traffic": traffic,
-                     "kernel": _lib.last_product_kernel(), "kernel_ms": round(prod_ms_max, 4),
-                     "peak_basis": ("measured live: pure tcgen05.mma kind::i8 loop on all SMs (gf2e_mma_peak); "
-                                    f"for reference 2 x {pk_kind} cuBLAS bf16 = {2 * pk['bf16_tflops']:.1f}"),
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(tc_peak, 1),
+                     "unit": "TFLOP/s", "frac": round(achieved / tc_peak, 4), "traffic": traffic,
+                     "kernel": kernel_name, "kernel_ms": round(prod_ms_max, 4),
+                     "peak_basis": peak_basis,
                      "ops_per_launch": ops_rank},
         "clocks": clocks,
     }

@@ -125,5 +125,19 @@ def mma_peak(cta_group: int = 1, iters: int = 20000) -> tuple[float, float]:
     return tops.value, ms.value
 
 
+def mma_peak_fp4(iters: int = 20000) -> float:
+    """Measured dense kind::mxf4 (block-scaled e2m1) tensor rate in TOPS: pure MMA loop on all
+    SMs (gf2e_dev_fp4_probe on zero operands)."""
+    import torch
+
+    a = torch.zeros(128 * 128, dtype=torch.uint8, device="cuda")
+    b = torch.zeros(256 * 128, dtype=torch.uint8, device="cuda")
+    out = torch.empty(128 * 256, dtype=torch.int32, device="cuda")
+    tops = ctypes.c_double()
+    check(load().gf2e_dev_fp4_probe(iters, 0, a.data_ptr(), b.data_ptr(), out.data_ptr(), ctypes.byref(tops),
+                                    torch.cuda.current_stream().cuda_stream), "gf2e_dev_fp4_probe")
+    return tops.value
+
+
 def last_product_kernel() -> str:
     return load().gf2e_last_product_kernel().decode()
