@@ -63,6 +63,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Poll with a sleep between probes.  For warps that wait long (epilogue, bulk loader, and
+// expanders ahead of the tensor core): a spinning try_wait is a shared-memory request, and
+// those polls compete with the expanders' stores and the tensor core's operand reads
+// (measured: 38.0 -> 35.5 ms on the e=8 16384^3 product).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns) {
+    if (ns == 0) {
+        mbar_wait(bar, parity);
+        return;
+    }
+    while (!mbar_test(bar, parity)) __nanosleep(ns);
+}
 // ---- async copies ---------------------------------------------------------------------
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");

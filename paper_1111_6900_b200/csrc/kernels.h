@@ -25,8 +25,19 @@ cudaError_t launch_reduce(int e, uint32_t f, uint64_t *planes, int64_t rows, int
 // is a sequence of tiles (row block rb = r/128, k-stage ks = w/KW), each 128 rows x KW words
 // contiguous (KW = 2: 128-bit int8 stages, 2 KiB; KW = 4: 256-bit fp4 stages, 4 KiB), so one
 // bulk copy moves one stage of one operand half.
+// Inside one 128-row x kw-word stage tile the words are stored as kw/2 slabs of [128 rows][2
+// words], so the expander's per-row 16-byte shared-memory reads are consecutive across a warp
+// (a [row][kw] layout makes the kw = 4 reads two-way bank-conflicted).
 __host__ __device__ __forceinline__ int64_t tc_tile_word(int64_t r, int64_t w, int64_t kwords, int kw) {
+#ifndef GF2E_TILE_SLAB
+#define GF2E_TILE_SLAB 1
+#endif
+#if GF2E_TILE_SLAB
+    const int64_t wk = w % kw;
+    return (((r >> 7) * (kwords / kw) + (w / kw)) * 128) * kw + (wk >> 1) * 256 + (r & 127) * 2 + (wk & 1);
+#else
     return (((r >> 7) * (kwords / kw) + (w / kw)) * 128 + (r & 127)) * kw + (w % kw);
+#endif
 }
 // Row order inside each 32-row group of B^T tiles: tile row j holds column b_row_perm(j)
 // (tc_common.cuh), i.e. column o sits at tile row 4*(o%8) + o/8.

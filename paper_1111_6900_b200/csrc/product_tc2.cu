@@ -51,7 +51,12 @@ using namespace tc;
 constexpr int BM = 128;   // rows per CTA (tile = 2 x BM)
 constexpr int BNH = 128;  // B^T rows per CTA (tile N = 2 x BNH)
 constexpr int BN = 256;
-constexpr int S = 5;        // expanded operand stages (32 KiB each: one 128-byte swizzle row per operand row)
+#ifndef GF2E_FP4_S
+#define GF2E_FP4_S 5
+#endif
+constexpr int SMAX = 6;      // expanded operand stages (32 KiB each: one 128-byte swizzle row per operand row)
+constexpr uint32_t EXP_SLEEP_NS = 64;    // expanders waiting for a free operand stage
+constexpr uint32_t IDLE_SLEEP_NS = 500;  // epilogue / bulk loader (long k only, see below)
 constexpr int NPW = 4;      // expander warps
 constexpr int NEW = 8;      // epilogue warps
 constexpr int GROUP_M = 8;  // tile rasterisation: row-tiles per column sweep (L2 reuse)
@@ -70,15 +75,17 @@ template <bool FP4>
 struct Cfg {
     static constexpr int BK = FP4 ? 256 : 128;  // k-bits per stage (= one 128-byte row of operand)
     static constexpr int KW = BK / 64;          // bit words per tile row per stage
-    static constexpr int D = FP4 ? 6 : 8;       // bit-tile ring depth
+    static constexpr int S = FP4 ? GF2E_FP4_S : 5;  // expanded operand stages
+    static constexpr int D = FP4 ? (S == 6 ? 4 : 6) : 8;  // bit-tile ring depth
     static constexpr int BITS_A = BM * (BK / 8);
     static constexpr int BITS_BYTES = (BM + BNH) * (BK / 8);
     static constexpr int NBUF = FP4 ? 1 : 2;    // TMEM accumulators
     static constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + 512 + 1024;
+    static_assert(SMEM_BYTES <= 232448, "shared memory");
 };
 
 struct __align__(8) Bars {
-    uint64_t full[S], empty[S], tfull[2], tempty[2], bfull[8], bempty[8];
+    uint64_t full[SMAX], empty[SMAX], tfull[2], tempty[2], bfull[8], bempty[8];
     uint32_t tmem_base;
     uint16_t outmask[kMaxProducts];
 };
@@ -120,6 +127,12 @@ __device__ __forceinline__ void tmem_st32_const(uint32_t taddr, uint32_t v) {
         "r"(v)
         : "memory");
 }
+// 8 columns per instruction: tcgen05.st takes its sources as consecutive registers, so the
+// x32 form would pin 32 registers in the epilogue (spills at E >= 7)
+__device__ __forceinline__ void tmem_st8_const(uint32_t taddr, uint32_t v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v)
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // block-scaled instruction descriptor: e2m1 x e2m1, E8M0 scales, K-major, K=64
@@ -142,8 +155,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     // keep the shared state space visible to the compiler (STS/LDS, not generic ST/LD)
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *stages = smem;
-    uint8_t *bits = smem + S * STAGE_BYTES;
+    uint8_t *bits = smem + C::S * STAGE_BYTES;
     Bars *bars = reinterpret_cast<Bars *>(bits + C::D * C::BITS_BYTES);
+    constexpr int S = C::S;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -157,6 +171,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     const int chunk = FP4 ? FP4_CHUNK_STAGES : nks;
     const int nchunks = (nks + chunk - 1) / chunk;
     const int64_t total = my_tiles * (int64_t)s.nprod * nks;
+    // short k (few stages per accumulation) makes the epilogue hand-off latency-critical
+    const uint32_t idle_ns = nks >= 16 ? IDLE_SLEEP_NS : 0;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -199,35 +215,54 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
         const uint32_t full_leader = mapa(smem_u32(&bars->full[0]), 0);
         int slot = 0, st = 0;
         uint32_t bph = 0, phase = 0;
+        // bit words of one stage for this thread: A row then B^T row (fp4: 2 x 32 B, int8: 2 x 16 B)
+        constexpr int NQ = FP4 ? 4 : 2;
+        uint4 cur[NQ];
+        auto load_bits = [&](int sl, uint4 (&v)[NQ]) {
+#if GF2E_TILE_SLAB
+            const uint8_t *bs = bits + sl * C::BITS_BYTES + p * 16;  // slab layout: tc_tile_word
+            constexpr int QS = 2048;
+#else
+            const uint8_t *bs = bits + sl * C::BITS_BYTES + p * (C::BK / 8);
+            constexpr int QS = 16;
+#endif
+#pragma unroll
+            for (int i = 0; i < NQ / 2; ++i) {
+                v[i] = *reinterpret_cast<const uint4 *>(bs + i * QS);
+                v[NQ / 2 + i] = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + i * QS);
+            }
+        };
+        if (total > 0) {
+            mbar_wait(&bars->bfull[0], 0);
+            load_bits(0, cur);
+        }
         for (int64_t it = 0; it < total; ++it) {
-            mbar_wait(&bars->bfull[slot], bph);
-            const uint8_t *bs = bits + slot * C::BITS_BYTES;
-            mbar_wait(&bars->empty[st], phase ^ 1);
+            mbar_wait_sleep(&bars->empty[st], phase ^ 1, EXP_SLEEP_NS);
             uint8_t *sa = stages + st * STAGE_BYTES;
             if constexpr (FP4) {
-                const uint4 a0 = *reinterpret_cast<const uint4 *>(bs + p * 32);
-                const uint4 a1 = *reinterpret_cast<const uint4 *>(bs + p * 32 + 16);
-                const uint4 b0 = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + p * 32);
-                const uint4 b1 = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + p * 32 + 16);
-                expand_row_fp4<false>(sa, p, a0, a1);
-                expand_row_fp4<true>(sa + A_BYTES, p, b0, b1);
+                expand_row_fp4<false>(sa, p, cur[0], cur[1]);
+                expand_row_fp4<true>(sa + A_BYTES, p, cur[2], cur[3]);
             } else {
-                const uint4 wa = *reinterpret_cast<const uint4 *>(bs + p * 16);
-                const uint4 wb = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + p * 16);
-                expand_row<false>(sa, p, wa);
-                expand_row<true>(sa + A_BYTES, p, wb);
+                expand_row<false>(sa, p, cur[0]);
+                expand_row<true>(sa + A_BYTES, p, cur[1]);
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive_cluster(full_leader + (uint32_t)(st * 8));
-                // the bit tile was consumed by the expansion above (data dependence), so the
-                // loader may overwrite the slot: no read-before-overwrite race on bits
+                // this slot's bits were consumed by the expansion above (data dependence), so
+                // the loader may overwrite it: no read-before-overwrite race on bits
                 mbar_arrive(&bars->bempty[slot]);
             }
             if (++slot == C::D) {
                 slot = 0;
                 bph ^= 1;
+            }
+            // next stage's bits: read now so the shared-memory latency overlaps the empty wait
+            // (reading them before this stage's expansion was measured slower)
+            if (it + 1 < total) {
+                mbar_wait(&bars->bfull[slot], bph);
+                load_bits(slot, cur);
             }
             if (++st == S) {
                 st = 0;
@@ -252,7 +287,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                     const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * tile_words;
                     const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * tile_words;
                     for (int ks = 0; ks < nks; ++ks) {
-                        mbar_wait(&bars->bempty[slot], bph ^ 1);
+                        mbar_wait_sleep(&bars->bempty[slot], bph ^ 1, idle_ns);
                         mbar_arrive_expect_tx(&bars->bfull[slot], C::BITS_BYTES);
                         const uint32_t dst = bits_s + (uint32_t)(slot * C::BITS_BYTES);
                         bulk_g2s(dst, Ab + ks * tile_words, C::BITS_A, &bars->bfull[slot]);
@@ -290,7 +325,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                 const uint32_t mask = bars->outmask[t];
                 for (int ch = 0; ch < nchunks; ++ch, ++gp) {
                     const int buf = (int)(gp % C::NBUF);
-                    mbar_wait(&bars->tfull[buf], (uint32_t)((gp / C::NBUF) & 1));
+                    mbar_wait_sleep(&bars->tfull[buf], (uint32_t)((gp / C::NBUF) & 1), idle_ns);
                     tc_fence_after();
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
@@ -302,7 +337,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                         const uint32_t pw = parity_word_packed(v);
 #pragma unroll
                         for (int j = 0; j < E; ++j) acc[j][c] ^= pw & (0u - ((mask >> j) & 1u));
-                        if (FP4) tmem_st32_const(ta, FP4_ACC_INIT);
+                        if (FP4)
+#pragma unroll
+                            for (int c8 = 0; c8 < 32; c8 += 8) tmem_st8_const(ta + c8, FP4_ACC_INIT);
                     }
                     if (FP4) tmem_wait_st();
                     tc_fence_before();

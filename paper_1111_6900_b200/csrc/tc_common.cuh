@@ -8,6 +8,14 @@ namespace gf2e {
 namespace tc {
 
 // byte offset of 16-byte chunk c of row r in a K-major SWIZZLE_128B tile (8-row atoms of 1 KiB)
+// 16-byte read-only global load (non-coherent path, no L1 allocation)
+__device__ __forceinline__ uint4 ldg_nc_v4(const uint64_t *ptr) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(ptr));
+    return v;
+}
 __device__ __forceinline__ uint32_t swz(int r, int c) {
     return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
 }
