@@ -284,7 +284,8 @@ def run_ours(args):
     fp4_form = "fp4" in kernel_name
     if fp4_form:
         tc_peak = max(_lib.mma_peak_fp4(20000), _lib.mma_peak_fp4(20000))
-        peak_basis = ("measured live: pure tcgen05.mma kind::mxf4 (e2m1, scale 1.0) loop on all SMs; "
+        peak_basis = ("measured live: pure tcgen05.mma kind::mxf4 (e2m1, scale 1.0) loop on all SMs "
+                      "(zero operands; random GF(2)-encoded operands and 0.25 s loops measure the same); "
                       f"for reference 4 x {pk_kind} cuBLAS bf16 = {4 * pk['bf16_tflops']:.1f}")
     else:
         tc_peak = max(_lib.mma_peak(2, 20000)[0], _lib.mma_peak(1, 20000)[0])
@@ -315,6 +316,7 @@ def run_ours(args):
                      "ops_per_launch": ops_rank},
         "clocks": clocks,
     }
+
     if e2e:
         line["e2e"] = e2e
     if not args.no_cpu_baseline:

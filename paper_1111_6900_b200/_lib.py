@@ -125,13 +125,31 @@ def mma_peak(cta_group: int = 1, iters: int = 20000) -> tuple[float, float]:
     return tops.value, ms.value
 
 
-def mma_peak_fp4(iters: int = 20000) -> float:
+def mma_peak_fp4(iters: int = 20000, operands: str = "zero") -> float:
     """Measured dense kind::mxf4 (block-scaled e2m1) tensor rate in TOPS: pure MMA loop on all
-    SMs (gf2e_dev_fp4_probe on zero operands)."""
+    SMs (gf2e_dev_fp4_probe).  operands="zero": all-zero tiles (burst rate, lowest power);
+    "random": random GF(2) bits in the product kernel's e2m1 encoding (A nibbles 0 or
+    0.5/1/2/1, B nibbles 0 or 2/1/0.5/1) -- with a long loop this is the sustained rate the
+    product kernel can meet under the board power limit."""
+    import numpy as np
     import torch
 
-    a = torch.zeros(128 * 128, dtype=torch.uint8, device="cuda")
-    b = torch.zeros(256 * 128, dtype=torch.uint8, device="cuda")
+    if operands == "zero":
+        a = torch.zeros(128 * 128, dtype=torch.uint8, device="cuda")
+        b = torch.zeros(256 * 128, dtype=torch.uint8, device="cuda")
+    elif operands == "random":
+        rng = np.random.default_rng(7)
+
+        def img(rows, vals):
+            bits = rng.integers(0, 2, size=(rows, 32, 4, 2), dtype=np.uint8)  # [row][word][byte][nibble]
+            plane = (np.arange(32) % 4)[None, :, None, None]
+            v = np.asarray(vals, dtype=np.uint8)[plane] * bits
+            return torch.from_numpy((v[..., 0] | (v[..., 1] << 4)).reshape(-1).copy()).cuda()
+
+        a = img(128, [1, 2, 4, 2])
+        b = img(256, [4, 2, 1, 2])
+    else:
+        raise ValueError("operands must be 'zero' or 'random'")
     out = torch.empty(128 * 256, dtype=torch.int32, device="cuda")
     tops = ctypes.c_double()
     check(load().gf2e_dev_fp4_probe(iters, 0, a.data_ptr(), b.data_ptr(), out.data_ptr(), ctypes.byref(tops),

@@ -54,9 +54,38 @@ constexpr int BN = 256;
 #ifndef GF2E_FP4_S
 #define GF2E_FP4_S 5
 #endif
-constexpr int SMAX = 6;      // expanded operand stages (32 KiB each: one 128-byte swizzle row per operand row)
-constexpr uint32_t EXP_SLEEP_NS = 64;    // expanders waiting for a free operand stage
-constexpr uint32_t IDLE_SLEEP_NS = 500;  // epilogue / bulk loader (long k only, see below)
+constexpr int DMAX = 16;  // bit-tile ring slots (upper bound)
+constexpr int SMAX = 6;
+constexpr int BARS_BYTES = 1024;  // Bars (static_assert below)      // expanded operand stages (32 KiB each: one 128-byte swizzle row per operand row)
+#ifndef GF2E_INSTR
+#define GF2E_INSTR 0
+#endif
+#if GF2E_INSTR
+// dev-only: per-CTA cycle counters [block][16] (1: per-wait counters, 2: totals only)
+__device__ unsigned long long g_instr[1024][16];
+#endif
+#if GF2E_INSTR == 1
+#define TW(acc, stmt)                          \
+    do {                                       \
+        const long long _t0 = clock64();       \
+        stmt;                                  \
+        acc += (unsigned long long)(clock64() - _t0); \
+    } while (0)
+#else
+#define TW(acc, stmt) stmt
+#endif
+#ifndef GF2E_LOAD_SLEEP_NS
+#define GF2E_LOAD_SLEEP_NS 500
+#endif
+constexpr uint32_t LOAD_SLEEP_NS = GF2E_LOAD_SLEEP_NS;  // bulk loader waiting for a free bit slot
+#ifndef GF2E_EXP_SLEEP_NS
+#define GF2E_EXP_SLEEP_NS 64
+#endif
+constexpr uint32_t EXP_SLEEP_NS = GF2E_EXP_SLEEP_NS;  // expanders waiting for a free operand stage
+#ifndef GF2E_IDLE_SLEEP_NS
+#define GF2E_IDLE_SLEEP_NS 500
+#endif
+constexpr uint32_t IDLE_SLEEP_NS = GF2E_IDLE_SLEEP_NS;  // epilogue (long k only, see below)
 constexpr int NPW = 4;      // expander warps
 constexpr int NEW = 8;      // epilogue warps
 constexpr int GROUP_M = 8;  // tile rasterisation: row-tiles per column sweep (L2 reuse)
@@ -76,20 +105,23 @@ struct Cfg {
     static constexpr int BK = FP4 ? 256 : 128;  // k-bits per stage (= one 128-byte row of operand)
     static constexpr int KW = BK / 64;          // bit words per tile row per stage
     static constexpr int S = FP4 ? GF2E_FP4_S : 5;  // expanded operand stages
-    static constexpr int D = FP4 ? (S == 6 ? 4 : 6) : 8;  // bit-tile ring depth
+#ifndef GF2E_FP4_D
+#define GF2E_FP4_D 6
+#endif
+    static constexpr int D = FP4 ? GF2E_FP4_D : 8;  // bit-tile ring depth
     static constexpr int BITS_A = BM * (BK / 8);
     static constexpr int BITS_BYTES = (BM + BNH) * (BK / 8);
     static constexpr int NBUF = FP4 ? 1 : 2;    // TMEM accumulators
-    static constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + 512 + 1024;
+    static constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + BARS_BYTES + 1024;
     static_assert(SMEM_BYTES <= 232448, "shared memory");
 };
 
 struct __align__(8) Bars {
-    uint64_t full[SMAX], empty[SMAX], tfull[2], tempty[2], bfull[8], bempty[8];
+    uint64_t full[SMAX], empty[SMAX], tfull[2], tempty[2], bfull[DMAX], bempty[DMAX];
     uint32_t tmem_base;
     uint16_t outmask[kMaxProducts];
 };
-static_assert(sizeof(Bars) <= 512, "barrier block");
+static_assert(sizeof(Bars) <= BARS_BYTES, "barrier block");
 
 // tile index -> (row-tile, column-tile): sweep GROUP_M row-tiles down each column before
 // moving right, so the ~74 CTA pairs in flight share a few A row-blocks and B^T column-blocks
@@ -207,6 +239,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     cluster_sync();  // barriers and TMEM of both CTAs ready before any remote arrive / MMA
     tc_fence_after();
 
+    unsigned long long i_empty = 0, i_bfull = 0, i_tfull = 0, i_tempty = 0, i_full = 0;
+    (void)i_empty, (void)i_bfull, (void)i_tfull, (void)i_tempty, (void)i_full;
+#if GF2E_INSTR
+    const long long i_t0 = clock64();
+    unsigned long long i_g0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(i_g0));
+#endif
     if (warp < NPW) {
         // ===================== expanders (both CTAs) =====================
         // bit tiles arrive by bulk copy (loader warp); these warps keep no global loads in
@@ -237,7 +276,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             load_bits(0, cur);
         }
         for (int64_t it = 0; it < total; ++it) {
-            mbar_wait_sleep(&bars->empty[st], phase ^ 1, EXP_SLEEP_NS);
+            TW(i_empty, mbar_wait_sleep(&bars->empty[st], phase ^ 1, EXP_SLEEP_NS));
             uint8_t *sa = stages + st * STAGE_BYTES;
             if constexpr (FP4) {
                 expand_row_fp4<false>(sa, p, cur[0], cur[1]);
@@ -261,7 +300,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             // next stage's bits: read now so the shared-memory latency overlaps the empty wait
             // (reading them before this stage's expansion was measured slower)
             if (it + 1 < total) {
-                mbar_wait(&bars->bfull[slot], bph);
+                TW(i_bfull, mbar_wait(&bars->bfull[slot], bph));
                 load_bits(slot, cur);
             }
             if (++st == S) {
@@ -287,7 +326,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                     const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * tile_words;
                     const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * tile_words;
                     for (int ks = 0; ks < nks; ++ks) {
-                        mbar_wait_sleep(&bars->bempty[slot], bph ^ 1, idle_ns);
+                        mbar_wait_sleep(&bars->bempty[slot], bph ^ 1, LOAD_SLEEP_NS);
                         mbar_arrive_expect_tx(&bars->bfull[slot], C::BITS_BYTES);
                         const uint32_t dst = bits_s + (uint32_t)(slot * C::BITS_BYTES);
                         bulk_g2s(dst, Ab + ks * tile_words, C::BITS_A, &bars->bfull[slot]);
@@ -325,7 +364,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                 const uint32_t mask = bars->outmask[t];
                 for (int ch = 0; ch < nchunks; ++ch, ++gp) {
                     const int buf = (int)(gp % C::NBUF);
-                    mbar_wait_sleep(&bars->tfull[buf], (uint32_t)((gp / C::NBUF) & 1), idle_ns);
+                    TW(i_tfull, mbar_wait_sleep(&bars->tfull[buf], (uint32_t)((gp / C::NBUF) & 1), idle_ns));
                     tc_fence_after();
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
@@ -393,12 +432,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                 for (int t = 0; t < s.nprod; ++t) {
                     for (int ch = 0; ch < nchunks; ++ch, ++gp) {
                         const int buf = (int)(gp % C::NBUF);
-                        mbar_wait(&bars->tempty[buf], (uint32_t)((gp / C::NBUF) & 1) ^ 1);
+                        TW(i_tempty, mbar_wait(&bars->tempty[buf], (uint32_t)((gp / C::NBUF) & 1) ^ 1));
                         tc_fence_after();
                         const uint32_t dt = tmem + (uint32_t)(buf * BN);
                         const int ks1 = (ch + 1) * chunk < nks ? (ch + 1) * chunk : nks;
                         for (int ks = ch * chunk; ks < ks1; ++ks) {
-                            mbar_wait(&bars->full[st], phase);
+                            TW(i_full, mbar_wait(&bars->full[st], phase));
                             tc_fence_after();
                             const uint32_t sa = st0 + (uint32_t)(st * STAGE_BYTES);
                             const uint32_t sb = sa + A_BYTES;
@@ -423,6 +462,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
         }
         __syncwarp();
     }
+#if GF2E_INSTR
+    {
+        const unsigned long long i_tot = (unsigned long long)(clock64() - i_t0);
+        if (lane == 0 && warp == 0) {
+            g_instr[blockIdx.x][0] = i_empty;
+            g_instr[blockIdx.x][1] = i_bfull;
+            g_instr[blockIdx.x][2] = i_tot;
+        }
+        if (lane == 0 && warp == EPI_W0) {
+            g_instr[blockIdx.x][3] = i_tfull;
+            g_instr[blockIdx.x][4] = i_tot;
+        }
+        if (lane == 0 && warp == MMA_WARP) {
+            g_instr[blockIdx.x][5] = i_full;
+            g_instr[blockIdx.x][6] = i_tempty;
+            g_instr[blockIdx.x][7] = i_tot;
+            unsigned long long i_g1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(i_g1));
+            g_instr[blockIdx.x][8] = i_g1 - i_g0;
+        }
+    }
+#endif
 
     tc_fence_before();
     __syncthreads();
@@ -488,3 +549,9 @@ cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, bool fp4, cudaSt
 }
 
 }  // namespace gf2e
+
+#if GF2E_INSTR
+extern "C" int gf2e_debug_instr(unsigned long long *out, int nblocks) {
+    return (int)cudaMemcpyFromSymbol(out, gf2e::g_instr, sizeof(unsigned long long) * 16 * nblocks);
+}
+#endif
