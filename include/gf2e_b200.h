@@ -168,6 +168,38 @@ int gf2e_trsm(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T_dev
               uint64_t *B_dev, int64_t ldb, int64_t pb, int64_t m, int64_t n, void *workspace,
               int64_t workspace_bytes, void *stream, int64_t *bad_row);
 
+/*
+ * In-place PLE decomposition of the m x n plane stack S (ple_echelon.ple, ple_echelon.py:240-300,
+ * with the quadratic base case newton_john.nj_ple, newton_john.py:207-260): afterwards S holds
+ * L strictly below the diagonal of its leading `rank` columns (original pivot values on the
+ * diagonal) and E (leading ones implicit) on and above it; P_host / Q_host (length min(m, n),
+ * optional) receive the LAPACK-style row / column swap vectors, *rank the rank.  Same pivot
+ * rule as the reference (first nonzero entry top-down in the leftmost unfinished column), so
+ * the result is bit-identical to ple() for every crossover.  Recursion on the host over
+ * 64-column-aligned splits; 64-column base panels on device (k_ple_find / k_ple_apply);
+ * Schur updates are gf2e_slice_mul(GF2E_ACCUMULATE); corner solves are gf2e_trsm.
+ * Synchronises the stream (the recursion needs each panel's rank).
+ */
+int gf2e_ple(int e, uint32_t f, uint64_t *S_dev, int64_t ld, int64_t ps, int64_t m, int64_t n, int64_t *P_host,
+             int64_t *Q_host, int64_t *rank, void *stream);
+
+/* echelonize (ple_echelon.py:343-374): row echelon form (full = 0) or reduced row echelon form
+ * (full != 0) of S in place via gf2e_ple; *rank receives the rank. */
+int gf2e_echelonize(int e, uint32_t f, uint64_t *S_dev, int64_t ld, int64_t ps, int64_t m, int64_t n, int full,
+                    int64_t *rank, void *stream);
+
+/* apply_perm_rows (ple_echelon.py:81-91): swap vector swaps_host[0..n) applied in ascending
+ * (backward = 0) or descending order to rows of `planes` word arrays (planes = e for a plane
+ * stack, 1 for packed words) of nwords words each. */
+int gf2e_row_swaps(int planes, uint64_t *S_dev, int64_t ld, int64_t ps, int64_t rows, int64_t nwords,
+                   const int64_t *swaps_host, int64_t n, int backward, void *stream);
+
+/* PackedMatrix.col_swap sequence (mat_packed.py col_swap; ple_echelon.py:94-107, 275-279):
+ * triples_host[3i..3i+2] = (column a, column b, first row); w = slot width (1 for plane
+ * stacks, the pack width for packed words). */
+int gf2e_col_swaps(int planes, int w, uint64_t *S_dev, int64_t ld, int64_t ps, int64_t rows, int64_t cols,
+                   const int64_t *triples_host, int64_t n, void *stream);
+
 /* mul_by_x (mat_sliced.py:109-122): out planes = alpha * in planes (alpha = class of x). */
 int gf2e_mul_by_x(int e, uint32_t f, const uint64_t *in_dev, int64_t ld, int64_t pin, uint64_t *out_dev,
                   int64_t pout, int64_t rows, int64_t cols, void *stream);

@@ -7,7 +7,8 @@ This package is the parity checker (and the "port" CPU baseline) for the CUDA li
 Two halves:
 
 * ``liboracle.so`` (``oracle/gf2e_oracle.c``) — a C restatement of the reference functions
-  (generator, slice, cling, M4RM GF(2) product, recursive Karatsuba, reduce mod f), wrapped
+  (generator, slice, cling, M4RM GF(2) product, recursive Karatsuba, reduce mod f, the PLE
+  base case nj_ple), wrapped
   here with numpy.  Each C function cites the reference file:line it follows.
 * ``schedule`` — a symbolic replay of the reference Karatsuba recursion
   (``poly_mul.py:166-242``) that yields the operand subsets S_t, the combine map Γ, the
@@ -59,6 +60,9 @@ def lib():
                                     ctypes.POINTER(ctypes.c_int64)]
         L.orc_karatsuba.restype = ctypes.c_int
         L.orc_max_threads.restype = ctypes.c_int
+        L.orc_ple.argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint16), I64, I64,
+                              ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+        L.orc_ple.restype = I64
         _lib = L
     return _lib
 
@@ -309,3 +313,16 @@ def apply_schedule(sch: Schedule, A: np.ndarray, B: np.ndarray, m: int, k: int, 
             if (sch.outmap[j] >> t) & 1:
                 C[j] ^= P
     return C
+
+
+def ple(e: int, f: int, arr: np.ndarray):
+    """nj_ple (newton_john.py:207-260) on an element array; returns (factored array, P, Q, rank).
+    Equals the reference's recursive ple() for every crossover (ple_echelon.py:8-10)."""
+    a = np.ascontiguousarray(arr, dtype=np.uint16).copy()
+    m, n = a.shape
+    k = min(m, n)
+    P = np.zeros(k, dtype=np.int64)
+    Q = np.zeros(k, dtype=np.int64)
+    r = lib().orc_ple(e, f, a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)), m, n,
+                      P.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), Q.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    return a, P, Q, int(r)

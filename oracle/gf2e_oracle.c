@@ -381,6 +381,71 @@ int orc_karatsuba(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa,
     return 0;
 }
 
+/* ---- PLE base case ----------------------------------------------------------------------
+ * newton_john.py:207-260 (nj_ple), restated on a row-major element array a[m][n] (uint16):
+ * for each column j, the first row i >= r with a nonzero entry is the pivot; rows i, r are
+ * swapped; the pivot row right of j is scaled by 1/pivot (the pivot stays as L's diagonal);
+ * every row below r gets x * (pivot row right of j) added, x = its entry in column j (kept
+ * as the multiplier).  Finally columns t <-> Q[t] are swapped in rows >= t (L compression).
+ * Returns the rank; P, Q (length min(m, n)) are LAPACK-style swap vectors.  The recursive
+ * ple() (ple_echelon.py:240-300) returns the same factors for every crossover. */
+static uint32_t orc_gf_mul(uint32_t a, uint32_t b, int e, uint32_t f) { /* gf2e.py:40-56 */
+    uint32_t acc = 0;
+    for (int i = 0; i < e; ++i)
+        if ((b >> i) & 1u) acc ^= a << i;
+    for (int d = 2 * e - 2; d >= e; --d)
+        if ((acc >> d) & 1u) acc ^= f << (d - e);
+    return acc;
+}
+
+int64_t orc_ple(int e, uint32_t f, uint16_t *a, int64_t m, int64_t n, int64_t *P, int64_t *Q) {
+    const int q = 1 << e;
+    uint16_t *mt = (uint16_t *)malloc((size_t)q * q * sizeof(uint16_t));
+    for (int x = 0; x < q; ++x)
+        for (int y = 0; y < q; ++y) mt[x * q + y] = (uint16_t)orc_gf_mul((uint32_t)x, (uint32_t)y, e, f);
+    const int64_t k = m < n ? m : n;
+    for (int64_t i = 0; i < k; ++i) P[i] = Q[i] = i;
+    int64_t r = 0;
+    for (int64_t j = 0; j < n && r < k; ++j) {
+        int64_t i = r;
+        while (i < m && a[i * n + j] == 0) ++i;
+        if (i == m) continue;
+        const uint32_t piv = a[i * n + j];
+        P[r] = i;
+        Q[r] = j;
+        if (i != r)
+            for (int64_t c = 0; c < n; ++c) {
+                uint16_t t = a[i * n + c];
+                a[i * n + c] = a[r * n + c];
+                a[r * n + c] = t;
+            }
+        uint32_t inv = 1;
+        for (uint32_t y = 1; y < (uint32_t)q; ++y)
+            if (mt[piv * q + y] == 1) inv = y;
+        uint16_t *pr = a + r * n;
+        if (piv != 1)
+            for (int64_t c = j + 1; c < n; ++c) pr[c] = mt[inv * q + pr[c]];
+#pragma omp parallel for schedule(static)
+        for (int64_t i2 = r + 1; i2 < m; ++i2) {
+            uint16_t *row = a + i2 * n;
+            const uint32_t x = row[j];
+            if (!x) continue;
+            const uint16_t *mx = mt + x * q;
+            for (int64_t c = j + 1; c < n; ++c) row[c] ^= mx[pr[c]];
+        }
+        ++r;
+    }
+    for (int64_t t = 0; t < r; ++t)
+        if (Q[t] != t)
+            for (int64_t i = t; i < m; ++i) {
+                uint16_t x = a[i * n + t];
+                a[i * n + t] = a[i * n + Q[t]];
+                a[i * n + Q[t]] = x;
+            }
+    free(mt);
+    return r;
+}
+
 int orc_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

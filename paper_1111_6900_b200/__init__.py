@@ -11,7 +11,24 @@ from .gf2e import DEFAULT_POLYS, FieldCtx, field_new, is_irreducible, is_primiti
 from .mat_gf2 import BitMatrix, RowOpCounters, addmul as gf2_addmul, mul, mzd_addmul, mzd_mul, words_for
 from .mat_packed import PackedMatrix, pack_width
 from .mat_sliced import SlicedMatrix, cling, mul_by_x, mzed_cling, mzed_slice, slice_packed
-from .ple_echelon import SingularMatrixError, trsm_lower_left, trsm_lower_left_unit, trsm_sliced, trsm_upper_left
+from .ple_echelon import (
+    PermVector,
+    PleFactors,
+    SingularMatrixError,
+    apply_perm_cols,
+    apply_perm_rows,
+    col_swap,
+    echelonize,
+    echelonize_sliced,
+    ple,
+    ple_reconstruct,
+    ple_sliced,
+    ple_unpack,
+    trsm_lower_left,
+    trsm_lower_left_unit,
+    trsm_sliced,
+    trsm_upper_left,
+)
 from .poly_mul import (
     MulCounters,
     Schedule,
@@ -36,6 +53,8 @@ __all__ = [
     "PackedMatrix", "pack_width",
     "SlicedMatrix", "slice_packed", "cling", "mzed_slice", "mzed_cling", "mul_by_x",
     "SingularMatrixError", "trsm_upper_left", "trsm_lower_left", "trsm_lower_left_unit", "trsm_sliced",
+    "PermVector", "PleFactors", "apply_perm_rows", "apply_perm_cols", "col_swap", "ple", "ple_sliced", "ple_unpack",
+    "ple_reconstruct", "echelonize", "echelonize_sliced",
     "MulCounters", "Schedule", "schedule", "karatsuba_mul", "karatsuba_mul_packed", "karatsuba_mul_packed_host", "mzed_mul_host", "addmul", "addmul_packed",
     "reduce_mod_f", "count_products", "mzd_slice_mul", "mzd_slice_addmul", "mzed_mul", "mzed_addmul",
 ]

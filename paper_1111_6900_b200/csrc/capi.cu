@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -437,6 +438,146 @@ int check_flags(uint32_t flags) {
     return GF2E_OK;
 }
 
+// ---- PLE / echelonize over plane views (consumers of run_product and the TRSM) ----------------
+// Stream-ordered temporaries from the CUDA memory pool (freed at scope exit, reused by the pool).
+struct DevTmp {
+    void *p = nullptr;
+    cudaStream_t st;
+    DevTmp(size_t bytes, cudaStream_t s) : st(s) {
+        if (bytes && cudaMallocAsync(&p, bytes, st) != cudaSuccess) p = nullptr;
+    }
+    ~DevTmp() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    DevTmp(const DevTmp &) = delete;
+    DevTmp &operator=(const DevTmp &) = delete;
+};
+
+struct PleCtx {
+    int e;
+    uint32_t f;
+    Sched ks;
+    uint64_t *S;
+    int64_t ld, ps;
+    cudaStream_t st;
+    PanelOut *pout;  // device
+    int64_t *idx;    // device index scratch (3 * max(m, n) + 3 entries)
+    int64_t panels = 0;
+};
+
+// host vector -> device index scratch (synchronous staging: the host buffer may be reused)
+int put_idx(PleCtx &c, const std::vector<int64_t> &v) {
+    if (v.empty()) return GF2E_OK;
+    CKH(cudaMemcpyAsync(c.idx, v.data(), v.size() * 8, cudaMemcpyHostToDevice, c.st), "cudaMemcpyAsync");
+    CKH(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+    return GF2E_OK;
+}
+
+// ple_echelon.py:240-287 on the view rows [r0, r0+m), columns [c0, c0+n) (c0 % 64 == 0).  The
+// column split is rounded to a plane word: the factorisation does not depend on it (the
+// reference makes the same claim for its crossover, ple_echelon.py:8-10, and every split is
+// checked against its fixtures).  P, Q: length min(m, n), LAPACK-style swap vectors.
+int ple_rec(PleCtx &c, int64_t r0, int64_t c0, int64_t m, int64_t n, int64_t *P, int64_t *Q, int64_t &rank) {
+    const int64_t k = m < n ? m : n;
+    for (int64_t i = 0; i < k; ++i) P[i] = Q[i] = i;
+    rank = 0;
+    if (m == 0 || n == 0) return GF2E_OK;
+    uint64_t *V = c.S + r0 * c.ld + c0 / 64;
+    if (n <= kPlePanel) {  // base case nj_ple (newton_john.py:207-260) on one plane word
+        CK(launch_ple_panel(c.e, c.f, V, c.ld, c.ps, m, (int)n, c.pout, c.st), "ple_panel");
+        g_launches += m > 512 ? 2 : 1;
+        ++c.panels;
+        PanelOut h;
+        CKH(cudaMemcpyAsync(&h, c.pout, offsetof(PanelOut, jcol), cudaMemcpyDeviceToHost, c.st), "cudaMemcpyAsync");
+        CKH(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+        rank = h.rank;
+        for (int64_t t = 0; t < rank; ++t) {
+            P[t] = h.P[t];
+            Q[t] = h.Q[t];
+        }
+        return GF2E_OK;
+    }
+    int64_t n1 = round_up(n / 2, 64);
+    if (n1 >= n) n1 -= 64;
+    const int64_t k1 = m < n1 ? m : n1;
+    std::vector<int64_t> P1(k1), Q1(k1);
+    int64_t r1 = 0;
+    if (int rc = ple_rec(c, r0, c0, m, n1, P1.data(), Q1.data(), r1)) return rc;
+    uint64_t *R = V + n1 / 64;  // right half view
+    const int64_t nr = n - n1;
+    if (r1 > 0) {
+        std::vector<int64_t> sw(P1.begin(), P1.begin() + r1);
+        if (int rc = put_idx(c, sw)) return rc;
+        CK(launch_row_swaps(c.e, R, c.ld, c.ps, words_for(nr), c.idx, (int)r1, false, c.st), "row_swaps");
+        // L_top X = right[0:r1]  (the corner with its diagonal = pivots, ple_echelon.py:255-258)
+        const int64_t lw = words_for(r1);
+        DevTmp lt((size_t)c.e * r1 * lw * 8, c.st);
+        if (!lt.p) return fail(GF2E_ENOMEM, "out of device memory (PLE corner)");
+        uint64_t *L = static_cast<uint64_t *>(lt.p);
+        CK(launch_tril_copy(c.e, V, c.ld, c.ps, r1, L, lw, r1 * lw, c.st), "tril_copy");
+        const int64_t tws = gf2e_trsm_workspace(c.e, c.f, r1, nr);
+        DevTmp tw((size_t)(tws > 0 ? tws : 256), c.st);
+        if (!tw.p) return fail(GF2E_ENOMEM, "out of device memory (PLE trsm workspace)");
+        int64_t bad = -1;
+        if (int rc = gf2e_trsm(c.e, c.f, 0, 0, L, lw, r1 * lw, R, c.ld, c.ps, r1, nr, tw.p, tws, c.st, &bad))
+            return rc;
+        if (m - r1 > 0) {  // right[r1:] ^= left[r1:, :r1] . right[:r1]  (ple_echelon.py:259-260)
+            const int64_t mws = gf2e_slice_mul_workspace(c.e, c.f, m - r1, r1, nr, GF2E_ACCUMULATE);
+            DevTmp mw((size_t)(mws > 0 ? mws : 256), c.st);
+            if (!mw.p) return fail(GF2E_ENOMEM, "out of device memory (PLE update workspace)");
+            if (int rc = run_product(c.ks, V + r1 * c.ld, c.ld, c.ps, R, c.ld, c.ps, R + r1 * c.ld, c.ld, c.ps, m - r1,
+                                     r1, nr, GF2E_ACCUMULATE, mw.p, mws, c.st))
+                return rc;
+        }
+    }
+    const int64_t k2 = (m - r1) < nr ? (m - r1) : nr;
+    std::vector<int64_t> P2(k2 > 0 ? k2 : 0), Q2(k2 > 0 ? k2 : 0);
+    int64_t r2 = 0;
+    if (m - r1 > 0)
+        if (int rc = ple_rec(c, r0 + r1, c0 + n1, m - r1, nr, P2.data(), Q2.data(), r2)) return rc;
+    if (r2 > 0) {
+        std::vector<int64_t> sw(P2.begin(), P2.begin() + r2);  // left rows r1.. (ple_echelon.py:268-271)
+        if (int rc = put_idx(c, sw)) return rc;
+        CK(launch_row_swaps(c.e, V + r1 * c.ld, c.ld, c.ps, n1 / 64, c.idx, (int)r2, false, c.st), "row_swaps");
+        std::vector<int64_t> tr;  // compress the right half's L into the leading columns (:275-279)
+        for (int64_t u = 0; u < r2; ++u)
+            if (n1 + u != r1 + u) tr.insert(tr.end(), {r1 + u, n1 + u, r1 + u});
+        if (!tr.empty()) {
+            if (int rc = put_idx(c, tr)) return rc;
+            CK(launch_col_swaps(c.e, 1, V, c.ld, c.ps, m, c.idx, (int)(tr.size() / 3), c.st), "col_swaps");
+        }
+    }
+    for (int64_t t = 0; t < r1; ++t) {
+        P[t] = P1[t];
+        Q[t] = Q1[t];
+    }
+    for (int64_t t = 0; t < r2; ++t) {
+        P[r1 + t] = r1 + P2[t];
+        Q[r1 + t] = n1 + Q2[t];
+    }
+    rank = r1 + r2;
+    return GF2E_OK;
+}
+
+int ple_top(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int64_t n, int64_t *P, int64_t *Q,
+            int64_t *rank, cudaStream_t st) {
+    const int64_t k = m < n ? m : n;
+    DevTmp po(sizeof(PanelOut), st);
+    DevTmp ix((size_t)(3 * (m > n ? m : n) + 3) * 8, st);
+    if (!po.p || !ix.p) return fail(GF2E_ENOMEM, "out of device memory (PLE scratch)");
+    PleCtx c{e, f, to_kernel_sched(e, get_schedule(e, f)), S, ld, ps, st, static_cast<PanelOut *>(po.p),
+             static_cast<int64_t *>(ix.p)};
+    std::vector<int64_t> hp(k), hq(k);
+    int64_t r = 0;
+    if (int rc = ple_rec(c, 0, 0, m, n, hp.data(), hq.data(), r)) return rc;
+    for (int64_t i = 0; i < k; ++i) {
+        if (P) P[i] = hp[i];
+        if (Q) Q[i] = hq[i];
+    }
+    if (rank) *rank = r;
+    return GF2E_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -858,6 +999,108 @@ int gf2e_plane_mul(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ld
     if (int rc = check_device()) return rc;
     return run_product(plane_sched(), A, lda, 0, B, ldb, 0, C, ldc, 0, m, k, n, flags, ws, ws_bytes,
                        (cudaStream_t)stream);
+}
+
+
+int gf2e_ple(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int64_t n, int64_t *P, int64_t *Q,
+             int64_t *rank, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (rank) *rank = 0;
+    if (int rc = check_field(e, f)) return rc;
+    if (int rc = check_mat(S, m, words_for(n), ld, "A")) return rc;
+    if (m == 0 || n == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    return ple_top(e, f, S, ld, ps, m, n, P, Q, rank, (cudaStream_t)stream);
+}
+
+int gf2e_echelonize(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int64_t n, int full,
+                    int64_t *rank, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (rank) *rank = 0;
+    if (int rc = check_field(e, f)) return rc;
+    if (int rc = check_mat(S, m, words_for(n), ld, "A")) return rc;
+    if (m == 0 || n == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t k = m < n ? m : n;
+    std::vector<int64_t> P(k), Q(k);
+    int64_t r = 0;
+    if (int rc = ple_top(e, f, S, ld, ps, m, n, P.data(), Q.data(), &r, st)) return rc;
+    if (rank) *rank = r;
+    if (r == 0) return GF2E_OK;
+    DevTmp ix((size_t)(3 * r + 3) * 8, st);
+    if (!ix.p) return fail(GF2E_ENOMEM, "out of device memory (echelonize scratch)");
+    int64_t *idx = static_cast<int64_t *>(ix.p);
+    std::vector<int64_t> tr;  // undo the L compression (ple_echelon.py:359-362)
+    for (int64_t t = r - 1; t >= 0; --t)
+        if (Q[t] != t) tr.insert(tr.end(), {t, Q[t], t});
+    if (!tr.empty()) {
+        CKH(cudaMemcpyAsync(idx, tr.data(), tr.size() * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+        CK(launch_col_swaps(e, 1, S, ld, ps, m, idx, (int)(tr.size() / 3), st), "col_swaps");
+        CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    }
+    CKH(cudaMemcpyAsync(idx, Q.data(), r * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    CK(launch_echelon_marks(e, S, ld, ps, m, idx, (int)r, st), "echelon_marks");  // (:364-370)
+    if (full) {  // rows[:r] = upper^-1 rows[:r], upper = pivot columns (:371-375)
+        const int64_t lw = words_for(r);
+        DevTmp ut((size_t)e * r * lw * 8, st);
+        if (!ut.p) return fail(GF2E_ENOMEM, "out of device memory (echelonize corner)");
+        uint64_t *U = static_cast<uint64_t *>(ut.p);
+        CK(launch_gather_cols(e, S, ld, ps, idx, r, U, lw, r * lw, st), "gather_cols");
+        const int64_t tws = gf2e_trsm_workspace(e, f, r, n);
+        DevTmp tw((size_t)(tws > 0 ? tws : 256), st);
+        if (!tw.p) return fail(GF2E_ENOMEM, "out of device memory (echelonize trsm workspace)");
+        int64_t bad = -1;
+        if (int rc = gf2e_trsm(e, f, 1, 0, U, lw, r * lw, S, ld, ps, r, n, tw.p, tws, st, &bad)) return rc;
+    }
+    CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    return GF2E_OK;
+}
+
+int gf2e_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t rows, int64_t nwords,
+                   const int64_t *swaps, int64_t n, int backward, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (planes < 1 || n < 0 || n > rows) return fail(GF2E_EINVAL, "bad swap vector arguments");
+    if (int rc = check_mat(S, rows, nwords, ld, "A")) return rc;
+    for (int64_t i = 0; i < n; ++i)
+        if (swaps[i] < i || swaps[i] >= rows)
+            return fail(GF2E_EINVAL, "swap target %lld at index %lld invalid for %lld rows", (long long)swaps[i],
+                        (long long)i, (long long)rows);
+    if (n == 0 || nwords == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    DevTmp ix((size_t)n * 8, st);
+    if (!ix.p) return fail(GF2E_ENOMEM, "out of device memory");
+    CKH(cudaMemcpyAsync(ix.p, swaps, n * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    CK(launch_row_swaps(planes, S, ld, ps, nwords, static_cast<int64_t *>(ix.p), (int)n, backward != 0, st),
+       "row_swaps");
+    CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    return GF2E_OK;
+}
+
+int gf2e_col_swaps(int planes, int w, uint64_t *S, int64_t ld, int64_t ps, int64_t rows, int64_t cols,
+                   const int64_t *triples, int64_t n, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (planes < 1 || n < 0 || (w != 1 && w != 2 && w != 4 && w != 8 && w != 16))
+        return fail(GF2E_EINVAL, "bad column swap arguments");
+    if (int rc = check_mat(S, rows, words_for(cols * w), ld, "A")) return rc;
+    for (int64_t i = 0; i < n; ++i)
+        if (triples[3 * i] < 0 || triples[3 * i] >= cols || triples[3 * i + 1] < 0 || triples[3 * i + 1] >= cols ||
+            triples[3 * i + 2] < 0)
+            return fail(GF2E_EINVAL, "column swap %lld out of range for %lld columns", (long long)i, (long long)cols);
+    if (n == 0 || rows == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    DevTmp ix((size_t)n * 24, st);
+    if (!ix.p) return fail(GF2E_ENOMEM, "out of device memory");
+    CKH(cudaMemcpyAsync(ix.p, triples, n * 24, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    CK(launch_col_swaps(planes, w, S, ld, ps, rows, static_cast<int64_t *>(ix.p), (int)n, st), "col_swaps");
+    CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    return GF2E_OK;
 }
 
 }  // extern "C"

@@ -101,6 +101,30 @@ cudaError_t launch_mul_by_x(int e, uint32_t f, const uint64_t *in, int64_t ld, i
 cudaError_t launch_scalar_mul(int e, uint32_t f, uint32_t c, int w, const uint64_t *in, int64_t ldi, uint64_t *out,
                               int64_t ldo, int64_t rows, int64_t nwords, cudaStream_t st);
 
+// ple.cu — PLE base case on one 64-column panel + permutation / mask helpers
+constexpr int kPlePanel = 64;
+struct PanelOut {
+    int rank, ndisp, window, pad;
+    int64_t P[64], Q[64];
+    int jcol[64];
+    int64_t dpos[64];
+    int dstep[64];
+    uint64_t dval[64][kMaxE];
+    uint64_t bt[64 * kMaxE * kMaxE];  // alpha^s * T_t, [t][s][plane]
+};
+cudaError_t launch_ple_panel(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb, PanelOut *out,
+                             cudaStream_t st);
+cudaError_t launch_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t nwords, const int64_t *swaps,
+                             int n, bool backward, cudaStream_t st);
+cudaError_t launch_col_swaps(int planes, int w, uint64_t *S, int64_t ld, int64_t ps, int64_t rows, const int64_t *trip,
+                             int n, cudaStream_t st);
+cudaError_t launch_tril_copy(int e, const uint64_t *S, int64_t ld, int64_t ps, int64_t r, uint64_t *out, int64_t ldo,
+                             int64_t po, cudaStream_t st);
+cudaError_t launch_echelon_marks(int e, uint64_t *S, int64_t ld, int64_t ps, int64_t m, const int64_t *Q, int r,
+                                 cudaStream_t st);
+cudaError_t launch_gather_cols(int e, const uint64_t *S, int64_t ld, int64_t ps, const int64_t *Q, int64_t r,
+                               uint64_t *out, int64_t ldo, int64_t po, cudaStream_t st);
+
 cudaError_t run_fp4_probe(int iters, int mode, const uint8_t *a_img, const uint8_t *b_img, uint32_t *out, int nctas,
                           cudaStream_t st, float *ms);
 cudaError_t run_mma_peak(int cta_group, int iters, int nsms, cudaStream_t st, float *ms);

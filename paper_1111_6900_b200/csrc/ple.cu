@@ -1,0 +1,474 @@
+// ple.cu — device kernels of the PLE decomposition consumer:
+//
+//   k_ple_find / k_ple_apply: the quadratic base case `nj_ple` (newton_john.py:207-260) on one
+//     64-column panel of a sliced matrix (one plane word per row per plane).  nj_ple walks the
+//     panel's columns; for column j it takes the first row at or below position r whose entry
+//     is nonzero as pivot, swaps it to r, rescales the pivot row right of j by 1/pivot, and
+//     XORs x_i * (pivot row right of j) into every row below (the multiplier x_i stays in
+//     place as L).  Only the pivot search and the pivot row are sequential, so:
+//       phase 1 (one CTA): keeps a window of the first 512 row positions in shared memory,
+//         reduced step by step; finds each pivot there (or, if the window has none, scans the
+//         rows below it lazily, reducing each candidate by the pivots found so far); records
+//         the pivots, the swaps, and the basis tables alpha^s * T_t of every scaled pivot
+//         suffix T_t; writes the window rows back.
+//       phase 2 (all SMs): every row below the window applies the panel's <= 64 eliminations
+//         in order (x = entry at the pivot column, row ^= sum_s x_s * alpha^s * T_t) — one
+//         independent job per row.
+//     Both phases finish with the base case's L compression (column swaps t <-> Q[t] for rows
+//     >= t, newton_john.py:257-259).
+//   k_row_swaps:  LAPACK-style swap vectors on a window (apply_perm_rows, ple_echelon.py:81-91).
+//   k_col_swaps:  a sequence of (column a, column b, first row) swaps on w-bit slots — bit
+//     planes (w = 1) or packed words (w = pack width) (PackedMatrix.col_swap, used at
+//     ple_echelon.py:275-279, 311-313, 359-362).
+//   k_tril_copy:  the r x r corner with entries above the diagonal cleared (_tril_with_diag,
+//     ple_echelon.py:223-237).
+//   k_echelon_marks: echelonize's "drop L, set the implicit leading ones" (ple_echelon.py:364-370).
+//   k_gather_cols: pivot columns of the leading rows as an r x r matrix (_gather_columns,
+//     ple_echelon.py:338-340).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gf2e {
+namespace {
+
+__device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
+
+constexpr int PT = 512;  // phase-1 threads = window rows
+constexpr int KP = 64;   // pivots per panel (one plane word)
+
+__device__ __forceinline__ uint32_t elem(const uint64_t *v, int e, int c) {
+    uint32_t x = 0;
+    for (int b = 0; b < e; ++b) x |= (uint32_t)((v[b] >> c) & 1ULL) << b;
+    return x;
+}
+// v <- alpha * v on one sliced word per plane (x^e = f - x^e folded into the low planes)
+__device__ __forceinline__ void mul_alpha(uint64_t *v, int e, uint32_t f) {
+    const uint64_t top = v[e - 1];
+    for (int b = e - 1; b > 0; --b) v[b] = v[b - 1] ^ (((f >> b) & 1u) ? top : 0ULL);
+    v[0] = ((f & 1u) ? top : 0ULL);
+}
+__device__ uint32_t gf_mul_s(uint32_t a, uint32_t b, int e, uint32_t f) {
+    uint32_t acc = 0;
+    for (int i = 0; i < e; ++i)
+        if ((b >> i) & 1u) acc ^= a << i;
+    for (int d = 2 * e - 2; d >= e; --d)
+        if ((acc >> d) & 1u) acc ^= f << (d - e);
+    return acc;
+}
+__device__ uint32_t gf_inv_s(uint32_t a, int e, uint32_t f) {  // a^(2^e - 2)
+    uint32_t r = 1, p = a;
+    uint32_t n = (1u << e) - 2;
+    while (n) {
+        if (n & 1u) r = gf_mul_s(r, p, e, f);
+        p = gf_mul_s(p, p, e, f);
+        n >>= 1;
+    }
+    return r;
+}
+// row ^= x * T_t  with Bt = alpha^s * T_t (s = 0..e-1), one word per plane
+__device__ __forceinline__ void apply_step(uint64_t *v, int e, uint32_t x, const uint64_t *bt) {
+    for (int s = 0; s < e; ++s)
+        if ((x >> s) & 1u)
+            for (int b = 0; b < e; ++b) v[b] ^= bt[s * kMaxE + b];
+}
+__device__ __forceinline__ uint64_t swap_bits(uint64_t w, int a, int b) {
+    const uint64_t d = ((w >> a) ^ (w >> b)) & 1ULL;
+    return w ^ (d << a) ^ (d << b);
+}
+
+__global__ void __launch_bounds__(PT) k_ple_find(int e, uint32_t f, uint64_t *__restrict__ S, int64_t ld, int64_t ps,
+                                                 int64_t m, int nb, PanelOut *__restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint64_t *win = reinterpret_cast<uint64_t *>(smem);                 // [PT][kMaxE]
+    uint64_t *bt = win + PT * kMaxE;                                    // [KP][kMaxE][kMaxE]
+    uint64_t *ext = bt + KP * kMaxE * kMaxE;                            // [kMaxE] scanned pivot row
+    int64_t *worig = reinterpret_cast<int64_t *>(ext + kMaxE);          // [PT] original row of a slot
+    int64_t *dpos = worig + PT;                                         // [KP] displaced positions
+    int64_t *dorig = dpos + KP;                                         // [KP]
+    int *dstep = reinterpret_cast<int *>(dorig + KP);                   // [KP]
+    __shared__ uint64_t s_dval[KP][kMaxE];
+    __shared__ int s_jcol[KP];
+    __shared__ int64_t s_P[KP], s_Q[KP];
+    __shared__ int s_min, s_nd, s_supp_ok;
+    __shared__ unsigned long long s_supp;
+    __shared__ int64_t s_pmin;
+
+    const int tid = threadIdx.x;
+    const int W = (int)(m < PT ? m : PT);
+    const uint64_t cmask = nb >= 64 ? ~0ULL : ((1ULL << nb) - 1);
+    const int k = (int)(m < nb ? m : nb);
+    for (int s = tid; s < W; s += PT) {
+        for (int b = 0; b < e; ++b) win[s * kMaxE + b] = S[b * ps + s * ld] & cmask;
+        worig[s] = s;
+    }
+    if (tid == 0) {
+        s_nd = 0;
+        s_supp_ok = 0;
+        s_supp = 0;
+    }
+    __syncthreads();
+    int r = 0;
+    for (int j = 0; j < nb && r < k; ++j) {
+        if (tid == 0) {
+            s_min = 0x7fffffff;
+            s_pmin = INT64_MAX;
+        }
+        __syncthreads();
+        for (int s = r + tid; s < W; s += PT) {
+            uint64_t any = 0;
+            for (int b = 0; b < e; ++b) any |= win[s * kMaxE + b];
+            if ((any >> j) & 1ULL) atomicMin(&s_min, s);
+        }
+        __syncthreads();
+        int64_t ipos = s_min;
+        if (s_min == 0x7fffffff && W < m) {
+            // Column support of the rows below the window: their original bits OR the scaled
+            // pivot suffixes (the only things ever XOR-ed into them).  Computed at the first
+            // miss; a column outside it has no pivot below the window either.
+            if (!s_supp_ok) {
+                uint64_t acc = 0;
+                for (int64_t p = W + tid; p < m; p += PT)
+                    for (int b = 0; b < e; ++b) acc |= S[b * ps + p * ld];
+                if (acc) atomicOr(&s_supp, acc & cmask);
+                for (int t = tid; t < r; t += PT)
+                    for (int b = 0; b < e; ++b) atomicOr(&s_supp, bt[t * kMaxE * kMaxE + b]);
+                __syncthreads();
+                if (tid == 0) s_supp_ok = 1;
+            }
+            __syncthreads();
+            if (!((s_supp >> j) & 1ULL)) continue;  // uniform
+        }
+        if (s_min == 0x7fffffff) {
+            // no pivot in the window: scan the rows below it, reducing each candidate lazily
+            const int nd = s_nd;
+            for (int64_t base = W; base < m; base += PT) {
+                const int64_t p = base + tid;
+                uint64_t v[kMaxE];
+                bool hit = false;
+                if (p < m) {
+                    int st0 = 0, di = -1;
+                    for (int d = 0; d < nd; ++d)
+                        if (dpos[d] == p) di = d;
+                    if (di >= 0) {
+                        for (int b = 0; b < e; ++b) v[b] = s_dval[di][b];
+                        st0 = dstep[di];
+                    } else {
+                        for (int b = 0; b < e; ++b) v[b] = S[b * ps + p * ld] & cmask;
+                    }
+                    for (int t = st0; t < r; ++t) apply_step(v, e, elem(v, e, s_jcol[t]), bt + t * kMaxE * kMaxE);
+                    uint64_t any = 0;
+                    for (int b = 0; b < e; ++b) any |= v[b];
+                    hit = (any >> j) & 1ULL;
+                    if (hit) atomicMin((unsigned long long *)&s_pmin, (unsigned long long)p);
+                }
+                __syncthreads();
+                if (hit && s_pmin == p)
+                    for (int b = 0; b < e; ++b) ext[b] = v[b];
+                __syncthreads();
+                if (s_pmin != INT64_MAX) break;
+            }
+            ipos = s_pmin;
+            if (ipos == INT64_MAX) continue;  // uniform: no pivot in column j
+        }
+        if (tid == 0) {
+            uint64_t *pr = win + r * kMaxE;
+            if (ipos < W) {
+                const int i = (int)ipos;
+                if (i != r) {
+                    for (int b = 0; b < e; ++b) {
+                        const uint64_t t = pr[b];
+                        pr[b] = win[i * kMaxE + b];
+                        win[i * kMaxE + b] = t;
+                    }
+                    const int64_t o = worig[r];
+                    worig[r] = worig[i];
+                    worig[i] = o;
+                }
+            } else {
+                // the row at position r moves below the window: remember it (reduced by steps < r)
+                int di = -1;
+                for (int d = 0; d < s_nd; ++d)
+                    if (dpos[d] == ipos) di = d;
+                int64_t porig = ipos;
+                if (di < 0) {
+                    di = s_nd++;
+                } else {
+                    porig = dorig[di];
+                }
+                dpos[di] = ipos;
+                dorig[di] = worig[r];
+                dstep[di] = r;
+                for (int b = 0; b < e; ++b) {
+                    s_dval[di][b] = pr[b];
+                    pr[b] = ext[b];
+                }
+                worig[r] = porig;
+            }
+            s_P[r] = ipos;
+            s_Q[r] = j;
+            s_jcol[r] = j;
+            // scale the pivot row right of j by 1/pivot; the pivot entry stays (diagonal of L)
+            const uint32_t piv = elem(pr, e, j);
+            const uint32_t inv = gf_inv_s(piv, e, f);
+            const uint64_t sm = (j >= 63 ? 0ULL : (~0ULL << (j + 1))) & cmask;
+            uint64_t cur[kMaxE], acc[kMaxE];
+            for (int b = 0; b < e; ++b) {
+                cur[b] = pr[b] & sm;
+                acc[b] = 0;
+            }
+            for (int s = 0; s < e; ++s) {
+                if ((inv >> s) & 1u)
+                    for (int b = 0; b < e; ++b) acc[b] ^= cur[b];
+                mul_alpha(cur, e, f);
+            }
+            for (int b = 0; b < e; ++b) {
+                pr[b] = (pr[b] & ~sm) | acc[b];
+                cur[b] = acc[b];
+            }
+            if (s_supp_ok)
+                for (int b = 0; b < e; ++b) s_supp |= cur[b];
+            uint64_t *btr = bt + r * kMaxE * kMaxE;
+            for (int s = 0; s < e; ++s) {
+                for (int b = 0; b < e; ++b) btr[s * kMaxE + b] = cur[b];
+                mul_alpha(cur, e, f);
+            }
+        }
+        __syncthreads();
+        const uint64_t *btr = bt + r * kMaxE * kMaxE;
+        for (int s = r + 1 + tid; s < W; s += PT) {
+            uint64_t *v = win + s * kMaxE;
+            const uint32_t x = elem(v, e, j);
+            if (x) apply_step(v, e, x, btr);
+        }
+        ++r;
+        __syncthreads();
+    }
+    // L compression of the base case (newton_john.py:257-259) and write-back of the window
+    for (int s = tid; s < W; s += PT) {
+        uint64_t v[kMaxE];
+        for (int b = 0; b < e; ++b) v[b] = win[s * kMaxE + b];
+        for (int t = 0; t < r && t <= s; ++t) {
+            const int q = (int)s_Q[t];
+            if (q != t)
+                for (int b = 0; b < e; ++b) v[b] = swap_bits(v[b], t, q);
+        }
+        for (int b = 0; b < e; ++b) {
+            uint64_t *d = S + b * ps + s * ld;
+            *d = (*d & ~cmask) | v[b];
+        }
+    }
+    // outputs for phase 2 and the host
+    for (int i = tid; i < r * kMaxE * kMaxE; i += PT) out->bt[i] = bt[i];
+    if (tid < r) {
+        out->P[tid] = s_P[tid];
+        out->Q[tid] = s_Q[tid];
+        out->jcol[tid] = s_jcol[tid];
+    }
+    if (tid < s_nd) {
+        out->dpos[tid] = dpos[tid];
+        out->dstep[tid] = dstep[tid];
+        for (int b = 0; b < e; ++b) out->dval[tid][b] = s_dval[tid][b];
+    }
+    if (tid == 0) {
+        out->rank = r;
+        out->ndisp = s_nd;
+        out->window = W;
+    }
+}
+
+// phase 2: rows at positions >= window apply the panel's eliminations and the L compression
+__global__ void __launch_bounds__(256) k_ple_apply(int e, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t m,
+                                                   int nb, const PanelOut *__restrict__ in) {
+    extern __shared__ __align__(16) uint8_t smem2[];
+    uint64_t *bt = reinterpret_cast<uint64_t *>(smem2);  // [KP][kMaxE][kMaxE]
+    __shared__ int jc[KP], qc[KP];
+    __shared__ int r_s, nd_s, w_s;
+    if (threadIdx.x == 0) {
+        r_s = in->rank;
+        nd_s = in->ndisp;
+        w_s = in->window;
+    }
+    __syncthreads();
+    const int r = r_s, nd = nd_s;
+    for (int i = threadIdx.x; i < r * kMaxE * kMaxE; i += blockDim.x) bt[i] = in->bt[i];
+    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+        jc[i] = in->jcol[i];
+        qc[i] = (int)in->Q[i];
+    }
+    __syncthreads();
+    const uint64_t cmask = nb >= 64 ? ~0ULL : ((1ULL << nb) - 1);
+    for (int64_t p = w_s + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t v[kMaxE];
+        int st0 = 0, di = -1;
+        for (int d = 0; d < nd; ++d)
+            if (in->dpos[d] == p) di = d;
+        if (di >= 0) {
+            for (int b = 0; b < e; ++b) v[b] = in->dval[di][b];
+            st0 = in->dstep[di];
+        } else {
+            for (int b = 0; b < e; ++b) v[b] = S[b * ps + p * ld] & cmask;
+        }
+        for (int t = st0; t < r; ++t) apply_step(v, e, elem(v, e, jc[t]), bt + t * kMaxE * kMaxE);
+        for (int t = 0; t < r; ++t)
+            if (qc[t] != t)
+                for (int b = 0; b < e; ++b) v[b] = swap_bits(v[b], t, qc[t]);
+        for (int b = 0; b < e; ++b) {
+            uint64_t *d = S + b * ps + p * ld;
+            *d = (*d & ~cmask) | v[b];
+        }
+    }
+}
+
+// swaps[t] (t < n) applied in order to rows row0+t <-> row0+swaps[t]; thread = (plane, word)
+__global__ void k_row_swaps(int planes, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t nwords,
+                            const int64_t *__restrict__ swaps, int n, int backward) {
+    const int64_t total = (int64_t)planes * nwords;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        const int64_t b = idx / nwords, w = idx % nwords;
+        uint64_t *col = S + b * ps + w;
+        for (int i = 0; i < n; ++i) {
+            const int t = backward ? n - 1 - i : i;
+            const int64_t q = swaps[t];
+            if (q != t) {
+                const uint64_t x = col[t * ld];
+                col[t * ld] = col[q * ld];
+                col[q * ld] = x;
+            }
+        }
+    }
+}
+
+// (a, b, first row) triples applied in order to w-bit slots; thread = (plane, row)
+__global__ void k_col_swaps(int planes, int w, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t rows,
+                            const int64_t *__restrict__ trip, int n) {
+    const int64_t total = (int64_t)planes * rows;
+    const uint64_t fm = w >= 64 ? ~0ULL : ((1ULL << w) - 1);
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        const int64_t b = idx / rows, i = idx % rows;
+        uint64_t *row = S + b * ps + i * ld;
+        for (int t = 0; t < n; ++t) {
+            const int64_t ca = trip[3 * t], cb = trip[3 * t + 1], r0 = trip[3 * t + 2];
+            if (i < r0 || ca == cb) continue;
+            const int64_t ba = ca * w, bb = cb * w;
+            uint64_t *wa = row + (ba >> 6), *wb = row + (bb >> 6);
+            const int sa = (int)(ba & 63), sb = (int)(bb & 63);
+            const uint64_t va = (*wa >> sa) & fm, vb = (*wb >> sb) & fm;
+            *wa = (*wa & ~(fm << sa)) | (vb << sa);
+            *wb = (*wb & ~(fm << sb)) | (va << sb);
+        }
+    }
+}
+
+// out[i][c] = S[i][c] for c <= i < r, 0 above the diagonal
+__global__ void k_tril_copy(int e, const uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t r,
+                            uint64_t *__restrict__ out, int64_t ldo, int64_t po) {
+    const int64_t nw = words_for(r);
+    const int64_t total = (int64_t)e * r * nw;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        const int64_t b = idx / (r * nw), rem = idx % (r * nw), i = rem / nw, w = rem % nw;
+        uint64_t v = S[b * ps + i * ld + w];
+        const int64_t lo = w * 64;
+        uint64_t keep;
+        if (i < lo) keep = 0;
+        else if (i - lo >= 63) keep = ~0ULL;
+        else keep = (2ULL << (i - lo)) - 1;
+        if (w == nw - 1) keep &= tail_mask(r);
+        out[b * po + i * ldo + w] = v & keep;
+    }
+}
+
+// echelonize: rows >= t lose column Q[t]; row t < r gets the leading one at Q[t]
+__global__ void k_echelon_marks(int e, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t m,
+                                const int64_t *__restrict__ Q, int r) {
+    for (int64_t i = gtid(); i < m; i += gstride()) {
+        const int tmax = (int)(i < r - 1 ? i : r - 1);
+        for (int t = 0; t <= tmax; ++t) {
+            const int64_t c = Q[t];
+            const uint64_t bit = 1ULL << (c & 63);
+            for (int b = 0; b < e; ++b) S[b * ps + i * ld + (c >> 6)] &= ~bit;
+        }
+        if (i < r) S[i * ld + (Q[i] >> 6)] |= 1ULL << (Q[i] & 63);
+    }
+}
+
+// out[i][t] = S[i][Q[t]], i, t < r
+__global__ void k_gather_cols(int e, const uint64_t *__restrict__ S, int64_t ld, int64_t ps, const int64_t *__restrict__ Q,
+                              int64_t r, uint64_t *__restrict__ out, int64_t ldo, int64_t po) {
+    const int64_t nw = words_for(r);
+    const int64_t total = (int64_t)e * r * nw;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        const int64_t b = idx / (r * nw), rem = idx % (r * nw), i = rem / nw, w = rem % nw;
+        uint64_t v = 0;
+        for (int u = 0; u < 64 && w * 64 + u < r; ++u) {
+            const int64_t c = Q[w * 64 + u];
+            v |= ((S[b * ps + i * ld + (c >> 6)] >> (c & 63)) & 1ULL) << u;
+        }
+        out[b * po + i * ldo + w] = v;
+    }
+}
+
+inline int grid_for(int64_t total, int threads) {
+    int64_t g = (total + threads - 1) / threads;
+    if (g > 148 * 32) g = 148 * 32;
+    return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+size_t ple_find_smem() {
+    return (size_t)PT * kMaxE * 8 + (size_t)KP * kMaxE * kMaxE * 8 + kMaxE * 8 + PT * 8 + 2 * KP * 8 + KP * 4;
+}
+
+cudaError_t launch_ple_panel(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb, PanelOut *out,
+                             cudaStream_t st) {
+    const size_t smem = ple_find_smem();
+    cudaError_t err = cudaFuncSetAttribute(k_ple_find, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    k_ple_find<<<1, PT, smem, st>>>(e, f, S, ld, ps, m, nb, out);
+    err = cudaGetLastError();
+    if (err != cudaSuccess || m <= PT) return err;
+    const int smem2 = KP * kMaxE * kMaxE * 8;
+    err = cudaFuncSetAttribute(k_ple_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    if (err != cudaSuccess) return err;
+    k_ple_apply<<<grid_for(m - PT, 256), 256, smem2, st>>>(e, S, ld, ps, m, nb, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t nwords, const int64_t *swaps,
+                             int n, bool backward, cudaStream_t st) {
+    if (n == 0 || nwords == 0) return cudaSuccess;
+    k_row_swaps<<<grid_for((int64_t)planes * nwords, 128), 128, 0, st>>>(planes, S, ld, ps, nwords, swaps, n,
+                                                                        backward ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_col_swaps(int planes, int w, uint64_t *S, int64_t ld, int64_t ps, int64_t rows, const int64_t *trip,
+                             int n, cudaStream_t st) {
+    if (n == 0 || rows == 0) return cudaSuccess;
+    k_col_swaps<<<grid_for((int64_t)planes * rows, 256), 256, 0, st>>>(planes, w, S, ld, ps, rows, trip, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tril_copy(int e, const uint64_t *S, int64_t ld, int64_t ps, int64_t r, uint64_t *out, int64_t ldo,
+                             int64_t po, cudaStream_t st) {
+    if (r == 0) return cudaSuccess;
+    k_tril_copy<<<grid_for((int64_t)e * r * words_for(r), 256), 256, 0, st>>>(e, S, ld, ps, r, out, ldo, po);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_echelon_marks(int e, uint64_t *S, int64_t ld, int64_t ps, int64_t m, const int64_t *Q, int r,
+                                 cudaStream_t st) {
+    if (r == 0 || m == 0) return cudaSuccess;
+    k_echelon_marks<<<grid_for(m, 256), 256, 0, st>>>(e, S, ld, ps, m, Q, r);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_cols(int e, const uint64_t *S, int64_t ld, int64_t ps, const int64_t *Q, int64_t r,
+                               uint64_t *out, int64_t ldo, int64_t po, cudaStream_t st) {
+    if (r == 0) return cudaSuccess;
+    k_gather_cols<<<grid_for((int64_t)e * r * words_for(r), 256), 256, 0, st>>>(e, S, ld, ps, Q, r, out, ldo, po);
+    return cudaGetLastError();
+}
+
+}  // namespace gf2e

@@ -176,6 +176,63 @@ def main():
         sc.append(tag)
     store["scal_tags"] = np.array(sc)
 
+    # PLE decomposition and echelon forms (ple_echelon.py:240-374): random, low-rank and
+    # structured inputs; the reference's result is crossover-independent (checked here)
+    pl = []
+    # The reference's window paste raises for many unaligned splits (mat_gf2.py:240-251: the
+    # shifted buffer is one word short when the window does not spill into an extra word), so
+    # shapes are chosen where its recursion survives; failures are reported and skipped.
+    for e, m, n, seed, kind in [(8, 150, 256, 11, "rand"), (2, 200, 128, 12, "rand"), (4, 257, 256, 13, "rand"),
+                                (8, 300, 256, 14, "lowrank"), (3, 1, 5, 15, "rand"), (5, 5, 1, 16, "rand"),
+                                (10, 70, 70, 17, "rand"), (8, 129, 192, 18, "zerocols"), (2, 90, 64, 19, "lowrank"),
+                                (8, 64, 128, 20, "dup"), (8, 200, 130, 21, "rand"), (4, 300, 512, 22, "lowrank"),
+                                (10, 100, 256, 23, "zerocols"), (6, 100, 96, 24, "rand")]:
+        ctx = gf2e.field_new(e)
+        if kind == "rand":
+            A = mat_packed.PackedMatrix.random(ctx, m, n, seed)
+        else:
+            if kind == "lowrank":  # rank <= 37: A = X . Y
+                X = mat_packed.PackedMatrix.random(ctx, m, 37, seed)
+                Y = mat_packed.PackedMatrix.random(ctx, 37, n, seed + 1)
+                A = poly_mul.karatsuba_mul_packed(X, Y)
+            else:
+                arr = mat_packed.PackedMatrix.random(ctx, m, n, seed).to_array()
+                if kind == "zerocols":
+                    arr[:, 3:70] = 0
+                    arr[:, 130:131] = 0
+                    arr[:40, 0] = 0
+                else:  # duplicated / scaled rows and an all-zero row
+                    arr[10:20] = arr[0:10]
+                    arr[30] = 0
+                    arr[40:50] = (arr[0:10].astype(np.int64) * 0 + arr[50:60]).astype(arr.dtype)
+                A = mat_packed.PackedMatrix.from_array(ctx, arr)
+        tag = f"ple/e{e}/{m}x{n}/{kind}"
+        try:
+            F = ple_echelon.ple(A.copy())
+            ech = []
+            for full in (True, False):
+                X = A.copy()
+                ech.append((ple_echelon.echelonize(X, full=full), X))
+        except ValueError as ex:
+            print(f"skip {tag}: reference raised {ex!s:.60}")
+            continue
+        try:
+            F16 = ple_echelon.ple(A.copy(), crossover=16)
+            assert F.rank == F16.rank and F.P == F16.P and F.Q == F16.Q and F.matrix == F16.matrix
+        except ValueError:
+            pass
+        store[f"{tag}/meta"] = np.array([e, ctx.f, m, n], dtype=np.int64)
+        store[f"{tag}/A"] = A.storage.words.copy()
+        store[f"{tag}/ple"] = F.matrix.storage.words.copy()
+        store[f"{tag}/P"] = F.P.entries.copy()
+        store[f"{tag}/Q"] = F.Q.entries.copy()
+        store[f"{tag}/rank"] = np.array([F.rank], dtype=np.int64)
+        for full, (r, X) in zip((True, False), ech):
+            assert r == F.rank
+            store[f"{tag}/ech{int(full)}"] = X.storage.words.copy()
+        pl.append(tag)
+    store["ple_tags"] = np.array(pl)
+
     np.savez_compressed(OUT, **store)
     print(f"wrote {OUT}: {len(store)} arrays, {os.path.getsize(OUT)} bytes")
 

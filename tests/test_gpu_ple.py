@@ -1,0 +1,117 @@
+"""SURVEY §8f rank 1 on device: PLE decomposition and echelon forms (ple_echelon.py:240-374)
+built on the fused addmul, the device TRSM and the two-phase nj_ple panel kernel.
+Bit-exact against fixtures the reference produced (tests/golden/make_golden.py) and, at sizes
+the reference cannot reach, against the oracle's restatement of nj_ple (itself pinned to the
+same fixtures in test_oracle_golden.py)."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def g():
+    import torch
+
+    import paper_1111_6900_b200 as g
+
+    torch.cuda.set_device(0)
+    return g
+
+
+def test_ple_golden(g, golden):
+    for tag in (str(t) for t in golden["ple_tags"]):
+        e, f, m, n = (int(x) for x in golden[f"{tag}/meta"])
+        ctx = g.field_new(e, f)
+        A = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/A"], n)
+        F = g.ple(A.copy())
+        assert F.rank == int(golden[f"{tag}/rank"][0]), tag
+        assert np.array_equal(F.P.entries, golden[f"{tag}/P"]), tag
+        assert np.array_equal(F.Q.entries, golden[f"{tag}/Q"]), tag
+        assert np.array_equal(F.matrix.to_numpy(), golden[f"{tag}/ple"]), tag
+        for full in (True, False):
+            X = A.copy()
+            assert g.echelonize(X, full=full) == F.rank
+            assert np.array_equal(X.to_numpy(), golden[f"{tag}/ech{int(full)}"]), (tag, full)
+
+
+def _lowrank(g, ctx, m, n, r, seed):
+    X = g.PackedMatrix.random(ctx, m, r, seed)
+    Y = g.PackedMatrix.random(ctx, r, n, seed + 1)
+    return g.karatsuba_mul_packed(X, Y)
+
+
+@pytest.mark.parametrize("e,m,n,kind", [(8, 1000, 1300, "rand"), (2, 1500, 700, "rand"), (4, 900, 700, "lowrank"),
+                                        (10, 2000, 200, "rand"), (6, 600, 900, "zeros"), (8, 700, 64, "lowrank"),
+                                        (3, 520, 130, "dup")])
+def test_ple_vs_oracle(g, e, m, n, kind):
+    ctx = g.field_new(e)
+    if kind == "lowrank":
+        A = _lowrank(g, ctx, m, n, 45, 30 + e)
+    else:
+        A = g.PackedMatrix.random(ctx, m, n, 30 + e)
+        if kind != "rand":
+            arr = A.to_array()
+            if kind == "zeros":  # zero column band, zero rows at the top: pivots below the window
+                arr[:, 100:400] = 0
+                arr[:600, 0] = 0
+            else:  # duplicated rows below the 512-row window
+                arr[515:519] = arr[0:4]
+                arr[:, 7] = 0
+            A = g.PackedMatrix.from_array(ctx, arr)
+    ref, P, Q, r = oracle.ple(e, ctx.f, A.to_array())
+    F = g.ple(A.copy())
+    assert F.rank == r
+    assert np.array_equal(F.P.entries, P) and np.array_equal(F.Q.entries, Q)
+    assert np.array_equal(F.matrix.to_array(), ref)
+
+
+def test_ple_reconstruct_and_echelon(g):
+    ctx = g.field_new(5)
+    A = _lowrank(g, ctx, 700, 600, 333, 7)
+    F = g.ple(A.copy())
+    assert F.rank == 333
+    assert g.ple_reconstruct(F) == A
+    R = A.copy()
+    assert g.echelonize(R, full=True) == 333
+    arr = R.to_array()
+    assert not arr[333:].any()
+    piv = [int(np.nonzero(arr[i])[0][0]) for i in range(333)]
+    assert piv == sorted(piv) and np.all(arr[:333, piv] == np.eye(333, dtype=arr.dtype))
+
+
+def test_perm_helpers(g):
+    ctx = g.field_new(4)
+    A = g.PackedMatrix.random(ctx, 50, 70, 3)
+    S = g.slice_packed(A)
+    P = g.PermVector([3, 1, 9, 5, 4])
+    B = A.copy()
+    g.apply_perm_rows(B, P)
+    ref = A.to_array()
+    for i, j in enumerate(P.entries):
+        ref[[i, j]] = ref[[j, i]]
+    assert np.array_equal(B.to_array(), ref)
+    g.apply_perm_rows(B, P, forward=False)
+    assert B == A
+    g.apply_perm_rows(S, P)
+    assert np.array_equal(S.to_array(), ref)
+    Q = g.PermVector([2, 1, 69])
+    C = A.copy()
+    g.apply_perm_cols(C, Q)
+    refc = A.to_array()
+    for i, j in enumerate(Q.entries):
+        refc[:, [i, j]] = refc[:, [j, i]]
+    assert np.array_equal(C.to_array(), refc)
+    g.col_swap(C, 0, 5, row_start=10)
+    refc[10:, [0, 5]] = refc[10:, [5, 0]]
+    assert np.array_equal(C.to_array(), refc)
+    with pytest.raises(ValueError, match="swap target"):
+        g.apply_perm_rows(A, [0, 50])
+    with pytest.raises(ValueError, match="violates"):
+        g.PermVector([1, 0])
+    X = g.PackedMatrix.random(ctx, 0, 5, 1)
+    F = g.ple(X)
+    assert F.rank == 0 and len(F.P) == 0

@@ -101,3 +101,22 @@ def test_sampled_block_generator():
     full = oracle.sliced_random(e, m, n, 7)
     win = oracle.sliced_random(e, 10, 64, 7, row0=20, col0=64, gcols=n)
     assert np.array_equal(win[:, :, 0], full[:, 20:30, 1])
+
+
+def _elements(words, e, m, n):
+    w = oracle.pack_width(e)
+    arr = np.zeros((m, n), dtype=np.uint16)
+    for j in range(n):
+        wd, s = divmod(j * w, 64)
+        arr[:, j] = ((words[:, wd] >> np.uint64(s)) & np.uint64((1 << w) - 1)).astype(np.uint16)
+    return arr
+
+
+def test_oracle_ple_vs_reference(golden):
+    # nj_ple restated in C (oracle/gf2e_oracle.c: orc_ple) against the reference's ple()
+    for tag in (str(t) for t in golden["ple_tags"]):
+        e, f, m, n = (int(x) for x in golden[f"{tag}/meta"])
+        a, P, Q, r = oracle.ple(e, f, _elements(golden[f"{tag}/A"], e, m, n))
+        assert r == int(golden[f"{tag}/rank"][0]), tag
+        assert np.array_equal(P, golden[f"{tag}/P"]) and np.array_equal(Q, golden[f"{tag}/Q"]), tag
+        assert np.array_equal(a, _elements(golden[f"{tag}/ple"], e, m, n)), tag
