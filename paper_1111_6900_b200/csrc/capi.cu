@@ -438,6 +438,10 @@ int check_flags(uint32_t flags) {
     return GF2E_OK;
 }
 
+int trsm_impl(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, int64_t ldt, int64_t pt, uint64_t *B,
+              int64_t ldb, int64_t pb, int64_t m, int64_t n, void *ws, int64_t ws_bytes, void *stream,
+              int64_t *bad_row, bool check);
+
 // ---- PLE / echelonize over plane views (consumers of run_product and the TRSM) ----------------
 // Stream-ordered temporaries from the CUDA memory pool (freed at scope exit, reused by the pool).
 struct DevTmp {
@@ -462,14 +466,24 @@ struct PleCtx {
     cudaStream_t st;
     PanelOut *pout;  // device
     int64_t *idx;    // device index scratch (3 * max(m, n) + 3 entries)
+    const FieldTab *tab;
     int64_t panels = 0;
+    static constexpr int kRing = 4;
+    int64_t *ring[kRing] = {};  // pinned staging, 3 * max(m, n) + 3 entries each
+    cudaEvent_t ring_ev[kRing] = {};
+    int ring_next = 0;
 };
 
 // host vector -> device index scratch (synchronous staging: the host buffer may be reused)
+// Upload through a ring of pinned staging slots (an event guards each slot's reuse), so the
+// copies stay asynchronous; the device index buffer itself is reused in stream order.
 int put_idx(PleCtx &c, const std::vector<int64_t> &v) {
     if (v.empty()) return GF2E_OK;
-    CKH(cudaMemcpyAsync(c.idx, v.data(), v.size() * 8, cudaMemcpyHostToDevice, c.st), "cudaMemcpyAsync");
-    CKH(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+    const int slot = c.ring_next++ % PleCtx::kRing;
+    CKH(cudaEventSynchronize(c.ring_ev[slot]), "cudaEventSynchronize");
+    std::memcpy(c.ring[slot], v.data(), v.size() * 8);
+    CKH(cudaMemcpyAsync(c.idx, c.ring[slot], v.size() * 8, cudaMemcpyHostToDevice, c.st), "cudaMemcpyAsync");
+    CKH(cudaEventRecord(c.ring_ev[slot], c.st), "cudaEventRecord");
     return GF2E_OK;
 }
 
@@ -484,7 +498,7 @@ int ple_rec(PleCtx &c, int64_t r0, int64_t c0, int64_t m, int64_t n, int64_t *P,
     if (m == 0 || n == 0) return GF2E_OK;
     uint64_t *V = c.S + r0 * c.ld + c0 / 64;
     if (n <= kPlePanel) {  // base case nj_ple (newton_john.py:207-260) on one plane word
-        CK(launch_ple_panel(c.e, c.f, V, c.ld, c.ps, m, (int)n, c.pout, c.st), "ple_panel");
+        CK(launch_ple_panel(c.e, c.tab, V, c.ld, c.ps, m, (int)n, c.pout, c.st), "ple_panel");
         g_launches += m > 512 ? 2 : 1;
         ++c.panels;
         PanelOut h;
@@ -519,7 +533,7 @@ int ple_rec(PleCtx &c, int64_t r0, int64_t c0, int64_t m, int64_t n, int64_t *P,
         DevTmp tw((size_t)(tws > 0 ? tws : 256), c.st);
         if (!tw.p) return fail(GF2E_ENOMEM, "out of device memory (PLE trsm workspace)");
         int64_t bad = -1;
-        if (int rc = gf2e_trsm(c.e, c.f, 0, 0, L, lw, r1 * lw, R, c.ld, c.ps, r1, nr, tw.p, tws, c.st, &bad))
+        if (int rc = trsm_impl(c.e, c.f, 0, 0, L, lw, r1 * lw, R, c.ld, c.ps, r1, nr, tw.p, tws, c.st, &bad, false))
             return rc;
         if (m - r1 > 0) {  // right[r1:] ^= left[r1:, :r1] . right[:r1]  (ple_echelon.py:259-260)
             const int64_t mws = gf2e_slice_mul_workspace(c.e, c.f, m - r1, r1, nr, GF2E_ACCUMULATE);
@@ -565,8 +579,25 @@ int ple_top(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, i
     DevTmp po(sizeof(PanelOut), st);
     DevTmp ix((size_t)(3 * (m > n ? m : n) + 3) * 8, st);
     if (!po.p || !ix.p) return fail(GF2E_ENOMEM, "out of device memory (PLE scratch)");
+    const FieldTab *tab = field_tab(e, f, primitive_element(e, f));
+    if (!tab) return fail(GF2E_ECUDA, "field table upload failed");
     PleCtx c{e, f, to_kernel_sched(e, get_schedule(e, f)), S, ld, ps, st, static_cast<PanelOut *>(po.p),
-             static_cast<int64_t *>(ix.p)};
+             static_cast<int64_t *>(ix.p), tab};
+    const size_t ring_bytes = (size_t)(3 * (m > n ? m : n) + 3) * 8;
+    struct RingGuard {
+        PleCtx &c;
+        ~RingGuard() {
+            for (int i = 0; i < PleCtx::kRing; ++i) {
+                if (c.ring_ev[i]) cudaEventSynchronize(c.ring_ev[i]), cudaEventDestroy(c.ring_ev[i]);
+                if (c.ring[i]) cudaFreeHost(c.ring[i]);
+            }
+        }
+    } guard{c};
+    for (int i = 0; i < PleCtx::kRing; ++i) {
+        if (cudaMallocHost(reinterpret_cast<void **>(&c.ring[i]), ring_bytes) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c.ring_ev[i], cudaEventDisableTiming) != cudaSuccess)
+            return fail(GF2E_ENOMEM, "out of pinned host memory (PLE staging)");
+    }
     std::vector<int64_t> hp(k), hq(k);
     int64_t r = 0;
     if (int rc = ple_rec(c, 0, 0, m, n, hp.data(), hq.data(), r)) return rc;
@@ -922,6 +953,14 @@ int64_t gf2e_trsm_workspace(int e, uint32_t f, int64_t m, int64_t n) {
 int gf2e_trsm(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, int64_t ldt, int64_t pt, uint64_t *B,
               int64_t ldb, int64_t pb, int64_t m, int64_t n, void *ws, int64_t ws_bytes, void *stream,
               int64_t *bad_row) {
+    return trsm_impl(e, f, upper, unit_diag, T, ldt, pt, B, ldb, pb, m, n, ws, ws_bytes, stream, bad_row, true);
+}
+}  // extern "C"
+
+namespace {
+int trsm_impl(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, int64_t ldt, int64_t pt, uint64_t *B,
+              int64_t ldb, int64_t pb, int64_t m, int64_t n, void *ws, int64_t ws_bytes, void *stream,
+              int64_t *bad_row, bool check) {
     g_err.clear();
     g_launches = 0;
     if (bad_row) *bad_row = -1;
@@ -948,8 +987,10 @@ int gf2e_trsm(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, in
     CK(launch_tri_inverse(e, f, primitive_element(e, f), T, ldt, pt, m, upper != 0, unit_diag != 0, inv, flag, st),
        "tri_inverse");
     int bad = big;
-    CKH(cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
-    CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (check) {  // PLE corners skip this: their diagonal is the (nonzero) pivots
+        CKH(cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+        CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    }
     if (bad != big) {
         if (bad_row) *bad_row = bad;
         return fail(GF2E_ESINGULAR, "zero diagonal entry at index %d", bad);
@@ -957,6 +998,9 @@ int gf2e_trsm(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, in
     TrsmCtx c{to_kernel_sched(e, S), upper != 0, T, ldt, pt, B, ldb, pb, n, inv, tmp, mulws, L.mul_bytes, e, st};
     return trsm_rec(c, 0, m);
 }
+}  // namespace
+
+extern "C" {
 
 int gf2e_mul_by_x(int e, uint32_t f, const uint64_t *in, int64_t ld, int64_t pin, uint64_t *out, int64_t pout,
                   int64_t rows, int64_t cols, void *stream) {

@@ -112,8 +112,15 @@ struct PanelOut {
     uint64_t dval[64][kMaxE];
     uint64_t bt[64 * kMaxE * kMaxE];  // alpha^s * T_t, [t][s][plane]
 };
-cudaError_t launch_ple_panel(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb, PanelOut *out,
-                             cudaStream_t st);
+// GF(2^e) tables for one field, in static device memory (kFieldTabSlots fields cached)
+constexpr int kFieldTabSlots = 16;
+struct FieldTab {
+    uint16_t ex[1024], lg[1024], inv[1024];  // exp/log over a primitive element; inverses
+    uint16_t mulmask[1024][kMaxE];           // bit p of [c][b] = coefficient b of c * x^p
+};
+const FieldTab *field_tab(int e, uint32_t f, uint32_t g);  // device pointer (synchronous fill)
+cudaError_t launch_ple_panel(int e, const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb,
+                             PanelOut *out, cudaStream_t st);
 cudaError_t launch_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t nwords, const int64_t *swaps,
                              int n, bool backward, cudaStream_t st);
 cudaError_t launch_col_swaps(int planes, int w, uint64_t *S, int64_t ld, int64_t ps, int64_t rows, const int64_t *trip,

@@ -25,6 +25,10 @@
 //   k_echelon_marks: echelonize's "drop L, set the implicit leading ones" (ple_echelon.py:364-370).
 //   k_gather_cols: pivot columns of the leading rows as an r x r matrix (_gather_columns,
 //     ple_echelon.py:338-340).
+#include <cstring>
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -34,63 +38,50 @@ namespace {
 __device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
 
+// ---- per-field constant tables (static module memory, filled once per (e, f)) ----------------
+__device__ FieldTab g_field_tabs[kFieldTabSlots];
+
 constexpr int PT = 512;  // phase-1 threads = window rows
 constexpr int KP = 64;   // pivots per panel (one plane word)
 
-__device__ __forceinline__ uint32_t elem(const uint64_t *v, int e, int c) {
-    uint32_t x = 0;
-    for (int b = 0; b < e; ++b) x |= (uint32_t)((v[b] >> c) & 1ULL) << b;
-    return x;
-}
-// v <- alpha * v on one sliced word per plane (x^e = f - x^e folded into the low planes)
-__device__ __forceinline__ void mul_alpha(uint64_t *v, int e, uint32_t f) {
-    const uint64_t top = v[e - 1];
-    for (int b = e - 1; b > 0; --b) v[b] = v[b - 1] ^ (((f >> b) & 1u) ? top : 0ULL);
-    v[0] = ((f & 1u) ? top : 0ULL);
-}
-__device__ uint32_t gf_mul_s(uint32_t a, uint32_t b, int e, uint32_t f) {
-    uint32_t acc = 0;
-    for (int i = 0; i < e; ++i)
-        if ((b >> i) & 1u) acc ^= a << i;
-    for (int d = 2 * e - 2; d >= e; --d)
-        if ((acc >> d) & 1u) acc ^= f << (d - e);
-    return acc;
-}
-__device__ uint32_t gf_inv_s(uint32_t a, int e, uint32_t f) {  // a^(2^e - 2)
-    uint32_t r = 1, p = a;
-    uint32_t n = (1u << e) - 2;
-    while (n) {
-        if (n & 1u) r = gf_mul_s(r, p, e, f);
-        p = gf_mul_s(p, p, e, f);
-        n >>= 1;
-    }
-    return r;
-}
-// row ^= x * T_t  with Bt = alpha^s * T_t (s = 0..e-1), one word per plane
-__device__ __forceinline__ void apply_step(uint64_t *v, int e, uint32_t x, const uint64_t *bt) {
-    for (int s = 0; s < e; ++s)
-        if ((x >> s) & 1u)
-            for (int b = 0; b < e; ++b) v[b] ^= bt[s * kMaxE + b];
-}
 __device__ __forceinline__ uint64_t swap_bits(uint64_t w, int a, int b) {
     const uint64_t d = ((w >> a) ^ (w >> b)) & 1ULL;
     return w ^ (d << a) ^ (d << b);
 }
 
-__global__ void __launch_bounds__(PT) k_ple_find(int e, uint32_t f, uint64_t *__restrict__ S, int64_t ld, int64_t ps,
-                                                 int64_t m, int nb, PanelOut *__restrict__ out) {
+template <int E>
+__device__ __forceinline__ uint32_t elemE(const uint64_t *v, int c) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int b = 0; b < E; ++b) x |= (uint32_t)((v[b] >> c) & 1ULL) << b;
+    return x;
+}
+// v ^= x * T_t, bt = [alpha^s * T_t][plane]
+template <int E>
+__device__ __forceinline__ void stepE(uint64_t *v, uint32_t x, const uint64_t *bt) {
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+        const uint64_t sel = 0ULL - (uint64_t)((x >> s) & 1u);
+#pragma unroll
+        for (int b = 0; b < E; ++b) v[b] ^= bt[s * E + b] & sel;
+    }
+}
+
+template <int E>
+__global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ tab, uint64_t *__restrict__ S, int64_t ld,
+                                                 int64_t ps, int64_t m, int nb, PanelOut *__restrict__ out) {
     extern __shared__ __align__(16) uint8_t smem[];
-    uint64_t *win = reinterpret_cast<uint64_t *>(smem);                 // [PT][kMaxE]
-    uint64_t *bt = win + PT * kMaxE;                                    // [KP][kMaxE][kMaxE]
-    uint64_t *ext = bt + KP * kMaxE * kMaxE;                            // [kMaxE] scanned pivot row
-    int64_t *worig = reinterpret_cast<int64_t *>(ext + kMaxE);          // [PT] original row of a slot
-    int64_t *dpos = worig + PT;                                         // [KP] displaced positions
-    int64_t *dorig = dpos + KP;                                         // [KP]
-    int *dstep = reinterpret_cast<int *>(dorig + KP);                   // [KP]
+    uint64_t *win = reinterpret_cast<uint64_t *>(smem);  // [PT][E]
+    uint64_t *bt = win + PT * E;                         // [KP][E][E]
+    uint16_t *sinv = reinterpret_cast<uint16_t *>(bt + KP * E * E);  // [2^E] inverses
+    uint16_t *smk = sinv + (1 << E);                                   // [2^E][E] multiplication matrices
+    __shared__ uint64_t ext[kMaxE], sT[kMaxE], sF[kMaxE];
     __shared__ uint64_t s_dval[KP][kMaxE];
-    __shared__ int s_jcol[KP];
+    __shared__ int64_t dpos[KP];
+    __shared__ int dstep[KP], s_jcol[KP];
     __shared__ int64_t s_P[KP], s_Q[KP];
     __shared__ int s_min, s_nd, s_supp_ok;
+    __shared__ uint32_t s_inv;
     __shared__ unsigned long long s_supp;
     __shared__ int64_t s_pmin;
 
@@ -98,168 +89,204 @@ __global__ void __launch_bounds__(PT) k_ple_find(int e, uint32_t f, uint64_t *__
     const int W = (int)(m < PT ? m : PT);
     const uint64_t cmask = nb >= 64 ? ~0ULL : ((1ULL << nb) - 1);
     const int k = (int)(m < nb ? m : nb);
-    for (int s = tid; s < W; s += PT) {
-        for (int b = 0; b < e; ++b) win[s * kMaxE + b] = S[b * ps + s * ld] & cmask;
-        worig[s] = s;
-    }
     if (tid == 0) {
         s_nd = 0;
         s_supp_ok = 0;
         s_supp = 0;
+        s_min = 0x7fffffff;
+    }
+    for (int i = tid; i < (1 << E); i += PT) {
+        sinv[i] = tab->inv[i];
+#pragma unroll
+        for (int b = 0; b < E; ++b) smk[i * E + b] = tab->mulmask[i][b];
+    }
+    __syncthreads();
+    for (int s = tid; s < W; s += PT) {
+        uint64_t any = 0;
+#pragma unroll
+        for (int b = 0; b < E; ++b) {
+            const uint64_t x = S[b * ps + s * ld] & cmask;
+            win[s * E + b] = x;
+            any |= x;
+        }
+        if (any & 1ULL) atomicMin(&s_min, s);  // candidates for column 0
     }
     __syncthreads();
     int r = 0;
     for (int j = 0; j < nb && r < k; ++j) {
+        int64_t ipos = s_min;
+        __syncthreads();
         if (tid == 0) {
-            s_min = 0x7fffffff;
+            s_min = 0x7fffffff;  // candidates for column j + 1 (collected in the elimination)
             s_pmin = INT64_MAX;
         }
-        __syncthreads();
-        for (int s = r + tid; s < W; s += PT) {
-            uint64_t any = 0;
-            for (int b = 0; b < e; ++b) any |= win[s * kMaxE + b];
-            if ((any >> j) & 1ULL) atomicMin(&s_min, s);
-        }
-        __syncthreads();
-        int64_t ipos = s_min;
-        if (s_min == 0x7fffffff && W < m) {
+        if (ipos == 0x7fffffff && W < m) {
             // Column support of the rows below the window: their original bits OR the scaled
             // pivot suffixes (the only things ever XOR-ed into them).  Computed at the first
             // miss; a column outside it has no pivot below the window either.
             if (!s_supp_ok) {
                 uint64_t acc = 0;
                 for (int64_t p = W + tid; p < m; p += PT)
-                    for (int b = 0; b < e; ++b) acc |= S[b * ps + p * ld];
+#pragma unroll
+                    for (int b = 0; b < E; ++b) acc |= S[b * ps + p * ld];
                 if (acc) atomicOr(&s_supp, acc & cmask);
                 for (int t = tid; t < r; t += PT)
-                    for (int b = 0; b < e; ++b) atomicOr(&s_supp, bt[t * kMaxE * kMaxE + b]);
+#pragma unroll
+                    for (int b = 0; b < E; ++b) atomicOr(&s_supp, bt[t * E * E + b]);
                 __syncthreads();
                 if (tid == 0) s_supp_ok = 1;
             }
             __syncthreads();
-            if (!((s_supp >> j) & 1ULL)) continue;  // uniform
-        }
-        if (s_min == 0x7fffffff) {
-            // no pivot in the window: scan the rows below it, reducing each candidate lazily
-            const int nd = s_nd;
-            for (int64_t base = W; base < m; base += PT) {
-                const int64_t p = base + tid;
-                uint64_t v[kMaxE];
-                bool hit = false;
-                if (p < m) {
-                    int st0 = 0, di = -1;
-                    for (int d = 0; d < nd; ++d)
-                        if (dpos[d] == p) di = d;
-                    if (di >= 0) {
-                        for (int b = 0; b < e; ++b) v[b] = s_dval[di][b];
-                        st0 = dstep[di];
-                    } else {
-                        for (int b = 0; b < e; ++b) v[b] = S[b * ps + p * ld] & cmask;
+            if ((s_supp >> j) & 1ULL) {
+                // scan the rows below the window, reducing each candidate lazily
+                const int nd = s_nd;
+                for (int64_t base = W; base < m; base += PT) {
+                    const int64_t p = base + tid;
+                    uint64_t v[E];
+                    bool hit = false;
+                    if (p < m) {
+                        int st0 = 0, di = -1;
+                        for (int d = 0; d < nd; ++d)
+                            if (dpos[d] == p) di = d;
+                        if (di >= 0) {
+#pragma unroll
+                            for (int b = 0; b < E; ++b) v[b] = s_dval[di][b];
+                            st0 = dstep[di];
+                        } else {
+#pragma unroll
+                            for (int b = 0; b < E; ++b) v[b] = S[b * ps + p * ld] & cmask;
+                        }
+                        for (int t = st0; t < r; ++t) stepE<E>(v, elemE<E>(v, s_jcol[t]), bt + t * E * E);
+                        uint64_t any = 0;
+#pragma unroll
+                        for (int b = 0; b < E; ++b) any |= v[b];
+                        hit = (any >> j) & 1ULL;
+                        if (hit) atomicMin((unsigned long long *)&s_pmin, (unsigned long long)p);
                     }
-                    for (int t = st0; t < r; ++t) apply_step(v, e, elem(v, e, s_jcol[t]), bt + t * kMaxE * kMaxE);
-                    uint64_t any = 0;
-                    for (int b = 0; b < e; ++b) any |= v[b];
-                    hit = (any >> j) & 1ULL;
-                    if (hit) atomicMin((unsigned long long *)&s_pmin, (unsigned long long)p);
+                    __syncthreads();
+                    if (hit && s_pmin == p)
+#pragma unroll
+                        for (int b = 0; b < E; ++b) ext[b] = v[b];
+                    __syncthreads();
+                    if (s_pmin != INT64_MAX) break;
                 }
-                __syncthreads();
-                if (hit && s_pmin == p)
-                    for (int b = 0; b < e; ++b) ext[b] = v[b];
-                __syncthreads();
-                if (s_pmin != INT64_MAX) break;
+                ipos = s_pmin;
             }
-            ipos = s_pmin;
-            if (ipos == INT64_MAX) continue;  // uniform: no pivot in column j
+        }
+        if (ipos == 0x7fffffff || ipos == INT64_MAX) {
+            // no pivot in column j: collect the window's candidates for column j + 1
+            __syncthreads();
+            if (j + 1 < nb)
+                for (int s = r + tid; s < W; s += PT) {
+                    uint64_t any = 0;
+#pragma unroll
+                    for (int b = 0; b < E; ++b) any |= win[s * E + b];
+                    if ((any >> (j + 1)) & 1ULL) atomicMin(&s_min, s);
+                }
+            __syncthreads();
+            continue;
         }
         if (tid == 0) {
-            uint64_t *pr = win + r * kMaxE;
+            uint64_t *pr = win + r * E;
             if (ipos < W) {
                 const int i = (int)ipos;
-                if (i != r) {
-                    for (int b = 0; b < e; ++b) {
+                if (i != r)
+#pragma unroll
+                    for (int b = 0; b < E; ++b) {
                         const uint64_t t = pr[b];
-                        pr[b] = win[i * kMaxE + b];
-                        win[i * kMaxE + b] = t;
+                        pr[b] = win[i * E + b];
+                        win[i * E + b] = t;
                     }
-                    const int64_t o = worig[r];
-                    worig[r] = worig[i];
-                    worig[i] = o;
-                }
             } else {
                 // the row at position r moves below the window: remember it (reduced by steps < r)
                 int di = -1;
                 for (int d = 0; d < s_nd; ++d)
                     if (dpos[d] == ipos) di = d;
-                int64_t porig = ipos;
-                if (di < 0) {
-                    di = s_nd++;
-                } else {
-                    porig = dorig[di];
-                }
+                if (di < 0) di = s_nd++;
                 dpos[di] = ipos;
-                dorig[di] = worig[r];
                 dstep[di] = r;
-                for (int b = 0; b < e; ++b) {
+#pragma unroll
+                for (int b = 0; b < E; ++b) {
                     s_dval[di][b] = pr[b];
                     pr[b] = ext[b];
                 }
-                worig[r] = porig;
             }
             s_P[r] = ipos;
             s_Q[r] = j;
             s_jcol[r] = j;
-            // scale the pivot row right of j by 1/pivot; the pivot entry stays (diagonal of L)
-            const uint32_t piv = elem(pr, e, j);
-            const uint32_t inv = gf_inv_s(piv, e, f);
-            const uint64_t sm = (j >= 63 ? 0ULL : (~0ULL << (j + 1))) & cmask;
-            uint64_t cur[kMaxE], acc[kMaxE];
-            for (int b = 0; b < e; ++b) {
-                cur[b] = pr[b] & sm;
-                acc[b] = 0;
-            }
-            for (int s = 0; s < e; ++s) {
-                if ((inv >> s) & 1u)
-                    for (int b = 0; b < e; ++b) acc[b] ^= cur[b];
-                mul_alpha(cur, e, f);
-            }
-            for (int b = 0; b < e; ++b) {
-                pr[b] = (pr[b] & ~sm) | acc[b];
-                cur[b] = acc[b];
-            }
-            if (s_supp_ok)
-                for (int b = 0; b < e; ++b) s_supp |= cur[b];
-            uint64_t *btr = bt + r * kMaxE * kMaxE;
-            for (int s = 0; s < e; ++s) {
-                for (int b = 0; b < e; ++b) btr[s * kMaxE + b] = cur[b];
-                mul_alpha(cur, e, f);
-            }
+            s_inv = sinv[elemE<E>(pr, j)];
         }
         __syncthreads();
-        const uint64_t *btr = bt + r * kMaxE * kMaxE;
+        // scale the pivot row right of j by 1/pivot (the pivot stays as L's diagonal):
+        // plane b of c * v is the XOR of the planes p in mulmask[c][b]
+        const uint64_t sm = (j >= 63 ? 0ULL : (~0ULL << (j + 1))) & cmask;
+        if (tid < E) {
+            const uint32_t mk = smk[s_inv * E + tid];
+            const uint64_t *pr = win + r * E;
+            uint64_t acc = 0;
+#pragma unroll
+            for (int p = 0; p < E; ++p)
+                if ((mk >> p) & 1u) acc ^= pr[p] & sm;
+            sT[tid] = acc;
+            sF[tid] = (pr[tid] & ~sm) | acc;
+        }
+        __syncthreads();
+        if (tid < E * E) {  // basis alpha^s * T (s = tid / E, plane tid % E)
+            const int sidx = tid / E, b = tid % E;
+            const uint32_t mk = smk[(1u << sidx) * E + b];
+            uint64_t acc = 0;
+#pragma unroll
+            for (int p = 0; p < E; ++p)
+                if ((mk >> p) & 1u) acc ^= sT[p];
+            bt[r * E * E + tid] = acc;
+        }
+        if (tid < E) win[r * E + tid] = sF[tid];
+        if (tid == 0 && s_supp_ok)
+#pragma unroll
+            for (int b = 0; b < E; ++b) s_supp |= sT[b];
+        __syncthreads();
+        const uint64_t *btr = bt + r * E * E;
+        const bool next = j + 1 < nb;
         for (int s = r + 1 + tid; s < W; s += PT) {
-            uint64_t *v = win + s * kMaxE;
-            const uint32_t x = elem(v, e, j);
-            if (x) apply_step(v, e, x, btr);
+            uint64_t v[E];
+#pragma unroll
+            for (int b = 0; b < E; ++b) v[b] = win[s * E + b];
+            const uint32_t x = elemE<E>(v, j);
+            if (x) {
+                stepE<E>(v, x, btr);
+#pragma unroll
+                for (int b = 0; b < E; ++b) win[s * E + b] = v[b];
+            }
+            if (next) {
+                uint64_t any = 0;
+#pragma unroll
+                for (int b = 0; b < E; ++b) any |= v[b];
+                if ((any >> (j + 1)) & 1ULL) atomicMin(&s_min, s);
+            }
         }
         ++r;
         __syncthreads();
     }
+    __syncthreads();
     // L compression of the base case (newton_john.py:257-259) and write-back of the window
     for (int s = tid; s < W; s += PT) {
-        uint64_t v[kMaxE];
-        for (int b = 0; b < e; ++b) v[b] = win[s * kMaxE + b];
+        uint64_t v[E];
+#pragma unroll
+        for (int b = 0; b < E; ++b) v[b] = win[s * E + b];
         for (int t = 0; t < r && t <= s; ++t) {
             const int q = (int)s_Q[t];
             if (q != t)
-                for (int b = 0; b < e; ++b) v[b] = swap_bits(v[b], t, q);
+#pragma unroll
+                for (int b = 0; b < E; ++b) v[b] = swap_bits(v[b], t, q);
         }
-        for (int b = 0; b < e; ++b) {
+#pragma unroll
+        for (int b = 0; b < E; ++b) {
             uint64_t *d = S + b * ps + s * ld;
             *d = (*d & ~cmask) | v[b];
         }
     }
     // outputs for phase 2 and the host
-    for (int i = tid; i < r * kMaxE * kMaxE; i += PT) out->bt[i] = bt[i];
+    for (int i = tid; i < r * E * E; i += PT) out->bt[i] = bt[i];
     if (tid < r) {
         out->P[tid] = s_P[tid];
         out->Q[tid] = s_Q[tid];
@@ -268,7 +295,8 @@ __global__ void __launch_bounds__(PT) k_ple_find(int e, uint32_t f, uint64_t *__
     if (tid < s_nd) {
         out->dpos[tid] = dpos[tid];
         out->dstep[tid] = dstep[tid];
-        for (int b = 0; b < e; ++b) out->dval[tid][b] = s_dval[tid][b];
+#pragma unroll
+        for (int b = 0; b < E; ++b) out->dval[tid][b] = s_dval[tid][b];
     }
     if (tid == 0) {
         out->rank = r;
@@ -278,10 +306,11 @@ __global__ void __launch_bounds__(PT) k_ple_find(int e, uint32_t f, uint64_t *__
 }
 
 // phase 2: rows at positions >= window apply the panel's eliminations and the L compression
-__global__ void __launch_bounds__(256) k_ple_apply(int e, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t m,
-                                                   int nb, const PanelOut *__restrict__ in) {
+template <int E>
+__global__ void __launch_bounds__(256) k_ple_apply(uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t m, int nb,
+                                                   const PanelOut *__restrict__ in) {
     extern __shared__ __align__(16) uint8_t smem2[];
-    uint64_t *bt = reinterpret_cast<uint64_t *>(smem2);  // [KP][kMaxE][kMaxE]
+    uint64_t *bt = reinterpret_cast<uint64_t *>(smem2);  // [KP][E][E]
     __shared__ int jc[KP], qc[KP];
     __shared__ int r_s, nd_s, w_s;
     if (threadIdx.x == 0) {
@@ -291,7 +320,7 @@ __global__ void __launch_bounds__(256) k_ple_apply(int e, uint64_t *__restrict__
     }
     __syncthreads();
     const int r = r_s, nd = nd_s;
-    for (int i = threadIdx.x; i < r * kMaxE * kMaxE; i += blockDim.x) bt[i] = in->bt[i];
+    for (int i = threadIdx.x; i < r * E * E; i += blockDim.x) bt[i] = in->bt[i];
     for (int i = threadIdx.x; i < r; i += blockDim.x) {
         jc[i] = in->jcol[i];
         qc[i] = (int)in->Q[i];
@@ -299,21 +328,25 @@ __global__ void __launch_bounds__(256) k_ple_apply(int e, uint64_t *__restrict__
     __syncthreads();
     const uint64_t cmask = nb >= 64 ? ~0ULL : ((1ULL << nb) - 1);
     for (int64_t p = w_s + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t v[kMaxE];
+        uint64_t v[E];
         int st0 = 0, di = -1;
         for (int d = 0; d < nd; ++d)
             if (in->dpos[d] == p) di = d;
         if (di >= 0) {
-            for (int b = 0; b < e; ++b) v[b] = in->dval[di][b];
+#pragma unroll
+            for (int b = 0; b < E; ++b) v[b] = in->dval[di][b];
             st0 = in->dstep[di];
         } else {
-            for (int b = 0; b < e; ++b) v[b] = S[b * ps + p * ld] & cmask;
+#pragma unroll
+            for (int b = 0; b < E; ++b) v[b] = S[b * ps + p * ld] & cmask;
         }
-        for (int t = st0; t < r; ++t) apply_step(v, e, elem(v, e, jc[t]), bt + t * kMaxE * kMaxE);
+        for (int t = st0; t < r; ++t) stepE<E>(v, elemE<E>(v, jc[t]), bt + t * E * E);
         for (int t = 0; t < r; ++t)
             if (qc[t] != t)
-                for (int b = 0; b < e; ++b) v[b] = swap_bits(v[b], t, qc[t]);
-        for (int b = 0; b < e; ++b) {
+#pragma unroll
+                for (int b = 0; b < E; ++b) v[b] = swap_bits(v[b], t, qc[t]);
+#pragma unroll
+        for (int b = 0; b < E; ++b) {
             uint64_t *d = S + b * ps + p * ld;
             *d = (*d & ~cmask) | v[b];
         }
@@ -416,23 +449,79 @@ inline int grid_for(int64_t total, int threads) {
 
 }  // namespace
 
-size_t ple_find_smem() {
-    return (size_t)PT * kMaxE * 8 + (size_t)KP * kMaxE * kMaxE * 8 + kMaxE * 8 + PT * 8 + 2 * KP * 8 + KP * 4;
-}
-
-cudaError_t launch_ple_panel(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb, PanelOut *out,
-                             cudaStream_t st) {
-    const size_t smem = ple_find_smem();
-    cudaError_t err = cudaFuncSetAttribute(k_ple_find, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int E>
+cudaError_t launch_ple_e(const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb, PanelOut *out,
+                         cudaStream_t st) {
+    const int smem = (PT * E + KP * E * E) * 8 + (1 << E) * (E + 1) * 2;
+    cudaError_t err = cudaFuncSetAttribute(k_ple_find<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    k_ple_find<<<1, PT, smem, st>>>(e, f, S, ld, ps, m, nb, out);
+    k_ple_find<E><<<1, PT, smem, st>>>(tab, S, ld, ps, m, nb, out);
     err = cudaGetLastError();
     if (err != cudaSuccess || m <= PT) return err;
-    const int smem2 = KP * kMaxE * kMaxE * 8;
-    err = cudaFuncSetAttribute(k_ple_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    const int smem2 = KP * E * E * 8;
+    err = cudaFuncSetAttribute(k_ple_apply<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
     if (err != cudaSuccess) return err;
-    k_ple_apply<<<grid_for(m - PT, 256), 256, smem2, st>>>(e, S, ld, ps, m, nb, out);
+    k_ple_apply<E><<<grid_for(m - PT, 256), 256, smem2, st>>>(S, ld, ps, m, nb, out);
     return cudaGetLastError();
+}
+
+cudaError_t launch_ple_panel(int e, const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb,
+                             PanelOut *out, cudaStream_t st) {
+    switch (e) {
+        case 2: return launch_ple_e<2>(tab, S, ld, ps, m, nb, out, st);
+        case 3: return launch_ple_e<3>(tab, S, ld, ps, m, nb, out, st);
+        case 4: return launch_ple_e<4>(tab, S, ld, ps, m, nb, out, st);
+        case 5: return launch_ple_e<5>(tab, S, ld, ps, m, nb, out, st);
+        case 6: return launch_ple_e<6>(tab, S, ld, ps, m, nb, out, st);
+        case 7: return launch_ple_e<7>(tab, S, ld, ps, m, nb, out, st);
+        case 8: return launch_ple_e<8>(tab, S, ld, ps, m, nb, out, st);
+        case 9: return launch_ple_e<9>(tab, S, ld, ps, m, nb, out, st);
+        case 10: return launch_ple_e<10>(tab, S, ld, ps, m, nb, out, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// host: gf(2^e) tables over a primitive element g; mulmask[c][b] bit p = coefficient b of c*x^p
+static uint32_t gf_mul_h(uint32_t a, uint32_t b, int e, uint32_t f) {
+    uint32_t acc = 0;
+    for (int i = 0; i < e; ++i)
+        if ((b >> i) & 1u) acc ^= a << i;
+    for (int d = 2 * e - 2; d >= e; --d)
+        if ((acc >> d) & 1u) acc ^= f << (d - e);
+    return acc;
+}
+
+const FieldTab *field_tab(int e, uint32_t f, uint32_t g) {
+    static std::mutex mu;
+    static std::map<std::pair<int, uint32_t>, int> slots;
+    static int next = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    FieldTab *base = nullptr;
+    if (cudaGetSymbolAddress(reinterpret_cast<void **>(&base), g_field_tabs) != cudaSuccess) return nullptr;
+    auto it = slots.find({e, f});
+    if (it != slots.end()) return base + it->second;
+    const int slot = next++ % kFieldTabSlots;
+    for (auto i = slots.begin(); i != slots.end();)
+        i = (i->second == slot) ? slots.erase(i) : std::next(i);
+    static FieldTab h;
+    std::memset(&h, 0, sizeof(h));
+    const uint32_t q1 = (1u << e) - 1;
+    uint32_t v = 1;
+    for (uint32_t i = 0; i < q1; ++i) {
+        h.ex[i] = (uint16_t)v;
+        h.lg[v] = (uint16_t)i;
+        v = gf_mul_h(v, g, e, f);
+    }
+    for (uint32_t a = 1; a <= q1; ++a) h.inv[a] = h.ex[(q1 - h.lg[a]) % q1];
+    for (uint32_t c = 0; c <= q1; ++c)
+        for (int p = 0; p < e; ++p) {
+            const uint32_t prod = gf_mul_h(c, 1u << p, e, f);
+            for (int b = 0; b < e; ++b)
+                if ((prod >> b) & 1u) h.mulmask[c][b] |= (uint16_t)(1u << p);
+        }
+    if (cudaMemcpyToSymbol(g_field_tabs, &h, sizeof(h), slot * sizeof(FieldTab)) != cudaSuccess) return nullptr;
+    slots[{e, f}] = slot;
+    return base + slot;
 }
 
 cudaError_t launch_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t nwords, const int64_t *swaps,

@@ -4,7 +4,8 @@
 //     updates are all addmul calls into the tensor-core product kernel);
 //   * k_mul_by_x: sliced multiplication by alpha (mat_sliced.py:109-122);
 //   * k_scalar_mul: packed multiplication by a scalar (mat_packed.py:192-199).
-// Field arithmetic uses exp/log tables over a primitive element g, built in shared memory.
+// Field arithmetic uses the per-field tables of ple.cu (field_tab: inverses, multiplication
+// matrices; the scalar kernels build their own small tables).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -21,91 +22,108 @@ __device__ __forceinline__ uint32_t gf_mul_slow(uint32_t a, uint32_t b, int e, u
     return acc;
 }
 
-struct Tables {
-    uint16_t ex[1024];
-    uint16_t lg[1024];
-};
-
-__device__ void build_tables(Tables &t, int e, uint32_t f, uint32_t g) {
-    if (threadIdx.x == 0) {
-        const int q1 = (1 << e) - 1;
-        uint32_t v = 1;
-        for (int i = 0; i < q1; ++i) {
-            t.ex[i] = (uint16_t)v;
-            t.lg[v] = (uint16_t)i;
-            v = gf_mul_slow(v, g, e, f);
-        }
-        t.lg[0] = 0;
-    }
-    __syncthreads();
-}
-
-__device__ __forceinline__ uint32_t gmul(const Tables &t, uint32_t a, uint32_t b, int q1) {
-    if (a == 0 || b == 0) return 0;
-    uint32_t s = (uint32_t)t.lg[a] + t.lg[b];
-    if (s >= (uint32_t)q1) s -= q1;
-    return t.ex[s];
-}
-__device__ __forceinline__ uint32_t ginv(const Tables &t, uint32_t a, int q1) {
-    uint32_t l = t.lg[a];
-    return t.ex[l == 0 ? 0 : q1 - l];
-}
-
 constexpr int TB = kTrsmBlock;  // 128
 
-// grid = number of diagonal blocks; 128 threads (thread j owns column j of the inverse)
-__global__ void __launch_bounds__(TB) k_tri_inverse(int e, uint32_t f, uint32_t g, const uint64_t *__restrict__ T,
+// Inverse of each 128 x 128 diagonal block by bitsliced substitution: thread k owns row k of
+// the block and of its inverse X (two words per plane each, in registers).  Lower triangular:
+// for i = 0 .. rows-1, thread i finalises X_i = T_ii^-1 X_i and publishes it; every thread
+// k > i then adds T_ki * X_i (T's own entries are the multipliers: X_k = T_kk^-1 (e_k -
+// sum_{i<k} T_ki X_i)).  Upper: the same from the bottom.  Scalar * bitsliced word uses the
+// field's multiplication matrices (FieldTab.mulmask: plane b of c*v = XOR of the planes in
+// mulmask[c][b]).
+template <int E>
+__global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__ ftab, const uint64_t *__restrict__ T,
                                                    int64_t ldt, int64_t pt, int64_t m, int upper, int unit,
                                                    uint64_t *__restrict__ Tinv, int *__restrict__ bad_row) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    Tables &tab = *reinterpret_cast<Tables *>(smem);
-    uint16_t *tb = reinterpret_cast<uint16_t *>(smem + sizeof(Tables));  // TB x TB elements of the block
-    uint16_t *xs = tb + TB * TB;                                          // TB x TB inverse
-    const int q1 = (1 << e) - 1;
+    __shared__ uint64_t pub[2][E];  // the published row X_i
+    __shared__ uint16_t sinv[1 << E], smk[(1 << E) * E];
+    for (int i = threadIdx.x; i < (1 << E); i += TB) {
+        sinv[i] = ftab->inv[i];
+#pragma unroll
+        for (int b = 0; b < E; ++b) smk[i * E + b] = ftab->mulmask[i][b];
+    }
+    __syncthreads();
     const int64_t r0 = (int64_t)blockIdx.x * TB;
     const int rows = (int)((m - r0) < TB ? (m - r0) : TB);
-    build_tables(tab, e, f, g);
-    // gather the block's elements from the planes (r0 is a multiple of 128: word aligned)
-    for (int idx = threadIdx.x; idx < TB * TB; idx += TB) {
-        const int i = idx / TB, j = idx % TB;
+    const int k = threadIdx.x;
+    uint64_t t[E][2], x[E][2];
+#pragma unroll
+    for (int b = 0; b < E; ++b)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            t[b][w] = 0;
+            x[b][w] = 0;
+        }
+    if (k < rows) {
+        const uint64_t *src = T + (r0 + k) * ldt + (r0 >> 6);
+        const int nw = (int)((r0 + TB <= m) ? 2 : ((rows + 63) >> 6));
+#pragma unroll
+        for (int b = 0; b < E; ++b)
+        {
+            t[b][0] = src[b * pt];
+            if (nw > 1) t[b][1] = src[b * pt + 1];
+        }
+        x[0][0] = (k < 64) ? (1ULL << k) : 0ULL;  // identity row
+        x[0][1] = (k < 64) ? 0ULL : (1ULL << (k - 64));
+    }
+    auto entry = [&](int c) {  // T[k][c] as a field element
         uint32_t v = 0;
-        if (i < rows && j < rows) {
-            const uint64_t *w = T + (r0 + i) * ldt + (r0 >> 6) + (j >> 6);
-            for (int b = 0; b < e; ++b) v |= (uint32_t)((w[b * pt] >> (j & 63)) & 1ULL) << b;
-        }
-        tb[idx] = (uint16_t)v;
-        xs[idx] = 0;
-    }
-    __syncthreads();
-    const int j = threadIdx.x;
-    if (!unit && j < rows && tb[j * TB + j] == 0) atomicMin(bad_row, (int)(r0 + j));
-    if (j < rows) {
-        if (upper) {
-            for (int i = j; i >= 0; --i) {  // column j of U^-1: rows j .. 0
-                uint32_t s = (i == j) ? 1u : 0u;
-                for (int k = i + 1; k <= j; ++k) s ^= gmul(tab, tb[i * TB + k], xs[k * TB + j], q1);
-                const uint32_t d = tb[i * TB + i];
-                xs[i * TB + j] = (uint16_t)(unit ? s : (d ? gmul(tab, s, ginv(tab, d, q1), q1) : 0));
+#pragma unroll
+        for (int b = 0; b < E; ++b) v |= (uint32_t)((((c >> 6) ? t[b][1] : t[b][0]) >> (c & 63)) & 1ULL) << b;
+        return v;
+    };
+    if (!unit && k < rows && entry(k) == 0) atomicMin(bad_row, (int)(r0 + k));
+    for (int step = 0; step < rows; ++step) {
+        const int i = upper ? rows - 1 - step : step;
+        if (k == i) {
+            uint32_t c = unit ? 1u : sinv[entry(i)];
+            if (c == 0) c = 1;  // singular block: reported above, result unused
+            uint64_t y[E][2];
+#pragma unroll
+            for (int b = 0; b < E; ++b) {
+                const uint32_t mk = smk[c * E + b];
+#pragma unroll
+                for (int w = 0; w < 2; ++w) {
+                    uint64_t acc = 0;
+#pragma unroll
+                    for (int p = 0; p < E; ++p) acc ^= x[p][w] & (0ULL - (uint64_t)((mk >> p) & 1u));
+                    y[b][w] = acc;
+                }
             }
-        } else {
-            for (int i = j; i < rows; ++i) {  // column j of L^-1: rows j .. rows-1
-                uint32_t s = (i == j) ? 1u : 0u;
-                for (int k = j; k < i; ++k) s ^= gmul(tab, tb[i * TB + k], xs[k * TB + j], q1);
-                const uint32_t d = tb[i * TB + i];
-                xs[i * TB + j] = (uint16_t)(unit ? s : (d ? gmul(tab, s, ginv(tab, d, q1), q1) : 0));
+#pragma unroll
+            for (int b = 0; b < E; ++b)
+#pragma unroll
+                for (int w = 0; w < 2; ++w) {
+                    x[b][w] = y[b][w];
+                    pub[w][b] = y[b][w];
+                }
+        }
+        __syncthreads();
+        const bool below = upper ? (k < i) : (k > i && k < rows);
+        if (below) {
+            const uint32_t c = entry(i);
+            if (c) {
+#pragma unroll
+                for (int b = 0; b < E; ++b) {
+                    const uint32_t mk = smk[c * E + b];
+#pragma unroll
+                    for (int w = 0; w < 2; ++w) {
+                        uint64_t acc = 0;
+#pragma unroll
+                        for (int p = 0; p < E; ++p) acc ^= pub[w][p] & (0ULL - (uint64_t)((mk >> p) & 1u));
+                        x[b][w] ^= acc;
+                    }
+                }
             }
         }
+        __syncthreads();
     }
-    __syncthreads();
-    // scatter into planes: Tinv block = e planes of TB rows x TB/64 words
-    uint64_t *out = Tinv + (int64_t)blockIdx.x * e * TB * (TB / 64);
-    for (int task = threadIdx.x; task < e * TB * (TB / 64); task += TB) {
-        const int b = task / (TB * (TB / 64)), rem = task % (TB * (TB / 64));
-        const int i = rem / (TB / 64), wq = rem % (TB / 64);
-        uint64_t word = 0;
-        for (int c = 0; c < 64; ++c) word |= (uint64_t)((xs[i * TB + wq * 64 + c] >> b) & 1u) << c;
-        out[(int64_t)b * TB * (TB / 64) + i * (TB / 64) + wq] = word;
-    }
+    // Tinv block = e planes of TB rows x TB/64 words
+    uint64_t *out = Tinv + (int64_t)blockIdx.x * E * TB * (TB / 64);
+#pragma unroll
+    for (int b = 0; b < E; ++b)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) out[(int64_t)b * TB * (TB / 64) + k * (TB / 64) + w] = (k < rows) ? x[b][w] : 0;
 }
 
 // mat_sliced.py:109-122: slices shift up one degree, the top slice folds into the slices
@@ -152,17 +170,33 @@ inline int grid_for(int64_t total, int threads) {
 
 }  // namespace
 
-size_t tri_inverse_smem() { return sizeof(Tables) + 2 * TB * TB * sizeof(uint16_t); }
+size_t tri_inverse_smem() { return 0; }
+
+template <int E>
+cudaError_t launch_tri_e(const FieldTab *ftab, const uint64_t *T, int64_t ldt, int64_t pt, int64_t m, bool upper,
+                         bool unit, uint64_t *Tinv, int *bad_row, int64_t nblk, cudaStream_t st) {
+    k_tri_inverse<E><<<(unsigned)nblk, TB, 0, st>>>(ftab, T, ldt, pt, m, upper ? 1 : 0, unit ? 1 : 0, Tinv, bad_row);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_tri_inverse(int e, uint32_t f, uint32_t g, const uint64_t *T, int64_t ldt, int64_t pt, int64_t m,
                                bool upper, bool unit, uint64_t *Tinv, int *bad_row, cudaStream_t st) {
+    const FieldTab *ftab = field_tab(e, f, g);
+    if (!ftab) return cudaErrorUnknown;
     const int64_t nblk = (m + TB - 1) / TB;
     if (nblk == 0) return cudaSuccess;
-    const size_t sm = tri_inverse_smem();
-    cudaError_t err = cudaFuncSetAttribute(k_tri_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (err != cudaSuccess) return err;
-    k_tri_inverse<<<(unsigned)nblk, TB, sm, st>>>(e, f, g, T, ldt, pt, m, upper ? 1 : 0, unit ? 1 : 0, Tinv, bad_row);
-    return cudaGetLastError();
+    switch (e) {
+        case 2: return launch_tri_e<2>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 3: return launch_tri_e<3>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 4: return launch_tri_e<4>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 5: return launch_tri_e<5>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 6: return launch_tri_e<6>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 7: return launch_tri_e<7>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 8: return launch_tri_e<8>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 9: return launch_tri_e<9>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 10: return launch_tri_e<10>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t launch_mul_by_x(int e, uint32_t f, const uint64_t *in, int64_t ld, int64_t pin, uint64_t *out,

@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--m", type=int, default=16384)
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--trsm-m", type=int, default=8192)
+    ap.add_argument("--ple-n", type=int, default=8192)
+    ap.add_argument("--skip-hbm", action="store_true")
     a = ap.parse_args()
     try:
         hbm = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -55,6 +57,8 @@ def main():
         d.update(extra or {})
         print(json.dumps(d), flush=True)
 
+    if a.skip_hbm:
+        return ple_lines(a, ctx)
     line("slice (K1)", timed(lambda: g.slice_packed(P, out=S)), packed_b + planes_b)
     line("cling (K2)", timed(lambda: g.cling(S, out=P)), packed_b + planes_b)
     line("mul_by_x", timed(lambda: g.mul_by_x(S)), 2 * planes_b)
@@ -82,6 +86,52 @@ def main():
                       "eff_Tbit-op/s": round(ops / (ms * 1e-3) / 1e12, 1),
                       "note": "K(e)*m^2*n GF(2) bit-ops; updates via addmul, 128-row diagonal blocks inverted on device"}),
           flush=True)
+
+
+def ple_lines(a, ctx):
+    """PLE / echelonize consumers: device time at n x n, and the oracle's nj_ple (C, all host
+    threads) at a size it finishes, for scale."""
+    import time
+
+    import oracle
+
+    e = ctx.e
+    n = a.ple_n
+    A = g.PackedMatrix.random(ctx, n, n, 11)
+    S0 = g.slice_packed(A)
+    S = S0.copy()
+
+    def run_ple():
+        S.planes.copy_(S0.planes)
+        g.ple_sliced(S)
+
+    ms = timed(run_ple, reps=2, warm=1)
+    K = g.count_products(e)
+    print(json.dumps({"op": "ple (sliced, in place)", "e": e, "m": n, "n": n, "ms": round(ms, 2),
+                      "eff_Tbit-op/s": round(K * 2 * n ** 3 / 3 / (ms * 1e-3) / 1e12, 1),
+                      "note": "work ~ K(e)*2n^3/3 GF(2) bit-ops (LU-like); 64-col panels on device, Schur "
+                              "updates via addmul, corner solves via device TRSM; host recursion syncs per panel"}),
+          flush=True)
+
+    def run_ech():
+        S.planes.copy_(S0.planes)
+        g.echelonize_sliced(S, True)
+
+    ms = timed(run_ech, reps=2, warm=1)
+    print(json.dumps({"op": "echelonize full (sliced)", "e": e, "m": n, "n": n, "ms": round(ms, 2)}), flush=True)
+    nc = 1024
+    arr = g.PackedMatrix.random(ctx, nc, nc, 11).to_array()
+    t0 = time.perf_counter()
+    oracle.ple(e, ctx.f, arr)
+    dt = time.perf_counter() - t0
+    B = g.slice_packed(g.PackedMatrix.random(ctx, nc, nc, 11))
+
+    def small():
+        g.ple_sliced(B)
+
+    ms_small = timed(small, reps=3, warm=1)
+    print(json.dumps({"op": "ple 1024^2 GPU vs oracle nj_ple (C)", "e": e, "gpu_ms": round(ms_small, 2),
+                      "cpu_ms": round(dt * 1e3, 1), "cpu_threads": oracle.max_threads()}), flush=True)
 
 
 if __name__ == "__main__":
