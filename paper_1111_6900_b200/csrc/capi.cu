@@ -240,13 +240,20 @@ struct Layout {
 
 int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 
-// Tensor-core form: fp4 (kind::mxf4, 2x the int8 rate) unless forced to int8; int8 for short
-// inner dimensions, where the single fp4 accumulator's per-product hand-off would dominate.
+// Tensor-core form: fp4 (kind::mxf4, 2x the int8 rate) unless forced to int8.  Below k = 2048
+// the single fp4 accumulator's per-product hand-off would dominate, so short inner dimensions
+// use the paired fp4 form (two products per TMEM drain) or int8 (double-buffered TMEM).
 constexpr int64_t kFp4MinK = 2048;
-bool use_fp4(uint32_t flags, int64_t k) {
-    if (flags & GF2E_TC_FP4) return true;
-    if (flags & GF2E_TC_INT8) return false;
-    return k >= kFp4MinK;
+constexpr int kSmallKForm = kFormI8;
+int tc_form(uint32_t flags, int64_t k) {
+    if (flags & GF2E_TC_INT8) return kFormI8;
+    if (k >= kFp4MinK) return kFormFp4;
+    if (flags & GF2E_TC_FP4) return kFormFp4Pair;
+    return kSmallKForm;
+}
+bool use_fp4(uint32_t flags, int64_t k) { return tc_form(flags, k) != kFormI8; }
+const char *form_name(int form) {
+    return form == kFormFp4Pair ? "k_product_tc2<fp4x2>" : form == kFormFp4 ? "k_product_tc2<fp4>" : "k_product_tc2<i8>";
 }
 
 Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags) {
@@ -312,8 +319,9 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
            "combos(B^T)");
         TcArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, m, n, L.m_pad, L.n_pad, C, ldc, pc, acc ? 1 : 0};
         ProfScope prof(st);
-        CK(launch_product_tc2(ks, a, fp4, st), "product_tc2");
-        g_kernel = fp4 ? "k_product_tc2<fp4>" : "k_product_tc2<i8>";
+        const int form = tc_form(flags, k);
+        CK(launch_product_tc2(ks, a, form, st), "product_tc2");
+        g_kernel = form_name(form);
     }
     return GF2E_OK;
 }
@@ -904,8 +912,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     CKH(cudaStreamWaitEvent(P.sc, ev_b, 0), "cudaStreamWaitEvent");
     CK(launch_slice(e, w, k, n, dBp, wb, dBs, nwn, k * nwn, P.sc), "slice(B)");
     const bool fp4 = use_fp4(0, k);
-    CK(launch_combos_bt(ks, dBs, nwn, k * nwn, k, n, dBt, LB.kwords, LB.b_pstride, LB.kwords, LB.n_pad / 64, fp4,
-                        P.sc),
+    CK(launch_combos_bt(ks, dBs, nwn, k * nwn, k, n, dBt, LB.kwords, LB.b_pstride, LB.kwords, LB.n_pad / 64, fp4, P.sc),
        "combos(B^T)");
     for (int64_t i = 0; i < nchunks; ++i) {
         const int sl = (int)(i % nslots);
@@ -923,7 +930,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
                   acc ? 1 : 0};
         {
             ProfScope prof(P.sc);
-            CK(launch_product_tc2(ks, ta, fp4, P.sc), "product_tc2");
+            CK(launch_product_tc2(ks, ta, tc_form(0, k), P.sc), "product_tc2");
         }
         CK(launch_cling(e, w, rows, n, dCs[sl], nwn, rows * nwn, dCp[sl], wb, P.sc), "cling(C)");
         CKH(cudaEventRecord(out_ready[sl], P.sc), "cudaEventRecord");
@@ -938,7 +945,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     float ms = 0;
     CKH(cudaEventElapsedTime(&ms, ev_t0, ev_t1), "cudaEventElapsedTime");
     if (device_ms) *device_ms = ms;
-    g_kernel = fp4 ? "k_product_tc2<fp4>" : "k_product_tc2<i8>";
+    g_kernel = form_name(tc_form(0, k));
     return GF2E_OK;
 }
 

@@ -411,7 +411,7 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
                 b[h][i] = (i < s.e && nb < nw && r1 < k) ? (B[i * pb + r1 * ldb + nb] & tm) : 0;
             }
         }
-        const int64_t ra = tc_b_row_inv(nb * 64 + lane), rb = tc_b_row_inv(nb * 64 + lane + 32);
+        const int64_t ra = tc_b_row_inv(nb * 64 + lane), rbw = tc_b_row_inv(nb * 64 + lane + 32);
         for (int t = 0; t < s.nprod; ++t) {
             const uint32_t sub = s.subset[t];
             uint64_t xa[2] = {0, 0}, xb[2] = {0, 0};
@@ -428,7 +428,7 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
             transpose64(xa[1], xb[1], lane);
             uint64_t *o = out + t * po;
             *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(ra, 2 * ks, ldo, kw)) = make_ulonglong2(xa[0], xa[1]);
-            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(rb, 2 * ks, ldo, kw)) = make_ulonglong2(xb[0], xb[1]);
+            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(rbw, 2 * ks, ldo, kw)) = make_ulonglong2(xb[0], xb[1]);
         }
     }
 }

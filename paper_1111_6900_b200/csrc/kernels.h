@@ -29,15 +29,8 @@ cudaError_t launch_reduce(int e, uint32_t f, uint64_t *planes, int64_t rows, int
 // words], so the expander's per-row 16-byte shared-memory reads are consecutive across a warp
 // (a [row][kw] layout makes the kw = 4 reads two-way bank-conflicted).
 __host__ __device__ __forceinline__ int64_t tc_tile_word(int64_t r, int64_t w, int64_t kwords, int kw) {
-#ifndef GF2E_TILE_SLAB
-#define GF2E_TILE_SLAB 1
-#endif
-#if GF2E_TILE_SLAB
     const int64_t wk = w % kw;
     return (((r >> 7) * (kwords / kw) + (w / kw)) * 128) * kw + (wk >> 1) * 256 + (r & 127) * 2 + (wk & 1);
-#else
-    return (((r >> 7) * (kwords / kw) + (w / kw)) * 128 + (r & 127)) * kw + (w % kw);
-#endif
 }
 // Row order inside each 32-row group of B^T tiles: tile row j holds column b_row_perm(j)
 // (tc_common.cuh), i.e. column o sits at tile row 4*(o%8) + o/8.
@@ -73,7 +66,11 @@ constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 128;  // tile rows, tile cols, k
 // 128 (int8) / 256 (fp4); Ac / Bt stage-tiled (tc_tile_word, KW 2 / 4), Bt rows in
 // tc_b_row_inv order.
 constexpr int kTcBKFp4 = 256;
-cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, bool fp4, cudaStream_t st);
+// tensor-core forms of the product kernel: int8; fp4 (k chunks <= 32768); fp4 with two
+// products per accumulator (k < 2048 only)
+constexpr int kFormI8 = 0, kFormFp4 = 1, kFormFp4Pair = 2;
+constexpr int64_t kFp4PairMaxK = 2047;
+cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, int form, cudaStream_t st);
 
 // INT-pipe M4RM product (product_m4rm.cu).  Operands: Ac as above, Bc [nprod][k_pad][n_pad/64].
 struct M4rmArgs {

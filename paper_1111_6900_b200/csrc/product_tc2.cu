@@ -27,6 +27,13 @@
 //    epilogue re-initialises it to 65536.0f after each read-out.  2x the int8 rate, half the
 //    expanded bytes per k-bit.
 //
+//  fp4 paired (template PAIR, k < 2048): two consecutive products share the accumulator; the
+//    second one's A scale factors are 2^11 (E8M0 0x8A, TMEM columns 320..383).  The
+//    accumulator starts at 2^23 (ulp 1), so its low 16 bits are c0 + 2^11 c1 with c0, c1 <=
+//    k < 2^11: the parities are bits 0 and 11, and one TMEM drain serves two products.  Exact
+//    and parity-tested; at k = 256 it matches (does not beat) the double-buffered int8 form,
+//    which stays the default below k = 2048 (the drain, not the MMA, bounds short k).
+//
 // Warp roles (448 threads per CTA, 1 CTA / SM):
 //   warps 0-3   expanders: expand this CTA's A and B^T rows of each stage into the UMMA
 //               K-major SWIZZLE_128B layout, fence.proxy.async, arrive on the leader's full[s]
@@ -49,8 +56,6 @@ namespace {
 using namespace tc;
 
 constexpr int BM = 128;   // rows per CTA (tile = 2 x BM)
-constexpr int BNH = 128;  // B^T rows per CTA (tile N = 2 x BNH)
-constexpr int BN = 256;
 #ifndef GF2E_FP4_S
 #define GF2E_FP4_S 5
 #endif
@@ -94,14 +99,22 @@ constexpr int MMA_WARP = NPW + NEW;
 constexpr int LOAD_WARP = MMA_WARP + 1;
 constexpr int NTHREADS = (NPW + NEW + 2) * 32;
 constexpr int A_BYTES = BM * 128;
-constexpr int B_BYTES = BNH * 128;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
 constexpr uint32_t FP4_ACC_INIT = 0x47800000u;  // 65536.0f
+constexpr uint32_t FP4_PAIR_INIT = 0x4B000000u;  // 2^23: ulp 1, count sum in mantissa bits 0..22
+constexpr uint32_t SF_ONE = 0x7F7F7F7Fu;         // E8M0 1.0
+constexpr uint32_t SF_2P11 = 0x8A8A8A8Au;        // E8M0 2^11 (second product of a pair)
 constexpr int FP4_CHUNK_STAGES = 32768 / 256;   // k-bits per accumulation chunk / bits per stage
 
-template <bool FP4>
+template <bool FP4, bool PAIR>
 struct Cfg {
+    // tile N = 256: two 256-column accumulators for int8; one for fp4 (scale factors in the
+    // other 256 TMEM columns).  (An N = 192 double-buffered paired form measured slower: the
+    // TMEM read-out competes with the MMAs, so overlap buys little at k < 2048.)
+    static constexpr int BN = 256;
+    static constexpr int BNH = BN / 2;          // B^T rows per CTA
+    static constexpr int B_BYTES = BNH * 128;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int BK = FP4 ? 256 : 128;  // k-bits per stage (= one 128-byte row of operand)
     static constexpr int KW = BK / 64;          // bit words per tile row per stage
     static constexpr int S = FP4 ? GF2E_FP4_S : 5;  // expanded operand stages
@@ -111,9 +124,13 @@ struct Cfg {
     static constexpr int D = FP4 ? GF2E_FP4_D : 8;  // bit-tile ring depth
     static constexpr int BITS_A = BM * (BK / 8);
     static constexpr int BITS_BYTES = (BM + BNH) * (BK / 8);
-    static constexpr int NBUF = FP4 ? 1 : 2;    // TMEM accumulators
+    static constexpr int NBUF = FP4 ? 1 : 2;  // TMEM accumulators
+    static constexpr int CH = BNH / 32;                   // 32-column chunks per epilogue half
+    // scale-factor TMEM columns (fp4): A (first / second product of a pair) and B
+    static constexpr uint32_t SFA0 = 256, SFA1 = 320, SFB = 384;
     static constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + BARS_BYTES + 1024;
     static_assert(SMEM_BYTES <= 232448, "shared memory");
+    static_assert(NBUF * BN <= (FP4 ? 384 : 512), "accumulators overlap the scale factors");
 };
 
 struct __align__(8) Bars {
@@ -180,9 +197,15 @@ __device__ __forceinline__ void mma2_mxf4(uint32_t d, uint64_t ad, uint64_t bd, 
         : "memory");
 }
 
-template <int E, bool FP4>
+template <int E, bool FP4, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, const TcArgs a) {
-    using C = Cfg<FP4>;
+    using C = Cfg<FP4, PAIR>;
+    constexpr int BN = C::BN, BNH = C::BNH, STAGE_BYTES = C::STAGE_BYTES;
+    static_assert(FP4 || !PAIR, "product pairing is an fp4 form");
+    // PAIR (k < 2048): two products share one accumulator, the second scaled by 2^11 through
+    // its E8M0 scale factors, so one TMEM drain serves two products (see the header comment)
+    constexpr uint32_t ACC_INIT = PAIR ? FP4_PAIR_INIT : FP4_ACC_INIT;
+    constexpr int STEP = PAIR ? 2 : 1;
     extern __shared__ uint8_t smem_raw[];
     // keep the shared state space visible to the compiler (STS/LDS, not generic ST/LD)
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -200,7 +223,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     const int64_t my_tiles = ntiles > cluster ? (ntiles - cluster + nclusters - 1) / nclusters : 0;
     const int nks = (int)(a.kwords / C::KW);
     // accumulation chunks per product: int8 wraps harmlessly mod 2^32; fp4 keeps count < 2^16
-    const int chunk = FP4 ? FP4_CHUNK_STAGES : nks;
+    const int chunk = (FP4 && !PAIR) ? FP4_CHUNK_STAGES : nks;
     const int nchunks = (nks + chunk - 1) / chunk;
     const int64_t total = my_tiles * (int64_t)s.nprod * nks;
     // short k (few stages per accumulation) makes the epilogue hand-off latency-critical
@@ -230,8 +253,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     if (FP4 && warp >= EPI_W0 && warp < EPI_W0 + 4) {
         // scale factors (columns 256..511: every byte E8M0 1.0) and the first accumulator init
         const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
-        for (int c = 256; c < 512; c += 32) tmem_st32_const(tmem + lb + c, 0x7F7F7F7Fu);
-        for (int c = 0; c < 256; c += 32) tmem_st32_const(tmem + lb + c, FP4_ACC_INIT);
+        for (int c = (int)C::SFA0; c < 512; c += 32)
+            tmem_st32_const(tmem + lb + c, (PAIR && c >= (int)C::SFA1 && c < (int)C::SFB) ? SF_2P11 : SF_ONE);
+        for (int c = 0; c < C::NBUF * BN; c += 32) tmem_st32_const(tmem + lb + c, ACC_INIT);
         tmem_wait_st();
     }
     tc_fence_before();
@@ -258,17 +282,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
         constexpr int NQ = FP4 ? 4 : 2;
         uint4 cur[NQ];
         auto load_bits = [&](int sl, uint4 (&v)[NQ]) {
-#if GF2E_TILE_SLAB
-            const uint8_t *bs = bits + sl * C::BITS_BYTES + p * 16;  // slab layout: tc_tile_word
-            constexpr int QS = 2048;
-#else
-            const uint8_t *bs = bits + sl * C::BITS_BYTES + p * (C::BK / 8);
-            constexpr int QS = 16;
-#endif
+            // slab layout (tc_tile_word): [KW/2 slabs][rows][16 B]
+            const uint8_t *bs = bits + sl * C::BITS_BYTES + p * 16;
 #pragma unroll
             for (int i = 0; i < NQ / 2; ++i) {
-                v[i] = *reinterpret_cast<const uint4 *>(bs + i * QS);
-                v[NQ / 2 + i] = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + i * QS);
+                v[i] = *reinterpret_cast<const uint4 *>(bs + i * (BM * 16));
+                if (p < BNH) v[NQ / 2 + i] = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + i * (BNH * 16));
             }
         };
         if (total > 0) {
@@ -280,7 +299,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             uint8_t *sa = stages + st * STAGE_BYTES;
             if constexpr (FP4) {
                 expand_row_fp4<false>(sa, p, cur[0], cur[1]);
-                expand_row_fp4<true>(sa + A_BYTES, p, cur[2], cur[3]);
+                if (p < BNH) expand_row_fp4<true>(sa + A_BYTES, p, cur[2], cur[3]);
             } else {
                 expand_row<false>(sa, p, cur[0]);
                 expand_row<true>(sa + A_BYTES, p, cur[1]);
@@ -312,7 +331,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
         // ===================== bit-tile loader (both CTAs, one thread) =====================
         if (lane == 0) {
             const int64_t KS = a.kwords / C::KW;  // k-stages per row block
-            const int64_t tile_words = 128 * C::KW;
+            const int64_t tile_words = BM * C::KW, tile_words_b = BNH * C::KW;
             const uint32_t bits_s = smem_u32(bits);
             int slot = 0;
             uint32_t bph = 0;
@@ -321,16 +340,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                 int64_t tm, tn;
                 tile_coords(tile, tiles_m, tiles_n, tm, tn);
                 const int64_t rbA = tm * 2 + rank;  // 128-row block of A
-                const int64_t rbB = tn * 2 + rank;  // 128-row block of B^T
+                const int64_t rbB = tn * 2 + rank;  // BNH-row block of B^T
                 for (int t = 0; t < s.nprod; ++t) {
                     const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * tile_words;
-                    const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * tile_words;
+                    const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * tile_words_b;
                     for (int ks = 0; ks < nks; ++ks) {
                         mbar_wait_sleep(&bars->bempty[slot], bph ^ 1, LOAD_SLEEP_NS);
                         mbar_arrive_expect_tx(&bars->bfull[slot], C::BITS_BYTES);
                         const uint32_t dst = bits_s + (uint32_t)(slot * C::BITS_BYTES);
                         bulk_g2s(dst, Ab + ks * tile_words, C::BITS_A, &bars->bfull[slot]);
-                        bulk_g2s(dst + C::BITS_A, Bb + ks * tile_words, C::BITS_BYTES - C::BITS_A,
+                        bulk_g2s(dst + C::BITS_A, Bb + ks * tile_words_b, C::BITS_BYTES - C::BITS_A,
                                  &bars->bfull[slot]);
                         if (++slot == C::D) {
                             slot = 0;
@@ -355,30 +374,52 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             int64_t tm, tn;
             tile_coords(tile, tiles_m, tiles_n, tm, tn);
             const int64_t m0 = tm * (2 * BM), n0 = tn * BN;
-            uint32_t acc[E][4];
+            constexpr int CH = C::CH;
+            uint32_t acc[E][CH];
 #pragma unroll
             for (int j = 0; j < E; ++j)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[j][c] = 0;
-            for (int t = 0; t < s.nprod; ++t) {
+                for (int c = 0; c < CH; ++c) acc[j][c] = 0;
+            for (int t = 0; t < s.nprod; t += STEP) {
                 const uint32_t mask = bars->outmask[t];
+                const uint32_t mask1 = (PAIR && t + 1 < s.nprod) ? bars->outmask[t + 1] : 0u;
                 for (int ch = 0; ch < nchunks; ++ch, ++gp) {
                     const int buf = (int)(gp % C::NBUF);
                     TW(i_tfull, mbar_wait_sleep(&bars->tfull[buf], (uint32_t)((gp / C::NBUF) & 1), idle_ns));
                     tc_fence_after();
+                    constexpr int LB = 1;  // chunks per tcgen05.ld wait (batching measured no gain)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const uint32_t ta =
-                            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + c * 32);
-                        uint32_t v[16];
-                        tmem_ld32_pack16(ta, v);
+                    for (int c0 = 0; c0 < CH; c0 += LB) {
+                        uint32_t v[LB][16];
+#pragma unroll
+                        for (int cc = 0; cc < LB; ++cc)
+                            tmem_ld32_pack16(tmem + ((uint32_t)(q * 32) << 16) +
+                                                 (uint32_t)(buf * BN + h * BNH + (c0 + cc) * 32),
+                                             v[cc]);
                         tmem_wait_ld();
-                        const uint32_t pw = parity_word_packed(v);
 #pragma unroll
-                        for (int j = 0; j < E; ++j) acc[j][c] ^= pw & (0u - ((mask >> j) & 1u));
-                        if (FP4)
+                        for (int cc = 0; cc < LB; ++cc) {
+                            const int c = c0 + cc;
+                            if constexpr (PAIR) {
+                                // low 16 bits of each cell = c0 + 2^11 c1: parities at bits 0 and 11
+                                const uint32_t pw0 = parity_word_packed_shl<7, 0xECA8>(v[cc]);
+                                const uint32_t pw1 = parity_word_packed_shl<4, 0xFDB9>(v[cc]);
 #pragma unroll
-                            for (int c8 = 0; c8 < 32; c8 += 8) tmem_st8_const(ta + c8, FP4_ACC_INIT);
+                                for (int j = 0; j < E; ++j)
+                                    acc[j][c] ^=
+                                        (pw0 & (0u - ((mask >> j) & 1u))) ^ (pw1 & (0u - ((mask1 >> j) & 1u)));
+                            } else {
+                                const uint32_t pw = parity_word_packed(v[cc]);
+#pragma unroll
+                                for (int j = 0; j < E; ++j) acc[j][c] ^= pw & (0u - ((mask >> j) & 1u));
+                            }
+                            if (FP4) {
+                                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) +
+                                                    (uint32_t)(buf * BN + h * BNH + c * 32);
+#pragma unroll
+                                for (int c8 = 0; c8 < 32; c8 += 8) tmem_st8_const(ta + c8, ACC_INIT);
+                            }
+                        }
                     }
                     if (FP4) tmem_wait_st();
                     tc_fence_before();
@@ -428,31 +469,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             uint32_t phase = 0;
             const uint32_t st0 = smem_u32(stages);
             const uint32_t idesc = FP4 ? idesc_mxf4(2 * BM, BN) : idesc_i8(2 * BM, BN);
+            static_assert(BN % 16 == 0 && BN <= 256, "cta_group::2 MMA N");
             for (int64_t ti = 0; ti < my_tiles; ++ti) {
-                for (int t = 0; t < s.nprod; ++t) {
+                for (int t = 0; t < s.nprod; t += STEP) {
+                    const int units = (PAIR && t + 1 < s.nprod) ? 2 : 1;
                     for (int ch = 0; ch < nchunks; ++ch, ++gp) {
                         const int buf = (int)(gp % C::NBUF);
                         TW(i_tempty, mbar_wait(&bars->tempty[buf], (uint32_t)((gp / C::NBUF) & 1) ^ 1));
                         tc_fence_after();
                         const uint32_t dt = tmem + (uint32_t)(buf * BN);
                         const int ks1 = (ch + 1) * chunk < nks ? (ch + 1) * chunk : nks;
-                        for (int ks = ch * chunk; ks < ks1; ++ks) {
-                            TW(i_full, mbar_wait(&bars->full[st], phase));
-                            tc_fence_after();
-                            const uint32_t sa = st0 + (uint32_t)(st * STAGE_BYTES);
-                            const uint32_t sb = sa + A_BYTES;
+                        for (int u = 0; u < units; ++u) {
+                            const uint32_t sfa = tmem + (u ? C::SFA1 : C::SFA0);
+                            for (int ks = ch * chunk; ks < ks1; ++ks) {
+                                TW(i_full, mbar_wait(&bars->full[st], phase));
+                                tc_fence_after();
+                                const uint32_t sa = st0 + (uint32_t)(st * STAGE_BYTES);
+                                const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-                            for (int kk = 0; kk < 4; ++kk) {
-                                const uint64_t ad = umma_desc_sw128(sa + kk * 32), bd = umma_desc_sw128(sb + kk * 32);
-                                if constexpr (FP4)
-                                    mma2_mxf4(dt, ad, bd, idesc, tmem + 256, tmem + 384);
-                                else
-                                    mma2_i8(dt, ad, bd, idesc, (ks != ch * chunk) | kk);
-                            }
-                            mma2_commit_both(&bars->empty[st]);
-                            if (++st == S) {
-                                st = 0;
-                                phase ^= 1;
+                                for (int kk = 0; kk < 4; ++kk) {
+                                    const uint64_t ad = umma_desc_sw128(sa + kk * 32),
+                                                   bd = umma_desc_sw128(sb + kk * 32);
+                                    if constexpr (FP4)
+                                        mma2_mxf4(dt, ad, bd, idesc, sfa, tmem + C::SFB);
+                                    else
+                                        mma2_i8(dt, ad, bd, idesc, (ks != ch * chunk) | kk);
+                                }
+                                mma2_commit_both(&bars->empty[st]);
+                                if (++st == S) {
+                                    st = 0;
+                                    phase ^= 1;
+                                }
                             }
                         }
                         mma2_commit_both(&bars->tfull[buf]);
@@ -496,12 +543,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
 
 int g_num_sms2 = 0;
 
-template <int E, bool FP4>
+template <int E, bool FP4, bool PAIR>
 cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
-    const int smem = Cfg<FP4>::SMEM_BYTES;
-    cudaError_t err = cudaFuncSetAttribute(k_product_tc2<E, FP4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int smem = Cfg<FP4, PAIR>::SMEM_BYTES;
+    cudaError_t err =
+        cudaFuncSetAttribute(k_product_tc2<E, FP4, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    const int64_t tiles = (a.m_pad / (2 * BM)) * (a.n_pad / BN);
+    const int64_t tiles = (a.m_pad / (2 * BM)) * (a.n_pad / Cfg<FP4, PAIR>::BN);
     if (tiles == 0) return cudaSuccess;
     if (g_num_sms2 == 0) {
         int dev = 0;
@@ -522,30 +570,35 @@ cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_product_tc2<E, FP4>, s, a);
+    return cudaLaunchKernelEx(&cfg, k_product_tc2<E, FP4, PAIR>, s, a);
 }
 
-template <bool FP4>
+template <bool FP4, bool PAIR>
 cudaError_t launch_any(const Sched &s, const TcArgs &a, cudaStream_t st) {
     switch (s.nout) {
-        case 1: return launch_e<1, FP4>(s, a, st);
-        case 2: return launch_e<2, FP4>(s, a, st);
-        case 3: return launch_e<3, FP4>(s, a, st);
-        case 4: return launch_e<4, FP4>(s, a, st);
-        case 5: return launch_e<5, FP4>(s, a, st);
-        case 6: return launch_e<6, FP4>(s, a, st);
-        case 7: return launch_e<7, FP4>(s, a, st);
-        case 8: return launch_e<8, FP4>(s, a, st);
-        case 9: return launch_e<9, FP4>(s, a, st);
-        case 10: return launch_e<10, FP4>(s, a, st);
+        case 1: return launch_e<1, FP4, PAIR>(s, a, st);
+        case 2: return launch_e<2, FP4, PAIR>(s, a, st);
+        case 3: return launch_e<3, FP4, PAIR>(s, a, st);
+        case 4: return launch_e<4, FP4, PAIR>(s, a, st);
+        case 5: return launch_e<5, FP4, PAIR>(s, a, st);
+        case 6: return launch_e<6, FP4, PAIR>(s, a, st);
+        case 7: return launch_e<7, FP4, PAIR>(s, a, st);
+        case 8: return launch_e<8, FP4, PAIR>(s, a, st);
+        case 9: return launch_e<9, FP4, PAIR>(s, a, st);
+        case 10: return launch_e<10, FP4, PAIR>(s, a, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
 }  // namespace
 
-cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, bool fp4, cudaStream_t st) {
-    return fp4 ? launch_any<true>(s, a, st) : launch_any<false>(s, a, st);
+cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, int form, cudaStream_t st) {
+    switch (form) {
+        case kFormI8: return launch_any<false, false>(s, a, st);
+        case kFormFp4: return launch_any<true, false>(s, a, st);
+        case kFormFp4Pair: return launch_any<true, true>(s, a, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace gf2e

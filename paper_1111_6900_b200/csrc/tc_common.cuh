@@ -63,6 +63,21 @@ __device__ __forceinline__ uint32_t parity_word_packed(const uint32_t (&v)[16]) 
     return r;
 }
 
+// The same for the paired fp4 form: the parity sits at bit SH' of each 16-bit half; shifting
+// left by SHIFT moves it to bit 7 of a byte, SEL picks (and sign-replicates) that byte of each
+// of the four halves: 0xECA8 = low bytes (bits 0 + 7), 0xFDB9 = high bytes (bits 11 + 4).
+template <int SHIFT, uint32_t SEL>
+__device__ __forceinline__ uint32_t parity_word_packed_shl(const uint32_t (&v)[16]) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        uint32_t w;
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w) : "r"(v[2 * g] << SHIFT), "r"(v[2 * g + 1] << SHIFT), "n"(SEL));
+        r |= w & (0x01010101u << g);
+    }
+    return r;
+}
+
 // Half of parity_word: 16 accumulators = groups g0 .. g0+3 of a 32-column chunk.
 __device__ __forceinline__ uint32_t parity_half(const uint32_t (&v)[16], int g0) {
     uint32_t r = 0;

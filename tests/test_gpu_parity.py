@@ -247,6 +247,8 @@ def test_native_code_used(g):
     B = g.SlicedMatrix.random(ctx, 4096, 256, 2)
     g.karatsuba_mul(g.SlicedMatrix.random(ctx, 256, 4096, 1), B)
     assert g._lib.last_product_kernel() == "k_product_tc2<fp4>"
+    g.karatsuba_mul(A, A, backend="tc_fp4")
+    assert g._lib.last_product_kernel() == "k_product_tc2<fp4x2>"  # k < 2048 forced fp4: paired form
 
 
 @pytest.mark.parametrize("acc", [False, True])
