@@ -319,7 +319,7 @@ def run_ours(args):
 
     if e2e:
         line["e2e"] = e2e
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 figure
         import oracle
 
         rows = args.cpu_rows or (256 if k * n >= 16384 * 16384 else min(m, 1024))
