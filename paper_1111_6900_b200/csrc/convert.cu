@@ -398,7 +398,9 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
     const int64_t nw = words_for(n);
     const int64_t kstages = kblocks >> 1;
     for (int64_t blk = warp; blk < kstages * nblocks; blk += nwarps) {
-        const int64_t ks = blk % kstages, nb = blk / kstages;
+        // nb fastest: neighbouring warps read neighbouring words of the same rows, so every
+        // 32-byte sector of B is fetched from DRAM once (L2 serves the other three warps)
+        const int64_t nb = blk % nblocks, ks = blk / nblocks;
         const uint64_t tm = (nb == nw - 1) ? tail_mask(n) : ~0ULL;
         uint64_t a[2][kMaxE], b[2][kMaxE];
 #pragma unroll
@@ -412,6 +414,14 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
             }
         }
         const int64_t ra = tc_b_row_inv(nb * 64 + lane), rbw = tc_b_row_inv(nb * 64 + lane + 32);
+        // the transpose is GF(2)-linear: transpose the e planes once, then form every
+        // product's subset XOR from the transposed words (e instead of K(e) transposes)
+#pragma unroll
+        for (int i = 0; i < kMaxE; ++i)
+            if (i < s.e) {
+                transpose64(a[0][i], b[0][i], lane);
+                transpose64(a[1][i], b[1][i], lane);
+            }
         for (int t = 0; t < s.nprod; ++t) {
             const uint32_t sub = s.subset[t];
             uint64_t xa[2] = {0, 0}, xb[2] = {0, 0};
@@ -424,8 +434,6 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
                     xb[h] ^= b[h][i] & sel;
                 }
             }
-            transpose64(xa[0], xb[0], lane);
-            transpose64(xa[1], xb[1], lane);
             uint64_t *o = out + t * po;
             *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(ra, 2 * ks, ldo, kw)) = make_ulonglong2(xa[0], xa[1]);
             *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(rbw, 2 * ks, ldo, kw)) = make_ulonglong2(xb[0], xb[1]);
