@@ -59,8 +59,11 @@ constexpr int BM = 128;   // rows per CTA (tile = 2 x BM)
 #ifndef GF2E_FP4_S
 #define GF2E_FP4_S 5
 #endif
+#ifndef GF2E_ATMEM
+#define GF2E_ATMEM 1
+#endif
 constexpr int DMAX = 16;  // bit-tile ring slots (upper bound)
-constexpr int SMAX = 6;
+constexpr int SMAX = 8;
 constexpr int BARS_BYTES = 1024;  // Bars (static_assert below)      // expanded operand stages (32 KiB each: one 128-byte swizzle row per operand row)
 #ifndef GF2E_INSTR
 #define GF2E_INSTR 0
@@ -112,12 +115,19 @@ struct Cfg {
     // other 256 TMEM columns).  (An N = 192 double-buffered paired form measured slower: the
     // TMEM read-out competes with the MMAs, so overlap buys little at k < 2048.)
     static constexpr int BN = 256;
+    // fp4 (not paired): the expanded A operand lives in TMEM (tcgen05.st by the expanders,
+    // tcgen05.mma A-from-TMEM), so shared memory carries only B: half the shared-memory traffic
+    static constexpr bool ATMEM = FP4 && !PAIR && GF2E_ATMEM;
+    static constexpr int A_SMEM = ATMEM ? 0 : A_BYTES;
     static constexpr int BNH = BN / 2;          // B^T rows per CTA
     static constexpr int B_BYTES = BNH * 128;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGE_BYTES = A_SMEM + B_BYTES;
     static constexpr int BK = FP4 ? 256 : 128;  // k-bits per stage (= one 128-byte row of operand)
     static constexpr int KW = BK / 64;          // bit words per tile row per stage
-    static constexpr int S = FP4 ? GF2E_FP4_S : 5;  // expanded operand stages
+#ifndef GF2E_ATMEM_S
+#define GF2E_ATMEM_S 7
+#endif
+    static constexpr int S = ATMEM ? GF2E_ATMEM_S : FP4 ? GF2E_FP4_S : 5;  // operand stages (TMEM A: S x 32 columns)
 #ifndef GF2E_FP4_D
 #define GF2E_FP4_D 6
 #endif
@@ -127,7 +137,9 @@ struct Cfg {
     static constexpr int NBUF = FP4 ? 1 : 2;  // TMEM accumulators
     static constexpr int CH = BNH / 32;                   // 32-column chunks per epilogue half
     // scale-factor TMEM columns (fp4): A (first / second product of a pair) and B
-    static constexpr uint32_t SFA0 = 256, SFA1 = 320, SFB = 384;
+    static constexpr uint32_t SFA0 = ATMEM ? 256 + 32 * S : 256, SFA1 = 320, SFB = ATMEM ? SFA0 + (S >= 7 ? 16 : 32) : 384;
+    static_assert(!ATMEM || SFB + (S >= 7 ? 16 : 32) <= 512, "TMEM columns: A stages overlap the scale factors");
+    static constexpr uint32_t ATM0 = 256;  // TMEM column of A stage 0 (ATMEM)
     static constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + BARS_BYTES + 1024;
     static_assert(SMEM_BYTES <= 232448, "shared memory");
     static_assert(NBUF * BN <= (FP4 ? 384 : 512), "accumulators overlap the scale factors");
@@ -168,6 +180,30 @@ __device__ __forceinline__ void expand_row_fp4(uint8_t *tile, int r, uint4 lo, u
     }
 }
 
+// A row of one fp4 stage into TMEM (this thread's lane): 32 columns = the 8 chunks of
+// expand_row_fp4 in order (column 4q + i = word i of chunk q)
+__device__ __forceinline__ void expand_row_fp4_tmem(uint32_t taddr, uint4 lo, uint4 hi) {
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    uint32_t o[32];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t x = w[q];
+        o[4 * q] = x & 0x11111111u;
+        o[4 * q + 1] = x & 0x22222222u;
+        o[4 * q + 2] = x & 0x44444444u;
+        o[4 * q + 3] = (x >> 2) & 0x22222222u;
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%"
+        "29,%30,%31,%32};" ::"r"(taddr),
+        "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]), "r"(o[9]),
+        "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]), "r"(o[16]), "r"(o[17]), "r"(o[18]),
+        "r"(o[19]), "r"(o[20]), "r"(o[21]), "r"(o[22]), "r"(o[23]), "r"(o[24]), "r"(o[25]), "r"(o[26]), "r"(o[27]),
+        "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31])
+        : "memory");
+}
+
 __device__ __forceinline__ void tmem_st32_const(uint32_t taddr, uint32_t v) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -187,6 +223,15 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 // block-scaled instruction descriptor: e2m1 x e2m1, E8M0 scales, K-major, K=64
 __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
     return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+// A operand from TMEM (tcgen05 "TS" form)
+__device__ __forceinline__ void mma2_mxf4_ts(uint32_t d, uint32_t at, uint64_t bd, uint32_t idesc, uint32_t sfa,
+                                             uint32_t sfb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.eq.u32 p, 1, 1;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%4], [%5], p;\n\t}" ::"r"(d),
+        "r"(at), "l"(bd), "r"(idesc), "r"(sfa), "r"(sfb)
+        : "memory");
 }
 __device__ __forceinline__ void mma2_mxf4(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t sfa,
                                           uint32_t sfb) {
@@ -297,7 +342,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
         for (int64_t it = 0; it < total; ++it) {
             TW(i_empty, mbar_wait_sleep(&bars->empty[st], phase ^ 1, EXP_SLEEP_NS));
             uint8_t *sa = stages + st * STAGE_BYTES;
-            if constexpr (FP4) {
+            if constexpr (C::ATMEM) {
+                expand_row_fp4_tmem(tmem + ((uint32_t)((warp & 3) * 32) << 16) + C::ATM0 + (uint32_t)(st * 32), cur[0],
+                                    cur[1]);
+                expand_row_fp4<true>(sa, p, cur[2], cur[3]);
+                tmem_wait_st();
+                tc_fence_before();
+            } else if constexpr (FP4) {
                 expand_row_fp4<false>(sa, p, cur[0], cur[1]);
                 if (p < BNH) expand_row_fp4<true>(sa + A_BYTES, p, cur[2], cur[3]);
             } else {
@@ -485,12 +536,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                                 TW(i_full, mbar_wait(&bars->full[st], phase));
                                 tc_fence_after();
                                 const uint32_t sa = st0 + (uint32_t)(st * STAGE_BYTES);
-                                const uint32_t sb = sa + A_BYTES;
+                                const uint32_t sb = sa + C::A_SMEM;
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk) {
                                     const uint64_t ad = umma_desc_sw128(sa + kk * 32),
                                                    bd = umma_desc_sw128(sb + kk * 32);
-                                    if constexpr (FP4)
+                                    if constexpr (C::ATMEM)
+                                        mma2_mxf4_ts(dt, tmem + C::ATM0 + (uint32_t)(st * 32 + kk * 8), bd, idesc, sfa,
+                                                     tmem + C::SFB);
+                                    else if constexpr (FP4)
                                         mma2_mxf4(dt, ad, bd, idesc, sfa, tmem + C::SFB);
                                     else
                                         mma2_i8(dt, ad, bd, idesc, (ks != ch * chunk) | kk);
