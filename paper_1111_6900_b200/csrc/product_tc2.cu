@@ -131,7 +131,10 @@ struct Cfg {
 #ifndef GF2E_FP4_D
 #define GF2E_FP4_D 6
 #endif
-    static constexpr int D = FP4 ? GF2E_FP4_D : 8;  // bit-tile ring depth
+#ifndef GF2E_ATMEM_D
+#define GF2E_ATMEM_D 6
+#endif
+    static constexpr int D = ATMEM ? GF2E_ATMEM_D : FP4 ? GF2E_FP4_D : 8;  // bit-tile ring depth
     static constexpr int BITS_A = BM * (BK / 8);
     static constexpr int BITS_BYTES = (BM + BNH) * (BK / 8);
     static constexpr int NBUF = FP4 ? 1 : 2;  // TMEM accumulators
