@@ -139,6 +139,23 @@ def test_word_boundary_shapes(g, e, backend):
         assert np.array_equal(C.to_numpy(), ref), (m, k, n, backend)
 
 
+@pytest.mark.parametrize("e", range(2, 11))
+def test_long_k_all_e(g, e):
+    # k >= 2048 takes the fp4 form with A in TMEM (7 TMEM stages); k = 32768 + 300 crosses
+    # the fp4 accumulation-chunk boundary (count < 2^16 per chunk); addmul through the same path
+    ctx = g.field_new(e)
+    for (m, k, n) in [(300, 2048, 260), (257, 4100, 65), (33, 32768 + 300, 129)]:
+        SA = g.SlicedMatrix.random(ctx, m, k, 1)
+        SB = g.SlicedMatrix.random(ctx, k, n, 2)
+        C0 = g.SlicedMatrix.random(ctx, m, n, 3)
+        C = C0.copy()
+        g.addmul(C, SA, SB)
+        assert g._lib.last_product_kernel() == "k_product_tc2<fp4>"
+        ref, _ = oracle.karatsuba(e, ctx.f, oracle.sliced_random(e, m, k, 1), oracle.sliced_random(e, k, n, 2),
+                                  m, k, n, C0=oracle.sliced_random(e, m, n, 3))
+        assert np.array_equal(C.to_numpy(), ref), (e, m, k, n)
+
+
 @pytest.mark.parametrize("backend", BACKENDS)
 def test_errors_match_reference(g, backend):
     A = g.SlicedMatrix.random(g.field_new(4), 5, 6, 1)
