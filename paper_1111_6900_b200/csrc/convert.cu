@@ -387,8 +387,8 @@ __device__ __forceinline__ void transpose64(uint64_t &xa, uint64_t &xb, int lane
 // parity packer emits columns in b_row_perm order).  One warp per 64x64 block.
 __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb, int64_t pb, int64_t k,
                             int64_t n, uint64_t *__restrict__ out, int64_t ldo, int64_t po, int64_t kblocks,
-                            int64_t nblocks, int fp4) {
-    // one warp per (2 x 64 k-rows, 64-column block): two 64x64 transposes, then each lane
+                            int64_t nblocks, int fp4, int tsplit) {
+    // one warp per (2 x 64 k-rows, 64-column block[, product group]): two 64x64 transposes, then each lane
     // writes 16-byte pieces of tile rows.  Input row r of a 64-block lands at bit sigma(r):
     // int8 reverses bits inside bytes (r ^ 7), fp4 swaps bits 0 and 2 of every nibble.
     const int kw = fp4 ? 4 : 2;
@@ -397,7 +397,12 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
     const int64_t nwarps = gstride() >> 5;
     const int64_t nw = words_for(n);
     const int64_t kstages = kblocks >> 1;
-    for (int64_t blk = warp; blk < kstages * nblocks; blk += nwarps) {
+    // small problems (the TRSM / PLE blocks) split the products over tsplit warps per block, so
+    // the latency of the per-product loop is spread over more SMs
+    const int tper = (s.nprod + tsplit - 1) / tsplit;
+    for (int64_t wb = warp; wb < kstages * nblocks * tsplit; wb += nwarps) {
+        const int tg = (int)(wb % tsplit);
+        const int64_t blk = wb / tsplit;
         // nb fastest: neighbouring warps read neighbouring words of the same rows, so every
         // 32-byte sector of B is fetched from DRAM once (L2 serves the other three warps)
         const int64_t nb = blk % nblocks, ks = blk / nblocks;
@@ -422,7 +427,8 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
                 transpose64(a[0][i], b[0][i], lane);
                 transpose64(a[1][i], b[1][i], lane);
             }
-        for (int t = 0; t < s.nprod; ++t) {
+        const int t1 = (tg + 1) * tper < s.nprod ? (tg + 1) * tper : s.nprod;
+        for (int t = tg * tper; t < t1; ++t) {
             const uint32_t sub = s.subset[t];
             uint64_t xa[2] = {0, 0}, xb[2] = {0, 0};
 #pragma unroll
@@ -549,8 +555,10 @@ cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int
                              cudaStream_t st) {
     int64_t warps = (kblocks >> 1) * nblocks;  // kblocks is even (k_pad is a multiple of 128)
     if (warps == 0) return cudaSuccess;
-    int g = grid_for(warps * 32, 256);
-    k_combos_bt<<<g, 256, 0, st>>>(s, B, ldb, pb, k, n, out, ldo, po, kblocks, nblocks, fp4 ? 1 : 0);
+    int tsplit = 1;
+    while (tsplit < s.nprod && warps * tsplit * 2 <= 148 * 16) tsplit *= 2;
+    int g = grid_for(warps * tsplit * 32, 256);
+    k_combos_bt<<<g, 256, 0, st>>>(s, B, ldb, pb, k, n, out, ldo, po, kblocks, nblocks, fp4 ? 1 : 0, tsplit);
     return cudaGetLastError();
 }
 
