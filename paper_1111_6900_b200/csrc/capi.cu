@@ -218,6 +218,18 @@ int check_device() {
     e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
     if (e != cudaSuccess) return fail(GF2E_ENODEV, "cannot query device: %s", cudaGetErrorString(e));
     if (major != 10) return fail(GF2E_ENODEV, "libgf2e_b200 needs an sm_100 (B200) device, found sm_%d", major * 10);
+    // Temporaries (host-buffer API, PLE) come from the device's default stream-ordered pool.
+    // Its default release threshold (0) hands freed blocks back to the driver at every
+    // synchronisation, so each call would re-map gigabytes; keep them pooled instead.
+    static bool pool_set[64] = {};
+    if (dev >= 0 && dev < 64 && !pool_set[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool_set[dev] = true;
+    }
     return GF2E_OK;
 }
 
@@ -507,7 +519,7 @@ int ple_rec(PleCtx &c, int64_t r0, int64_t c0, int64_t m, int64_t n, int64_t *P,
     uint64_t *V = c.S + r0 * c.ld + c0 / 64;
     if (n <= kPlePanel) {  // base case nj_ple (newton_john.py:207-260) on one plane word
         CK(launch_ple_panel(c.e, c.tab, V, c.ld, c.ps, m, (int)n, c.pout, c.st), "ple_panel");
-        g_launches += m > 512 ? 2 : 1;
+        g_launches += m > ple_window() ? 2 : 1;
         ++c.panels;
         PanelOut h;
         CKH(cudaMemcpyAsync(&h, c.pout, offsetof(PanelOut, jcol), cudaMemcpyDeviceToHost, c.st), "cudaMemcpyAsync");

@@ -114,8 +114,10 @@ constexpr int kFieldTabSlots = 16;
 struct FieldTab {
     uint16_t ex[1024], lg[1024], inv[1024];  // exp/log over a primitive element; inverses
     uint16_t mulmask[1024][kMaxE];           // bit p of [c][b] = coefficient b of c * x^p
+    uint32_t f;                              // the field polynomial (bit e set)
 };
 const FieldTab *field_tab(int e, uint32_t f, uint32_t g);  // device pointer (synchronous fill)
+int ple_window();  // rows kept in shared memory by the panel kernel (launches = 1 + (m > window))
 cudaError_t launch_ple_panel(int e, const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb,
                              PanelOut *out, cudaStream_t st);
 cudaError_t launch_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t nwords, const int64_t *swaps,

@@ -41,7 +41,10 @@ __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * block
 // ---- per-field constant tables (static module memory, filled once per (e, f)) ----------------
 __device__ FieldTab g_field_tabs[kFieldTabSlots];
 
-constexpr int PT = 512;  // phase-1 threads = window rows
+#ifndef GF2E_PLE_WIN
+#define GF2E_PLE_WIN 512
+#endif
+constexpr int PT = GF2E_PLE_WIN;  // phase-1 threads = window rows
 constexpr int KP = 64;   // pivots per panel (one plane word)
 
 __device__ __forceinline__ uint64_t swap_bits(uint64_t w, int a, int b) {
@@ -75,17 +78,18 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
     uint64_t *bt = win + PT * E;                         // [KP][E][E]
     uint16_t *sinv = reinterpret_cast<uint16_t *>(bt + KP * E * E);  // [2^E] inverses
     uint16_t *smk = sinv + (1 << E);                                   // [2^E][E] multiplication matrices
-    __shared__ uint64_t ext[kMaxE], sT[kMaxE], sF[kMaxE];
+    __shared__ uint64_t ext[kMaxE];
     __shared__ uint64_t s_dval[KP][kMaxE];
     __shared__ int64_t dpos[KP];
     __shared__ int dstep[KP], s_jcol[KP];
     __shared__ int64_t s_P[KP], s_Q[KP];
-    __shared__ int s_min, s_nd, s_supp_ok;
+    __shared__ int s_mn[2], s_nd, s_supp_ok;
     __shared__ uint32_t s_inv;
     __shared__ unsigned long long s_supp;
     __shared__ int64_t s_pmin;
 
     const int tid = threadIdx.x;
+    const uint32_t fpoly = tab->f;  // x * c mod f: shift, fold with f (bit E included)
     const int W = (int)(m < PT ? m : PT);
     const uint64_t cmask = nb >= 64 ? ~0ULL : ((1ULL << nb) - 1);
     const int k = (int)(m < nb ? m : nb);
@@ -93,7 +97,7 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
         s_nd = 0;
         s_supp_ok = 0;
         s_supp = 0;
-        s_min = 0x7fffffff;
+        s_mn[0] = 0x7fffffff;
     }
     for (int i = tid; i < (1 << E); i += PT) {
         sinv[i] = tab->inv[i];
@@ -109,21 +113,22 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
             win[s * E + b] = x;
             any |= x;
         }
-        if (any & 1ULL) atomicMin(&s_min, s);  // candidates for column 0
+        if (any & 1ULL) atomicMin(&s_mn[0], s);  // candidates for column 0
     }
     __syncthreads();
     int r = 0;
+    // Three barriers per pivot: (bookkeeping) | (basis) | (elimination + candidates for the next
+    // column).  The candidate minimum is double-buffered (s_mn[j & 1]) so no barrier is needed
+    // to reset it; the basis alpha^s * T is formed straight from the unscaled pivot row with
+    // the multiplication matrix of alpha^s / pivot.
     for (int j = 0; j < nb && r < k; ++j) {
-        int64_t ipos = s_min;
-        __syncthreads();
-        if (tid == 0) {
-            s_min = 0x7fffffff;  // candidates for column j + 1 (collected in the elimination)
-            s_pmin = INT64_MAX;
-        }
+        const int cb = j & 1;
+        int64_t ipos = s_mn[cb];
         if (ipos == 0x7fffffff && W < m) {
             // Column support of the rows below the window: their original bits OR the scaled
             // pivot suffixes (the only things ever XOR-ed into them).  Computed at the first
             // miss; a column outside it has no pivot below the window either.
+            if (tid == 0) s_pmin = INT64_MAX;
             if (!s_supp_ok) {
                 uint64_t acc = 0;
                 for (int64_t p = W + tid; p < m; p += PT)
@@ -175,13 +180,14 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
         }
         if (ipos == 0x7fffffff || ipos == INT64_MAX) {
             // no pivot in column j: collect the window's candidates for column j + 1
+            if (tid == 0) s_mn[cb ^ 1] = 0x7fffffff;
             __syncthreads();
             if (j + 1 < nb)
                 for (int s = r + tid; s < W; s += PT) {
                     uint64_t any = 0;
 #pragma unroll
                     for (int b = 0; b < E; ++b) any |= win[s * E + b];
-                    if ((any >> (j + 1)) & 1ULL) atomicMin(&s_min, s);
+                    if ((any >> (j + 1)) & 1ULL) atomicMin(&s_mn[cb ^ 1], s);
                 }
             __syncthreads();
             continue;
@@ -215,37 +221,31 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
             s_Q[r] = j;
             s_jcol[r] = j;
             s_inv = sinv[elemE<E>(pr, j)];
+            s_mn[cb ^ 1] = 0x7fffffff;  // candidates for column j + 1 (collected below)
         }
         __syncthreads();
-        // scale the pivot row right of j by 1/pivot (the pivot stays as L's diagonal):
-        // plane b of c * v is the XOR of the planes p in mulmask[c][b]
+        // basis alpha^s * T_r, T_r = pivot row right of j scaled by 1/pivot (s = tid / E,
+        // plane tid % E): plane b of c * v is the XOR of the planes p in mulmask[c][b]
         const uint64_t sm = (j >= 63 ? 0ULL : (~0ULL << (j + 1))) & cmask;
-        if (tid < E) {
-            const uint32_t mk = smk[s_inv * E + tid];
+        if (tid < E * E) {
+            const int sidx = tid / E, b = tid % E;
+            uint32_t c = s_inv;  // alpha^sidx / pivot
+            for (int q = 0; q < sidx; ++q) c = (c << 1) ^ (((c >> (E - 1)) & 1u) ? fpoly : 0u);
+            const uint32_t mk = smk[c * E + b];
             const uint64_t *pr = win + r * E;
             uint64_t acc = 0;
 #pragma unroll
             for (int p = 0; p < E; ++p)
                 if ((mk >> p) & 1u) acc ^= pr[p] & sm;
-            sT[tid] = acc;
-            sF[tid] = (pr[tid] & ~sm) | acc;
-        }
-        __syncthreads();
-        if (tid < E * E) {  // basis alpha^s * T (s = tid / E, plane tid % E)
-            const int sidx = tid / E, b = tid % E;
-            const uint32_t mk = smk[(1u << sidx) * E + b];
-            uint64_t acc = 0;
-#pragma unroll
-            for (int p = 0; p < E; ++p)
-                if ((mk >> p) & 1u) acc ^= sT[p];
             bt[r * E * E + tid] = acc;
         }
-        if (tid < E) win[r * E + tid] = sF[tid];
-        if (tid == 0 && s_supp_ok)
-#pragma unroll
-            for (int b = 0; b < E; ++b) s_supp |= sT[b];
         __syncthreads();
         const uint64_t *btr = bt + r * E * E;
+        if (tid < E) {
+            const uint64_t t0 = btr[tid];  // s = 0: the scaled suffix itself
+            win[r * E + tid] = (win[r * E + tid] & ~sm) | t0;
+            if (s_supp_ok) atomicOr(&s_supp, t0);
+        }
         const bool next = j + 1 < nb;
         for (int s = r + 1 + tid; s < W; s += PT) {
             uint64_t v[E];
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
                 uint64_t any = 0;
 #pragma unroll
                 for (int b = 0; b < E; ++b) any |= v[b];
-                if ((any >> (j + 1)) & 1ULL) atomicMin(&s_min, s);
+                if ((any >> (j + 1)) & 1ULL) atomicMin(&s_mn[cb ^ 1], s);
             }
         }
         ++r;
@@ -465,6 +465,8 @@ cudaError_t launch_ple_e(const FieldTab *tab, uint64_t *S, int64_t ld, int64_t p
     return cudaGetLastError();
 }
 
+int ple_window() { return PT; }
+
 cudaError_t launch_ple_panel(int e, const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb,
                              PanelOut *out, cudaStream_t st) {
     switch (e) {
@@ -505,6 +507,7 @@ const FieldTab *field_tab(int e, uint32_t f, uint32_t g) {
         i = (i->second == slot) ? slots.erase(i) : std::next(i);
     static FieldTab h;
     std::memset(&h, 0, sizeof(h));
+    h.f = f;
     const uint32_t q1 = (1u << e) - 1;
     uint32_t v = 1;
     for (uint32_t i = 0; i < q1; ++i) {

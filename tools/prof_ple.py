@@ -14,9 +14,11 @@ S0 = g.slice_packed(g.PackedMatrix.random(ctx, n, n, 11))
 S = S0.copy()
 g.ple_sliced(S)
 torch.cuda.synchronize()
-S.planes.copy_(S0.planes)
-torch.cuda.synchronize()
-t0 = time.perf_counter()
-P, Q, r = g.ple_sliced(S)
-torch.cuda.synchronize()
-print(f"ple e={e} n={n}: {1e3 * (time.perf_counter() - t0):.2f} ms wall, rank {r}")
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+for _ in range(reps):
+    S.planes.copy_(S0.planes)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    P, Q, r = g.ple_sliced(S)
+    torch.cuda.synchronize()
+    print(f"ple e={e} n={n}: {1e3 * (time.perf_counter() - t0):.2f} ms wall, rank {r}", flush=True)
