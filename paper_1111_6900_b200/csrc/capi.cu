@@ -885,9 +885,16 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         CKH(P.alloc(&dCs[sl], (int64_t)e * chunk * nwn * 8), "cudaMallocAsync");
         CKH(P.alloc(&dCp[sl], chunk * wb * 8), "cudaMallocAsync");
     }
-    cudaEvent_t ev_alloc, ev_t0, ev_t1, ev_b, in_ready[2], out_ready[2], d2h_done[2];
-    cudaEvent_t *all[] = {&ev_alloc, &ev_t0, &ev_t1, &ev_b, &in_ready[0], &in_ready[1], &out_ready[0],
-                          &out_ready[1], &d2h_done[0], &d2h_done[1]};
+    // B arrives in column parts (multiples of 256 columns) so the first row chunk's products
+    // start after the first part's upload instead of all of B's
+    constexpr int kMaxBParts = 4;
+    const int nbp = (n >= 4096 && w <= 64) ? kMaxBParts : 1;
+    int64_t cb[kMaxBParts + 1];
+    for (int p = 0; p <= nbp; ++p) cb[p] = p == nbp ? n : round_up(n * p / nbp, 2 * kTcBM);
+    cudaEvent_t ev_alloc, ev_t0, ev_t1, ev_b, in_ready[2], out_ready[2], d2h_done[2], ev_bp[kMaxBParts];
+    cudaEvent_t *all[] = {&ev_alloc,     &ev_t0,       &ev_t1,       &ev_b,     &in_ready[0], &in_ready[1],
+                          &out_ready[0], &out_ready[1], &d2h_done[0], &d2h_done[1], &ev_bp[0],    &ev_bp[1],
+                          &ev_bp[2],     &ev_bp[3]};
     for (cudaEvent_t *ev : all) CKH(cudaEventCreate(ev), "cudaEventCreate");
     struct EvGuard {
         cudaEvent_t **evs;
@@ -895,15 +902,21 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         ~EvGuard() {
             for (int i = 0; i < n; ++i) cudaEventDestroy(*evs[i]);
         }
-    } guard{all, 10};
+    } guard{all, 14};
     CKH(cudaEventRecord(ev_alloc, P.sc), "cudaEventRecord");
     CKH(cudaStreamWaitEvent(P.sh, ev_alloc, 0), "cudaStreamWaitEvent");
     CKH(cudaStreamWaitEvent(P.sd, ev_alloc, 0), "cudaStreamWaitEvent");
 
     CKH(cudaEventRecord(ev_t0, P.sh), "cudaEventRecord");
-    // B once: H2D, slice, transposed operand combinations
-    CKH(cudaMemcpy2DAsync(dBp, wb * 8, B_h, ldb * 8, wb * 8, k, cudaMemcpyHostToDevice, P.sh), "H2D(B)");
-    CKH(cudaEventRecord(ev_b, P.sh), "cudaEventRecord");
+    // B once: H2D (by column parts), slice, transposed operand combinations
+    auto h2d_bpart = [&](int p) -> int {
+        const int64_t w0 = cb[p] * w / 64, w1 = p + 1 == nbp ? wb : cb[p + 1] * w / 64;
+        CKH(cudaMemcpy2DAsync(dBp + w0, wb * 8, B_h + w0, ldb * 8, (w1 - w0) * 8, k, cudaMemcpyHostToDevice, P.sh),
+            "H2D(B)");
+        CKH(cudaEventRecord(ev_bp[p], P.sh), "cudaEventRecord");
+        return GF2E_OK;
+    };
+    if (int rc = h2d_bpart(0)) return rc;
     auto h2d_chunk = [&](int64_t i) -> int {
         const int sl = (int)(i % nslots);
         const int64_t r0 = i * chunk, rows = (m - r0) < chunk ? (m - r0) : chunk;
@@ -921,11 +934,22 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         return GF2E_OK;
     };
     if (int rc = h2d_chunk(0)) return rc;
-    CKH(cudaStreamWaitEvent(P.sc, ev_b, 0), "cudaStreamWaitEvent");
-    CK(launch_slice(e, w, k, n, dBp, wb, dBs, nwn, k * nwn, P.sc), "slice(B)");
+    for (int p = 1; p < nbp; ++p)
+        if (int rc = h2d_bpart(p)) return rc;
+    CKH(cudaEventRecord(ev_b, P.sh), "cudaEventRecord");
     const bool fp4 = use_fp4(0, k);
-    CK(launch_combos_bt(ks, dBs, nwn, k * nwn, k, n, dBt, LB.kwords, LB.b_pstride, LB.kwords, LB.n_pad / 64, fp4, P.sc),
-       "combos(B^T)");
+    // B part p: slice its columns, write its rows [cb[p], cb[p+1]) of the B^T combinations
+    auto prep_bpart = [&](int p) -> int {
+        CKH(cudaStreamWaitEvent(P.sc, ev_bp[p], 0), "cudaStreamWaitEvent");
+        const int64_t c0 = cb[p], nc = cb[p + 1] - c0;
+        const int64_t npad = (p + 1 == nbp ? LB.n_pad : cb[p + 1]) - c0;
+        CK(launch_slice(e, w, k, nc, dBp + c0 * w / 64, wb, dBs + c0 / 64, nwn, k * nwn, P.sc, words_for(nc)),
+           "slice(B)");
+        CK(launch_combos_bt(ks, dBs + c0 / 64, nwn, k * nwn, k, nc, dBt + c0 * LB.kwords, LB.kwords, LB.b_pstride,
+                            LB.kwords, npad / 64, fp4, P.sc),
+           "combos(B^T)");
+        return GF2E_OK;
+    };
     for (int64_t i = 0; i < nchunks; ++i) {
         const int sl = (int)(i % nslots);
         const int64_t r0 = i * chunk, rows = (m - r0) < chunk ? (m - r0) : chunk;
@@ -938,9 +962,14 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         CK(launch_combos_rows(ks, dAs[sl], nwk, rows * nwk, rows, k, dAc, L.kwords, L.a_pstride, L.m_pad, L.kwords,
                               fp4 ? 4 : 2, P.sc),
            "combos(A)");
-        TcArgs ta{dAc, dBt, L.a_pstride, LB.b_pstride, L.kwords, rows, n, L.m_pad, LB.n_pad, dCs[sl], nwn, rows * nwn,
-                  acc ? 1 : 0};
-        {
+        // the first chunk runs one product per B part as the parts arrive; later chunks see all of B
+        for (int p = 0; p < (i == 0 ? nbp : 1); ++p) {
+            const int64_t c0 = i == 0 ? cb[p] : 0, c1 = i == 0 ? cb[p + 1] : n;
+            const int64_t npad = (i == 0 && p + 1 < nbp ? cb[p + 1] : LB.n_pad) - c0;
+            if (i == 0)
+                if (int rc = prep_bpart(p)) return rc;
+            TcArgs ta{dAc, dBt + c0 * LB.kwords, L.a_pstride, LB.b_pstride, L.kwords, rows, c1 - c0, L.m_pad, npad,
+                      dCs[sl] + c0 / 64, nwn, rows * nwn, acc ? 1 : 0};
             ProfScope prof(P.sc);
             CK(launch_product_tc2(ks, ta, tc_form(0, k), P.sc), "product_tc2");
         }

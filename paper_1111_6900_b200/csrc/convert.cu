@@ -80,7 +80,7 @@ __global__ void k_random_sliced(int e, int64_t rows, int64_t cols, uint64_t seed
         }
 #pragma unroll
         for (int t = 0; t < kMaxE; ++t)
-            if (t < e) planes[t * pstride + idx] = acc[t];
+            if (t < e) planes[t * pstride + r * ld + wi] = acc[t];
     }
 }
 
@@ -101,13 +101,13 @@ __global__ void k_random_words(int64_t rows, int64_t ncols, uint64_t seed, uint6
 
 template <int W>
 __global__ void k_slice(int e, int64_t rows, int64_t cols, const uint64_t *__restrict__ packed, int64_t ldp,
-                        uint64_t *__restrict__ planes, int64_t ld, int64_t pstride) {
+                        uint64_t *__restrict__ planes, int64_t ld, int64_t pstride, int64_t wn) {
     constexpr int P = 64 / W;
     const int64_t nw = words_for(cols);
     const int64_t pwords = words_for(cols * W);
-    const int64_t total = rows * ld;
+    const int64_t total = rows * wn;  // wn <= ld plane words written per row (pad words zeroed)
     for (int64_t idx = gtid(); idx < total; idx += gstride()) {
-        int64_t r = idx / ld, wi = idx - r * ld;
+        int64_t r = idx / wn, wi = idx - r * wn;
         uint64_t acc[kMaxE];
 #pragma unroll
         for (int t = 0; t < kMaxE; ++t) acc[t] = 0;
@@ -128,7 +128,7 @@ __global__ void k_slice(int e, int64_t rows, int64_t cols, const uint64_t *__res
         }
 #pragma unroll
         for (int t = 0; t < kMaxE; ++t)
-            if (t < e) planes[t * pstride + idx] = acc[t];
+            if (t < e) planes[t * pstride + r * ld + wi] = acc[t];
     }
 }
 
@@ -182,13 +182,13 @@ __device__ __forceinline__ uint64_t gather_byte(const uint64_t (&v)[8], int b) {
 
 // K1, w = 8: thread = one 64-bit plane word position (64 elements = 8 packed words)
 __global__ void k_slice_w8(int e, int64_t rows, int64_t cols, const uint64_t *__restrict__ packed, int64_t ldp,
-                           uint64_t *__restrict__ planes, int64_t ld, int64_t pstride) {
+                           uint64_t *__restrict__ planes, int64_t ld, int64_t pstride, int64_t wn) {
     const int64_t nw = words_for(cols);
     const int64_t pwords = words_for(cols * 8);
     const uint64_t tm = tail_mask(cols);
-    const int64_t total = rows * ld;
+    const int64_t total = rows * wn;
     for (int64_t idx = gtid(); idx < total; idx += gstride()) {
-        const int64_t r = idx / ld, wi = idx - r * ld;
+        const int64_t r = idx / wn, wi = idx - r * wn;
         uint64_t v[8];
         if (wi < nw) {
             const uint64_t *src = packed + r * ldp + wi * 8;
@@ -214,7 +214,7 @@ __global__ void k_slice_w8(int e, int64_t rows, int64_t cols, const uint64_t *__
             if (t < e) {
                 uint64_t p = gather_byte(v, t);
                 if (wi == nw - 1) p &= tm;
-                planes[t * pstride + idx] = p;
+                planes[t * pstride + r * ld + wi] = p;
             }
         }
     }
@@ -483,15 +483,16 @@ cudaError_t launch_random_words(int64_t rows, int64_t ncols, uint64_t seed, uint
 }
 
 cudaError_t launch_slice(int e, int w, int64_t rows, int64_t cols, const uint64_t *packed, int64_t ldp,
-                         uint64_t *planes, int64_t ld, int64_t pstride, cudaStream_t st) {
-    int64_t total = rows * ld;
+                         uint64_t *planes, int64_t ld, int64_t pstride, cudaStream_t st, int64_t wwords) {
+    const int64_t wn = wwords < 0 ? ld : wwords;
+    int64_t total = rows * wn;
     if (total == 0) return cudaSuccess;
     int g = grid_for(total, 256);
     switch (w) {
-        case 2: k_slice<2><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
-        case 4: k_slice<4><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
-        case 8: k_slice_w8<<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
-        case 16: k_slice<16><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride); break;
+        case 2: k_slice<2><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride, wn); break;
+        case 4: k_slice<4><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride, wn); break;
+        case 8: k_slice_w8<<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride, wn); break;
+        case 16: k_slice<16><<<g, 256, 0, st>>>(e, rows, cols, packed, ldp, planes, ld, pstride, wn); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -13,8 +13,10 @@ cudaError_t launch_random_sliced(int e, int64_t rows, int64_t cols, uint64_t see
                                  int64_t gcols, uint64_t *planes, int64_t ld, int64_t pstride, cudaStream_t st);
 cudaError_t launch_random_words(int64_t rows, int64_t ncols, uint64_t seed, uint64_t *out, int64_t ld,
                                 cudaStream_t st);
+// wwords: plane words written per row (default ld: the words past cols are zeroed); a column
+// window of a wider plane passes words_for(cols) so its neighbours are left alone
 cudaError_t launch_slice(int e, int w, int64_t rows, int64_t cols, const uint64_t *packed, int64_t ldp,
-                         uint64_t *planes, int64_t ld, int64_t pstride, cudaStream_t st);
+                         uint64_t *planes, int64_t ld, int64_t pstride, cudaStream_t st, int64_t wwords = -1);
 cudaError_t launch_cling(int e, int w, int64_t rows, int64_t cols, const uint64_t *planes, int64_t ld,
                          int64_t pstride, uint64_t *packed, int64_t ldp, cudaStream_t st);
 cudaError_t launch_xor(uint64_t *x, int64_t ldx, const uint64_t *y, int64_t ldy, int64_t rows, int64_t nwords,
