@@ -888,7 +888,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     // B arrives in column parts (multiples of 256 columns) so the first row chunk's products
     // start after the first part's upload instead of all of B's
     constexpr int kMaxBParts = 4;
-    const int nbp = (n >= 4096 && w <= 64) ? kMaxBParts : 1;
+    const int nbp = (n >= 8192 && m > chunk) ? kMaxBParts : 1;
     int64_t cb[kMaxBParts + 1];
     for (int p = 0; p <= nbp; ++p) cb[p] = p == nbp ? n : round_up(n * p / nbp, 2 * kTcBM);
     cudaEvent_t ev_alloc, ev_t0, ev_t1, ev_b, in_ready[2], out_ready[2], d2h_done[2], ev_bp[kMaxBParts];
