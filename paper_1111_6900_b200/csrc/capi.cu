@@ -257,15 +257,19 @@ int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 // use the paired fp4 form (two products per TMEM drain) or int8 (double-buffered TMEM).
 constexpr int64_t kFp4MinK = 2048;
 constexpr int kSmallKForm = kFormI8;
+constexpr int64_t kFp4LongK = 8192;  // 8 expander / 4 epilogue warps pay off for long accumulations
 int tc_form(uint32_t flags, int64_t k) {
     if (flags & GF2E_TC_INT8) return kFormI8;
+    if (k >= kFp4LongK) return kFormFp4Long;
     if (k >= kFp4MinK) return kFormFp4;
     if (flags & GF2E_TC_FP4) return kFormFp4Pair;
     return kSmallKForm;
 }
 bool use_fp4(uint32_t flags, int64_t k) { return tc_form(flags, k) != kFormI8; }
 const char *form_name(int form) {
-    return form == kFormFp4Pair ? "k_product_tc2<fp4x2>" : form == kFormFp4 ? "k_product_tc2<fp4>" : "k_product_tc2<i8>";
+    return form == kFormFp4Pair ? "k_product_tc2<fp4x2>"
+           : (form == kFormFp4 || form == kFormFp4Long) ? "k_product_tc2<fp4>"
+                                                        : "k_product_tc2<i8>";
 }
 
 Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags) {

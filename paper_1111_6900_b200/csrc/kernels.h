@@ -70,7 +70,7 @@ constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 128;  // tile rows, tile cols, k
 constexpr int kTcBKFp4 = 256;
 // tensor-core forms of the product kernel: int8; fp4 (k chunks <= 32768); fp4 with two
 // products per accumulator (k < 2048 only)
-constexpr int kFormI8 = 0, kFormFp4 = 1, kFormFp4Pair = 2;
+constexpr int kFormI8 = 0, kFormFp4 = 1, kFormFp4Pair = 2, kFormFp4Long = 3;  // Long: k >= 8192
 constexpr int64_t kFp4PairMaxK = 2047;
 cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, int form, cudaStream_t st);
 

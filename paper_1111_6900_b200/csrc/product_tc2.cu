@@ -94,10 +94,18 @@ constexpr uint32_t EXP_SLEEP_NS = GF2E_EXP_SLEEP_NS;  // expanders waiting for a
 #define GF2E_IDLE_SLEEP_NS 500
 #endif
 constexpr uint32_t IDLE_SLEEP_NS = GF2E_IDLE_SLEEP_NS;  // epilogue (long k only, see below)
-constexpr int NPW = 4;      // expander warps
-constexpr int NEW = 8;      // epilogue warps
+#ifndef GF2E_SPLITX
+#define GF2E_SPLITX 1
+#endif
+// Warp roles (14 warps): expanders 0 .. NPW-1, epilogue NPW .. 11, MMA 12, loader 13.  The
+// fp4 form with A in TMEM (Cfg::SPLIT) uses 8 expander warps — 0-3 expand A rows into TMEM,
+// 4-7 B^T rows into shared memory — and 4 epilogue warps (one per TMEM lane quarter, all 256
+// columns, the E x 8 output words kept in shared memory): its long accumulations leave the
+// epilogue idle, while the MMA waited on expansion.  The other forms use 4 expander warps
+// (A and B^T rows) and 8 epilogue warps (lane quarter x column half).
+constexpr int NPW = 4;  // expander warps (non-split forms)
+constexpr int NEW = 8;  // epilogue warps (non-split forms)
 constexpr int GROUP_M = 8;  // tile rasterisation: row-tiles per column sweep (L2 reuse)
-constexpr int EPI_W0 = NPW;
 constexpr int MMA_WARP = NPW + NEW;
 constexpr int LOAD_WARP = MMA_WARP + 1;
 constexpr int NTHREADS = (NPW + NEW + 2) * 32;
@@ -109,7 +117,7 @@ constexpr uint32_t SF_ONE = 0x7F7F7F7Fu;         // E8M0 1.0
 constexpr uint32_t SF_2P11 = 0x8A8A8A8Au;        // E8M0 2^11 (second product of a pair)
 constexpr int FP4_CHUNK_STAGES = 32768 / 256;   // k-bits per accumulation chunk / bits per stage
 
-template <bool FP4, bool PAIR>
+template <bool FP4, bool PAIR, bool WIDE = false>
 struct Cfg {
     // tile N = 256: two 256-column accumulators for int8; one for fp4 (scale factors in the
     // other 256 TMEM columns).  (An N = 192 double-buffered paired form measured slower: the
@@ -138,12 +146,18 @@ struct Cfg {
     static constexpr int BITS_A = BM * (BK / 8);
     static constexpr int BITS_BYTES = (BM + BNH) * (BK / 8);
     static constexpr int NBUF = FP4 ? 1 : 2;  // TMEM accumulators
-    static constexpr int CH = BNH / 32;                   // 32-column chunks per epilogue half
+    static constexpr bool SPLIT = ATMEM && WIDE && GF2E_SPLITX;  // k >= 8192 (host: kFormFp4Long)
+    static constexpr int NPW = SPLIT ? 8 : 4;             // expander warps
+    static constexpr int NEW = SPLIT ? 4 : 8;             // epilogue warps
+    static constexpr int EPI_W0 = NPW;
+    static_assert(NPW + NEW == MMA_WARP, "warp roles");
+    static constexpr int CH = BN * 4 / NEW / 32;          // 32-column chunks per epilogue warp
+    static constexpr int ACC_SMEM = SPLIT ? kMaxE * CH * 128 * 4 : 0;  // epilogue output words
     // scale-factor TMEM columns (fp4): A (first / second product of a pair) and B
     static constexpr uint32_t SFA0 = ATMEM ? 256 + 32 * S : 256, SFA1 = 320, SFB = ATMEM ? SFA0 + (S >= 7 ? 16 : 32) : 384;
     static_assert(!ATMEM || SFB + (S >= 7 ? 16 : 32) <= 512, "TMEM columns: A stages overlap the scale factors");
     static constexpr uint32_t ATM0 = 256;  // TMEM column of A stage 0 (ATMEM)
-    static constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + BARS_BYTES + 1024;
+    static constexpr int SMEM_BYTES = S * STAGE_BYTES + D * BITS_BYTES + BARS_BYTES + ACC_SMEM + 1024;
     static_assert(SMEM_BYTES <= 232448, "shared memory");
     static_assert(NBUF * BN <= (FP4 ? 384 : 512), "accumulators overlap the scale factors");
 };
@@ -245,9 +259,9 @@ __device__ __forceinline__ void mma2_mxf4(uint32_t d, uint64_t ad, uint64_t bd, 
         : "memory");
 }
 
-template <int E, bool FP4, bool PAIR>
+template <int E, bool FP4, bool PAIR, bool WIDE>
 __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, const TcArgs a) {
-    using C = Cfg<FP4, PAIR>;
+    using C = Cfg<FP4, PAIR, WIDE>;
     constexpr int BN = C::BN, BNH = C::BNH, STAGE_BYTES = C::STAGE_BYTES;
     static_assert(FP4 || !PAIR, "product pairing is an fp4 form");
     // PAIR (k < 2048): two products share one accumulator, the second scaled by 2^11 through
@@ -279,16 +293,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
-            mbar_init(&bars->full[i], 2 * NPW);
+            mbar_init(&bars->full[i], 2 * C::NPW);
             mbar_init(&bars->empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->tfull[i], 1);
-            mbar_init(&bars->tempty[i], 2 * NEW);
+            mbar_init(&bars->tempty[i], 2 * C::NEW);
         }
         for (int i = 0; i < C::D; ++i) {
             mbar_init(&bars->bfull[i], 1);
-            mbar_init(&bars->bempty[i], NPW);
+            mbar_init(&bars->bempty[i], C::NPW);
         }
         mbar_fence_init();
     }
@@ -298,7 +312,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
-    if (FP4 && warp >= EPI_W0 && warp < EPI_W0 + 4) {
+    if (FP4 && warp >= C::EPI_W0 && warp < C::EPI_W0 + 4) {
         // scale factors (columns 256..511: every byte E8M0 1.0) and the first accumulator init
         const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
         for (int c = (int)C::SFA0; c < 512; c += 32)
@@ -318,11 +332,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
     unsigned long long i_g0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(i_g0));
 #endif
-    if (warp < NPW) {
+    if (warp < C::NPW) {
         // ===================== expanders (both CTAs) =====================
         // bit tiles arrive by bulk copy (loader warp); these warps keep no global loads in
         // flight, so the per-stage fence.proxy.async (MEMBAR.ALL.CTA) only drains their STS.
-        const int p = threadIdx.x;  // A row and B^T row of this CTA's half
+        const int p = threadIdx.x & 127;  // A row and B^T row of this CTA's half
+        const bool doA = !C::SPLIT || warp < 4, doB = !C::SPLIT || warp >= 4;  // SPLIT: A or B^T rows
         const uint32_t full_leader = mapa(smem_u32(&bars->full[0]), 0);
         int slot = 0, st = 0;
         uint32_t bph = 0, phase = 0;
@@ -334,8 +349,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             const uint8_t *bs = bits + sl * C::BITS_BYTES + p * 16;
 #pragma unroll
             for (int i = 0; i < NQ / 2; ++i) {
-                v[i] = *reinterpret_cast<const uint4 *>(bs + i * (BM * 16));
-                if (p < BNH) v[NQ / 2 + i] = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + i * (BNH * 16));
+                if (doA) v[i] = *reinterpret_cast<const uint4 *>(bs + i * (BM * 16));
+                if (doB && p < BNH) v[NQ / 2 + i] = *reinterpret_cast<const uint4 *>(bs + C::BITS_A + i * (BNH * 16));
             }
         };
         if (total > 0) {
@@ -346,19 +361,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             TW(i_empty, mbar_wait_sleep(&bars->empty[st], phase ^ 1, EXP_SLEEP_NS));
             uint8_t *sa = stages + st * STAGE_BYTES;
             if constexpr (C::ATMEM) {
-                expand_row_fp4_tmem(tmem + ((uint32_t)((warp & 3) * 32) << 16) + C::ATM0 + (uint32_t)(st * 32), cur[0],
-                                    cur[1]);
-                expand_row_fp4<true>(sa, p, cur[2], cur[3]);
-                tmem_wait_st();
-                tc_fence_before();
+                if (doA) {
+                    expand_row_fp4_tmem(tmem + ((uint32_t)((warp & 3) * 32) << 16) + C::ATM0 + (uint32_t)(st * 32),
+                                        cur[0], cur[1]);
+                }
+                if (doB) expand_row_fp4<true>(sa, p, cur[2], cur[3]);
+                if (doA) {
+                    tmem_wait_st();
+                    tc_fence_before();
+                }
             } else if constexpr (FP4) {
-                expand_row_fp4<false>(sa, p, cur[0], cur[1]);
-                if (p < BNH) expand_row_fp4<true>(sa + A_BYTES, p, cur[2], cur[3]);
+                if (doA) expand_row_fp4<false>(sa, p, cur[0], cur[1]);
+                if (doB && p < BNH) expand_row_fp4<true>(sa + A_BYTES, p, cur[2], cur[3]);
             } else {
-                expand_row<false>(sa, p, cur[0]);
-                expand_row<true>(sa + A_BYTES, p, cur[1]);
+                if (doA) expand_row<false>(sa, p, cur[0]);
+                if (doB) expand_row<true>(sa + A_BYTES, p, cur[1]);
             }
-            fence_proxy_async_smem();
+            if (!C::ATMEM || doB) fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive_cluster(full_leader + (uint32_t)(st * 8));
@@ -416,9 +435,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
         __syncwarp();
     } else if (warp < MMA_WARP) {
         // ===================== epilogue (both CTAs) =====================
-        const int ew = warp - EPI_W0;
+        const int ew = warp - C::EPI_W0;
+        const int et = ew * 32 + lane;  // epilogue thread index
         const int q = warp & 3;  // TMEM lane quarter (hardware: warp id % 4)
-        const int h = ew >> 2;   // column half
+        const int h = ew >> 2;   // column group (two halves with 8 epilogue warps, one with 4)
+        constexpr int EPI_COLS = C::CH * 32;
         const int row_local = (int)rank * BM + q * 32 + lane;
         const int64_t nw = words_for(a.n);
         const uint32_t tempty_leader = mapa(smem_u32(&bars->tempty[0]), 0);
@@ -429,11 +450,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             tile_coords(tile, tiles_m, tiles_n, tm, tn);
             const int64_t m0 = tm * (2 * BM), n0 = tn * BN;
             constexpr int CH = C::CH;
-            uint32_t acc[E][CH];
+            // output words: registers, or shared memory for the 4-warp epilogue (E x 8 words)
+            uint32_t acc_r[C::SPLIT ? 1 : E][C::SPLIT ? 1 : CH];
+            uint32_t *acc_s = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(bars) + BARS_BYTES) + et;
+            auto ACC = [&](int j, int c) -> uint32_t & {
+                if constexpr (C::SPLIT)
+                    return acc_s[(j * CH + c) * 128];
+                else
+                    return acc_r[j][c];
+            };
 #pragma unroll
             for (int j = 0; j < E; ++j)
 #pragma unroll
-                for (int c = 0; c < CH; ++c) acc[j][c] = 0;
+                for (int c = 0; c < CH; ++c) ACC(j, c) = 0;
             for (int t = 0; t < s.nprod; t += STEP) {
                 const uint32_t mask = bars->outmask[t];
                 const uint32_t mask1 = (PAIR && t + 1 < s.nprod) ? bars->outmask[t + 1] : 0u;
@@ -441,15 +470,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                     const int buf = (int)(gp % C::NBUF);
                     TW(i_tfull, mbar_wait_sleep(&bars->tfull[buf], (uint32_t)((gp / C::NBUF) & 1), idle_ns));
                     tc_fence_after();
-                    constexpr int LB = 1;  // chunks per tcgen05.ld wait (batching measured no gain)
+#ifndef GF2E_LDX64
+#define GF2E_LDX64 0
+#endif
+                    // chunks per tcgen05.ld: 1 (x16: 32 columns) or 2 (x32: 64 columns)
+                    constexpr int LB = GF2E_LDX64 ? 2 : 1;
 #pragma unroll
                     for (int c0 = 0; c0 < CH; c0 += LB) {
                         uint32_t v[LB][16];
-#pragma unroll
-                        for (int cc = 0; cc < LB; ++cc)
-                            tmem_ld32_pack16(tmem + ((uint32_t)(q * 32) << 16) +
-                                                 (uint32_t)(buf * BN + h * BNH + (c0 + cc) * 32),
-                                             v[cc]);
+                        const uint32_t ta0 =
+                            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * EPI_COLS + c0 * 32);
+                        if constexpr (LB == 2)
+                            tmem_ld64_pack16(ta0, *reinterpret_cast<uint32_t(*)[32]>(&v[0][0]));
+                        else
+                            tmem_ld32_pack16(ta0, v[0]);
                         tmem_wait_ld();
 #pragma unroll
                         for (int cc = 0; cc < LB; ++cc) {
@@ -460,16 +494,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                                 const uint32_t pw1 = parity_word_packed_shl<4, 0xFDB9>(v[cc]);
 #pragma unroll
                                 for (int j = 0; j < E; ++j)
-                                    acc[j][c] ^=
+                                    ACC(j, c) ^=
                                         (pw0 & (0u - ((mask >> j) & 1u))) ^ (pw1 & (0u - ((mask1 >> j) & 1u)));
                             } else {
                                 const uint32_t pw = parity_word_packed(v[cc]);
+                                if constexpr (C::SPLIT) {
 #pragma unroll
-                                for (int j = 0; j < E; ++j) acc[j][c] ^= pw & (0u - ((mask >> j) & 1u));
+                                    for (int j = 0; j < E; ++j)
+                                        if ((mask >> j) & 1u) ACC(j, c) ^= pw;
+                                } else {
+#pragma unroll
+                                    for (int j = 0; j < E; ++j) ACC(j, c) ^= pw & (0u - ((mask >> j) & 1u));
+                                }
                             }
                             if (FP4) {
                                 const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) +
-                                                    (uint32_t)(buf * BN + h * BNH + c * 32);
+                                                    (uint32_t)(buf * BN + h * EPI_COLS + c * 32);
 #pragma unroll
                                 for (int c8 = 0; c8 < 32; c8 += 8) tmem_st8_const(ta + c8, ACC_INIT);
                             }
@@ -483,32 +523,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             }
             const int64_t row = m0 + row_local;
             if (row < a.m) {
-                const int64_t w0 = (n0 >> 6) + 2 * h;
-                const bool v0 = w0 < nw, v1 = w0 + 1 < nw;
 #pragma unroll
-                for (int j0 = 0; j0 < E; j0 += 4) {  // C0 loads of up to 4 planes in flight per batch
-                    uint64_t old[4][2];
+                for (int wp = 0; wp < CH / 4; ++wp) {  // pairs of 64-bit words of this warp's columns
+                    const int64_t w0 = (n0 >> 6) + (CH / 2) * h + 2 * wp;
+                    const bool v0 = w0 < nw, v1 = w0 + 1 < nw;
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        const int j = j0 + jj;
-                        if (j < E) {
-                            const uint64_t *crow = a.C + j * a.c_pstride + row * a.ldc + w0;
-                            old[jj][0] = (a.accumulate && v0) ? crow[0] : 0;
-                            old[jj][1] = (a.accumulate && v1) ? crow[1] : 0;
+                    for (int j0 = 0; j0 < E; j0 += 4) {  // C0 loads of up to 4 planes in flight per batch
+                        uint64_t old[4][2];
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const int j = j0 + jj;
+                            if (j < E) {
+                                const uint64_t *crow = a.C + j * a.c_pstride + row * a.ldc + w0;
+                                old[jj][0] = (a.accumulate && v0) ? crow[0] : 0;
+                                old[jj][1] = (a.accumulate && v1) ? crow[1] : 0;
+                            }
                         }
-                    }
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        const int j = j0 + jj;
-                        if (j < E) {
-                            uint64_t *crow = a.C + j * a.c_pstride + row * a.ldc + w0;
-                            const uint64_t x0 = ((uint64_t)acc[j][0] | ((uint64_t)acc[j][1] << 32)) ^ old[jj][0];
-                            const uint64_t x1 = ((uint64_t)acc[j][2] | ((uint64_t)acc[j][3] << 32)) ^ old[jj][1];
-                            if (v0 && v1 && !(reinterpret_cast<uintptr_t>(crow) & 15)) {
-                                *reinterpret_cast<ulonglong2 *>(crow) = make_ulonglong2(x0, x1);
-                            } else {
-                                if (v0) crow[0] = x0;
-                                if (v1) crow[1] = x1;
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const int j = j0 + jj;
+                            if (j < E) {
+                                uint64_t *crow = a.C + j * a.c_pstride + row * a.ldc + w0;
+                                const uint64_t x0 =
+                                    ((uint64_t)ACC(j, 4 * wp) | ((uint64_t)ACC(j, 4 * wp + 1) << 32)) ^ old[jj][0];
+                                const uint64_t x1 =
+                                    ((uint64_t)ACC(j, 4 * wp + 2) | ((uint64_t)ACC(j, 4 * wp + 3) << 32)) ^ old[jj][1];
+                                if (v0 && v1 && !(reinterpret_cast<uintptr_t>(crow) & 15)) {
+                                    *reinterpret_cast<ulonglong2 *>(crow) = make_ulonglong2(x0, x1);
+                                } else {
+                                    if (v0) crow[0] = x0;
+                                    if (v1) crow[1] = x1;
+                                }
                             }
                         }
                     }
@@ -574,7 +619,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             g_instr[blockIdx.x][1] = i_bfull;
             g_instr[blockIdx.x][2] = i_tot;
         }
-        if (lane == 0 && warp == EPI_W0) {
+        if (lane == 0 && warp == C::EPI_W0) {
             g_instr[blockIdx.x][3] = i_tfull;
             g_instr[blockIdx.x][4] = i_tot;
         }
@@ -600,13 +645,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
 
 int g_num_sms2 = 0;
 
-template <int E, bool FP4, bool PAIR>
+template <int E, bool FP4, bool PAIR, bool WIDE>
 cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
-    const int smem = Cfg<FP4, PAIR>::SMEM_BYTES;
+    const int smem = Cfg<FP4, PAIR, WIDE>::SMEM_BYTES;
     cudaError_t err =
-        cudaFuncSetAttribute(k_product_tc2<E, FP4, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_product_tc2<E, FP4, PAIR, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    const int64_t tiles = (a.m_pad / (2 * BM)) * (a.n_pad / Cfg<FP4, PAIR>::BN);
+    const int64_t tiles = (a.m_pad / (2 * BM)) * (a.n_pad / Cfg<FP4, PAIR, WIDE>::BN);
     if (tiles == 0) return cudaSuccess;
     if (g_num_sms2 == 0) {
         int dev = 0;
@@ -627,22 +672,22 @@ cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_product_tc2<E, FP4, PAIR>, s, a);
+    return cudaLaunchKernelEx(&cfg, k_product_tc2<E, FP4, PAIR, WIDE>, s, a);
 }
 
-template <bool FP4, bool PAIR>
+template <bool FP4, bool PAIR, bool WIDE>
 cudaError_t launch_any(const Sched &s, const TcArgs &a, cudaStream_t st) {
     switch (s.nout) {
-        case 1: return launch_e<1, FP4, PAIR>(s, a, st);
-        case 2: return launch_e<2, FP4, PAIR>(s, a, st);
-        case 3: return launch_e<3, FP4, PAIR>(s, a, st);
-        case 4: return launch_e<4, FP4, PAIR>(s, a, st);
-        case 5: return launch_e<5, FP4, PAIR>(s, a, st);
-        case 6: return launch_e<6, FP4, PAIR>(s, a, st);
-        case 7: return launch_e<7, FP4, PAIR>(s, a, st);
-        case 8: return launch_e<8, FP4, PAIR>(s, a, st);
-        case 9: return launch_e<9, FP4, PAIR>(s, a, st);
-        case 10: return launch_e<10, FP4, PAIR>(s, a, st);
+        case 1: return launch_e<1, FP4, PAIR, WIDE>(s, a, st);
+        case 2: return launch_e<2, FP4, PAIR, WIDE>(s, a, st);
+        case 3: return launch_e<3, FP4, PAIR, WIDE>(s, a, st);
+        case 4: return launch_e<4, FP4, PAIR, WIDE>(s, a, st);
+        case 5: return launch_e<5, FP4, PAIR, WIDE>(s, a, st);
+        case 6: return launch_e<6, FP4, PAIR, WIDE>(s, a, st);
+        case 7: return launch_e<7, FP4, PAIR, WIDE>(s, a, st);
+        case 8: return launch_e<8, FP4, PAIR, WIDE>(s, a, st);
+        case 9: return launch_e<9, FP4, PAIR, WIDE>(s, a, st);
+        case 10: return launch_e<10, FP4, PAIR, WIDE>(s, a, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -651,9 +696,10 @@ cudaError_t launch_any(const Sched &s, const TcArgs &a, cudaStream_t st) {
 
 cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, int form, cudaStream_t st) {
     switch (form) {
-        case kFormI8: return launch_any<false, false>(s, a, st);
-        case kFormFp4: return launch_any<true, false>(s, a, st);
-        case kFormFp4Pair: return launch_any<true, true>(s, a, st);
+        case kFormI8: return launch_any<false, false, false>(s, a, st);
+        case kFormFp4: return launch_any<true, false, false>(s, a, st);
+        case kFormFp4Long: return launch_any<true, false, true>(s, a, st);
+        case kFormFp4Pair: return launch_any<true, true, false>(s, a, st);
         default: return cudaErrorInvalidValue;
     }
 }
