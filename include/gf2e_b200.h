@@ -200,6 +200,13 @@ int gf2e_row_swaps(int planes, uint64_t *S_dev, int64_t ld, int64_t ps, int64_t 
 int gf2e_col_swaps(int planes, int w, uint64_t *S_dev, int64_t ld, int64_t ps, int64_t rows, int64_t cols,
                    const int64_t *triples_host, int64_t n, void *stream);
 
+/* Row-wise scalar multiples on packed words: out row r = scalars_host[r] * (in row r, or in row
+ * 0 when broadcast != 0).  With broadcast and scalars 0 .. 2^e - 1 this is the Newton-John
+ * multiple table of one row (newton_john.make_table / _table_words, newton_john.py:55-88);
+ * without, PackedMatrix.scale_row for many rows (mat_packed.py:201-205). */
+int gf2e_row_scales(int e, uint32_t f, const uint64_t *in_dev, int64_t ldi, int broadcast, const uint32_t *scalars_host,
+                    uint64_t *out_dev, int64_t ldo, int64_t rows, int64_t cols, void *stream);
+
 /* mul_by_x (mat_sliced.py:109-122): out planes = alpha * in planes (alpha = class of x). */
 int gf2e_mul_by_x(int e, uint32_t f, const uint64_t *in_dev, int64_t ld, int64_t pin, uint64_t *out_dev,
                   int64_t pout, int64_t rows, int64_t cols, void *stream);

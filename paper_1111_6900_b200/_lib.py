@@ -55,6 +55,7 @@ SIGNATURES = {
     "gf2e_echelonize": (_INT, [_INT, _U32, _P, _I64, _I64, _I64, _I64, _INT, ctypes.POINTER(_I64), _P]),
     "gf2e_row_swaps": (_INT, [_INT, _P, _I64, _I64, _I64, _I64, ctypes.POINTER(_I64), _I64, _INT, _P]),
     "gf2e_col_swaps": (_INT, [_INT, _INT, _P, _I64, _I64, _I64, _I64, ctypes.POINTER(_I64), _I64, _P]),
+    "gf2e_row_scales": (_INT, [_INT, _U32, _P, _I64, _INT, ctypes.POINTER(_U32), _P, _I64, _I64, _I64, _P]),
     "gf2e_mul_by_x": (_INT, [_INT, _U32, _P, _I64, _I64, _P, _I64, _I64, _I64, _P]),
     "gf2e_scalar_mul": (_INT, [_INT, _U32, _U32, _P, _I64, _P, _I64, _I64, _I64, _P]),
     "gf2e_plane_mul": (_INT, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _U32, _P, _I64, _P]),

@@ -1199,4 +1199,29 @@ int gf2e_col_swaps(int planes, int w, uint64_t *S, int64_t ld, int64_t ps, int64
     return GF2E_OK;
 }
 
+
+int gf2e_row_scales(int e, uint32_t f, const uint64_t *in, int64_t ldi, int broadcast, const uint32_t *scalars,
+                    uint64_t *out, int64_t ldo, int64_t rows, int64_t cols, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    if (int rc = check_field(e, f)) return rc;
+    const int w = gf2e_pack_width(e);
+    const int64_t nwords = words_for(cols * w);
+    if (int rc = check_mat(in, broadcast ? 1 : rows, nwords, ldi, "in")) return rc;
+    if (int rc = check_mat(out, rows, nwords, ldo, "out")) return rc;
+    for (int64_t r = 0; r < rows; ++r)
+        if (scalars[r] >> e) return fail(GF2E_EINVAL, "scalar %u out of range for GF(2^%d)", scalars[r], e);
+    if (rows == 0 || nwords == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    DevTmp cs((size_t)rows * 4, st);
+    if (!cs.p) return fail(GF2E_ENOMEM, "out of device memory");
+    CKH(cudaMemcpyAsync(cs.p, scalars, rows * 4, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    CK(launch_row_scales(e, f, primitive_element(e, f), w, in, ldi, broadcast != 0, static_cast<uint32_t *>(cs.p), out,
+                         ldo, rows, nwords, st),
+       "row_scales");
+    CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    return GF2E_OK;
+}
+
 }  // extern "C"

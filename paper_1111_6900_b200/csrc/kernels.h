@@ -133,6 +133,10 @@ cudaError_t launch_echelon_marks(int e, uint64_t *S, int64_t ld, int64_t ps, int
 cudaError_t launch_gather_cols(int e, const uint64_t *S, int64_t ld, int64_t ps, const int64_t *Q, int64_t r,
                                uint64_t *out, int64_t ldo, int64_t po, cudaStream_t st);
 
+cudaError_t launch_row_scales(int e, uint32_t f, uint32_t g, int w, const uint64_t *in, int64_t ldi, bool bcast,
+                              const uint32_t *cs, uint64_t *out, int64_t ldo, int64_t rows, int64_t nwords,
+                              cudaStream_t st);
+
 cudaError_t run_fp4_probe(int iters, int mode, const uint8_t *a_img, const uint8_t *b_img, uint32_t *out, int nctas,
                           cudaStream_t st, float *ms);
 cudaError_t run_mma_peak(int cta_group, int iters, int nsms, cudaStream_t st, float *ms);

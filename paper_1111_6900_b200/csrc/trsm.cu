@@ -207,11 +207,57 @@ cudaError_t launch_mul_by_x(int e, uint32_t f, const uint64_t *in, int64_t ld, i
     return cudaGetLastError();
 }
 
+// out row r = c_r * (in row r, or in row 0 when broadcast) on packed words: the NJ multiple
+// table (newton_john.py:55-88) is broadcast row x scalars 0 .. 2^e - 1.  Products via exp/log
+// tables of the field (ple.cu: field_tab).
+__global__ void k_row_scales(int e, const FieldTab *__restrict__ ftab, int w, const uint64_t *__restrict__ in,
+                             int64_t ldi, int bcast, const uint32_t *__restrict__ cs, uint64_t *__restrict__ out,
+                             int64_t ldo, int64_t rows, int64_t nwords) {
+    __shared__ uint16_t ex[1024], lg[1024];
+    const int q1 = (1 << e) - 1;
+    for (int i = threadIdx.x; i <= q1; i += blockDim.x) {
+        ex[i] = ftab->ex[i];
+        lg[i] = ftab->lg[i];
+    }
+    __syncthreads();
+    const int per = 64 / w;
+    const uint64_t emask = (1ULL << e) - 1;
+    const int64_t total = rows * nwords;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / nwords, wi = idx - r * nwords;
+        const uint64_t x = in[(bcast ? 0 : r) * ldi + wi];
+        const uint32_t c = cs[r];
+        uint64_t y = 0;
+        if (c)
+            for (int sl = 0; sl < per; ++sl) {
+                const uint32_t a = (uint32_t)((x >> (sl * w)) & emask);
+                if (a) {
+                    int l = lg[a] + lg[c];
+                    if (l >= q1) l -= q1;
+                    y |= (uint64_t)ex[l] << (sl * w);
+                }
+            }
+        out[r * ldo + wi] = y;
+    }
+}
+
 cudaError_t launch_scalar_mul(int e, uint32_t f, uint32_t c, int w, const uint64_t *in, int64_t ldi, uint64_t *out,
                               int64_t ldo, int64_t rows, int64_t nwords, cudaStream_t st) {
     const int64_t total = rows * nwords;
     if (total == 0) return cudaSuccess;
     k_scalar_mul<<<grid_for(total, 256), 256, 0, st>>>(e, f, c, w, in, ldi, out, ldo, rows, nwords);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_scales(int e, uint32_t f, uint32_t g, int w, const uint64_t *in, int64_t ldi, bool bcast,
+                              const uint32_t *cs, uint64_t *out, int64_t ldo, int64_t rows, int64_t nwords,
+                              cudaStream_t st) {
+    const FieldTab *ftab = field_tab(e, f, g);
+    if (!ftab) return cudaErrorUnknown;
+    const int64_t total = rows * nwords;
+    if (total == 0) return cudaSuccess;
+    k_row_scales<<<grid_for(total, 256), 256, 0, st>>>(e, ftab, w, in, ldi, bcast ? 1 : 0, cs, out, ldo, rows, nwords);
     return cudaGetLastError();
 }
 

@@ -233,6 +233,52 @@ def main():
         pl.append(tag)
     store["ple_tags"] = np.array(pl)
 
+    # Newton-John table routines (newton_john.py): tables, products, elimination, PLE, TRSM,
+    # with the reference's RowOpCounters
+    from gf2elin import newton_john, mat_gf2 as mg
+
+    nj = []
+    for e, m, k, n, seed in [(3, 40, 33, 70, 31), (8, 65, 64, 129, 32), (10, 20, 17, 9, 33)]:
+        ctx = gf2e.field_new(e)
+        A = mat_packed.PackedMatrix.random(ctx, m, k, seed)
+        B = mat_packed.PackedMatrix.random(ctx, k, n, seed + 1)
+        tag = f"nj/e{e}"
+        store[f"{tag}/meta"] = np.array([e, ctx.f, m, k, n], dtype=np.int64)
+        store[f"{tag}/A"] = A.storage.words.copy()
+        store[f"{tag}/B"] = B.storage.words.copy()
+        cnt = mg.RowOpCounters()
+        store[f"{tag}/table"] = newton_john.make_table(B.copy_window(0, 0, 1, n), cnt).words.copy()
+        store[f"{tag}/table_cnt"] = np.array([cnt.scalar_row_muls, cnt.row_adds], dtype=np.int64)
+        cnt = mg.RowOpCounters()
+        store[f"{tag}/mul"] = newton_john.nj_mul(A, B, cnt).storage.words.copy()
+        store[f"{tag}/mul_cnt"] = np.array([cnt.scalar_row_muls, cnt.row_adds], dtype=np.int64)
+        store[f"{tag}/cubic"] = newton_john.cubic_mul(A, B).storage.words.copy()
+        for full in (True, False):
+            X = A.copy()
+            cnt = mg.RowOpCounters()
+            r = newton_john.nj_gauss(X, full=full, counters=cnt)
+            store[f"{tag}/gauss{int(full)}"] = X.storage.words.copy()
+            store[f"{tag}/gauss{int(full)}_meta"] = np.array([r, cnt.scalar_row_muls, cnt.row_adds], dtype=np.int64)
+        X = A.copy()
+        cnt = mg.RowOpCounters()
+        P, Q, r = newton_john.nj_ple(X, cnt)
+        store[f"{tag}/ple"] = X.storage.words.copy()
+        store[f"{tag}/ple_P"] = np.asarray(P, dtype=np.int64)
+        store[f"{tag}/ple_Q"] = np.asarray(Q, dtype=np.int64)
+        store[f"{tag}/ple_meta"] = np.array([r, cnt.scalar_row_muls, cnt.row_adds], dtype=np.int64)
+        R = mat_packed.PackedMatrix.random(ctx, k, k, seed + 2).to_array()
+        up = np.triu(R, 1)
+        np.fill_diagonal(up, (np.arange(k) % (ctx.order - 1)) + 1)
+        U = mat_packed.PackedMatrix.from_array(ctx, up)
+        X = B.copy()
+        cnt = mg.RowOpCounters()
+        newton_john.nj_trsm_upper_left(U, X, cnt)
+        store[f"{tag}/U"] = U.storage.words.copy()
+        store[f"{tag}/trsm"] = X.storage.words.copy()
+        store[f"{tag}/trsm_cnt"] = np.array([cnt.scalar_row_muls, cnt.row_adds], dtype=np.int64)
+        nj.append(tag)
+    store["nj_tags"] = np.array(nj)
+
     np.savez_compressed(OUT, **store)
     print(f"wrote {OUT}: {len(store)} arrays, {os.path.getsize(OUT)} bytes")
 

@@ -115,3 +115,42 @@ def test_perm_helpers(g):
     X = g.PackedMatrix.random(ctx, 0, 5, 1)
     F = g.ple(X)
     assert F.rank == 0 and len(F.P) == 0
+
+
+def test_newton_john_golden(g, golden):
+    # newton_john.py API on device: tables, products, elimination, PLE, TRSM, counters
+    for tag in (str(t) for t in golden["nj_tags"]):
+        e, f, m, k, n = (int(x) for x in golden[f"{tag}/meta"])
+        ctx = g.field_new(e, f)
+        A = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/A"], k)
+        B = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/B"], n)
+        cnt = g.RowOpCounters()
+        row0 = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/B"][:1], n)
+        T = g.make_table(row0, cnt)
+        assert np.array_equal(g._device.to_host_words(T.words), golden[f"{tag}/table"]), tag
+        assert [cnt.scalar_row_muls, cnt.row_adds] == golden[f"{tag}/table_cnt"].tolist()
+        assert np.array_equal(T.row(3).to_numpy(), golden[f"{tag}/table"][3:4])
+        cnt = g.RowOpCounters()
+        assert np.array_equal(g.nj_mul(A, B, cnt).to_numpy(), golden[f"{tag}/mul"]), tag
+        assert [cnt.scalar_row_muls, cnt.row_adds] == golden[f"{tag}/mul_cnt"].tolist()
+        assert np.array_equal(g.cubic_mul(A, B).to_numpy(), golden[f"{tag}/cubic"]), tag
+        for full in (True, False):
+            X = A.copy()
+            cnt = g.RowOpCounters()
+            r = g.nj_gauss(X, full=full, counters=cnt)
+            assert [r, cnt.scalar_row_muls, cnt.row_adds] == golden[f"{tag}/gauss{int(full)}_meta"].tolist()
+            assert np.array_equal(X.to_numpy(), golden[f"{tag}/gauss{int(full)}"]), (tag, full)
+        X = A.copy()
+        cnt = g.RowOpCounters()
+        P, Q, r = g.nj_ple(X, cnt)
+        assert [r, cnt.scalar_row_muls, cnt.row_adds] == golden[f"{tag}/ple_meta"].tolist()
+        assert np.array_equal(P, golden[f"{tag}/ple_P"]) and np.array_equal(Q, golden[f"{tag}/ple_Q"])
+        assert np.array_equal(X.to_numpy(), golden[f"{tag}/ple"]), tag
+        U = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/U"], k)
+        X = B.copy()
+        cnt = g.RowOpCounters()
+        g.nj_trsm_upper_left(U, X, cnt)
+        assert [cnt.scalar_row_muls, cnt.row_adds] == golden[f"{tag}/trsm_cnt"].tolist()
+        assert np.array_equal(X.to_numpy(), golden[f"{tag}/trsm"]), tag
+    with pytest.raises(ValueError, match="single row"):
+        g.make_table(g.PackedMatrix.random(g.field_new(4), 2, 5, 1))
