@@ -29,6 +29,7 @@ from .ple_echelon import (
     trsm_sliced,
     trsm_upper_left,
 )
+from .matfile import load_matrix, parse as parse_matrix, save_matrix, serialize as serialize_matrix
 from .newton_john import NJTable, cubic_mul, make_table, nj_gauss, nj_mul, nj_ple, nj_trsm_upper_left
 from .poly_mul import (
     MulCounters,
@@ -56,6 +57,7 @@ __all__ = [
     "SingularMatrixError", "trsm_upper_left", "trsm_lower_left", "trsm_lower_left_unit", "trsm_sliced",
     "PermVector", "PleFactors", "apply_perm_rows", "apply_perm_cols", "col_swap", "ple", "ple_sliced", "ple_unpack",
     "ple_reconstruct", "echelonize", "echelonize_sliced",
+    "load_matrix", "save_matrix", "parse_matrix", "serialize_matrix",
     "NJTable", "make_table", "cubic_mul", "nj_mul", "nj_gauss", "nj_ple", "nj_trsm_upper_left",
     "MulCounters", "Schedule", "schedule", "karatsuba_mul", "karatsuba_mul_packed", "karatsuba_mul_packed_host", "mzed_mul_host", "addmul", "addmul_packed",
     "reduce_mod_f", "count_products", "mzd_slice_mul", "mzd_slice_addmul", "mzed_mul", "mzed_addmul",

@@ -88,3 +88,32 @@ def test_mul_by_x_and_scalar_mul_golden(g, golden):
             assert np.array_equal(A.scalar_mul(int(c)).to_numpy(), ref), (tag, int(c))
         with pytest.raises(ValueError):
             A.scalar_mul(ctx.order)
+
+
+@pytest.mark.parametrize("e", range(2, 11))
+def test_matrix_file_roundtrip(g, e, tmp_path):
+    # SPEC cli MatrixFile: parse(serialize(A)) == A, canonical text round-trips byte for byte
+    ctx = g.field_new(e)
+    for (m, n) in [(7, 65), (1, 1), (0, 3), (4, 0), (33, 128)]:
+        A = g.PackedMatrix.random(ctx, m, n, 5 + e)
+        text = g.serialize_matrix(A)
+        assert text.startswith(f"gf2e-mat v1 e={e} f={ctx.f:x} rows={m} cols={n} repr=packed\n")
+        B = g.parse_matrix(text)
+        assert isinstance(B, g.PackedMatrix) and B == A
+        assert g.serialize_matrix(B) == text
+        S = g.slice_packed(A)
+        p = tmp_path / f"s{e}_{m}_{n}.txt"
+        g.save_matrix(p, S)
+        T = g.load_matrix(p)
+        assert isinstance(T, g.SlicedMatrix) and np.array_equal(T.to_numpy(), S.to_numpy())
+    ok = "gf2e-mat v1 e=2 f=7 rows=1 cols=2 repr=packed\n1 3\n"
+    assert g.parse_matrix(ok).to_array().tolist() == [[1, 3]]
+    for bad in ["gf2e-mat v1 e=2 f=7 rows=1 cols=2 repr=packed\n1 4\n",   # entry >= 2^e
+                "gf2e-mat v1 e=2 f=7 rows=2 cols=2 repr=packed\n1 3\n",   # missing row
+                "gf2e-mat v1 e=2 f=7 rows=1 cols=2 repr=packed\n1  3\n",  # double space
+                "gf2e-mat v1 e=2 f=7 rows=1 cols=2 repr=packed\n1 A\n",   # uppercase
+                "gf2e-mat v2 e=2 f=7 rows=1 cols=2 repr=packed\n1 3\n",   # version
+                "gf2e-mat v1 e=2 f=5 rows=1 cols=2 repr=packed\n1 3\n",   # reducible f
+                "gf2e-mat v1 e=2 f=7 rows=1 cols=2 repr=packed\n1 3"]:    # no trailing newline
+        with pytest.raises(ValueError):
+            g.parse_matrix(bad)
