@@ -891,14 +891,18 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     }
     // B arrives in column parts (multiples of 256 columns) so the first row chunk's products
     // start after the first part's upload instead of all of B's
-    constexpr int kMaxBParts = 4;
-    const int nbp = (n >= 8192 && m > chunk) ? kMaxBParts : 1;
+    constexpr int kMaxBParts = 8;
+#ifndef GF2E_BPARTS
+#define GF2E_BPARTS 8
+#endif
+    const int nbp = (n >= 8192 && m > chunk) ? GF2E_BPARTS : 1;
+    static_assert(GF2E_BPARTS >= 1 && GF2E_BPARTS <= kMaxBParts, "B parts");
     int64_t cb[kMaxBParts + 1];
     for (int p = 0; p <= nbp; ++p) cb[p] = p == nbp ? n : round_up(n * p / nbp, 2 * kTcBM);
     cudaEvent_t ev_alloc, ev_t0, ev_t1, ev_b, in_ready[2], out_ready[2], d2h_done[2], ev_bp[kMaxBParts];
-    cudaEvent_t *all[] = {&ev_alloc,     &ev_t0,       &ev_t1,       &ev_b,     &in_ready[0], &in_ready[1],
+    cudaEvent_t *all[] = {&ev_alloc,    &ev_t0,       &ev_t1,       &ev_b,        &in_ready[0], &in_ready[1],
                           &out_ready[0], &out_ready[1], &d2h_done[0], &d2h_done[1], &ev_bp[0],    &ev_bp[1],
-                          &ev_bp[2],     &ev_bp[3]};
+                          &ev_bp[2],    &ev_bp[3],    &ev_bp[4],    &ev_bp[5],    &ev_bp[6],    &ev_bp[7]};
     for (cudaEvent_t *ev : all) CKH(cudaEventCreate(ev), "cudaEventCreate");
     struct EvGuard {
         cudaEvent_t **evs;
@@ -906,7 +910,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         ~EvGuard() {
             for (int i = 0; i < n; ++i) cudaEventDestroy(*evs[i]);
         }
-    } guard{all, 14};
+    } guard{all, 18};
     CKH(cudaEventRecord(ev_alloc, P.sc), "cudaEventRecord");
     CKH(cudaStreamWaitEvent(P.sh, ev_alloc, 0), "cudaStreamWaitEvent");
     CKH(cudaStreamWaitEvent(P.sd, ev_alloc, 0), "cudaStreamWaitEvent");
