@@ -499,6 +499,17 @@ struct PleCtx {
 };
 
 // host vector -> device index scratch (synchronous staging: the host buffer may be reused)
+// LAPACK-style swap vector -> the (t, P[t]) pairs that move something
+std::vector<int64_t> swap_pairs(const int64_t *P, int64_t n) {
+    std::vector<int64_t> v;
+    for (int64_t t = 0; t < n; ++t)
+        if (P[t] != t) {
+            v.push_back(t);
+            v.push_back(P[t]);
+        }
+    return v;
+}
+
 // Upload through a ring of pinned staging slots (an event guards each slot's reuse), so the
 // copies stay asynchronous; the device index buffer itself is reused in stream order.
 int put_idx(PleCtx &c, const std::vector<int64_t> &v) {
@@ -544,9 +555,12 @@ int ple_rec(PleCtx &c, int64_t r0, int64_t c0, int64_t m, int64_t n, int64_t *P,
     uint64_t *R = V + n1 / 64;  // right half view
     const int64_t nr = n - n1;
     if (r1 > 0) {
-        std::vector<int64_t> sw(P1.begin(), P1.begin() + r1);
-        if (int rc = put_idx(c, sw)) return rc;
-        CK(launch_row_swaps(c.e, R, c.ld, c.ps, words_for(nr), c.idx, (int)r1, false, c.st), "row_swaps");
+        std::vector<int64_t> sw = swap_pairs(P1.data(), r1);
+        if (!sw.empty()) {
+            if (int rc = put_idx(c, sw)) return rc;
+            CK(launch_row_swaps(c.e, R, c.ld, c.ps, words_for(nr), c.idx, (int)(sw.size() / 2), false, c.st),
+               "row_swaps");
+        }
         // L_top X = right[0:r1]  (the corner with its diagonal = pivots, ple_echelon.py:255-258)
         const int64_t lw = words_for(r1);
         DevTmp lt((size_t)c.e * r1 * lw * 8, c.st);
@@ -574,9 +588,12 @@ int ple_rec(PleCtx &c, int64_t r0, int64_t c0, int64_t m, int64_t n, int64_t *P,
     if (m - r1 > 0)
         if (int rc = ple_rec(c, r0 + r1, c0 + n1, m - r1, nr, P2.data(), Q2.data(), r2)) return rc;
     if (r2 > 0) {
-        std::vector<int64_t> sw(P2.begin(), P2.begin() + r2);  // left rows r1.. (ple_echelon.py:268-271)
-        if (int rc = put_idx(c, sw)) return rc;
-        CK(launch_row_swaps(c.e, V + r1 * c.ld, c.ld, c.ps, n1 / 64, c.idx, (int)r2, false, c.st), "row_swaps");
+        std::vector<int64_t> sw = swap_pairs(P2.data(), r2);  // left rows r1.. (ple_echelon.py:268-271)
+        if (!sw.empty()) {
+            if (int rc = put_idx(c, sw)) return rc;
+            CK(launch_row_swaps(c.e, V + r1 * c.ld, c.ld, c.ps, n1 / 64, c.idx, (int)(sw.size() / 2), false, c.st),
+               "row_swaps");
+        }
         std::vector<int64_t> tr;  // compress the right half's L into the leading columns (:275-279)
         for (int64_t u = 0; u < r2; ++u)
             if (n1 + u != r1 + u) tr.insert(tr.end(), {r1 + u, n1 + u, r1 + u});
@@ -1169,13 +1186,15 @@ int gf2e_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t rows
         if (swaps[i] < i || swaps[i] >= rows)
             return fail(GF2E_EINVAL, "swap target %lld at index %lld invalid for %lld rows", (long long)swaps[i],
                         (long long)i, (long long)rows);
-    if (n == 0 || nwords == 0) return GF2E_OK;
+    std::vector<int64_t> pr = swap_pairs(swaps, n);
+    if (pr.empty() || nwords == 0) return GF2E_OK;
     if (int rc = check_device()) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    DevTmp ix((size_t)n * 8, st);
+    DevTmp ix(pr.size() * 8, st);
     if (!ix.p) return fail(GF2E_ENOMEM, "out of device memory");
-    CKH(cudaMemcpyAsync(ix.p, swaps, n * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
-    CK(launch_row_swaps(planes, S, ld, ps, nwords, static_cast<int64_t *>(ix.p), (int)n, backward != 0, st),
+    CKH(cudaMemcpyAsync(ix.p, pr.data(), pr.size() * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    CK(launch_row_swaps(planes, S, ld, ps, nwords, static_cast<int64_t *>(ix.p), (int)(pr.size() / 2), backward != 0,
+                        st),
        "row_swaps");
     CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     return GF2E_OK;

@@ -353,21 +353,21 @@ __global__ void __launch_bounds__(256) k_ple_apply(uint64_t *__restrict__ S, int
     }
 }
 
-// swaps[t] (t < n) applied in order to rows row0+t <-> row0+swaps[t]; thread = (plane, word)
+// (a, b) row pairs applied in order (backward: reverse order); the host drops identity
+// entries of a swap vector, so a random matrix's factorisation swaps almost nothing.
+// Thread = (plane, word).
 __global__ void k_row_swaps(int planes, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t nwords,
-                            const int64_t *__restrict__ swaps, int n, int backward) {
+                            const int64_t *__restrict__ pairs, int n, int backward) {
     const int64_t total = (int64_t)planes * nwords;
     for (int64_t idx = gtid(); idx < total; idx += gstride()) {
         const int64_t b = idx / nwords, w = idx % nwords;
         uint64_t *col = S + b * ps + w;
         for (int i = 0; i < n; ++i) {
-            const int t = backward ? n - 1 - i : i;
-            const int64_t q = swaps[t];
-            if (q != t) {
-                const uint64_t x = col[t * ld];
-                col[t * ld] = col[q * ld];
-                col[q * ld] = x;
-            }
+            const int u = backward ? n - 1 - i : i;
+            const int64_t ra = pairs[2 * u], rb = pairs[2 * u + 1];
+            const uint64_t x = col[ra * ld];
+            col[ra * ld] = col[rb * ld];
+            col[rb * ld] = x;
         }
     }
 }
