@@ -7,15 +7,6 @@
 namespace gf2e {
 namespace tc {
 
-// byte offset of 16-byte chunk c of row r in a K-major SWIZZLE_128B tile (8-row atoms of 1 KiB)
-// 16-byte read-only global load (non-coherent path, no L1 allocation)
-__device__ __forceinline__ uint4 ldg_nc_v4(const uint64_t *ptr) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(ptr));
-    return v;
-}
 __device__ __forceinline__ uint32_t swz(int r, int c) {
     return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
 }
@@ -33,25 +24,10 @@ __device__ __forceinline__ void expand_row(uint8_t *tile, int r, uint4 w4) {
     }
 }
 
-// 32 parity bits (bit 7 of each s32 accumulator) packed into one word with 3 PRMT per 4
-// values plus one shift+LOP3 per 4 values.  Result bit 8b+g = parity of v[4g+b]; the
-// producers load B^T rows in the matching order (b_row_perm) so this is column n0+8b+g.
-__device__ __forceinline__ uint32_t parity_word(const uint32_t (&v)[32]) {
-    uint32_t r = 0;
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        const uint32_t lo = __byte_perm(v[4 * g], v[4 * g + 1], 0x0040);
-        const uint32_t hi = __byte_perm(v[4 * g + 2], v[4 * g + 3], 0x0040);
-        const uint32_t z = __byte_perm(lo, hi, 0x5410);  // bytes: v[4g].b0 .. v[4g+3].b0
-        r |= (z >> (7 - g)) & (0x01010101u << g);
-    }
-    return r;
-}
-
 // parity_word from pack::16b registers (v[i] = column 2i | column 2i+1 << 16): PRMT with
 // sign-replicating selectors turns the bit-7 of 4 columns into 4 byte masks (0x00 / 0xFF) in
-// one instruction, and one LOP3 merges them: 16 ALU ops per 32 columns, same bit order as
-// parity_word (bit 8b+g = column 4g+b).
+// one instruction, and one LOP3 merges them: 16 ALU ops per 32 columns; bit 8b+g of the
+// result = column 4g+b (the B^T row permutation tc_b_row_inv undoes this order).
 __device__ __forceinline__ uint32_t parity_word_packed(const uint32_t (&v)[16]) {
     uint32_t r = 0;
 #pragma unroll
@@ -74,20 +50,6 @@ __device__ __forceinline__ uint32_t parity_word_packed_shl(const uint32_t (&v)[1
         uint32_t w;
         asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w) : "r"(v[2 * g] << SHIFT), "r"(v[2 * g + 1] << SHIFT), "n"(SEL));
         r |= w & (0x01010101u << g);
-    }
-    return r;
-}
-
-// Half of parity_word: 16 accumulators = groups g0 .. g0+3 of a 32-column chunk.
-__device__ __forceinline__ uint32_t parity_half(const uint32_t (&v)[16], int g0) {
-    uint32_t r = 0;
-#pragma unroll
-    for (int gg = 0; gg < 4; ++gg) {
-        const int g = g0 + gg;
-        const uint32_t lo = __byte_perm(v[4 * gg], v[4 * gg + 1], 0x0040);
-        const uint32_t hi = __byte_perm(v[4 * gg + 2], v[4 * gg + 3], 0x0040);
-        const uint32_t z = __byte_perm(lo, hi, 0x5410);
-        r |= (z >> (7 - g)) & (0x01010101u << g);
     }
     return r;
 }
@@ -121,17 +83,6 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
 // tcgen05.wait::ld.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra.uni DONEC_%=;\n\t"
-        "bra.uni WAITC_%=;\n"
-        "DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
 }
 __device__ __forceinline__ void tmem_alloc2(uint32_t *dst_smem, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
