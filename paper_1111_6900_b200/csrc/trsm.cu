@@ -35,7 +35,7 @@ template <int E>
 __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__ ftab, const uint64_t *__restrict__ T,
                                                    int64_t ldt, int64_t pt, int64_t m, int upper, int unit,
                                                    uint64_t *__restrict__ Tinv, int *__restrict__ bad_row) {
-    __shared__ uint64_t pub[2][E];  // the published row X_i
+    __shared__ uint64_t pub[2][2][E];  // the published row X_i, double-buffered by step parity
     __shared__ uint16_t sinv[1 << E], smk[(1 << E) * E];
     for (int i = threadIdx.x; i < (1 << E); i += TB) {
         sinv[i] = ftab->inv[i];
@@ -95,9 +95,11 @@ __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__
 #pragma unroll
                 for (int w = 0; w < 2; ++w) {
                     x[b][w] = y[b][w];
-                    pub[w][b] = y[b][w];
+                    pub[step & 1][w][b] = y[b][w];
                 }
         }
+        // one barrier per row: pub[step & 1] is rewritten two steps later, after every reader
+        // of this step has passed the next step's barrier
         __syncthreads();
         const bool below = upper ? (k < i) : (k > i && k < rows);
         if (below) {
@@ -110,13 +112,12 @@ __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__
                     for (int w = 0; w < 2; ++w) {
                         uint64_t acc = 0;
 #pragma unroll
-                        for (int p = 0; p < E; ++p) acc ^= pub[w][p] & (0ULL - (uint64_t)((mk >> p) & 1u));
+                        for (int p = 0; p < E; ++p) acc ^= pub[step & 1][w][p] & (0ULL - (uint64_t)((mk >> p) & 1u));
                         x[b][w] ^= acc;
                     }
                 }
             }
         }
-        __syncthreads();
     }
     // Tinv block = e planes of TB rows x TB/64 words
     uint64_t *out = Tinv + (int64_t)blockIdx.x * E * TB * (TB / 64);
