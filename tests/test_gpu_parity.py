@@ -295,3 +295,25 @@ def test_config5_sampled_blocks(g):
     if free < 60 * 2**30:
         pytest.skip("needs ~60 GiB of free HBM")
     _sampled_blocks(g, 8, 65536, 65536, 65536, False, [0, 255, 40000, 65535], (65536 - 256, 65536))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_shapes(g, seed):
+    # random e, shapes (ragged, word-boundary-crossing, some long-k for the fp4 forms) and
+    # addmul/mul, every backend, against the oracle
+    rng = np.random.default_rng(1000 + seed)
+    e = int(rng.integers(2, 11))
+    m, n = (int(x) for x in rng.integers(1, 700, size=2))
+    k = int(rng.integers(1, 700)) if seed % 3 else int(rng.integers(2048, 9000))
+    ctx = g.field_new(e)
+    SA = g.SlicedMatrix.random(ctx, m, k, seed + 1)
+    SB = g.SlicedMatrix.random(ctx, k, n, seed + 2)
+    ref, _ = oracle.karatsuba(e, ctx.f, oracle.sliced_random(e, m, k, seed + 1),
+                              oracle.sliced_random(e, k, n, seed + 2), m, k, n)
+    c0 = oracle.sliced_random(e, m, n, seed + 3)
+    for backend in BACKENDS:
+        C = g.karatsuba_mul(SA, SB, backend=backend)
+        assert np.array_equal(C.to_numpy(), ref), (e, m, k, n, backend)
+        C0 = g.SlicedMatrix.random(ctx, m, n, seed + 3)
+        g.addmul(C0, SA, SB, backend=backend)
+        assert np.array_equal(C0.to_numpy(), ref ^ c0), (e, m, k, n, backend, "addmul")
