@@ -401,11 +401,15 @@ struct TrsmLayout {
     int64_t nblk, inv_bytes, tmp_bytes, mul_bytes, total;
 };
 
+// diagonal block size: 256 when the solve is big enough that leaf products dominate
+int trsm_block(int64_t m, int64_t n) { return (m >= 1024 && n >= 4096) ? 256 : 128; }
+
 TrsmLayout trsm_layout(int nprod, int e, int64_t m, int64_t n) {
     TrsmLayout T;
-    T.nblk = (m + kTrsmBlock - 1) / kTrsmBlock;
-    T.inv_bytes = align256(T.nblk * e * kTrsmBlock * (kTrsmBlock / 64) * 8);
-    T.tmp_bytes = align256((int64_t)e * kTrsmBlock * words_for(n) * 8);
+    const int64_t tb = trsm_block(m, n);
+    T.nblk = (m + tb - 1) / tb;
+    T.inv_bytes = align256(T.nblk * e * tb * (tb / 64) * 8);
+    T.tmp_bytes = align256((int64_t)e * tb * words_for(n) * 8);
     T.mul_bytes = layout_for(nprod, m, m, n, 0).total;  // bounds every update and block product
     T.total = T.inv_bytes + T.tmp_bytes + 256 + T.mul_bytes;
     return T;
@@ -423,23 +427,25 @@ struct TrsmCtx {
     int64_t mulws_bytes;
     int e;
     cudaStream_t st;
+    int64_t tb;  // diagonal block rows
 };
 
 int trsm_rec(TrsmCtx &c, int64_t i0, int64_t i1) {
     const int64_t rows = i1 - i0;
     const int64_t nw = words_for(c.n);
-    if (rows <= kTrsmBlock) {  // X = inv(T_blk) . B_blk  (tensor-core product), then copy back
-        const uint64_t *Ib = c.inv + (i0 / kTrsmBlock) * c.e * kTrsmBlock * (kTrsmBlock / 64);
-        if (int rc = run_product(c.ks, Ib, kTrsmBlock / 64, kTrsmBlock * (kTrsmBlock / 64), c.B + i0 * c.ldb, c.ldb,
-                                 c.pb, c.tmp, nw, kTrsmBlock * nw, rows, rows, c.n, 0, c.mulws, c.mulws_bytes, c.st))
+    const int64_t tb = c.tb;
+    if (rows <= tb) {  // X = inv(T_blk) . B_blk  (tensor-core product), then copy back
+        const uint64_t *Ib = c.inv + (i0 / tb) * c.e * tb * (tb / 64);
+        if (int rc = run_product(c.ks, Ib, tb / 64, tb * (tb / 64), c.B + i0 * c.ldb, c.ldb, c.pb, c.tmp, nw, tb * nw,
+                                 rows, rows, c.n, 0, c.mulws, c.mulws_bytes, c.st))
             return rc;
         for (int t = 0; t < c.e; ++t)
-            CKH(cudaMemcpy2DAsync(c.B + t * c.pb + i0 * c.ldb, c.ldb * 8, c.tmp + t * kTrsmBlock * nw, nw * 8, nw * 8,
+            CKH(cudaMemcpy2DAsync(c.B + t * c.pb + i0 * c.ldb, c.ldb * 8, c.tmp + t * tb * nw, nw * 8, nw * 8,
                                   rows, cudaMemcpyDeviceToDevice, c.st),
                 "trsm copy");
         return GF2E_OK;
     }
-    const int64_t h = i0 + round_up(rows / 2, kTrsmBlock);  // aligned split: plane views stay word aligned
+    const int64_t h = i0 + round_up(rows / 2, tb);  // aligned split: plane views stay word aligned
     auto update = [&](int64_t r0, int64_t r1, int64_t k0, int64_t k1) {  // B[r0:r1] ^= T[r0:r1, k0:k1] X[k0:k1]
         return run_product(c.ks, c.T + r0 * c.ldt + k0 / 64, c.ldt, c.pt, c.B + k0 * c.ldb, c.ldb, c.pb,
                            c.B + r0 * c.ldb, c.ldb, c.pb, r1 - r0, k1 - k0, c.n, GF2E_ACCUMULATE, c.mulws,
@@ -1057,7 +1063,8 @@ int trsm_impl(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, in
     void *mulws = w + L.inv_bytes + L.tmp_bytes + 256;
     const int big = 0x7fffffff;
     CKH(cudaMemcpyAsync(flag, &big, sizeof(int), cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
-    CK(launch_tri_inverse(e, f, primitive_element(e, f), T, ldt, pt, m, upper != 0, unit_diag != 0, inv, flag, st),
+    CK(launch_tri_inverse(e, f, primitive_element(e, f), T, ldt, pt, m, upper != 0, unit_diag != 0, inv, flag,
+                          trsm_block(m, n), st),
        "tri_inverse");
     int bad = big;
     if (check) {  // PLE corners skip this: their diagonal is the (nonzero) pivots
@@ -1068,7 +1075,8 @@ int trsm_impl(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, in
         if (bad_row) *bad_row = bad;
         return fail(GF2E_ESINGULAR, "zero diagonal entry at index %d", bad);
     }
-    TrsmCtx c{to_kernel_sched(e, S), upper != 0, T, ldt, pt, B, ldb, pb, n, inv, tmp, mulws, L.mul_bytes, e, st};
+    TrsmCtx c{to_kernel_sched(e, S), upper != 0, T, ldt, pt, B, ldb, pb, n, inv, tmp, mulws, L.mul_bytes, e, st,
+              trsm_block(m, n)};
     return trsm_rec(c, 0, m);
 }
 }  // namespace

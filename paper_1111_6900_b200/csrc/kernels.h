@@ -91,10 +91,11 @@ constexpr int kM4BM = 512, kM4BN = 1024, kM4KPAD = 64;
 cudaError_t launch_product_m4rm(const Sched &s, const M4rmArgs &a, cudaStream_t st);
 
 // trsm.cu
-constexpr int kTrsmBlock = 128;  // diagonal block of the blocked TRSM (plane-word aligned)
-size_t tri_inverse_smem();
+// diagonal blocks of the blocked TRSM: 256 rows (full product tiles, k = 256 leaf products)
+// for large solves, 128 rows for small / narrow ones (half the inverse's sequential chain)
+constexpr int kTrsmBlockMax = 256;
 cudaError_t launch_tri_inverse(int e, uint32_t f, uint32_t g, const uint64_t *T, int64_t ldt, int64_t pt, int64_t m,
-                               bool upper, bool unit, uint64_t *Tinv, int *bad_row, cudaStream_t st);
+                               bool upper, bool unit, uint64_t *Tinv, int *bad_row, int block, cudaStream_t st);
 cudaError_t launch_mul_by_x(int e, uint32_t f, const uint64_t *in, int64_t ld, int64_t pin, uint64_t *out,
                             int64_t pout, int64_t rows, int64_t nwords, cudaStream_t st);
 cudaError_t launch_scalar_mul(int e, uint32_t f, uint32_t c, int w, const uint64_t *in, int64_t ldi, uint64_t *out,

@@ -22,7 +22,6 @@ __device__ __forceinline__ uint32_t gf_mul_slow(uint32_t a, uint32_t b, int e, u
     return acc;
 }
 
-constexpr int TB = kTrsmBlock;  // 128
 
 // Inverse of each 128 x 128 diagonal block by bitsliced substitution: thread k owns row k of
 // the block and of its inverse X (two words per plane each, in registers).  Lower triangular:
@@ -31,11 +30,12 @@ constexpr int TB = kTrsmBlock;  // 128
 // sum_{i<k} T_ki X_i)).  Upper: the same from the bottom.  Scalar * bitsliced word uses the
 // field's multiplication matrices (FieldTab.mulmask: plane b of c*v = XOR of the planes in
 // mulmask[c][b]).
-template <int E>
+template <int E, int TB>  // TB = diagonal block rows = threads
 __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__ ftab, const uint64_t *__restrict__ T,
                                                    int64_t ldt, int64_t pt, int64_t m, int upper, int unit,
                                                    uint64_t *__restrict__ Tinv, int *__restrict__ bad_row) {
-    __shared__ uint64_t pub[2][2][E];  // the published row X_i, double-buffered by step parity
+    constexpr int NW = TB / 64;           // plane words per block row
+    __shared__ uint64_t pub[2][NW][E];    // the published row X_i, double-buffered by step parity
     __shared__ uint16_t sinv[1 << E], smk[(1 << E) * E];
     for (int i = threadIdx.x; i < (1 << E); i += TB) {
         sinv[i] = ftab->inv[i];
@@ -46,30 +46,35 @@ __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__
     const int64_t r0 = (int64_t)blockIdx.x * TB;
     const int rows = (int)((m - r0) < TB ? (m - r0) : TB);
     const int k = threadIdx.x;
-    uint64_t t[E][2], x[E][2];
+    uint64_t t[E][NW], x[E][NW];
 #pragma unroll
     for (int b = 0; b < E; ++b)
 #pragma unroll
-        for (int w = 0; w < 2; ++w) {
+        for (int w = 0; w < NW; ++w) {
             t[b][w] = 0;
             x[b][w] = 0;
         }
     if (k < rows) {
         const uint64_t *src = T + (r0 + k) * ldt + (r0 >> 6);
-        const int nw = (int)((r0 + TB <= m) ? 2 : ((rows + 63) >> 6));
+        const int nw = (rows + 63) >> 6;
 #pragma unroll
         for (int b = 0; b < E; ++b)
-        {
-            t[b][0] = src[b * pt];
-            if (nw > 1) t[b][1] = src[b * pt + 1];
-        }
-        x[0][0] = (k < 64) ? (1ULL << k) : 0ULL;  // identity row
-        x[0][1] = (k < 64) ? 0ULL : (1ULL << (k - 64));
+#pragma unroll
+            for (int w = 0; w < NW; ++w)
+                if (w < nw) t[b][w] = src[b * pt + w];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) x[0][w] = ((k >> 6) == w) ? (1ULL << (k & 63)) : 0ULL;  // identity row
     }
     auto entry = [&](int c) {  // T[k][c] as a field element
         uint32_t v = 0;
 #pragma unroll
-        for (int b = 0; b < E; ++b) v |= (uint32_t)((((c >> 6) ? t[b][1] : t[b][0]) >> (c & 63)) & 1ULL) << b;
+        for (int b = 0; b < E; ++b) {
+            uint64_t wv = t[b][0];
+#pragma unroll
+            for (int w = 1; w < NW; ++w)
+                if ((c >> 6) == w) wv = t[b][w];
+            v |= (uint32_t)((wv >> (c & 63)) & 1ULL) << b;
+        }
         return v;
     };
     if (!unit && k < rows && entry(k) == 0) atomicMin(bad_row, (int)(r0 + k));
@@ -78,25 +83,23 @@ __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__
         if (k == i) {
             uint32_t c = unit ? 1u : sinv[entry(i)];
             if (c == 0) c = 1;  // singular block: reported above, result unused
-            uint64_t y[E][2];
 #pragma unroll
-            for (int b = 0; b < E; ++b) {
-                const uint32_t mk = smk[c * E + b];
+            for (int w = 0; w < NW; ++w) {
+                uint64_t y[E];
 #pragma unroll
-                for (int w = 0; w < 2; ++w) {
+                for (int b = 0; b < E; ++b) {
+                    const uint32_t mk = smk[c * E + b];
                     uint64_t acc = 0;
 #pragma unroll
                     for (int p = 0; p < E; ++p) acc ^= x[p][w] & (0ULL - (uint64_t)((mk >> p) & 1u));
-                    y[b][w] = acc;
+                    y[b] = acc;
+                }
+#pragma unroll
+                for (int b = 0; b < E; ++b) {
+                    x[b][w] = y[b];
+                    pub[step & 1][w][b] = y[b];
                 }
             }
-#pragma unroll
-            for (int b = 0; b < E; ++b)
-#pragma unroll
-                for (int w = 0; w < 2; ++w) {
-                    x[b][w] = y[b][w];
-                    pub[step & 1][w][b] = y[b][w];
-                }
         }
         // one barrier per row: pub[step & 1] is rewritten two steps later, after every reader
         // of this step has passed the next step's barrier
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__
                 for (int b = 0; b < E; ++b) {
                     const uint32_t mk = smk[c * E + b];
 #pragma unroll
-                    for (int w = 0; w < 2; ++w) {
+                    for (int w = 0; w < NW; ++w) {
                         uint64_t acc = 0;
 #pragma unroll
                         for (int p = 0; p < E; ++p) acc ^= pub[step & 1][w][p] & (0ULL - (uint64_t)((mk >> p) & 1u));
@@ -119,12 +122,12 @@ __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__
             }
         }
     }
-    // Tinv block = e planes of TB rows x TB/64 words
-    uint64_t *out = Tinv + (int64_t)blockIdx.x * E * TB * (TB / 64);
+    // Tinv block = e planes of TB rows x NW words
+    uint64_t *out = Tinv + (int64_t)blockIdx.x * E * TB * NW;
 #pragma unroll
     for (int b = 0; b < E; ++b)
 #pragma unroll
-        for (int w = 0; w < 2; ++w) out[(int64_t)b * TB * (TB / 64) + k * (TB / 64) + w] = (k < rows) ? x[b][w] : 0;
+        for (int w = 0; w < NW; ++w) out[(int64_t)b * TB * NW + k * NW + w] = (k < rows) ? x[b][w] : 0;
 }
 
 // mat_sliced.py:109-122: slices shift up one degree, the top slice folds into the slices
@@ -171,33 +174,40 @@ inline int grid_for(int64_t total, int threads) {
 
 }  // namespace
 
-size_t tri_inverse_smem() { return 0; }
-
-template <int E>
+template <int E, int TB>
 cudaError_t launch_tri_e(const FieldTab *ftab, const uint64_t *T, int64_t ldt, int64_t pt, int64_t m, bool upper,
                          bool unit, uint64_t *Tinv, int *bad_row, int64_t nblk, cudaStream_t st) {
-    k_tri_inverse<E><<<(unsigned)nblk, TB, 0, st>>>(ftab, T, ldt, pt, m, upper ? 1 : 0, unit ? 1 : 0, Tinv, bad_row);
+    k_tri_inverse<E, TB><<<(unsigned)nblk, TB, 0, st>>>(ftab, T, ldt, pt, m, upper ? 1 : 0, unit ? 1 : 0, Tinv,
+                                                        bad_row);
     return cudaGetLastError();
 }
 
-cudaError_t launch_tri_inverse(int e, uint32_t f, uint32_t g, const uint64_t *T, int64_t ldt, int64_t pt, int64_t m,
-                               bool upper, bool unit, uint64_t *Tinv, int *bad_row, cudaStream_t st) {
-    const FieldTab *ftab = field_tab(e, f, g);
-    if (!ftab) return cudaErrorUnknown;
+template <int TB>
+cudaError_t launch_tri_tb(int e, const FieldTab *ftab, const uint64_t *T, int64_t ldt, int64_t pt, int64_t m,
+                          bool upper, bool unit, uint64_t *Tinv, int *bad_row, cudaStream_t st) {
     const int64_t nblk = (m + TB - 1) / TB;
     if (nblk == 0) return cudaSuccess;
     switch (e) {
-        case 2: return launch_tri_e<2>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
-        case 3: return launch_tri_e<3>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
-        case 4: return launch_tri_e<4>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
-        case 5: return launch_tri_e<5>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
-        case 6: return launch_tri_e<6>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
-        case 7: return launch_tri_e<7>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
-        case 8: return launch_tri_e<8>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
-        case 9: return launch_tri_e<9>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
-        case 10: return launch_tri_e<10>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 2: return launch_tri_e<2, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 3: return launch_tri_e<3, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 4: return launch_tri_e<4, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 5: return launch_tri_e<5, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 6: return launch_tri_e<6, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 7: return launch_tri_e<7, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 8: return launch_tri_e<8, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 9: return launch_tri_e<9, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 10: return launch_tri_e<10, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_tri_inverse(int e, uint32_t f, uint32_t g, const uint64_t *T, int64_t ldt, int64_t pt, int64_t m,
+                               bool upper, bool unit, uint64_t *Tinv, int *bad_row, int block, cudaStream_t st) {
+    const FieldTab *ftab = field_tab(e, f, g);
+    if (!ftab) return cudaErrorUnknown;
+    if (block == 256) return launch_tri_tb<256>(e, ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, st);
+    if (block == 128) return launch_tri_tb<128>(e, ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, st);
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_mul_by_x(int e, uint32_t f, const uint64_t *in, int64_t ld, int64_t pin, uint64_t *out,

@@ -37,7 +37,7 @@ def test_trsm_golden(g, golden):
             assert np.array_equal(B.to_numpy(), golden[f"{tag}/{key}"]), (tag, key)
 
 
-@pytest.mark.parametrize("e,m,n", [(8, 1000, 3000), (4, 2048, 700), (10, 513, 1025)])
+@pytest.mark.parametrize("e,m,n", [(8, 1000, 3000), (4, 2048, 700), (10, 513, 1025), (8, 1100, 4200), (5, 2304, 4096)])
 def test_trsm_identity_large(g, e, m, n):
     # U X = B and L X = B checked with the (separately verified) product kernel
     import torch
