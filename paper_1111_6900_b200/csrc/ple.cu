@@ -6,7 +6,7 @@
 //     is nonzero as pivot, swaps it to r, rescales the pivot row right of j by 1/pivot, and
 //     XORs x_i * (pivot row right of j) into every row below (the multiplier x_i stays in
 //     place as L).  Only the pivot search and the pivot row are sequential, so:
-//       phase 1 (one CTA): keeps a window of the first 512 row positions in shared memory,
+//       phase 1 (one CTA): keeps a window of the first 128 row positions in shared memory,
 //         reduced step by step; finds each pivot there (or, if the window has none, scans the
 //         rows below it lazily, reducing each candidate by the pivots found so far); records
 //         the pivots, the swaps, and the basis tables alpha^s * T_t of every scaled pivot
@@ -42,7 +42,7 @@ __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * block
 __device__ FieldTab g_field_tabs[kFieldTabSlots];
 
 #ifndef GF2E_PLE_WIN
-#define GF2E_PLE_WIN 512
+#define GF2E_PLE_WIN 128
 #endif
 constexpr int PT = GF2E_PLE_WIN;  // phase-1 threads = window rows
 constexpr int KP = 64;   // pivots per panel (one plane word)
