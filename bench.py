@@ -167,9 +167,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the multi-rank flow on a one-GPU box (not a measurement): every rank
+    # on cuda:0, host-side gloo collectives (kernels of different ranks never wait on each other)
+    if args.dist_backend == "gloo-shared-gpu":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "gloo-shared-gpu":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
     name, e, m, k, n, acc, scaling = workload(args.config, args.e, world)
@@ -347,6 +354,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunk-rows", type=int, default=0, help="row chunk of the host-buffer e2e call (0: library default)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo-shared-gpu"],
+                    help="gloo-shared-gpu: functional multi-rank check with every rank on cuda:0 (no timing meaning)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
