@@ -111,6 +111,15 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+def host_threads() -> int:
+    """All host cores this process may use (torchrun sets OMP_NUM_THREADS=1 per rank; the CPU
+    baseline and the reference arm run on rank 0 only and use every core)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
 def cpu_sample(e: int, k: int, n: int, rows: int, threads: int = 0):
     """Oracle ("port") karatsuba on C rows [0, rows) — a bounded slice of the same workload."""
     import oracle
@@ -133,12 +142,12 @@ def run_reference(args):
 
     name, e, m, k, n, acc, scaling = workload(args.config, args.e, 1)
     rows = args.cpu_rows or (256 if k * n >= 16384 * 16384 else min(m, 1024))
-    cores = oracle.max_threads()
+    cores = host_threads()
     vals = []
     for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_sample(e, k, n, min(rows, 64))
+        cpu_sample(e, k, n, min(rows, 64), cores)
     for _ in range(args.steps):
-        v, dt = cpu_sample(e, k, n, rows)
+        v, dt = cpu_sample(e, k, n, rows, cores)
         vals.append((v, dt))
     v = statistics.median(x[0] for x in vals)
     dt = statistics.median(x[1] for x in vals)
@@ -330,8 +339,8 @@ def run_ours(args):
         import oracle
 
         rows = args.cpu_rows or (256 if k * n >= 16384 * 16384 else min(m, 1024))
-        v, dt = cpu_sample(e, k, n, rows)
-        line["cpu_baseline"] = {"value": round(v, 4), "unit": "Tbit-op/s", "cores": oracle.max_threads(),
+        v, dt = cpu_sample(e, k, n, rows, host_threads())
+        line["cpu_baseline"] = {"value": round(v, 4), "unit": "Tbit-op/s", "cores": host_threads(),
                                 "kind": "port",
                                 "sample": f"rows 0..{rows - 1} of C ({rows}x{k}x{n}, e={e}) via oracle.karatsuba, "
                                           f"{dt:.2f} s"}
