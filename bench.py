@@ -286,7 +286,7 @@ def run_ours(args):
                "h2d_bytes_per_step": int(hA.numel() * 8 + hB.numel() * 8 + (hC.numel() * 8 if acc else 0)),
                "d2h_bytes_per_step": int(hC.numel() * 8), "ms_per_step": round(float(te[0]), 3),
                "path": "gf2e_mzed_mul_host: pinned packed A,B -> H2D -> slice -> combos -> product -> cling -> D2H, "
-                       "row chunks pipelined on 3 streams"}
+                       "row chunks pipelined on 4 streams"}
 
     if rank != 0:
         if world > 1:

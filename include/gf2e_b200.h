@@ -135,8 +135,9 @@ int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, int64_
  * and C ^= A*B on packed matrices, with A (m x k), B (k x n), C (m x n) in host memory in
  * the reference PackedMatrix.storage.words layout (row stride in words; pinned memory gives
  * full copy/compute overlap).  Synchronous.  B is uploaded, sliced and combined once; rows of
- * A (and C0) then stream through in chunks of `chunk_rows` (<= 0: 2048) with H2D, the
- * kernels and D2H of consecutive chunks overlapped on three internal streams.  Device memory
+ * A (and C0) then stream through in chunks of `chunk_rows` rows (<= 0: a wave-aware plan
+ * around 2048 rows) with the copies, operand preparation, products and copy-out of
+ * consecutive chunks overlapped on four internal streams.  Device memory
  * comes from the stream-ordered pool.  *device_ms (optional) = CUDA-event time from the first
  * H2D to the last D2H.
  */

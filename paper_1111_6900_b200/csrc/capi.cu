@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -344,12 +345,99 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
 
 
 // ---- host-buffer packed multiply (e2e entry) ----------------------------------------------
+int pair_count() {
+    int dev = 0, nsms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsms, cudaDevAttrMultiProcessorCount, dev);
+    return nsms / 2;
+}
+
+// Row chunks of the host pipeline.  The first chunk meets B part by part: it gets as many
+// 256-row tiles as fill the CTA pairs next to one part's column tiles (9 x 8 = 72 of 74 at
+// n = 16384), so the products that run while B is still arriving use the whole GPU.  The
+// rest go in `chunk`-row chunks, the remainder merged into the first of them (at 16384 rows:
+// 2304, 3840, 5 x 2048 — 97-99.8% wave fill each, against 86% for a 1792-row chunk).
+std::vector<int64_t> host_row_plan(int64_t m, int64_t n, int64_t chunk, int nbp, bool fixed) {
+    std::vector<int64_t> rb{0};
+    int64_t first = chunk;
+    if (!fixed && nbp > 1) {
+        const int64_t part_tiles = ((n + 255) / 256 + nbp - 1) / nbp;
+        const int64_t rt0 = pair_count() / part_tiles;
+        if (rt0 >= 1) first = rt0 * 256;
+    }
+    if (first >= m) return {0, m};
+    rb.push_back(first);
+    const int64_t rest = m - first, nfull = rest / chunk, rem = rest - nfull * chunk;
+    if (nfull == 0) {
+        rb.push_back(m);
+        return rb;
+    }
+    int64_t r = first + (fixed ? chunk : chunk + rem);
+    rb.push_back(r);
+    while (r < m) {
+        r = r + chunk < m ? r + chunk : m;
+        rb.push_back(r);
+    }
+    return rb;
+}
+
+
+// Column split of the host pipeline's last row chunk: the first part a whole number of waves
+// of CTA pairs (row tiles x column tiles a multiple of the pair count), about half of n.
+int64_t last_split_cols(int64_t rows, int64_t n) {
+    if (n < 8192) return n;
+    const int64_t pairs = pair_count(), rt = (rows + 255) / 256, nt = (n + 255) / 256;
+    int64_t g = pairs, b = rt;
+    while (b) {
+        const int64_t t = g % b;
+        g = b;
+        b = t;
+    }
+    const int64_t q = pairs / g;  // column tiles per whole wave step
+    const int64_t ct = (nt / 2 + q - 1) / q * q;
+    return ct > 0 && ct < nt ? ct * 256 : n;
+}
+
+// GF2E_E2E_TRACE=1: per-stage completion times of the host-buffer pipeline on stderr
+struct Trace {
+    bool on = getenv("GF2E_E2E_TRACE") != nullptr;
+    cudaEvent_t t0 = nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> ev;
+    void start(cudaStream_t s) {
+        if (!on) return;
+        cudaEventCreate(&t0);
+        cudaEventRecord(t0, s);
+    }
+    void mark(cudaStream_t s, const char *what, int64_t i, int64_t j = -1) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        char buf[64];
+        snprintf(buf, sizeof buf, j < 0 ? "%s %lld" : "%s %lld.%lld", what, (long long)i, (long long)j);
+        ev.emplace_back(buf, e);
+    }
+    ~Trace() {
+        if (!on) return;
+        for (auto &x : ev) {
+            float ms = 0;
+            cudaEventSynchronize(x.second);
+            cudaEventElapsedTime(&ms, t0, x.second);
+            fprintf(stderr, "trace %-14s %8.3f\n", x.first.c_str(), ms);
+            cudaEventDestroy(x.second);
+        }
+        cudaEventDestroy(t0);
+    }
+};
+
 struct HostPlan {
-    cudaStream_t sc = nullptr, sh = nullptr, sd = nullptr;
+    cudaStream_t sc = nullptr, sh = nullptr, sd = nullptr, sp = nullptr;
     std::vector<void *> allocs;
     ~HostPlan() {
-        if (sh) cudaStreamSynchronize(sh);  // error paths: no copy may outlive its buffers
+        if (sh) cudaStreamSynchronize(sh);  // error paths: no copy or kernel may outlive its buffers
         if (sd) cudaStreamSynchronize(sd);
+        if (sp) cudaStreamSynchronize(sp);
+        if (sp) cudaStreamDestroy(sp);
         for (void *p : allocs) cudaFreeAsync(p, sc);
         if (sc) cudaStreamSynchronize(sc);
         if (sc) cudaStreamDestroy(sc);
@@ -893,64 +981,82 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     Sched ks = to_kernel_sched(e, get_schedule(e, f));
     int64_t chunk = chunk_rows > 0 ? round_up(chunk_rows, 2 * kTcBM) : 2048;
     if (chunk > round_up(m, 2 * kTcBM)) chunk = round_up(m, 2 * kTcBM);
-    const int64_t nchunks = (m + chunk - 1) / chunk;
+    constexpr int kMaxBParts = 8;
+#ifndef GF2E_BPARTS
+#define GF2E_BPARTS 8
+#endif
+    // B arrives in column parts (multiples of 256 columns) so the first row chunk's products
+    // start after the first part's upload instead of all of B's
+    const int nbp = (n >= 8192 && m > chunk) ? GF2E_BPARTS : 1;
+    static_assert(GF2E_BPARTS >= 1 && GF2E_BPARTS <= kMaxBParts, "B parts");
+    const std::vector<int64_t> rb = host_row_plan(m, n, chunk, nbp, chunk_rows > 0);
+    for (size_t i = 1; i < rb.size(); ++i)
+        if (rb[i] - rb[i - 1] > chunk) chunk = rb[i] - rb[i - 1];  // slot size
+    const int64_t nchunks = (int64_t)rb.size() - 1;
     const int nslots = nchunks > 1 ? 2 : 1;
 
+    // Streams: sh host->device copies, sp operand preparation (slice + combinations of A and
+    // B), sc products + cling, sd device->host copies.  Preparation runs beside the previous
+    // product (on the SMs a partial last wave leaves idle) instead of between products.
     HostPlan P;
     CKH(cudaStreamCreateWithFlags(&P.sc, cudaStreamNonBlocking), "stream");
     CKH(cudaStreamCreateWithFlags(&P.sh, cudaStreamNonBlocking), "stream");
     CKH(cudaStreamCreateWithFlags(&P.sd, cudaStreamNonBlocking), "stream");
+    CKH(cudaStreamCreateWithFlags(&P.sp, cudaStreamNonBlocking), "stream");
     Layout LB = layout_for(ks.nprod, chunk, k, n, 0);  // Ac sized for one chunk, Bt for all of B
-    uint64_t *dBp, *dBs, *dAc, *dBt, *dAp[2], *dAs[2], *dCs[2], *dCp[2];
+    uint64_t *dBp, *dBs, *dBt, *dAc[2], *dAp[2], *dAs[2], *dCs[2], *dCp[2];
     CKH(P.alloc(&dBp, k * wb * 8), "cudaMallocAsync");
     CKH(P.alloc(&dBs, (int64_t)e * k * nwn * 8), "cudaMallocAsync");
-    CKH(P.alloc(&dAc, LB.a_bytes), "cudaMallocAsync");
     CKH(P.alloc(&dBt, LB.b_bytes), "cudaMallocAsync");
     for (int sl = 0; sl < nslots; ++sl) {
+        CKH(P.alloc(&dAc[sl], LB.a_bytes), "cudaMallocAsync");
         CKH(P.alloc(&dAp[sl], chunk * wa * 8), "cudaMallocAsync");
         CKH(P.alloc(&dAs[sl], (int64_t)e * chunk * nwk * 8), "cudaMallocAsync");
         CKH(P.alloc(&dCs[sl], (int64_t)e * chunk * nwn * 8), "cudaMallocAsync");
         CKH(P.alloc(&dCp[sl], chunk * wb * 8), "cudaMallocAsync");
     }
-    // B arrives in column parts (multiples of 256 columns) so the first row chunk's products
-    // start after the first part's upload instead of all of B's
-    constexpr int kMaxBParts = 8;
-#ifndef GF2E_BPARTS
-#define GF2E_BPARTS 8
-#endif
-    const int nbp = (n >= 8192 && m > chunk) ? GF2E_BPARTS : 1;
-    static_assert(GF2E_BPARTS >= 1 && GF2E_BPARTS <= kMaxBParts, "B parts");
     int64_t cb[kMaxBParts + 1];
     for (int p = 0; p <= nbp; ++p) cb[p] = p == nbp ? n : round_up(n * p / nbp, 2 * kTcBM);
-    cudaEvent_t ev_alloc, ev_t0, ev_t1, ev_b, in_ready[2], out_ready[2], d2h_done[2], ev_bp[kMaxBParts];
-    cudaEvent_t *all[] = {&ev_alloc,    &ev_t0,       &ev_t1,       &ev_b,        &in_ready[0], &in_ready[1],
-                          &out_ready[0], &out_ready[1], &d2h_done[0], &d2h_done[1], &ev_bp[0],    &ev_bp[1],
-                          &ev_bp[2],    &ev_bp[3],    &ev_bp[4],    &ev_bp[5],    &ev_bp[6],    &ev_bp[7]};
-    for (cudaEvent_t *ev : all) CKH(cudaEventCreate(ev), "cudaEventCreate");
+    // events: copies in (A chunk / B part), preparation done, products done (frees that
+    // slot's A combinations), cling done, copy out done
+    cudaEvent_t part_out, ev_alloc, ev_t0, ev_t1, in_ready[2], prep_a[2], prod_done[2], out_ready[2], d2h_done[2],
+        ev_bp[kMaxBParts], prep_b[kMaxBParts];
+    std::vector<cudaEvent_t *> all{&part_out, &ev_alloc, &ev_t0, &ev_t1};
+    for (int sl = 0; sl < 2; ++sl)
+        for (cudaEvent_t *ev : {&in_ready[sl], &prep_a[sl], &prod_done[sl], &out_ready[sl], &d2h_done[sl]})
+            all.push_back(ev);
+    for (int p = 0; p < kMaxBParts; ++p) {
+        all.push_back(&ev_bp[p]);
+        all.push_back(&prep_b[p]);
+    }
     struct EvGuard {
-        cudaEvent_t **evs;
-        int n;
+        std::vector<cudaEvent_t *> evs;
+        size_t made = 0;
         ~EvGuard() {
-            for (int i = 0; i < n; ++i) cudaEventDestroy(*evs[i]);
+            for (size_t i = 0; i < made; ++i) cudaEventDestroy(*evs[i]);
         }
-    } guard{all, 18};
+    } guard{all};
+    for (cudaEvent_t *ev : all) {
+        CKH(cudaEventCreateWithFlags(ev, cudaEventDefault), "cudaEventCreate");
+        ++guard.made;
+    }
     CKH(cudaEventRecord(ev_alloc, P.sc), "cudaEventRecord");
-    CKH(cudaStreamWaitEvent(P.sh, ev_alloc, 0), "cudaStreamWaitEvent");
-    CKH(cudaStreamWaitEvent(P.sd, ev_alloc, 0), "cudaStreamWaitEvent");
+    for (cudaStream_t s2 : {P.sh, P.sd, P.sp}) CKH(cudaStreamWaitEvent(s2, ev_alloc, 0), "cudaStreamWaitEvent");
 
     CKH(cudaEventRecord(ev_t0, P.sh), "cudaEventRecord");
-    // B once: H2D (by column parts), slice, transposed operand combinations
+    Trace tr;
+    tr.start(P.sh);
     auto h2d_bpart = [&](int p) -> int {
         const int64_t w0 = cb[p] * w / 64, w1 = p + 1 == nbp ? wb : cb[p + 1] * w / 64;
         CKH(cudaMemcpy2DAsync(dBp + w0, wb * 8, B_h + w0, ldb * 8, (w1 - w0) * 8, k, cudaMemcpyHostToDevice, P.sh),
             "H2D(B)");
         CKH(cudaEventRecord(ev_bp[p], P.sh), "cudaEventRecord");
+        tr.mark(P.sh, "h2d B", p);
         return GF2E_OK;
     };
-    if (int rc = h2d_bpart(0)) return rc;
     auto h2d_chunk = [&](int64_t i) -> int {
         const int sl = (int)(i % nslots);
-        const int64_t r0 = i * chunk, rows = (m - r0) < chunk ? (m - r0) : chunk;
+        const int64_t r0 = rb[i], rows = rb[i + 1] - rb[i];
         if (i >= nslots) {  // slot reuse: chunk i-2 fully consumed (its cling and its D2H)
             CKH(cudaStreamWaitEvent(P.sh, out_ready[sl], 0), "cudaStreamWaitEvent");
             CKH(cudaStreamWaitEvent(P.sh, d2h_done[sl], 0), "cudaStreamWaitEvent");
@@ -962,54 +1068,99 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
                                   P.sh),
                 "H2D(C0)");
         CKH(cudaEventRecord(in_ready[sl], P.sh), "cudaEventRecord");
+        tr.mark(P.sh, "h2d A", i);
         return GF2E_OK;
     };
+    const bool fp4 = use_fp4(0, k);
+    // chunk i's A on sp: slice, row combinations into its slot's Ac (free once chunk i-2's
+    // products are done)
+    auto prep_chunk = [&](int64_t i) -> int {
+        const int sl = (int)(i % nslots);
+        const int64_t rows = rb[i + 1] - rb[i];
+        CKH(cudaStreamWaitEvent(P.sp, in_ready[sl], 0), "cudaStreamWaitEvent");
+        if (i >= nslots) CKH(cudaStreamWaitEvent(P.sp, prod_done[sl], 0), "cudaStreamWaitEvent");
+        CK(launch_slice(e, w, rows, k, dAp[sl], wa, dAs[sl], nwk, rows * nwk, P.sp), "slice(A)");
+        Layout L = layout_for(ks.nprod, rows, k, n, 0);
+        CK(launch_combos_rows(ks, dAs[sl], nwk, rows * nwk, rows, k, dAc[sl], L.kwords, L.a_pstride, L.m_pad,
+                              L.kwords, fp4 ? 4 : 2, P.sp),
+           "combos(A)");
+        CKH(cudaEventRecord(prep_a[sl], P.sp), "cudaEventRecord");
+        tr.mark(P.sp, "prep A", i);
+        return GF2E_OK;
+    };
+    // B part p on sp: slice its columns, write its rows [cb[p], cb[p+1]) of the B^T combinations
+    auto prep_bpart = [&](int p) -> int {
+        CKH(cudaStreamWaitEvent(P.sp, ev_bp[p], 0), "cudaStreamWaitEvent");
+        const int64_t c0 = cb[p], nc = cb[p + 1] - c0;
+        const int64_t npad = (p + 1 == nbp ? LB.n_pad : cb[p + 1]) - c0;
+        CK(launch_slice(e, w, k, nc, dBp + c0 * w / 64, wb, dBs + c0 / 64, nwn, k * nwn, P.sp, words_for(nc)),
+           "slice(B)");
+        CK(launch_combos_bt(ks, dBs + c0 / 64, nwn, k * nwn, k, nc, dBt + c0 * LB.kwords, LB.kwords, LB.b_pstride,
+                            LB.kwords, npad / 64, fp4, P.sp),
+           "combos(B^T)");
+        CKH(cudaEventRecord(prep_b[p], P.sp), "cudaEventRecord");
+        tr.mark(P.sp, "prep B", p);
+        return GF2E_OK;
+    };
+    // enqueue order (each event recorded before any wait on it): B part 0, chunk 0, the other
+    // B parts; A's preparation one chunk ahead of the products
+    if (int rc = h2d_bpart(0)) return rc;
     if (int rc = h2d_chunk(0)) return rc;
     for (int p = 1; p < nbp; ++p)
         if (int rc = h2d_bpart(p)) return rc;
-    CKH(cudaEventRecord(ev_b, P.sh), "cudaEventRecord");
-    const bool fp4 = use_fp4(0, k);
-    // B part p: slice its columns, write its rows [cb[p], cb[p+1]) of the B^T combinations
-    auto prep_bpart = [&](int p) -> int {
-        CKH(cudaStreamWaitEvent(P.sc, ev_bp[p], 0), "cudaStreamWaitEvent");
-        const int64_t c0 = cb[p], nc = cb[p + 1] - c0;
-        const int64_t npad = (p + 1 == nbp ? LB.n_pad : cb[p + 1]) - c0;
-        CK(launch_slice(e, w, k, nc, dBp + c0 * w / 64, wb, dBs + c0 / 64, nwn, k * nwn, P.sc, words_for(nc)),
-           "slice(B)");
-        CK(launch_combos_bt(ks, dBs + c0 / 64, nwn, k * nwn, k, nc, dBt + c0 * LB.kwords, LB.kwords, LB.b_pstride,
-                            LB.kwords, npad / 64, fp4, P.sc),
-           "combos(B^T)");
-        return GF2E_OK;
-    };
+    if (int rc = prep_chunk(0)) return rc;
+    for (int p = 0; p < nbp; ++p)
+        if (int rc = prep_bpart(p)) return rc;
     for (int64_t i = 0; i < nchunks; ++i) {
         const int sl = (int)(i % nslots);
-        const int64_t r0 = i * chunk, rows = (m - r0) < chunk ? (m - r0) : chunk;
-        if (i + 1 < nchunks)
+        const int64_t r0 = rb[i], rows = rb[i + 1] - rb[i];
+        if (i + 1 < nchunks) {
             if (int rc = h2d_chunk(i + 1)) return rc;  // overlaps this chunk's kernels
-        CKH(cudaStreamWaitEvent(P.sc, in_ready[sl], 0), "cudaStreamWaitEvent");
-        CK(launch_slice(e, w, rows, k, dAp[sl], wa, dAs[sl], nwk, rows * nwk, P.sc), "slice(A)");
-        if (acc) CK(launch_slice(e, w, rows, n, dCp[sl], wb, dCs[sl], nwn, rows * nwn, P.sc), "slice(C0)");
+            if (int rc = prep_chunk(i + 1)) return rc;
+        }
+        CKH(cudaStreamWaitEvent(P.sc, prep_a[sl], 0), "cudaStreamWaitEvent");
+        if (acc) {
+            CKH(cudaStreamWaitEvent(P.sc, in_ready[sl], 0), "cudaStreamWaitEvent");
+            CK(launch_slice(e, w, rows, n, dCp[sl], wb, dCs[sl], nwn, rows * nwn, P.sc), "slice(C0)");
+        }
         Layout L = layout_for(ks.nprod, rows, k, n, 0);
-        CK(launch_combos_rows(ks, dAs[sl], nwk, rows * nwk, rows, k, dAc, L.kwords, L.a_pstride, L.m_pad, L.kwords,
-                              fp4 ? 4 : 2, P.sc),
-           "combos(A)");
-        // the first chunk runs one product per B part as the parts arrive; later chunks see all of B
-        for (int p = 0; p < (i == 0 ? nbp : 1); ++p) {
-            const int64_t c0 = i == 0 ? cb[p] : 0, c1 = i == 0 ? cb[p + 1] : n;
-            const int64_t npad = (i == 0 && p + 1 < nbp ? cb[p + 1] : LB.n_pad) - c0;
-            if (i == 0)
-                if (int rc = prep_bpart(p)) return rc;
-            TcArgs ta{dAc, dBt + c0 * LB.kwords, L.a_pstride, LB.b_pstride, L.kwords, rows, c1 - c0, L.m_pad, npad,
+        // the first chunk runs one product per B part as the parts arrive; later chunks see all of
+        // B.  The last chunk runs as two column parts, the first sized to whole waves of CTA
+        // pairs, so its cling and copy-out overlap the second part's product.
+        const bool last = i + 1 == nchunks && i > 0;
+        const int64_t cs = last ? last_split_cols(rows, n) : n;
+        const int nprods = i == 0 ? nbp : (cs < n ? 2 : 1);
+        for (int p = 0; p < nprods; ++p) {
+            const int64_t c0 = i == 0 ? cb[p] : (p ? cs : 0), c1 = i == 0 ? cb[p + 1] : (p || cs == n ? n : cs);
+            const int64_t npad = (c1 == n ? LB.n_pad : c1) - c0;
+            if (i == 0) CKH(cudaStreamWaitEvent(P.sc, prep_b[p], 0), "cudaStreamWaitEvent");
+            TcArgs ta{dAc[sl], dBt + c0 * LB.kwords, L.a_pstride, LB.b_pstride, L.kwords, rows, c1 - c0, L.m_pad, npad,
                       dCs[sl] + c0 / 64, nwn, rows * nwn, acc ? 1 : 0};
             ProfScope prof(P.sc);
             CK(launch_product_tc2(ks, ta, tc_form(0, k), P.sc), "product_tc2");
+            tr.mark(P.sc, "product", i, p);
+            if (last && p == 0 && cs < n) {  // first column part out while the second computes
+                const int64_t cw = cs * w / 64;
+                CK(launch_cling(e, w, rows, cs, dCs[sl], nwn, rows * nwn, dCp[sl], wb, P.sc), "cling(C)");
+                CKH(cudaEventRecord(part_out, P.sc), "cudaEventRecord");
+                CKH(cudaStreamWaitEvent(P.sd, part_out, 0), "cudaStreamWaitEvent");
+                CKH(cudaMemcpy2DAsync(C_h + r0 * ldc, ldc * 8, dCp[sl], wb * 8, cw * 8, rows, cudaMemcpyDeviceToHost,
+                                      P.sd),
+                    "D2H(C)");
+            }
         }
-        CK(launch_cling(e, w, rows, n, dCs[sl], nwn, rows * nwn, dCp[sl], wb, P.sc), "cling(C)");
+        CKH(cudaEventRecord(prod_done[sl], P.sc), "cudaEventRecord");
+        const int64_t cx = cs < n ? cs : 0, cwx = cx * w / 64;  // columns not yet copied out
+        CK(launch_cling(e, w, rows, n - cx, dCs[sl] + cx / 64, nwn, rows * nwn, dCp[sl] + cwx, wb, P.sc),
+           "cling(C)");
         CKH(cudaEventRecord(out_ready[sl], P.sc), "cudaEventRecord");
+        tr.mark(P.sc, "cling", i);
         CKH(cudaStreamWaitEvent(P.sd, out_ready[sl], 0), "cudaStreamWaitEvent");
-        CKH(cudaMemcpy2DAsync(C_h + r0 * ldc, ldc * 8, dCp[sl], wb * 8, wb * 8, rows, cudaMemcpyDeviceToHost, P.sd),
+        CKH(cudaMemcpy2DAsync(C_h + r0 * ldc + cwx, ldc * 8, dCp[sl] + cwx, wb * 8, (wb - cwx) * 8, rows,
+                              cudaMemcpyDeviceToHost, P.sd),
             "D2H(C)");
         CKH(cudaEventRecord(d2h_done[sl], P.sd), "cudaEventRecord");
+        tr.mark(P.sd, "d2h C", i);
     }
     CKH(cudaStreamWaitEvent(P.sh, d2h_done[(nchunks - 1) % nslots], 0), "cudaStreamWaitEvent");
     CKH(cudaEventRecord(ev_t1, P.sh), "cudaEventRecord");

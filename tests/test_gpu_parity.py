@@ -271,7 +271,9 @@ def test_native_code_used(g):
 @pytest.mark.parametrize("acc", [False, True])
 @pytest.mark.parametrize("e,m,k,n,chunk", [(8, 1000, 700, 600, 256), (4, 4096, 4096, 4096, 0), (2, 300, 0, 65, 0),
                                            (2, 600, 300, 8300, 256), (8, 520, 2100, 8192, 256),
-                                           (10, 513, 129, 257, 512), (3, 1, 1, 1, 0)])
+                                           (10, 513, 129, 257, 512), (3, 1, 1, 1, 0),
+                                           (4, 1324, 200, 9800, 512), (5, 1300, 2100, 9900, 512),
+                                           (2, 5000, 300, 8500, 0), (3, 7000, 260, 10000, 0)])
 def test_host_buffer_api(g, e, m, k, n, chunk, acc):
     # gf2e_mzed_mul_host: packed host words in, packed host words out, chunked + overlapped
     ctx = g.field_new(e)
