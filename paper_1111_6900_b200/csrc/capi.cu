@@ -352,14 +352,17 @@ int pair_count() {
     return nsms / 2;
 }
 
-// Row chunks of the host pipeline.  The first chunk meets B part by part: it gets as many
-// 256-row tiles as fill the CTA pairs next to one part's column tiles (9 x 8 = 72 of 74 at
-// n = 16384), so the products that run while B is still arriving use the whole GPU.  The
-// rest go in `chunk`-row chunks, the remainder merged into the first of them (at 16384 rows:
-// 2304, 3840, 5 x 2048 — 97-99.8% wave fill each, against 86% for a 1792-row chunk).
-std::vector<int64_t> host_row_plan(int64_t m, int64_t n, int64_t chunk, int nbp, bool fixed) {
+// Row chunks of the host pipeline (k >= 4096).  The first chunk meets B part by part: it
+// gets as many 256-row tiles as fill the CTA pairs next to one part's column tiles (9 x 8 =
+// 72 of 74 at n = 16384), so the products that run while B is still arriving use the whole
+// GPU.  The rest go in `chunk`-row chunks, the remainder merged into the first of them (at
+// 16384 rows: 2304, 3840, 5 x 2048 — 97-99.8% wave fill each, against 86% for 1792 rows).
+std::vector<int64_t> host_row_plan(int64_t m, int64_t n, int64_t k, int64_t chunk, int nbp, bool fixed) {
     std::vector<int64_t> rb{0};
     int64_t first = chunk;
+    // only where the products, not the copies, bound the pipeline (long k; at k = 256 the
+    // C0/C copies dominate and uniform chunks pipeline them best)
+    fixed = fixed || k < 4096;
     if (!fixed && nbp > 1) {
         const int64_t part_tiles = ((n + 255) / 256 + nbp - 1) / nbp;
         const int64_t rt0 = pair_count() / part_tiles;
@@ -989,7 +992,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     // start after the first part's upload instead of all of B's
     const int nbp = (n >= 8192 && m > chunk) ? GF2E_BPARTS : 1;
     static_assert(GF2E_BPARTS >= 1 && GF2E_BPARTS <= kMaxBParts, "B parts");
-    const std::vector<int64_t> rb = host_row_plan(m, n, chunk, nbp, chunk_rows > 0);
+    const std::vector<int64_t> rb = host_row_plan(m, n, k, chunk, nbp, chunk_rows > 0);
     for (size_t i = 1; i < rb.size(); ++i)
         if (rb[i] - rb[i - 1] > chunk) chunk = rb[i] - rb[i - 1];  // slot size
     const int64_t nchunks = (int64_t)rb.size() - 1;
@@ -1072,34 +1075,39 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         return GF2E_OK;
     };
     const bool fp4 = use_fp4(0, k);
-    // chunk i's A on sp: slice, row combinations into its slot's Ac (free once chunk i-2's
-    // products are done)
+    // Preparation runs on its own stream, one chunk ahead, where the products bound the
+    // pipeline (k >= 4096); at short k the copies do, and preparing in line on sc pipelines
+    // them with the fewest cross-stream dependencies.
+    const bool side = k >= 4096;
+    cudaStream_t sp = side ? P.sp : P.sc;
+    // chunk i's A: slice, row combinations into its slot's Ac (free once chunk i-2's products
+    // are done)
     auto prep_chunk = [&](int64_t i) -> int {
         const int sl = (int)(i % nslots);
         const int64_t rows = rb[i + 1] - rb[i];
-        CKH(cudaStreamWaitEvent(P.sp, in_ready[sl], 0), "cudaStreamWaitEvent");
-        if (i >= nslots) CKH(cudaStreamWaitEvent(P.sp, prod_done[sl], 0), "cudaStreamWaitEvent");
-        CK(launch_slice(e, w, rows, k, dAp[sl], wa, dAs[sl], nwk, rows * nwk, P.sp), "slice(A)");
+        CKH(cudaStreamWaitEvent(sp, in_ready[sl], 0), "cudaStreamWaitEvent");
+        if (i >= nslots) CKH(cudaStreamWaitEvent(sp, prod_done[sl], 0), "cudaStreamWaitEvent");
+        CK(launch_slice(e, w, rows, k, dAp[sl], wa, dAs[sl], nwk, rows * nwk, sp), "slice(A)");
         Layout L = layout_for(ks.nprod, rows, k, n, 0);
         CK(launch_combos_rows(ks, dAs[sl], nwk, rows * nwk, rows, k, dAc[sl], L.kwords, L.a_pstride, L.m_pad,
-                              L.kwords, fp4 ? 4 : 2, P.sp),
+                              L.kwords, fp4 ? 4 : 2, sp),
            "combos(A)");
-        CKH(cudaEventRecord(prep_a[sl], P.sp), "cudaEventRecord");
-        tr.mark(P.sp, "prep A", i);
+        CKH(cudaEventRecord(prep_a[sl], sp), "cudaEventRecord");
+        tr.mark(sp, "prep A", i);
         return GF2E_OK;
     };
-    // B part p on sp: slice its columns, write its rows [cb[p], cb[p+1]) of the B^T combinations
+    // B part p: slice its columns, write its rows [cb[p], cb[p+1]) of the B^T combinations
     auto prep_bpart = [&](int p) -> int {
-        CKH(cudaStreamWaitEvent(P.sp, ev_bp[p], 0), "cudaStreamWaitEvent");
+        CKH(cudaStreamWaitEvent(sp, ev_bp[p], 0), "cudaStreamWaitEvent");
         const int64_t c0 = cb[p], nc = cb[p + 1] - c0;
         const int64_t npad = (p + 1 == nbp ? LB.n_pad : cb[p + 1]) - c0;
-        CK(launch_slice(e, w, k, nc, dBp + c0 * w / 64, wb, dBs + c0 / 64, nwn, k * nwn, P.sp, words_for(nc)),
+        CK(launch_slice(e, w, k, nc, dBp + c0 * w / 64, wb, dBs + c0 / 64, nwn, k * nwn, sp, words_for(nc)),
            "slice(B)");
         CK(launch_combos_bt(ks, dBs + c0 / 64, nwn, k * nwn, k, nc, dBt + c0 * LB.kwords, LB.kwords, LB.b_pstride,
-                            LB.kwords, npad / 64, fp4, P.sp),
+                            LB.kwords, npad / 64, fp4, sp),
            "combos(B^T)");
-        CKH(cudaEventRecord(prep_b[p], P.sp), "cudaEventRecord");
-        tr.mark(P.sp, "prep B", p);
+        CKH(cudaEventRecord(prep_b[p], sp), "cudaEventRecord");
+        tr.mark(sp, "prep B", p);
         return GF2E_OK;
     };
     // enqueue order (each event recorded before any wait on it): B part 0, chunk 0, the other
@@ -1108,16 +1116,20 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     if (int rc = h2d_chunk(0)) return rc;
     for (int p = 1; p < nbp; ++p)
         if (int rc = h2d_bpart(p)) return rc;
-    if (int rc = prep_chunk(0)) return rc;
-    for (int p = 0; p < nbp; ++p)
-        if (int rc = prep_bpart(p)) return rc;
+    if (side) {
+        if (int rc = prep_chunk(0)) return rc;
+        for (int p = 0; p < nbp; ++p)
+            if (int rc = prep_bpart(p)) return rc;
+    }
     for (int64_t i = 0; i < nchunks; ++i) {
         const int sl = (int)(i % nslots);
         const int64_t r0 = rb[i], rows = rb[i + 1] - rb[i];
-        if (i + 1 < nchunks) {
+        if (i + 1 < nchunks)
             if (int rc = h2d_chunk(i + 1)) return rc;  // overlaps this chunk's kernels
+        if (side && i + 1 < nchunks)
             if (int rc = prep_chunk(i + 1)) return rc;
-        }
+        if (!side)
+            if (int rc = prep_chunk(i)) return rc;
         CKH(cudaStreamWaitEvent(P.sc, prep_a[sl], 0), "cudaStreamWaitEvent");
         if (acc) {
             CKH(cudaStreamWaitEvent(P.sc, in_ready[sl], 0), "cudaStreamWaitEvent");
@@ -1128,11 +1140,13 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         // B.  The last chunk runs as two column parts, the first sized to whole waves of CTA
         // pairs, so its cling and copy-out overlap the second part's product.
         const bool last = i + 1 == nchunks && i > 0;
-        const int64_t cs = last ? last_split_cols(rows, n) : n;
+        const int64_t cs = last && side ? last_split_cols(rows, n) : n;
         const int nprods = i == 0 ? nbp : (cs < n ? 2 : 1);
         for (int p = 0; p < nprods; ++p) {
             const int64_t c0 = i == 0 ? cb[p] : (p ? cs : 0), c1 = i == 0 ? cb[p + 1] : (p || cs == n ? n : cs);
             const int64_t npad = (c1 == n ? LB.n_pad : c1) - c0;
+            if (i == 0 && !side)
+                if (int rc = prep_bpart(p)) return rc;
             if (i == 0) CKH(cudaStreamWaitEvent(P.sc, prep_b[p], 0), "cudaStreamWaitEvent");
             TcArgs ta{dAc[sl], dBt + c0 * LB.kwords, L.a_pstride, LB.b_pstride, L.kwords, rows, c1 - c0, L.m_pad, npad,
                       dCs[sl] + c0 / 64, nwn, rows * nwn, acc ? 1 : 0};
