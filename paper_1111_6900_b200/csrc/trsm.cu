@@ -36,9 +36,12 @@ __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__
                                                    uint64_t *__restrict__ Tinv, int *__restrict__ bad_row) {
     constexpr int NW = TB / 64;           // plane words per block row
     __shared__ uint64_t pub[2][NW][E];    // the published row X_i, double-buffered by step parity
-    __shared__ uint16_t sinv[1 << E], smk[(1 << E) * E];
+    __shared__ uint16_t sinv[1 << E], smk[(1 << E) * E], sex[1 << E], slg[1 << E], sdlog[TB];
+    constexpr int ORD = (1 << E) - 1;     // multiplicative group order
     for (int i = threadIdx.x; i < (1 << E); i += TB) {
         sinv[i] = ftab->inv[i];
+        sex[i] = ftab->ex[i < ORD ? i : 0];
+        slg[i] = ftab->lg[i];
 #pragma unroll
         for (int b = 0; b < E; ++b) smk[i * E + b] = ftab->mulmask[i][b];
     }
@@ -77,36 +80,31 @@ __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__
         }
         return v;
     };
-    if (!unit && k < rows && entry(k) == 0) atomicMin(bad_row, (int)(r0 + k));
+    // T = U D with D = diag(T) and U = T D^-1 unit triangular, so T^-1 = D^-1 U^-1: the
+    // substitution runs on U (multipliers T_ki / T_ii, from the log tables) with no scaling on
+    // the per-row critical path, and each thread scales its own row of the result at the end.
+    const uint32_t dk = k < rows ? entry(k) : 1u;
+    if (!unit && k < rows && dk == 0) atomicMin(bad_row, (int)(r0 + k));
+    sdlog[k] = (unit || dk == 0) ? 0 : slg[dk];
+    __syncthreads();
     for (int step = 0; step < rows; ++step) {
         const int i = upper ? rows - 1 - step : step;
-        if (k == i) {
-            uint32_t c = unit ? 1u : sinv[entry(i)];
-            if (c == 0) c = 1;  // singular block: reported above, result unused
+        if (k == i) {  // X_i of U^-1 is final as it stands
 #pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                uint64_t y[E];
+            for (int w = 0; w < NW; ++w)
 #pragma unroll
-                for (int b = 0; b < E; ++b) {
-                    const uint32_t mk = smk[c * E + b];
-                    uint64_t acc = 0;
-#pragma unroll
-                    for (int p = 0; p < E; ++p) acc ^= x[p][w] & (0ULL - (uint64_t)((mk >> p) & 1u));
-                    y[b] = acc;
-                }
-#pragma unroll
-                for (int b = 0; b < E; ++b) {
-                    x[b][w] = y[b];
-                    pub[step & 1][w][b] = y[b];
-                }
-            }
+                for (int b = 0; b < E; ++b) pub[step & 1][w][b] = x[b][w];
         }
         // one barrier per row: pub[step & 1] is rewritten two steps later, after every reader
         // of this step has passed the next step's barrier
         __syncthreads();
         const bool below = upper ? (k < i) : (k > i && k < rows);
         if (below) {
-            const uint32_t c = entry(i);
+            uint32_t c = entry(i);
+            if (c && !unit) {  // U_ki = T_ki / T_ii
+                int l = (int)slg[c] - (int)sdlog[i];
+                c = sex[l < 0 ? l + ORD : l];
+            }
             if (c) {
 #pragma unroll
                 for (int b = 0; b < E; ++b) {
@@ -120,6 +118,24 @@ __global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__
                     }
                 }
             }
+        }
+    }
+    if (!unit && k < rows) {  // row k of T^-1 = T_kk^-1 * row k of U^-1
+        uint32_t c = sinv[dk];
+        if (c == 0) c = 1;  // singular block: reported above, result unused
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            uint64_t y[E];
+#pragma unroll
+            for (int b = 0; b < E; ++b) {
+                const uint32_t mk = smk[c * E + b];
+                uint64_t acc = 0;
+#pragma unroll
+                for (int p = 0; p < E; ++p) acc ^= x[p][w] & (0ULL - (uint64_t)((mk >> p) & 1u));
+                y[b] = acc;
+            }
+#pragma unroll
+            for (int b = 0; b < E; ++b) x[b][w] = y[b];
         }
     }
     // Tinv block = e planes of TB rows x NW words
