@@ -721,20 +721,34 @@ int ple_top(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, i
     if (!tab) return fail(GF2E_ECUDA, "field table upload failed");
     PleCtx c{e, f, to_kernel_sched(e, get_schedule(e, f)), S, ld, ps, st, static_cast<PanelOut *>(po.p),
              static_cast<int64_t *>(ix.p), tab};
+    // The pinned staging ring persists per host thread and only grows: pinning and unpinning
+    // host pages on every call (cudaMallocHost / cudaFreeHost) stalled some calls for
+    // hundreds of milliseconds.  It is never freed (process lifetime).
+    struct PinnedRing {
+        int64_t *buf[PleCtx::kRing] = {};
+        cudaEvent_t ev[PleCtx::kRing] = {};
+        size_t bytes = 0;
+    };
+    thread_local PinnedRing pr;
     const size_t ring_bytes = (size_t)(3 * (m > n ? m : n) + 3) * 8;
-    struct RingGuard {
-        PleCtx &c;
-        ~RingGuard() {
-            for (int i = 0; i < PleCtx::kRing; ++i) {
-                if (c.ring_ev[i]) cudaEventSynchronize(c.ring_ev[i]), cudaEventDestroy(c.ring_ev[i]);
-                if (c.ring[i]) cudaFreeHost(c.ring[i]);
-            }
+    if (pr.bytes < ring_bytes) {
+        for (int i = 0; i < PleCtx::kRing; ++i) {
+            if (pr.ev[i]) CKH(cudaEventSynchronize(pr.ev[i]), "cudaEventSynchronize");
+            if (pr.buf[i]) cudaFreeHost(pr.buf[i]);
+            pr.buf[i] = nullptr;
         }
-    } guard{c};
+        pr.bytes = 0;
+        const size_t want = ring_bytes > (size_t)1 << 20 ? ring_bytes : (size_t)1 << 20;
+        for (int i = 0; i < PleCtx::kRing; ++i)
+            if (cudaMallocHost(reinterpret_cast<void **>(&pr.buf[i]), want) != cudaSuccess)
+                return fail(GF2E_ENOMEM, "out of pinned host memory (PLE staging)");
+        pr.bytes = want;
+    }
     for (int i = 0; i < PleCtx::kRing; ++i) {
-        if (cudaMallocHost(reinterpret_cast<void **>(&c.ring[i]), ring_bytes) != cudaSuccess ||
-            cudaEventCreateWithFlags(&c.ring_ev[i], cudaEventDisableTiming) != cudaSuccess)
-            return fail(GF2E_ENOMEM, "out of pinned host memory (PLE staging)");
+        if (!pr.ev[i] && cudaEventCreateWithFlags(&pr.ev[i], cudaEventDisableTiming) != cudaSuccess)
+            return fail(GF2E_ECUDA, "cudaEventCreate (PLE staging)");
+        c.ring[i] = pr.buf[i];
+        c.ring_ev[i] = pr.ev[i];
     }
     std::vector<int64_t> hp(k), hq(k);
     int64_t r = 0;

@@ -18,7 +18,11 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 for _ in range(reps):
     S.planes.copy_(S0.planes)
     torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
+    ev0.record()
     P, Q, r = g.ple_sliced(S)
+    ev1.record()
     torch.cuda.synchronize()
-    print(f"ple e={e} n={n}: {1e3 * (time.perf_counter() - t0):.2f} ms wall, rank {r}", flush=True)
+    print(f"ple e={e} n={n}: {1e3 * (time.perf_counter() - t0):.2f} ms wall, {ev0.elapsed_time(ev1):.2f} ms "
+          f"default-stream events, rank {r}", flush=True)
