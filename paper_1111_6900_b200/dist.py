@@ -41,7 +41,7 @@ def row_partition(m: int, world: int, align: int = ROW_ALIGN) -> list[tuple[int,
 
 def broadcast_planes(planes: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
     """In-place broadcast of a plane stack from `src` (the one data-path collective)."""
-    if dist.is_initialized() and dist.get_world_size(group) > 1:
+    if dist.is_initialized():
         dist.broadcast(planes, src=src, group=group)
     return planes
 

@@ -84,8 +84,10 @@ def main():
     ops = K * tm * tm * n  # ~K(e) * 2 * (m^2/2) * n GF(2) bit-ops for the triangular product
     print(json.dumps({"op": "trsm_upper (sliced)", "e": e, "m": tm, "n": n, "ms": round(ms, 3),
                       "eff_Tbit-op/s": round(ops / (ms * 1e-3) / 1e12, 1),
-                      "note": "K(e)*m^2*n GF(2) bit-ops; updates via addmul, 128-row diagonal blocks inverted on device"}),
+                      "note": "K(e)*m^2*n GF(2) bit-ops; updates via addmul, 256-row diagonal blocks (128 below "
+                              "m = 1024 or n = 4096) inverted on device"}),
           flush=True)
+    ple_lines(a, ctx)
 
 
 def ple_lines(a, ctx):

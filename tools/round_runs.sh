@@ -11,4 +11,8 @@ for e in 2 8 10; do timeout 300 python bench.py --config 4 --e $e --no-cpu-basel
 timeout 900 python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r/bench_config5.json 2>&1
 timeout 600 python tools/bench_ops.py > gpurun_out/r/ops.jsonl 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r/ncu_launch.log 2>&1
+# the NCCL code path (process group, B broadcast, max-over-ranks timing) under torchrun, 1 rank
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 \
+  bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r/bench_torchrun_nccl1.json 2> gpurun_out/r/bench_torchrun_nccl1.err
+tail -c 200 gpurun_out/r/bench_torchrun_nccl1.json
 echo done
