@@ -6,7 +6,7 @@ cd "$(dirname "$0")/../paper_1111_6900_b200/csrc"
 make -s >/dev/null
 mkdir -p ../../build/variants
 NV=/usr/local/cuda/bin/nvcc
-FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr"
+FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -warn-spills"
 $NV $FL $2 -c product_tc2.cu -o /tmp/variant_$1.o
 objs=$(ls _obj/*.o | grep -v product_tc2)
 $NV -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o ../../build/variants/lib_$1.so $objs /tmp/variant_$1.o
