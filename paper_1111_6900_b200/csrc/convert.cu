@@ -3,6 +3,8 @@
 //   K2 cling (mat_sliced.py:104-106), plane XOR (mat_gf2.py:161-164), reduce_mod_f
 //   (poly_mul.py:223-242), and K3 operand combinations of the Karatsuba schedule
 //   (poly_mul.py:153-163,184-186,200-201) in the layouts the product kernels read.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -319,40 +321,42 @@ __global__ void k_combos_rows(Sched s, const uint64_t *__restrict__ X, int64_t l
 // Stage-tiled A'_t (tensor-core layout): thread = (row r, pair of k-stages); reads 32 B of each
 // input plane row (one sector), writes 16 B to each of two tiles; a warp's writes are 32
 // consecutive tile rows = 512 contiguous bytes.
+template <int E, int Q>  // planes at compile time; Q words (Q / 2 16-byte pieces) per thread
 __global__ void k_combos_tiled(Sched s, const uint64_t *__restrict__ X, int64_t ldx, int64_t px, int64_t rows,
                                int64_t ncols, uint64_t *__restrict__ out, int64_t po, int64_t rows_pad,
                                int64_t kwords, int kw) {
     const int64_t nw = words_for(ncols);
     const uint64_t tm = tail_mask(ncols);
-    const int64_t KP = (kwords + 3) >> 2;  // groups of 4 words (2 int8 stages / 1 fp4 stage)
+    const int64_t KP = (kwords + Q - 1) / Q;  // groups of Q words
     const int64_t total = rows_pad * KP;
     for (int64_t idx = gtid(); idx < total; idx += gstride()) {
         const int64_t rb = idx / (KP * 128), rem = idx - rb * KP * 128;
         const int64_t kp = rem >> 7, r = rb * 128 + (rem & 127);
-        const int64_t w0 = kp * 4;
-        uint64_t x[kMaxE][4];
+        const int64_t w0 = kp * Q;
+        uint64_t x[E][Q];
 #pragma unroll
-        for (int i = 0; i < kMaxE; ++i)
+        for (int i = 0; i < E; ++i)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < Q; ++q) {
                 const int64_t w = w0 + q;
-                uint64_t v = (i < s.e && r < rows && w < nw) ? X[i * px + r * ldx + w] : 0;
+                uint64_t v = (r < rows && w < nw) ? X[i * px + r * ldx + w] : 0;
                 x[i][q] = (w == nw - 1) ? (v & tm) : v;
             }
-        const bool two = w0 + 2 < kwords;
         for (int t = 0; t < s.nprod; ++t) {
             const uint32_t sub = s.subset[t];
-            uint64_t a[4] = {0, 0, 0, 0};
+            uint64_t a[Q] = {};
 #pragma unroll
-            for (int i = 0; i < kMaxE; ++i) {
+            for (int i = 0; i < E; ++i) {
                 const uint64_t sel = 0ULL - (uint64_t)((sub >> i) & 1u);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) a[q] ^= x[i][q] & sel;
+                for (int q = 0; q < Q; ++q) a[q] ^= x[i][q] & sel;
             }
             uint64_t *o = out + t * po;
-            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(r, w0, kwords, kw)) = make_ulonglong2(a[0], a[1]);
-            if (two)
-                *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(r, w0 + 2, kwords, kw)) = make_ulonglong2(a[2], a[3]);
+#pragma unroll
+            for (int q = 0; q < Q; q += 2)
+                if (w0 + q < kwords)
+                    *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(r, w0 + q, kwords, kw)) =
+                        make_ulonglong2(a[q], a[q + 1]);
         }
     }
 }
@@ -385,6 +389,7 @@ __device__ __forceinline__ void transpose64(uint64_t &xa, uint64_t &xb, int lane
 // tensor-core producer expands with one AND per output word (product_tc2.cu) — stored
 // stage-tiled with the rows of every 32-row group in tc_b_row_inv order (the epilogue's
 // parity packer emits columns in b_row_perm order).  One warp per 64x64 block.
+template <int E>  // planes at compile time (register arrays of E words)
 __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb, int64_t pb, int64_t k,
                             int64_t n, uint64_t *__restrict__ out, int64_t ldo, int64_t po, int64_t kblocks,
                             int64_t nblocks, int fp4, int tsplit) {
@@ -407,32 +412,31 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
         // 32-byte sector of B is fetched from DRAM once (L2 serves the other three warps)
         const int64_t nb = blk % nblocks, ks = blk / nblocks;
         const uint64_t tm = (nb == nw - 1) ? tail_mask(n) : ~0ULL;
-        uint64_t a[2][kMaxE], b[2][kMaxE];
+        uint64_t a[2][E], b[2][E];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int sl = fp4 ? (lane ^ ((~lane & 1) << 1)) : (lane ^ 7);
             const int64_t r0 = (2 * ks + h) * 64 + sl, r1 = r0 + 32;
 #pragma unroll
-            for (int i = 0; i < kMaxE; ++i) {
-                a[h][i] = (i < s.e && nb < nw && r0 < k) ? (B[i * pb + r0 * ldb + nb] & tm) : 0;
-                b[h][i] = (i < s.e && nb < nw && r1 < k) ? (B[i * pb + r1 * ldb + nb] & tm) : 0;
+            for (int i = 0; i < E; ++i) {
+                a[h][i] = (nb < nw && r0 < k) ? (B[i * pb + r0 * ldb + nb] & tm) : 0;
+                b[h][i] = (nb < nw && r1 < k) ? (B[i * pb + r1 * ldb + nb] & tm) : 0;
             }
         }
         const int64_t ra = tc_b_row_inv(nb * 64 + lane), rbw = tc_b_row_inv(nb * 64 + lane + 32);
         // the transpose is GF(2)-linear: transpose the e planes once, then form every
         // product's subset XOR from the transposed words (e instead of K(e) transposes)
 #pragma unroll
-        for (int i = 0; i < kMaxE; ++i)
-            if (i < s.e) {
-                transpose64(a[0][i], b[0][i], lane);
-                transpose64(a[1][i], b[1][i], lane);
-            }
+        for (int i = 0; i < E; ++i) {
+            transpose64(a[0][i], b[0][i], lane);
+            transpose64(a[1][i], b[1][i], lane);
+        }
         const int t1 = (tg + 1) * tper < s.nprod ? (tg + 1) * tper : s.nprod;
         for (int t = tg * tper; t < t1; ++t) {
             const uint32_t sub = s.subset[t];
             uint64_t xa[2] = {0, 0}, xb[2] = {0, 0};
 #pragma unroll
-            for (int i = 0; i < kMaxE; ++i) {
+            for (int i = 0; i < E; ++i) {
                 const uint64_t sel = 0ULL - (uint64_t)((sub >> i) & 1u);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -444,6 +448,24 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
             *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(ra, 2 * ks, ldo, kw)) = make_ulonglong2(xa[0], xa[1]);
             *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(rbw, 2 * ks, ldo, kw)) = make_ulonglong2(xb[0], xb[1]);
         }
+    }
+}
+
+// f(std::integral_constant<int, e>) for e = 1 .. kMaxE (compile-time plane count)
+template <typename F>
+cudaError_t dispatch_e(int e, F &&f) {
+    switch (e) {
+        case 1: return f(std::integral_constant<int, 1>{});
+        case 2: return f(std::integral_constant<int, 2>{});
+        case 3: return f(std::integral_constant<int, 3>{});
+        case 4: return f(std::integral_constant<int, 4>{});
+        case 5: return f(std::integral_constant<int, 5>{});
+        case 6: return f(std::integral_constant<int, 6>{});
+        case 7: return f(std::integral_constant<int, 7>{});
+        case 8: return f(std::integral_constant<int, 8>{});
+        case 9: return f(std::integral_constant<int, 9>{});
+        case 10: return f(std::integral_constant<int, 10>{});
+        default: return cudaErrorInvalidValue;
     }
 }
 
@@ -538,11 +560,17 @@ cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, i
                                int64_t ncols, uint64_t *out, int64_t ldo, int64_t po, int64_t rows_pad,
                                int64_t words_pad, int tiled_kw, cudaStream_t st) {
     if (tiled_kw) {
-        const int64_t tot = rows_pad * ((words_pad + 3) >> 2);
+#ifndef GF2E_COMBOS_Q
+#define GF2E_COMBOS_Q 2
+#endif
+        constexpr int Q = GF2E_COMBOS_Q;
+        const int64_t tot = rows_pad * ((words_pad + Q - 1) / Q);
         if (tot == 0) return cudaSuccess;
-        k_combos_tiled<<<grid_for(tot, 256), 256, 0, st>>>(s, X, ldx, px, rows, ncols, out, po, rows_pad, words_pad,
-                                                           tiled_kw);
-        return cudaGetLastError();
+        return dispatch_e(s.e, [&](auto ec) {
+            k_combos_tiled<decltype(ec)::value, Q><<<grid_for(tot, 256), 256, 0, st>>>(
+                s, X, ldx, px, rows, ncols, out, po, rows_pad, words_pad, tiled_kw);
+            return cudaGetLastError();
+        });
     }
     int64_t total = rows_pad * words_pad;
     if (total == 0) return cudaSuccess;
@@ -559,8 +587,11 @@ cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int
     int tsplit = 1;
     while (tsplit < s.nprod && warps * tsplit * 2 <= 148 * 16) tsplit *= 2;
     int g = grid_for(warps * tsplit * 32, 256);
-    k_combos_bt<<<g, 256, 0, st>>>(s, B, ldb, pb, k, n, out, ldo, po, kblocks, nblocks, fp4 ? 1 : 0, tsplit);
-    return cudaGetLastError();
+    return dispatch_e(s.e, [&](auto ec) {
+        k_combos_bt<decltype(ec)::value><<<g, 256, 0, st>>>(s, B, ldb, pb, k, n, out, ldo, po, kblocks, nblocks,
+                                                            fp4 ? 1 : 0, tsplit);
+        return cudaGetLastError();
+    });
 }
 
 }  // namespace gf2e
