@@ -5,8 +5,6 @@ Bit-exact against fixtures produced by the reference (tests/golden/make_golden.p
 import numpy as np
 import pytest
 
-import oracle
-
 pytestmark = pytest.mark.gpu
 
 
