@@ -2,6 +2,8 @@
 recursive TRSM, whose updates are addmul calls), sliced mul_by_x, packed scalar_mul.
 Bit-exact against fixtures produced by the reference (tests/golden/make_golden.py)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -54,6 +56,30 @@ def test_trsm_identity_large(g, e, m, n):
         (g.trsm_upper_left if T is U else g.trsm_lower_left)(T, X)
         assert g.karatsuba_mul_packed(T, X) == B0
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("GF2E_FUZZ_SEEDS", "12"))))
+def test_trsm_fuzz(g, seed):
+    # random field, shapes, triangle, unit/non-unit diagonal (random nonzero pivots):
+    # T X = B checked with the separately verified product kernel
+    rng = np.random.default_rng(9000 + seed)
+    e = int(rng.integers(2, 11))
+    m, n = int(rng.integers(1, 1400)), int(rng.integers(1, 1400))
+    ctx = g.field_new(e)
+    R = g.PackedMatrix.random(ctx, m, m, 40 + seed).to_array()
+    upper, unit = bool(seed & 1), (seed % 4 == 2)
+    T = np.triu(R, 1) if upper else np.tril(R, -1)
+    np.fill_diagonal(T, 1 if unit else rng.integers(1, ctx.order, size=m))
+    Tm = g.PackedMatrix.from_array(ctx, T)
+    B0 = g.PackedMatrix.random(ctx, m, n, 41 + seed)
+    X = B0.copy()
+    if upper:
+        g.trsm_upper_left(Tm, X)
+    elif unit:
+        g.trsm_lower_left_unit(Tm, X)
+    else:
+        g.trsm_lower_left(Tm, X)
+    assert g.karatsuba_mul_packed(Tm, X) == B0, (e, m, n, upper, unit)
 
 
 def test_trsm_singular(g):

@@ -1,6 +1,8 @@
 """Parity of the CUDA path (through the C ABI) with the oracle and the reference fixtures.
 Bit-exact everywhere: this path is integer/bitwise only."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -299,7 +301,7 @@ def test_config5_sampled_blocks(g):
     _sampled_blocks(g, 8, 65536, 65536, 65536, False, [0, 255, 40000, 65535], (65536 - 256, 65536))
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("GF2E_FUZZ_SEEDS", "12"))))
 def test_fuzz_shapes(g, seed):
     # random e, shapes (ragged, word-boundary-crossing, some long-k for the fp4 forms) and
     # addmul/mul, every backend, against the oracle

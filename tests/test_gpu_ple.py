@@ -4,6 +4,8 @@ Bit-exact against fixtures the reference produced (tests/golden/make_golden.py) 
 the reference cannot reach, against the oracle's restatement of nj_ple (itself pinned to the
 same fixtures in test_oracle_golden.py)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -67,6 +69,32 @@ def test_ple_vs_oracle(g, e, m, n, kind):
     assert F.rank == r
     assert np.array_equal(F.P.entries, P) and np.array_equal(F.Q.entries, Q)
     assert np.array_equal(F.matrix.to_array(), ref)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("GF2E_FUZZ_SEEDS", "12"))))
+def test_ple_fuzz(g, seed):
+    # random field, shape (ragged, word-boundary-crossing), rank profile (full, low rank,
+    # zero column bands) against the oracle's nj_ple; reconstruction P L E = A
+    rng = np.random.default_rng(5000 + seed)
+    e = int(rng.integers(2, 11))
+    m, n = (int(x) for x in rng.integers(1, 600, size=2))
+    ctx = g.field_new(e)
+    kind = seed % 3
+    if kind == 1:
+        A = _lowrank(g, ctx, m, n, int(rng.integers(1, 1 + min(m, n))), 70 + seed)
+    else:
+        A = g.PackedMatrix.random(ctx, m, n, 70 + seed)
+        if kind == 2 and n > 8:
+            arr = A.to_array()
+            c0 = int(rng.integers(0, n - 4))
+            arr[:, c0:c0 + int(rng.integers(1, n - c0))] = 0
+            A = g.PackedMatrix.from_array(ctx, arr)
+    ref, P, Q, r = oracle.ple(e, ctx.f, A.to_array())
+    F = g.ple(A.copy())
+    assert F.rank == r, (e, m, n, kind)
+    assert np.array_equal(F.P.entries, P) and np.array_equal(F.Q.entries, Q), (e, m, n, kind)
+    assert np.array_equal(F.matrix.to_array(), ref), (e, m, n, kind)
+    assert g.ple_reconstruct(F) == A
 
 
 def test_ple_reconstruct_and_echelon(g):
