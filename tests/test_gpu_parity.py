@@ -289,6 +289,36 @@ def test_host_buffer_api(g, e, m, k, n, chunk, acc):
     assert ms >= 0
 
 
+@pytest.mark.parametrize("seed", range(int(os.environ.get("GF2E_FUZZ_SEEDS", "12")) // 2 + 2))
+def test_host_buffer_fuzz(g, seed):
+    # the host-buffer pipeline's chunking (row plan, B column parts, side-stream preparation,
+    # split last chunk) against the device product on the same operands
+    import torch
+
+    rng = np.random.default_rng(7000 + seed)
+    e = int(rng.integers(2, 11))
+    m = int(rng.integers(1, 3000))
+    k = int(rng.integers(1, 600)) if seed % 2 else int(rng.integers(4096, 5200))
+    n = int(rng.integers(1, 900)) if seed % 3 == 0 else int(rng.integers(8192, 9800))
+    chunk = [0, 256, 512, 768][seed % 4]
+    acc = seed % 5 == 1
+    ctx = g.field_new(e)
+    A = g.PackedMatrix.random(ctx, m, k, 80 + seed)
+    B = g.PackedMatrix.random(ctx, k, n, 81 + seed)
+    if acc:
+        C = g.PackedMatrix.random(ctx, m, n, 82 + seed)
+        C0 = C.to_numpy().copy()
+        g.addmul_packed(C, A, B)
+        ref = C.to_numpy()
+        out, _ = g.karatsuba_mul_packed_host(ctx, A.to_numpy(), k, B.to_numpy(), n, C_words=C0, chunk_rows=chunk)
+    else:
+        ref = g.karatsuba_mul_packed(A, B).to_numpy()
+        out, _ = g.karatsuba_mul_packed_host(ctx, A.to_numpy(), k, B.to_numpy(), n, chunk_rows=chunk)
+    torch.cuda.synchronize()
+    wb = g.words_for(n * g.pack_width(e))
+    assert np.array_equal(out[:, :wb], ref[:, :wb]), (e, m, k, n, chunk, acc)
+
+
 @pytest.mark.slow
 def test_config5_sampled_blocks(g):
     # BASELINE config 5: F_256, 65536^3 on one GPU (the per-GPU problem of the 1-GPU point of the
