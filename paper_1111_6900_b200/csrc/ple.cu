@@ -503,8 +503,14 @@ const FieldTab *field_tab(int e, uint32_t f, uint32_t g) {
     auto it = slots.find({e, f});
     if (it != slots.end()) return base + it->second;
     const int slot = next++ % kFieldTabSlots;
-    for (auto i = slots.begin(); i != slots.end();)
+    bool evict = false;
+    for (auto i = slots.begin(); i != slots.end();) {
+        evict = evict || i->second == slot;
         i = (i->second == slot) ? slots.erase(i) : std::next(i);
+    }
+    // a slot is reused only after every kernel that may read it has finished (the callers'
+    // streams are non-blocking, so the upload below would not wait for them by itself)
+    if (evict && cudaDeviceSynchronize() != cudaSuccess) return nullptr;
     static FieldTab h;
     std::memset(&h, 0, sizeof(h));
     h.f = f;
