@@ -52,6 +52,8 @@ cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int
 
 // Tensor-core product.  Operands: Ac [nprod] x (m_pad x k_pad bits) natural bit order,
 // Bt [nprod] x (n_pad x k_pad bits) = B^T with bits reversed in each byte.
+constexpr int kMaxDevices = 64;  // per-device launch-attribute caches
+
 struct TcArgs {
     const uint64_t *Ac;
     const uint64_t *Bt;

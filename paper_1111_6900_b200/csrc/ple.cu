@@ -453,14 +453,22 @@ template <int E>
 cudaError_t launch_ple_e(const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb, PanelOut *out,
                          cudaStream_t st) {
     const int smem = (PT * E + KP * E * E) * 8 + (1 << E) * (E + 1) * 2;
-    cudaError_t err = cudaFuncSetAttribute(k_ple_find<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
+    const int smem2 = KP * E * E * 8;
+    // launch attributes once per instantiation and device (idempotent)
+    static bool attr_set[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaError_t err = cudaSuccess;
+    if (dev >= kMaxDevices || !attr_set[dev]) {
+        err = cudaFuncSetAttribute(k_ple_find<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(k_ple_apply<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        if (err != cudaSuccess) return err;
+        if (dev < kMaxDevices) attr_set[dev] = true;
+    }
     k_ple_find<E><<<1, PT, smem, st>>>(tab, S, ld, ps, m, nb, out);
     err = cudaGetLastError();
     if (err != cudaSuccess || m <= PT) return err;
-    const int smem2 = KP * E * E * 8;
-    err = cudaFuncSetAttribute(k_ple_apply<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-    if (err != cudaSuccess) return err;
     k_ple_apply<E><<<grid_for(m - PT, 256), 256, smem2, st>>>(S, ld, ps, m, nb, out);
     return cudaGetLastError();
 }

@@ -647,9 +647,16 @@ int g_num_sms2 = 0;
 template <int E, bool FP4, bool PAIR, bool WIDE>
 cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
     const int smem = Cfg<FP4, PAIR, WIDE>::SMEM_BYTES;
-    cudaError_t err =
-        cudaFuncSetAttribute(k_product_tc2<E, FP4, PAIR, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
+    // once per instantiation and device (idempotent, so a race is harmless)
+    static bool attr_set[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= kMaxDevices || !attr_set[dev]) {
+        cudaError_t err =
+            cudaFuncSetAttribute(k_product_tc2<E, FP4, PAIR, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (err != cudaSuccess) return err;
+        if (dev < kMaxDevices) attr_set[dev] = true;
+    }
     const int64_t tiles = (a.m_pad / (2 * BM)) * (a.n_pad / Cfg<FP4, PAIR, WIDE>::BN);
     if (tiles == 0) return cudaSuccess;
     if (g_num_sms2 == 0) {
