@@ -766,7 +766,7 @@ int ple_top(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, i
 extern "C" {
 
 const char *gf2e_last_error(void) { return g_err.c_str(); }
-const char *gf2e_version(void) { return "gf2e_b200 0.1 (sm_100a; tcgen05 kind::i8 + M4RM)"; }
+const char *gf2e_version(void) { return "gf2e_b200 0.2 (sm_100a; tcgen05 cta_group::2 kind::mxf4 + kind::i8, M4RM)"; }
 int gf2e_last_launch_count(void) { return g_launches; }
 const char *gf2e_last_product_kernel(void) { return g_kernel; }
 
