@@ -39,7 +39,7 @@
 //               K-major SWIZZLE_128B layout, fence.proxy.async, arrive on the leader's full[s]
 //   warps 4-11  epilogue: tcgen05.ld pack::16b, parity via sign-replicating PRMT, fold into
 //               E register-resident output planes (the columns of M), store the tile once
-//   warp 12     MMA issuer (leader CTA, one thread)
+//   warp 12     MMA issuer (leader CTA, one elected lane of the warp)
 //   warp 13     loader: cp.async.bulk of the stage-tiled bit tiles into a ring (mbarrier tx)
 // Synchronisation across the pair:
 //   full[s]   (leader)   <- 4 expander warps x 2 CTAs (relaxed remote arrive after the fence;
@@ -560,30 +560,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             }
         }
     } else if (warp == MMA_WARP && rank == 0) {
-        // ===================== MMA issuer (leader CTA, one thread) =====================
-        if (lane == 0) {
-            int64_t gp = 0;
-            int st = 0;
-            uint32_t phase = 0;
-            const uint32_t st0 = smem_u32(stages);
-            const uint32_t idesc = FP4 ? idesc_mxf4(2 * BM, BN) : idesc_i8(2 * BM, BN);
-            static_assert(BN % 16 == 0 && BN <= 256, "cta_group::2 MMA N");
-            for (int64_t ti = 0; ti < my_tiles; ++ti) {
-                for (int t = 0; t < s.nprod; t += STEP) {
-                    const int units = (PAIR && t + 1 < s.nprod) ? 2 : 1;
-                    for (int ch = 0; ch < nchunks; ++ch, ++gp) {
-                        const int buf = (int)(gp % C::NBUF);
-                        TW(i_tempty, mbar_wait(&bars->tempty[buf], (uint32_t)((gp / C::NBUF) & 1) ^ 1));
-                        tc_fence_after();
-                        const uint32_t dt = tmem + (uint32_t)(buf * BN);
-                        const int ks1 = (ch + 1) * chunk < nks ? (ch + 1) * chunk : nks;
-                        for (int u = 0; u < units; ++u) {
-                            const uint32_t sfa = tmem + (u ? C::SFA1 : C::SFA0);
-                            for (int ks = ch * chunk; ks < ks1; ++ks) {
-                                TW(i_full, mbar_wait(&bars->full[st], phase));
-                                tc_fence_after();
-                                const uint32_t sa = st0 + (uint32_t)(st * STAGE_BYTES);
-                                const uint32_t sb = sa + C::A_SMEM;
+        // ===================== MMA issuer (leader CTA, one elected thread) =====================
+        // The whole warp runs the loop, so the descriptors and TMEM addresses are warp-uniform
+        // (uniform registers); one elected lane issues the MMAs and commits.
+        const bool issuer = elect_one();
+        int64_t gp = 0;
+        int st = 0;
+        uint32_t phase = 0;
+        const uint32_t st0 = smem_u32(stages);
+        const uint32_t idesc = FP4 ? idesc_mxf4(2 * BM, BN) : idesc_i8(2 * BM, BN);
+        static_assert(BN % 16 == 0 && BN <= 256, "cta_group::2 MMA N");
+        for (int64_t ti = 0; ti < my_tiles; ++ti) {
+            for (int t = 0; t < s.nprod; t += STEP) {
+                const int units = (PAIR && t + 1 < s.nprod) ? 2 : 1;
+                for (int ch = 0; ch < nchunks; ++ch, ++gp) {
+                    const int buf = (int)(gp % C::NBUF);
+                    TW(i_tempty, mbar_wait(&bars->tempty[buf], (uint32_t)((gp / C::NBUF) & 1) ^ 1));
+                    tc_fence_after();
+                    const uint32_t dt = tmem + (uint32_t)(buf * BN);
+                    const int ks1 = (ch + 1) * chunk < nks ? (ch + 1) * chunk : nks;
+                    for (int u = 0; u < units; ++u) {
+                        const uint32_t sfa = tmem + (u ? C::SFA1 : C::SFA0);
+                        for (int ks = ch * chunk; ks < ks1; ++ks) {
+                            TW(i_full, mbar_wait(&bars->full[st], phase));
+                            tc_fence_after();
+                            const uint32_t sa = st0 + (uint32_t)(st * STAGE_BYTES);
+                            const uint32_t sb = sa + C::A_SMEM;
+                            if (issuer) {
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk) {
                                     const uint64_t ad = umma_desc_sw128(sa + kk * 32),
@@ -597,14 +600,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                                         mma2_i8(dt, ad, bd, idesc, (ks != ch * chunk) | kk);
                                 }
                                 mma2_commit_both(&bars->empty[st]);
-                                if (++st == S) {
-                                    st = 0;
-                                    phase ^= 1;
-                                }
+                            }
+                            __syncwarp();
+                            if (++st == S) {
+                                st = 0;
+                                phase ^= 1;
                             }
                         }
-                        mma2_commit_both(&bars->tfull[buf]);
                     }
+                    if (issuer) mma2_commit_both(&bars->tfull[buf]);
+                    __syncwarp();
                 }
             }
         }
