@@ -40,7 +40,8 @@
 //   warps 4-11  epilogue: tcgen05.ld pack::16b, parity via sign-replicating PRMT, fold into
 //               E register-resident output planes (the columns of M), store the tile once
 //   warp 12     MMA issuer (leader CTA, one elected lane of the warp)
-//   warp 13     loader: cp.async.bulk of the stage-tiled bit tiles into a ring (mbarrier tx)
+//   warp 13     loader: cp.async.bulk of the stage-tiled bit tiles into a ring (mbarrier tx),
+//               one elected lane issuing
 // Synchronisation across the pair:
 //   full[s]   (leader)   <- 4 expander warps x 2 CTAs (relaxed remote arrive after the fence;
 //                           release.cluster would compile to MEMBAR.ALL.GPU)
@@ -401,33 +402,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
             }
         }
     } else if (warp == LOAD_WARP) {
-        // ===================== bit-tile loader (both CTAs, one thread) =====================
-        if (lane == 0) {
-            const int64_t KS = a.kwords / C::KW;  // k-stages per row block
-            const int64_t tile_words = BM * C::KW, tile_words_b = BNH * C::KW;
-            const uint32_t bits_s = smem_u32(bits);
-            int slot = 0;
-            uint32_t bph = 0;
-            for (int64_t ti = 0; ti < my_tiles; ++ti) {
-                const int64_t tile = cluster + ti * nclusters;
-                int64_t tm, tn;
-                tile_coords(tile, tiles_m, tiles_n, tm, tn);
-                const int64_t rbA = tm * 2 + rank;  // 128-row block of A
-                const int64_t rbB = tn * 2 + rank;  // BNH-row block of B^T
-                for (int t = 0; t < s.nprod; ++t) {
-                    const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * tile_words;
-                    const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * tile_words_b;
-                    for (int ks = 0; ks < nks; ++ks) {
-                        mbar_wait_sleep(&bars->bempty[slot], bph ^ 1, LOAD_SLEEP_NS);
+        // ===================== bit-tile loader (both CTAs, one elected lane) =====================
+        // the whole warp walks the stages (addresses warp-uniform), one lane issues the copies
+        const bool issuer = elect_one();
+        const int64_t KS = a.kwords / C::KW;  // k-stages per row block
+        const int64_t tile_words = BM * C::KW, tile_words_b = BNH * C::KW;
+        const uint32_t bits_s = smem_u32(bits);
+        int slot = 0;
+        uint32_t bph = 0;
+        for (int64_t ti = 0; ti < my_tiles; ++ti) {
+            const int64_t tile = cluster + ti * nclusters;
+            int64_t tm, tn;
+            tile_coords(tile, tiles_m, tiles_n, tm, tn);
+            const int64_t rbA = tm * 2 + rank;  // 128-row block of A
+            const int64_t rbB = tn * 2 + rank;  // BNH-row block of B^T
+            for (int t = 0; t < s.nprod; ++t) {
+                const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * tile_words;
+                const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * tile_words_b;
+                for (int ks = 0; ks < nks; ++ks) {
+                    mbar_wait_sleep(&bars->bempty[slot], bph ^ 1, LOAD_SLEEP_NS);
+                    const uint32_t dst = bits_s + (uint32_t)(slot * C::BITS_BYTES);
+                    if (issuer) {
                         mbar_arrive_expect_tx(&bars->bfull[slot], C::BITS_BYTES);
-                        const uint32_t dst = bits_s + (uint32_t)(slot * C::BITS_BYTES);
                         bulk_g2s(dst, Ab + ks * tile_words, C::BITS_A, &bars->bfull[slot]);
                         bulk_g2s(dst + C::BITS_A, Bb + ks * tile_words_b, C::BITS_BYTES - C::BITS_A,
                                  &bars->bfull[slot]);
-                        if (++slot == C::D) {
-                            slot = 0;
-                            bph ^= 1;
-                        }
+                    }
+                    __syncwarp();
+                    if (++slot == C::D) {
+                        slot = 0;
+                        bph ^= 1;
                     }
                 }
             }
