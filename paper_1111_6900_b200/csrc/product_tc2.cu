@@ -475,9 +475,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_tc2(const Sched s, cons
                     TW(i_tfull, mbar_wait_sleep(&bars->tfull[buf], (uint32_t)((gp / C::NBUF) & 1), idle_ns));
                     tc_fence_after();
                     // chunks per tcgen05.ld: 2 (x32: 64 columns, half the load/wait round trips of
-                    // the drain) where the output words live in shared memory (long-k form); 1
-                    // (x16: 32 columns) for the register-resident forms (register pressure)
-                    constexpr int LB = C::SPLIT ? 2 : 1;
+                    // the drain) where the output words live in shared memory (long-k form) or
+                    // the accumulator is not re-initialised (int8); 1 (x16: 32 columns) for the
+                    // other register-resident forms (register pressure)
+                    constexpr int LB = (C::SPLIT || !FP4) ? 2 : 1;
 #pragma unroll
                     for (int c0 = 0; c0 < CH; c0 += LB) {
                         uint32_t v[LB][16];
