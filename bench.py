@@ -120,18 +120,20 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_sample(e: int, k: int, n: int, rows: int, threads: int = 0):
-    """Oracle ("port") karatsuba on C rows [0, rows) — a bounded slice of the same workload."""
+def cpu_sample(e: int, k: int, n: int, rows: int, threads: int = 0, acc: bool = False, row0: int = 0):
+    """Oracle ("port") karatsuba on C rows [row0, row0 + rows) — a bounded slice of the same
+    workload (A seed 1, B seed 2, C0 seed 3 for addmul).  Returns (Tbit-op/s, s, C rows)."""
     import oracle
 
     f = DEFAULT_F[e]
-    a = oracle.sliced_random(e, rows, k, 1)
+    a = oracle.sliced_random(e, rows, k, 1, row0=row0, gcols=k)
     b = oracle.sliced_random(e, k, n, 2)
+    c0 = oracle.sliced_random(e, rows, n, 3, row0=row0, gcols=n) if acc else None
     t0 = time.perf_counter()
-    oracle.karatsuba(e, f, a, b, rows, k, n, nthreads=threads)
+    ref, _ = oracle.karatsuba(e, f, a, b, rows, k, n, C0=c0, nthreads=threads)
     dt = time.perf_counter() - t0
     ops = K_OF_E[e] * 2.0 * rows * k * n
-    return ops / dt / 1e12, dt
+    return ops / dt / 1e12, dt, ref
 
 
 def run_reference(args):
@@ -145,9 +147,9 @@ def run_reference(args):
     cores = host_threads()
     vals = []
     for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_sample(e, k, n, min(rows, 64), cores)
+        cpu_sample(e, k, n, min(rows, 64), cores, acc)
     for _ in range(args.steps):
-        v, dt = cpu_sample(e, k, n, rows, cores)
+        v, dt, _ = cpu_sample(e, k, n, rows, cores, acc)
         vals.append((v, dt))
     v = statistics.median(x[0] for x in vals)
     dt = statistics.median(x[1] for x in vals)
@@ -210,11 +212,13 @@ def run_ours(args):
          else g.SlicedMatrix(ctx, m, n, torch.empty((e, m, g.words_for(n)), dtype=torch.int64, device=dev)))
     torch.cuda.synchronize()
 
+    out = [C]
+
     def step():
         if acc:
             g.addmul(C, A, B, backend=backend)
         else:
-            g.karatsuba_mul(A, B, backend=backend)
+            out[0] = g.karatsuba_mul(A, B, backend=backend)
         return _lib.last_launch_count()
 
     for _ in range(args.warmup):
@@ -250,6 +254,15 @@ def run_ours(args):
     ms_max, prod_ms_max = float(t[0]), float(t[1])
     value = world * ops_rank / (ms_max * 1e-3) / 1e12
 
+    # parity sample of the timed result: C rows [0, prow) of this rank's block (C0 ^ A.B for
+    # addmul: one more untimed step when the step count left C at C0), compared on rank 0
+    # with the oracle rows computed for cpu_baseline
+    prow = min(m, args.cpu_rows or (256 if k * n >= 16384 * 16384 else min(m, 1024)))
+    if acc and (args.warmup + args.steps) % 2 == 0:
+        step()
+    dev_rows = out[0].planes[:, :prow].cpu().numpy().view("uint64").copy()
+    del out
+
     # ---- e2e through the public host-buffer API (gf2e_mzed_mul_host), per step: H2D of packed A
     #      and B from pinned host memory, slice, combos, product, cling, D2H of packed C; the
     #      library overlaps copies of one row chunk with the kernels of another.  Timed by CUDA
@@ -266,8 +279,8 @@ def run_ours(args):
         hB.copy_(Bp.storage.words)
         wpc = g.words_for(n * g.pack_width(e))
         hC = torch.empty((m, wpc), dtype=torch.int64, pin_memory=True)
-        if acc:
-            hC.copy_(g.cling(C).storage.words)
+        if acc:  # C0 again (the device C above holds C0 ^ A.B)
+            hC.copy_(g.cling(g.SlicedMatrix.random(ctx, m, n, 3, row0=row0, gcols=n)).storage.words)
         del Ap, Bp
         nA, nB, nC = (t.numpy().view(np.uint64) for t in (hA, hB, hC))
 
@@ -276,11 +289,15 @@ def run_ours(args):
                 return g.karatsuba_mul_packed_host(ctx, nA, k, nB, n, C_words=nC, chunk_rows=args.chunk_rows)[1]
             return g.karatsuba_mul_packed_host(ctx, nA, k, nB, n, out=nC, chunk_rows=args.chunk_rows)[1]
 
-        for _ in range(max(1, args.warmup)):
+        e2e_warm = max(1, args.warmup)
+        for _ in range(e2e_warm):
             e2e_step()
         if use_pg:
             dist.barrier()
         ms_list = [e2e_step() for _ in range(args.steps)]
+        if acc and (e2e_warm + args.steps) % 2 == 0:
+            e2e_step()  # leave hC = C0 ^ A.B for the parity sample
+        e2e_rows = nC[:prow].copy()
         te = torch.tensor([sum(ms_list) / len(ms_list)], dtype=torch.float64, device=dev)
         if use_pg:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -337,15 +354,21 @@ def run_ours(args):
 
     if e2e:
         line["e2e"] = e2e
-    if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 figure
+    if not args.no_cpu_baseline:
         import oracle
 
-        rows = args.cpu_rows or (256 if k * n >= 16384 * 16384 else min(m, 1024))
-        v, dt = cpu_sample(e, k, n, rows, host_threads())
-        line["cpu_baseline"] = {"value": round(v, 4), "unit": "Tbit-op/s", "cores": host_threads(),
-                                "kind": "port",
-                                "sample": f"rows 0..{rows - 1} of C ({rows}x{k}x{n}, e={e}) via oracle.karatsuba, "
-                                          f"{dt:.2f} s"}
+        # rank 0's rows 0..prow-1 are rows 0..prow-1 of the global C at every N
+        v, dt, ref = cpu_sample(e, k, n, prow, host_threads(), acc)
+        if world == 1:  # the CPU baseline is an N=1 figure
+            line["cpu_baseline"] = {"value": round(v, 4), "unit": "Tbit-op/s", "cores": host_threads(),
+                                    "kind": "port",
+                                    "sample": f"rows 0..{prow - 1} of C ({prow}x{k}x{n}, e={e}) via oracle.karatsuba, "
+                                              f"{dt:.2f} s"}
+        par = {"rows": f"C rows 0..{prow - 1} (all {n} columns, all {e} planes) vs oracle.karatsuba",
+               "device": "ok" if (dev_rows == ref).all() else "MISMATCH"}
+        if e2e:
+            par["e2e"] = "ok" if (e2e_rows == oracle.cling_words(e, prow, n, ref)).all() else "MISMATCH"
+        line["parity"] = par
     print(json.dumps(line), flush=True)
     if use_pg:
         dist.destroy_process_group()

@@ -39,10 +39,12 @@ extern "C" {
 
 /* gf2e_slice_mul flags */
 #define GF2E_ACCUMULATE 1u   /* C ^= A*B (addmul) instead of C = A*B              */
-#define GF2E_BACKEND_TC 0u   /* K4 on tcgen05 kind::i8 tensor cores (default)     */
+#define GF2E_BACKEND_TC 0u   /* K4 on tcgen05 tensor cores (default): kind::mxf4 (e2m1 0/1,
+                                exact fp32 accumulation) for k >= 2048, kind::i8 below      */
 #define GF2E_BACKEND_M4RM 2u /* K4 as M4RM Gray tables in shared memory (INT pipe) */
-#define GF2E_TC_INT8 4u      /* tensor-core K4 forced to kind::i8                          */
-#define GF2E_TC_FP4 8u       /* tensor-core K4 forced to kind::mxf4 (default for k >= 2048)  */
+#define GF2E_TC_INT8 4u      /* tensor-core K4 forced to kind::i8 at every k                */
+#define GF2E_TC_FP4 8u       /* tensor-core K4 forced to kind::mxf4 at every k (paired form
+                                below k = 2048)                                             */
 
 /* Last error message of the calling thread ("" if none). */
 const char *gf2e_last_error(void);
@@ -138,7 +140,7 @@ int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, int64_
  * A (and C0) then stream through in chunks of `chunk_rows` rows (<= 0: a wave-aware plan
  * around 2048 rows) with the copies, operand preparation, products and copy-out of
  * consecutive chunks overlapped on four internal streams.  Device memory
- * comes from the stream-ordered pool.  *device_ms (optional) = CUDA-event time from the first
+ * comes from the library's own stream-ordered pool (gf2e_trim_pool).  *device_ms (optional) = CUDA-event time from the first
  * H2D to the last D2H.
  */
 int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_host, int64_t lda, const uint64_t *B_host,
@@ -245,6 +247,25 @@ int gf2e_mma_peak(int cta_group, int iters, double *tops, double *ms, void *stre
 int gf2e_dev_fp4_probe(int iters, int mode, const uint8_t *a_dev, const uint8_t *b_dev, uint32_t *out_dev,
                        double *tops, void *stream);
 int gf2e_profile_read(double *total_ms, int *launches);
+
+/*
+ * fp4 exactness self-check.  The kind::mxf4 forms of the product assume exact fp32
+ * accumulation of 0/1 products (measured, not architecturally guaranteed).  Before the first
+ * fp4 product on a device the library compares every fp4 form with the int8 form (integer
+ * arithmetic) on random and all-ones GF(2) planes, k up to 33024 (across the 32768-bit
+ * accumulation chunk); on any mismatch fp4 is disabled on that device and every product uses
+ * kind::i8.  This entry runs the check if it has not run (rerun != 0: again) and reports
+ * *ok = 1 (fp4 in use) or -1 (disabled).  inject_fault != 0 (tests) corrupts the fp4 results
+ * of this check, so it must fail and disable fp4.
+ */
+int gf2e_fp4_selfcheck(int rerun, int inject_fault, int *ok);
+
+/*
+ * Release the current device's cached temporaries of the library pool (host-buffer
+ * pipeline, PLE/echelonize scratch) down to keep_bytes; synchronises the device.  The pool
+ * keeps at most 4 GiB between calls on its own.
+ */
+int gf2e_trim_pool(int64_t keep_bytes);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,8 @@ SIGNATURES = {
     "gf2e_profile_read": (_INT, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_INT)]),
     "gf2e_dev_fp4_probe": (_INT, [_INT, _INT, _P, _P, _P, ctypes.POINTER(ctypes.c_double), _P]),
     "gf2e_mma_peak": (_INT, [_INT, _INT, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
+    "gf2e_trim_pool": (_INT, [_I64]),
+    "gf2e_fp4_selfcheck": (_INT, [_INT, _INT, ctypes.POINTER(_INT)]),
 }
 
 _lib = None
@@ -161,6 +163,15 @@ def mma_peak_fp4(iters: int = 20000, operands: str = "zero") -> float:
     check(load().gf2e_dev_fp4_probe(iters, 0, a.data_ptr(), b.data_ptr(), out.data_ptr(), ctypes.byref(tops),
                                     torch.cuda.current_stream().cuda_stream), "gf2e_dev_fp4_probe")
     return tops.value
+
+
+def fp4_selfcheck(rerun: bool = False, inject_fault: bool = False) -> int:
+    """Run (once per device, or again with rerun) the fp4 exactness self-check: 1 = the fp4
+    forms matched the int8 form bit for bit and stay in use, -1 = mismatch, fp4 disabled."""
+    ok = ctypes.c_int()
+    check(load().gf2e_fp4_selfcheck(1 if rerun else 0, 1 if inject_fault else 0, ctypes.byref(ok)),
+          "gf2e_fp4_selfcheck")
+    return ok.value
 
 
 def last_product_kernel() -> str:

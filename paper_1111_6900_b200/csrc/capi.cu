@@ -62,6 +62,12 @@ int cuda_fail(cudaError_t e, const char *what) {
     return fail(GF2E_ECUDA, "CUDA error in %s: %s", what, cudaGetErrorString(e));
 }
 
+#define CKH(expr, what)                                    \
+    do {                                                   \
+        cudaError_t _e = (expr);                           \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
 #define CK(expr, what)                               \
     do {                                             \
         cudaError_t _e = (expr);                     \
@@ -210,6 +216,54 @@ Sched plane_sched() {
     return k;
 }
 
+// ---- library memory pool ----------------------------------------------------------------
+// Temporaries of the host-buffer pipeline and of PLE/echelonize come from a pool the library
+// owns (one per device), not the device's default pool, so the process-wide default pool and
+// the PyTorch caching allocator are untouched.  The pool keeps up to kPoolKeep bytes mapped
+// across calls (re-mapping gigabytes per call costs milliseconds) and returns the rest to the
+// driver at each synchronisation; gf2e_trim_pool() releases the cached memory on demand.
+constexpr uint64_t kPoolKeep = 4ull << 30;
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[kMaxDevices] = {};
+
+cudaMemPool_t lib_pool() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (!g_pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+        uint64_t keep = kPoolKeep;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        g_pools[dev] = pool;
+    }
+    return g_pools[dev];
+}
+
+cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st) {
+    cudaMemPool_t pool = lib_pool();
+    if (!pool) return cudaErrorMemoryAllocation;
+    return cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
+
+// stream-ordered temporary from the library pool, freed at scope exit
+struct DevTmpAny {
+    void *p = nullptr;
+    cudaStream_t st;
+    DevTmpAny(size_t bytes, cudaStream_t s) : st(s) {
+        if (bytes && pool_alloc(&p, bytes, st) != cudaSuccess) p = nullptr;
+    }
+    ~DevTmpAny() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    DevTmpAny(const DevTmpAny &) = delete;
+    DevTmpAny &operator=(const DevTmpAny &) = delete;
+};
+
 // ---- device check ---------------------------------------------------------------------
 int check_device() {
     int dev = 0;
@@ -219,18 +273,6 @@ int check_device() {
     e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
     if (e != cudaSuccess) return fail(GF2E_ENODEV, "cannot query device: %s", cudaGetErrorString(e));
     if (major != 10) return fail(GF2E_ENODEV, "libgf2e_b200 needs an sm_100 (B200) device, found sm_%d", major * 10);
-    // Temporaries (host-buffer API, PLE) come from the device's default stream-ordered pool.
-    // Its default release threshold (0) hands freed blocks back to the driver at every
-    // synchronisation, so each call would re-map gigabytes; keep them pooled instead.
-    static bool pool_set[64] = {};
-    if (dev >= 0 && dev < 64 && !pool_set[dev]) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-        pool_set[dev] = true;
-    }
     return GF2E_OK;
 }
 
@@ -259,8 +301,19 @@ int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 constexpr int64_t kFp4MinK = 2048;
 constexpr int kSmallKForm = kFormI8;
 constexpr int64_t kFp4LongK = 8192;  // 8 expander / 4 epilogue warps pay off for long accumulations
+// fp4 exactness self-check state per device: 0 not run, 1 passed, -1 failed (fp4 disabled)
+int g_fp4_state[kMaxDevices] = {};
+std::mutex g_fp4_mu;
+int fp4_state() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
+    std::lock_guard<std::mutex> lk(g_fp4_mu);
+    return g_fp4_state[dev];
+}
+
 int tc_form(uint32_t flags, int64_t k) {
     if (flags & GF2E_TC_INT8) return kFormI8;
+    if (fp4_state() < 0) return kFormI8;  // the fp4 self-check failed on this device
     if (k >= kFp4LongK) return kFormFp4Long;
     if (k >= kFp4MinK) return kFormFp4;
     if (flags & GF2E_TC_FP4) return kFormFp4Pair;
@@ -273,7 +326,7 @@ const char *form_name(int form) {
                                                         : "k_product_tc2<i8>";
 }
 
-Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags) {
+Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags, int fp4 = -1) {
     Layout L;
     if (flags & GF2E_BACKEND_M4RM) {
         L.m_pad = round_up(m, kM4BM);
@@ -285,7 +338,7 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags) {
     } else {
         L.m_pad = round_up(m, 2 * kTcBM);  // CTA-pair tiles are 256 rows
         L.n_pad = round_up(n, kTcBN);
-        L.k_pad = round_up(k, use_fp4(flags, k) ? kTcBKFp4 : kTcBK);
+        L.k_pad = round_up(k, (fp4 < 0 ? use_fp4(flags, k) : fp4 != 0) ? kTcBKFp4 : kTcBK);
         L.kwords = L.k_pad / 64;
         L.a_pstride = L.m_pad * L.kwords;
         L.b_pstride = L.n_pad * L.kwords;
@@ -297,9 +350,11 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags) {
 }
 
 // The shared launch sequence: K3 combos -> fused K4/K5 product.
+int ensure_fp4_checked();
+
 int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, const uint64_t *B, int64_t ldb,
                 int64_t pb, uint64_t *C, int64_t ldc, int64_t pc, int64_t m, int64_t k, int64_t n, uint32_t flags,
-                void *ws, int64_t ws_bytes, cudaStream_t st) {
+                void *ws, int64_t ws_bytes, cudaStream_t st, int form_override = -1) {
     const bool acc = (flags & GF2E_ACCUMULATE) != 0;
     const int64_t nw = words_for(n);
     if (m == 0 || n == 0) return GF2E_OK;
@@ -309,15 +364,18 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
                 CK(cudaMemset2DAsync(C + j * pc, ldc * 8, 0, nw * 8, m, st), "cudaMemset2DAsync");
         return GF2E_OK;
     }
-    Layout L = layout_for(ks.nprod, m, k, n, flags);
+    const bool tc = !(flags & GF2E_BACKEND_M4RM);
+    if (tc && form_override < 0 && !(flags & GF2E_TC_INT8))
+        if (int rc = ensure_fp4_checked()) return rc;
+    const int form = form_override >= 0 ? form_override : tc_form(flags, k);
+    const bool fp4 = tc && form != kFormI8;
+    Layout L = layout_for(ks.nprod, m, k, n, flags, fp4);
     if (ws_bytes < L.total)
         return fail(GF2E_ENOMEM, "workspace too small: %lld < %lld bytes", (long long)ws_bytes, (long long)L.total);
     if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255))
         return fail(GF2E_EINVAL, "workspace must be a 256-byte aligned device pointer");
     uint64_t *Ac = static_cast<uint64_t *>(ws);
     uint64_t *Bx = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + L.a_bytes);
-    const bool tc = !(flags & GF2E_BACKEND_M4RM);
-    const bool fp4 = tc && use_fp4(flags, k);
     CK(launch_combos_rows(ks, A, lda, pa, m, k, Ac, L.kwords, L.a_pstride, L.m_pad, L.kwords, tc ? (fp4 ? 4 : 2) : 0,
                           st),
        "combos(A)");
@@ -336,13 +394,95 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
            "combos(B^T)");
         TcArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, m, n, L.m_pad, L.n_pad, C, ldc, pc, acc ? 1 : 0};
         ProfScope prof(st);
-        const int form = tc_form(flags, k);
         CK(launch_product_tc2(ks, a, form, st), "product_tc2");
         g_kernel = form_name(form);
     }
     return GF2E_OK;
 }
 
+
+// ---- fp4 exactness self-check ---------------------------------------------------------------
+// The fp4 forms rely on kind::mxf4 accumulating exact small integers in fp32 (parity = bit 7
+// of the pattern, product_tc2.cu header).  That is measured behaviour (tools/fp4_probe.py),
+// not an architectural guarantee, so before the first fp4 product on a device the library
+// multiplies GF(2) planes in every fp4 form and in the int8 form (integer arithmetic, exact
+// by construction) and compares them bit for bit: random operands and all-ones operands
+// (count = k, the largest accumulator values) at k = 33024, across the 32768-bit accumulation
+// chunk boundary of the long form; k = 4096 (short form); k = 1024 (paired form).  On any
+// mismatch fp4 is disabled on that device (every product takes the int8 form) and
+// gf2e_fp4_selfcheck reports it.
+bool g_fp4_inject = false;  // test hook: corrupt the fp4 results of the next check
+
+int fp4_probe_run(bool inject, int *ok) {
+    *ok = 0;
+    const int64_t m = 256, n = 256;
+    const struct {
+        int form;
+        int64_t k;
+    } cases[] = {{kFormFp4Long, 33024}, {kFormFp4, 4096}, {kFormFp4Pair, 1024}};
+    cudaStream_t st = nullptr;
+    CKH(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    } sg{st};
+    const Sched ks = plane_sched();
+    const int64_t kmax = 33024, nw = n / 64;
+    const int64_t ws_bytes = layout_for(1, m, kmax, n, 0, 1).total;
+    DevTmpAny A((size_t)m * (kmax / 64) * 8, st), B((size_t)kmax * nw * 8, st), C8((size_t)m * nw * 8, st),
+        C4((size_t)m * nw * 8, st), ws((size_t)ws_bytes, st);
+    if (!A.p || !B.p || !C8.p || !C4.p || !ws.p) return fail(GF2E_ENOMEM, "out of device memory (fp4 self-check)");
+    uint64_t *a = static_cast<uint64_t *>(A.p), *b = static_cast<uint64_t *>(B.p);
+    uint64_t *c8 = static_cast<uint64_t *>(C8.p), *c4 = static_cast<uint64_t *>(C4.p);
+    std::vector<uint64_t> h8((size_t)m * nw), h4((size_t)m * nw);
+    bool good = true;
+    for (const auto &cs : cases) {
+        const int64_t kw = cs.k / 64;
+        for (int ones = 0; ones < 2; ++ones) {
+            if (ones) {
+                CKH(cudaMemsetAsync(a, 0xFF, (size_t)m * kw * 8, st), "cudaMemsetAsync");
+                CKH(cudaMemsetAsync(b, 0xFF, (size_t)cs.k * nw * 8, st), "cudaMemsetAsync");
+            } else {
+                CKH(launch_random_words(m, cs.k, 0x5eed0 + (uint64_t)cs.k, a, kw, st), "random_words");
+                CKH(launch_random_words(cs.k, n, 0x5eed1 + (uint64_t)cs.k, b, nw, st), "random_words");
+            }
+            if (int rc = run_product(ks, a, kw, 0, b, nw, 0, c8, nw, 0, m, cs.k, n, GF2E_TC_INT8, ws.p, ws_bytes, st,
+                                     kFormI8))
+                return rc;
+            if (int rc = run_product(ks, a, kw, 0, b, nw, 0, c4, nw, 0, m, cs.k, n, 0, ws.p, ws_bytes, st, cs.form))
+                return rc;
+            CKH(cudaMemcpyAsync(h8.data(), c8, h8.size() * 8, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+            CKH(cudaMemcpyAsync(h4.data(), c4, h4.size() * 8, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+            CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            if (inject) h4[(size_t)cs.k % h4.size()] ^= 1;
+            if (std::memcmp(h8.data(), h4.data(), h8.size() * 8) != 0) good = false;
+        }
+    }
+    *ok = good ? 1 : -1;
+    return GF2E_OK;
+}
+
+// run the self-check once per device (first fp4-capable product); 0 or an error status
+int ensure_fp4_checked() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return GF2E_OK;
+    {
+        std::lock_guard<std::mutex> lk(g_fp4_mu);
+        if (g_fp4_state[dev] != 0) return GF2E_OK;
+    }
+    const int launches = g_launches;
+    int ok = 0;
+    int rc = fp4_probe_run(g_fp4_inject, &ok);
+    g_launches = launches;  // the check's launches are not the caller's
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_fp4_mu);
+    g_fp4_state[dev] = ok;
+    g_fp4_inject = false;
+    return GF2E_OK;
+}
 
 // ---- host-buffer packed multiply (e2e entry) ----------------------------------------------
 int pair_count() {
@@ -450,18 +590,13 @@ struct HostPlan {
     template <typename T>
     cudaError_t alloc(T **p, int64_t bytes) {
         void *q = nullptr;
-        cudaError_t e = cudaMallocAsync(&q, (size_t)(bytes > 256 ? bytes : 256), sc);
+        cudaError_t e = pool_alloc(&q, (size_t)(bytes > 256 ? bytes : 256), sc);
         if (e == cudaSuccess) allocs.push_back(q);
         *p = static_cast<T *>(q);
         return e;
     }
 };
 
-#define CKH(expr, what)                                    \
-    do {                                                   \
-        cudaError_t _e = (expr);                           \
-        if (_e != cudaSuccess) return cuda_fail(_e, what); \
-    } while (0)
 
 
 // ---- blocked TRSM over plane views (consumer of run_product) ------------------------------
@@ -569,7 +704,7 @@ struct DevTmp {
     void *p = nullptr;
     cudaStream_t st;
     DevTmp(size_t bytes, cudaStream_t s) : st(s) {
-        if (bytes && cudaMallocAsync(&p, bytes, st) != cudaSuccess) p = nullptr;
+        if (bytes && pool_alloc(&p, bytes, st) != cudaSuccess) p = nullptr;
     }
     ~DevTmp() {
         if (p) cudaFreeAsync(p, st);
@@ -723,13 +858,18 @@ int ple_top(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, i
              static_cast<int64_t *>(ix.p), tab};
     // The pinned staging ring persists per host thread and only grows: pinning and unpinning
     // host pages on every call (cudaMallocHost / cudaFreeHost) stalled some calls for
-    // hundreds of milliseconds.  It is never freed (process lifetime).
+    // hundreds of milliseconds.  It is never freed (process lifetime).  One ring per device:
+    // its events belong to the device that was current when they were created.
     struct PinnedRing {
         int64_t *buf[PleCtx::kRing] = {};
         cudaEvent_t ev[PleCtx::kRing] = {};
         size_t bytes = 0;
     };
-    thread_local PinnedRing pr;
+    thread_local PinnedRing rings[kMaxDevices];
+    int dev = 0;
+    CKH(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= kMaxDevices) return fail(GF2E_ENODEV, "device index %d out of range", dev);
+    PinnedRing &pr = rings[dev];
     const size_t ring_bytes = (size_t)(3 * (m > n ? m : n) + 3) * 8;
     if (pr.bytes < ring_bytes) {
         for (int i = 0; i < PleCtx::kRing; ++i) {
@@ -829,6 +969,37 @@ int gf2e_dev_fp4_probe(int iters, int mode, const uint8_t *a_dev, const uint8_t 
     if (e != cudaSuccess) return cuda_fail(e, "fp4_probe");
     if (tops) *tops = (double)nsms * iters * 4.0 * 2.0 * 128.0 * 256.0 * 64.0 / (ms * 1e-3) / 1e12;
     return GF2E_OK;
+}
+
+int gf2e_fp4_selfcheck(int rerun, int inject_fault, int *ok) {
+    g_err.clear();
+    if (ok) *ok = 0;
+    if (int rc = check_device()) return rc;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (rerun || inject_fault) {
+        std::lock_guard<std::mutex> lk(g_fp4_mu);
+        g_fp4_state[dev] = 0;
+        g_fp4_inject = inject_fault != 0;
+    }
+    if (int rc = ensure_fp4_checked()) return rc;
+    if (ok) *ok = fp4_state();
+    return GF2E_OK;
+}
+
+int gf2e_trim_pool(int64_t keep_bytes) {
+    g_err.clear();
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return fail(GF2E_ENODEV, "no CUDA device");
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        pool = g_pools[dev];
+    }
+    if (!pool) return GF2E_OK;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemPoolTrimTo(pool, (size_t)(keep_bytes > 0 ? keep_bytes : 0));
+    return e == cudaSuccess ? GF2E_OK : cuda_fail(e, "gf2e_trim_pool");
 }
 
 int gf2e_pack_width(int e) {
@@ -995,6 +1166,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         return GF2E_OK;
     }
     if (int rc = check_device()) return rc;
+    if (int rc = ensure_fp4_checked()) return rc;
     Sched ks = to_kernel_sched(e, get_schedule(e, f));
     int64_t chunk = chunk_rows > 0 ? round_up(chunk_rows, 2 * kTcBM) : 2048;
     if (chunk > round_up(m, 2 * kTcBM)) chunk = round_up(m, 2 * kTcBM);
@@ -1022,15 +1194,15 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     CKH(cudaStreamCreateWithFlags(&P.sp, cudaStreamNonBlocking), "stream");
     Layout LB = layout_for(ks.nprod, chunk, k, n, 0);  // Ac sized for one chunk, Bt for all of B
     uint64_t *dBp, *dBs, *dBt, *dAc[2], *dAp[2], *dAs[2], *dCs[2], *dCp[2];
-    CKH(P.alloc(&dBp, k * wb * 8), "cudaMallocAsync");
-    CKH(P.alloc(&dBs, (int64_t)e * k * nwn * 8), "cudaMallocAsync");
-    CKH(P.alloc(&dBt, LB.b_bytes), "cudaMallocAsync");
+    CKH(P.alloc(&dBp, k * wb * 8), "pool_alloc");
+    CKH(P.alloc(&dBs, (int64_t)e * k * nwn * 8), "pool_alloc");
+    CKH(P.alloc(&dBt, LB.b_bytes), "pool_alloc");
     for (int sl = 0; sl < nslots; ++sl) {
-        CKH(P.alloc(&dAc[sl], LB.a_bytes), "cudaMallocAsync");
-        CKH(P.alloc(&dAp[sl], chunk * wa * 8), "cudaMallocAsync");
-        CKH(P.alloc(&dAs[sl], (int64_t)e * chunk * nwk * 8), "cudaMallocAsync");
-        CKH(P.alloc(&dCs[sl], (int64_t)e * chunk * nwn * 8), "cudaMallocAsync");
-        CKH(P.alloc(&dCp[sl], chunk * wb * 8), "cudaMallocAsync");
+        CKH(P.alloc(&dAc[sl], LB.a_bytes), "pool_alloc");
+        CKH(P.alloc(&dAp[sl], chunk * wa * 8), "pool_alloc");
+        CKH(P.alloc(&dAs[sl], (int64_t)e * chunk * nwk * 8), "pool_alloc");
+        CKH(P.alloc(&dCs[sl], (int64_t)e * chunk * nwn * 8), "pool_alloc");
+        CKH(P.alloc(&dCp[sl], chunk * wb * 8), "pool_alloc");
     }
     int64_t cb[kMaxBParts + 1];
     for (int p = 0; p <= nbp; ++p) cb[p] = p == nbp ? n : round_up(n * p / nbp, 2 * kTcBM);

@@ -114,8 +114,7 @@ struct PanelOut {
     uint64_t dval[64][kMaxE];
     uint64_t bt[64 * kMaxE * kMaxE];  // alpha^s * T_t, [t][s][plane]
 };
-// GF(2^e) tables for one field, in static device memory (kFieldTabSlots fields cached)
-constexpr int kFieldTabSlots = 16;
+// GF(2^e) tables for one field (one device allocation per (device, e, f), ple.cu: field_tab)
 struct FieldTab {
     uint16_t ex[1024], lg[1024], inv[1024];  // exp/log over a primitive element; inverses
     uint16_t mulmask[1024][kMaxE];           // bit p of [c][b] = coefficient b of c * x^p

@@ -27,6 +27,7 @@
 //     ple_echelon.py:338-340).
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <mutex>
 
 #include "common.cuh"
@@ -39,7 +40,6 @@ __device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDi
 __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
 
 // ---- per-field constant tables (static module memory, filled once per (e, f)) ----------------
-__device__ FieldTab g_field_tabs[kFieldTabSlots];
 
 #ifndef GF2E_PLE_WIN
 #define GF2E_PLE_WIN 128
@@ -501,24 +501,17 @@ static uint32_t gf_mul_h(uint32_t a, uint32_t b, int e, uint32_t f) {
     return acc;
 }
 
+// One table per (device, e, f), allocated on first use and kept for the process lifetime:
+// a returned pointer is never reused for another field, so no kernel can read a table that
+// another thread replaced (at most ~230 irreducible f of degree 2..10, 26 KiB each).
 const FieldTab *field_tab(int e, uint32_t f, uint32_t g) {
     static std::mutex mu;
-    static std::map<std::pair<int, uint32_t>, int> slots;
-    static int next = 0;
+    static std::map<std::tuple<int, int, uint32_t>, FieldTab *> tabs;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lk(mu);
-    FieldTab *base = nullptr;
-    if (cudaGetSymbolAddress(reinterpret_cast<void **>(&base), g_field_tabs) != cudaSuccess) return nullptr;
-    auto it = slots.find({e, f});
-    if (it != slots.end()) return base + it->second;
-    const int slot = next++ % kFieldTabSlots;
-    bool evict = false;
-    for (auto i = slots.begin(); i != slots.end();) {
-        evict = evict || i->second == slot;
-        i = (i->second == slot) ? slots.erase(i) : std::next(i);
-    }
-    // a slot is reused only after every kernel that may read it has finished (the callers'
-    // streams are non-blocking, so the upload below would not wait for them by itself)
-    if (evict && cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+    auto it = tabs.find({dev, e, f});
+    if (it != tabs.end()) return it->second;
     static FieldTab h;
     std::memset(&h, 0, sizeof(h));
     h.f = f;
@@ -536,9 +529,17 @@ const FieldTab *field_tab(int e, uint32_t f, uint32_t g) {
             for (int b = 0; b < e; ++b)
                 if ((prod >> b) & 1u) h.mulmask[c][b] |= (uint16_t)(1u << p);
         }
-    if (cudaMemcpyToSymbol(g_field_tabs, &h, sizeof(h), slot * sizeof(FieldTab)) != cudaSuccess) return nullptr;
-    slots[{e, f}] = slot;
-    return base + slot;
+    FieldTab *d = nullptr;
+    if (cudaMalloc(reinterpret_cast<void **>(&d), sizeof(FieldTab)) != cudaSuccess) return nullptr;
+    // complete before any kernel (on any stream) can be enqueued with d: a pageable cudaMemcpy
+    // may return before its DMA lands, so wait for the legacy stream it ran on
+    if (cudaMemcpy(d, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaStreamSynchronize(cudaStreamLegacy) != cudaSuccess) {
+        cudaFree(d);
+        return nullptr;
+    }
+    tabs[{dev, e, f}] = d;
+    return d;
 }
 
 cudaError_t launch_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t nwords, const int64_t *swaps,

@@ -192,24 +192,41 @@ def karatsuba_mul_packed_host(ctx: FieldCtx, A_words, k: int, B_words, n: int, C
     ``out``: optional preallocated (pinned) result array for C = A*B."""
     import numpy as np
 
+    from .mat_packed import pack_width
+
     A = np.ascontiguousarray(A_words, dtype=np.uint64)
     B = np.ascontiguousarray(B_words, dtype=np.uint64)
+    w = pack_width(ctx.e)
+    wa, wb = words_for(k * w), words_for(n * w)
+    if A.ndim != 2 or B.ndim != 2:
+        raise ValueError("A_words and B_words must be 2-D arrays of packed words")
     m = A.shape[0]
     if B.shape[0] != k:
         raise ValueError(f"inner dimensions differ: {m}x{k} times {B.shape[0]}x{n}")
+    if A.shape[1] < wa:
+        raise ValueError(f"A_words has {A.shape[1]} words per row, need {wa} for {k} columns")
+    if B.shape[1] < wb:
+        raise ValueError(f"B_words has {B.shape[1]} words per row, need {wb} for {n} columns")
+
+    def _check_out(C, name):
+        if not isinstance(C, np.ndarray) or C.dtype != np.uint64 or not C.flags.c_contiguous:
+            raise ValueError(f"{name} must be a C-contiguous uint64 array")
+        if C.ndim != 2 or C.shape[0] != m or C.shape[1] < wb:
+            raise ValueError(f"{name} must have shape ({m}, >= {wb}), got {C.shape}")
+        if not C.flags.writeable:
+            raise ValueError(f"{name} must be writeable")
+
     acc = C_words is not None
     if acc:
         C = C_words
-        if C.dtype != np.uint64 or not C.flags.c_contiguous:
-            raise ValueError("C_words must be a C-contiguous uint64 array")
+        _check_out(C, "C_words")
     elif out is not None:
         C = out
-        if C.dtype != np.uint64 or not C.flags.c_contiguous or C.shape[0] != m:
-            raise ValueError("out must be a C-contiguous uint64 array with one row per row of A")
+        _check_out(C, "out")
     else:
-        C = np.empty((m, B.shape[1]), dtype=np.uint64)
+        C = np.empty((m, wb), dtype=np.uint64)
     ms = ctypes.c_double()
-    _lib.call("gf2e_mzed_mul_host", ctx.e, ctx.f, A.ctypes.data, A.shape[1] if A.ndim == 2 else 0, B.ctypes.data,
+    _lib.call("gf2e_mzed_mul_host", ctx.e, ctx.f, A.ctypes.data, A.shape[1], B.ctypes.data,
               B.shape[1], C.ctypes.data, C.shape[1], m, k, n, _lib.ACCUMULATE if acc else 0, chunk_rows,
               ctypes.byref(ms))
     _bump(counters, ctx)

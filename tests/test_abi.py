@@ -106,3 +106,29 @@ def test_field_tables_match_reference(golden):
 
     for e in (2, 3, 4):
         assert np.array_equal(g.field_new(e).mul_table, golden[f"field/e{e}/mul"])
+
+
+def test_host_buffer_api_rejects_bad_shapes():
+    # karatsuba_mul_packed_host validates every host array before the library touches it
+    # (a short C would otherwise be read / written past its end by the H2D / D2H copies)
+    import numpy as np
+
+    ctx = g.field_new(8)
+    m, k, n = 10, 70, 90
+    A = np.zeros((m, g.words_for(k * 8)), dtype=np.uint64)
+    B = np.zeros((k, g.words_for(n * 8)), dtype=np.uint64)
+    C = np.zeros((m, g.words_for(n * 8)), dtype=np.uint64)
+    with pytest.raises(ValueError, match="shape"):
+        g.karatsuba_mul_packed_host(ctx, A, k, B, n, C_words=C[:m - 1].copy())
+    with pytest.raises(ValueError, match="shape"):
+        g.karatsuba_mul_packed_host(ctx, A, k, B, n, out=np.zeros((m, 3), dtype=np.uint64))
+    with pytest.raises(ValueError, match="shape"):
+        g.karatsuba_mul_packed_host(ctx, A, k, B, n, C_words=C.reshape(-1))
+    with pytest.raises(ValueError, match="C-contiguous uint64"):
+        g.karatsuba_mul_packed_host(ctx, A, k, B, n, C_words=C.astype(np.int64))
+    with pytest.raises(ValueError, match="words per row"):
+        g.karatsuba_mul_packed_host(ctx, A[:, :1], k, B, n)
+    with pytest.raises(ValueError, match="words per row"):
+        g.karatsuba_mul_packed_host(ctx, A, k, B[:, :2], n)
+    with pytest.raises(ValueError, match="inner dimensions differ"):
+        g.karatsuba_mul_packed_host(ctx, A, k + 1, B, n)

@@ -217,6 +217,20 @@ def _sampled_blocks(g, e, m, k, n, accumulate, rows, col_block, backend="tc"):
         assert np.array_equal(got[:, i:i + 1, :], ref), (r, col_block)
 
 
+def _row_blocks(g, C, e, k, n, accumulate, blocks, col_block):
+    """Contiguous row blocks [r0, r0 + nr) x columns [c0, c1) of the device result against the
+    oracle on the same windows of the generator streams (A seed 1, B seed 2, C0 seed 3)."""
+    ctx = C.ctx
+    c0, c1 = col_block
+    b = oracle.sliced_random(e, k, c1 - c0, 2, col0=c0, gcols=n)
+    for r0, nr in blocks:
+        got = C.planes[:, r0:r0 + nr, c0 // 64:-(-c1 // 64)].cpu().numpy().view(np.uint64)
+        a = oracle.sliced_random(e, nr, k, 1, row0=r0, gcols=k)
+        C0 = oracle.sliced_random(e, nr, c1 - c0, 3, row0=r0, col0=c0, gcols=n) if accumulate else None
+        ref, _ = oracle.karatsuba(e, ctx.f, a, b, nr, k, c1 - c0, C0=C0)
+        assert np.array_equal(got, ref), (e, r0, nr, col_block)
+
+
 @pytest.mark.slow
 def test_config3_sampled_blocks(g):
     # BASELINE config 3: F_256, 16384^3 on one GPU; sampled rows x 256-column blocks
@@ -226,10 +240,36 @@ def test_config3_sampled_blocks(g):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("e", [2, 5, 8, 10])
+def test_config3_full(g):
+    # BASELINE config 3 in full: every element of the 16384^3 F_256 product
+    # against the oracle's C restatement of the reference (poly_mul.py:245-259) on all host
+    # cores (~100 s on 16 threads)
+    e, m = 8, 16384
+    ctx = g.field_new(e)
+    C = g.karatsuba_mul(g.SlicedMatrix.random(ctx, m, m, 1), g.SlicedMatrix.random(ctx, m, m, 2))
+    got = C.to_numpy()
+    del C
+    ref, cnt = oracle.karatsuba(e, ctx.f, oracle.sliced_random(e, m, m, 1), oracle.sliced_random(e, m, m, 2), m, m, m)
+    assert cnt.gf2_matmul_count == 27
+    bad = np.nonzero((got != ref).any(axis=(0, 2)))[0]
+    assert bad.size == 0, f"{bad.size} rows differ, first {bad[:8]}"
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("e", range(2, 11))
 def test_config4_sampled_blocks(g, e):
-    # BASELINE config 4: C += A.B, A 65536x256, B 256x65536, C pre-filled (seed 3)
-    _sampled_blocks(g, e, 65536, 256, 65536, True, [0, 77, 32768, 65535], (65536 - 512, 65536))
+    # BASELINE config 4: C += A.B, A 65536x256, B 256x65536, C pre-filled (seed 3), every e;
+    # 64 rows (the first tile, a middle tile boundary, the last row tile) x the rightmost 512
+    # columns, and 16 rows x the first 256 columns
+    m, k, n = 65536, 256, 65536
+    ctx = g.field_new(e)
+    SA = g.SlicedMatrix.random(ctx, m, k, 1)
+    SB = g.SlicedMatrix.random(ctx, k, n, 2)
+    C = g.SlicedMatrix.random(ctx, m, n, 3)
+    g.addmul(C, SA, SB)
+    _sync()
+    _row_blocks(g, C, e, k, n, True, [(0, 16), (32760, 16), (m - 32, 32)], (n - 512, n))
+    _row_blocks(g, C, e, k, n, True, [(40000, 16)], (0, 256))
 
 
 @pytest.mark.parametrize("backend", BACKENDS)
@@ -351,3 +391,24 @@ def test_fuzz_shapes(g, seed):
         C0 = g.SlicedMatrix.random(ctx, m, n, seed + 3)
         g.addmul(C0, SA, SB, backend=backend)
         assert np.array_equal(C0.to_numpy(), ref ^ c0), (e, m, k, n, backend, "addmul")
+
+
+def test_fp4_selfcheck_guard(g):
+    # the fp4 exactness self-check: passes on this device; an injected mismatch disables the
+    # fp4 forms (products fall back to kind::i8 and stay bit-exact); a re-run restores them
+    assert g._lib.fp4_selfcheck() == 1
+    ctx = g.field_new(6)
+    m, k, n = 300, 9000, 200
+    SA = g.SlicedMatrix.random(ctx, m, k, 1)
+    SB = g.SlicedMatrix.random(ctx, k, n, 2)
+    ref, _ = oracle.karatsuba(6, ctx.f, oracle.sliced_random(6, m, k, 1), oracle.sliced_random(6, k, n, 2), m, k, n)
+    try:
+        assert g._lib.fp4_selfcheck(rerun=True, inject_fault=True) == -1
+        C = g.karatsuba_mul(SA, SB)
+        assert g._lib.last_product_kernel() == "k_product_tc2<i8>"
+        assert np.array_equal(C.to_numpy(), ref)
+    finally:
+        assert g._lib.fp4_selfcheck(rerun=True) == 1
+    C = g.karatsuba_mul(SA, SB)
+    assert g._lib.last_product_kernel() == "k_product_tc2<fp4>"
+    assert np.array_equal(C.to_numpy(), ref)
