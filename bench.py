@@ -383,7 +383,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--e", type=int, default=None, help="field degree for config 4")
-    ap.add_argument("--backend", default=None, choices=[None, "tc", "tc_i8", "tc_fp4", "m4rm"])
+    ap.add_argument("--backend", default=None, choices=[None, "tc", "tc_i8", "tc_fp4", "tc_run", "m4rm"])
     ap.add_argument("--cpu-rows", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

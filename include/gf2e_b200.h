@@ -45,6 +45,8 @@ extern "C" {
 #define GF2E_TC_INT8 4u      /* tensor-core K4 forced to kind::i8 at every k                */
 #define GF2E_TC_FP4 8u       /* tensor-core K4 forced to kind::mxf4 at every k (paired form
                                 below k = 2048)                                             */
+#define GF2E_TC_RUN 16u      /* tensor-core K4 forced to the kind::mxf4 running-sum form
+                                (double-buffered accumulators, 256 x 192 tiles) at every k  */
 
 /* Last error message of the calling thread ("" if none). */
 const char *gf2e_last_error(void);
@@ -220,10 +222,13 @@ int gf2e_scalar_mul(int e, uint32_t f, uint32_t c, const uint64_t *in_dev, int64
 
 /*
  * Instrumentation: number of kernels the last successful call on this thread launched,
- * and the name of the product kernel it used.
+ * the name of the product kernel it used, and the GF(2) plane products it launched (K(e)
+ * per fused product launch: the device-side counterpart of MulCounters.gf2_matmul_count,
+ * e.g. every Schur update and diagonal-block product of a TRSM / PLE call).
  */
 int gf2e_last_launch_count(void);
 const char *gf2e_last_product_kernel(void);
+int64_t gf2e_last_gf2_products(void);
 
 /*
  * Live kernel timing for bench.py: while enabled, every product-kernel launch is bracketed

@@ -20,6 +20,7 @@ BACKEND_TC = 0
 BACKEND_M4RM = 2
 TC_INT8 = 4
 TC_FP4 = 8
+TC_RUN = 16
 
 _I64 = ctypes.c_int64
 _U64 = ctypes.c_uint64
@@ -60,6 +61,7 @@ SIGNATURES = {
     "gf2e_scalar_mul": (_INT, [_INT, _U32, _U32, _P, _I64, _P, _I64, _I64, _I64, _P]),
     "gf2e_plane_mul": (_INT, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _U32, _P, _I64, _P]),
     "gf2e_last_launch_count": (_INT, []),
+    "gf2e_last_gf2_products": (_I64, []),
     "gf2e_last_product_kernel": (ctypes.c_char_p, []),
     "gf2e_profile_enable": (_INT, [_INT]),
     "gf2e_profile_read": (_INT, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_INT)]),
@@ -108,6 +110,11 @@ def call(name: str, *args) -> None:
 
 def last_launch_count() -> int:
     return int(load().gf2e_last_launch_count())
+
+
+def last_gf2_products() -> int:
+    """GF(2) plane products the last library call launched (K(e) per fused product launch)."""
+    return int(load().gf2e_last_gf2_products())
 
 
 def profile_enable(on: bool) -> None:

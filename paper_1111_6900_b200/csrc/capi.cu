@@ -23,6 +23,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+thread_local int64_t g_products = 0;  // GF(2) plane products launched by the last entry call
 thread_local const char *g_kernel = "";
 
 // live product-kernel timing (gf2e_profile_*)
@@ -314,19 +315,25 @@ int fp4_state() {
 int tc_form(uint32_t flags, int64_t k) {
     if (flags & GF2E_TC_INT8) return kFormI8;
     if (fp4_state() < 0) return kFormI8;  // the fp4 self-check failed on this device
+    if (flags & GF2E_TC_RUN) return kFormFp4Run;
     if (k >= kFp4LongK) return kFormFp4Long;
     if (k >= kFp4MinK) return kFormFp4;
     if (flags & GF2E_TC_FP4) return kFormFp4Pair;
     return kSmallKForm;
 }
-bool use_fp4(uint32_t flags, int64_t k) { return tc_form(flags, k) != kFormI8; }
 const char *form_name(int form) {
-    return form == kFormFp4Pair ? "k_product_tc2<fp4x2>"
+    return form == kFormFp4Pair                            ? "k_product_tc2<fp4x2>"
            : (form == kFormFp4 || form == kFormFp4Long) ? "k_product_tc2<fp4>"
-                                                        : "k_product_tc2<i8>";
+           : form == kFormFp4Run                          ? "k_product_run<fp4>"
+                                                          : "k_product_tc2<i8>";
 }
+// tile columns of a form (CTA-pair tile width; B^T is stage-tiled in half-width row blocks)
+int64_t form_bn(int form) { return form == kFormFp4Run ? kRunBN : kTcBN; }
+int form_br(int form) { return (int)(form_bn(form) / 2); }
 
-Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags, int fp4 = -1) {
+constexpr int kFormAny = -2;  // workspace bound over every tensor-core form
+
+Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags, int form = -1) {
     Layout L;
     if (flags & GF2E_BACKEND_M4RM) {
         L.m_pad = round_up(m, kM4BM);
@@ -336,9 +343,16 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags, in
         L.a_pstride = L.m_pad * L.kwords;
         L.b_pstride = L.k_pad * (L.n_pad / 64);
     } else {
+        if (form == -1) form = tc_form(flags, k);
         L.m_pad = round_up(m, 2 * kTcBM);  // CTA-pair tiles are 256 rows
-        L.n_pad = round_up(n, kTcBN);
-        L.k_pad = round_up(k, (fp4 < 0 ? use_fp4(flags, k) : fp4 != 0) ? kTcBKFp4 : kTcBK);
+        if (form == kFormAny) {
+            const int64_t a = round_up(n, kTcBN), b = round_up(n, kRunBN);
+            L.n_pad = a > b ? a : b;
+            L.k_pad = round_up(k, kTcBKFp4);
+        } else {
+            L.n_pad = round_up(n, form_bn(form));
+            L.k_pad = round_up(k, form == kFormI8 ? kTcBK : kTcBKFp4);
+        }
         L.kwords = L.k_pad / 64;
         L.a_pstride = L.m_pad * L.kwords;
         L.b_pstride = L.n_pad * L.kwords;
@@ -347,6 +361,10 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags, in
     L.b_bytes = align256((int64_t)nprod * L.b_pstride * 8);
     L.total = L.a_bytes + L.b_bytes;
     return L;
+}
+
+cudaError_t launch_form(const Sched &ks, const TcArgs &a, int form, cudaStream_t st) {
+    return form == kFormFp4Run ? launch_product_run(ks, a, st) : launch_product_tc2(ks, a, form, st);
 }
 
 // The shared launch sequence: K3 combos -> fused K4/K5 product.
@@ -369,7 +387,7 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
         if (int rc = ensure_fp4_checked()) return rc;
     const int form = form_override >= 0 ? form_override : tc_form(flags, k);
     const bool fp4 = tc && form != kFormI8;
-    Layout L = layout_for(ks.nprod, m, k, n, flags, fp4);
+    Layout L = layout_for(ks.nprod, m, k, n, flags, form);
     if (ws_bytes < L.total)
         return fail(GF2E_ENOMEM, "workspace too small: %lld < %lld bytes", (long long)ws_bytes, (long long)L.total);
     if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255))
@@ -388,13 +406,16 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
         M4rmArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, nwp, L.k_pad, m, n, L.m_pad, L.n_pad, C, ldc, pc};
         ProfScope prof(st);
         CK(launch_product_m4rm(ks, a, st), "product_m4rm");
+        g_products += ks.nprod;
         g_kernel = "k_product_m4rm";
     } else {
-        CK(launch_combos_bt(ks, B, ldb, pb, k, n, Bx, L.kwords, L.b_pstride, L.kwords, L.n_pad / 64, fp4, st),
+        CK(launch_combos_bt(ks, B, ldb, pb, k, n, Bx, L.kwords, L.b_pstride, L.kwords, L.n_pad / 64, fp4, st,
+                            form_br(form)),
            "combos(B^T)");
         TcArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, m, n, L.m_pad, L.n_pad, C, ldc, pc, acc ? 1 : 0};
         ProfScope prof(st);
-        CK(launch_product_tc2(ks, a, form, st), "product_tc2");
+        CK(launch_form(ks, a, form, st), "product");
+        g_products += ks.nprod;
         g_kernel = form_name(form);
     }
     return GF2E_OK;
@@ -431,7 +452,7 @@ int fp4_probe_run(bool inject, int *ok) {
     } sg{st};
     const Sched ks = plane_sched();
     const int64_t kmax = 33024, nw = n / 64;
-    const int64_t ws_bytes = layout_for(1, m, kmax, n, 0, 1).total;
+    const int64_t ws_bytes = layout_for(1, m, kmax, n, 0, kFormAny).total;
     DevTmpAny A((size_t)m * (kmax / 64) * 8, st), B((size_t)kmax * nw * 8, st), C8((size_t)m * nw * 8, st),
         C4((size_t)m * nw * 8, st), ws((size_t)ws_bytes, st);
     if (!A.p || !B.p || !C8.p || !C4.p || !ws.p) return fail(GF2E_ENOMEM, "out of device memory (fp4 self-check)");
@@ -474,9 +495,11 @@ int ensure_fp4_checked() {
         if (g_fp4_state[dev] != 0) return GF2E_OK;
     }
     const int launches = g_launches;
+    const int64_t products = g_products;
     int ok = 0;
     int rc = fp4_probe_run(g_fp4_inject, &ok);
     g_launches = launches;  // the check's launches are not the caller's
+    g_products = products;
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(g_fp4_mu);
     g_fp4_state[dev] = ok;
@@ -497,14 +520,14 @@ int pair_count() {
 // 72 of 74 at n = 16384), so the products that run while B is still arriving use the whole
 // GPU.  The rest go in `chunk`-row chunks, the remainder merged into the first of them (at
 // 16384 rows: 2304, 3840, 5 x 2048 — 97-99.8% wave fill each, against 86% for 1792 rows).
-std::vector<int64_t> host_row_plan(int64_t m, int64_t n, int64_t k, int64_t chunk, int nbp, bool fixed) {
+std::vector<int64_t> host_row_plan(int64_t m, int64_t n, int64_t k, int64_t chunk, int nbp, bool fixed, int64_t tw) {
     std::vector<int64_t> rb{0};
     int64_t first = chunk;
     // only where the products, not the copies, bound the pipeline (long k; at k = 256 the
     // C0/C copies dominate and uniform chunks pipeline them best)
     fixed = fixed || k < 4096;
     if (!fixed && nbp > 1) {
-        const int64_t part_tiles = ((n + 255) / 256 + nbp - 1) / nbp;
+        const int64_t part_tiles = ((n + tw - 1) / tw + nbp - 1) / nbp;
         const int64_t rt0 = pair_count() / part_tiles;
         if (rt0 >= 1) first = rt0 * 256;
     }
@@ -527,9 +550,9 @@ std::vector<int64_t> host_row_plan(int64_t m, int64_t n, int64_t k, int64_t chun
 
 // Column split of the host pipeline's last row chunk: the first part a whole number of waves
 // of CTA pairs (row tiles x column tiles a multiple of the pair count), about half of n.
-int64_t last_split_cols(int64_t rows, int64_t n) {
+int64_t last_split_cols(int64_t rows, int64_t n, int64_t tw) {
     if (n < 8192) return n;
-    const int64_t pairs = pair_count(), rt = (rows + 255) / 256, nt = (n + 255) / 256;
+    const int64_t pairs = pair_count(), rt = (rows + 255) / 256, nt = (n + tw - 1) / tw;
     int64_t g = pairs, b = rt;
     while (b) {
         const int64_t t = g % b;
@@ -538,7 +561,7 @@ int64_t last_split_cols(int64_t rows, int64_t n) {
     }
     const int64_t q = pairs / g;  // column tiles per whole wave step
     const int64_t ct = (nt / 2 + q - 1) / q * q;
-    return ct > 0 && ct < nt ? ct * 256 : n;
+    return ct > 0 && ct < nt ? ct * tw : n;
 }
 
 // GF2E_E2E_TRACE=1: per-stage completion times of the host-buffer pipeline on stderr
@@ -636,7 +659,7 @@ TrsmLayout trsm_layout(int nprod, int e, int64_t m, int64_t n) {
     T.nblk = (m + tb - 1) / tb;
     T.inv_bytes = align256(T.nblk * e * tb * (tb / 64) * 8);
     T.tmp_bytes = align256((int64_t)e * tb * words_for(n) * 8);
-    T.mul_bytes = layout_for(nprod, m, m, n, 0).total;  // bounds every update and block product
+    T.mul_bytes = layout_for(nprod, m, m, n, 0, kFormAny).total;  // bounds every update and block product
     T.total = T.inv_bytes + T.tmp_bytes + 256 + T.mul_bytes;
     return T;
 }
@@ -688,9 +711,10 @@ int trsm_rec(TrsmCtx &c, int64_t i0, int64_t i1) {
 }
 
 int check_flags(uint32_t flags) {
-    if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM | GF2E_TC_INT8 | GF2E_TC_FP4))
+    if (flags & ~(GF2E_ACCUMULATE | GF2E_BACKEND_M4RM | GF2E_TC_INT8 | GF2E_TC_FP4 | GF2E_TC_RUN))
         return fail(GF2E_EINVAL, "unknown flags 0x%x", flags);
-    if ((flags & GF2E_TC_INT8) && (flags & GF2E_TC_FP4)) return fail(GF2E_EINVAL, "conflicting flags 0x%x", flags);
+    const uint32_t forced = flags & (GF2E_TC_INT8 | GF2E_TC_FP4 | GF2E_TC_RUN);
+    if (forced & (forced - 1)) return fail(GF2E_EINVAL, "conflicting flags 0x%x", flags);
     return GF2E_OK;
 }
 
@@ -908,6 +932,7 @@ extern "C" {
 const char *gf2e_last_error(void) { return g_err.c_str(); }
 const char *gf2e_version(void) { return "gf2e_b200 0.2 (sm_100a; tcgen05 cta_group::2 kind::mxf4 + kind::i8, M4RM)"; }
 int gf2e_last_launch_count(void) { return g_launches; }
+int64_t gf2e_last_gf2_products(void) { return g_products; }
 const char *gf2e_last_product_kernel(void) { return g_kernel; }
 
 int gf2e_profile_enable(int on) {
@@ -1028,6 +1053,7 @@ int gf2e_random_packed(int e, int64_t rows, int64_t cols, uint64_t seed, int64_t
                        uint64_t *out, int64_t ldp, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     int w = gf2e_pack_width(e);
     if (w < 0) return fail(GF2E_EINVAL, "extension degree must be in 2..10, got %d", e);
     if (int rc = check_mat(out, rows, words_for(cols * w), ldp, "packed")) return rc;
@@ -1042,6 +1068,7 @@ int gf2e_random_sliced(int e, int64_t rows, int64_t cols, uint64_t seed, int64_t
                        uint64_t *planes, int64_t ld, int64_t pstride, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (e < 2 || e > 10) return fail(GF2E_EINVAL, "extension degree must be in 2..10, got %d", e);
     if (int rc = check_mat(planes, rows, words_for(cols), ld, "planes")) return rc;
     if (rows == 0 || ld == 0) return GF2E_OK;
@@ -1054,6 +1081,7 @@ int gf2e_random_sliced(int e, int64_t rows, int64_t cols, uint64_t seed, int64_t
 int gf2e_random_words(int64_t rows, int64_t ncols, uint64_t seed, uint64_t *out, int64_t ld, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (int rc = check_mat(out, rows, words_for(ncols), ld, "words")) return rc;
     if (rows == 0 || ncols == 0) return GF2E_OK;
     if (int rc = check_device()) return rc;
@@ -1065,6 +1093,7 @@ int gf2e_slice(int e, int64_t rows, int64_t cols, const uint64_t *packed, int64_
                int64_t pstride, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     int w = gf2e_pack_width(e);
     if (w < 0) return fail(GF2E_EINVAL, "extension degree must be in 2..10, got %d", e);
     if (int rc = check_mat(packed, rows, words_for(cols * w), ldp, "packed")) return rc;
@@ -1079,6 +1108,7 @@ int gf2e_cling(int e, int64_t rows, int64_t cols, const uint64_t *planes, int64_
                uint64_t *packed, int64_t ldp, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     int w = gf2e_pack_width(e);
     if (w < 0) return fail(GF2E_EINVAL, "extension degree must be in 2..10, got %d", e);
     if (int rc = check_mat(packed, rows, words_for(cols * w), ldp, "packed")) return rc;
@@ -1092,6 +1122,7 @@ int gf2e_cling(int e, int64_t rows, int64_t cols, const uint64_t *planes, int64_
 int gf2e_xor(uint64_t *x, int64_t ldx, const uint64_t *y, int64_t ldy, int64_t rows, int64_t nwords, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (int rc = check_mat(x, rows, nwords, ldx, "x")) return rc;
     if (int rc = check_mat(y, rows, nwords, ldy, "y")) return rc;
     if (rows == 0 || nwords == 0) return GF2E_OK;
@@ -1104,6 +1135,7 @@ int gf2e_reduce_mod_f(int e, uint32_t f, uint64_t *planes, int64_t rows, int64_t
                       void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (int rc = check_field(e, f)) return rc;
     if (int rc = check_mat(planes, rows, nwords, ld, "planes")) return rc;
     if (rows == 0 || nwords == 0) return GF2E_OK;
@@ -1118,7 +1150,9 @@ int64_t gf2e_slice_mul_workspace(int e, uint32_t f, int64_t m, int64_t k, int64_
     if (m < 0 || k < 0 || n < 0) return fail(GF2E_EINVAL, "matrix dimensions must be non-negative"), -1;
     if (m == 0 || k == 0 || n == 0) return 0;
     const Schedule &S = get_schedule(e, f);
-    return layout_for((int)S.subsets.size(), m, k, n, flags).total;
+    // a bound over the tensor-core forms: the form is picked at call time (it can change when
+    // the fp4 self-check disables fp4 between this query and the product)
+    return layout_for((int)S.subsets.size(), m, k, n, flags, kFormAny).total;
 }
 
 int64_t gf2e_plane_mul_workspace(int64_t m, int64_t k, int64_t n, uint32_t flags) {
@@ -1126,7 +1160,7 @@ int64_t gf2e_plane_mul_workspace(int64_t m, int64_t k, int64_t n, uint32_t flags
     if (check_flags(flags)) return -1;
     if (m < 0 || k < 0 || n < 0) return fail(GF2E_EINVAL, "matrix dimensions must be non-negative"), -1;
     if (m == 0 || k == 0 || n == 0) return 0;
-    return layout_for(1, m, k, n, flags).total;
+    return layout_for(1, m, k, n, flags, kFormAny).total;
 }
 
 int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa, const uint64_t *B, int64_t ldb,
@@ -1134,6 +1168,7 @@ int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa
                    void *ws, int64_t ws_bytes, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (int rc = check_field(e, f)) return rc;
     if (int rc = check_flags(flags)) return rc;
     if (int rc = check_mat(A, m, words_for(k), lda, "A")) return rc;
@@ -1150,6 +1185,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
                        int64_t chunk_rows, double *device_ms) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (device_ms) *device_ms = 0;
     if (int rc = check_field(e, f)) return rc;
     if (flags & ~GF2E_ACCUMULATE) return fail(GF2E_EINVAL, "gf2e_mzed_mul_host: unsupported flags 0x%x", flags);
@@ -1168,6 +1204,8 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     if (int rc = check_device()) return rc;
     if (int rc = ensure_fp4_checked()) return rc;
     Sched ks = to_kernel_sched(e, get_schedule(e, f));
+    const int form = tc_form(0, k);
+    const int64_t tw = form_bn(form);  // column tile width: B parts and column splits align to it
     int64_t chunk = chunk_rows > 0 ? round_up(chunk_rows, 2 * kTcBM) : 2048;
     if (chunk > round_up(m, 2 * kTcBM)) chunk = round_up(m, 2 * kTcBM);
     constexpr int kMaxBParts = 8;
@@ -1178,7 +1216,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     // start after the first part's upload instead of all of B's
     const int nbp = (n >= 8192 && m > chunk) ? GF2E_BPARTS : 1;
     static_assert(GF2E_BPARTS >= 1 && GF2E_BPARTS <= kMaxBParts, "B parts");
-    const std::vector<int64_t> rb = host_row_plan(m, n, k, chunk, nbp, chunk_rows > 0);
+    const std::vector<int64_t> rb = host_row_plan(m, n, k, chunk, nbp, chunk_rows > 0, tw);
     for (size_t i = 1; i < rb.size(); ++i)
         if (rb[i] - rb[i - 1] > chunk) chunk = rb[i] - rb[i - 1];  // slot size
     const int64_t nchunks = (int64_t)rb.size() - 1;
@@ -1192,7 +1230,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     CKH(cudaStreamCreateWithFlags(&P.sh, cudaStreamNonBlocking), "stream");
     CKH(cudaStreamCreateWithFlags(&P.sd, cudaStreamNonBlocking), "stream");
     CKH(cudaStreamCreateWithFlags(&P.sp, cudaStreamNonBlocking), "stream");
-    Layout LB = layout_for(ks.nprod, chunk, k, n, 0);  // Ac sized for one chunk, Bt for all of B
+    Layout LB = layout_for(ks.nprod, chunk, k, n, 0, form);  // Ac sized for one chunk, Bt for all of B
     uint64_t *dBp, *dBs, *dBt, *dAc[2], *dAp[2], *dAs[2], *dCs[2], *dCp[2];
     CKH(P.alloc(&dBp, k * wb * 8), "pool_alloc");
     CKH(P.alloc(&dBs, (int64_t)e * k * nwn * 8), "pool_alloc");
@@ -1205,7 +1243,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         CKH(P.alloc(&dCp[sl], chunk * wb * 8), "pool_alloc");
     }
     int64_t cb[kMaxBParts + 1];
-    for (int p = 0; p <= nbp; ++p) cb[p] = p == nbp ? n : round_up(n * p / nbp, 2 * kTcBM);
+    for (int p = 0; p <= nbp; ++p) cb[p] = p == nbp ? n : round_up(n * p / nbp, tw);
     // events: copies in (A chunk / B part), preparation done, products done (frees that
     // slot's A combinations), cling done, copy out done
     cudaEvent_t part_out, ev_alloc, ev_t0, ev_t1, in_ready[2], prep_a[2], prod_done[2], out_ready[2], d2h_done[2],
@@ -1260,7 +1298,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         tr.mark(P.sh, "h2d A", i);
         return GF2E_OK;
     };
-    const bool fp4 = use_fp4(0, k);
+    const bool fp4 = form != kFormI8;
     // Preparation runs on its own stream, one chunk ahead, where the products bound the
     // pipeline (k >= 4096); at short k the copies do, and preparing in line on sc pipelines
     // them with the fewest cross-stream dependencies.
@@ -1274,7 +1312,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         CKH(cudaStreamWaitEvent(sp, in_ready[sl], 0), "cudaStreamWaitEvent");
         if (i >= nslots) CKH(cudaStreamWaitEvent(sp, prod_done[sl], 0), "cudaStreamWaitEvent");
         CK(launch_slice(e, w, rows, k, dAp[sl], wa, dAs[sl], nwk, rows * nwk, sp), "slice(A)");
-        Layout L = layout_for(ks.nprod, rows, k, n, 0);
+        Layout L = layout_for(ks.nprod, rows, k, n, 0, form);
         CK(launch_combos_rows(ks, dAs[sl], nwk, rows * nwk, rows, k, dAc[sl], L.kwords, L.a_pstride, L.m_pad,
                               L.kwords, fp4 ? 4 : 2, sp),
            "combos(A)");
@@ -1290,7 +1328,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         CK(launch_slice(e, w, k, nc, dBp + c0 * w / 64, wb, dBs + c0 / 64, nwn, k * nwn, sp, words_for(nc)),
            "slice(B)");
         CK(launch_combos_bt(ks, dBs + c0 / 64, nwn, k * nwn, k, nc, dBt + c0 * LB.kwords, LB.kwords, LB.b_pstride,
-                            LB.kwords, npad / 64, fp4, sp),
+                            LB.kwords, npad / 64, fp4, sp, form_br(form)),
            "combos(B^T)");
         CKH(cudaEventRecord(prep_b[p], sp), "cudaEventRecord");
         tr.mark(sp, "prep B", p);
@@ -1321,12 +1359,12 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
             CKH(cudaStreamWaitEvent(P.sc, in_ready[sl], 0), "cudaStreamWaitEvent");
             CK(launch_slice(e, w, rows, n, dCp[sl], wb, dCs[sl], nwn, rows * nwn, P.sc), "slice(C0)");
         }
-        Layout L = layout_for(ks.nprod, rows, k, n, 0);
+        Layout L = layout_for(ks.nprod, rows, k, n, 0, form);
         // the first chunk runs one product per B part as the parts arrive; later chunks see all of
         // B.  The last chunk runs as two column parts, the first sized to whole waves of CTA
         // pairs, so its cling and copy-out overlap the second part's product.
         const bool last = i + 1 == nchunks && i > 0;
-        const int64_t cs = last && side ? last_split_cols(rows, n) : n;
+        const int64_t cs = last && side ? last_split_cols(rows, n, tw) : n;
         const int nprods = i == 0 ? nbp : (cs < n ? 2 : 1);
         for (int p = 0; p < nprods; ++p) {
             const int64_t c0 = i == 0 ? cb[p] : (p ? cs : 0), c1 = i == 0 ? cb[p + 1] : (p || cs == n ? n : cs);
@@ -1337,7 +1375,8 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
             TcArgs ta{dAc[sl], dBt + c0 * LB.kwords, L.a_pstride, LB.b_pstride, L.kwords, rows, c1 - c0, L.m_pad, npad,
                       dCs[sl] + c0 / 64, nwn, rows * nwn, acc ? 1 : 0};
             ProfScope prof(P.sc);
-            CK(launch_product_tc2(ks, ta, tc_form(0, k), P.sc), "product_tc2");
+            CK(launch_form(ks, ta, form, P.sc), "product");
+            g_products += ks.nprod;
             tr.mark(P.sc, "product", i, p);
             if (last && p == 0 && cs < n) {  // first column part out while the second computes
                 const int64_t cw = cs * w / 64;
@@ -1368,7 +1407,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     float ms = 0;
     CKH(cudaEventElapsedTime(&ms, ev_t0, ev_t1), "cudaEventElapsedTime");
     if (device_ms) *device_ms = ms;
-    g_kernel = form_name(tc_form(0, k));
+    g_kernel = form_name(form);
     return GF2E_OK;
 }
 
@@ -1393,6 +1432,7 @@ int trsm_impl(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, in
               int64_t *bad_row, bool check) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (bad_row) *bad_row = -1;
     if (int rc = check_field(e, f)) return rc;
     if (unit_diag && upper) return fail(GF2E_EINVAL, "unit_diag is only defined for lower triangular solves");
@@ -1438,6 +1478,7 @@ int gf2e_mul_by_x(int e, uint32_t f, const uint64_t *in, int64_t ld, int64_t pin
                   int64_t rows, int64_t cols, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (int rc = check_field(e, f)) return rc;
     if (int rc = check_mat(in, rows, words_for(cols), ld, "in")) return rc;
     if (int rc = check_mat(out, rows, words_for(cols), ld, "out")) return rc;
@@ -1451,6 +1492,7 @@ int gf2e_scalar_mul(int e, uint32_t f, uint32_t c, const uint64_t *in, int64_t l
                     int64_t rows, int64_t cols, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (int rc = check_field(e, f)) return rc;
     if (c >= (1u << e)) return fail(GF2E_EINVAL, "scalar %u out of range for GF(2^%d)", c, e);
     const int w = gf2e_pack_width(e);
@@ -1467,6 +1509,7 @@ int gf2e_plane_mul(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ld
                    int64_t k, int64_t n, uint32_t flags, void *ws, int64_t ws_bytes, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (int rc = check_flags(flags)) return rc;
     if (int rc = check_mat(A, m, words_for(k), lda, "A")) return rc;
     if (int rc = check_mat(B, k, words_for(n), ldb, "B")) return rc;
@@ -1482,6 +1525,7 @@ int gf2e_ple(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, 
              int64_t *rank, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (rank) *rank = 0;
     if (int rc = check_field(e, f)) return rc;
     if (int rc = check_mat(S, m, words_for(n), ld, "A")) return rc;
@@ -1494,6 +1538,7 @@ int gf2e_echelonize(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int6
                     int64_t *rank, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (rank) *rank = 0;
     if (int rc = check_field(e, f)) return rc;
     if (int rc = check_mat(S, m, words_for(n), ld, "A")) return rc;
@@ -1539,6 +1584,7 @@ int gf2e_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t rows
                    const int64_t *swaps, int64_t n, int backward, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (planes < 1 || n < 0 || n > rows) return fail(GF2E_EINVAL, "bad swap vector arguments");
     if (int rc = check_mat(S, rows, nwords, ld, "A")) return rc;
     for (int64_t i = 0; i < n; ++i)
@@ -1563,6 +1609,7 @@ int gf2e_col_swaps(int planes, int w, uint64_t *S, int64_t ld, int64_t ps, int64
                    const int64_t *triples, int64_t n, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (planes < 1 || n < 0 || (w != 1 && w != 2 && w != 4 && w != 8 && w != 16))
         return fail(GF2E_EINVAL, "bad column swap arguments");
     if (int rc = check_mat(S, rows, words_for(cols * w), ld, "A")) return rc;
@@ -1586,6 +1633,7 @@ int gf2e_row_scales(int e, uint32_t f, const uint64_t *in, int64_t ldi, int broa
                     uint64_t *out, int64_t ldo, int64_t rows, int64_t cols, void *stream) {
     g_err.clear();
     g_launches = 0;
+    g_products = 0;
     if (int rc = check_field(e, f)) return rc;
     const int w = gf2e_pack_width(e);
     const int64_t nwords = words_for(cols * w);

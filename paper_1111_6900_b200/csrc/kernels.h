@@ -30,9 +30,12 @@ cudaError_t launch_reduce(int e, uint32_t f, uint64_t *planes, int64_t rows, int
 // Inside one 128-row x kw-word stage tile the words are stored as kw/2 slabs of [128 rows][2
 // words], so the expander's per-row 16-byte shared-memory reads are consecutive across a warp
 // (a [row][kw] layout makes the kw = 4 reads two-way bank-conflicted).
-__host__ __device__ __forceinline__ int64_t tc_tile_word(int64_t r, int64_t w, int64_t kwords, int kw) {
+// br: rows per tile (128; 96 for the B^T operand of the running-sum form, whose CTA pairs
+// cover 192 columns)
+__host__ __device__ __forceinline__ int64_t tc_tile_word(int64_t r, int64_t w, int64_t kwords, int kw,
+                                                         int br = 128) {
     const int64_t wk = w % kw;
-    return (((r >> 7) * (kwords / kw) + (w / kw)) * 128) * kw + (wk >> 1) * 256 + (r & 127) * 2 + (wk & 1);
+    return (((r / br) * (kwords / kw) + (w / kw)) * br) * kw + (wk >> 1) * (2 * br) + (r % br) * 2 + (wk & 1);
 }
 // Row order inside each 32-row group of B^T tiles: tile row j holds column b_row_perm(j)
 // (tc_common.cuh), i.e. column o sits at tile row 4*(o%8) + o/8.
@@ -48,7 +51,7 @@ cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, i
 // KW = 2 and bits reversed inside every byte
 cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int64_t pb, int64_t k, int64_t n,
                              uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks, bool fp4,
-                             cudaStream_t st);
+                             cudaStream_t st, int br = 128);
 
 // Tensor-core product.  Operands: Ac [nprod] x (m_pad x k_pad bits) natural bit order,
 // Bt [nprod] x (n_pad x k_pad bits) = B^T with bits reversed in each byte.
@@ -73,6 +76,11 @@ constexpr int kTcBKFp4 = 256;
 // tensor-core forms of the product kernel: int8; fp4 (k chunks <= 32768); fp4 with two
 // products per accumulator (k < 2048 only)
 constexpr int kFormI8 = 0, kFormFp4 = 1, kFormFp4Pair = 2, kFormFp4Long = 3;  // Long: k >= 8192
+// fp4 running-sum form (product_run.cu): double-buffered accumulators, no per-product
+// re-initialisation; tiles 256 x kRunBN, B^T stage-tiled in kRunBN/2-row blocks
+constexpr int kFormFp4Run = 4;
+constexpr int kRunBN = 192;
+cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st);
 constexpr int64_t kFp4PairMaxK = 2047;
 cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, int form, cudaStream_t st);
 

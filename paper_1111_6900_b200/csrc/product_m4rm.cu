@@ -65,8 +65,10 @@ __global__ void __launch_bounds__(NT, 1) k_product_m4rm(const Sched s, const M4r
                 T[(16 * bg) * 32 + bw] = cur;
 #pragma unroll
                 for (int x = 1; x < 16; ++x) {
-                    const int gcode = x ^ (x >> 1), prev = (x - 1) ^ ((x - 1) >> 1);
-                    const int bit = __ffs(gcode ^ prev) - 1;
+                    const int gcode = x ^ (x >> 1);
+                    // the bit that flips between gray(x-1) and gray(x) is ctz(x); written so it
+                    // folds to a constant after unrolling (a runtime index sent r[] to local memory)
+                    const int bit = (x & 1) ? 0 : (x & 2) ? 1 : (x & 4) ? 2 : 3;
                     cur ^= r[bit];
                     T[(16 * bg + gcode) * 32 + bw] = cur;
                 }

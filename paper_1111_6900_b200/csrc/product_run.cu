@@ -1,0 +1,431 @@
+// product_run.cu — the short-k tensor-core form of the fused Karatsuba product (k < 2048: the
+// config-4 addmul 65536x256x65536, the TRSM / PLE Schur updates ple_echelon.py:130-136,259).
+//
+// Same GF(2) encoding as the fp4 forms of product_tc2.cu (kind::mxf4 block-scaled e2m1, all
+// scale factors 1.0: A nibbles 0.5/1/2/1, B^T nibbles 2/1/0.5/1, every product of aligned bits
+// exactly 1.0), but short accumulations make the per-product TMEM traffic, not the MMA, the
+// bound.  Measured (tools/tmem_bench.cu, profiles/r02): tcgen05.ld reaches ~100 cells/clk/SM
+// alone and ~50 while MMAs run; tcgen05.st ~40-58 cells/clk.  The fp4 forms re-initialise the
+// accumulator after every drain (one tcgen05.st per cell per product) and have a single
+// accumulator; this form removes both:
+//
+//  * running sums.  Each accumulator starts at 2^23 (fp32 ulp 1) once per tile and is never
+//    re-initialised between products: after product t it holds 2^23 + S_t, S_t = the sum of
+//    the counts of the products accumulated into it so far (exact while S_t < 2^23: at most
+//    ceil(K/2) * k < 2^23).  parity(count_t) = bit0(S_t) ^ bit0(S_{t-2}), so the epilogue
+//    keeps the previous parity word of each buffer and XORs.  No tcgen05.st per product.
+//  * double buffering.  Two accumulators of N = 192 columns (products alternate between
+//    them), so the drain of product t overlaps the MMAs of product t+1.  TMEM: accumulators
+//    0-191 and 192-383, three A stages 384-479 (the expanded A operand lives in TMEM, as in
+//    the long-k fp4 form), scale factors 480-511.  N = 192 (not 256) is what makes both
+//    accumulators, the A stages and the scale factors fit in 512 columns.
+//
+// Tiles are 256 x 192 (CTA pair, cta_group::2, M = 256, N = 192); B^T is stage-tiled in
+// 96-row blocks (tc_tile_word br = 96).  Output words are written 32 bits at a time (a tile
+// covers 6 words of 32 columns).  Warp roles as in product_tc2.cu: 4 expander warps (A rows
+// into TMEM, B^T rows into shared memory), 8 epilogue warps (lane quarter x column half),
+// MMA issuer (leader CTA), bulk loader.
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace gf2e {
+namespace {
+using namespace tc;
+
+constexpr int BM = 128;               // A rows per CTA (tile = 2 x BM)
+constexpr int BN = kRunBN;            // tile columns
+constexpr int BNH = BN / 2;           // B^T rows per CTA
+constexpr int KW = 4;                 // 64-bit words per row per stage (256 k-bits)
+constexpr int S = 3;                  // operand stages (A: 3 x 32 TMEM columns)
+constexpr int D = 8;                  // raw bit-tile ring
+constexpr int NEXP = 4, NEPI = 8;
+constexpr int EPI_W0 = NEXP, MMA_WARP = NEXP + NEPI, LOAD_WARP = MMA_WARP + 1;
+constexpr int NTHREADS = (NEXP + NEPI + 2) * 32;
+constexpr int B_BYTES = BNH * 128;                     // expanded B^T stage (12 KiB)
+constexpr int BITS_A = BM * KW * 8, BITS_B = BNH * KW * 8, BITS_BYTES = BITS_A + BITS_B;
+constexpr uint32_t ACC1 = BN;  // TMEM column of the second accumulator (the first starts at 0)
+constexpr uint32_t ATM0 = 2 * BN, SFA = 480, SFB = 496;
+static_assert(ATM0 + 32 * S <= SFA, "TMEM: A stages overlap the scale factors");
+constexpr uint32_t RUN_INIT = 0x4B000000u;             // 2^23
+constexpr uint32_t SF_ONE = 0x7F7F7F7Fu;               // E8M0 1.0
+constexpr int CH = BN / 2 / 32;                        // 32-column chunks per epilogue thread
+constexpr int GROUP_M = 8;
+constexpr int BARS_BYTES = 1024;
+constexpr int SMEM_BYTES = S * B_BYTES + D * BITS_BYTES + BARS_BYTES + 1024;
+static_assert(B_BYTES % 1024 == 0, "swizzle atoms need 1024-byte aligned stages");
+static_assert(SMEM_BYTES <= 232448, "shared memory");
+
+struct __align__(8) Bars {
+    uint64_t full[S], empty[S], tfull[2], tempty[2], bfull[D], bempty[D];
+    uint32_t tmem_base;
+    uint16_t outmask[kMaxProducts];
+};
+static_assert(sizeof(Bars) <= BARS_BYTES, "barrier block");
+
+__device__ __forceinline__ void tile_coords(int64_t tile, int64_t tiles_m, int64_t tiles_n, int64_t &tm,
+                                            int64_t &tn) {
+    const int64_t per_group = (int64_t)GROUP_M * tiles_n;
+    const int64_t g = tile / per_group, r = tile - g * per_group;
+    const int64_t first = g * GROUP_M;
+    const int64_t gsize = tiles_m - first < GROUP_M ? tiles_m - first : GROUP_M;
+    tm = first + r % gsize;
+    tn = r / gsize;
+}
+
+__device__ __forceinline__ void st32_const(uint32_t taddr, uint32_t v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+            taddr),
+        "r"(v)
+        : "memory");
+}
+__device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// A row of one stage into this thread's TMEM lane: 32 columns, word i of chunk q = nibble
+// plane i of 32-bit word q (k-bit 32q + 4j + i <-> nibble j)
+__device__ __forceinline__ void expand_a_tmem(uint32_t taddr, uint4 lo, uint4 hi) {
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    uint32_t o[32];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t x = w[q];
+        o[4 * q] = x & 0x11111111u;
+        o[4 * q + 1] = x & 0x22222222u;
+        o[4 * q + 2] = x & 0x44444444u;
+        o[4 * q + 3] = (x >> 2) & 0x22222222u;
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%"
+        "29,%30,%31,%32};" ::"r"(taddr),
+        "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]), "r"(o[9]),
+        "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]), "r"(o[16]), "r"(o[17]), "r"(o[18]),
+        "r"(o[19]), "r"(o[20]), "r"(o[21]), "r"(o[22]), "r"(o[23]), "r"(o[24]), "r"(o[25]), "r"(o[26]), "r"(o[27]),
+        "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31])
+        : "memory");
+}
+
+// B^T row (bits 0 and 2 of every nibble pre-swapped by k_combos_bt) into its swizzle row
+__device__ __forceinline__ void expand_b_smem(uint8_t *tile, int r, uint4 lo, uint4 hi) {
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t x = w[q];
+        *reinterpret_cast<uint4 *>(tile + swz(r, q)) =
+            make_uint4(x & 0x44444444u, x & 0x22222222u, x & 0x11111111u, (x >> 2) & 0x22222222u);
+    }
+}
+
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+    return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma2_mxf4_ts(uint32_t d, uint32_t at, uint64_t bd, uint32_t idesc, uint32_t sfa,
+                                             uint32_t sfb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.eq.u32 p, 1, 1;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%4], [%5], p;\n\t}" ::"r"(d),
+        "r"(at), "l"(bd), "r"(idesc), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+
+template <int E>
+__global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, const TcArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t *stages = smem;
+    uint8_t *bits = smem + S * B_BYTES;
+    Bars *bars = reinterpret_cast<Bars *>(bits + D * BITS_BYTES);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+    const int64_t tiles_n = a.n_pad / BN;
+    const int64_t tiles_m = a.m_pad / (2 * BM);
+    const int64_t ntiles = tiles_m * tiles_n;
+    const int64_t my_tiles = ntiles > cluster ? (ntiles - cluster + nclusters - 1) / nclusters : 0;
+    const int nks = (int)(a.kwords / KW);
+    const int64_t total = my_tiles * (int64_t)s.nprod * nks;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&bars->full[i], 2 * NEXP);
+            mbar_init(&bars->empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->tfull[i], 1);
+            mbar_init(&bars->tempty[i], 2 * NEPI);
+        }
+        for (int i = 0; i < D; ++i) {
+            mbar_init(&bars->bfull[i], 1);
+            mbar_init(&bars->bempty[i], NEXP);
+        }
+        mbar_fence_init();
+    }
+    if (threadIdx.x < kMaxProducts) bars->outmask[threadIdx.x] = s.outmask[threadIdx.x];
+    if (warp == MMA_WARP) tmem_alloc2(&bars->tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+    if (warp >= EPI_W0 && warp < EPI_W0 + 4) {
+        // scale factors (every byte E8M0 1.0) and both running-sum accumulators at 2^23
+        const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+        st32_const(tmem + lb + SFA, SF_ONE);
+        for (int c = 0; c < 2 * BN; c += 32) st32_const(tmem + lb + c, RUN_INIT);
+        wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+
+    if (warp < NEXP) {
+        // ===================== expanders =====================
+        const int p = threadIdx.x;  // A row p; B^T row p (p < BNH)
+        const bool doB = p < BNH;
+        const uint32_t full_leader = mapa(smem_u32(&bars->full[0]), 0);
+        const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16) + ATM0;
+        int slot = 0, st = 0;
+        uint32_t bph = 0, phase = 0;
+        uint4 cur[4];
+        auto load_bits = [&](int sl) {
+            const uint8_t *bs = bits + sl * BITS_BYTES + p * 16;
+            cur[0] = *reinterpret_cast<const uint4 *>(bs);
+            cur[1] = *reinterpret_cast<const uint4 *>(bs + BM * 16);
+            if (doB) {
+                cur[2] = *reinterpret_cast<const uint4 *>(bs + BITS_A);
+                cur[3] = *reinterpret_cast<const uint4 *>(bs + BITS_A + BNH * 16);
+            }
+        };
+        if (total > 0) {
+            mbar_wait(&bars->bfull[0], 0);
+            load_bits(0);
+        }
+        for (int64_t it = 0; it < total; ++it) {
+            mbar_wait_sleep(&bars->empty[st], phase ^ 1, 32);
+            expand_a_tmem(tl + (uint32_t)(st * 32), cur[0], cur[1]);
+            if (doB) expand_b_smem(stages + st * B_BYTES, p, cur[2], cur[3]);
+            wait_st();
+            tc_fence_before();
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive_cluster(full_leader + (uint32_t)(st * 8));
+                mbar_arrive(&bars->bempty[slot]);
+            }
+            if (++slot == D) {
+                slot = 0;
+                bph ^= 1;
+            }
+            if (it + 1 < total) {
+                mbar_wait(&bars->bfull[slot], bph);
+                load_bits(slot);
+            }
+            if (++st == S) {
+                st = 0;
+                phase ^= 1;
+            }
+        }
+    } else if (warp == LOAD_WARP) {
+        // ===================== bit-tile loader =====================
+        const bool issuer = elect_one();
+        const int64_t KS = a.kwords / KW;
+        const int64_t tw_a = BM * KW, tw_b = BNH * KW;
+        const uint32_t bits_s = smem_u32(bits);
+        int slot = 0;
+        uint32_t bph = 0;
+        for (int64_t ti = 0; ti < my_tiles; ++ti) {
+            const int64_t tile = cluster + ti * nclusters;
+            int64_t tm, tn;
+            tile_coords(tile, tiles_m, tiles_n, tm, tn);
+            const int64_t rbA = tm * 2 + rank, rbB = tn * 2 + rank;
+            for (int t = 0; t < s.nprod; ++t) {
+                const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * tw_a;
+                const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * tw_b;
+                for (int ks = 0; ks < nks; ++ks) {
+                    mbar_wait_sleep(&bars->bempty[slot], bph ^ 1, 64);
+                    const uint32_t dst = bits_s + (uint32_t)(slot * BITS_BYTES);
+                    if (issuer) {
+                        mbar_arrive_expect_tx(&bars->bfull[slot], BITS_BYTES);
+                        bulk_g2s(dst, Ab + ks * tw_a, BITS_A, &bars->bfull[slot]);
+                        bulk_g2s(dst + BITS_A, Bb + ks * tw_b, BITS_B, &bars->bfull[slot]);
+                    }
+                    __syncwarp();
+                    if (++slot == D) {
+                        slot = 0;
+                        bph ^= 1;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp < MMA_WARP) {
+        // ===================== epilogue =====================
+        const int ew = warp - EPI_W0;
+        const int q = warp & 3;  // TMEM lane quarter
+        const int h = ew >> 2;   // column half: tile columns [h*96, h*96+96)
+        const int row_local = (int)rank * BM + q * 32 + lane;
+        const int64_t nw32 = (a.n + 31) >> 5;
+        const uint32_t tempty_leader = mapa(smem_u32(&bars->tempty[0]), 0);
+        const uint32_t lq = (uint32_t)(q * 32) << 16;
+        uint32_t pc[CH], po[CH];  // previous parity words: current buffer / the other buffer
+#pragma unroll
+        for (int c = 0; c < CH; ++c) pc[c] = po[c] = 0;
+        int64_t gp = 0;
+        for (int64_t ti = 0; ti < my_tiles; ++ti) {
+            const int64_t tile = cluster + ti * nclusters;
+            int64_t tm, tn;
+            tile_coords(tile, tiles_m, tiles_n, tm, tn);
+            uint32_t acc[E][CH];
+#pragma unroll
+            for (int j = 0; j < E; ++j)
+#pragma unroll
+                for (int c = 0; c < CH; ++c) acc[j][c] = 0;
+            for (int t = 0; t < s.nprod; ++t, ++gp) {
+                const int b = (int)(gp & 1);
+                const uint32_t mask = bars->outmask[t];
+                mbar_wait(&bars->tfull[b], (uint32_t)((gp >> 1) & 1));
+                tc_fence_after();
+                const uint32_t ta = tmem + lq + (b ? ACC1 : 0u) + (uint32_t)(h * (BN / 2));
+                const bool last = t + 2 >= s.nprod;  // this buffer's last product in the tile
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    uint32_t v[16];
+                    tmem_ld32_pack16(ta + (uint32_t)(c * 32), v);
+                    tmem_wait_ld();
+                    if (last) st32_const(ta + (uint32_t)(c * 32), RUN_INIT);
+                    // bit 0 of each cell = parity of the running sum; shifted to bit 7 of a byte
+                    const uint32_t w = parity_word_packed_shl<7, 0xECA8>(v);
+                    const uint32_t pw = w ^ pc[c];
+                    pc[c] = po[c];
+                    po[c] = last ? 0u : w;
+#pragma unroll
+                    for (int j = 0; j < E; ++j) acc[j][c] ^= pw & (0u - ((mask >> j) & 1u));
+                }
+                if (last) wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(b * 8));
+            }
+            const int64_t row = tm * (2 * BM) + row_local;
+            if (row < a.m) {
+                const int64_t w0 = tn * (BN / 32) + h * CH;  // first 32-bit word of this thread
+                uint32_t old[E][CH];
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const uint32_t *crow =
+                        reinterpret_cast<const uint32_t *>(a.C + j * a.c_pstride + row * a.ldc) + w0;
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) old[j][c] = (a.accumulate && w0 + c < nw32) ? crow[c] : 0u;
+                }
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    uint32_t *crow = reinterpret_cast<uint32_t *>(a.C + j * a.c_pstride + row * a.ldc) + w0;
+#pragma unroll
+                    for (int c = 0; c < CH; ++c)
+                        if (w0 + c < nw32) crow[c] = acc[j][c] ^ old[j][c];
+                }
+            }
+        }
+    } else if (warp == MMA_WARP && rank == 0) {
+        // ===================== MMA issuer (leader CTA) =====================
+        const bool issuer = elect_one();
+        const uint32_t st0 = smem_u32(stages);
+        const uint32_t idesc = idesc_mxf4(2 * BM, BN);
+        int st = 0;
+        uint32_t phase = 0;
+        int64_t gp = 0;
+        for (int64_t ti = 0; ti < my_tiles; ++ti) {
+            for (int t = 0; t < s.nprod; ++t, ++gp) {
+                const int b = (int)(gp & 1);
+                mbar_wait(&bars->tempty[b], (uint32_t)((gp >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dt = tmem + (b ? ACC1 : 0u);
+                for (int ks = 0; ks < nks; ++ks) {
+                    mbar_wait(&bars->full[st], phase);
+                    tc_fence_after();
+                    const uint32_t sb = st0 + (uint32_t)(st * B_BYTES);
+                    if (issuer) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma2_mxf4_ts(dt, tmem + ATM0 + (uint32_t)(st * 32 + kk * 8), umma_desc_sw128(sb + kk * 32),
+                                         idesc, tmem + SFA, tmem + SFB);
+                        mma2_commit_both(&bars->empty[st]);
+                    }
+                    __syncwarp();
+                    if (++st == S) {
+                        st = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (issuer) mma2_commit_both(&bars->tfull[b]);
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == MMA_WARP) {
+        tc_fence_after();
+        tmem_dealloc2(tmem, 512);
+    }
+}
+
+int g_num_sms_run = 0;
+
+template <int E>
+cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
+    static bool attr_set[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= kMaxDevices || !attr_set[dev]) {
+        cudaError_t err = cudaFuncSetAttribute(k_product_run<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        if (err != cudaSuccess) return err;
+        if (dev < kMaxDevices) attr_set[dev] = true;
+    }
+    const int64_t tiles = (a.m_pad / (2 * BM)) * (a.n_pad / BN);
+    if (tiles == 0) return cudaSuccess;
+    if (g_num_sms_run == 0) {
+        cudaDeviceGetAttribute(&g_num_sms_run, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms_run <= 1) g_num_sms_run = 148;
+    }
+    const int64_t clusters = tiles < g_num_sms_run / 2 ? tiles : g_num_sms_run / 2;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(2 * clusters));
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_product_run<E>, s, a);
+}
+
+}  // namespace
+
+cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st) {
+    switch (s.nout) {
+        case 1: return launch_e<1>(s, a, st);
+        case 2: return launch_e<2>(s, a, st);
+        case 3: return launch_e<3>(s, a, st);
+        case 4: return launch_e<4>(s, a, st);
+        case 5: return launch_e<5>(s, a, st);
+        case 6: return launch_e<6>(s, a, st);
+        case 7: return launch_e<7>(s, a, st);
+        case 8: return launch_e<8>(s, a, st);
+        case 9: return launch_e<9>(s, a, st);
+        case 10: return launch_e<10>(s, a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace gf2e

@@ -25,7 +25,7 @@ from .mat_packed import PackedMatrix
 from .mat_sliced import SlicedMatrix, cling, slice_packed
 
 _BACKENDS = {"tc": _lib.BACKEND_TC, "tc_i8": _lib.BACKEND_TC | _lib.TC_INT8, "tc_fp4": _lib.BACKEND_TC | _lib.TC_FP4,
-             "m4rm": _lib.BACKEND_M4RM}
+             "tc_run": _lib.BACKEND_TC | _lib.TC_RUN, "m4rm": _lib.BACKEND_M4RM}
 DEFAULT_BACKEND = os.environ.get("GF2E_BACKEND", "tc")
 
 

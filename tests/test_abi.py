@@ -70,13 +70,19 @@ def test_count_products_host_only():
 
 def test_workspace_sizes():
     L = _lib.load()
-    # tensor-core layout: K(e) * (m_pad * k_pad + n_pad * k_pad) / 8 bytes
+    # tensor-core layout: K(e) * (m_pad * k_pad + n_pad * k_pad) / 8 bytes, bounded over the
+    # forms the call may pick (n padded to 256-column tiles, or 192 for the running-sum form;
+    # k to 256-bit stages)
+    def rup(x, q):
+        return -(-x // q) * q
+
     ws = L.gf2e_slice_mul_workspace(8, 0x11D, 16384, 16384, 16384, 0)
-    assert ws == 27 * 2 * 16384 * 16384 // 8
+    assert ws == 27 * (16384 + max(rup(16384, 256), rup(16384, 192))) * 16384 // 8
     assert L.gf2e_slice_mul_workspace(8, 0x11D, 0, 5, 5, 0) == 0
     assert L.gf2e_slice_mul_workspace(8, 0x11D, 5, 5, 5, 1 << 7) == -1  # bad flag
-    # m padded to the 256-row CTA-pair tile, n to 256 columns, k to 128-bit stages
-    assert L.gf2e_plane_mul_workspace(100, 1, 300, 0) == (256 * 128 + 512 * 128) // 8
+    assert L.gf2e_slice_mul_workspace(8, 0x11D, 5, 5, 5, _lib.TC_INT8 | _lib.TC_RUN) == -1  # conflicting
+    # m padded to the 256-row CTA-pair tile
+    assert L.gf2e_plane_mul_workspace(100, 1, 300, 0) == (256 * 256 + max(512, 384) * 256) // 8
 
 
 def test_invalid_arguments_fail_before_device():

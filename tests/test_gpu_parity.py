@@ -10,7 +10,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-BACKENDS = ["tc_i8", "tc_fp4", "m4rm"]
+BACKENDS = ["tc_i8", "tc_fp4", "tc_run", "m4rm"]
 
 
 @pytest.fixture(scope="module")
@@ -412,3 +412,46 @@ def test_fp4_selfcheck_guard(g):
     C = g.karatsuba_mul(SA, SB)
     assert g._lib.last_product_kernel() == "k_product_tc2<fp4>"
     assert np.array_equal(C.to_numpy(), ref)
+
+
+@pytest.mark.parametrize("e", range(2, 11))
+def test_run_form_all_e(g, e):
+    # the running-sum form (double-buffered accumulators, 256 x 192 tiles): k = 256 (the
+    # config-4 / Schur-update shape), ragged m, n across 192-column tiles, an odd number of
+    # 256-bit stages, and a long k whose running sums stay below 2^23; mul and addmul
+    ctx = g.field_new(e)
+    for (m, k, n) in [(513, 256, 577), (256, 256, 192), (300, 700, 1000), (70, 33000, 200), (1, 1, 1)]:
+        SA = g.SlicedMatrix.random(ctx, m, k, 1)
+        SB = g.SlicedMatrix.random(ctx, k, n, 2)
+        C0 = g.SlicedMatrix.random(ctx, m, n, 3)
+        ref, _ = oracle.karatsuba(e, ctx.f, oracle.sliced_random(e, m, k, 1), oracle.sliced_random(e, k, n, 2),
+                                  m, k, n)
+        C = g.karatsuba_mul(SA, SB, backend="tc_run")
+        assert g._lib.last_product_kernel() == "k_product_run<fp4>"
+        assert np.array_equal(C.to_numpy(), ref), (e, m, k, n)
+        g.addmul(C0, SA, SB, backend="tc_run")
+        assert np.array_equal(C0.to_numpy(), ref ^ oracle.sliced_random(e, m, n, 3)), (e, m, k, n, "addmul")
+
+
+def test_run_form_column_view(g):
+    # C as a column window of a wider plane stack (ldc > words(n)): the 32-bit stores must
+    # leave the neighbouring words alone
+    ctx = g.field_new(5)
+    m, k, n, wide = 300, 256, 640, 1000
+    SA = g.SlicedMatrix.random(ctx, m, k, 1)
+    SB = g.SlicedMatrix.random(ctx, k, n, 2)
+    W = g.SlicedMatrix.random(ctx, m, wide, 9)
+    before = W.to_numpy()
+    L = g._lib
+    flags = L.ACCUMULATE | L.TC_RUN
+    ws = g._device.workspace.get(int(L.load().gf2e_slice_mul_workspace(5, ctx.f, m, k, n, flags)))
+    ldw, lda, ldb = W.planes.shape[2], SA.planes.shape[2], SB.planes.shape[2]
+    L.call("gf2e_slice_mul", 5, ctx.f, SA.planes.data_ptr(), lda, m * lda, SB.planes.data_ptr(), ldb, k * ldb,
+           W.planes.data_ptr() + 2 * 8, ldw, m * ldw, m, k, n, flags, ws.data_ptr(), ws.numel(),
+           g._device.stream_handle())
+    assert L.last_product_kernel() == "k_product_run<fp4>"
+    after = W.to_numpy()
+    ref, _ = oracle.karatsuba(5, ctx.f, oracle.sliced_random(5, m, k, 1), oracle.sliced_random(5, k, n, 2), m, k, n)
+    assert np.array_equal(after[:, :, 2:2 + g.words_for(n)], before[:, :, 2:2 + g.words_for(n)] ^ ref)
+    assert np.array_equal(after[:, :, :2], before[:, :, :2])
+    assert np.array_equal(after[:, :, 2 + g.words_for(n):], before[:, :, 2 + g.words_for(n):])

@@ -1,0 +1,14 @@
+#!/bin/bash
+# round 2: the running-sum short-k form — parity first, then config-4 lines vs int8, ncu
+O=gpurun_out/r2c; mkdir -p $O
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "run_form" > $O/pytest_run.log 2>&1; tail -3 $O/pytest_run.log
+if grep -q failed $O/pytest_run.log; then echo "run-form parity failed"; exit 0; fi
+timeout 1200 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; tail -3 $O/pytest_gpu.log
+for e in 2 8 10; do
+  for b in tc_run tc_i8; do
+    timeout 300 python bench.py --config 4 --e $e --backend $b --no-e2e --no-cpu-baseline > $O/c4_e${e}_$b.json 2>&1
+    python -c "import json,sys;d=json.loads(open('$O/c4_e${e}_$b.json').read().strip().splitlines()[-1]);print('$e $b',d['value'],d['ms_per_step'],d['roofline']['kernel'],d['roofline']['kernel_ms'],d['parity'])" 2>&1 | tail -1
+  done
+done
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name k_product_run --launch-skip 1 --launch-count 1 -o $O/run_c4e8 -f python tools/prof_case.py 8 65536 256 65536 --acc --reps 2 --backend tc_run > $O/ncu_run.log 2>&1; tail -1 $O/ncu_run.log
+echo done
