@@ -1422,6 +1422,9 @@ int64_t gf2e_trsm_workspace(int e, uint32_t f, int64_t m, int64_t n) {
 int gf2e_trsm(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, int64_t ldt, int64_t pt, uint64_t *B,
               int64_t ldb, int64_t pb, int64_t m, int64_t n, void *ws, int64_t ws_bytes, void *stream,
               int64_t *bad_row) {
+    g_err.clear();
+    g_launches = 0;
+    g_products = 0;
     return trsm_impl(e, f, upper, unit_diag, T, ldt, pt, B, ldb, pb, m, n, ws, ws_bytes, stream, bad_row, true);
 }
 }  // extern "C"
@@ -1430,9 +1433,6 @@ namespace {
 int trsm_impl(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, int64_t ldt, int64_t pt, uint64_t *B,
               int64_t ldb, int64_t pb, int64_t m, int64_t n, void *ws, int64_t ws_bytes, void *stream,
               int64_t *bad_row, bool check) {
-    g_err.clear();
-    g_launches = 0;
-    g_products = 0;
     if (bad_row) *bad_row = -1;
     if (int rc = check_field(e, f)) return rc;
     if (unit_diag && upper) return fail(GF2E_EINVAL, "unit_diag is only defined for lower triangular solves");
@@ -1574,7 +1574,7 @@ int gf2e_echelonize(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int6
         DevTmp tw((size_t)(tws > 0 ? tws : 256), st);
         if (!tw.p) return fail(GF2E_ENOMEM, "out of device memory (echelonize trsm workspace)");
         int64_t bad = -1;
-        if (int rc = gf2e_trsm(e, f, 1, 0, U, lw, r * lw, S, ld, ps, r, n, tw.p, tws, st, &bad)) return rc;
+        if (int rc = trsm_impl(e, f, 1, 0, U, lw, r * lw, S, ld, ps, r, n, tw.p, tws, st, &bad, true)) return rc;
     }
     CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     return GF2E_OK;

@@ -267,7 +267,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         const int q = warp & 3;  // TMEM lane quarter
         const int h = ew >> 2;   // column half: tile columns [h*96, h*96+96)
         const int row_local = (int)rank * BM + q * 32 + lane;
-        const int64_t nw32 = (a.n + 31) >> 5;
+        // 32-bit output words up to the end of the row's last 64-bit word: the bits past n in
+        // it are written as zero (C = A.B into uninitialised memory keeps tail bits zero)
+        const int64_t nw32 = 2 * words_for(a.n);
         const uint32_t tempty_leader = mapa(smem_u32(&bars->tempty[0]), 0);
         const uint32_t lq = (uint32_t)(q * 32) << 16;
         uint32_t pc[CH], po[CH];  // previous parity words: current buffer / the other buffer

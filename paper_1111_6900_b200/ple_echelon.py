@@ -41,6 +41,54 @@ class SingularMatrixError(ValueError):
         self.index = index
 
 
+# -- reference MulCounters accounting (ple_echelon.py:130-136, 159-217, 240-287) -------------
+# The device recursion splits at tile-aligned points and multiplies every block on the tensor
+# cores, so it cannot count what the reference counts.  The reference's counters are a pure
+# function of the shapes, the crossover and (for PLE) the column rank profile: _dispatch_mul
+# runs karatsuba_mul (K(e) products + the schedule's additions) iff min(m, k, n) > crossover.
+# These replays reproduce them; device_products receives the products actually launched.
+DEFAULT_PLE_CROSSOVER = 64  # tuning.py:24
+
+
+def _crossover(crossover: int | None) -> int:
+    return max(1, DEFAULT_PLE_CROSSOVER if crossover is None else int(crossover))
+
+
+def _ref_trsm_calls(m: int, n: int, cx: int) -> int:
+    """Karatsuba calls of _trsm_lower_rec / _trsm_upper_rec (ple_echelon.py:159-175,201-217)
+    on an m x m triangle against n columns; both split at h = m // 2 and dispatch one
+    (m-h) x h x n (lower) or h x (m-h) x n (upper) update."""
+    if m <= cx:
+        return 0
+    h = m // 2
+    return (_ref_trsm_calls(h, n, cx) + _ref_trsm_calls(m - h, n, cx)
+            + (1 if min(m - h, h, n) > cx else 0))
+
+
+def _ref_ple_calls(m: int, n: int, c0: int, pivots: np.ndarray, cx: int) -> int:
+    """Karatsuba calls of _ple_rec (ple_echelon.py:240-287) on rows m, columns [c0, c0 + n):
+    the left half's rank r1 is the number of pivot columns it holds (PLE finds the column rank
+    profile, and a node's Schur complement keeps the global profile's columns)."""
+    if n <= cx or n < 2:
+        return 0
+    n1 = n // 2
+    calls = _ref_ple_calls(m, n1, c0, pivots, cx)
+    r1 = int(np.count_nonzero((pivots >= c0) & (pivots < c0 + n1)))
+    if r1 > 0:
+        calls += _ref_trsm_calls(r1, n - n1, cx)
+        if m - r1 > 0 and min(m - r1, r1, n - n1) > cx:
+            calls += 1
+    if m - r1 > 0:
+        calls += _ref_ple_calls(m - r1, n - n1, c0 + n1, pivots, cx)
+    return calls
+
+
+def _account(counters: MulCounters | None, ctx, calls: int) -> None:
+    from .poly_mul import _bump
+
+    _bump(counters, ctx, calls, device_products=_lib.last_gf2_products())
+
+
 def _check(T: PackedMatrix, B: PackedMatrix) -> None:
     if T.ctx != B.ctx:
         raise ValueError(f"field mismatch: {T.ctx} vs {B.ctx}")
@@ -70,31 +118,33 @@ def trsm_sliced(T: SlicedMatrix, B: SlicedMatrix, upper: bool, unit_diag: bool =
     _lib.check(rc, "gf2e_trsm")
 
 
-def _trsm_packed(T: PackedMatrix, B: PackedMatrix, upper: bool, unit_diag: bool) -> None:
+def _trsm_packed(T: PackedMatrix, B: PackedMatrix, upper: bool, unit_diag: bool, crossover: int | None,
+                 counters: MulCounters | None) -> None:
     _check(T, B)
     if T.nrows == 0 or B.ncols == 0:
         return
     Bs = slice_packed(B)
     trsm_sliced(slice_packed(T), Bs, upper, unit_diag)
     cling(Bs, out=B)
+    _account(counters, T.ctx, _ref_trsm_calls(T.nrows, B.ncols, _crossover(crossover)))
 
 
 def trsm_upper_left(U: PackedMatrix, B: PackedMatrix, crossover: int | None = None,
                     counters: MulCounters | None = None) -> None:
     """Solve U X = B in place for upper triangular U (ple_echelon.py:187-198)."""
-    _trsm_packed(U, B, True, False)
+    _trsm_packed(U, B, True, False, crossover, counters)
 
 
 def trsm_lower_left(L: PackedMatrix, B: PackedMatrix, unit_diag: bool = False, crossover: int | None = None,
                     counters: MulCounters | None = None) -> None:
     """Solve L X = B in place for lower triangular L (ple_echelon.py:138-156)."""
-    _trsm_packed(L, B, False, unit_diag)
+    _trsm_packed(L, B, False, unit_diag, crossover, counters)
 
 
 def trsm_lower_left_unit(L: PackedMatrix, B: PackedMatrix, crossover: int | None = None,
                          counters: MulCounters | None = None) -> None:
     """Solve L X = B with L unit lower triangular (diagonal implicit; ple_echelon.py:178-184)."""
-    _trsm_packed(L, B, False, True)
+    _trsm_packed(L, B, False, True, crossover, counters)
 
 
 # -- permutations (ple_echelon.py:36-107) ----------------------------------------------------
@@ -230,7 +280,13 @@ def ple(A: PackedMatrix, crossover: int | None = None, counters: MulCounters | N
     API parity; like the reference's, it cannot change the result."""
     S = slice_packed(A)
     P, Q, r = ple_sliced(S)
+    device = _lib.last_gf2_products()
     cling(S, out=A)
+    if counters is not None:
+        from .poly_mul import _bump
+
+        calls = _ref_ple_calls(A.nrows, A.ncols, 0, Q.entries[:r], _crossover(crossover))
+        _bump(counters, A.ctx, calls, device_products=device)
     return PleFactors(P, Q, r, A)
 
 
@@ -279,8 +335,25 @@ def echelonize(A: PackedMatrix, full: bool = True, crossover: int | None = None,
     """Reduce A in place via PLE; returns the rank (ple_echelon.py:343-374).  full=False leaves
     the row echelon form, full=True the reduced row echelon form."""
     S = slice_packed(A)
+    if counters is None:
+        r = echelonize_sliced(S, full)
+        cling(S, out=A)
+        return r
+    # the accounting needs the column rank profile: PLE + the echelon steps on the same planes
+    from .poly_mul import _bump
+
+    cx = _crossover(crossover)
+    m, n = A.nrows, A.ncols
     r = echelonize_sliced(S, full)
+    device = _lib.last_gf2_products()
     cling(S, out=A)
+    # pivot columns = the leading entry of each of the first r rows of the echelon form
+    lead = A.to_array()[:r] != 0
+    pivots = np.argmax(lead, axis=1) if r else np.zeros(0, dtype=np.int64)
+    calls = _ref_ple_calls(m, n, 0, pivots, cx)
+    if full and r > 0:
+        calls += _ref_trsm_calls(r, n, cx)
+    _bump(counters, A.ctx, calls, device_products=device)
     return r
 
 

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 from . import _device, _lib
 from .gf2e import FieldCtx, field_new
@@ -38,16 +38,25 @@ def _resolve_backend(backend: str | None) -> int:
 
 @dataclass
 class MulCounters:
-    """Operation counts accumulated over one multiplication call (poly_mul.py:32-43)."""
+    """Operation counts accumulated over one multiplication call (poly_mul.py:32-43).
+
+    The three reference fields carry the reference's accounting exactly: every Karatsuba
+    multiplication the reference would perform adds K(e) GF(2) products and the schedule's
+    additions (replayed from the same schedule), including those inside TRSM / PLE /
+    echelonize, where the reference's recursion with the given crossover is replayed on the
+    factorisation's rank profile (ple_echelon.py:130-136).  ``device_products`` (not part of
+    equality) counts the GF(2) plane products this library actually launched on the GPU."""
 
     gf2_matmul_count: int = 0
     additions: int = 0
     peak_live_products: int = 0
+    device_products: int = field(default=0, compare=False)
 
     def reset(self) -> None:
         self.gf2_matmul_count = 0
         self.additions = 0
         self.peak_live_products = 0
+        self.device_products = 0
 
 
 @dataclass(frozen=True)
@@ -85,14 +94,17 @@ def schedule(e: int, f: int | None = None) -> Schedule:
     return s
 
 
-def _bump(counters: MulCounters | None, ctx: FieldCtx) -> None:
+def _bump(counters: MulCounters | None, ctx: FieldCtx, calls: int = 1, device_products: int | None = None) -> None:
+    """Add `calls` reference Karatsuba multiplications (poly_mul.py:146-150 / 245-259
+    bookkeeping) and the GF(2) products launched on the device (default: K(e) per call)."""
     if counters is None:
         return
     g, adds, peak = schedule(ctx.e, ctx.f).counters
-    counters.gf2_matmul_count += g
-    counters.additions += adds
-    if peak > counters.peak_live_products:
+    counters.gf2_matmul_count += g * calls
+    counters.additions += adds * calls
+    if calls and peak > counters.peak_live_products:
         counters.peak_live_products = peak
+    counters.device_products += g * calls if device_products is None else device_products
 
 
 def _check_operands(A: SlicedMatrix, B: SlicedMatrix) -> None:

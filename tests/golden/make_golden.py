@@ -152,6 +152,15 @@ def main():
         ple_echelon.trsm_lower_left(L, XL)
         ple_echelon.trsm_lower_left_unit(L, XLu)
         tag = f"trsm/e{e}/{m}x{n}"
+        # MulCounters of the three solves at the default crossover and at 16 (ple_echelon.py:130-136)
+        cnts = []
+        for cx in (None, 16):
+            for fn, T in ((ple_echelon.trsm_upper_left, U), (ple_echelon.trsm_lower_left, L),
+                          (ple_echelon.trsm_lower_left_unit, L)):
+                c = poly_mul.MulCounters()
+                fn(T, B.copy(), crossover=cx, counters=c)
+                cnts.append([c.gf2_matmul_count, c.additions, c.peak_live_products])
+        store[f"{tag}/counters"] = np.array(cnts, dtype=np.int64)
         store[f"{tag}/meta"] = np.array([e, ctx.f, m, n], dtype=np.int64)
         store[f"{tag}/U"] = U.storage.words.copy()
         store[f"{tag}/L"] = L.storage.words.copy()
@@ -227,6 +236,21 @@ def main():
         store[f"{tag}/P"] = F.P.entries.copy()
         store[f"{tag}/Q"] = F.Q.entries.copy()
         store[f"{tag}/rank"] = np.array([F.rank], dtype=np.int64)
+        # MulCounters: ple and echelonize (full, row) at the default crossover and at 16
+        cnts = []
+        for cx in (None, 16):
+            try:
+                c = poly_mul.MulCounters()
+                ple_echelon.ple(A.copy(), crossover=cx, counters=c)
+                row = [c.gf2_matmul_count, c.additions, c.peak_live_products]
+                for full in (True, False):
+                    c = poly_mul.MulCounters()
+                    ple_echelon.echelonize(A.copy(), full=full, crossover=cx, counters=c)
+                    row += [c.gf2_matmul_count, c.additions, c.peak_live_products]
+            except ValueError:
+                row = [-1] * 9  # the reference's recursion raised at this crossover
+            cnts.append(row)
+        store[f"{tag}/counters"] = np.array(cnts, dtype=np.int64)
         for full, (r, X) in zip((True, False), ech):
             assert r == F.rank
             store[f"{tag}/ech{int(full)}"] = X.storage.words.copy()
