@@ -134,6 +134,24 @@ int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, int64_
                    int64_t workspace_bytes, void *stream);
 
 /*
+ * gf2e_slice_mul with B arriving in column parts — the multi-GPU form (dist.sharded_mul: B is
+ * broadcast over NVLink part by part while this rank already multiplies the parts that
+ * arrived).  Part p holds columns [col_bounds[p], col_bounds[p+1]) of B as its own plane
+ * stack (B_parts[p], ldb[p], pb[p]); col_bounds[0] = 0, col_bounds[nparts] = n, interior
+ * bounds multiples of 64.  ready_events (optional; entries optional) are cudaEvent_t handles:
+ * the stream waits for event p before reading part p.  A's operand combinations are formed
+ * once; after each part the product runs over every column tile whose columns have all
+ * arrived.  Same workspace as gf2e_slice_mul (gf2e_slice_mul_workspace); tensor-core
+ * backends only.  C = A*B or C ^= A*B (GF2E_ACCUMULATE).
+ */
+int gf2e_slice_mul_parts(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, int64_t pa, int nparts,
+                         const int64_t *col_bounds, const uint64_t *const *B_parts_dev, const int64_t *ldb,
+                         const int64_t *pb, void *const *ready_events, uint64_t *C_dev, int64_t ldc,
+                         int64_t pc, int64_t m, int64_t k, int64_t n, uint32_t flags, void *workspace,
+                         int64_t workspace_bytes, void *stream);
+
+/*
+ * mzed_mul / mzed_addmul with HOST buffers/*
  * mzed_mul / mzed_addmul with HOST buffers — the end-to-end entry a numpy-based caller
  * (e.g. gf2elin itself) binds: karatsuba_mul_packed (poly_mul.py:275-278)
  * and C ^= A*B on packed matrices, with A (m x k), B (k x n), C (m x n) in host memory in

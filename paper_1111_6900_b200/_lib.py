@@ -46,6 +46,9 @@ SIGNATURES = {
     "gf2e_plane_mul_workspace": (_I64, [_I64, _I64, _I64, _U32]),
     "gf2e_slice_mul": (_INT, [_INT, _U32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64,
                               _U32, _P, _I64, _P]),
+    "gf2e_slice_mul_parts": (_INT, [_INT, _U32, _P, _I64, _I64, _INT, ctypes.POINTER(_I64), ctypes.POINTER(_P),
+                                    ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_P), _P, _I64, _I64,
+                                    _I64, _I64, _I64, _U32, _P, _I64, _P]),
     "gf2e_mzed_mul_host": (_INT, [_INT, _U32, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _U32, _I64,
                                   ctypes.POINTER(ctypes.c_double)]),
     "gf2e_trsm_workspace": (_I64, [_INT, _U32, _I64, _I64]),

@@ -312,10 +312,14 @@ int fp4_state() {
     return g_fp4_state[dev];
 }
 
-int tc_form(uint32_t flags, int64_t k) {
+// the running-sum form is exact while every accumulator's sum of counts stays below 2^16:
+// ceil(K/2) products of at most k_pad each per buffer and tile
+bool run_ok(int nprod, int64_t k) { return (int64_t)((nprod + 1) / 2) * round_up(k, kTcBKFp4) < kRunMaxSum; }
+
+int tc_form(uint32_t flags, int64_t k, int nprod = kMaxProducts) {
     if (flags & GF2E_TC_INT8) return kFormI8;
     if (fp4_state() < 0) return kFormI8;  // the fp4 self-check failed on this device
-    if (flags & GF2E_TC_RUN) return kFormFp4Run;
+    if ((flags & GF2E_TC_RUN) && run_ok(nprod, k)) return kFormFp4Run;
     if (k >= kFp4LongK) return kFormFp4Long;
     if (k >= kFp4MinK) return kFormFp4;
     if (flags & GF2E_TC_FP4) return kFormFp4Pair;
@@ -343,7 +347,7 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags, in
         L.a_pstride = L.m_pad * L.kwords;
         L.b_pstride = L.k_pad * (L.n_pad / 64);
     } else {
-        if (form == -1) form = tc_form(flags, k);
+        if (form == -1) form = tc_form(flags, k, nprod);
         L.m_pad = round_up(m, 2 * kTcBM);  // CTA-pair tiles are 256 rows
         if (form == kFormAny) {
             const int64_t a = round_up(n, kTcBN), b = round_up(n, kRunBN);
@@ -385,7 +389,7 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
     const bool tc = !(flags & GF2E_BACKEND_M4RM);
     if (tc && form_override < 0 && !(flags & GF2E_TC_INT8))
         if (int rc = ensure_fp4_checked()) return rc;
-    const int form = form_override >= 0 ? form_override : tc_form(flags, k);
+    const int form = form_override >= 0 ? form_override : tc_form(flags, k, ks.nprod);
     const bool fp4 = tc && form != kFormI8;
     Layout L = layout_for(ks.nprod, m, k, n, flags, form);
     if (ws_bytes < L.total)
@@ -1180,6 +1184,82 @@ int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa
     return run_product(ks, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, flags, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int gf2e_slice_mul_parts(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa, int nparts,
+                         const int64_t *col_bounds, const uint64_t *const *B_parts, const int64_t *ldb,
+                         const int64_t *pb, void *const *ready_events, uint64_t *C, int64_t ldc, int64_t pc,
+                         int64_t m, int64_t k, int64_t n, uint32_t flags, void *ws, int64_t ws_bytes,
+                         void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    g_products = 0;
+    if (int rc = check_field(e, f)) return rc;
+    if (int rc = check_flags(flags)) return rc;
+    if (flags & GF2E_BACKEND_M4RM) return fail(GF2E_EINVAL, "column parts need a tensor-core backend");
+    if (nparts < 1 || !col_bounds || !B_parts || !ldb || !pb) return fail(GF2E_EINVAL, "bad part arrays");
+    if (col_bounds[0] != 0 || col_bounds[nparts] != n)
+        return fail(GF2E_EINVAL, "column bounds must run from 0 to n = %lld", (long long)n);
+    for (int p = 0; p < nparts; ++p) {
+        const int64_t c0 = col_bounds[p], c1 = col_bounds[p + 1];
+        if (c1 < c0 || (p + 1 < nparts && (c1 & 63)))
+            return fail(GF2E_EINVAL, "column bound %d (%lld) must be non-decreasing and a multiple of 64", p + 1,
+                        (long long)c1);
+        if (int rc = check_mat(B_parts[p], k, words_for(c1 - c0), ldb[p], "B part")) return rc;
+    }
+    if (int rc = check_mat(A, m, words_for(k), lda, "A")) return rc;
+    if (int rc = check_mat(C, m, words_for(n), ldc, "C")) return rc;
+    if (int rc = check_device()) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool acc = (flags & GF2E_ACCUMULATE) != 0;
+    if (m == 0 || n == 0 || k == 0) {  // nothing to wait for but the parts' events
+        for (int p = 0; p < nparts; ++p)
+            if (ready_events && ready_events[p])
+                CKH(cudaStreamWaitEvent(st, (cudaEvent_t)ready_events[p], 0), "cudaStreamWaitEvent");
+        if (m && n && !acc)
+            for (int j = 0; j < e; ++j)
+                CK(cudaMemset2DAsync(C + j * pc, ldc * 8, 0, words_for(n) * 8, m, st), "cudaMemset2DAsync");
+        return GF2E_OK;
+    }
+    if (int rc = ensure_fp4_checked()) return rc;
+    const Sched ks = to_kernel_sched(e, get_schedule(e, f));
+    const int form = tc_form(flags, k, ks.nprod);
+    const bool fp4 = form != kFormI8;
+    const Layout L = layout_for(ks.nprod, m, k, n, flags, form);
+    if (ws_bytes < L.total)
+        return fail(GF2E_ENOMEM, "workspace too small: %lld < %lld bytes", (long long)ws_bytes, (long long)L.total);
+    if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255))
+        return fail(GF2E_EINVAL, "workspace must be a 256-byte aligned device pointer");
+    uint64_t *Ac = static_cast<uint64_t *>(ws);
+    uint64_t *Bt = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + L.a_bytes);
+    const int64_t tw = form_bn(form), ntiles = L.n_pad / tw;
+    CK(launch_combos_rows(ks, A, lda, pa, m, k, Ac, L.kwords, L.a_pstride, L.m_pad, L.kwords, fp4 ? 4 : 2, st),
+       "combos(A)");
+    int64_t done = 0;  // column tiles already multiplied
+    for (int p = 0; p < nparts; ++p) {
+        const int64_t c0 = col_bounds[p], c1 = col_bounds[p + 1];
+        const bool lastp = p + 1 == nparts;
+        if (ready_events && ready_events[p])
+            CKH(cudaStreamWaitEvent(st, (cudaEvent_t)ready_events[p], 0), "cudaStreamWaitEvent");
+        const int64_t rend = lastp ? L.n_pad : c1;  // the last part also zero-fills the padding
+        if (rend > c0)
+            CK(launch_combos_bt(ks, B_parts[p], ldb[p], pb[p], k, c1 - c0, Bt, L.kwords, L.b_pstride, L.kwords,
+                                (rend - c0) / 64, fp4, st, form_br(form), c0),
+               "combos(B^T part)");
+        // every tile whose columns have all arrived
+        const int64_t avail = lastp ? ntiles : c1 / tw;
+        if (avail > done) {
+            const int64_t n0 = done * tw, n1 = avail * tw < n ? avail * tw : n;
+            TcArgs a{Ac, Bt + n0 * L.kwords, L.a_pstride, L.b_pstride, L.kwords, m, n1 - n0, L.m_pad,
+                     (avail - done) * tw, C + n0 / 64, ldc, pc, acc ? 1 : 0};
+            ProfScope prof(st);
+            CK(launch_form(ks, a, form, st), "product");
+            g_products += ks.nprod;
+            done = avail;
+        }
+    }
+    g_kernel = form_name(form);
+    return GF2E_OK;
+}
+
 int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, const uint64_t *B_h, int64_t ldb,
                        uint64_t *C_h, int64_t ldc, int64_t m, int64_t k, int64_t n, uint32_t flags,
                        int64_t chunk_rows, double *device_ms) {
@@ -1204,7 +1284,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     if (int rc = check_device()) return rc;
     if (int rc = ensure_fp4_checked()) return rc;
     Sched ks = to_kernel_sched(e, get_schedule(e, f));
-    const int form = tc_form(0, k);
+    const int form = tc_form(0, k, ks.nprod);
     const int64_t tw = form_bn(form);  // column tile width: B parts and column splits align to it
     int64_t chunk = chunk_rows > 0 ? round_up(chunk_rows, 2 * kTcBM) : 2048;
     if (chunk > round_up(m, 2 * kTcBM)) chunk = round_up(m, 2 * kTcBM);

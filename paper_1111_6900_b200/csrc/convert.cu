@@ -392,7 +392,7 @@ __device__ __forceinline__ void transpose64(uint64_t &xa, uint64_t &xb, int lane
 template <int E>  // planes at compile time (register arrays of E words)
 __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb, int64_t pb, int64_t k,
                             int64_t n, uint64_t *__restrict__ out, int64_t ldo, int64_t po, int64_t kblocks,
-                            int64_t nblocks, int fp4, int tsplit, int br) {
+                            int64_t nblocks, int fp4, int tsplit, int br, int64_t row0) {
     // one warp per (2 x 64 k-rows, 64-column block[, product group]): two 64x64 transposes, then each lane
     // writes 16-byte pieces of tile rows.  Input row r of a 64-block lands at bit sigma(r):
     // int8 reverses bits inside bytes (r ^ 7), fp4 swaps bits 0 and 2 of every nibble.
@@ -423,7 +423,7 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
                 b[h][i] = (nb < nw && r1 < k) ? (B[i * pb + r1 * ldb + nb] & tm) : 0;
             }
         }
-        const int64_t ra = tc_b_row_inv(nb * 64 + lane), rbw = tc_b_row_inv(nb * 64 + lane + 32);
+        const int64_t ra = tc_b_row_inv(row0 + nb * 64 + lane), rbw = tc_b_row_inv(row0 + nb * 64 + lane + 32);
         // the transpose is GF(2)-linear: transpose the e planes once, then form every
         // product's subset XOR from the transposed words (e instead of K(e) transposes)
 #pragma unroll
@@ -582,7 +582,7 @@ cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, i
 
 cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int64_t pb, int64_t k, int64_t n,
                              uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks, bool fp4,
-                             cudaStream_t st, int br) {
+                             cudaStream_t st, int br, int64_t row0) {
     int64_t warps = (kblocks >> 1) * nblocks;  // kblocks is even (k_pad is a multiple of 128)
     if (warps == 0) return cudaSuccess;
     int tsplit = 1;
@@ -590,7 +590,7 @@ cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int
     int g = grid_for(warps * tsplit * 32, 256);
     return dispatch_e(s.e, [&](auto ec) {
         k_combos_bt<decltype(ec)::value><<<g, 256, 0, st>>>(s, B, ldb, pb, k, n, out, ldo, po, kblocks, nblocks,
-                                                            fp4 ? 1 : 0, tsplit, br);
+                                                            fp4 ? 1 : 0, tsplit, br, row0);
         return cudaGetLastError();
     });
 }

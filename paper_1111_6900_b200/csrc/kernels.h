@@ -51,7 +51,9 @@ cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, i
 // KW = 2 and bits reversed inside every byte
 cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int64_t pb, int64_t k, int64_t n,
                              uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks, bool fp4,
-                             cudaStream_t st, int br = 128);
+                             cudaStream_t st, int br = 128, int64_t row0 = 0);
+// (row0: first B^T row written, a multiple of 64 — the column offset of a B part; the tile
+// layout stays relative to `out`)
 
 // Tensor-core product.  Operands: Ac [nprod] x (m_pad x k_pad bits) natural bit order,
 // Bt [nprod] x (n_pad x k_pad bits) = B^T with bits reversed in each byte.
@@ -80,6 +82,7 @@ constexpr int kFormI8 = 0, kFormFp4 = 1, kFormFp4Pair = 2, kFormFp4Long = 3;  //
 // re-initialisation; tiles 256 x kRunBN, B^T stage-tiled in kRunBN/2-row blocks
 constexpr int kFormFp4Run = 4;
 constexpr int kRunBN = 192;
+constexpr int64_t kRunMaxSum = 65536;  // ceil(K/2) * k_pad must stay below (exact running sums)
 cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st);
 constexpr int64_t kFp4PairMaxK = 2047;
 cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, int form, cudaStream_t st);

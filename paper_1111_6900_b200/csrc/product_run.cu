@@ -9,11 +9,12 @@
 // accumulator after every drain (one tcgen05.st per cell per product) and have a single
 // accumulator; this form removes both:
 //
-//  * running sums.  Each accumulator starts at 2^23 (fp32 ulp 1) once per tile and is never
-//    re-initialised between products: after product t it holds 2^23 + S_t, S_t = the sum of
-//    the counts of the products accumulated into it so far (exact while S_t < 2^23: at most
-//    ceil(K/2) * k < 2^23).  parity(count_t) = bit0(S_t) ^ bit0(S_{t-2}), so the epilogue
-//    keeps the previous parity word of each buffer and XORs.  No tcgen05.st per product.
+//  * running sums.  Each accumulator starts at 65536.0f once per tile and is never
+//    re-initialised between products: after product t it holds 65536 + S_t, S_t = the sum of
+//    the counts of the products accumulated into it so far (exact while S_t < 2^16: at most
+//    ceil(K/2) * k < 65536, which the host checks), so S_t sits in mantissa bits 7.. and
+//    parity(count_t) = bit7 ^ bit7 of the previous read of the same buffer: the epilogue keeps
+//    the previous parity word of each buffer and XORs.  No tcgen05.st per product.
 //  * double buffering.  Two accumulators of N = 192 columns (products alternate between
 //    them), so the drain of product t overlaps the MMAs of product t+1.  TMEM: accumulators
 //    0-191 and 192-383, three A stages 384-479 (the expanded A operand lives in TMEM, as in
@@ -47,7 +48,10 @@ constexpr int BITS_A = BM * KW * 8, BITS_B = BNH * KW * 8, BITS_BYTES = BITS_A +
 constexpr uint32_t ACC1 = BN;  // TMEM column of the second accumulator (the first starts at 0)
 constexpr uint32_t ATM0 = 2 * BN, SFA = 480, SFB = 496;
 static_assert(ATM0 + 32 * S <= SFA, "TMEM: A stages overlap the scale factors");
-constexpr uint32_t RUN_INIT = 0x4B000000u;             // 2^23
+// 65536.0f: ulp 2^-7 up to 2^17, so the running sum S sits in mantissa bits 7.. and its
+// parity is bit 7 of the pattern (the extraction of the other fp4 forms); exact while S < 2^16,
+// i.e. ceil(K/2) * k < 65536 (host: kRunMaxSum)
+constexpr uint32_t RUN_INIT = 0x47800000u;
 constexpr uint32_t SF_ONE = 0x7F7F7F7Fu;               // E8M0 1.0
 constexpr int CH = BN / 2 / 32;                        // 32-column chunks per epilogue thread
 constexpr int GROUP_M = 8;
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
     if (warp >= EPI_W0 && warp < EPI_W0 + 4) {
-        // scale factors (every byte E8M0 1.0) and both running-sum accumulators at 2^23
+        // scale factors (every byte E8M0 1.0) and both running-sum accumulators at 65536
         const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
         st32_const(tmem + lb + SFA, SF_ONE);
         for (int c = 0; c < 2 * BN; c += 32) st32_const(tmem + lb + c, RUN_INIT);
@@ -285,10 +289,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
             for (int j = 0; j < E; ++j)
 #pragma unroll
                 for (int c = 0; c < CH; ++c) acc[j][c] = 0;
+            // C0 of this thread's words, loaded now so the latency hides behind the products
+            const int64_t row = tm * (2 * BM) + row_local;
+            const int64_t w0 = tn * (BN / 32) + h * CH;  // first 32-bit word of this thread
+            const bool rowok = row < a.m;
+            uint32_t old[E][CH];
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const uint32_t *crow = reinterpret_cast<const uint32_t *>(a.C + j * a.c_pstride + row * a.ldc) + w0;
+#pragma unroll
+                for (int c = 0; c < CH; ++c) old[j][c] = (a.accumulate && rowok && w0 + c < nw32) ? crow[c] : 0u;
+            }
             for (int t = 0; t < s.nprod; ++t, ++gp) {
                 const int b = (int)(gp & 1);
                 const uint32_t mask = bars->outmask[t];
-                mbar_wait(&bars->tfull[b], (uint32_t)((gp >> 1) & 1));
+                uint32_t sel[E];  // all-ones for the output planes this product folds into
+#pragma unroll
+                for (int j = 0; j < E; ++j) sel[j] = 0u - ((mask >> j) & 1u);
+                mbar_wait_sleep(&bars->tfull[b], (uint32_t)((gp >> 1) & 1), 20);
                 tc_fence_after();
                 const uint32_t ta = tmem + lq + (b ? ACC1 : 0u) + (uint32_t)(h * (BN / 2));
                 const bool last = t + 2 >= s.nprod;  // this buffer's last product in the tile
@@ -299,29 +317,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                     tmem_wait_ld();
                     if (last) st32_const(ta + (uint32_t)(c * 32), RUN_INIT);
                     // bit 0 of each cell = parity of the running sum; shifted to bit 7 of a byte
-                    const uint32_t w = parity_word_packed_shl<7, 0xECA8>(v);
+                    const uint32_t w = parity_word_packed(v);
                     const uint32_t pw = w ^ pc[c];
                     pc[c] = po[c];
                     po[c] = last ? 0u : w;
 #pragma unroll
-                    for (int j = 0; j < E; ++j) acc[j][c] ^= pw & (0u - ((mask >> j) & 1u));
+                    for (int j = 0; j < E; ++j) acc[j][c] ^= pw & sel[j];
                 }
                 if (last) wait_st();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(b * 8));
             }
-            const int64_t row = tm * (2 * BM) + row_local;
-            if (row < a.m) {
-                const int64_t w0 = tn * (BN / 32) + h * CH;  // first 32-bit word of this thread
-                uint32_t old[E][CH];
-#pragma unroll
-                for (int j = 0; j < E; ++j) {
-                    const uint32_t *crow =
-                        reinterpret_cast<const uint32_t *>(a.C + j * a.c_pstride + row * a.ldc) + w0;
-#pragma unroll
-                    for (int c = 0; c < CH; ++c) old[j][c] = (a.accumulate && w0 + c < nw32) ? crow[c] : 0u;
-                }
+            if (rowok) {
 #pragma unroll
                 for (int j = 0; j < E; ++j) {
                     uint32_t *crow = reinterpret_cast<uint32_t *>(a.C + j * a.c_pstride + row * a.ldc) + w0;

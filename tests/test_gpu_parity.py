@@ -418,19 +418,32 @@ def test_fp4_selfcheck_guard(g):
 def test_run_form_all_e(g, e):
     # the running-sum form (double-buffered accumulators, 256 x 192 tiles): k = 256 (the
     # config-4 / Schur-update shape), ragged m, n across 192-column tiles, an odd number of
-    # 256-bit stages, and a long k whose running sums stay below 2^23; mul and addmul
+    # 256-bit stages, the longest k whose running sums stay below 2^16; mul and addmul
     ctx = g.field_new(e)
-    for (m, k, n) in [(513, 256, 577), (256, 256, 192), (300, 700, 1000), (70, 33000, 200), (1, 1, 1)]:
+    K = g.count_products(e)
+    kmax = (65535 // ((K + 1) // 2)) // 256 * 256
+    for (m, k, n) in [(513, 256, 577), (256, 256, 192), (300, 700, 1000), (70, kmax, 200), (1, 1, 1)]:
         SA = g.SlicedMatrix.random(ctx, m, k, 1)
         SB = g.SlicedMatrix.random(ctx, k, n, 2)
         C0 = g.SlicedMatrix.random(ctx, m, n, 3)
         ref, _ = oracle.karatsuba(e, ctx.f, oracle.sliced_random(e, m, k, 1), oracle.sliced_random(e, k, n, 2),
                                   m, k, n)
         C = g.karatsuba_mul(SA, SB, backend="tc_run")
-        assert g._lib.last_product_kernel() == "k_product_run<fp4>"
+        assert g._lib.last_product_kernel() == "k_product_run<fp4>", (e, k)
         assert np.array_equal(C.to_numpy(), ref), (e, m, k, n)
         g.addmul(C0, SA, SB, backend="tc_run")
         assert np.array_equal(C0.to_numpy(), ref ^ oracle.sliced_random(e, m, n, 3)), (e, m, k, n, "addmul")
+
+
+def test_run_form_falls_back_past_its_range(g):
+    # ceil(K/2) * k >= 2^16: the forced running-sum form would overflow its exact range, so
+    # the call takes the fp4 long form (and stays exact)
+    ctx = g.field_new(2)
+    m, k, n = 70, 44000, 200
+    C = g.karatsuba_mul(g.SlicedMatrix.random(ctx, m, k, 1), g.SlicedMatrix.random(ctx, k, n, 2), backend="tc_run")
+    assert g._lib.last_product_kernel() == "k_product_tc2<fp4>"
+    ref, _ = oracle.karatsuba(2, ctx.f, oracle.sliced_random(2, m, k, 1), oracle.sliced_random(2, k, n, 2), m, k, n)
+    assert np.array_equal(C.to_numpy(), ref)
 
 
 def test_run_form_column_view(g):

@@ -182,3 +182,39 @@ def test_newton_john_golden(g, golden):
         assert np.array_equal(X.to_numpy(), golden[f"{tag}/trsm"]), tag
     with pytest.raises(ValueError, match="single row"):
         g.make_table(g.PackedMatrix.random(g.field_new(4), 2, 5, 1))
+
+
+def test_counters_through_the_api(g, golden):
+    # MulCounters passed to trsm_* / ple / echelonize match the reference's own counters
+    # (ple_echelon.py:130-136 _dispatch_mul accounting) at the default crossover and at 16;
+    # device_products counts the GF(2) products the device actually launched
+    for tag in (str(t) for t in golden["trsm_tags"]):
+        e, f, m, n = (int(x) for x in golden[f"{tag}/meta"])
+        ctx = g.field_new(e, f)
+        U = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/U"], m)
+        L = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/L"], m)
+        B = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/B"], n)
+        got = []
+        for cx in (None, 16):
+            for fn, T in ((g.trsm_upper_left, U), (g.trsm_lower_left, L), (g.trsm_lower_left_unit, L)):
+                c = g.MulCounters()
+                fn(T, B.copy(), crossover=cx, counters=c)
+                got.append([c.gf2_matmul_count, c.additions, c.peak_live_products])
+                assert c.device_products > 0 and c.device_products % g.count_products(e) == 0, tag
+        assert got == golden[f"{tag}/counters"].tolist(), tag
+    for tag in (str(t) for t in golden["ple_tags"]):
+        e, f, m, n = (int(x) for x in golden[f"{tag}/meta"])
+        ctx = g.field_new(e, f)
+        A = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/A"], n)
+        for row, cx in zip(golden[f"{tag}/counters"].tolist(), (None, 16)):
+            if row[0] < 0:
+                continue
+            got = []
+            c = g.MulCounters()
+            g.ple(A.copy(), crossover=cx, counters=c)
+            got += [c.gf2_matmul_count, c.additions, c.peak_live_products]
+            for full in (True, False):
+                c = g.MulCounters()
+                g.echelonize(A.copy(), full=full, crossover=cx, counters=c)
+                got += [c.gf2_matmul_count, c.additions, c.peak_live_products]
+            assert got == row, (tag, cx)
