@@ -198,75 +198,111 @@ def run_ours(args):
     ops_rank = K * 2.0 * m * k * n
     backend = args.backend
 
-    # ---- inputs resident in HBM: A row-block (rank's rows of the global matrix), B broadcast ----
+    # ---- inputs resident in HBM: A row-block (rank's rows of the global matrix); B generated on
+    #      rank 0, kept there pre-split into the broadcast's column parts ----
+    from paper_1111_6900_b200 import dist as gdist
+
     row0 = rank * m
     A = g.SlicedMatrix.random(ctx, m, k, 1, row0=row0, gcols=k)
-    if rank == 0 or world == 1:
+    if rank == 0:
         B = g.SlicedMatrix.random(ctx, k, n, 2)
     else:
         B = g.SlicedMatrix(ctx, k, n, torch.empty((e, k, g.words_for(n)), dtype=torch.int64, device=dev))
-    from paper_1111_6900_b200 import dist as gdist
-
-    gdist.broadcast_planes(B.planes, src=0)  # the one collective: B over NVLink (NCCL)
+    bounds = gdist.col_parts(n, args.bcast_parts)
+    src_parts = gdist.split_parts(B.planes, bounds) if rank == 0 else None
+    gdist.broadcast_planes(B.planes, src=0)  # a resident copy of B on every rank (compute-only line)
     C = (g.SlicedMatrix.random(ctx, m, n, 3, row0=row0, gcols=n) if acc
          else g.SlicedMatrix(ctx, m, n, torch.empty((e, m, g.words_for(n)), dtype=torch.int64, device=dev)))
     torch.cuda.synchronize()
 
     out = [C]
 
-    def step():
+    def step_compute():
+        """B resident on every GPU: operand combinations + the fused product."""
         if acc:
             g.addmul(C, A, B, backend=backend)
         else:
             out[0] = g.karatsuba_mul(A, B, backend=backend)
         return _lib.last_launch_count()
 
+    def step_comm():
+        """The data-path collective included: B broadcast from rank 0 in column parts on a side
+        stream (NCCL over NVLink), each part multiplied as it arrives (gf2e_slice_mul_parts)."""
+        pieces, events = gdist.broadcast_parts(B.planes if rank == 0 else None, (e, k, g.words_for(n)), bounds,
+                                               src=0, device=dev, src_parts=src_parts)
+        if acc:
+            gdist.mul_parts(e, ctx.f, A.planes, pieces, events, bounds, k, n, C.planes, True, backend)
+        else:
+            Cn = torch.empty((e, m, g.words_for(n)), dtype=torch.int64, device=dev)
+            gdist.mul_parts(e, ctx.f, A.planes, pieces, events, bounds, k, n, Cn, False, backend)
+            out[0] = g.SlicedMatrix(ctx, m, n, Cn)
+        return _lib.last_launch_count()
+
+    # under torchrun (any N, including 1) the headline step includes the B broadcast
+    step = step_comm if use_pg else step_compute
+
+    def timed(fn, nsteps, sample_clocks=False):
+        """max over ranks of the per-step ms (CUDA events on the launching stream, barrier +
+        sync on both sides) and of the product-kernel ms per step; launches per step."""
+        sampler = ClockSampler(local) if sample_clocks else None
+        if sampler:
+            sampler.start()
+        _lib.profile_enable(True)
+        _lib.profile_read()
+        if use_pg:
+            dist.barrier()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(st)
+        nl = 0
+        for _ in range(nsteps):
+            nl += fn()
+        ev1.record(st)
+        torch.cuda.synchronize()
+        if use_pg:
+            dist.barrier()
+        clk = sampler.stop() if sampler else None
+        pms, _ = _lib.profile_read()
+        kname = _lib.last_product_kernel()
+        _lib.profile_enable(False)
+        t = torch.tensor([ev0.elapsed_time(ev1) / nsteps, pms / nsteps], dtype=torch.float64, device=dev)
+        if use_pg:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0]), float(t[1]), nl, clk, kname
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-
-    # ---- timed region: device events, barrier + sync on both sides, max over ranks ----
-    sampler = ClockSampler(local)
-    sampler.start()
-    _lib.profile_enable(True)
-    _lib.profile_read()
-    if use_pg:
-        dist.barrier()
-    torch.cuda.synchronize()
-    st = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(st)
-    launches = 0
-    for _ in range(args.steps):
-        launches += step()
-    ev1.record(st)
-    torch.cuda.synchronize()
-    if use_pg:
-        dist.barrier()
-    clocks = sampler.stop()
-    prod_ms, prod_launches = _lib.profile_read()
-    kernel_name = _lib.last_product_kernel()
-    _lib.profile_enable(False)
-    ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms, prod_ms / max(prod_launches, 1)], dtype=torch.float64, device=dev)
-    if use_pg:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, prod_ms_max = float(t[0]), float(t[1])
+    ms_max, prod_ms_max, launches, clocks, kernel_name = timed(step, args.steps, sample_clocks=True)
     value = world * ops_rank / (ms_max * 1e-3) / 1e12
+    nsteps_done = args.warmup + args.steps
+    compute_only = None
+    if use_pg:
+        for _ in range(args.warmup):
+            step_compute()
+        c_ms, c_prod, _, _, _ = timed(step_compute, args.steps)
+        nsteps_done += args.warmup + args.steps
+        compute_only = {"value": round(world * ops_rank / (c_ms * 1e-3) / 1e12, 4), "ms_per_step": round(c_ms, 4),
+                        "kernel_ms": round(c_prod, 4),
+                        "what": "B resident on every GPU (broadcast before timing): combos + fused product only"}
 
     # parity sample of the timed result: C rows [0, prow) of this rank's block (C0 ^ A.B for
     # addmul: one more untimed step when the step count left C at C0), compared on rank 0
     # with the oracle rows computed for cpu_baseline
     prow = min(m, args.cpu_rows or (256 if k * n >= 16384 * 16384 else min(m, 1024)))
-    if acc and (args.warmup + args.steps) % 2 == 0:
-        step()
+    if acc and nsteps_done % 2 == 0:
+        step_compute()
     dev_rows = out[0].planes[:, :prow].cpu().numpy().view("uint64").copy()
     del out
 
     # ---- e2e through the public host-buffer API (gf2e_mzed_mul_host), per step: H2D of packed A
-    #      and B from pinned host memory, slice, combos, product, cling, D2H of packed C; the
-    #      library overlaps copies of one row chunk with the kernels of another.  Timed by CUDA
-    #      events inside the call (first H2D -> last D2H), max over ranks. ----
+    #      from pinned host memory, slice, combos, product, cling, D2H of packed C; the library
+    #      overlaps copies of one row chunk with the kernels of another.  N = 1: B is uploaded
+    #      by the same call (in column parts, overlapped).  torchrun: rank 0 uploads packed B once,
+    #      NCCL broadcasts it, and every rank runs the call with B already on its GPU.  Timed by
+    #      CUDA events (N = 1: inside the call, first H2D -> last D2H; torchrun: from rank 0's B
+    #      upload to the call's return), max over ranks. ----
     e2e = None
     if not args.no_e2e:
         import numpy as np
@@ -274,20 +310,36 @@ def run_ours(args):
         Ap = g.cling(A)
         Bp = g.cling(B)
         hA = torch.empty(tuple(Ap.storage.words.shape), dtype=torch.int64, pin_memory=True)
-        hB = torch.empty(tuple(Bp.storage.words.shape), dtype=torch.int64, pin_memory=True)
         hA.copy_(Ap.storage.words)
-        hB.copy_(Bp.storage.words)
+        hB = torch.empty(tuple(Bp.storage.words.shape), dtype=torch.int64, pin_memory=rank == 0)
+        if rank == 0:
+            hB.copy_(Bp.storage.words)
         wpc = g.words_for(n * g.pack_width(e))
         hC = torch.empty((m, wpc), dtype=torch.int64, pin_memory=True)
         if acc:  # C0 again (the device C above holds C0 ^ A.B)
             hC.copy_(g.cling(g.SlicedMatrix.random(ctx, m, n, 3, row0=row0, gcols=n)).storage.words)
         del Ap, Bp
         nA, nB, nC = (t.numpy().view(np.uint64) for t in (hA, hB, hC))
+        dB = torch.empty(tuple(hB.shape), dtype=torch.int64, device=dev) if use_pg else None
+
+        def e2e_call(bwords):
+            if acc:
+                return g.karatsuba_mul_packed_host(ctx, nA, k, bwords, n, C_words=nC, chunk_rows=args.chunk_rows)[1]
+            return g.karatsuba_mul_packed_host(ctx, nA, k, bwords, n, out=nC, chunk_rows=args.chunk_rows)[1]
 
         def e2e_step():
-            if acc:
-                return g.karatsuba_mul_packed_host(ctx, nA, k, nB, n, C_words=nC, chunk_rows=args.chunk_rows)[1]
-            return g.karatsuba_mul_packed_host(ctx, nA, k, nB, n, out=nC, chunk_rows=args.chunk_rows)[1]
+            if not use_pg:
+                return e2e_call(nB)
+            st = torch.cuda.current_stream()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(st)
+            if rank == 0:
+                dB.copy_(hB, non_blocking=True)
+            gdist.broadcast_planes(dB, src=0)
+            e2e_call(dB)
+            ev1.record(st)
+            ev1.synchronize()
+            return ev0.elapsed_time(ev1)
 
         e2e_warm = max(1, args.warmup)
         for _ in range(e2e_warm):
@@ -301,11 +353,14 @@ def run_ours(args):
         te = torch.tensor([sum(ms_list) / len(ms_list)], dtype=torch.float64, device=dev)
         if use_pg:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        # whole-job bytes per step: every rank's A (and C0 / C) rows, B once
         e2e = {"value": round(world * ops_rank / (float(te[0]) * 1e-3) / 1e12, 4), "unit": "Tbit-op/s",
-               "h2d_bytes_per_step": int(hA.numel() * 8 + hB.numel() * 8 + (hC.numel() * 8 if acc else 0)),
-               "d2h_bytes_per_step": int(hC.numel() * 8), "ms_per_step": round(float(te[0]), 3),
-               "path": "gf2e_mzed_mul_host: pinned packed A,B -> H2D -> slice -> combos -> product -> cling -> D2H, "
-                       "row chunks pipelined on 4 streams"}
+               "h2d_bytes_per_step": int(world * (hA.numel() * 8 + (hC.numel() * 8 if acc else 0)) + hB.numel() * 8),
+               "d2h_bytes_per_step": int(world * hC.numel() * 8), "ms_per_step": round(float(te[0]), 3),
+               "path": ("gf2e_mzed_mul_host: pinned packed A,B -> H2D -> slice -> combos -> product -> cling -> D2H, "
+                        "row chunks pipelined on 4 streams") if not use_pg else
+                       ("rank 0: pinned packed B -> H2D -> NCCL broadcast; every rank: gf2e_mzed_mul_host with B on "
+                        "its GPU (GF2E_B_DEVICE), pinned packed A rows -> H2D ... -> D2H of its C rows")}
 
     if rank != 0:
         if use_pg:
@@ -326,6 +381,7 @@ def run_ours(args):
         tc_peak = max(_lib.mma_peak(2, 20000)[0], _lib.mma_peak(1, 20000)[0])
         peak_basis = ("measured live: pure tcgen05.mma kind::i8 loop on all SMs (gf2e_mma_peak); "
                       f"for reference 2 x {pk_kind} cuBLAS bf16 = {2 * pk['bf16_tflops']:.1f}")
+    # per step: one launch (N = 1) or one per broadcast part with complete tiles (torchrun)
     achieved = ops_rank / (prod_ms_max * 1e-3) / 1e12  # GF(2) bit-ops == int8 tensor ops (1 MAC = 2 ops)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -343,6 +399,7 @@ def run_ours(args):
                    "gf2_products": K, "backend": backend or "tc", "parallelism": f"C row-blocks x{world}",
                    "l2": "inputs larger than L2 (A planes + combos >> 126 MB)"},
         "time_s": round(ms_max / 1e3, 6),
+        "comm_included": bool(use_pg),
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(tc_peak, 1),
                      "unit": "TFLOP/s", "frac": round(achieved / tc_peak, 4), "traffic": traffic,
@@ -352,6 +409,11 @@ def run_ours(args):
         "clocks": clocks,
     }
 
+    if compute_only:
+        line["compute_only"] = compute_only
+        line["config"]["broadcast"] = (f"B ({e} planes, {e * k * g.words_for(n) * 8} bytes) from rank 0 in "
+                                       f"{len(bounds) - 1} column parts {bounds}, NCCL on a side stream, each "
+                                       "part multiplied as it arrives; included in value / ms_per_step")
     if e2e:
         line["e2e"] = e2e
     if not args.no_cpu_baseline:
@@ -388,6 +450,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunk-rows", type=int, default=0, help="row chunk of the host-buffer e2e call (0: library default)")
+    ap.add_argument("--bcast-parts", type=int, default=4, help="column parts of B's broadcast under torchrun")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo-shared-gpu"],
                     help="gloo-shared-gpu: functional multi-rank check with every rank on cuda:0 (no timing meaning)")
     args = ap.parse_args()

@@ -45,6 +45,8 @@ extern "C" {
 #define GF2E_TC_INT8 4u      /* tensor-core K4 forced to kind::i8 at every k                */
 #define GF2E_TC_FP4 8u       /* tensor-core K4 forced to kind::mxf4 at every k (paired form
                                 below k = 2048)                                             */
+#define GF2E_B_DEVICE 32u    /* gf2e_mzed_mul_host: B_host is a DEVICE pointer (B already
+                                resident, e.g. broadcast to this GPU by the multi-GPU path)  */
 #define GF2E_TC_RUN 16u      /* tensor-core K4 forced to the kind::mxf4 running-sum form
                                 (double-buffered accumulators, 256 x 192 tiles) at every k  */
 
@@ -160,7 +162,9 @@ int gf2e_slice_mul_parts(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, 
  * A (and C0) then stream through in chunks of `chunk_rows` rows (<= 0: a wave-aware plan
  * around 2048 rows) with the copies, operand preparation, products and copy-out of
  * consecutive chunks overlapped on four internal streams.  Device memory
- * comes from the library's own stream-ordered pool (gf2e_trim_pool).  *device_ms (optional) = CUDA-event time from the first
+ * comes from the library's own stream-ordered pool (gf2e_trim_pool).  flags: GF2E_ACCUMULATE,
+ * GF2E_B_DEVICE (B_host is a device pointer: no B upload; B must be complete before the call,
+ * which runs on its own streams).  *device_ms (optional) = CUDA-event time from the first
  * H2D to the last D2H.
  */
 int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_host, int64_t lda, const uint64_t *B_host,
@@ -275,9 +279,9 @@ int gf2e_profile_read(double *total_ms, int *launches);
  * fp4 exactness self-check.  The kind::mxf4 forms of the product assume exact fp32
  * accumulation of 0/1 products (measured, not architecturally guaranteed).  Before the first
  * fp4 product on a device the library compares every fp4 form with the int8 form (integer
- * arithmetic) on random and all-ones GF(2) planes, k up to 33024 (across the 32768-bit
- * accumulation chunk); on any mismatch fp4 is disabled on that device and every product uses
- * kind::i8.  This entry runs the check if it has not run (rerun != 0: again) and reports
+ * arithmetic) on random and all-ones GF(2) planes: plane products up to k = 33024 (across the
+ * 32768-bit accumulation chunk) and the running-sum form with the 9-product GF(16) schedule;
+ * on any mismatch fp4 is disabled on that device and every product uses kind::i8.  This entry runs the check if it has not run (rerun != 0: again) and reports
  * *ok = 1 (fp4 in use) or -1 (disabled).  inject_fault != 0 (tests) corrupts the fp4 results
  * of this check, so it must fail and disable fp4.
  */

@@ -21,6 +21,7 @@ BACKEND_M4RM = 2
 TC_INT8 = 4
 TC_FP4 = 8
 TC_RUN = 16
+B_DEVICE = 32
 
 _I64 = ctypes.c_int64
 _U64 = ctypes.c_uint64

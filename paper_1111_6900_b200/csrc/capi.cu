@@ -297,10 +297,13 @@ struct Layout {
 int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 
 // Tensor-core form: fp4 (kind::mxf4, 2x the int8 rate) unless forced to int8.  Below k = 2048
-// the single fp4 accumulator's per-product hand-off would dominate, so short inner dimensions
-// use the paired fp4 form (two products per TMEM drain) or int8 (double-buffered TMEM).
+// the single-accumulator fp4 forms' per-product hand-off would dominate, so short inner
+// dimensions take the running-sum form (product_run.cu) while its sums stay exact, else int8;
+// backend "tc_fp4" forces the paired form there.
 constexpr int64_t kFp4MinK = 2048;
-constexpr int kSmallKForm = kFormI8;
+// short k: the running-sum fp4 form (double-buffered accumulators, no per-product
+// re-initialisation; config 4 e=8: 17.7 ms against 21.5 ms for int8, profiles/r02)
+constexpr int kSmallKForm = kFormFp4Run;
 constexpr int64_t kFp4LongK = 8192;  // 8 expander / 4 epilogue warps pay off for long accumulations
 // fp4 exactness self-check state per device: 0 not run, 1 passed, -1 failed (fp4 disabled)
 int g_fp4_state[kMaxDevices] = {};
@@ -323,7 +326,7 @@ int tc_form(uint32_t flags, int64_t k, int nprod = kMaxProducts) {
     if (k >= kFp4LongK) return kFormFp4Long;
     if (k >= kFp4MinK) return kFormFp4;
     if (flags & GF2E_TC_FP4) return kFormFp4Pair;
-    return kSmallKForm;
+    return run_ok(nprod, k) ? kSmallKForm : kFormI8;
 }
 const char *form_name(int form) {
     return form == kFormFp4Pair                            ? "k_product_tc2<fp4x2>"
@@ -441,10 +444,13 @@ bool g_fp4_inject = false;  // test hook: corrupt the fp4 results of the next ch
 int fp4_probe_run(bool inject, int *ok) {
     *ok = 0;
     const int64_t m = 256, n = 256;
+    // plane products (one GF(2) product) for the single-accumulator forms; the running-sum form
+    // with the GF(16) schedule (9 products, 4 input planes: several products per accumulator)
     const struct {
         int form;
         int64_t k;
-    } cases[] = {{kFormFp4Long, 33024}, {kFormFp4, 4096}, {kFormFp4Pair, 1024}};
+        int e;
+    } cases[] = {{kFormFp4Long, 33024, 1}, {kFormFp4, 4096, 1}, {kFormFp4Pair, 1024, 1}, {kFormFp4Run, 1792, 4}};
     cudaStream_t st = nullptr;
     CKH(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
     struct StreamGuard {
@@ -454,36 +460,37 @@ int fp4_probe_run(bool inject, int *ok) {
             cudaStreamDestroy(s);
         }
     } sg{st};
-    const Sched ks = plane_sched();
-    const int64_t kmax = 33024, nw = n / 64;
-    const int64_t ws_bytes = layout_for(1, m, kmax, n, 0, kFormAny).total;
-    DevTmpAny A((size_t)m * (kmax / 64) * 8, st), B((size_t)kmax * nw * 8, st), C8((size_t)m * nw * 8, st),
-        C4((size_t)m * nw * 8, st), ws((size_t)ws_bytes, st);
+    const int64_t kmax = 33024, nw = n / 64, emax = 4;
+    const int64_t ws_bytes = layout_for(9, m, kmax, n, 0, kFormAny).total;
+    DevTmpAny A((size_t)emax * m * (kmax / 64) * 8, st), B((size_t)emax * kmax * nw * 8, st),
+        C8((size_t)emax * m * nw * 8, st), C4((size_t)emax * m * nw * 8, st), ws((size_t)ws_bytes, st);
     if (!A.p || !B.p || !C8.p || !C4.p || !ws.p) return fail(GF2E_ENOMEM, "out of device memory (fp4 self-check)");
     uint64_t *a = static_cast<uint64_t *>(A.p), *b = static_cast<uint64_t *>(B.p);
     uint64_t *c8 = static_cast<uint64_t *>(C8.p), *c4 = static_cast<uint64_t *>(C4.p);
-    std::vector<uint64_t> h8((size_t)m * nw), h4((size_t)m * nw);
+    std::vector<uint64_t> h8((size_t)emax * m * nw), h4((size_t)emax * m * nw);
     bool good = true;
     for (const auto &cs : cases) {
-        const int64_t kw = cs.k / 64;
+        const Sched ks = cs.e == 1 ? plane_sched() : to_kernel_sched(cs.e, get_schedule(cs.e, 0x13));
+        const int64_t kw = cs.k / 64, pa = m * kw, pb = cs.k * nw, pc = m * nw;
+        const size_t cw = (size_t)cs.e * m * nw;
         for (int ones = 0; ones < 2; ++ones) {
             if (ones) {
-                CKH(cudaMemsetAsync(a, 0xFF, (size_t)m * kw * 8, st), "cudaMemsetAsync");
-                CKH(cudaMemsetAsync(b, 0xFF, (size_t)cs.k * nw * 8, st), "cudaMemsetAsync");
+                CKH(cudaMemsetAsync(a, 0xFF, (size_t)cs.e * pa * 8, st), "cudaMemsetAsync");
+                CKH(cudaMemsetAsync(b, 0xFF, (size_t)cs.e * pb * 8, st), "cudaMemsetAsync");
             } else {
-                CKH(launch_random_words(m, cs.k, 0x5eed0 + (uint64_t)cs.k, a, kw, st), "random_words");
-                CKH(launch_random_words(cs.k, n, 0x5eed1 + (uint64_t)cs.k, b, nw, st), "random_words");
+                CKH(launch_random_words((int64_t)cs.e * m, cs.k, 0x5eed0 + (uint64_t)cs.k, a, kw, st), "random_words");
+                CKH(launch_random_words((int64_t)cs.e * cs.k, n, 0x5eed1 + (uint64_t)cs.k, b, nw, st), "random_words");
             }
-            if (int rc = run_product(ks, a, kw, 0, b, nw, 0, c8, nw, 0, m, cs.k, n, GF2E_TC_INT8, ws.p, ws_bytes, st,
-                                     kFormI8))
+            if (int rc = run_product(ks, a, kw, pa, b, nw, pb, c8, nw, pc, m, cs.k, n, GF2E_TC_INT8, ws.p, ws_bytes,
+                                     st, kFormI8))
                 return rc;
-            if (int rc = run_product(ks, a, kw, 0, b, nw, 0, c4, nw, 0, m, cs.k, n, 0, ws.p, ws_bytes, st, cs.form))
+            if (int rc = run_product(ks, a, kw, pa, b, nw, pb, c4, nw, pc, m, cs.k, n, 0, ws.p, ws_bytes, st, cs.form))
                 return rc;
-            CKH(cudaMemcpyAsync(h8.data(), c8, h8.size() * 8, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
-            CKH(cudaMemcpyAsync(h4.data(), c4, h4.size() * 8, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+            CKH(cudaMemcpyAsync(h8.data(), c8, cw * 8, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+            CKH(cudaMemcpyAsync(h4.data(), c4, cw * 8, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
             CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-            if (inject) h4[(size_t)cs.k % h4.size()] ^= 1;
-            if (std::memcmp(h8.data(), h4.data(), h8.size() * 8) != 0) good = false;
+            if (inject) h4[(size_t)cs.k % cw] ^= 1;
+            if (std::memcmp(h8.data(), h4.data(), cw * 8) != 0) good = false;
         }
     }
     *ok = good ? 1 : -1;
@@ -1268,7 +1275,9 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     g_products = 0;
     if (device_ms) *device_ms = 0;
     if (int rc = check_field(e, f)) return rc;
-    if (flags & ~GF2E_ACCUMULATE) return fail(GF2E_EINVAL, "gf2e_mzed_mul_host: unsupported flags 0x%x", flags);
+    if (flags & ~(GF2E_ACCUMULATE | GF2E_B_DEVICE))
+        return fail(GF2E_EINVAL, "gf2e_mzed_mul_host: unsupported flags 0x%x", flags);
+    const bool b_dev = (flags & GF2E_B_DEVICE) != 0;  // B already in device memory (e.g. broadcast)
     const bool acc = (flags & GF2E_ACCUMULATE) != 0;
     const int w = gf2e_pack_width(e);
     const int64_t wa = words_for(k * w), wb = words_for(n * w), nwk = words_for(k), nwn = words_for(n);
@@ -1312,7 +1321,13 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     CKH(cudaStreamCreateWithFlags(&P.sp, cudaStreamNonBlocking), "stream");
     Layout LB = layout_for(ks.nprod, chunk, k, n, 0, form);  // Ac sized for one chunk, Bt for all of B
     uint64_t *dBp, *dBs, *dBt, *dAc[2], *dAp[2], *dAs[2], *dCs[2], *dCp[2];
-    CKH(P.alloc(&dBp, k * wb * 8), "pool_alloc");
+    int64_t ldbd = wb;  // row stride of the device copy of B
+    if (b_dev) {
+        dBp = const_cast<uint64_t *>(B_h);
+        ldbd = ldb;
+    } else {
+        CKH(P.alloc(&dBp, k * wb * 8), "pool_alloc");
+    }
     CKH(P.alloc(&dBs, (int64_t)e * k * nwn * 8), "pool_alloc");
     CKH(P.alloc(&dBt, LB.b_bytes), "pool_alloc");
     for (int sl = 0; sl < nslots; ++sl) {
@@ -1355,8 +1370,10 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     tr.start(P.sh);
     auto h2d_bpart = [&](int p) -> int {
         const int64_t w0 = cb[p] * w / 64, w1 = p + 1 == nbp ? wb : cb[p + 1] * w / 64;
-        CKH(cudaMemcpy2DAsync(dBp + w0, wb * 8, B_h + w0, ldb * 8, (w1 - w0) * 8, k, cudaMemcpyHostToDevice, P.sh),
-            "H2D(B)");
+        if (!b_dev)
+            CKH(cudaMemcpy2DAsync(dBp + w0, wb * 8, B_h + w0, ldb * 8, (w1 - w0) * 8, k, cudaMemcpyHostToDevice,
+                                  P.sh),
+                "H2D(B)");
         CKH(cudaEventRecord(ev_bp[p], P.sh), "cudaEventRecord");
         tr.mark(P.sh, "h2d B", p);
         return GF2E_OK;
@@ -1405,7 +1422,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         CKH(cudaStreamWaitEvent(sp, ev_bp[p], 0), "cudaStreamWaitEvent");
         const int64_t c0 = cb[p], nc = cb[p + 1] - c0;
         const int64_t npad = (p + 1 == nbp ? LB.n_pad : cb[p + 1]) - c0;
-        CK(launch_slice(e, w, k, nc, dBp + c0 * w / 64, wb, dBs + c0 / 64, nwn, k * nwn, sp, words_for(nc)),
+        CK(launch_slice(e, w, k, nc, dBp + c0 * w / 64, ldbd, dBs + c0 / 64, nwn, k * nwn, sp, words_for(nc)),
            "slice(B)");
         CK(launch_combos_bt(ks, dBs + c0 / 64, nwn, k * nwn, k, nc, dBt + c0 * LB.kwords, LB.kwords, LB.b_pstride,
                             LB.kwords, npad / 64, fp4, sp, form_br(form)),

@@ -40,7 +40,7 @@ constexpr int BNH = BN / 2;           // B^T rows per CTA
 constexpr int KW = 4;                 // 64-bit words per row per stage (256 k-bits)
 constexpr int S = 3;                  // operand stages (A: 3 x 32 TMEM columns)
 constexpr int D = 8;                  // raw bit-tile ring
-constexpr int NEXP = 4, NEPI = 8;
+constexpr int NEXP = 4, NEPI = 8;  // epilogue: lane quarter x column half (96 columns, one TMEM round trip)
 constexpr int EPI_W0 = NEXP, MMA_WARP = NEXP + NEPI, LOAD_WARP = MMA_WARP + 1;
 constexpr int NTHREADS = (NEXP + NEPI + 2) * 32;
 constexpr int B_BYTES = BNH * 128;                     // expanded B^T stage (12 KiB)
@@ -53,12 +53,31 @@ static_assert(ATM0 + 32 * S <= SFA, "TMEM: A stages overlap the scale factors");
 // i.e. ceil(K/2) * k < 65536 (host: kRunMaxSum)
 constexpr uint32_t RUN_INIT = 0x47800000u;
 constexpr uint32_t SF_ONE = 0x7F7F7F7Fu;               // E8M0 1.0
-constexpr int CH = BN / 2 / 32;                        // 32-column chunks per epilogue thread
+constexpr int CH = BN / (NEPI / 4) / 32;               // 32-column chunks per epilogue thread
 constexpr int GROUP_M = 8;
 constexpr int BARS_BYTES = 1024;
-constexpr int SMEM_BYTES = S * B_BYTES + D * BITS_BYTES + BARS_BYTES + 1024;
+// epilogue staging (per CTA and tile): the E x 128 x 192-bit output words and their C0
+// epilogue staging (per CTA and tile): the E x 128 x 192-bit output words and their C0
+constexpr int STAGE_OUT_BYTES = kMaxE * BM * 24, STAGE_OLD_BYTES = kMaxE * BM * 24;
+constexpr int SMEM_BYTES = S * B_BYTES + D * BITS_BYTES + BARS_BYTES + STAGE_OUT_BYTES + STAGE_OLD_BYTES + 1024;
 static_assert(B_BYTES % 1024 == 0, "swizzle atoms need 1024-byte aligned stages");
 static_assert(SMEM_BYTES <= 232448, "shared memory");
+
+#ifndef GF2E_INSTR
+#define GF2E_INSTR 0
+#endif
+#if GF2E_INSTR
+// dev-only (-DGF2E_INSTR=1): per-CTA cycle counters of each role's waits and work
+__device__ unsigned long long g_instr_run[1024][32];
+#define TWR(acc, stmt)                                \
+    do {                                              \
+        const long long _t0 = clock64();              \
+        stmt;                                         \
+        acc += (unsigned long long)(clock64() - _t0); \
+    } while (0)
+#else
+#define TWR(acc, stmt) stmt
+#endif
 
 struct __align__(8) Bars {
     uint64_t full[S], empty[S], tfull[2], tempty[2], bfull[D], bempty[D];
@@ -86,6 +105,21 @@ __device__ __forceinline__ void st32_const(uint32_t taddr, uint32_t v) {
         : "memory");
 }
 __device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// bit 7 of the 32 pack::16b cells of v -> one word (bit 8b+g = column 4g+b, as
+// parity_word_packed), merged as a tree: 8 PRMT, 8 masks, 4 + 2 + 1 ORs, depth 4 instead of 8
+__device__ __forceinline__ uint32_t parity_word_tree(const uint32_t (&v)[16]) {
+    uint32_t w[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        asm("prmt.b32 %0, %1, %2, 0xECA8;" : "=r"(w[g]) : "r"(v[2 * g]), "r"(v[2 * g + 1]));
+        w[g] &= 0x01010101u << g;
+    }
+    return ((w[0] | w[1]) | (w[2] | w[3])) | ((w[4] | w[5]) | (w[6] | w[7]));
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // A row of one stage into this thread's TMEM lane: 32 columns, word i of chunk q = nibble
 // plane i of 32-bit word q (k-bit 32q + 4j + i <-> nibble j)
@@ -203,17 +237,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                 cur[3] = *reinterpret_cast<const uint4 *>(bs + BITS_A + BNH * 16);
             }
         };
+        unsigned long long i_empty = 0, i_bfull = 0, i_work = 0, i_sa = 0, i_sb = 0, i_sw = 0;
+        (void)i_sa, (void)i_sb, (void)i_sw;
+        const long long i_t0 = clock64();
+        (void)i_empty, (void)i_bfull, (void)i_work, (void)i_t0;
         if (total > 0) {
             mbar_wait(&bars->bfull[0], 0);
             load_bits(0);
         }
         for (int64_t it = 0; it < total; ++it) {
-            mbar_wait_sleep(&bars->empty[st], phase ^ 1, 32);
+            TWR(i_empty, mbar_wait_sleep(&bars->empty[st], phase ^ 1, 32));
+#if GF2E_INSTR
+            const long long i_w0 = clock64();
+#endif
             expand_a_tmem(tl + (uint32_t)(st * 32), cur[0], cur[1]);
+#if GF2E_INSTR
+            const long long i_w1 = clock64();
+#endif
             if (doB) expand_b_smem(stages + st * B_BYTES, p, cur[2], cur[3]);
+#if GF2E_INSTR
+            const long long i_w2 = clock64();
+#endif
             wait_st();
             tc_fence_before();
             fence_proxy_async_smem();
+#if GF2E_INSTR
+            const long long i_w3 = clock64();
+            i_work += (unsigned long long)(i_w3 - i_w0);
+            i_sa += (unsigned long long)(i_w1 - i_w0);
+            i_sb += (unsigned long long)(i_w2 - i_w1);
+            i_sw += (unsigned long long)(i_w3 - i_w2);
+#endif
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive_cluster(full_leader + (uint32_t)(st * 8));
@@ -224,7 +278,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                 bph ^= 1;
             }
             if (it + 1 < total) {
-                mbar_wait(&bars->bfull[slot], bph);
+                TWR(i_bfull, mbar_wait(&bars->bfull[slot], bph));
                 load_bits(slot);
             }
             if (++st == S) {
@@ -232,6 +286,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                 phase ^= 1;
             }
         }
+#if GF2E_INSTR
+        if (threadIdx.x == 0) {
+            g_instr_run[blockIdx.x][0] = i_empty;
+            g_instr_run[blockIdx.x][1] = i_bfull;
+            g_instr_run[blockIdx.x][2] = i_work;
+            g_instr_run[blockIdx.x][3] = (unsigned long long)(clock64() - i_t0);
+            g_instr_run[blockIdx.x][12] = i_sa;
+            g_instr_run[blockIdx.x][13] = i_sb;
+            g_instr_run[blockIdx.x][14] = i_sw;
+        }
+#endif
     } else if (warp == LOAD_WARP) {
         // ===================== bit-tile loader =====================
         const bool issuer = elect_one();
@@ -267,78 +332,152 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         __syncwarp();
     } else if (warp < MMA_WARP) {
         // ===================== epilogue =====================
+        // Per product: two TMEM round trips per warp (chunks 0+1, then 2; the tempty arrive
+        // after the second), parity words folded into E x 3 register words.  Per tile: the words
+        // go through shared memory (stage_out) and leave as coalesced 64-bit row segments; C0
+        // (addmul) is prefetched into shared memory with cp.async at the tile start by the
+        // thread that later XORs it in.
         const int ew = warp - EPI_W0;
-        const int q = warp & 3;  // TMEM lane quarter
-        const int h = ew >> 2;   // column half: tile columns [h*96, h*96+96)
-        const int row_local = (int)rank * BM + q * 32 + lane;
-        // 32-bit output words up to the end of the row's last 64-bit word: the bits past n in
-        // it are written as zero (C = A.B into uninitialised memory keeps tail bits zero)
-        const int64_t nw32 = 2 * words_for(a.n);
+        const int et = ew * 32 + lane;  // 0..255
+        const int q = warp & 3;         // TMEM lane quarter
+        const int h = ew >> 2;          // column half: tile columns [h*96, h*96+96)
+        const int r_cta = q * 32 + lane;  // this thread's accumulator row within the CTA's 128
+        const int64_t nw = words_for(a.n);
         const uint32_t tempty_leader = mapa(smem_u32(&bars->tempty[0]), 0);
         const uint32_t lq = (uint32_t)(q * 32) << 16;
-        uint32_t pc[CH], po[CH];  // previous parity words: current buffer / the other buffer
+        uint32_t *stage_out = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(bars) + BARS_BYTES);
+        uint64_t *stage_old = reinterpret_cast<uint64_t *>(stage_out + E * BM * 6);
+        const uint64_t *stage_out64 = reinterpret_cast<const uint64_t *>(stage_out);
+        constexpr int NOUT = E * BM * 3;  // 64-bit output words per CTA and tile
+        uint32_t pc[CH], po[CH];          // previous parity words: current buffer / the other buffer
 #pragma unroll
         for (int c = 0; c < CH; ++c) pc[c] = po[c] = 0;
         int64_t gp = 0;
+        unsigned long long i_tfull = 0, i_drain = 0, i_store = 0, i_e[5] = {0, 0, 0, 0, 0};
+        const long long i_t0 = clock64();
+        (void)i_tfull, (void)i_drain, (void)i_store, (void)i_t0, (void)i_e;
+        // 64-bit output word idx = (j * 128 + r) * 3 + w of the CTA's tile -> global address
+        auto out_ptr = [&](int idx, int64_t m0, int64_t n0w, bool &ok) -> uint64_t * {
+            const int j = idx / (BM * 3), rem = idx - j * (BM * 3), r = rem / 3, w = rem - r * 3;
+            const int64_t row = m0 + r, gw = n0w + w;
+            ok = row < a.m && gw < nw;
+            return a.C + j * a.c_pstride + row * a.ldc + gw;
+        };
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             const int64_t tile = cluster + ti * nclusters;
             int64_t tm, tn;
             tile_coords(tile, tiles_m, tiles_n, tm, tn);
+            const int64_t m0 = tm * (2 * BM) + (int64_t)rank * BM, n0w = tn * (BN / 64);
+            if (a.accumulate) {  // C0 of the words this thread writes out, into shared memory
+                for (int idx = et; idx < NOUT; idx += NEPI * 32) {
+                    bool ok;
+                    const uint64_t *src = out_ptr(idx, m0, n0w, ok);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(stage_old + idx)),
+                                 "l"(ok ? src : a.C), "r"(ok ? 8 : 0)
+                                 : "memory");
+                }
+                cp_async_commit();
+            }
             uint32_t acc[E][CH];
 #pragma unroll
             for (int j = 0; j < E; ++j)
 #pragma unroll
                 for (int c = 0; c < CH; ++c) acc[j][c] = 0;
-            // C0 of this thread's words, loaded now so the latency hides behind the products
-            const int64_t row = tm * (2 * BM) + row_local;
-            const int64_t w0 = tn * (BN / 32) + h * CH;  // first 32-bit word of this thread
-            const bool rowok = row < a.m;
-            uint32_t old[E][CH];
-#pragma unroll
-            for (int j = 0; j < E; ++j) {
-                const uint32_t *crow = reinterpret_cast<const uint32_t *>(a.C + j * a.c_pstride + row * a.ldc) + w0;
-#pragma unroll
-                for (int c = 0; c < CH; ++c) old[j][c] = (a.accumulate && rowok && w0 + c < nw32) ? crow[c] : 0u;
-            }
             for (int t = 0; t < s.nprod; ++t, ++gp) {
                 const int b = (int)(gp & 1);
                 const uint32_t mask = bars->outmask[t];
+                TWR(i_tfull, mbar_wait_sleep(&bars->tfull[b], (uint32_t)((gp >> 1) & 1), 20));
+#if GF2E_INSTR
+                const long long i_d0 = clock64();
+#endif
+                tc_fence_after();
+                const uint32_t ta = tmem + lq + (b ? ACC1 : 0u) + (uint32_t)(h * (CH * 32));
+                const bool last = t + 2 >= s.nprod;  // this buffer's last product in the tile
                 uint32_t sel[E];  // all-ones for the output planes this product folds into
 #pragma unroll
                 for (int j = 0; j < E; ++j) sel[j] = 0u - ((mask >> j) & 1u);
-                mbar_wait_sleep(&bars->tfull[b], (uint32_t)((gp >> 1) & 1), 20);
-                tc_fence_after();
-                const uint32_t ta = tmem + lq + (b ? ACC1 : 0u) + (uint32_t)(h * (BN / 2));
-                const bool last = t + 2 >= s.nprod;  // this buffer's last product in the tile
-#pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    uint32_t v[16];
-                    tmem_ld32_pack16(ta + (uint32_t)(c * 32), v);
-                    tmem_wait_ld();
-                    if (last) st32_const(ta + (uint32_t)(c * 32), RUN_INIT);
-                    // bit 0 of each cell = parity of the running sum; shifted to bit 7 of a byte
-                    const uint32_t w = parity_word_packed(v);
+                auto fold = [&](int c, uint32_t w) {
                     const uint32_t pw = w ^ pc[c];
                     pc[c] = po[c];
                     po[c] = last ? 0u : w;
 #pragma unroll
                     for (int j = 0; j < E; ++j) acc[j][c] ^= pw & sel[j];
+                };
+                static_assert(CH == 3, "three 32-column chunks per epilogue thread");
+                uint32_t v[2][16];
+                tmem_ld32_pack16(ta, v[0]);
+                tmem_ld32_pack16(ta + 32, v[1]);
+                tmem_wait_ld();
+#if GF2E_INSTR
+                const long long i_e1 = clock64();
+#endif
+                if (last) {
+                    st32_const(ta, RUN_INIT);
+                    st32_const(ta + 32, RUN_INIT);
                 }
-                if (last) wait_st();
+                const uint32_t w0 = parity_word_tree(v[0]);  // bit 7 of each cell
+                tmem_ld32_pack16(ta + 64, v[0]);
+                const uint32_t w1 = parity_word_tree(v[1]);
+                fold(0, w0);
+                fold(1, w1);
+#if GF2E_INSTR
+                const long long i_e2 = clock64();
+#endif
+                tmem_wait_ld();
+#if GF2E_INSTR
+                const long long i_e3 = clock64();
+#endif
+                if (last) {
+                    st32_const(ta + 64, RUN_INIT);
+                    wait_st();
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(b * 8));
+#if GF2E_INSTR
+                const long long i_e4 = clock64();
+#endif
+                fold(2, parity_word_tree(v[0]));
+#if GF2E_INSTR
+                i_e[0] += (unsigned long long)(i_e1 - i_d0);
+                i_e[1] += (unsigned long long)(i_e2 - i_e1);
+                i_e[2] += (unsigned long long)(i_e3 - i_e2);
+                i_e[3] += (unsigned long long)(i_e4 - i_e3);
+                i_e[4] += (unsigned long long)(clock64() - i_e4);
+#endif
+#if GF2E_INSTR
+                i_drain += (unsigned long long)(clock64() - i_d0);
+#endif
             }
-            if (rowok) {
+#if GF2E_INSTR
+            const long long i_s0 = clock64();
+#endif
+            // stage: row r_cta's 96 columns of each plane -> stage_out[j][r][h*3 .. h*3+2]
+            named_bar_sync(1, NEPI * 32);  // the previous tile's copy-out has read stage_out
 #pragma unroll
-                for (int j = 0; j < E; ++j) {
-                    uint32_t *crow = reinterpret_cast<uint32_t *>(a.C + j * a.c_pstride + row * a.ldc) + w0;
+            for (int j = 0; j < E; ++j)
 #pragma unroll
-                    for (int c = 0; c < CH; ++c)
-                        if (w0 + c < nw32) crow[c] = acc[j][c] ^ old[j][c];
-                }
+                for (int c = 0; c < CH; ++c) stage_out[(j * BM + r_cta) * 6 + h * CH + c] = acc[j][c];
+            if (a.accumulate) cp_async_wait<0>();
+            named_bar_sync(1, NEPI * 32);
+            for (int idx = et; idx < NOUT; idx += NEPI * 32) {
+                bool ok;
+                uint64_t *dst = out_ptr(idx, m0, n0w, ok);
+                if (ok) *dst = stage_out64[idx] ^ (a.accumulate ? stage_old[idx] : 0ull);
             }
+#if GF2E_INSTR
+            i_store += (unsigned long long)(clock64() - i_s0);
+#endif
         }
+#if GF2E_INSTR
+        if (lane == 0 && warp == EPI_W0) {
+            g_instr_run[blockIdx.x][4] = i_tfull;
+            g_instr_run[blockIdx.x][5] = i_drain;
+            g_instr_run[blockIdx.x][6] = i_store;
+            g_instr_run[blockIdx.x][7] = (unsigned long long)(clock64() - i_t0);
+            for (int i = 0; i < 5; ++i) g_instr_run[blockIdx.x][16 + i] = i_e[i];
+        }
+#endif
     } else if (warp == MMA_WARP && rank == 0) {
         // ===================== MMA issuer (leader CTA) =====================
         const bool issuer = elect_one();
@@ -347,14 +486,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         int st = 0;
         uint32_t phase = 0;
         int64_t gp = 0;
+        unsigned long long i_full = 0, i_tempty = 0;
+        const long long i_t0 = clock64();
+        (void)i_full, (void)i_tempty, (void)i_t0;
+#if GF2E_INSTR
+        unsigned long long i_g0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(i_g0));
+#endif
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             for (int t = 0; t < s.nprod; ++t, ++gp) {
                 const int b = (int)(gp & 1);
-                mbar_wait(&bars->tempty[b], (uint32_t)((gp >> 1) & 1) ^ 1);
+                TWR(i_tempty, mbar_wait(&bars->tempty[b], (uint32_t)((gp >> 1) & 1) ^ 1));
                 tc_fence_after();
                 const uint32_t dt = tmem + (b ? ACC1 : 0u);
                 for (int ks = 0; ks < nks; ++ks) {
-                    mbar_wait(&bars->full[st], phase);
+                    TWR(i_full, mbar_wait(&bars->full[st], phase));
                     tc_fence_after();
                     const uint32_t sb = st0 + (uint32_t)(st * B_BYTES);
                     if (issuer) {
@@ -375,6 +521,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
             }
         }
         __syncwarp();
+#if GF2E_INSTR
+        if (lane == 0) {
+            unsigned long long i_g1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(i_g1));
+            g_instr_run[blockIdx.x][8] = i_full;
+            g_instr_run[blockIdx.x][9] = i_tempty;
+            g_instr_run[blockIdx.x][10] = (unsigned long long)(clock64() - i_t0);
+            g_instr_run[blockIdx.x][11] = i_g1 - i_g0;
+        }
+#endif
     }
 
     tc_fence_before();
@@ -439,3 +595,9 @@ cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st)
 }
 
 }  // namespace gf2e
+
+#if GF2E_INSTR
+extern "C" int gf2e_debug_instr_run(unsigned long long *out, int nblocks) {
+    return (int)cudaMemcpyFromSymbol(out, gf2e::g_instr_run, sizeof(unsigned long long) * 32 * nblocks);
+}
+#endif

@@ -79,22 +79,26 @@ def broadcast_planes(planes: torch.Tensor, src: int = 0, group=None) -> torch.Te
     return planes
 
 
+def split_parts(B: torch.Tensor, bounds: list[int]) -> list[torch.Tensor]:
+    """Contiguous copies of B's column parts [bounds[p], bounds[p+1]) (word-aligned bounds)."""
+    return [B[:, :, b0 // 64:words_for(b1)].contiguous() for b0, b1 in zip(bounds, bounds[1:])]
+
+
 def broadcast_parts(B: torch.Tensor | None, shape: tuple[int, int, int], bounds: list[int], src: int = 0,
-                    group=None, stream=None, device=None):
+                    group=None, stream=None, device=None, src_parts: list[torch.Tensor] | None = None):
     """Broadcast B [e, k, words(n)] as contiguous column parts (one per `bounds` interval).
     On `src`, B holds the matrix; elsewhere it may be None.  Returns (parts, events): on CUDA
     the broadcasts are issued on `stream` (a side stream) and events[p] fires when part p has
-    arrived; on CPU (gloo) the calls are synchronous and events are None."""
+    arrived; on CPU (gloo) the calls are synchronous and events are None.  src_parts: the
+    source's parts already split (split_parts), so no copy is made on `src`."""
     e, k, _ = shape
     rank = dist.get_rank(group) if dist.is_initialized() else src
     dev = B.device if B is not None else (device or torch.device("cuda", torch.cuda.current_device()))
-    parts = []
-    for p in range(len(bounds) - 1):
-        w0, w1 = bounds[p] // 64, words_for(bounds[p + 1])
-        if rank == src:
-            parts.append(B[:, :, w0:w1].contiguous())
-        else:
-            parts.append(torch.empty((e, k, w1 - w0), dtype=torch.int64, device=dev))
+    if rank == src:
+        parts = src_parts if src_parts is not None else split_parts(B, bounds)
+    else:
+        parts = [torch.empty((e, k, words_for(b1) - b0 // 64), dtype=torch.int64, device=dev)
+                 for b0, b1 in zip(bounds, bounds[1:])]
     if dev.type != "cuda":
         for t in parts:
             broadcast_planes(t, src, group)

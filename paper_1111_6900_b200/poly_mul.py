@@ -206,8 +206,17 @@ def karatsuba_mul_packed_host(ctx: FieldCtx, A_words, k: int, B_words, n: int, C
 
     from .mat_packed import pack_width
 
+    import torch
+
     A = np.ascontiguousarray(A_words, dtype=np.uint64)
-    B = np.ascontiguousarray(B_words, dtype=np.uint64)
+    b_dev = isinstance(B_words, torch.Tensor) and B_words.is_cuda
+    if b_dev:  # B already on this GPU (e.g. broadcast by the multi-GPU path): no upload
+        if B_words.dtype != torch.int64 or B_words.dim() != 2 or not B_words.is_contiguous():
+            raise ValueError("a device B_words must be a contiguous 2-D int64 tensor of packed words")
+        B = B_words
+        torch.cuda.current_stream().synchronize()  # the call runs on its own streams
+    else:
+        B = np.ascontiguousarray(B_words, dtype=np.uint64)
     w = pack_width(ctx.e)
     wa, wb = words_for(k * w), words_for(n * w)
     if A.ndim != 2 or B.ndim != 2:
@@ -238,9 +247,10 @@ def karatsuba_mul_packed_host(ctx: FieldCtx, A_words, k: int, B_words, n: int, C
     else:
         C = np.empty((m, wb), dtype=np.uint64)
     ms = ctypes.c_double()
-    _lib.call("gf2e_mzed_mul_host", ctx.e, ctx.f, A.ctypes.data, A.shape[1], B.ctypes.data,
-              B.shape[1], C.ctypes.data, C.shape[1], m, k, n, _lib.ACCUMULATE if acc else 0, chunk_rows,
-              ctypes.byref(ms))
+    flags = (_lib.ACCUMULATE if acc else 0) | (_lib.B_DEVICE if b_dev else 0)
+    _lib.call("gf2e_mzed_mul_host", ctx.e, ctx.f, A.ctypes.data, A.shape[1],
+              B.data_ptr() if b_dev else B.ctypes.data, B.shape[1], C.ctypes.data, C.shape[1], m, k, n, flags,
+              chunk_rows, ctypes.byref(ms))
     _bump(counters, ctx)
     return C, ms.value
 

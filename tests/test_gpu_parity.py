@@ -301,8 +301,11 @@ def test_native_code_used(g):
     ctx = g.field_new(8)
     A = g.SlicedMatrix.random(ctx, 256, 256, 1)
     g.karatsuba_mul(A, A)
-    assert g._lib.last_product_kernel() == "k_product_tc2<i8>"  # k < 2048: int8 form
+    assert g._lib.last_product_kernel() == "k_product_run<fp4>"  # k < 2048: running-sum form
     assert g._lib.last_launch_count() == 3  # combos(A), combos(B^T), fused product
+    assert g._lib.last_gf2_products() == 27
+    g.karatsuba_mul(A, A, backend="tc_i8")
+    assert g._lib.last_product_kernel() == "k_product_tc2<i8>"
     B = g.SlicedMatrix.random(ctx, 4096, 256, 2)
     g.karatsuba_mul(g.SlicedMatrix.random(ctx, 256, 4096, 1), B)
     assert g._lib.last_product_kernel() == "k_product_tc2<fp4>"
