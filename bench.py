@@ -208,7 +208,11 @@ def run_ours(args):
         B = g.SlicedMatrix.random(ctx, k, n, 2)
     else:
         B = g.SlicedMatrix(ctx, k, n, torch.empty((e, k, g.words_for(n)), dtype=torch.int64, device=dev))
-    bounds = gdist.col_parts(n, args.bcast_parts)
+    flags = g.poly_mul._resolve_backend(backend) | (_lib.ACCUMULATE if acc else 0)
+    tile = int(_lib.load().gf2e_tile_cols(e, ctx.f, k, flags))
+    pairs = torch.cuda.get_device_properties(dev).multi_processor_count // 2
+    # first part = the smallest whole number of product waves >= n/8: no partial wave is added
+    bounds = gdist.col_parts(n, args.bcast_parts, tile=tile, rows=m, pairs=pairs)
     src_parts = gdist.split_parts(B.planes, bounds) if rank == 0 else None
     gdist.broadcast_planes(B.planes, src=0)  # a resident copy of B on every rank (compute-only line)
     C = (g.SlicedMatrix.random(ctx, m, n, 3, row0=row0, gcols=n) if acc
@@ -450,7 +454,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunk-rows", type=int, default=0, help="row chunk of the host-buffer e2e call (0: library default)")
-    ap.add_argument("--bcast-parts", type=int, default=4, help="column parts of B's broadcast under torchrun")
+    ap.add_argument("--bcast-parts", type=int, default=2, help="column parts of B's broadcast under torchrun")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo-shared-gpu"],
                     help="gloo-shared-gpu: functional multi-rank check with every rank on cuda:0 (no timing meaning)")
     args = ap.parse_args()

@@ -153,6 +153,13 @@ int gf2e_slice_mul_parts(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, 
                          int64_t workspace_bytes, void *stream);
 
 /*
+ * Columns of C per product tile (CTA pair) of the form a product with inner dimension k and
+ * these flags would use (256, or 192 for the short-k running-sum form) — the quantum for
+ * gf2e_slice_mul_parts bounds that keep every tile inside one part.  -1 on bad arguments.
+ */
+int64_t gf2e_tile_cols(int e, uint32_t f, int64_t k, uint32_t flags);
+
+/*
  * mzed_mul / mzed_addmul with HOST buffers/*
  * mzed_mul / mzed_addmul with HOST buffers — the end-to-end entry a numpy-based caller
  * (e.g. gf2elin itself) binds: karatsuba_mul_packed (poly_mul.py:275-278)

@@ -72,6 +72,7 @@ SIGNATURES = {
     "gf2e_dev_fp4_probe": (_INT, [_INT, _INT, _P, _P, _P, ctypes.POINTER(ctypes.c_double), _P]),
     "gf2e_mma_peak": (_INT, [_INT, _INT, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
     "gf2e_trim_pool": (_INT, [_I64]),
+    "gf2e_tile_cols": (_I64, [_INT, _U32, _I64, _U32]),
     "gf2e_fp4_selfcheck": (_INT, [_INT, _INT, ctypes.POINTER(_INT)]),
 }
 

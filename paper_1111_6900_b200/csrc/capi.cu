@@ -1023,6 +1023,13 @@ int gf2e_fp4_selfcheck(int rerun, int inject_fault, int *ok) {
     return GF2E_OK;
 }
 
+int64_t gf2e_tile_cols(int e, uint32_t f, int64_t k, uint32_t flags) {
+    g_err.clear();
+    if (check_field(e, f) || check_flags(flags)) return -1;
+    if (flags & GF2E_BACKEND_M4RM) return kM4BN;
+    return form_bn(tc_form(flags, k, (int)get_schedule(e, f).subsets.size()));
+}
+
 int gf2e_trim_pool(int64_t keep_bytes) {
     g_err.clear();
     int dev = 0;

@@ -21,6 +21,7 @@ the oracle — test infrastructure only).
 from __future__ import annotations
 
 import ctypes
+import math
 from typing import Callable
 
 import torch
@@ -54,18 +55,28 @@ def row_partition(m: int, world: int, align: int = ROW_ALIGN) -> list[tuple[int,
     return out
 
 
-def col_parts(n: int, parts: int, first_fraction: float = 0.125) -> list[int]:
-    """Column bounds of B's broadcast parts: a small first part (its transfer is the only one
-    not hidden behind products), the rest split evenly; interior bounds multiples of 768
-    (whole 256- and 192-column product tiles, so no tile waits for two parts)."""
-    q = 768
-    if parts <= 1 or n <= 2 * q:
+def col_parts(n: int, parts: int, first_fraction: float = 0.125, tile: int = 768, rows: int | None = None,
+              pairs: int | None = None) -> list[int]:
+    """Column bounds of B's broadcast parts.  The first part is small (its transfer is the only
+    one not hidden behind products); interior bounds are multiples of `tile` (whole product
+    tiles, so no tile waits for two parts; 768 suits both the 256- and the 192-column forms).
+    With `rows` (this rank's rows of C) and `pairs` (CTA pairs of the GPU) the first part is the
+    smallest whole number of waves of tiles, so splitting the product costs no partial wave."""
+    if parts <= 1 or n <= 2 * tile:
         return [0, n]
-    first = max(q, int(n * first_fraction) // q * q)
+    first = max(tile, int(n * first_fraction) // tile * tile)
+    if rows and pairs:
+        rt = -(-rows // 256)
+        step = pairs // math.gcd(rt, pairs)  # column tiles per whole wave
+        c = step
+        while c * tile < int(n * first_fraction):
+            c += step
+        if c * tile < n:
+            first = c * tile
     bounds = [0, first]
     rest = n - first
     for p in range(1, parts - 1):
-        b = first + -(-rest * p // (parts - 1) // q) * q
+        b = first + -(-rest * p // (parts - 1) // tile) * tile
         if bounds[-1] < b < n:
             bounds.append(b)
     bounds.append(n)

@@ -83,10 +83,10 @@ def _ref_ple_calls(m: int, n: int, c0: int, pivots: np.ndarray, cx: int) -> int:
     return calls
 
 
-def _account(counters: MulCounters | None, ctx, calls: int) -> None:
+def _account(counters: MulCounters | None, ctx, calls: int, device: int) -> None:
     from .poly_mul import _bump
 
-    _bump(counters, ctx, calls, device_products=_lib.last_gf2_products())
+    _bump(counters, ctx, calls, device_products=device)
 
 
 def _check(T: PackedMatrix, B: PackedMatrix) -> None:
@@ -124,9 +124,11 @@ def _trsm_packed(T: PackedMatrix, B: PackedMatrix, upper: bool, unit_diag: bool,
     if T.nrows == 0 or B.ncols == 0:
         return
     Bs = slice_packed(B)
-    trsm_sliced(slice_packed(T), Bs, upper, unit_diag)
+    Ts = slice_packed(T)
+    trsm_sliced(Ts, Bs, upper, unit_diag)
+    device = _lib.last_gf2_products()  # before cling (every library call resets it)
     cling(Bs, out=B)
-    _account(counters, T.ctx, _ref_trsm_calls(T.nrows, B.ncols, _crossover(crossover)))
+    _account(counters, T.ctx, _ref_trsm_calls(T.nrows, B.ncols, _crossover(crossover)), device)
 
 
 def trsm_upper_left(U: PackedMatrix, B: PackedMatrix, crossover: int | None = None,
