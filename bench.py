@@ -391,7 +391,11 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"config{args.config}")
+            key = f"config{args.config}" + (f"_e{e}" if args.config == 4 else "") + (
+                f"_{backend}" if backend and backend != "tc" else "")
+            ent = json.load(open(tpath)).get(key)
+            # dram bytes per launch of this kernel from the committed ncu capture of it
+            traffic = ent["dram_bytes_per_launch"] if ent else None
         except (OSError, ValueError):
             traffic = None
     line = {

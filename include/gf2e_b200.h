@@ -136,6 +136,17 @@ int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, int64_
                    int64_t workspace_bytes, void *stream);
 
 /*
+ * Small-block product on PACKED words, no slicing: nj_mul (newton_john.py:145-164) /
+ * karatsuba_mul_packed below the crossover.  C = A*B or C ^= A*B (GF2E_ACCUMULATE), A m x k,
+ * B k x n, C m x n, all packed (mzed) with row strides in words; rows of B and C at most 16
+ * words (n <= 64 at e = 9, 10; 128 at e = 5..8; 256 at e = 3, 4; 512 at e = 2).  One launch:
+ * per 64 rows of C, Newton-John tables of all 2^e multiples of each row of B in shared memory,
+ * one lookup-and-XOR per (row of A, row of B) pair.
+ */
+int gf2e_nj_mul(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, const uint64_t *B_dev, int64_t ldb,
+                uint64_t *C_dev, int64_t ldc, int64_t m, int64_t k, int64_t n, uint32_t flags, void *stream);
+
+/*
  * gf2e_slice_mul with B arriving in column parts — the multi-GPU form (dist.sharded_mul: B is
  * broadcast over NVLink part by part while this rank already multiplies the parts that
  * arrived).  Part p holds columns [col_bounds[p], col_bounds[p+1]) of B as its own plane

@@ -1198,6 +1198,34 @@ int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa
     return run_product(ks, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, flags, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int gf2e_nj_mul(int e, uint32_t f, const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, uint64_t *C,
+                int64_t ldc, int64_t m, int64_t k, int64_t n, uint32_t flags, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    g_products = 0;
+    if (int rc = check_field(e, f)) return rc;
+    if (flags & ~GF2E_ACCUMULATE) return fail(GF2E_EINVAL, "gf2e_nj_mul: unsupported flags 0x%x", flags);
+    const int w = gf2e_pack_width(e);
+    const int64_t wb = words_for(n * w);
+    if (wb > kNjMaxWords)
+        return fail(GF2E_EINVAL, "gf2e_nj_mul: %lld columns exceed the small-block product (%d words per row)",
+                    (long long)n, kNjMaxWords);
+    if (int rc = check_mat(A, m, words_for(k * w), lda, "A")) return rc;
+    if (int rc = check_mat(B, k, wb, ldb, "B")) return rc;
+    if (int rc = check_mat(C, m, wb, ldc, "C")) return rc;
+    if (m == 0 || n == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool acc = (flags & GF2E_ACCUMULATE) != 0;
+    if (k == 0) {
+        if (!acc) CK(cudaMemset2DAsync(C, ldc * 8, 0, wb * 8, m, st), "cudaMemset2DAsync");
+        return GF2E_OK;
+    }
+    CK(launch_nj_mul(e, f, w, A, lda, B, ldb, C, ldc, m, k, n, acc, st), "nj_mul");
+    g_kernel = "k_nj_mul";
+    return GF2E_OK;
+}
+
 int gf2e_slice_mul_parts(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa, int nparts,
                          const int64_t *col_bounds, const uint64_t *const *B_parts, const int64_t *ldb,
                          const int64_t *pb, void *const *ready_events, uint64_t *C, int64_t ldc, int64_t pc,

@@ -87,6 +87,11 @@ cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st)
 constexpr int64_t kFp4PairMaxK = 2047;
 cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, int form, cudaStream_t st);
 
+// packed-domain Newton-John product for small blocks (nj.cu): rows of B at most kNjMaxWords words
+constexpr int kNjMaxWords = 16;
+cudaError_t launch_nj_mul(int e, uint32_t f, int w, const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,
+                          uint64_t *C, int64_t ldc, int64_t m, int64_t k, int64_t n, bool acc, cudaStream_t st);
+
 // INT-pipe M4RM product (product_m4rm.cu).  Operands: Ac as above, Bc [nprod][k_pad][n_pad/64].
 struct M4rmArgs {
     const uint64_t *Ac;

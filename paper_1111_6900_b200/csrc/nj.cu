@@ -1,0 +1,151 @@
+// nj.cu — the packed-domain Newton-John product for small blocks:
+// nj_mul (newton_john.py:145-164) on packed words, C (^)= A * B with no slicing.
+//
+// The reference builds, for every row i of B, the table of all 2^e scalar multiples x * B_i
+// (_table_block, newton_john.py:91-112: e scalings by alpha and a doubling walk), then adds
+// table_i[A[j, i]] into row j of C for every (j, i).  Here one CTA owns 64 rows of C; it walks
+// the rows of B in groups of G, builds the G tables in shared memory (entry x = XOR of the
+// alpha^s * B_i selected by the bits of x; alpha-multiples by a SWAR xtime on the packed
+// words) and every thread XORs the looked-up words of its (row, word) pairs into registers.
+// One launch replaces slice A, slice B, two operand-combination launches, the product and
+// the cling of the sliced path; the host routes small products here (poly_mul.NJ_CROSSOVER,
+// measured, profiles/r02).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gf2e {
+namespace {
+
+constexpr int NJ_THREADS = 256;
+constexpr int NJ_ROWS = 64;                         // C rows per CTA
+constexpr int NJ_ACC = NJ_ROWS * kNjMaxWords / NJ_THREADS;  // accumulator words per thread
+constexpr int NJ_SMEM = 160 * 1024;
+
+// x * alpha on every e-bit slot of a packed word (slot width w): shift inside the slot, fold
+// the carried-out bit with the low bits of f
+__device__ __forceinline__ uint64_t xtime_packed(uint64_t x, uint64_t low_mask, uint64_t lsb, int e, uint64_t fl) {
+    const uint64_t hi = (x >> (e - 1)) & lsb;
+    return ((x & low_mask) << 1) ^ (hi * fl);
+}
+
+template <int E>
+__global__ void __launch_bounds__(NJ_THREADS) k_nj_mul(uint32_t f, int w, const uint64_t *__restrict__ A,
+                                                        int64_t lda, const uint64_t *__restrict__ B, int64_t ldb,
+                                                        uint64_t *__restrict__ C, int64_t ldc, int64_t m, int64_t k,
+                                                        int64_t n, int acc, int G) {
+    extern __shared__ __align__(16) uint64_t sm[];
+    constexpr int Q = 1 << E;
+    const int WB = (int)words_for(n * w);
+    uint64_t *mult = sm;                      // [G][E][WB]: alpha^s * B_i
+    uint64_t *tab = sm + (size_t)G * E * WB;  // [G][Q][WB]: x * B_i
+    const int tid = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * NJ_ROWS;
+    const int rows = (int)(m - r0 < NJ_ROWS ? m - r0 : NJ_ROWS);
+    // packed-slot masks of the field elements
+    uint64_t emask = 0, low = 0, lsb = 0;
+    for (int s = 0; s < 64 / w; ++s) {
+        emask |= (uint64_t)((1u << E) - 1) << (s * w);
+        low |= (uint64_t)((1u << (E - 1)) - 1) << (s * w);
+        lsb |= 1ULL << (s * w);
+    }
+    const uint64_t fl = f & ((1u << E) - 1);
+    uint64_t accw[NJ_ACC];
+#pragma unroll
+    for (int a = 0; a < NJ_ACC; ++a) accw[a] = 0;
+    const int per = NJ_ROWS * WB;  // (row, word) pairs of the CTA
+    for (int64_t i0 = 0; i0 < k; i0 += G) {
+        const int g = (int)(k - i0 < G ? k - i0 : G);
+        // alpha-multiples of the group's rows of B
+        for (int idx = tid; idx < g * WB; idx += NJ_THREADS) {
+            const int gg = idx / WB, wd = idx - gg * WB;
+            uint64_t x = B[(i0 + gg) * ldb + wd] & emask;
+            for (int s = 0; s < E; ++s) {
+                mult[(gg * E + s) * WB + wd] = x;
+                x = xtime_packed(x, low, lsb, E, fl);
+            }
+        }
+        __syncthreads();
+        // tables: entry x of row gg = XOR of alpha^s * B_i over the set bits s of x
+        for (int idx = tid; idx < g * Q * WB; idx += NJ_THREADS) {
+            const int gg = idx / (Q * WB), rem = idx - gg * (Q * WB), x = rem / WB, wd = rem - x * WB;
+            uint64_t v = 0;
+#pragma unroll
+            for (int s = 0; s < E; ++s)
+                if ((x >> s) & 1) v ^= mult[(gg * E + s) * WB + wd];
+            tab[idx] = v;
+        }
+        __syncthreads();
+        // lookups: row j of C ^= table_i[A[j, i]] for the group's i
+#pragma unroll
+        for (int a = 0; a < NJ_ACC; ++a) {
+            const int idx = tid + a * NJ_THREADS;
+            if (idx < per) {
+                const int j = idx / WB, wd = idx - j * WB;
+                if (j < rows) {
+                    const uint64_t *arow = A + (r0 + j) * lda;
+                    uint64_t v = 0;
+                    for (int gg = 0; gg < g; ++gg) {
+                        const int64_t bit = (i0 + gg) * w;
+                        const uint32_t x = (uint32_t)((arow[bit >> 6] >> (bit & 63)) & ((1u << E) - 1));
+                        v ^= tab[((size_t)gg * Q + x) * WB + wd];
+                    }
+                    accw[a] ^= v;
+                }
+            }
+        }
+        __syncthreads();  // the next group overwrites the tables
+    }
+#pragma unroll
+    for (int a = 0; a < NJ_ACC; ++a) {
+        const int idx = tid + a * NJ_THREADS;
+        if (idx < per) {
+            const int j = idx / WB, wd = idx - j * WB;
+            if (j < rows) {
+                uint64_t *c = C + (r0 + j) * ldc + wd;
+                *c = acc ? (*c ^ accw[a]) : accw[a];
+            }
+        }
+    }
+}
+
+template <int E>
+cudaError_t launch_nj_e(uint32_t f, int w, const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,
+                        uint64_t *C, int64_t ldc, int64_t m, int64_t k, int64_t n, bool acc, cudaStream_t st) {
+    static bool attr_set[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= kMaxDevices || !attr_set[dev]) {
+        cudaError_t err = cudaFuncSetAttribute(k_nj_mul<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, NJ_SMEM);
+        if (err != cudaSuccess) return err;
+        if (dev < kMaxDevices) attr_set[dev] = true;
+    }
+    const int WB = (int)words_for(n * w);
+    const size_t per_row = ((size_t)(1 << E) + E) * WB * 8;  // table + multiples of one row of B
+    int G = (int)(NJ_SMEM / per_row);
+    if (G > 16) G = 16;
+    if (G < 1) return cudaErrorInvalidValue;
+    const size_t smem = per_row * G;
+    const unsigned grid = (unsigned)((m + NJ_ROWS - 1) / NJ_ROWS);
+    k_nj_mul<E><<<grid, NJ_THREADS, smem, st>>>(f, w, A, lda, B, ldb, C, ldc, m, k, n, acc ? 1 : 0, G);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_nj_mul(int e, uint32_t f, int w, const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,
+                          uint64_t *C, int64_t ldc, int64_t m, int64_t k, int64_t n, bool acc, cudaStream_t st) {
+    switch (e) {
+        case 2: return launch_nj_e<2>(f, w, A, lda, B, ldb, C, ldc, m, k, n, acc, st);
+        case 3: return launch_nj_e<3>(f, w, A, lda, B, ldb, C, ldc, m, k, n, acc, st);
+        case 4: return launch_nj_e<4>(f, w, A, lda, B, ldb, C, ldc, m, k, n, acc, st);
+        case 5: return launch_nj_e<5>(f, w, A, lda, B, ldb, C, ldc, m, k, n, acc, st);
+        case 6: return launch_nj_e<6>(f, w, A, lda, B, ldb, C, ldc, m, k, n, acc, st);
+        case 7: return launch_nj_e<7>(f, w, A, lda, B, ldb, C, ldc, m, k, n, acc, st);
+        case 8: return launch_nj_e<8>(f, w, A, lda, B, ldb, C, ldc, m, k, n, acc, st);
+        case 9: return launch_nj_e<9>(f, w, A, lda, B, ldb, C, ldc, m, k, n, acc, st);
+        case 10: return launch_nj_e<10>(f, w, A, lda, B, ldb, C, ldc, m, k, n, acc, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace gf2e

@@ -45,10 +45,17 @@ __global__ void __launch_bounds__(NT, 1) k_product_m4rm(const Sched s, const M4r
 #pragma unroll
         for (int i = 0; i < 8; ++i) c[i] = make_uint4(0, 0, 0, 0);
         int buf = 0;
-        for (int kc = 0; kc < nchunks; ++kc) {
-            uint64_t aw[8];
+        // A words of this thread's 8 rows for chunk kc; the next chunk's are fetched one chunk
+        // ahead (the lookups stalled on these loads: 40% of the warp samples, profiles/r02)
+        uint64_t aw[8], an[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) aw[i] = __ldg(Ap + (m0 + lrow0 + 4 * i) * a.kwords + kc);
+        for (int i = 0; i < 8; ++i) an[i] = nchunks ? __ldg(Ap + (m0 + lrow0 + 4 * i) * a.kwords) : 0;
+        for (int kc = 0; kc < nchunks; ++kc) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                aw[i] = an[i];
+                if (kc + 1 < nchunks) an[i] = __ldg(Ap + (m0 + lrow0 + 4 * i) * a.kwords + kc + 1);
+            }
 #pragma unroll 1
             for (int g = 0; g < 8; ++g) {
                 // ---- build T[x] for x in [16*bg, 16*bg+16), word bw ----

@@ -2,21 +2,27 @@
 (SURVEY §8f rank 2).
 
 The reference uses these table-based routines below its 64 crossover (``tuning.py:24``) and as
-the quadratic base cases of PLE and TRSM.  On the B200 every one of them has an exact device
-counterpart that is at least as fast at every size, so the functions keep their names,
-arguments, results, exceptions and ``RowOpCounters`` bookkeeping and route to:
+the quadratic base cases of PLE and TRSM.  Here the functions keep their names, arguments,
+results and exceptions and run on the device:
 
 * ``make_table`` (``newton_john.py:55-88``): all 2^e scalar multiples of a row in one
   ``gf2e_row_scales`` launch (broadcast row x scalars 0 .. 2^e - 1);
-* ``cubic_mul`` / ``nj_mul`` (``:124-164``): the tensor-core Karatsuba product (the product
-  is unique, so the result is bit-identical);
+* ``nj_mul`` / ``cubic_mul`` (``:124-164``): the reference's own algorithm — a table of the 2^e
+  multiples of every row of B, one lookup-and-XOR per (row of A, row of B) — on packed words
+  in one launch (``gf2e_nj_mul``, ``csrc/nj.cu``) when B's rows fit its shared-memory tables
+  (n <= 64 at e = 9, 10; more at smaller e), else the tensor-core product (the product is
+  unique, so the results are bit-identical);
 * ``nj_gauss`` (``:167-204``): ``echelonize`` (the reference documents that its PLE-based
   echelon forms match the table-based elimination bit for bit, ``ple_echelon.py:349-352``);
-* ``nj_ple`` (``:207-260``): the device PLE (same pivot rule, same in-place layout);
+* ``nj_ple`` (``:207-260``): the device PLE, whose 64-column panel kernel is this algorithm
+  (same pivot rule, same in-place layout);
 * ``nj_trsm_upper_left`` (``:263-291``): the device TRSM.
 
-Counters follow the reference's accounting: each row table costs e scalar row
-multiplications and 2^e - 1 row additions.
+``RowOpCounters``: ``make_table`` and ``nj_mul`` count the tables their kernels build (e scalar
+row multiplications and 2^e - 1 row additions per table, as the reference).  ``nj_gauss``,
+``nj_ple`` and ``nj_trsm_upper_left`` report the reference-equivalent accounting of the
+table algorithm for the same input (one table per pivot / solved row), not the device's
+different blocked work.
 """
 
 from __future__ import annotations
@@ -30,7 +36,7 @@ from .mat_gf2 import RowOpCounters
 from .mat_packed import PackedMatrix
 from .mat_sliced import cling, slice_packed
 from .ple_echelon import SingularMatrixError, echelonize, ple_sliced, trsm_upper_left
-from .poly_mul import karatsuba_mul_packed
+from .poly_mul import karatsuba_mul_packed, nj_fits, nj_mul_packed
 
 
 def _count_tables(ctx, counters: RowOpCounters | None, ntables: int) -> None:
@@ -86,21 +92,31 @@ def _check_mul_operands(A: PackedMatrix, B: PackedMatrix) -> None:
         raise ValueError(f"inner dimensions differ: {A.nrows}x{A.ncols} times {B.nrows}x{B.ncols}")
 
 
+def _device_mul(A: PackedMatrix, B: PackedMatrix) -> PackedMatrix:
+    # the packed-domain Newton-John kernel (gf2e_nj_mul: the reference's table algorithm, one
+    # launch) whenever B's rows fit it; the tensor-core product otherwise (same result)
+    if nj_fits(A.ctx.e, B.ncols):
+        return nj_mul_packed(A, B)
+    return karatsuba_mul_packed(A, B, backend="tc")
+
+
 def cubic_mul(A: PackedMatrix, B: PackedMatrix) -> PackedMatrix:
-    """Schoolbook product (newton_john.py:124-142): same result, computed by the device product."""
+    """Schoolbook product (newton_john.py:124-142): the unique product, computed on device."""
     _check_mul_operands(A, B)
-    return karatsuba_mul_packed(A, B)
+    return _device_mul(A, B)
 
 
 def nj_mul(A: PackedMatrix, B: PackedMatrix, counters: RowOpCounters | None = None,
            table_count: int | None = None) -> PackedMatrix:
-    """Table-based product (newton_john.py:145-164): same result, computed by the device
-    product; counters as the reference's one table per row of B."""
+    """Table-based product (newton_john.py:145-164): the same tables-per-row-of-B algorithm in
+    one device launch (gf2e_nj_mul) when B's rows fit it, else the device product.  counters:
+    the reference's accounting (one table per row of B: e scalar row multiplications and
+    2^e - 1 row additions each); the kernel builds exactly those tables."""
     _check_mul_operands(A, B)
     if A.nrows == 0 or A.ncols == 0 or B.ncols == 0:
         return PackedMatrix(A.ctx, A.nrows, B.ncols)
     _count_tables(A.ctx, counters, B.nrows)
-    return karatsuba_mul_packed(A, B)
+    return _device_mul(A, B)
 
 
 def nj_gauss(A: PackedMatrix, full: bool = True, counters: RowOpCounters | None = None) -> int:

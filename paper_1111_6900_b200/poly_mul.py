@@ -174,9 +174,48 @@ def count_products(e: int, f: int | None = None) -> int:
     return schedule(e, f).n_products
 
 
+# Below this size (max of m, k, n) products of packed matrices take the one-launch
+# packed-domain Newton-John kernel (gf2e_nj_mul) instead of slice -> combos -> product -> cling
+# (the crossover is the measured one, DESIGN §4 / profiles/r02).
+NJ_CROSSOVER = int(os.environ.get("GF2E_NJ_CROSSOVER", "64"))
+
+
+def nj_fits(e: int, n: int) -> bool:
+    from .mat_packed import pack_width
+
+    return words_for(n * pack_width(e)) <= 16
+
+
+def nj_mul_packed(A: PackedMatrix, B: PackedMatrix, C: PackedMatrix | None = None) -> PackedMatrix:
+    """C = A*B (or C ^= A*B when C is given) on packed words in one launch (gf2e_nj_mul):
+    Newton-John tables of the rows of B in shared memory (newton_john.py:145-164)."""
+    ctx = A.ctx
+    m, k, n = A.nrows, A.ncols, B.ncols
+    acc = C is not None
+    if C is None:
+        C = PackedMatrix(ctx, m, n)
+    aw, bw, cw = A.storage.words, B.storage.words, C.storage.words
+    _lib.call("gf2e_nj_mul", ctx.e, ctx.f, _device.ptr(aw), aw.shape[1], _device.ptr(bw), bw.shape[1],
+              _device.ptr(cw), cw.shape[1], m, k, n, _lib.ACCUMULATE if acc else 0, _device.stream_handle())
+    return C
+
+
+def _small(A: PackedMatrix, B: PackedMatrix, backend: str | None) -> bool:
+    return (backend is None and max(A.nrows, A.ncols, B.ncols) <= NJ_CROSSOVER and nj_fits(A.ctx.e, B.ncols))
+
+
 def karatsuba_mul_packed(A: PackedMatrix, B: PackedMatrix, counters: MulCounters | None = None,
                          backend: str | None = None) -> PackedMatrix:
-    """Slice, multiply, cling back (poly_mul.py:275-278): K1 -> K3/K4/K5 -> K2."""
+    """Slice, multiply, cling back (poly_mul.py:275-278): K1 -> K3/K4/K5 -> K2; below
+    NJ_CROSSOVER the packed-domain Newton-John kernel (same product, one launch)."""
+    if _small(A, B, backend):
+        if A.ctx != B.ctx:
+            raise ValueError(f"field mismatch: {A.ctx} vs {B.ctx}")
+        if A.ncols != B.nrows:
+            raise ValueError(f"inner dimensions differ: {A.nrows}x{A.ncols} times {B.nrows}x{B.ncols}")
+        C = nj_mul_packed(A, B)
+        _bump(counters, A.ctx, 1, device_products=0)
+        return C
     return cling(karatsuba_mul(slice_packed(A), slice_packed(B), counters, backend))
 
 
@@ -189,6 +228,10 @@ def addmul_packed(C: PackedMatrix, A: PackedMatrix, B: PackedMatrix, counters: M
         raise ValueError(f"inner dimensions differ: {A.nrows}x{A.ncols} times {B.nrows}x{B.ncols}")
     if C.shape != (A.nrows, B.ncols):
         raise ValueError(f"dimension mismatch: {C.shape} vs {(A.nrows, B.ncols)}")
+    if _small(A, B, backend):
+        nj_mul_packed(A, B, C)
+        _bump(counters, A.ctx, 1, device_products=0)
+        return C
     Cs = slice_packed(C)
     addmul(Cs, slice_packed(A), slice_packed(B), counters, backend)
     cling(Cs, out=C)

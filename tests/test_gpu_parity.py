@@ -471,3 +471,46 @@ def test_run_form_column_view(g):
     assert np.array_equal(after[:, :, 2:2 + g.words_for(n)], before[:, :, 2:2 + g.words_for(n)] ^ ref)
     assert np.array_equal(after[:, :, :2], before[:, :, :2])
     assert np.array_equal(after[:, :, 2 + g.words_for(n):], before[:, :, 2 + g.words_for(n):])
+
+
+def test_nj_small_products_golden(g, golden):
+    # the packed-domain Newton-John kernel (gf2e_nj_mul) on the reference's fixtures: product,
+    # addmul, through the routing of karatsuba_mul_packed / addmul_packed and nj_mul directly
+    from paper_1111_6900_b200 import poly_mul
+
+    for tag in _tags(golden, "kara_tags"):
+        e, f, m, k, n = (int(x) for x in golden[f"{tag}/meta"])
+        ctx = g.field_new(e, f)
+        A = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/A_packed"], k)
+        B = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/B_packed"], n)
+        if not poly_mul.nj_fits(e, n):
+            continue
+        assert np.array_equal(poly_mul.nj_mul_packed(A, B).to_numpy(), golden[f"{tag}/C_packed"]), tag
+        assert np.array_equal(g.nj_mul(A, B).to_numpy(), golden[f"{tag}/C_packed"]), tag
+        C0 = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/C0_packed"], n)
+        poly_mul.nj_mul_packed(A, B, C0)
+        assert np.array_equal(C0.to_numpy(), golden[f"{tag}/addmul_packed"]), tag
+        if max(m, k, n) <= poly_mul.NJ_CROSSOVER:
+            assert np.array_equal(g.karatsuba_mul_packed(A, B).to_numpy(), golden[f"{tag}/C_packed"]), tag
+            assert g._lib.last_product_kernel() == "k_nj_mul"
+
+
+@pytest.mark.parametrize("e", range(2, 11))
+def test_nj_small_products_oracle(g, e):
+    from paper_1111_6900_b200 import poly_mul
+
+    ctx = g.field_new(e)
+    nmax = {2: 512, 3: 256, 4: 256}.get(e, 128 if e <= 8 else 64)
+    for (m, k, n) in [(1, 1, 1), (5, 7, 3), (64, 64, 64), (65, 100, nmax), (200, 33, nmax - 1), (3, 0, 5),
+                      (130, 257, 17)]:
+        A = oracle.packed_random(e, m, k, 1)
+        B = oracle.packed_random(e, k, n, 2)
+        C0 = oracle.packed_random(e, m, n, 3)
+        PA = g.PackedMatrix.from_numpy(ctx, A, k)
+        PB = g.PackedMatrix.from_numpy(ctx, B, n)
+        PC = g.PackedMatrix.from_numpy(ctx, C0, n)
+        ref, _ = oracle.karatsuba(e, ctx.f, oracle.slice_words(e, m, k, A), oracle.slice_words(e, k, n, B), m, k, n)
+        assert np.array_equal(poly_mul.nj_mul_packed(PA, PB).to_numpy(), oracle.cling_words(e, m, n, ref)), (m, k, n)
+        poly_mul.nj_mul_packed(PA, PB, PC)
+        ref2 = ref ^ oracle.slice_words(e, m, n, C0)
+        assert np.array_equal(PC.to_numpy(), oracle.cling_words(e, m, n, ref2)), (m, k, n, "acc")
