@@ -28,13 +28,24 @@ __device__ __forceinline__ uint64_t xtime_packed(uint64_t x, uint64_t low_mask, 
     return ((x & low_mask) << 1) ^ (hi * fl);
 }
 
+// Tables per row of B: one of all 2^e multiples for e <= 4; for larger e two half tables
+// (multiples by the low h1 bits and by the high e - h1 bits of the scalar, x*B = T_lo[x_lo] ^
+// T_hi[x_hi]), 2^h1 + 2^h2 entries instead of 2^e, one more lookup per element.
+template <int E>
+struct NjTab {
+    static constexpr bool SPLIT = E >= 5;
+    static constexpr int H1 = SPLIT ? E / 2 : E, H2 = SPLIT ? E - E / 2 : 0;
+    static constexpr int ENTRIES = (1 << H1) + (SPLIT ? (1 << H2) : 0);
+};
+
 template <int E>
 __global__ void __launch_bounds__(NJ_THREADS) k_nj_mul(uint32_t f, int w, const uint64_t *__restrict__ A,
                                                         int64_t lda, const uint64_t *__restrict__ B, int64_t ldb,
                                                         uint64_t *__restrict__ C, int64_t ldc, int64_t m, int64_t k,
                                                         int64_t n, int acc, int G) {
     extern __shared__ __align__(16) uint64_t sm[];
-    constexpr int Q = 1 << E;
+    using T = NjTab<E>;
+    constexpr int Q = T::ENTRIES;  // table entries per row of B
     const int WB = (int)words_for(n * w);
     uint64_t *mult = sm;                      // [G][E][WB]: alpha^s * B_i
     uint64_t *tab = sm + (size_t)G * E * WB;  // [G][Q][WB]: x * B_i
@@ -65,13 +76,16 @@ __global__ void __launch_bounds__(NJ_THREADS) k_nj_mul(uint32_t f, int w, const 
             }
         }
         __syncthreads();
-        // tables: entry x of row gg = XOR of alpha^s * B_i over the set bits s of x
+        // tables: entry x of row gg = XOR of alpha^s * B_i over the set bits s of x (low table:
+        // s < H1; high table at entries 2^H1 .., scalar bits H1 ..)
         for (int idx = tid; idx < g * Q * WB; idx += NJ_THREADS) {
             const int gg = idx / (Q * WB), rem = idx - gg * (Q * WB), x = rem / WB, wd = rem - x * WB;
+            const bool hi = x >= (1 << T::H1);
+            const int xs = hi ? x - (1 << T::H1) : x, s0 = hi ? T::H1 : 0;
             uint64_t v = 0;
 #pragma unroll
-            for (int s = 0; s < E; ++s)
-                if ((x >> s) & 1) v ^= mult[(gg * E + s) * WB + wd];
+            for (int s = 0; s < (T::H1 > T::H2 ? T::H1 : T::H2); ++s)
+                if ((xs >> s) & 1) v ^= mult[(gg * E + s0 + s) * WB + wd];
             tab[idx] = v;
         }
         __syncthreads();
@@ -87,7 +101,11 @@ __global__ void __launch_bounds__(NJ_THREADS) k_nj_mul(uint32_t f, int w, const 
                     for (int gg = 0; gg < g; ++gg) {
                         const int64_t bit = (i0 + gg) * w;
                         const uint32_t x = (uint32_t)((arow[bit >> 6] >> (bit & 63)) & ((1u << E) - 1));
-                        v ^= tab[((size_t)gg * Q + x) * WB + wd];
+                        const uint64_t *tg = tab + (size_t)gg * Q * WB + wd;
+                        if constexpr (T::SPLIT)
+                            v ^= tg[(x & ((1u << T::H1) - 1)) * WB] ^ tg[((1u << T::H1) + (x >> T::H1)) * WB];
+                        else
+                            v ^= tg[x * WB];
                     }
                     accw[a] ^= v;
                 }
@@ -120,7 +138,7 @@ cudaError_t launch_nj_e(uint32_t f, int w, const uint64_t *A, int64_t lda, const
         if (dev < kMaxDevices) attr_set[dev] = true;
     }
     const int WB = (int)words_for(n * w);
-    const size_t per_row = ((size_t)(1 << E) + E) * WB * 8;  // table + multiples of one row of B
+    const size_t per_row = ((size_t)NjTab<E>::ENTRIES + E) * WB * 8;  // tables + multiples of one row of B
     int G = (int)(NJ_SMEM / per_row);
     if (G > 16) G = 16;
     if (G < 1) return cudaErrorInvalidValue;

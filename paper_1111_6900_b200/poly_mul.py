@@ -174,10 +174,14 @@ def count_products(e: int, f: int | None = None) -> int:
     return schedule(e, f).n_products
 
 
-# Below this size (max of m, k, n) products of packed matrices take the one-launch
-# packed-domain Newton-John kernel (gf2e_nj_mul) instead of slice -> combos -> product -> cling
-# (the crossover is the measured one, DESIGN §4 / profiles/r02).
-NJ_CROSSOVER = int(os.environ.get("GF2E_NJ_CROSSOVER", "64"))
+# Up to this size (max of m, k, n) per field degree, products of packed matrices take the
+# one-launch packed-domain Newton-John kernel (gf2e_nj_mul) instead of slice -> combos ->
+# product -> cling.  Measured crossovers of square products on the B200
+# (tools/nj_crossover.py, profiles/r02/nj_crossover.jsonl): the table kernel wins up to these
+# sizes; GF2E_NJ_CROSSOVER overrides all degrees.
+NJ_CROSSOVER = {2: 256, 3: 128, 4: 128, 5: 96, 6: 96, 7: 96, 8: 64, 9: 32, 10: 32}
+if os.environ.get("GF2E_NJ_CROSSOVER"):
+    NJ_CROSSOVER = {e: int(os.environ["GF2E_NJ_CROSSOVER"]) for e in NJ_CROSSOVER}
 
 
 def nj_fits(e: int, n: int) -> bool:
@@ -201,7 +205,8 @@ def nj_mul_packed(A: PackedMatrix, B: PackedMatrix, C: PackedMatrix | None = Non
 
 
 def _small(A: PackedMatrix, B: PackedMatrix, backend: str | None) -> bool:
-    return (backend is None and max(A.nrows, A.ncols, B.ncols) <= NJ_CROSSOVER and nj_fits(A.ctx.e, B.ncols))
+    return (backend is None and max(A.nrows, A.ncols, B.ncols) <= NJ_CROSSOVER[A.ctx.e]
+            and nj_fits(A.ctx.e, B.ncols))
 
 
 def karatsuba_mul_packed(A: PackedMatrix, B: PackedMatrix, counters: MulCounters | None = None,

@@ -490,7 +490,7 @@ def test_nj_small_products_golden(g, golden):
         C0 = g.PackedMatrix.from_numpy(ctx, golden[f"{tag}/C0_packed"], n)
         poly_mul.nj_mul_packed(A, B, C0)
         assert np.array_equal(C0.to_numpy(), golden[f"{tag}/addmul_packed"]), tag
-        if max(m, k, n) <= poly_mul.NJ_CROSSOVER:
+        if max(m, k, n) <= poly_mul.NJ_CROSSOVER[e]:
             assert np.array_equal(g.karatsuba_mul_packed(A, B).to_numpy(), golden[f"{tag}/C_packed"]), tag
             assert g._lib.last_product_kernel() == "k_nj_mul"
 
