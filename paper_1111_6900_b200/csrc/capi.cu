@@ -3,6 +3,7 @@
 // schedule, workspace carving, and the launch sequence of the hot path.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdarg>
 #include <cstddef>
 #include <cstdio>
@@ -881,6 +882,162 @@ int ple_rec(PleCtx &c, int64_t r0, int64_t c0, int64_t m, int64_t n, int64_t *P,
     return GF2E_OK;
 }
 
+// ---- speculative PLE: no host synchronisation inside the recursion ---------------------------
+// The recursion's launch sequence depends on the data only through the ranks of the left halves
+// (the sizes of the corner solves, Schur updates and sub-problems) and the row pivots.  A
+// generic matrix has full rank at every node (r1 = min(m, n1)) and the column rank profile
+// 0, 1, 2, ...; so the whole recursion is enqueued with those ranks, the row pivots stay in
+// device memory (every panel commits its pivots into global swap vectors that the row-swap
+// kernels read), and every panel checks its rank against the speculated one.  One
+// synchronisation at the end reads the flag: if any panel fell short, the input is restored
+// from a device copy and the exact host-driven recursion (ple_rec) runs instead.
+struct PleSpec {
+    int e;
+    uint32_t f;
+    Sched ks;
+    uint64_t *S;
+    int64_t ld, ps;
+    cudaStream_t st;
+    PanelOut *pout;
+    const FieldTab *tab;
+    int64_t *Pg, *Qg;  // device swap vectors (length min(m, n))
+    int *flag;         // device: a panel's rank differed from the speculated one
+    int64_t *hstage, *dstage;  // column-swap triples: pinned host / device bump buffers
+    size_t cap, used;          // entries
+};
+
+int ple_rec_spec(PleSpec &c, int64_t r0, int64_t c0, int64_t m, int64_t n) {
+    if (m == 0 || n == 0) return GF2E_OK;
+    uint64_t *V = c.S + r0 * c.ld + c0 / 64;
+    if (n <= kPlePanel) {
+        CK(launch_ple_panel(c.e, c.tab, V, c.ld, c.ps, m, (int)n, c.pout, c.st), "ple_panel");
+        g_launches += m > ple_window() ? 1 : 0;
+        CK(launch_ple_commit(c.pout, c.Pg, c.Qg, r0, c0, (int)(m < n ? m : n), c.flag, c.st), "ple_commit");
+        return GF2E_OK;
+    }
+    int64_t n1 = round_up(n / 2, 64);
+    if (n1 >= n) n1 -= 64;
+    if (int rc = ple_rec_spec(c, r0, c0, m, n1)) return rc;
+    const int64_t r1 = m < n1 ? m : n1, nr = n - n1;
+    uint64_t *R = V + n1 / 64;
+    if (r1 > 0) {
+        CK(launch_row_swaps_vec(c.e, c.S + (c0 + n1) / 64, c.ld, c.ps, words_for(nr), c.Pg, r0, r0 + r1, c.st),
+           "row_swaps");
+        const int64_t lw = words_for(r1);
+        DevTmp lt((size_t)c.e * r1 * lw * 8, c.st);
+        if (!lt.p) return fail(GF2E_ENOMEM, "out of device memory (PLE corner)");
+        uint64_t *L = static_cast<uint64_t *>(lt.p);
+        CK(launch_tril_copy(c.e, V, c.ld, c.ps, r1, L, lw, r1 * lw, c.st), "tril_copy");
+        const int64_t tws = gf2e_trsm_workspace(c.e, c.f, r1, nr);
+        DevTmp tw((size_t)(tws > 0 ? tws : 256), c.st);
+        if (!tw.p) return fail(GF2E_ENOMEM, "out of device memory (PLE trsm workspace)");
+        int64_t bad = -1;
+        if (int rc = trsm_impl(c.e, c.f, 0, 0, L, lw, r1 * lw, R, c.ld, c.ps, r1, nr, tw.p, tws, c.st, &bad, false))
+            return rc;
+        if (m - r1 > 0) {
+            const int64_t mws = gf2e_slice_mul_workspace(c.e, c.f, m - r1, r1, nr, GF2E_ACCUMULATE);
+            DevTmp mw((size_t)(mws > 0 ? mws : 256), c.st);
+            if (!mw.p) return fail(GF2E_ENOMEM, "out of device memory (PLE update workspace)");
+            if (int rc = run_product(c.ks, V + r1 * c.ld, c.ld, c.ps, R, c.ld, c.ps, R + r1 * c.ld, c.ld, c.ps, m - r1,
+                                     r1, nr, GF2E_ACCUMULATE, mw.p, mws, c.st))
+                return rc;
+        }
+    }
+    if (m - r1 > 0)
+        if (int rc = ple_rec_spec(c, r0 + r1, c0 + n1, m - r1, nr)) return rc;
+    const int64_t r2 = (m - r1) < nr ? (m - r1) : nr;
+    if (r2 > 0) {
+        CK(launch_row_swaps_vec(c.e, c.S + c0 / 64, c.ld, c.ps, n1 / 64, c.Pg, r0 + r1, r0 + r1 + r2, c.st),
+           "row_swaps");
+        std::vector<int64_t> tr;  // compress the right half's L into the leading columns (:275-279)
+        for (int64_t u = 0; u < r2; ++u)
+            if (n1 + u != r1 + u) tr.insert(tr.end(), {r1 + u, n1 + u, r1 + u});
+        if (!tr.empty()) {
+            if (c.used + tr.size() > c.cap) return fail(GF2E_ENOMEM, "PLE staging overflow");
+            int64_t *h = c.hstage + c.used, *d = c.dstage + c.used;
+            std::memcpy(h, tr.data(), tr.size() * 8);
+            c.used += tr.size();
+            CKH(cudaMemcpyAsync(d, h, tr.size() * 8, cudaMemcpyHostToDevice, c.st), "cudaMemcpyAsync");
+            CK(launch_col_swaps(c.e, 1, V, c.ld, c.ps, m, d, (int)(tr.size() / 3), c.st), "col_swaps");
+        }
+    }
+    return GF2E_OK;
+}
+
+// column-swap triples the speculative recursion stages: 3 per compressed column per node, at
+// most 3 * min(m, n) per recursion level
+int64_t ple_spec_stage_entries(int64_t m, int64_t n) {
+    int64_t levels = 1;
+    for (int64_t w = n; w > kPlePanel; w = (w + 1) / 2) ++levels;
+    return 3 * (m < n ? m : n) * levels + 64;
+}
+
+// 1: done (P, Q, rank written); 0: a rank check failed, S restored; <0... errors as status
+int ple_try_spec(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int64_t n, int64_t *P,
+                 int64_t *Q, int64_t *rank, cudaStream_t st, const FieldTab *tab, PanelOut *pout, bool *done) {
+    *done = false;
+    const int64_t k = m < n ? m : n, nw = words_for(n);
+    DevTmp backup((size_t)e * m * nw * 8, st), pq((size_t)2 * k * 8 + 256, st);
+    const int64_t entries = ple_spec_stage_entries(m, n);
+    DevTmp dst((size_t)entries * 8, st);
+    if (!backup.p || !pq.p || !dst.p) return GF2E_OK;  // no room: take the exact path
+    // pinned host staging, persistent per host thread and device (grown on demand)
+    struct Stage {
+        int64_t *buf = nullptr;
+        size_t cap = 0;
+    };
+    thread_local Stage stages[kMaxDevices];
+    int dev = 0;
+    CKH(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= kMaxDevices) return GF2E_OK;
+    Stage &sg = stages[dev];
+    if (sg.cap < (size_t)entries) {
+        if (sg.buf) {
+            CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            cudaFreeHost(sg.buf);
+            sg.buf = nullptr;
+            sg.cap = 0;
+        }
+        const size_t want = (size_t)entries > ((size_t)1 << 17) ? (size_t)entries : ((size_t)1 << 17);
+        if (cudaMallocHost(reinterpret_cast<void **>(&sg.buf), want * 8) != cudaSuccess) return GF2E_OK;
+        sg.cap = want;
+    }
+    uint64_t *bk = static_cast<uint64_t *>(backup.p);
+    for (int t = 0; t < e; ++t)
+        CKH(cudaMemcpy2DAsync(bk + t * m * nw, nw * 8, S + t * ps, ld * 8, nw * 8, m, cudaMemcpyDeviceToDevice, st),
+            "backup");
+    int64_t *Pg = static_cast<int64_t *>(pq.p), *Qg = Pg + k;
+    int *flag = reinterpret_cast<int *>(Qg + k);
+    CKH(cudaMemsetAsync(flag, 0, sizeof(int), st), "cudaMemsetAsync");
+    PleSpec c{e, f, to_kernel_sched(e, get_schedule(e, f)), S, ld, ps, st, pout, tab, Pg, Qg, flag,
+              sg.buf, static_cast<int64_t *>(dst.p), (size_t)entries, 0};
+    const auto h0 = std::chrono::steady_clock::now();
+    if (int rc = ple_rec_spec(c, 0, 0, m, n)) return rc;
+    if (getenv("GF2E_PLE_TRACE"))
+        fprintf(stderr, "ple spec: host enqueue %.3f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+    int hflag = 0;
+    std::vector<int64_t> hp(k), hq(k);
+    CKH(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    CKH(cudaMemcpyAsync(hp.data(), Pg, k * 8, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    CKH(cudaMemcpyAsync(hq.data(), Qg, k * 8, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (hflag) {  // some left half was rank deficient: restore and take the exact path
+        for (int t = 0; t < e; ++t)
+            CKH(cudaMemcpy2DAsync(S + t * ps, ld * 8, bk + t * m * nw, nw * 8, nw * 8, m, cudaMemcpyDeviceToDevice,
+                                  st),
+                "restore");
+        return GF2E_OK;
+    }
+    for (int64_t i = 0; i < k; ++i) {
+        if (P) P[i] = hp[i];
+        if (Q) Q[i] = hq[i];
+    }
+    if (rank) *rank = k;
+    *done = true;
+    return GF2E_OK;
+}
+
 int ple_top(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int64_t n, int64_t *P, int64_t *Q,
             int64_t *rank, cudaStream_t st) {
     const int64_t k = m < n ? m : n;
@@ -889,6 +1046,12 @@ int ple_top(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int64_t m, i
     if (!po.p || !ix.p) return fail(GF2E_ENOMEM, "out of device memory (PLE scratch)");
     const FieldTab *tab = field_tab(e, f, primitive_element(e, f));
     if (!tab) return fail(GF2E_ECUDA, "field table upload failed");
+    if (!getenv("GF2E_PLE_EXACT")) {  // GF2E_PLE_EXACT=1: always the host-driven recursion
+        bool done = false;
+        if (int rc = ple_try_spec(e, f, S, ld, ps, m, n, P, Q, rank, st, tab, static_cast<PanelOut *>(po.p), &done))
+            return rc;
+        if (done) return GF2E_OK;
+    }
     PleCtx c{e, f, to_kernel_sched(e, get_schedule(e, f)), S, ld, ps, st, static_cast<PanelOut *>(po.p),
              static_cast<int64_t *>(ix.p), tab};
     // The pinned staging ring persists per host thread and only grows: pinning and unpinning

@@ -140,6 +140,12 @@ const FieldTab *field_tab(int e, uint32_t f, uint32_t g);  // device pointer (sy
 int ple_window();  // rows kept in shared memory by the panel kernel (launches = 1 + (m > window))
 cudaError_t launch_ple_panel(int e, const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb,
                              PanelOut *out, cudaStream_t st);
+// speculative PLE: swaps t <-> Pg[t] (t in [t0, t1)) read from device memory; a panel's pivots
+// committed into the global vectors, flag set if its rank differs from the speculated one
+cudaError_t launch_row_swaps_vec(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t nwords, const int64_t *Pg,
+                                 int64_t t0, int64_t t1, cudaStream_t st);
+cudaError_t launch_ple_commit(const PanelOut *po, int64_t *Pg, int64_t *Qg, int64_t r0, int64_t c0, int expected,
+                              int *flag, cudaStream_t st);
 cudaError_t launch_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t nwords, const int64_t *pairs,
                              int n, bool backward, cudaStream_t st);
 cudaError_t launch_col_swaps(int planes, int w, uint64_t *S, int64_t ld, int64_t ps, int64_t rows, const int64_t *trip,

@@ -372,6 +372,76 @@ __global__ void k_row_swaps(int planes, uint64_t *__restrict__ S, int64_t ld, in
     }
 }
 
+// LAPACK-style swaps t <-> Pg[t] for t in [t0, t1), in order, on a column window (the
+// speculative PLE: the pivots stay in device memory, ple_commit)
+__global__ void k_row_swaps_vec(int planes, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t nwords,
+                                const int64_t *__restrict__ Pg, int64_t t0, int64_t t1) {
+    // the pivots are staged in shared memory and compacted to the non-trivial swaps (a generic
+    // matrix pivots on the diagonal almost everywhere), 1024 pivot positions at a time; 128
+    // threads per block (the compaction's layout)
+    __shared__ int64_t sp[1024][2];
+    __shared__ int cnt;
+    const int64_t total = (int64_t)planes * nwords;
+    const int64_t idx = gtid();
+    const int64_t b = idx / nwords, w = idx % nwords;
+    uint64_t *col = idx < total ? S + b * ps + w : nullptr;
+    for (int64_t c0 = t0; c0 < t1; c0 += 1024) {
+        const int64_t c1 = c0 + 1024 < t1 ? c0 + 1024 : t1;
+        // ordered compaction: thread i owns positions c0 + 8i .. c0 + 8i + 7 (blockDim 128)
+        __shared__ int wsum[4];
+        int64_t u[8];
+        int mine = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t t = c0 + 8 * threadIdx.x + j;
+            u[j] = t < c1 ? Pg[t] : t;
+            mine += u[j] != t;
+        }
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) wsum[wid] = incl;
+        __syncthreads();
+        int base = incl - mine;
+        for (int q = 0; q < wid; ++q) base += wsum[q];
+        if (threadIdx.x == 127) cnt = base + mine;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t t = c0 + 8 * threadIdx.x + j;
+            if (u[j] != t) {
+                sp[base][0] = t;
+                sp[base][1] = u[j];
+                ++base;
+            }
+        }
+        __syncthreads();
+        if (col)
+            for (int i = 0; i < cnt; ++i) {
+                const int64_t t = sp[i][0], u = sp[i][1];
+                const uint64_t x = col[t * ld];
+                col[t * ld] = col[u * ld];
+                col[u * ld] = x;
+            }
+        __syncthreads();
+    }
+}
+
+// a panel's pivots into the global swap vectors (P[r0 + t] = r0 + P_panel[t], Q likewise with
+// the column offset); a rank other than the speculated one raises the flag
+__global__ void k_ple_commit(const PanelOut *__restrict__ po, int64_t *__restrict__ Pg, int64_t *__restrict__ Qg,
+                             int64_t r0, int64_t c0, int expected, int *__restrict__ flag) {
+    const int r = po->rank;
+    for (int t = threadIdx.x; t < expected; t += blockDim.x) {
+        Pg[r0 + t] = t < r ? r0 + po->P[t] : r0 + t;
+        Qg[r0 + t] = t < r ? c0 + po->Q[t] : c0 + t;
+    }
+    if (threadIdx.x == 0 && r != expected) atomicOr(flag, 1);
+}
+
 // (a, b, first row) triples applied in order to w-bit slots; thread = (plane, row)
 __global__ void k_col_swaps(int planes, int w, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t rows,
                             const int64_t *__restrict__ trip, int n) {
@@ -547,6 +617,21 @@ cudaError_t launch_row_swaps(int planes, uint64_t *S, int64_t ld, int64_t ps, in
     if (n == 0 || nwords == 0) return cudaSuccess;
     k_row_swaps<<<grid_for((int64_t)planes * nwords, 128), 128, 0, st>>>(planes, S, ld, ps, nwords, swaps, n,
                                                                         backward ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_swaps_vec(int planes, uint64_t *S, int64_t ld, int64_t ps, int64_t nwords, const int64_t *Pg,
+                                 int64_t t0, int64_t t1, cudaStream_t st) {
+    if (t1 <= t0 || nwords == 0) return cudaSuccess;
+    const int64_t total = (int64_t)planes * nwords;
+    k_row_swaps_vec<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(planes, S, ld, ps, nwords, Pg, t0, t1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ple_commit(const PanelOut *po, int64_t *Pg, int64_t *Qg, int64_t r0, int64_t c0, int expected,
+                              int *flag, cudaStream_t st) {
+    if (expected <= 0) return cudaSuccess;
+    k_ple_commit<<<1, 64, 0, st>>>(po, Pg, Qg, r0, c0, expected, flag);
     return cudaGetLastError();
 }
 

@@ -218,3 +218,23 @@ def test_counters_through_the_api(g, golden):
                 g.echelonize(A.copy(), full=full, crossover=cx, counters=c)
                 got += [c.gf2_matmul_count, c.additions, c.peak_live_products]
             assert got == row, (tag, cx)
+
+
+@pytest.mark.parametrize("e,m,n,kind", [(8, 700, 900, "rand"), (2, 1000, 640, "rand"), (4, 513, 300, "lowrank"),
+                                        (10, 300, 1300, "rand"), (3, 640, 640, "rand"), (5, 200, 64, "rand")])
+def test_ple_speculative_matches_exact(g, e, m, n, kind, monkeypatch):
+    # the speculative recursion (full rank at every node, pivots kept on device, one sync) and
+    # the host-driven exact recursion give the same factorisation; rank-deficient inputs fall
+    # back to the exact path after the rank check
+    ctx = g.field_new(e)
+    A = _lowrank(g, ctx, m, n, 45, 60 + e) if kind == "lowrank" else g.PackedMatrix.random(ctx, m, n, 60 + e)
+    F1 = g.ple(A.copy())
+    monkeypatch.setenv("GF2E_PLE_EXACT", "1")
+    F2 = g.ple(A.copy())
+    assert F1.rank == F2.rank
+    assert np.array_equal(F1.P.entries, F2.P.entries) and np.array_equal(F1.Q.entries, F2.Q.entries)
+    assert F1.matrix == F2.matrix
+    arr = A.to_array()
+    Fo = oracle.ple(e, ctx.f, arr)
+    assert F1.rank == Fo[3] and np.array_equal(F1.P.entries, Fo[1]) and np.array_equal(F1.Q.entries, Fo[2])
+    assert np.array_equal(F1.matrix.to_array(), Fo[0])
