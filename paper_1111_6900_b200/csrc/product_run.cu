@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
             for (int t = 0; t < s.nprod; ++t, ++gp) {
                 const int b = (int)(gp & 1);
                 const uint32_t mask = bars->outmask[t];
-                TWR(i_tfull, mbar_wait_sleep(&bars->tfull[b], (uint32_t)((gp >> 1) & 1), 20));
+                TWR(i_tfull, mbar_wait(&bars->tfull[b], (uint32_t)((gp >> 1) & 1)));
 #if GF2E_INSTR
                 const long long i_d0 = clock64();
 #endif
@@ -418,8 +418,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                 const uint32_t w0 = parity_word_tree(v[0]);  // bit 7 of each cell
                 tmem_ld32_pack16(ta + 64, v[0]);
                 const uint32_t w1 = parity_word_tree(v[1]);
-                fold(0, w0);
-                fold(1, w1);
+                if constexpr (E > 4) {  // registers: fold before the hand-off
+                    fold(0, w0);
+                    fold(1, w1);
+                }
 #if GF2E_INSTR
                 const long long i_e2 = clock64();
 #endif
@@ -437,6 +439,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
 #if GF2E_INSTR
                 const long long i_e4 = clock64();
 #endif
+                if constexpr (E <= 4) {  // small E: fold after the hand-off (the MMA may refill
+                    fold(0, w0);         // this accumulator meanwhile)
+                    fold(1, w1);
+                }
                 fold(2, parity_word_tree(v[0]));
 #if GF2E_INSTR
                 i_e[0] += (unsigned long long)(i_e1 - i_d0);
