@@ -376,7 +376,13 @@ def run_ours(args):
     # measured on THIS GPU right now by a pure-MMA loop on every SM.  MEASURED_PEAKS.json holds
     # only bf16 (its cuBLAS figure x2 understates the int8 pipe), reported alongside.
     fp4_form = "fp4" in kernel_name
-    if fp4_form:
+    bound = "tensor"
+    if "m4rm" in kernel_name:  # the INT-pipe form: its roofline is the shared-memory table reads
+        bps, tc_peak = _lib.int_peak(2000)
+        bound = "int-pipe (LDS.128)"
+        peak_basis = (f"measured live: conflict-free LDS.128 on all SMs = {bps / 1e12:.1f} TB/s; M4RM reads one "
+                      "16-byte table row per 128 columns x 8 k-bits (2048 GF(2) bit-ops)")
+    elif fp4_form:
         tc_peak = max(_lib.mma_peak_fp4(20000), _lib.mma_peak_fp4(20000))
         peak_basis = ("measured live: pure tcgen05.mma kind::mxf4 (e2m1, scale 1.0) loop on all SMs "
                       "(zero operands; random GF(2)-encoded operands and 0.25 s loops measure the same); "
@@ -409,7 +415,7 @@ def run_ours(args):
         "time_s": round(ms_max / 1e3, 6),
         "comm_included": bool(use_pg),
         "gpu_launches": launches,
-        "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(tc_peak, 1),
+        "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": round(tc_peak, 1),
                      "unit": "TFLOP/s", "frac": round(achieved / tc_peak, 4), "traffic": traffic,
                      "kernel": kernel_name, "kernel_ms": round(prod_ms_max, 4),
                      "peak_basis": peak_basis,

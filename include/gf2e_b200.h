@@ -294,6 +294,13 @@ int gf2e_dev_fp4_probe(int iters, int mode, const uint8_t *a_dev, const uint8_t 
 int gf2e_profile_read(double *total_ms, int *launches);
 
 /*
+ * INT-pipe roofline of the M4RM product form (GF2E_BACKEND_M4RM): conflict-free LDS.128 table
+ * reads on every SM (the form's bound, profiles/r02/ncu_m4rm_c3.txt), as bytes/s and as the
+ * GF(2) bit-op rate it allows (2048 bit-ops per 16-byte table read: 128 columns x 8 k-bits).
+ */
+int gf2e_int_peak(int iters, double *lds_bytes_per_s, double *m4rm_tops, void *stream);
+
+/*
  * fp4 exactness self-check.  The kind::mxf4 forms of the product assume exact fp32
  * accumulation of 0/1 products (measured, not architecturally guaranteed).  Before the first
  * fp4 product on a device the library compares every fp4 form with the int8 form (integer

@@ -74,6 +74,7 @@ SIGNATURES = {
     "gf2e_mma_peak": (_INT, [_INT, _INT, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
     "gf2e_trim_pool": (_INT, [_I64]),
     "gf2e_tile_cols": (_I64, [_INT, _U32, _I64, _U32]),
+    "gf2e_int_peak": (_INT, [_INT, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
     "gf2e_fp4_selfcheck": (_INT, [_INT, _INT, ctypes.POINTER(_INT)]),
 }
 
@@ -185,6 +186,17 @@ def fp4_selfcheck(rerun: bool = False, inject_fault: bool = False) -> int:
     check(load().gf2e_fp4_selfcheck(1 if rerun else 0, 1 if inject_fault else 0, ctypes.byref(ok)),
           "gf2e_fp4_selfcheck")
     return ok.value
+
+
+def int_peak(iters: int = 2000) -> tuple[float, float]:
+    """(LDS.128 bytes/s of the whole GPU, the M4RM form's GF(2) Tbit-op/s bound) measured live."""
+    import torch
+
+    bps = ctypes.c_double()
+    tops = ctypes.c_double()
+    check(load().gf2e_int_peak(iters, ctypes.byref(bps), ctypes.byref(tops),
+                               torch.cuda.current_stream().cuda_stream), "gf2e_int_peak")
+    return bps.value, tops.value
 
 
 def last_product_kernel() -> str:

@@ -1155,6 +1155,23 @@ int gf2e_mma_peak(int cta_group, int iters, double *tops, double *ms, void *stre
     return GF2E_OK;
 }
 
+int gf2e_int_peak(int iters, double *lds_bytes_per_s, double *m4rm_tops, void *stream) {
+    g_err.clear();
+    if (iters < 1) return fail(GF2E_EINVAL, "iters must be >= 1");
+    if (int rc = check_device()) return rc;
+    int dev = 0, nsms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsms, cudaDevAttrMultiProcessorCount, dev);
+    double bps = 0;
+    cudaError_t e = run_lds_peak(iters, nsms, (cudaStream_t)stream, &bps);
+    if (e != cudaSuccess) return cuda_fail(e, "lds_peak");
+    if (lds_bytes_per_s) *lds_bytes_per_s = bps;
+    // k_product_m4rm: one 16-byte table read (+ 4 LOP3) per (row, 128 columns, 8 k-bits) =
+    // 128 x 8 x 2 GF(2) bit-ops
+    if (m4rm_tops) *m4rm_tops = bps / 16.0 * 2048.0 / 1e12;
+    return GF2E_OK;
+}
+
 int gf2e_dev_fp4_probe(int iters, int mode, const uint8_t *a_dev, const uint8_t *b_dev, uint32_t *out_dev,
                        double *tops, void *stream) {
     g_err.clear();

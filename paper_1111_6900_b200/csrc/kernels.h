@@ -109,6 +109,8 @@ struct M4rmArgs {
 };
 constexpr int kM4BM = 512, kM4BN = 1024, kM4KPAD = 64;
 cudaError_t launch_product_m4rm(const Sched &s, const M4rmArgs &a, cudaStream_t st);
+// conflict-free LDS.128 throughput of the whole GPU (bytes/s): the M4RM form's INT-pipe roofline
+cudaError_t run_lds_peak(int iters, int nsms, cudaStream_t st, double *bytes_per_s);
 
 // trsm.cu
 // diagonal blocks of the blocked TRSM: 256 rows (full product tiles, k = 256 leaf products)

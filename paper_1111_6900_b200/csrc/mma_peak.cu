@@ -94,7 +94,51 @@ __global__ void __launch_bounds__(PK_THREADS, 1) k_mma_peak(int iters) {
     }
 }
 
+// INT-pipe roofline of the M4RM form (k_product_m4rm): conflict-free LDS.128 table reads
+// XOR-ed into registers, 2 CTAs x 1024 threads per SM
+__global__ void __launch_bounds__(1024) k_lds_peak(int iters, uint32_t *out) {
+    __shared__ uint4 tab[2048];
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) tab[i] = make_uint4(i, i * 3, i * 5, i * 7);
+    __syncthreads();
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    int idx = threadIdx.x & 2047;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const uint4 v = tab[(idx + r * 32) & 2047];
+            acc.x ^= v.x;
+            acc.y ^= v.y;
+            acc.z ^= v.z;
+            acc.w ^= v.w;
+        }
+        idx = (idx + (int)(acc.x & 1)) & 2047;
+    }
+    if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345u) out[0] = 1;
+}
+
 }  // namespace
+
+cudaError_t run_lds_peak(int iters, int nsms, cudaStream_t st, double *bytes_per_s) {
+    uint32_t *d = nullptr;
+    cudaError_t err = cudaMallocAsync(reinterpret_cast<void **>(&d), 64, st);
+    if (err != cudaSuccess) return err;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_lds_peak<<<nsms * 2, 1024, 0, st>>>(iters, d);  // warm-up
+    cudaEventRecord(a, st);
+    k_lds_peak<<<nsms * 2, 1024, 0, st>>>(iters, d);
+    cudaEventRecord(b, st);
+    err = cudaGetLastError();
+    float ms = 0;
+    if (err == cudaSuccess) err = cudaEventSynchronize(b);
+    if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFreeAsync(d, st);
+    if (err == cudaSuccess) *bytes_per_s = (double)nsms * 2 * 1024 * iters * 16 * 16 / (ms * 1e-3);
+    return err;
+}
 
 cudaError_t run_mma_peak(int cta_group, int iters, int nsms, cudaStream_t st, float *ms) {
     cudaEvent_t a, b;
