@@ -389,10 +389,30 @@ __device__ __forceinline__ void transpose64(uint64_t &xa, uint64_t &xb, int lane
 // tensor-core producer expands with one AND per output word (product_tc2.cu) — stored
 // stage-tiled with the rows of every 32-row group in tc_b_row_inv order (the epilogue's
 // parity packer emits columns in b_row_perm order).  One warp per 64x64 block.
+// fp4 B^T words (w2, w2 + 1) of row r, EXPANDED to the MMA operand (nibbles 2/1/0.5/1 per bit
+// as product_run.cu's expander would write them) inside the row's 128-byte-swizzled stage tile
+// of br rows: one bulk copy then moves a ready operand stage into shared memory
+__device__ __forceinline__ void put_expanded(uint64_t *o, int64_t r, int64_t w2, int64_t ldo, int br, uint64_t x0,
+                                             uint64_t x1) {
+    constexpr int kw = 4;
+    const int64_t stage = w2 / kw;
+    const int c0 = (int)(w2 % kw) * 2;
+    uint8_t *tile = reinterpret_cast<uint8_t *>(o + ((r / br) * (ldo / kw) + stage) * (int64_t)br * 16);
+    const int rr = (int)(r % br);
+    const uint32_t q[4] = {(uint32_t)x0, (uint32_t)(x0 >> 32), (uint32_t)x1, (uint32_t)(x1 >> 32)};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t x = q[i];
+        const int c = c0 + i;
+        *reinterpret_cast<uint4 *>(tile + (rr >> 3) * 1024 + (rr & 7) * 128 + ((c ^ (rr & 7)) << 4)) =
+            make_uint4(x & 0x44444444u, x & 0x22222222u, x & 0x11111111u, (x >> 2) & 0x22222222u);
+    }
+}
+
 template <int E>  // planes at compile time (register arrays of E words)
 __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb, int64_t pb, int64_t k,
                             int64_t n, uint64_t *__restrict__ out, int64_t ldo, int64_t po, int64_t kblocks,
-                            int64_t nblocks, int fp4, int tsplit, int br, int64_t row0) {
+                            int64_t nblocks, int fp4, int tsplit, int br, int64_t row0, int expand) {
     // one warp per (2 x 64 k-rows, 64-column block[, product group]): two 64x64 transposes, then each lane
     // writes 16-byte pieces of tile rows.  Input row r of a 64-block lands at bit sigma(r):
     // int8 reverses bits inside bytes (r ^ 7), fp4 swaps bits 0 and 2 of every nibble.
@@ -445,9 +465,15 @@ __global__ void k_combos_bt(Sched s, const uint64_t *__restrict__ B, int64_t ldb
                 }
             }
             uint64_t *o = out + t * po;
-            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(ra, 2 * ks, ldo, kw, br)) = make_ulonglong2(xa[0], xa[1]);
-            *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(rbw, 2 * ks, ldo, kw, br)) =
-                make_ulonglong2(xb[0], xb[1]);
+            if (expand) {
+                put_expanded(o, ra, 2 * ks, ldo, br, xa[0], xa[1]);
+                put_expanded(o, rbw, 2 * ks, ldo, br, xb[0], xb[1]);
+            } else {
+                *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(ra, 2 * ks, ldo, kw, br)) =
+                    make_ulonglong2(xa[0], xa[1]);
+                *reinterpret_cast<ulonglong2 *>(o + tc_tile_word(rbw, 2 * ks, ldo, kw, br)) =
+                    make_ulonglong2(xb[0], xb[1]);
+            }
         }
     }
 }
@@ -582,7 +608,7 @@ cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, i
 
 cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int64_t pb, int64_t k, int64_t n,
                              uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks, bool fp4,
-                             cudaStream_t st, int br, int64_t row0) {
+                             cudaStream_t st, int br, int64_t row0, bool expand) {
     int64_t warps = (kblocks >> 1) * nblocks;  // kblocks is even (k_pad is a multiple of 128)
     if (warps == 0) return cudaSuccess;
     int tsplit = 1;
@@ -590,7 +616,7 @@ cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int
     int g = grid_for(warps * tsplit * 32, 256);
     return dispatch_e(s.e, [&](auto ec) {
         k_combos_bt<decltype(ec)::value><<<g, 256, 0, st>>>(s, B, ldb, pb, k, n, out, ldo, po, kblocks, nblocks,
-                                                            fp4 ? 1 : 0, tsplit, br, row0);
+                                                            fp4 ? 1 : 0, tsplit, br, row0, expand ? 1 : 0);
         return cudaGetLastError();
     });
 }

@@ -51,7 +51,9 @@ cudaError_t launch_combos_rows(const Sched &s, const uint64_t *X, int64_t ldx, i
 // KW = 2 and bits reversed inside every byte
 cudaError_t launch_combos_bt(const Sched &s, const uint64_t *B, int64_t ldb, int64_t pb, int64_t k, int64_t n,
                              uint64_t *out, int64_t ldo, int64_t po, int64_t kblocks, int64_t nblocks, bool fp4,
-                             cudaStream_t st, int br = 128, int64_t row0 = 0);
+                             cudaStream_t st, int br = 128, int64_t row0 = 0, bool expand = false);
+// (expand: fp4 only — write the MMA-ready nibble expansion in 128-byte-swizzled br-row stage
+// tiles, 4 x the words: the running-sum form bulk-copies B stages straight into shared memory)
 // (row0: first B^T row written, a multiple of 64 — the column offset of a B part; the tile
 // layout stays relative to `out`)
 

@@ -13,4 +13,6 @@ timeout 900 python bench.py --config 5 --steps 3 --warmup 3 --no-e2e > $O/bench_
 for f in $O/bench_config*.json; do python -c "
 import json;d=json.loads(open('$f').read().strip().splitlines()[-1]);r=d['roofline'];print('$f'.split('/')[-1],d['value'],d['ms_per_step'],r['kernel'],r['frac'],d.get('e2e',{}).get('value'),d.get('parity'))" 2>&1 | tail -1; done
 timeout 600 python tools/bench_ops.py > $O/ops.jsonl 2>&1; tail -5 $O/ops.jsonl
+timeout 300 python bench.py --backend m4rm --no-e2e --no-cpu-baseline > $O/bench_config3_m4rm.json 2>&1; tail -c 700 $O/bench_config3_m4rm.json
+timeout 600 python bench.py --impl reference > $O/bench_reference.json 2>&1; tail -c 300 $O/bench_reference.json
 echo done
