@@ -338,6 +338,9 @@ const char *form_name(int form) {
 // tile columns of a form (CTA-pair tile width; B^T is stage-tiled in half-width row blocks)
 int64_t form_bn(int form) { return form == kFormFp4Run ? kRunBN : kTcBN; }
 int form_br(int form) { return (int)(form_bn(form) / 2); }
+// B^T words per row per bit word: 4 when the form's B operand is stored pre-expanded
+int64_t form_bx(int form) { return (form == kFormFp4Run && kRunBPre) ? 4 : 1; }
+bool form_bexp(int form) { return form_bx(form) > 1; }
 
 constexpr int kFormAny = -2;  // workspace bound over every tensor-core form
 
@@ -353,17 +356,21 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags, in
     } else {
         if (form == -1) form = tc_form(flags, k, nprod);
         L.m_pad = round_up(m, 2 * kTcBM);  // CTA-pair tiles are 256 rows
-        if (form == kFormAny) {
-            const int64_t a = round_up(n, kTcBN), b = round_up(n, kRunBN);
+        int64_t bx = 1;
+        if (form == kFormAny) {  // every form a call with these sizes may take
+            const bool run = run_ok(nprod, k);
+            const int64_t a = round_up(n, kTcBN), b = run ? round_up(n, kRunBN) : 0;
             L.n_pad = a > b ? a : b;
             L.k_pad = round_up(k, kTcBKFp4);
+            bx = run ? form_bx(kFormFp4Run) : 1;
         } else {
             L.n_pad = round_up(n, form_bn(form));
             L.k_pad = round_up(k, form == kFormI8 ? kTcBK : kTcBKFp4);
+            bx = form_bx(form);
         }
         L.kwords = L.k_pad / 64;
         L.a_pstride = L.m_pad * L.kwords;
-        L.b_pstride = L.n_pad * L.kwords;
+        L.b_pstride = L.n_pad * L.kwords * bx;
     }
     L.a_bytes = align256((int64_t)nprod * L.a_pstride * 8);
     L.b_bytes = align256((int64_t)nprod * L.b_pstride * 8);
@@ -418,7 +425,7 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
         g_kernel = "k_product_m4rm";
     } else {
         CK(launch_combos_bt(ks, B, ldb, pb, k, n, Bx, L.kwords, L.b_pstride, L.kwords, L.n_pad / 64, fp4, st,
-                            form_br(form)),
+                            form_br(form), 0, form_bexp(form)),
            "combos(B^T)");
         TcArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, m, n, L.m_pad, L.n_pad, C, ldc, pc, acc ? 1 : 0};
         ProfScope prof(st);
@@ -671,7 +678,12 @@ TrsmLayout trsm_layout(int nprod, int e, int64_t m, int64_t n) {
     T.nblk = (m + tb - 1) / tb;
     T.inv_bytes = align256(T.nblk * e * tb * (tb / 64) * 8);
     T.tmp_bytes = align256((int64_t)e * tb * words_for(n) * 8);
-    T.mul_bytes = layout_for(nprod, m, m, n, 0, kFormAny).total;  // bounds every update and block product
+    // bounds every update and block product (k <= m): the largest k of the 256-column forms and
+    // the largest k the running-sum form (4x B^T words) may take
+    const int64_t krun = ((kRunMaxSum - 1) / ((nprod + 1) / 2)) / kTcBKFp4 * kTcBKFp4;
+    const int64_t a = layout_for(nprod, m, m, n, 0, kFormAny).total;
+    const int64_t b = layout_for(nprod, m, m < krun ? m : krun, n, 0, kFormAny).total;
+    T.mul_bytes = a > b ? a : b;
     T.total = T.inv_bytes + T.tmp_bytes + 256 + T.mul_bytes;
     return T;
 }
@@ -1464,13 +1476,13 @@ int gf2e_slice_mul_parts(int e, uint32_t f, const uint64_t *A, int64_t lda, int6
         const int64_t rend = lastp ? L.n_pad : c1;  // the last part also zero-fills the padding
         if (rend > c0)
             CK(launch_combos_bt(ks, B_parts[p], ldb[p], pb[p], k, c1 - c0, Bt, L.kwords, L.b_pstride, L.kwords,
-                                (rend - c0) / 64, fp4, st, form_br(form), c0),
+                                (rend - c0) / 64, fp4, st, form_br(form), c0, form_bexp(form)),
                "combos(B^T part)");
         // every tile whose columns have all arrived
         const int64_t avail = lastp ? ntiles : c1 / tw;
         if (avail > done) {
             const int64_t n0 = done * tw, n1 = avail * tw < n ? avail * tw : n;
-            TcArgs a{Ac, Bt + n0 * L.kwords, L.a_pstride, L.b_pstride, L.kwords, m, n1 - n0, L.m_pad,
+            TcArgs a{Ac, Bt + n0 * L.kwords * form_bx(form), L.a_pstride, L.b_pstride, L.kwords, m, n1 - n0, L.m_pad,
                      (avail - done) * tw, C + n0 / 64, ldc, pc, acc ? 1 : 0};
             ProfScope prof(st);
             CK(launch_form(ks, a, form, st), "product");
@@ -1639,8 +1651,8 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
         const int64_t npad = (p + 1 == nbp ? LB.n_pad : cb[p + 1]) - c0;
         CK(launch_slice(e, w, k, nc, dBp + c0 * w / 64, ldbd, dBs + c0 / 64, nwn, k * nwn, sp, words_for(nc)),
            "slice(B)");
-        CK(launch_combos_bt(ks, dBs + c0 / 64, nwn, k * nwn, k, nc, dBt + c0 * LB.kwords, LB.kwords, LB.b_pstride,
-                            LB.kwords, npad / 64, fp4, sp, form_br(form)),
+        CK(launch_combos_bt(ks, dBs + c0 / 64, nwn, k * nwn, k, nc, dBt + c0 * LB.kwords * form_bx(form), LB.kwords,
+                            LB.b_pstride, LB.kwords, npad / 64, fp4, sp, form_br(form), 0, form_bexp(form)),
            "combos(B^T)");
         CKH(cudaEventRecord(prep_b[p], sp), "cudaEventRecord");
         tr.mark(sp, "prep B", p);
@@ -1684,7 +1696,8 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
             if (i == 0 && !side)
                 if (int rc = prep_bpart(p)) return rc;
             if (i == 0) CKH(cudaStreamWaitEvent(P.sc, prep_b[p], 0), "cudaStreamWaitEvent");
-            TcArgs ta{dAc[sl], dBt + c0 * LB.kwords, L.a_pstride, LB.b_pstride, L.kwords, rows, c1 - c0, L.m_pad, npad,
+            TcArgs ta{dAc[sl], dBt + c0 * LB.kwords * form_bx(form), L.a_pstride, LB.b_pstride, L.kwords, rows, c1 - c0,
+                      L.m_pad, npad,
                       dCs[sl] + c0 / 64, nwn, rows * nwn, acc ? 1 : 0};
             ProfScope prof(P.sc);
             CK(launch_form(ks, ta, form, P.sc), "product");

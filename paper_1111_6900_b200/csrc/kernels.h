@@ -87,6 +87,12 @@ constexpr int kRunBN = 192;  // tile columns (two 192-column accumulators, three
                              // scale factors fill the 512 TMEM columns; 128-column tiles with three
                              // accumulators measured slower: 23.1 vs 17.7 ms at config 4, e = 8)
 constexpr int64_t kRunMaxSum = 65536;  // ceil(K/2) * k_pad must stay below (exact running sums)
+#ifndef GF2E_RUN_BPRE
+#define GF2E_RUN_BPRE 1
+#endif
+// the running-sum form's B^T operand is stored pre-expanded (4 words per bit word, swizzled
+// stage tiles: launch_combos_bt(..., expand)) and bulk-copied straight into shared memory
+constexpr bool kRunBPre = GF2E_RUN_BPRE != 0;
 cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st);
 constexpr int64_t kFp4PairMaxK = 2047;
 cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, int form, cudaStream_t st);

@@ -44,7 +44,10 @@ constexpr int NEXP = 4, NEPI = 8;  // epilogue: lane quarter x column half (96 c
 constexpr int EPI_W0 = NEXP, MMA_WARP = NEXP + NEPI, LOAD_WARP = MMA_WARP + 1;
 constexpr int NTHREADS = (NEXP + NEPI + 2) * 32;
 constexpr int B_BYTES = BNH * 128;                     // expanded B^T stage (12 KiB)
-constexpr int BITS_A = BM * KW * 8, BITS_B = BNH * KW * 8, BITS_BYTES = BITS_A + BITS_B;
+// B^T operand stages: pre-expanded by k_combos_bt and bulk-copied ready for the MMA (kRunBPre),
+// or expanded here from bit tiles
+constexpr bool BPRE = kRunBPre;
+constexpr int BITS_A = BM * KW * 8, BITS_B = BPRE ? 0 : BNH * KW * 8, BITS_BYTES = BITS_A + BITS_B;
 constexpr uint32_t ACC1 = BN;  // TMEM column of the second accumulator (the first starts at 0)
 constexpr uint32_t ATM0 = 2 * BN, SFA = 480, SFB = 496;
 static_assert(ATM0 + 32 * S <= SFA, "TMEM: A stages overlap the scale factors");
@@ -80,7 +83,7 @@ __device__ unsigned long long g_instr_run[1024][32];
 #endif
 
 struct __align__(8) Bars {
-    uint64_t full[S], empty[S], tfull[2], tempty[2], bfull[D], bempty[D];
+    uint64_t full[S], empty[S], bfullB[S], tfull[2], tempty[2], bfull[D], bempty[D];
     uint32_t tmem_base;
     uint16_t outmask[kMaxProducts];
 };
@@ -189,6 +192,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(&bars->full[i], 2 * NEXP);
+            mbar_init(&bars->bfullB[i], 1);
             mbar_init(&bars->empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
     if (warp < NEXP) {
         // ===================== expanders =====================
         const int p = threadIdx.x;  // A row p; B^T row p (p < BNH)
-        const bool doB = p < BNH;
+        const bool doB = !BPRE && p < BNH;
         const uint32_t full_leader = mapa(smem_u32(&bars->full[0]), 0);
         const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16) + ATM0;
         int slot = 0, st = 0;
@@ -260,7 +264,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
 #endif
             wait_st();
             tc_fence_before();
-            fence_proxy_async_smem();
+            if constexpr (BPRE)
+                mbar_wait(&bars->bfullB[st], phase);  // the bulk-copied B stage has landed
+            else
+                fence_proxy_async_smem();
 #if GF2E_INSTR
             const long long i_w3 = clock64();
             i_work += (unsigned long long)(i_w3 - i_w0);
@@ -301,10 +308,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         // ===================== bit-tile loader =====================
         const bool issuer = elect_one();
         const int64_t KS = a.kwords / KW;
-        const int64_t tw_a = BM * KW, tw_b = BNH * KW;
-        const uint32_t bits_s = smem_u32(bits);
-        int slot = 0;
-        uint32_t bph = 0;
+        const int64_t tw_a = BM * KW, tw_b = BPRE ? BNH * KW * 4 : BNH * KW;  // B tile words (x4 expanded)
+        const uint32_t bits_s = smem_u32(bits), st0 = smem_u32(stages);
+        int slot = 0, bst = 0;
+        uint32_t bph = 0, sph = 0;
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             const int64_t tile = cluster + ti * nclusters;
             int64_t tm, tn;
@@ -319,12 +326,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                     if (issuer) {
                         mbar_arrive_expect_tx(&bars->bfull[slot], BITS_BYTES);
                         bulk_g2s(dst, Ab + ks * tw_a, BITS_A, &bars->bfull[slot]);
-                        bulk_g2s(dst + BITS_A, Bb + ks * tw_b, BITS_B, &bars->bfull[slot]);
+                        if (!BPRE) bulk_g2s(dst + BITS_A, Bb + ks * tw_b, BITS_B, &bars->bfull[slot]);
                     }
                     __syncwarp();
                     if (++slot == D) {
                         slot = 0;
                         bph ^= 1;
+                    }
+                    if constexpr (BPRE) {  // the ready B operand stage, once the MMA has freed it
+                        mbar_wait_sleep(&bars->empty[bst], sph ^ 1, 64);
+                        if (issuer) {
+                            mbar_arrive_expect_tx(&bars->bfullB[bst], B_BYTES);
+                            bulk_g2s(st0 + (uint32_t)(bst * B_BYTES), Bb + ks * tw_b, B_BYTES, &bars->bfullB[bst]);
+                        }
+                        __syncwarp();
+                        if (++bst == S) {
+                            bst = 0;
+                            sph ^= 1;
+                        }
                     }
                 }
             }

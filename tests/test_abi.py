@@ -77,12 +77,13 @@ def test_workspace_sizes():
         return -(-x // q) * q
 
     ws = L.gf2e_slice_mul_workspace(8, 0x11D, 16384, 16384, 16384, 0)
-    assert ws == 27 * (16384 + max(rup(16384, 256), rup(16384, 192))) * 16384 // 8
+    assert ws == 27 * (16384 + 16384) * 16384 // 8  # long k: the 256-column fp4 forms only
     assert L.gf2e_slice_mul_workspace(8, 0x11D, 0, 5, 5, 0) == 0
     assert L.gf2e_slice_mul_workspace(8, 0x11D, 5, 5, 5, 1 << 7) == -1  # bad flag
     assert L.gf2e_slice_mul_workspace(8, 0x11D, 5, 5, 5, _lib.TC_INT8 | _lib.TC_RUN) == -1  # conflicting
-    # m padded to the 256-row CTA-pair tile
-    assert L.gf2e_plane_mul_workspace(100, 1, 300, 0) == (256 * 256 + max(512, 384) * 256) // 8
+    # m padded to the 256-row CTA-pair tile; short k: the running-sum form's B^T is stored
+    # nibble-expanded (4 bits per bit)
+    assert L.gf2e_plane_mul_workspace(100, 1, 300, 0) == (256 * 256 + max(rup(300, 256), rup(300, 192)) * 256 * 4) // 8
 
 
 def test_invalid_arguments_fail_before_device():
