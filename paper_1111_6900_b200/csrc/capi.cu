@@ -382,6 +382,29 @@ cudaError_t launch_form(const Sched &ks, const TcArgs &a, int form, cudaStream_t
     return form == kFormFp4Run ? launch_product_run(ks, a, st) : launch_product_tc2(ks, a, form, st);
 }
 
+// Per host thread and device: a side stream and a fork / join event pair for running the
+// two operand-combination kernels of a product concurrently (created on first use, kept)
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream &side_stream() {
+    thread_local SideStream per_dev[kMaxDevices];
+    static SideStream none;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return none;
+    SideStream &ss = per_dev[dev];
+    if (!ss.s) {
+        if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+            ss = SideStream{};
+            return none;
+        }
+    }
+    return ss;
+}
+
 // The shared launch sequence: K3 combos -> fused K4/K5 product.
 int ensure_fp4_checked();
 
@@ -409,6 +432,15 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
         return fail(GF2E_EINVAL, "workspace must be a 256-byte aligned device pointer");
     uint64_t *Ac = static_cast<uint64_t *>(ws);
     uint64_t *Bx = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + L.a_bytes);
+    // tensor-core forms: the B^T combinations run beside the A combinations on a side stream
+    // (fork / join by events): two small independent kernels, latency-bound at small sizes
+    SideStream no_side;
+    SideStream &side = tc ? side_stream() : no_side;
+    const bool forked = tc && side.s;
+    if (forked) {
+        CKH(cudaEventRecord(side.fork, st), "cudaEventRecord");
+        CKH(cudaStreamWaitEvent(side.s, side.fork, 0), "cudaStreamWaitEvent");
+    }
     CK(launch_combos_rows(ks, A, lda, pa, m, k, Ac, L.kwords, L.a_pstride, L.m_pad, L.kwords, tc ? (fp4 ? 4 : 2) : 0,
                           st),
        "combos(A)");
@@ -424,9 +456,13 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
         g_products += ks.nprod;
         g_kernel = "k_product_m4rm";
     } else {
-        CK(launch_combos_bt(ks, B, ldb, pb, k, n, Bx, L.kwords, L.b_pstride, L.kwords, L.n_pad / 64, fp4, st,
-                            form_br(form), 0, form_bexp(form)),
+        CK(launch_combos_bt(ks, B, ldb, pb, k, n, Bx, L.kwords, L.b_pstride, L.kwords, L.n_pad / 64, fp4,
+                            forked ? side.s : st, form_br(form), 0, form_bexp(form)),
            "combos(B^T)");
+        if (forked) {
+            CKH(cudaEventRecord(side.join, side.s), "cudaEventRecord");
+            CKH(cudaStreamWaitEvent(st, side.join, 0), "cudaStreamWaitEvent");
+        }
         TcArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, m, n, L.m_pad, L.n_pad, C, ldc, pc, acc ? 1 : 0};
         ProfScope prof(st);
         CK(launch_form(ks, a, form, st), "product");
@@ -705,18 +741,14 @@ struct TrsmCtx {
 
 int trsm_rec(TrsmCtx &c, int64_t i0, int64_t i1) {
     const int64_t rows = i1 - i0;
-    const int64_t nw = words_for(c.n);
     const int64_t tb = c.tb;
-    if (rows <= tb) {  // X = inv(T_blk) . B_blk  (tensor-core product), then copy back
+    if (rows <= tb) {  // X = inv(T_blk) . B_blk  (tensor-core product), written over B_blk:
+        // the product reads only its operand combinations, which are formed from B_blk before
+        // the product kernel starts (stream order), so C may alias B here
         const uint64_t *Ib = c.inv + (i0 / tb) * c.e * tb * (tb / 64);
-        if (int rc = run_product(c.ks, Ib, tb / 64, tb * (tb / 64), c.B + i0 * c.ldb, c.ldb, c.pb, c.tmp, nw, tb * nw,
-                                 rows, rows, c.n, 0, c.mulws, c.mulws_bytes, c.st))
-            return rc;
-        for (int t = 0; t < c.e; ++t)
-            CKH(cudaMemcpy2DAsync(c.B + t * c.pb + i0 * c.ldb, c.ldb * 8, c.tmp + t * tb * nw, nw * 8, nw * 8,
-                                  rows, cudaMemcpyDeviceToDevice, c.st),
-                "trsm copy");
-        return GF2E_OK;
+        uint64_t *Bb = c.B + i0 * c.ldb;
+        return run_product(c.ks, Ib, tb / 64, tb * (tb / 64), Bb, c.ldb, c.pb, Bb, c.ldb, c.pb, rows, rows, c.n, 0,
+                           c.mulws, c.mulws_bytes, c.st);
     }
     const int64_t h = i0 + round_up(rows / 2, tb);  // aligned split: plane views stay word aligned
     auto update = [&](int64_t r0, int64_t r1, int64_t k0, int64_t k1) {  // B[r0:r1] ^= T[r0:r1, k0:k1] X[k0:k1]
