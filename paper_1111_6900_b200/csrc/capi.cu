@@ -706,11 +706,13 @@ struct TrsmLayout {
 };
 
 // diagonal block size: 256 when the solve is big enough that leaf products dominate
-int trsm_block(int64_t m, int64_t n) { return (m >= 1024 && n >= 4096) ? 256 : 128; }
+// 256-row diagonal blocks for big solves; e >= 9 keeps 128 (the 256-row inverse kernel runs
+// 1024 threads, whose 64-register budget cannot hold e = 9, 10 rows without spilling)
+int trsm_block(int e, int64_t m, int64_t n) { return (m >= 1024 && n >= 4096 && e <= 8) ? 256 : 128; }
 
 TrsmLayout trsm_layout(int nprod, int e, int64_t m, int64_t n) {
     TrsmLayout T;
-    const int64_t tb = trsm_block(m, n);
+    const int64_t tb = trsm_block(e, m, n);
     T.nblk = (m + tb - 1) / tb;
     T.inv_bytes = align256(T.nblk * e * tb * (tb / 64) * 8);
     T.tmp_bytes = align256((int64_t)e * tb * words_for(n) * 8);
@@ -848,8 +850,13 @@ int ple_rec(PleCtx &c, int64_t r0, int64_t c0, int64_t m, int64_t n, int64_t *P,
         CK(launch_ple_panel(c.e, c.tab, V, c.ld, c.ps, m, (int)n, c.pout, c.st), "ple_panel");
         g_launches += m > ple_window() ? 2 : 1;
         ++c.panels;
-        PanelOut h;
-        CKH(cudaMemcpyAsync(&h, c.pout, offsetof(PanelOut, jcol), cudaMemcpyDeviceToHost, c.st), "cudaMemcpyAsync");
+        struct Head {  // the leading members of PanelOut (rank .. Q)
+            int rank, ndisp, window, pad;
+            int64_t P[64], Q[64];
+        } h;
+        static_assert(sizeof(Head) == offsetof(PanelOut, jcol) && offsetof(Head, Q) == offsetof(PanelOut, Q),
+                      "PanelOut layout");
+        CKH(cudaMemcpyAsync(&h, c.pout, sizeof(Head), cudaMemcpyDeviceToHost, c.st), "cudaMemcpyAsync");
         CKH(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
         rank = h.rank;
         for (int64_t t = 0; t < rank; ++t) {
@@ -1812,7 +1819,7 @@ int trsm_impl(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, in
     const int big = 0x7fffffff;
     CKH(cudaMemcpyAsync(flag, &big, sizeof(int), cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
     CK(launch_tri_inverse(e, f, primitive_element(e, f), T, ldt, pt, m, upper != 0, unit_diag != 0, inv, flag,
-                          trsm_block(m, n), st),
+                          trsm_block(e, m, n), st),
        "tri_inverse");
     int bad = big;
     if (check) {  // PLE corners skip this: their diagonal is the (nonzero) pivots
@@ -1824,7 +1831,7 @@ int trsm_impl(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, in
         return fail(GF2E_ESINGULAR, "zero diagonal entry at index %d", bad);
     }
     TrsmCtx c{to_kernel_sched(e, S), upper != 0, T, ldt, pt, B, ldb, pb, n, inv, tmp, mulws, L.mul_bytes, e, st,
-              trsm_block(m, n)};
+              trsm_block(e, m, n)};
     return trsm_rec(c, 0, m);
 }
 }  // namespace

@@ -133,6 +133,16 @@ cudaError_t launch_scalar_mul(int e, uint32_t f, uint32_t c, int w, const uint64
 
 // ple.cu — PLE base case on one 64-column panel + permutation / mask helpers
 constexpr int kPlePanel = 64;
+// Multiples of a scaled pivot suffix T kept by the PLE panel kernels: x * T = lo[x_lo] ^
+// hi[x_hi], x_lo the low H1 bits of x, x_hi the high H2 (one table of all 2^e multiples for
+// e <= 4).  Q entries of e plane words.
+template <int E>
+struct PleSplit {
+    static constexpr int H1 = E <= 4 ? E : E / 2, H2 = E <= 4 ? 0 : E - E / 2;
+    static constexpr int Q = (1 << H1) + (H2 ? (1 << H2) : 0);
+    static constexpr int QE = Q * E;
+};
+constexpr int kPleTabWords = PleSplit<kMaxE>::QE;
 struct PanelOut {
     int rank, ndisp, window, pad;
     int64_t P[64], Q[64];
@@ -141,6 +151,7 @@ struct PanelOut {
     int dstep[64];
     uint64_t dval[64][kMaxE];
     uint64_t bt[64 * kMaxE * kMaxE];  // alpha^s * T_t, [t][s][plane]
+    uint64_t tabs[64 * kPleTabWords];  // multiples of T_t split by scalar bits, [t][entry][plane]
 };
 // GF(2^e) tables for one field (one device allocation per (device, e, f), ple.cu: field_tab)
 struct FieldTab {

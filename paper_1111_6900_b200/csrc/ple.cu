@@ -76,7 +76,9 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t *win = reinterpret_cast<uint64_t *>(smem);  // [PT][E]
     uint64_t *bt = win + PT * E;                         // [KP][E][E]
-    uint16_t *sinv = reinterpret_cast<uint16_t *>(bt + KP * E * E);  // [2^E] inverses
+    using SP = PleSplit<E>;
+    uint64_t *ptab = bt + KP * E * E;                    // [Q][E]: multiples of the current T_r
+    uint16_t *sinv = reinterpret_cast<uint16_t *>(ptab + SP::QE);  // [2^E] inverses
     uint16_t *smk = sinv + (1 << E);                                   // [2^E][E] multiplication matrices
     __shared__ uint64_t ext[kMaxE];
     __shared__ uint64_t s_dval[KP][kMaxE];
@@ -241,6 +243,20 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
         }
         __syncthreads();
         const uint64_t *btr = bt + r * E * E;
+        // table of the multiples of T_r (entry x of the low / high half: XOR of the basis rows
+        // selected by the bits of x), kept for phase 2 as well
+        for (int idx = tid; idx < SP::QE; idx += PT) {
+            const int x = idx / E, b = idx - (idx / E) * E;
+            const bool hi = x >= (1 << SP::H1);
+            const int xs = hi ? x - (1 << SP::H1) : x, s0 = hi ? SP::H1 : 0;
+            uint64_t acc = 0;
+#pragma unroll
+            for (int q = 0; q < (SP::H1 > SP::H2 ? SP::H1 : SP::H2); ++q)
+                if ((xs >> q) & 1) acc ^= btr[(s0 + q) * E + b];
+            ptab[idx] = acc;
+            out->tabs[r * kPleTabWords + idx] = acc;
+        }
+        __syncthreads();
         if (tid < E) {
             const uint64_t t0 = btr[tid];  // s = 0: the scaled suffix itself
             win[r * E + tid] = (win[r * E + tid] & ~sm) | t0;
@@ -253,7 +269,15 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
             for (int b = 0; b < E; ++b) v[b] = win[s * E + b];
             const uint32_t x = elemE<E>(v, j);
             if (x) {
-                stepE<E>(v, x, btr);
+                const uint64_t *lo = ptab + (x & ((1u << SP::H1) - 1)) * E;
+                if constexpr (SP::H2 > 0) {
+                    const uint64_t *hi = ptab + ((1u << SP::H1) + (x >> SP::H1)) * E;
+#pragma unroll
+                    for (int b = 0; b < E; ++b) v[b] ^= lo[b] ^ hi[b];
+                } else {
+#pragma unroll
+                    for (int b = 0; b < E; ++b) v[b] ^= lo[b];
+                }
 #pragma unroll
                 for (int b = 0; b < E; ++b) win[s * E + b] = v[b];
             }
@@ -305,13 +329,27 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
     }
 }
 
-// phase 2: rows at positions >= window apply the panel's eliminations and the L compression
+// phase 2: rows at positions >= window apply the panel's eliminations and the L compression.
+// Row p is owned by TPR lanes of one warp, lane b holding plane b: the entry at a pivot
+// column is one ballot, and the elimination row ^= x * T_t is two looked-up words of the
+// panel's multiple tables (PanelOut.tabs, staged in shared memory CH pivots at a time).
 template <int E>
-__global__ void __launch_bounds__(256) k_ple_apply(uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t m, int nb,
+struct ApplyShape {
+    static constexpr int THREADS = 512;
+    static constexpr int TPR = E <= 8 ? 8 : 16;      // lanes per row (planes >= E idle)
+    static constexpr int RPC = THREADS / TPR;         // rows per CTA
+    static constexpr int CH = 32;                     // pivots per table chunk
+    static constexpr size_t SMEM = (size_t)CH * PleSplit<E>::QE * 8;
+};
+
+template <int E>
+__global__ void __launch_bounds__(512) k_ple_apply(uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t m, int nb,
                                                    const PanelOut *__restrict__ in) {
-    extern __shared__ __align__(16) uint8_t smem2[];
-    uint64_t *bt = reinterpret_cast<uint64_t *>(smem2);  // [KP][E][E]
-    __shared__ int jc[KP], qc[KP];
+    using A = ApplyShape<E>;
+    using SP = PleSplit<E>;
+    extern __shared__ __align__(16) uint64_t ctab[];  // [CH][Q][E]
+    __shared__ int jc[KP], qc[KP], dst[KP];
+    __shared__ int64_t dps[KP];
     __shared__ int r_s, nd_s, w_s;
     if (threadIdx.x == 0) {
         r_s = in->rank;
@@ -320,36 +358,58 @@ __global__ void __launch_bounds__(256) k_ple_apply(uint64_t *__restrict__ S, int
     }
     __syncthreads();
     const int r = r_s, nd = nd_s;
-    for (int i = threadIdx.x; i < r * E * E; i += blockDim.x) bt[i] = in->bt[i];
-    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    for (int i = threadIdx.x; i < r; i += A::THREADS) {
         jc[i] = in->jcol[i];
         qc[i] = (int)in->Q[i];
     }
-    __syncthreads();
+    for (int i = threadIdx.x; i < nd; i += A::THREADS) {
+        dps[i] = in->dpos[i];
+        dst[i] = in->dstep[i];
+    }
     const uint64_t cmask = nb >= 64 ? ~0ULL : ((1ULL << nb) - 1);
-    for (int64_t p = w_s + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t v[E];
-        int st0 = 0, di = -1;
+    const int lane = threadIdx.x & 31, b = threadIdx.x % A::TPR, gl = lane - b;
+    const int64_t p = w_s + (int64_t)blockIdx.x * A::RPC + threadIdx.x / A::TPR;
+    const bool mine = p < m && b < E;
+    __syncthreads();
+    uint64_t v = 0;
+    int st0 = 0;
+    if (mine) {
+        int di = -1;
         for (int d = 0; d < nd; ++d)
-            if (in->dpos[d] == p) di = d;
+            if (dps[d] == p) di = d;
         if (di >= 0) {
-#pragma unroll
-            for (int b = 0; b < E; ++b) v[b] = in->dval[di][b];
-            st0 = in->dstep[di];
+            v = in->dval[di][b];
+            st0 = dst[di];
         } else {
-#pragma unroll
-            for (int b = 0; b < E; ++b) v[b] = S[b * ps + p * ld] & cmask;
+            v = S[b * ps + p * ld] & cmask;
         }
-        for (int t = st0; t < r; ++t) stepE<E>(v, elemE<E>(v, jc[t]), bt + t * E * E);
+    }
+    for (int c0 = 0; c0 < r; c0 += A::CH) {
+        const int c1 = c0 + A::CH < r ? c0 + A::CH : r;
+        if (c0) __syncthreads();  // the previous chunk's readers are done
+        const uint64_t *src = in->tabs + (size_t)c0 * kPleTabWords;
+        for (int i = threadIdx.x; i < (c1 - c0) * SP::QE; i += A::THREADS) {
+            const int t = i / SP::QE;
+            ctab[i] = src[(size_t)t * kPleTabWords + (i - t * SP::QE)];
+        }
+        __syncthreads();
+        for (int t = c0; t < c1; ++t) {
+            const unsigned bal = __ballot_sync(0xffffffffu, (v >> jc[t]) & 1ULL);
+            const uint32_t x = (bal >> gl) & ((1u << E) - 1);
+            if (mine && t >= st0 && x) {
+                const uint64_t *tt = ctab + (size_t)(t - c0) * SP::QE;
+                if constexpr (SP::H2 > 0)
+                    v ^= tt[(x & ((1u << SP::H1) - 1)) * E + b] ^ tt[((1u << SP::H1) + (x >> SP::H1)) * E + b];
+                else
+                    v ^= tt[x * E + b];
+            }
+        }
+    }
+    if (mine) {
         for (int t = 0; t < r; ++t)
-            if (qc[t] != t)
-#pragma unroll
-                for (int b = 0; b < E; ++b) v[b] = swap_bits(v[b], t, qc[t]);
-#pragma unroll
-        for (int b = 0; b < E; ++b) {
-            uint64_t *d = S + b * ps + p * ld;
-            *d = (*d & ~cmask) | v[b];
-        }
+            if (qc[t] != t) v = swap_bits(v, t, qc[t]);
+        uint64_t *d = S + b * ps + p * ld;
+        *d = (*d & ~cmask) | v;
     }
 }
 
@@ -522,8 +582,8 @@ inline int grid_for(int64_t total, int threads) {
 template <int E>
 cudaError_t launch_ple_e(const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb, PanelOut *out,
                          cudaStream_t st) {
-    const int smem = (PT * E + KP * E * E) * 8 + (1 << E) * (E + 1) * 2;
-    const int smem2 = KP * E * E * 8;
+    const int smem = (PT * E + KP * E * E + PleSplit<E>::QE) * 8 + (1 << E) * (E + 1) * 2;
+    const int smem2 = (int)ApplyShape<E>::SMEM;
     // launch attributes once per instantiation and device (idempotent)
     static bool attr_set[kMaxDevices] = {};
     int dev = 0;
@@ -539,7 +599,8 @@ cudaError_t launch_ple_e(const FieldTab *tab, uint64_t *S, int64_t ld, int64_t p
     k_ple_find<E><<<1, PT, smem, st>>>(tab, S, ld, ps, m, nb, out);
     err = cudaGetLastError();
     if (err != cudaSuccess || m <= PT) return err;
-    k_ple_apply<E><<<grid_for(m - PT, 256), 256, smem2, st>>>(S, ld, ps, m, nb, out);
+    using A = ApplyShape<E>;
+    k_ple_apply<E><<<(unsigned)((m - PT + A::RPC - 1) / A::RPC), A::THREADS, smem2, st>>>(S, ld, ps, m, nb, out);
     return cudaGetLastError();
 }
 

@@ -6,6 +6,8 @@
 //   * k_scalar_mul: packed multiplication by a scalar (mat_packed.py:192-199).
 // Field arithmetic uses the per-field tables of ple.cu (field_tab: inverses, multiplication
 // matrices; the scalar kernels build their own small tables).
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -23,127 +25,185 @@ __device__ __forceinline__ uint32_t gf_mul_slow(uint32_t a, uint32_t b, int e, u
 }
 
 
-// Inverse of each 128 x 128 diagonal block by bitsliced substitution: thread k owns row k of
-// the block and of its inverse X (two words per plane each, in registers).  Lower triangular:
-// for i = 0 .. rows-1, thread i finalises X_i = T_ii^-1 X_i and publishes it; every thread
-// k > i then adds T_ki * X_i (T's own entries are the multipliers: X_k = T_kk^-1 (e_k -
-// sum_{i<k} T_ki X_i)).  Upper: the same from the bottom.  Scalar * bitsliced word uses the
-// field's multiplication matrices (FieldTab.mulmask: plane b of c*v = XOR of the planes in
-// mulmask[c][b]).
-template <int E, int TB>  // TB = diagonal block rows = threads
-__global__ void __launch_bounds__(TB) k_tri_inverse(const FieldTab *__restrict__ ftab, const uint64_t *__restrict__ T,
-                                                   int64_t ldt, int64_t pt, int64_t m, int upper, int unit,
-                                                   uint64_t *__restrict__ Tinv, int *__restrict__ bad_row) {
-    constexpr int NW = TB / 64;           // plane words per block row
-    __shared__ uint64_t pub[2][NW][E];    // the published row X_i, double-buffered by step parity
+// Inverse of each TB x TB diagonal block by bitsliced substitution.  Lower triangular: for
+// i = 0 .. rows-1, row i of X is final and published; every row k > i adds U_ki * X_i (U =
+// T D^-1 unit triangular, so T^-1 = D^-1 U^-1 and each row is scaled once at the end).  Upper:
+// the same from the bottom.
+//   * Row k of X is owned by TPR = NW * BS consecutive threads, one per (plane word w, group h
+//     of PB planes): 512 threads for TB = 128, 1024 for TB = 256.
+//   * The multipliers U_ki are computed once up front into shared memory (cU, column-major so
+//     the rows of a warp read consecutive entries).
+//   * Per step the CTA builds, from the published X_i, the table of its scalar multiples split
+//     by the low H1 / high H2 bits of the scalar (c * X_i = lo[c_lo] ^ hi[c_hi], 2^H1 + 2^H2
+//     entries, FieldTab.mulmask: plane b of c*v = XOR of the planes in mulmask[c][b]); each
+//     row then adds two looked-up words per plane instead of an e x e plane product.
+// Two barriers per step: X_i published -> table built -> table consumed (and X_i+1 final).
+template <int E, int TB>
+struct TriShape {
+    static constexpr int NW = TB / 64;            // plane words per block row
+    static constexpr int BS = TB == 128 ? 2 : 1;  // plane groups per row
+    static constexpr int TPR = NW * BS;           // threads per row
+    static constexpr int THREADS = TB * TPR;
+    static constexpr int PB = (E + BS - 1) / BS;  // planes per thread
+    static constexpr int H1 = E <= 4 ? E : E / 2, H2 = E <= 4 ? 0 : E - E / 2;
+    static constexpr int Q = (1 << H1) + (H2 ? (1 << H2) : 0);  // table entries
+    static constexpr int TW = Q * E * NW;                        // table words
+    static constexpr int NB = (TW + THREADS - 1) / THREADS;      // table words per thread
+    using CT = typename std::conditional<(E <= 8), uint8_t, uint16_t>::type;
+    static constexpr size_t SMEM = (size_t)TW * 8 + (size_t)NW * E * 8 + (size_t)TB * TB * sizeof(CT);
+};
+
+template <int E, int TB>
+__global__ void __launch_bounds__(TriShape<E, TB>::THREADS)
+    k_tri_inverse(const FieldTab *__restrict__ ftab, const uint64_t *__restrict__ T, int64_t ldt, int64_t pt,
+                  int64_t m, int upper, int unit, uint64_t *__restrict__ Tinv, int *__restrict__ bad_row) {
+    using S = TriShape<E, TB>;
+    using CT = typename S::CT;
+    constexpr int NW = S::NW, TPR = S::TPR, PB = S::PB, H1 = S::H1;
+    extern __shared__ __align__(16) uint64_t dsm[];
+    uint64_t *tab = dsm;                                    // [Q][E][NW]
+    uint64_t *pub = tab + S::TW;                            // [NW][E]: the published row X_i
+    CT *cU = reinterpret_cast<CT *>(pub + NW * E);          // [TB (step)][TB (row)]
     __shared__ uint16_t sinv[1 << E], smk[(1 << E) * E], sex[1 << E], slg[1 << E], sdlog[TB];
-    constexpr int ORD = (1 << E) - 1;     // multiplicative group order
-    for (int i = threadIdx.x; i < (1 << E); i += TB) {
+    constexpr int ORD = (1 << E) - 1;  // multiplicative group order
+    for (int i = threadIdx.x; i < (1 << E); i += S::THREADS) {
         sinv[i] = ftab->inv[i];
         sex[i] = ftab->ex[i < ORD ? i : 0];
         slg[i] = ftab->lg[i];
 #pragma unroll
         for (int b = 0; b < E; ++b) smk[i * E + b] = ftab->mulmask[i][b];
     }
-    __syncthreads();
     const int64_t r0 = (int64_t)blockIdx.x * TB;
     const int rows = (int)((m - r0) < TB ? (m - r0) : TB);
-    const int k = threadIdx.x;
-    uint64_t t[E][NW], x[E][NW];
+    const int k = threadIdx.x / TPR, sub = threadIdx.x % TPR;
+    const int w = sub % NW, h = sub / NW, b0 = h * PB;
+    uint64_t t[E], x[PB];  // word w of every plane of row k of T; my planes of X
 #pragma unroll
-    for (int b = 0; b < E; ++b)
+    for (int b = 0; b < E; ++b) t[b] = 0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            t[b][w] = 0;
-            x[b][w] = 0;
-        }
+    for (int j = 0; j < PB; ++j) x[j] = 0;
     if (k < rows) {
         const uint64_t *src = T + (r0 + k) * ldt + (r0 >> 6);
-        const int nw = (rows + 63) >> 6;
+        if (w < ((rows + 63) >> 6)) {
 #pragma unroll
-        for (int b = 0; b < E; ++b)
-#pragma unroll
-            for (int w = 0; w < NW; ++w)
-                if (w < nw) t[b][w] = src[b * pt + w];
-#pragma unroll
-        for (int w = 0; w < NW; ++w) x[0][w] = ((k >> 6) == w) ? (1ULL << (k & 63)) : 0ULL;  // identity row
+            for (int b = 0; b < E; ++b) t[b] = src[b * pt + w];
+        }
+        if (h == 0 && (k >> 6) == w) x[0] = 1ULL << (k & 63);  // identity row
     }
-    auto entry = [&](int c) {  // T[k][c] as a field element
+    auto entry = [&](int c) {  // T[k][c] for c in this thread's word
         uint32_t v = 0;
 #pragma unroll
-        for (int b = 0; b < E; ++b) {
-            uint64_t wv = t[b][0];
-#pragma unroll
-            for (int w = 1; w < NW; ++w)
-                if ((c >> 6) == w) wv = t[b][w];
-            v |= (uint32_t)((wv >> (c & 63)) & 1ULL) << b;
-        }
+        for (int b = 0; b < E; ++b) v |= (uint32_t)((t[b] >> (c & 63)) & 1ULL) << b;
         return v;
     };
-    // T = U D with D = diag(T) and U = T D^-1 unit triangular, so T^-1 = D^-1 U^-1: the
-    // substitution runs on U (multipliers T_ki / T_ii, from the log tables) with no scaling on
-    // the per-row critical path, and each thread scales its own row of the result at the end.
-    const uint32_t dk = k < rows ? entry(k) : 1u;
-    if (!unit && k < rows && dk == 0) atomicMin(bad_row, (int)(r0 + k));
-    sdlog[k] = (unit || dk == 0) ? 0 : slg[dk];
-    __syncthreads();
+    __syncthreads();  // field tables
+    uint32_t dk = 1;  // T_kk (thread of the word holding column k)
+    if (k < rows && w == (k >> 6)) {
+        dk = entry(k);
+        if (!unit && dk == 0 && h == 0) atomicMin(bad_row, (int)(r0 + k));
+        if (h == 0) sdlog[k] = (unit || dk == 0) ? 0 : slg[dk];
+    }
+    dk = __shfl_sync(0xffffffffu, dk, ((threadIdx.x & 31) - sub) + (k >> 6) % NW);
+    __syncthreads();  // sdlog
+    // multipliers: this thread's half (h) of the 64 columns of its word
+    {
+        constexpr int CPT = 64 / S::BS;
+        for (int cc = 0; cc < CPT; ++cc) {
+            const int i = w * 64 + h * CPT + cc;
+            if (i >= TB) break;
+            uint32_t c = 0;
+            const bool below = k < rows && i < rows && (upper ? (k < i) : (k > i));
+            if (below) {
+                c = entry(i);
+                if (c && !unit) {  // U_ki = T_ki / T_ii
+                    int l = (int)slg[c] - (int)sdlog[i];
+                    c = sex[l < 0 ? l + ORD : l];
+                }
+            }
+            cU[i * TB + k] = (CT)c;
+        }
+    }
+    // this thread's table words: entry x, plane b, word wt; its multiplication mask is fixed
+    uint32_t tmask[S::NB];
+#pragma unroll
+    for (int q = 0; q < S::NB; ++q) {
+        const int idx = threadIdx.x + q * S::THREADS;
+        tmask[q] = 0;
+        if (idx < S::TW) {
+            const int xq = idx / (E * NW), b = (idx / NW) % E;
+            const uint32_t c = xq < (1 << H1) ? (uint32_t)xq : (uint32_t)(xq - (1 << H1)) << H1;
+            tmask[q] = smk[c * E + b];
+        }
+    }
+    __syncthreads();  // cU
     for (int step = 0; step < rows; ++step) {
         const int i = upper ? rows - 1 - step : step;
         if (k == i) {  // X_i of U^-1 is final as it stands
 #pragma unroll
-            for (int w = 0; w < NW; ++w)
-#pragma unroll
-                for (int b = 0; b < E; ++b) pub[step & 1][w][b] = x[b][w];
+            for (int j = 0; j < PB; ++j)
+                if (b0 + j < E) pub[w * E + b0 + j] = x[j];
         }
-        // one barrier per row: pub[step & 1] is rewritten two steps later, after every reader
-        // of this step has passed the next step's barrier
-        __syncthreads();
-        const bool below = upper ? (k < i) : (k > i && k < rows);
-        if (below) {
-            uint32_t c = entry(i);
-            if (c && !unit) {  // U_ki = T_ki / T_ii
-                int l = (int)slg[c] - (int)sdlog[i];
-                c = sex[l < 0 ? l + ORD : l];
-            }
-            if (c) {
+        const uint32_t c = cU[i * TB + k];
+        __syncthreads();  // X_i published
 #pragma unroll
-                for (int b = 0; b < E; ++b) {
-                    const uint32_t mk = smk[c * E + b];
+        for (int q = 0; q < S::NB; ++q) {
+            const int idx = threadIdx.x + q * S::THREADS;
+            if (idx < S::TW) {
+                const uint64_t *pv = pub + (idx % NW) * E;
+                uint64_t acc = 0;
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) {
-                        uint64_t acc = 0;
-#pragma unroll
-                        for (int p = 0; p < E; ++p) acc ^= pub[step & 1][w][p] & (0ULL - (uint64_t)((mk >> p) & 1u));
-                        x[b][w] ^= acc;
-                    }
-                }
+                for (int p = 0; p < E; ++p) acc ^= pv[p] & (0ULL - (uint64_t)((tmask[q] >> p) & 1u));
+                tab[idx] = acc;
             }
         }
+        __syncthreads();  // table built
+        if (c) {
+            const uint64_t *lo = tab + (size_t)(c & ((1u << H1) - 1)) * E * NW + w;
+            if constexpr (S::H2 > 0) {
+                const uint64_t *hi = tab + (size_t)((1u << H1) + (c >> H1)) * E * NW + w;
+#pragma unroll
+                for (int j = 0; j < PB; ++j)
+                    if (b0 + j < E) x[j] ^= lo[(b0 + j) * NW] ^ hi[(b0 + j) * NW];
+            } else {
+#pragma unroll
+                for (int j = 0; j < PB; ++j)
+                    if (b0 + j < E) x[j] ^= lo[(b0 + j) * NW];
+            }
+        }
+        // the next step's publish and table build come after its first barrier, which every
+        // reader of this step's table has passed
     }
-    if (!unit && k < rows) {  // row k of T^-1 = T_kk^-1 * row k of U^-1
+    if (!unit) {  // row k of T^-1 = T_kk^-1 * row k of U^-1 (needs all planes of word w)
+        uint64_t full[E];
+        if constexpr (S::BS == 1) {
+#pragma unroll
+            for (int p = 0; p < E; ++p) full[p] = x[p];
+        } else {
+            uint64_t other[PB];
+#pragma unroll
+            for (int j = 0; j < PB; ++j) other[j] = __shfl_xor_sync(0xffffffffu, x[j], NW);
+#pragma unroll
+            for (int p = 0; p < E; ++p)
+                full[p] = (p < PB) ? (h == 0 ? x[p % PB] : other[p % PB]) : (h == 0 ? other[p % PB] : x[p % PB]);
+        }
         uint32_t c = sinv[dk];
         if (c == 0) c = 1;  // singular block: reported above, result unused
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            uint64_t y[E];
-#pragma unroll
-            for (int b = 0; b < E; ++b) {
-                const uint32_t mk = smk[c * E + b];
+        for (int j = 0; j < PB; ++j) {
+            if (b0 + j < E) {
+                const uint32_t mk = smk[c * E + b0 + j];
                 uint64_t acc = 0;
 #pragma unroll
-                for (int p = 0; p < E; ++p) acc ^= x[p][w] & (0ULL - (uint64_t)((mk >> p) & 1u));
-                y[b] = acc;
+                for (int p = 0; p < E; ++p) acc ^= full[p] & (0ULL - (uint64_t)((mk >> p) & 1u));
+                x[j] = acc;
             }
-#pragma unroll
-            for (int b = 0; b < E; ++b) x[b][w] = y[b];
         }
     }
     // Tinv block = e planes of TB rows x NW words
     uint64_t *out = Tinv + (int64_t)blockIdx.x * E * TB * NW;
 #pragma unroll
-    for (int b = 0; b < E; ++b)
-#pragma unroll
-        for (int w = 0; w < NW; ++w) out[(int64_t)b * TB * NW + k * NW + w] = (k < rows) ? x[b][w] : 0;
+    for (int j = 0; j < PB; ++j)
+        if (b0 + j < E) out[(int64_t)(b0 + j) * TB * NW + k * NW + w] = (k < rows) ? x[j] : 0;
 }
 
 // mat_sliced.py:109-122: slices shift up one degree, the top slice folds into the slices
@@ -193,8 +253,18 @@ inline int grid_for(int64_t total, int threads) {
 template <int E, int TB>
 cudaError_t launch_tri_e(const FieldTab *ftab, const uint64_t *T, int64_t ldt, int64_t pt, int64_t m, bool upper,
                          bool unit, uint64_t *Tinv, int *bad_row, int64_t nblk, cudaStream_t st) {
-    k_tri_inverse<E, TB><<<(unsigned)nblk, TB, 0, st>>>(ftab, T, ldt, pt, m, upper ? 1 : 0, unit ? 1 : 0, Tinv,
-                                                        bad_row);
+    using S = TriShape<E, TB>;
+    static bool attr_set[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= kMaxDevices || !attr_set[dev]) {
+        cudaError_t err = cudaFuncSetAttribute(k_tri_inverse<E, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)S::SMEM);
+        if (err != cudaSuccess) return err;
+        if (dev < kMaxDevices) attr_set[dev] = true;
+    }
+    k_tri_inverse<E, TB><<<(unsigned)nblk, S::THREADS, S::SMEM, st>>>(ftab, T, ldt, pt, m, upper ? 1 : 0,
+                                                                      unit ? 1 : 0, Tinv, bad_row);
     return cudaGetLastError();
 }
 
@@ -211,8 +281,12 @@ cudaError_t launch_tri_tb(int e, const FieldTab *ftab, const uint64_t *T, int64_
         case 6: return launch_tri_e<6, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
         case 7: return launch_tri_e<7, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
         case 8: return launch_tri_e<8, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
-        case 9: return launch_tri_e<9, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
-        case 10: return launch_tri_e<10, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 9:
+            if constexpr (TB == 256) return cudaErrorInvalidValue;  // 128-row blocks only (trsm_block)
+            else return launch_tri_e<9, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
+        case 10:
+            if constexpr (TB == 256) return cudaErrorInvalidValue;  // 128-row blocks only (trsm_block)
+            else return launch_tri_e<10, TB>(ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, nblk, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -221,7 +295,7 @@ cudaError_t launch_tri_inverse(int e, uint32_t f, uint32_t g, const uint64_t *T,
                                bool upper, bool unit, uint64_t *Tinv, int *bad_row, int block, cudaStream_t st) {
     const FieldTab *ftab = field_tab(e, f, g);
     if (!ftab) return cudaErrorUnknown;
-    if (block == 256) return launch_tri_tb<256>(e, ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, st);
+    if (block == 256 && e <= 8) return launch_tri_tb<256>(e, ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, st);
     if (block == 128) return launch_tri_tb<128>(e, ftab, T, ldt, pt, m, upper, unit, Tinv, bad_row, st);
     return cudaErrorInvalidValue;
 }

@@ -20,7 +20,12 @@ def main():
         text=True).stdout)))
     hdr = src[1]
     ix = {h: i for i, h in enumerate(hdr)}
-    rows = [r for r in src[2:] if len(r) == len(hdr)]
+    rows = []
+    for r in src[2:]:  # first kernel of the report only (a later one repeats the header)
+        if len(r) == len(hdr) and r[ix["Address"]] == "Address":
+            break
+        if len(r) == len(hdr):
+            rows.append(r)
     base = int(rows[0][ix["Address"]], 16)
     samples = {int(r[ix["Address"]], 16) - base: int(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in rows}
     execd = {int(r[ix["Address"]], 16) - base: int(r[ix["Instructions Executed"]] or 0) for r in rows}
