@@ -147,6 +147,18 @@ int gf2e_nj_mul(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, const uin
                 uint64_t *C_dev, int64_t ldc, int64_t m, int64_t k, int64_t n, uint32_t flags, void *stream);
 
 /*
+ * The same Newton-John product on bit planes (sliced operands, strides as gf2e_slice_mul): the
+ * CUDA-core form that PLE's Schur updates and TRSM's updates take up to GF2E_NJS_MAXK (default
+ * 128) inner dimension.  Per 64-column word of C and block of rows, tables of the multiples of
+ * 32 rows of B at a time (split by the scalar's low / high bits) in shared memory; the entry
+ * A[r][i] is one warp ballot over the plane lanes of row r.  No workspace.  C must not overlap
+ * A or B.  flags: GF2E_ACCUMULATE.
+ */
+int gf2e_nj_slice_mul(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, int64_t pa, const uint64_t *B_dev,
+                      int64_t ldb, int64_t pb, uint64_t *C_dev, int64_t ldc, int64_t pc, int64_t m, int64_t k,
+                      int64_t n, uint32_t flags, void *stream);
+
+/*
  * gf2e_slice_mul with B arriving in column parts — the multi-GPU form (dist.sharded_mul: B is
  * broadcast over NVLink part by part while this rank already multiplies the parts that
  * arrived).  Part p holds columns [col_bounds[p], col_bounds[p+1]) of B as its own plane

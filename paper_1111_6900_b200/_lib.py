@@ -48,6 +48,8 @@ SIGNATURES = {
     "gf2e_slice_mul": (_INT, [_INT, _U32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64,
                               _U32, _P, _I64, _P]),
     "gf2e_nj_mul": (_INT, [_INT, _U32, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _U32, _P]),
+    "gf2e_nj_slice_mul": (_INT, [_INT, _U32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64,
+                                 _U32, _P]),
     "gf2e_slice_mul_parts": (_INT, [_INT, _U32, _P, _I64, _I64, _INT, ctypes.POINTER(_I64), ctypes.POINTER(_P),
                                     ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_P), _P, _I64, _I64,
                                     _I64, _I64, _I64, _U32, _P, _I64, _P]),

@@ -425,6 +425,8 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
         if (int rc = ensure_fp4_checked()) return rc;
     const int form = form_override >= 0 ? form_override : tc_form(flags, k, ks.nprod);
     const bool fp4 = tc && form != kFormI8;
+    static const bool trace = getenv("GF2E_PROD_TRACE") != nullptr;
+    if (trace) fprintf(stderr, "product m=%lld k=%lld n=%lld form=%d\n", (long long)m, (long long)k, (long long)n, form);
     Layout L = layout_for(ks.nprod, m, k, n, flags, form);
     if (ws_bytes < L.total)
         return fail(GF2E_ENOMEM, "workspace too small: %lld < %lld bytes", (long long)ws_bytes, (long long)L.total);
@@ -726,6 +728,29 @@ TrsmLayout trsm_layout(int nprod, int e, int64_t m, int64_t n) {
     return T;
 }
 
+// Small updates of the consumers (PLE Schur complements, TRSM updates and leaves) run on CUDA
+// cores through the sliced Newton-John kernel when the inner dimension is small: one launch
+// instead of two operand-combination launches and a tensor-core product, whose fixed cost
+// dominates there (the reference likewise multiplies small blocks with Newton-John tables
+// below its crossover).  GF2E_NJS_MAXK overrides the crossover (measured, profiles/r02).
+int64_t nj_sliced_max_k() {
+    static const int64_t v = getenv("GF2E_NJS_MAXK") ? atoll(getenv("GF2E_NJS_MAXK")) : 128;
+    return v;
+}
+
+int run_update(const Sched &ks, int e, const FieldTab *tab, const uint64_t *A, int64_t lda, int64_t pa,
+               const uint64_t *B, int64_t ldb, int64_t pb, uint64_t *C, int64_t ldc, int64_t pc, int64_t m,
+               int64_t k, int64_t n, uint32_t flags, void *ws, int64_t ws_bytes, cudaStream_t st,
+               bool c_aliases_b = false) {
+    if (tab && m > 0 && n > 0 && k > 0 && k <= nj_sliced_max_k() && (!c_aliases_b || m <= nj_sliced_alias_rows(e))) {
+        CK(launch_nj_sliced(e, tab, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, (flags & GF2E_ACCUMULATE) != 0,
+                            c_aliases_b, st),
+           "nj_sliced");
+        return GF2E_OK;
+    }
+    return run_product(ks, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, flags, ws, ws_bytes, st);
+}
+
 struct TrsmCtx {
     Sched ks;
     bool upper;
@@ -739,6 +764,7 @@ struct TrsmCtx {
     int e;
     cudaStream_t st;
     int64_t tb;  // diagonal block rows
+    const FieldTab *tab;
 };
 
 int trsm_rec(TrsmCtx &c, int64_t i0, int64_t i1) {
@@ -749,14 +775,14 @@ int trsm_rec(TrsmCtx &c, int64_t i0, int64_t i1) {
         // the product kernel starts (stream order), so C may alias B here
         const uint64_t *Ib = c.inv + (i0 / tb) * c.e * tb * (tb / 64);
         uint64_t *Bb = c.B + i0 * c.ldb;
-        return run_product(c.ks, Ib, tb / 64, tb * (tb / 64), Bb, c.ldb, c.pb, Bb, c.ldb, c.pb, rows, rows, c.n, 0,
-                           c.mulws, c.mulws_bytes, c.st);
+        return run_update(c.ks, c.e, c.tab, Ib, tb / 64, tb * (tb / 64), Bb, c.ldb, c.pb, Bb, c.ldb, c.pb, rows, rows,
+                          c.n, 0, c.mulws, c.mulws_bytes, c.st, true);
     }
     const int64_t h = i0 + round_up(rows / 2, tb);  // aligned split: plane views stay word aligned
     auto update = [&](int64_t r0, int64_t r1, int64_t k0, int64_t k1) {  // B[r0:r1] ^= T[r0:r1, k0:k1] X[k0:k1]
-        return run_product(c.ks, c.T + r0 * c.ldt + k0 / 64, c.ldt, c.pt, c.B + k0 * c.ldb, c.ldb, c.pb,
-                           c.B + r0 * c.ldb, c.ldb, c.pb, r1 - r0, k1 - k0, c.n, GF2E_ACCUMULATE, c.mulws,
-                           c.mulws_bytes, c.st);
+        return run_update(c.ks, c.e, c.tab, c.T + r0 * c.ldt + k0 / 64, c.ldt, c.pt, c.B + k0 * c.ldb, c.ldb, c.pb,
+                          c.B + r0 * c.ldb, c.ldb, c.pb, r1 - r0, k1 - k0, c.n, GF2E_ACCUMULATE, c.mulws,
+                          c.mulws_bytes, c.st);
     };
     if (c.upper) {  // ple_echelon.py:201-217 order: bottom block, update top, top block
         if (int rc = trsm_rec(c, h, i1)) return rc;
@@ -896,8 +922,8 @@ int ple_rec(PleCtx &c, int64_t r0, int64_t c0, int64_t m, int64_t n, int64_t *P,
             const int64_t mws = gf2e_slice_mul_workspace(c.e, c.f, m - r1, r1, nr, GF2E_ACCUMULATE);
             DevTmp mw((size_t)(mws > 0 ? mws : 256), c.st);
             if (!mw.p) return fail(GF2E_ENOMEM, "out of device memory (PLE update workspace)");
-            if (int rc = run_product(c.ks, V + r1 * c.ld, c.ld, c.ps, R, c.ld, c.ps, R + r1 * c.ld, c.ld, c.ps, m - r1,
-                                     r1, nr, GF2E_ACCUMULATE, mw.p, mws, c.st))
+            if (int rc = run_update(c.ks, c.e, c.tab, V + r1 * c.ld, c.ld, c.ps, R, c.ld, c.ps, R + r1 * c.ld, c.ld, c.ps,
+                                    m - r1, r1, nr, GF2E_ACCUMULATE, mw.p, mws, c.st))
                 return rc;
         }
     }
@@ -989,8 +1015,8 @@ int ple_rec_spec(PleSpec &c, int64_t r0, int64_t c0, int64_t m, int64_t n) {
             const int64_t mws = gf2e_slice_mul_workspace(c.e, c.f, m - r1, r1, nr, GF2E_ACCUMULATE);
             DevTmp mw((size_t)(mws > 0 ? mws : 256), c.st);
             if (!mw.p) return fail(GF2E_ENOMEM, "out of device memory (PLE update workspace)");
-            if (int rc = run_product(c.ks, V + r1 * c.ld, c.ld, c.ps, R, c.ld, c.ps, R + r1 * c.ld, c.ld, c.ps, m - r1,
-                                     r1, nr, GF2E_ACCUMULATE, mw.p, mws, c.st))
+            if (int rc = run_update(c.ks, c.e, c.tab, V + r1 * c.ld, c.ld, c.ps, R, c.ld, c.ps, R + r1 * c.ld, c.ld, c.ps,
+                                    m - r1, r1, nr, GF2E_ACCUMULATE, mw.p, mws, c.st))
                 return rc;
         }
     }
@@ -1429,6 +1455,34 @@ int gf2e_slice_mul(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa
     return run_product(ks, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, flags, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int gf2e_nj_slice_mul(int e, uint32_t f, const uint64_t *A, int64_t lda, int64_t pa, const uint64_t *B, int64_t ldb,
+                      int64_t pb, uint64_t *C, int64_t ldc, int64_t pc, int64_t m, int64_t k, int64_t n,
+                      uint32_t flags, void *stream) {
+    g_err.clear();
+    g_launches = 0;
+    g_products = 0;
+    if (int rc = check_field(e, f)) return rc;
+    if (flags & ~GF2E_ACCUMULATE) return fail(GF2E_EINVAL, "gf2e_nj_slice_mul: unsupported flags 0x%x", flags);
+    if (int rc = check_mat(A, m, words_for(k), lda, "A")) return rc;
+    if (int rc = check_mat(B, k, words_for(n), ldb, "B")) return rc;
+    if (int rc = check_mat(C, m, words_for(n), ldc, "C")) return rc;
+    if (m == 0 || n == 0) return GF2E_OK;
+    if (int rc = check_device()) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool acc = (flags & GF2E_ACCUMULATE) != 0;
+    if (k == 0) {
+        if (!acc)
+            for (int j = 0; j < e; ++j)
+                CK(cudaMemset2DAsync(C + j * pc, ldc * 8, 0, words_for(n) * 8, m, st), "cudaMemset2DAsync");
+        return GF2E_OK;
+    }
+    const FieldTab *tab = field_tab(e, f, primitive_element(e, f));
+    if (!tab) return fail(GF2E_ECUDA, "field table upload failed");
+    CK(launch_nj_sliced(e, tab, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, acc, false, st), "nj_sliced");
+    g_kernel = "k_nj_sliced";
+    return GF2E_OK;
+}
+
 int gf2e_nj_mul(int e, uint32_t f, const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, uint64_t *C,
                 int64_t ldc, int64_t m, int64_t k, int64_t n, uint32_t flags, void *stream) {
     g_err.clear();
@@ -1831,7 +1885,7 @@ int trsm_impl(int e, uint32_t f, int upper, int unit_diag, const uint64_t *T, in
         return fail(GF2E_ESINGULAR, "zero diagonal entry at index %d", bad);
     }
     TrsmCtx c{to_kernel_sched(e, S), upper != 0, T, ldt, pt, B, ldb, pb, n, inv, tmp, mulws, L.mul_bytes, e, st,
-              trsm_block(e, m, n)};
+              trsm_block(e, m, n), field_tab(e, f, primitive_element(e, f))};
     return trsm_rec(c, 0, m);
 }
 }  // namespace

@@ -99,6 +99,13 @@ cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, int form, cudaSt
 
 // packed-domain Newton-John product for small blocks (nj.cu): rows of B at most kNjMaxWords words
 constexpr int kNjMaxWords = 16;
+struct FieldTab;
+// sliced Newton-John product (nj.cu): C (^)= A * B on bit planes, CUDA cores, one launch;
+// c_aliases_b: C == B allowed (one row block per column word, m <= 256 rows)
+inline int nj_sliced_alias_rows(int e) { return 4 * (512 / (e <= 8 ? 8 : 16)); }
+cudaError_t launch_nj_sliced(int e, const FieldTab *ftab, const uint64_t *A, int64_t lda, int64_t pa,
+                             const uint64_t *B, int64_t ldb, int64_t pb, uint64_t *C, int64_t ldc, int64_t pc,
+                             int64_t m, int64_t k, int64_t n, bool acc, bool c_aliases_b, cudaStream_t st);
 cudaError_t launch_nj_mul(int e, uint32_t f, int w, const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,
                           uint64_t *C, int64_t ldc, int64_t m, int64_t k, int64_t n, bool acc, cudaStream_t st);
 
@@ -150,13 +157,13 @@ struct PanelOut {
     int64_t dpos[64];
     int dstep[64];
     uint64_t dval[64][kMaxE];
-    uint64_t bt[64 * kMaxE * kMaxE];  // alpha^s * T_t, [t][s][plane]
     uint64_t tabs[64 * kPleTabWords];  // multiples of T_t split by scalar bits, [t][entry][plane]
 };
 // GF(2^e) tables for one field (one device allocation per (device, e, f), ple.cu: field_tab)
 struct FieldTab {
     uint16_t ex[1024], lg[1024], inv[1024];  // exp/log over a primitive element; inverses
     uint16_t mulmask[1024][kMaxE];           // bit p of [c][b] = coefficient b of c * x^p
+    uint32_t mulmask2[1024][kMaxE];          // the same for p < 2e - 1 (c * x^s * x^p: >> s)
     uint32_t f;                              // the field polynomial (bit e set)
 };
 const FieldTab *field_tab(int e, uint32_t f, uint32_t g);  // device pointer (synchronous fill)

@@ -148,6 +148,144 @@ cudaError_t launch_nj_e(uint32_t f, int w, const uint64_t *A, int64_t lda, const
     return cudaGetLastError();
 }
 
+// ---- the same algorithm on bit planes (sliced operands): small updates of PLE and TRSM ----
+// C (^)= A * B with A m x k, B k x n, C m x n as e bit planes.  CTA (column word w, row block):
+// for each chunk of KC rows of B, the tables of multiples of those rows' word w (split by the
+// low H1 / high H2 bits of the scalar, PleSplit) are built in shared memory from the
+// multiplication matrices; row r of C is held by TPR lanes (lane b: plane b), the entry
+// A[r][i] is one ballot of the lanes' plane bits and the update is two table words per plane.
+// All tables of a CTA are built before it writes C, so with one row block per column word
+// (nblk_rows == 1) C may alias B (TRSM leaves: X = inv(T) B over B).
+template <int E>
+struct NjsShape {
+    static constexpr int THREADS = 512;
+    static constexpr int TPR = E <= 8 ? 8 : 16;
+    static constexpr int RPC = THREADS / TPR;  // rows per pass
+    static constexpr int KC = 32;              // rows of B per table chunk
+    static constexpr int MAXPASS = 4;
+    static constexpr size_t SMEM = (size_t)KC * PleSplit<E>::QE * 8 + (size_t)KC * E * 8;
+};
+
+template <int E>
+__global__ void __launch_bounds__(512, 1) k_nj_sliced(const FieldTab *__restrict__ ftab, const uint64_t *__restrict__ A,
+                                                   int64_t lda, int64_t pa, const uint64_t *B, int64_t ldb,
+                                                   int64_t pb, uint64_t *C, int64_t ldc, int64_t pc, int64_t m,
+                                                   int64_t k, int64_t n, int acc, int npass) {
+    using Sh = NjsShape<E>;
+    using SP = PleSplit<E>;
+    constexpr int TPR = Sh::TPR, KC = Sh::KC, QE = SP::QE, NH = SP::H2 ? 2 : 1;
+    constexpr uint32_t EMASK = (1u << E) - 1;
+    extern __shared__ __align__(16) uint64_t nsm[];
+    uint64_t *tab = nsm;                   // [KC][Q][E]
+    uint64_t *bs = tab + KC * QE;          // [KC][E]: the chunk's rows of B, word w
+    const int tid = threadIdx.x, lane = tid & 31, b = tid % TPR, gl = lane - b, rl = tid / TPR;
+    const int64_t w = blockIdx.x;
+    const int64_t row0 = (int64_t)blockIdx.y * Sh::RPC * npass;
+    uint64_t v[Sh::MAXPASS];
+#pragma unroll
+    for (int q = 0; q < Sh::MAXPASS; ++q) v[q] = 0;
+    for (int64_t i0 = 0; i0 < k; i0 += KC) {
+        const int kc = (int)(k - i0 < KC ? k - i0 : KC);
+        __syncthreads();  // the previous chunk's tables are consumed
+        for (int i = tid; i < kc * E; i += Sh::THREADS) bs[i] = B[(i % E) * pb + (i0 + i / E) * ldb + w];
+        __syncthreads();
+        // tables: thread (row i of the chunk, half h, plane q) forms plane q of the half's basis
+        // alpha^s * B_i (s in the half; mulmask of x^s = mulmask2[1] >> s), then the half's
+        // entries by doubling, one XOR each
+        for (int t = tid; t < kc * NH * E; t += Sh::THREADS) {
+            const int i = t / (NH * E), rem = t - i * (NH * E), h = rem / E, q = rem - h * E;
+            const int s0 = h ? SP::H1 : 0, hb = h ? SP::H2 : SP::H1;
+            uint64_t br[E];
+#pragma unroll
+            for (int p = 0; p < E; ++p) br[p] = bs[i * E + p];
+            const uint32_t m1 = ftab->mulmask2[1][q];
+            uint64_t basis[SP::H1 > SP::H2 ? SP::H1 : SP::H2];
+#pragma unroll
+            for (int u = 0; u < (SP::H1 > SP::H2 ? SP::H1 : SP::H2); ++u) {
+                const uint32_t mk = (m1 >> (s0 + u)) & EMASK;
+                uint64_t a = 0;
+#pragma unroll
+                for (int p = 0; p < E; ++p)
+                    if ((mk >> p) & 1u) a ^= br[p];
+                basis[u] = a;
+            }
+            // doubling: entry 2^u + t = entry t ^ basis[u] (this thread's own earlier stores)
+            uint64_t *dst = tab + i * QE + (h ? (1 << SP::H1) : 0) * E + q;
+            dst[0] = 0;
+#pragma unroll
+            for (int u = 0; u < (SP::H1 > SP::H2 ? SP::H1 : SP::H2); ++u) {
+                if (u >= hb) break;
+                for (int t = 0; t < (1 << u); ++t) dst[((1 << u) + t) * E] = dst[t * E] ^ basis[u];
+            }
+        }
+        __syncthreads();
+        const int sh = (int)(i0 & 63);
+#pragma unroll
+        for (int q = 0; q < Sh::MAXPASS; ++q) {
+            if (q >= npass) break;
+            const int64_t r = row0 + q * Sh::RPC + rl;
+            const uint64_t aw = (r < m && b < E) ? A[b * pa + r * lda + (i0 >> 6)] : 0;
+            for (int i = 0; i < kc; ++i) {
+                const unsigned bal = __ballot_sync(0xffffffffu, (aw >> (sh + i)) & 1ULL);
+                const uint32_t x = (bal >> gl) & EMASK;
+                if (x && b < E) {
+                    const uint64_t *ti = tab + i * QE + b;
+                    if constexpr (SP::H2 > 0)
+                        v[q] ^= ti[(x & ((1u << SP::H1) - 1)) * E] ^ ti[((1u << SP::H1) + (x >> SP::H1)) * E];
+                    else
+                        v[q] ^= ti[x * E];
+                }
+            }
+        }
+    }
+    // bits of the last word beyond column n keep their value
+    const int64_t nw = (n + 63) >> 6;
+    const uint64_t keep = (w == nw - 1 && (n & 63)) ? ~((1ULL << (n & 63)) - 1) : 0ULL;
+#pragma unroll
+    for (int q = 0; q < Sh::MAXPASS; ++q) {
+        if (q >= npass) break;
+        const int64_t r = row0 + q * Sh::RPC + rl;
+        if (r < m && b < E) {
+            uint64_t *c = C + b * pc + r * ldc + w;
+            const uint64_t old = *c;
+            const uint64_t nv = acc ? old ^ v[q] : v[q];
+            *c = (old & keep) | (nv & ~keep);
+        }
+    }
+}
+
+template <int E>
+cudaError_t launch_nj_sliced_e(const FieldTab *ftab, const uint64_t *A, int64_t lda, int64_t pa, const uint64_t *B,
+                               int64_t ldb, int64_t pb, uint64_t *C, int64_t ldc, int64_t pc, int64_t m, int64_t k,
+                               int64_t n, bool acc, bool c_aliases_b, cudaStream_t st) {
+    using Sh = NjsShape<E>;
+    static bool attr_set[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= kMaxDevices || !attr_set[dev]) {
+        cudaError_t err =
+            cudaFuncSetAttribute(k_nj_sliced<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
+        if (err != cudaSuccess) return err;
+        if (dev < kMaxDevices) attr_set[dev] = true;
+    }
+    const int64_t nw = (n + 63) >> 6;
+    const int64_t blocks1 = (m + Sh::RPC - 1) / Sh::RPC;  // row blocks at one pass
+    int npass = 1;
+    if (c_aliases_b) {
+        npass = (int)blocks1;  // one row block per column word
+        if (npass > Sh::MAXPASS) return cudaErrorInvalidValue;
+    } else {
+        // fewer, longer row blocks when the grid is far beyond one wave (tables amortised)
+        while (npass < Sh::MAXPASS && nw * ((blocks1 + npass - 1) / npass) > 4 * 148) npass *= 2;
+    }
+    const int64_t rb = (m + (int64_t)Sh::RPC * npass - 1) / ((int64_t)Sh::RPC * npass);
+    if (nw > 0x7fffffff || rb > 65535) return cudaErrorInvalidValue;
+    dim3 grid((unsigned)nw, (unsigned)rb);
+    k_nj_sliced<E><<<grid, Sh::THREADS, Sh::SMEM, st>>>(ftab, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, acc ? 1 : 0,
+                                                         npass);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_nj_mul(int e, uint32_t f, int w, const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,
@@ -166,4 +304,18 @@ cudaError_t launch_nj_mul(int e, uint32_t f, int w, const uint64_t *A, int64_t l
     }
 }
 
+}  // namespace gf2e
+
+namespace gf2e {
+cudaError_t launch_nj_sliced(int e, const FieldTab *ftab, const uint64_t *A, int64_t lda, int64_t pa,
+                             const uint64_t *B, int64_t ldb, int64_t pb, uint64_t *C, int64_t ldc, int64_t pc,
+                             int64_t m, int64_t k, int64_t n, bool acc, bool c_aliases_b, cudaStream_t st) {
+#define NJS(EE) \
+    case EE: return launch_nj_sliced_e<EE>(ftab, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, acc, c_aliases_b, st);
+    switch (e) {
+        NJS(2) NJS(3) NJS(4) NJS(5) NJS(6) NJS(7) NJS(8) NJS(9) NJS(10)
+        default: return cudaErrorInvalidValue;
+    }
+#undef NJS
+}
 }  // namespace gf2e

@@ -70,28 +70,46 @@ __device__ __forceinline__ void stepE(uint64_t *v, uint32_t x, const uint64_t *b
     }
 }
 
+// Window threads: TPR lanes of one warp per window row, lane b holding plane b (an entry is
+// one ballot); 1024 threads, RP rows per pass.
 template <int E>
-__global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ tab, uint64_t *__restrict__ S, int64_t ld,
-                                                 int64_t ps, int64_t m, int nb, PanelOut *__restrict__ out) {
+struct FindShape {
+    static constexpr int NT = 1024;
+    static constexpr int TPR = E <= 8 ? 8 : 16;
+    static constexpr int RP = NT / TPR;           // window rows per pass
+    static constexpr int PASSES = (PT + RP - 1) / RP;
+    static constexpr uint32_t EMASK = (1u << E) - 1;
+};
+
+// first row (of the ballot's row groups) whose group has a set bit: the lowest set lane
+template <int TPR>
+__device__ __forceinline__ int first_row(unsigned bal, int row_of_lane0) {
+    return row_of_lane0 + (__ffs(bal) - 1) / TPR;
+}
+
+template <int E>
+__global__ void __launch_bounds__(1024) k_ple_find(const FieldTab *__restrict__ tab, uint64_t *__restrict__ S,
+                                                   int64_t ld, int64_t ps, int64_t m, int nb,
+                                                   PanelOut *__restrict__ out) {
+    using F = FindShape<E>;
+    using SP = PleSplit<E>;
+    constexpr int NT = F::NT, TPR = F::TPR;
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t *win = reinterpret_cast<uint64_t *>(smem);  // [PT][E]
-    uint64_t *bt = win + PT * E;                         // [KP][E][E]
-    using SP = PleSplit<E>;
-    uint64_t *ptab = bt + KP * E * E;                    // [Q][E]: multiples of the current T_r
-    uint16_t *sinv = reinterpret_cast<uint16_t *>(ptab + SP::QE);  // [2^E] inverses
-    uint16_t *smk = sinv + (1 << E);                                   // [2^E][E] multiplication matrices
-    __shared__ uint64_t ext[kMaxE];
+    uint64_t *ptab = win + PT * E;                       // [Q][E]: multiples of the current T_r
+    uint32_t *smm = reinterpret_cast<uint32_t *>(ptab + SP::QE);  // [2^E][E] mulmask2
+    uint16_t *sinv = reinterpret_cast<uint16_t *>(smm + (1 << E) * E);  // [2^E] inverses
+    __shared__ uint64_t ext[kMaxE], prow[kMaxE], oldr[kMaxE];
     __shared__ uint64_t s_dval[KP][kMaxE];
     __shared__ int64_t dpos[KP];
     __shared__ int dstep[KP], s_jcol[KP];
     __shared__ int64_t s_P[KP], s_Q[KP];
     __shared__ int s_mn[2], s_nd, s_supp_ok;
-    __shared__ uint32_t s_inv;
     __shared__ unsigned long long s_supp;
     __shared__ int64_t s_pmin;
 
     const int tid = threadIdx.x;
-    const uint32_t fpoly = tab->f;  // x * c mod f: shift, fold with f (bit E included)
+    const int lane = tid & 31, b = tid % TPR, gl = lane - b, rl = tid / TPR;
     const int W = (int)(m < PT ? m : PT);
     const uint64_t cmask = nb >= 64 ? ~0ULL : ((1ULL << nb) - 1);
     const int k = (int)(m < nb ? m : nb);
@@ -101,28 +119,29 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
         s_supp = 0;
         s_mn[0] = 0x7fffffff;
     }
-    for (int i = tid; i < (1 << E); i += PT) {
+    for (int i = tid; i < (1 << E); i += NT) {
         sinv[i] = tab->inv[i];
 #pragma unroll
-        for (int b = 0; b < E; ++b) smk[i * E + b] = tab->mulmask[i][b];
+        for (int q = 0; q < E; ++q) smm[i * E + q] = tab->mulmask2[i][q];
     }
     __syncthreads();
-    for (int s = tid; s < W; s += PT) {
-        uint64_t any = 0;
+    // window rows; candidates for column 0 (lowest row of each warp with a nonzero entry)
 #pragma unroll
-        for (int b = 0; b < E; ++b) {
-            const uint64_t x = S[b * ps + s * ld] & cmask;
+    for (int pass = 0; pass < F::PASSES; ++pass) {
+        const int s = pass * F::RP + rl;
+        uint64_t x = 0;
+        if (s < W && b < E) {
+            x = S[b * ps + s * ld] & cmask;
             win[s * E + b] = x;
-            any |= x;
         }
-        if (any & 1ULL) atomicMin(&s_mn[0], s);  // candidates for column 0
+        const unsigned bal = __ballot_sync(0xffffffffu, x & 1ULL);
+        if (lane == 0 && bal) atomicMin(&s_mn[0], first_row<TPR>(bal, pass * F::RP + (tid - lane) / TPR));
     }
     __syncthreads();
     int r = 0;
-    // Three barriers per pivot: (bookkeeping) | (basis) | (elimination + candidates for the next
-    // column).  The candidate minimum is double-buffered (s_mn[j & 1]) so no barrier is needed
-    // to reset it; the basis alpha^s * T is formed straight from the unscaled pivot row with
-    // the multiplication matrix of alpha^s / pivot.
+    // Two barriers per pivot: (pivot found: table of its multiples, bookkeeping) | (pivot row
+    // written, rows below eliminated with two table words per plane, candidates for the next
+    // column).  The candidate minimum is double-buffered (s_mn[j & 1]).
     for (int j = 0; j < nb && r < k; ++j) {
         const int cb = j & 1;
         int64_t ipos = s_mn[cb];
@@ -133,21 +152,22 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
             if (tid == 0) s_pmin = INT64_MAX;
             if (!s_supp_ok) {
                 uint64_t acc = 0;
-                for (int64_t p = W + tid; p < m; p += PT)
+                for (int64_t p = W + tid; p < m; p += NT)
 #pragma unroll
-                    for (int b = 0; b < E; ++b) acc |= S[b * ps + p * ld];
+                    for (int q = 0; q < E; ++q) acc |= S[q * ps + p * ld];
                 if (acc) atomicOr(&s_supp, acc & cmask);
-                for (int t = tid; t < r; t += PT)
+                for (int t = tid; t < r; t += NT)
 #pragma unroll
-                    for (int b = 0; b < E; ++b) atomicOr(&s_supp, bt[t * E * E + b]);
+                    for (int q = 0; q < E; ++q) atomicOr(&s_supp, out->tabs[t * kPleTabWords + E + q]);
                 __syncthreads();
                 if (tid == 0) s_supp_ok = 1;
             }
             __syncthreads();
             if ((s_supp >> j) & 1ULL) {
-                // scan the rows below the window, reducing each candidate lazily
+                // scan the rows below the window, reducing each candidate lazily by the tables
+                // of the pivots so far (written to global memory by this CTA)
                 const int nd = s_nd;
-                for (int64_t base = W; base < m; base += PT) {
+                for (int64_t base = W; base < m; base += NT) {
                     const int64_t p = base + tid;
                     uint64_t v[E];
                     bool hit = false;
@@ -157,23 +177,36 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
                             if (dpos[d] == p) di = d;
                         if (di >= 0) {
 #pragma unroll
-                            for (int b = 0; b < E; ++b) v[b] = s_dval[di][b];
+                            for (int q = 0; q < E; ++q) v[q] = s_dval[di][q];
                             st0 = dstep[di];
                         } else {
 #pragma unroll
-                            for (int b = 0; b < E; ++b) v[b] = S[b * ps + p * ld] & cmask;
+                            for (int q = 0; q < E; ++q) v[q] = S[q * ps + p * ld] & cmask;
                         }
-                        for (int t = st0; t < r; ++t) stepE<E>(v, elemE<E>(v, s_jcol[t]), bt + t * E * E);
+                        for (int t = st0; t < r; ++t) {
+                            const uint32_t x = elemE<E>(v, s_jcol[t]);
+                            if (!x) continue;
+                            const uint64_t *tt = out->tabs + t * kPleTabWords;
+                            const uint64_t *lo = tt + (x & ((1u << SP::H1) - 1)) * E;
+                            if constexpr (SP::H2 > 0) {
+                                const uint64_t *hi = tt + ((1u << SP::H1) + (x >> SP::H1)) * E;
+#pragma unroll
+                                for (int q = 0; q < E; ++q) v[q] ^= lo[q] ^ hi[q];
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < E; ++q) v[q] ^= lo[q];
+                            }
+                        }
                         uint64_t any = 0;
 #pragma unroll
-                        for (int b = 0; b < E; ++b) any |= v[b];
+                        for (int q = 0; q < E; ++q) any |= v[q];
                         hit = (any >> j) & 1ULL;
                         if (hit) atomicMin((unsigned long long *)&s_pmin, (unsigned long long)p);
                     }
                     __syncthreads();
                     if (hit && s_pmin == p)
 #pragma unroll
-                        for (int b = 0; b < E; ++b) ext[b] = v[b];
+                        for (int q = 0; q < E; ++q) ext[q] = v[q];
                     __syncthreads();
                     if (s_pmin != INT64_MAX) break;
                 }
@@ -185,132 +218,118 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
             if (tid == 0) s_mn[cb ^ 1] = 0x7fffffff;
             __syncthreads();
             if (j + 1 < nb)
-                for (int s = r + tid; s < W; s += PT) {
-                    uint64_t any = 0;
 #pragma unroll
-                    for (int b = 0; b < E; ++b) any |= win[s * E + b];
-                    if ((any >> (j + 1)) & 1ULL) atomicMin(&s_mn[cb ^ 1], s);
+                for (int pass = 0; pass < F::PASSES; ++pass) {
+                    const int s = pass * F::RP + rl;
+                    const bool act = s >= r && s < W && b < E;
+                    const unsigned bal = __ballot_sync(0xffffffffu, act && ((win[s * E + b] >> (j + 1)) & 1ULL));
+                    if (lane == 0 && bal)
+                        atomicMin(&s_mn[cb ^ 1], first_row<TPR>(bal, pass * F::RP + (tid - lane) / TPR));
                 }
             __syncthreads();
             continue;
         }
-        if (tid == 0) {
-            uint64_t *pr = win + r * E;
-            if (ipos < W) {
-                const int i = (int)ipos;
-                if (i != r)
+        // ---- phase A: the pivot row P (window row ipos, or ext from below the window) ----
+        const uint64_t *P = ipos < W ? win + ipos * E : ext;
+        const uint64_t sm = (j >= 63 ? 0ULL : (~0ULL << (j + 1))) & cmask;  // suffix right of j
+        // table of the multiples of T_r = (P right of j) / pivot: entry x of the low half is
+        // x * T_r, of the high half (x << H1) * T_r; plane b of c * T_r is the XOR of the
+        // planes p of T_r with bit p of mulmask[c][b], and mulmask[y / pivot][b] is the XOR of
+        // mulmask2[1 / pivot][b] >> s over the bits s of y
+        for (int idx = tid; idx < SP::QE; idx += NT) {
+            const int x = idx / E, q = idx - (idx / E) * E;
+            const uint32_t y = x < (1 << SP::H1) ? (uint32_t)x : (uint32_t)(x - (1 << SP::H1)) << SP::H1;
+            uint64_t pv[E];
 #pragma unroll
-                    for (int b = 0; b < E; ++b) {
-                        const uint64_t t = pr[b];
-                        pr[b] = win[i * E + b];
-                        win[i * E + b] = t;
-                    }
-            } else {
-                // the row at position r moves below the window: remember it (reduced by steps < r)
-                int di = -1;
-                for (int d = 0; d < s_nd; ++d)
-                    if (dpos[d] == ipos) di = d;
-                if (di < 0) di = s_nd++;
-                dpos[di] = ipos;
-                dstep[di] = r;
+            for (int p = 0; p < E; ++p) pv[p] = P[p];
+            const uint32_t pinv = sinv[elemE<E>(pv, j)];
+            const uint32_t m2 = smm[pinv * E + q];
+            uint32_t mk = 0;
 #pragma unroll
-                for (int b = 0; b < E; ++b) {
-                    s_dval[di][b] = pr[b];
-                    pr[b] = ext[b];
-                }
-            }
-            s_P[r] = ipos;
-            s_Q[r] = j;
-            s_jcol[r] = j;
-            s_inv = sinv[elemE<E>(pr, j)];
-            s_mn[cb ^ 1] = 0x7fffffff;  // candidates for column j + 1 (collected below)
-        }
-        __syncthreads();
-        // basis alpha^s * T_r, T_r = pivot row right of j scaled by 1/pivot (s = tid / E,
-        // plane tid % E): plane b of c * v is the XOR of the planes p in mulmask[c][b]
-        const uint64_t sm = (j >= 63 ? 0ULL : (~0ULL << (j + 1))) & cmask;
-        if (tid < E * E) {
-            const int sidx = tid / E, b = tid % E;
-            uint32_t c = s_inv;  // alpha^sidx / pivot
-            for (int q = 0; q < sidx; ++q) c = (c << 1) ^ (((c >> (E - 1)) & 1u) ? fpoly : 0u);
-            const uint32_t mk = smk[c * E + b];
-            const uint64_t *pr = win + r * E;
+            for (int s = 0; s < E; ++s)
+                if ((y >> s) & 1u) mk ^= m2 >> s;
             uint64_t acc = 0;
 #pragma unroll
             for (int p = 0; p < E; ++p)
-                if ((mk >> p) & 1u) acc ^= pr[p] & sm;
-            bt[r * E * E + tid] = acc;
-        }
-        __syncthreads();
-        const uint64_t *btr = bt + r * E * E;
-        // table of the multiples of T_r (entry x of the low / high half: XOR of the basis rows
-        // selected by the bits of x), kept for phase 2 as well
-        for (int idx = tid; idx < SP::QE; idx += PT) {
-            const int x = idx / E, b = idx - (idx / E) * E;
-            const bool hi = x >= (1 << SP::H1);
-            const int xs = hi ? x - (1 << SP::H1) : x, s0 = hi ? SP::H1 : 0;
-            uint64_t acc = 0;
-#pragma unroll
-            for (int q = 0; q < (SP::H1 > SP::H2 ? SP::H1 : SP::H2); ++q)
-                if ((xs >> q) & 1) acc ^= btr[(s0 + q) * E + b];
+                if ((mk >> p) & 1u) acc ^= pv[p];
+            acc &= sm;
             ptab[idx] = acc;
             out->tabs[r * kPleTabWords + idx] = acc;
         }
+        if (tid >= NT - 32) {  // last warp: bookkeeping (no table words there)
+            if (tid - (NT - 32) < E) {
+                const int q = tid - (NT - 32);
+                prow[q] = P[q];
+                oldr[q] = win[r * E + q];
+            }
+            if (tid == NT - 1) {
+                if (ipos >= W) {
+                    // the row at position r moves below the window: remember it (reduced by
+                    // steps < r)
+                    int di = -1;
+                    for (int d = 0; d < s_nd; ++d)
+                        if (dpos[d] == ipos) di = d;
+                    if (di < 0) di = s_nd++;
+                    dpos[di] = ipos;
+                    dstep[di] = r;
+#pragma unroll
+                    for (int q = 0; q < E; ++q) s_dval[di][q] = win[r * E + q];
+                }
+                s_P[r] = ipos;
+                s_Q[r] = j;
+                s_jcol[r] = j;
+                s_mn[cb ^ 1] = 0x7fffffff;  // candidates for column j + 1 (collected below)
+            }
+        }
         __syncthreads();
+        // ---- phase B: pivot row to position r (prefix kept, suffix scaled), eliminations ----
         if (tid < E) {
-            const uint64_t t0 = btr[tid];  // s = 0: the scaled suffix itself
-            win[r * E + tid] = (win[r * E + tid] & ~sm) | t0;
+            const uint64_t t0 = ptab[E + tid];  // entry 1: the scaled suffix itself
+            win[r * E + tid] = (prow[tid] & ~sm) | t0;
             if (s_supp_ok) atomicOr(&s_supp, t0);
         }
         const bool next = j + 1 < nb;
-        for (int s = r + 1 + tid; s < W; s += PT) {
-            uint64_t v[E];
 #pragma unroll
-            for (int b = 0; b < E; ++b) v[b] = win[s * E + b];
-            const uint32_t x = elemE<E>(v, j);
-            if (x) {
-                const uint64_t *lo = ptab + (x & ((1u << SP::H1) - 1)) * E;
-                if constexpr (SP::H2 > 0) {
-                    const uint64_t *hi = ptab + ((1u << SP::H1) + (x >> SP::H1)) * E;
-#pragma unroll
-                    for (int b = 0; b < E; ++b) v[b] ^= lo[b] ^ hi[b];
-                } else {
-#pragma unroll
-                    for (int b = 0; b < E; ++b) v[b] ^= lo[b];
+        for (int pass = 0; pass < F::PASSES; ++pass) {
+            const int s = pass * F::RP + rl;
+            const bool act = s > r && s < W && b < E;
+            uint64_t v = 0;
+            if (act) v = (s == ipos) ? oldr[b] : win[s * E + b];  // the old row r moved to ipos
+            const unsigned bal = __ballot_sync(0xffffffffu, (v >> j) & 1ULL);
+            const uint32_t x = (bal >> gl) & F::EMASK;
+            if (act && (x || s == ipos)) {
+                if (x) {
+                    if constexpr (SP::H2 > 0)
+                        v ^= ptab[(x & ((1u << SP::H1) - 1)) * E + b] ^ ptab[((1u << SP::H1) + (x >> SP::H1)) * E + b];
+                    else
+                        v ^= ptab[x * E + b];
                 }
-#pragma unroll
-                for (int b = 0; b < E; ++b) win[s * E + b] = v[b];
+                win[s * E + b] = v;
             }
             if (next) {
-                uint64_t any = 0;
-#pragma unroll
-                for (int b = 0; b < E; ++b) any |= v[b];
-                if ((any >> (j + 1)) & 1ULL) atomicMin(&s_mn[cb ^ 1], s);
+                const unsigned bal2 = __ballot_sync(0xffffffffu, act && ((v >> (j + 1)) & 1ULL));
+                if (lane == 0 && bal2)
+                    atomicMin(&s_mn[cb ^ 1], first_row<TPR>(bal2, pass * F::RP + (tid - lane) / TPR));
             }
         }
         ++r;
         __syncthreads();
     }
-    __syncthreads();
     // L compression of the base case (newton_john.py:257-259) and write-back of the window
-    for (int s = tid; s < W; s += PT) {
-        uint64_t v[E];
 #pragma unroll
-        for (int b = 0; b < E; ++b) v[b] = win[s * E + b];
-        for (int t = 0; t < r && t <= s; ++t) {
-            const int q = (int)s_Q[t];
-            if (q != t)
-#pragma unroll
-                for (int b = 0; b < E; ++b) v[b] = swap_bits(v[b], t, q);
-        }
-#pragma unroll
-        for (int b = 0; b < E; ++b) {
+    for (int pass = 0; pass < F::PASSES; ++pass) {
+        const int s = pass * F::RP + rl;
+        if (s < W && b < E) {
+            uint64_t v = win[s * E + b];
+            for (int t = 0; t < r && t <= s; ++t) {
+                const int q = (int)s_Q[t];
+                if (q != t) v = swap_bits(v, t, q);
+            }
             uint64_t *d = S + b * ps + s * ld;
-            *d = (*d & ~cmask) | v[b];
+            *d = (*d & ~cmask) | v;
         }
     }
     // outputs for phase 2 and the host
-    for (int i = tid; i < r * E * E; i += PT) out->bt[i] = bt[i];
     if (tid < r) {
         out->P[tid] = s_P[tid];
         out->Q[tid] = s_Q[tid];
@@ -320,7 +339,7 @@ __global__ void __launch_bounds__(PT) k_ple_find(const FieldTab *__restrict__ ta
         out->dpos[tid] = dpos[tid];
         out->dstep[tid] = dstep[tid];
 #pragma unroll
-        for (int b = 0; b < E; ++b) out->dval[tid][b] = s_dval[tid][b];
+        for (int q = 0; q < E; ++q) out->dval[tid][q] = s_dval[tid][q];
     }
     if (tid == 0) {
         out->rank = r;
@@ -582,7 +601,7 @@ inline int grid_for(int64_t total, int threads) {
 template <int E>
 cudaError_t launch_ple_e(const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb, PanelOut *out,
                          cudaStream_t st) {
-    const int smem = (PT * E + KP * E * E + PleSplit<E>::QE) * 8 + (1 << E) * (E + 1) * 2;
+    const int smem = (PT * E + PleSplit<E>::QE) * 8 + (1 << E) * E * 4 + (1 << E) * 2;
     const int smem2 = (int)ApplyShape<E>::SMEM;
     // launch attributes once per instantiation and device (idempotent)
     static bool attr_set[kMaxDevices] = {};
@@ -596,7 +615,7 @@ cudaError_t launch_ple_e(const FieldTab *tab, uint64_t *S, int64_t ld, int64_t p
         if (err != cudaSuccess) return err;
         if (dev < kMaxDevices) attr_set[dev] = true;
     }
-    k_ple_find<E><<<1, PT, smem, st>>>(tab, S, ld, ps, m, nb, out);
+    k_ple_find<E><<<1, FindShape<E>::NT, smem, st>>>(tab, S, ld, ps, m, nb, out);
     err = cudaGetLastError();
     if (err != cudaSuccess || m <= PT) return err;
     using A = ApplyShape<E>;
@@ -660,6 +679,14 @@ const FieldTab *field_tab(int e, uint32_t f, uint32_t g) {
             for (int b = 0; b < e; ++b)
                 if ((prod >> b) & 1u) h.mulmask[c][b] |= (uint16_t)(1u << p);
         }
+    for (uint32_t c = 0; c <= q1; ++c) {
+        uint32_t prod = c;  // c * x^p
+        for (int p = 0; p < 2 * e - 1; ++p) {
+            for (int b = 0; b < e; ++b)
+                if ((prod >> b) & 1u) h.mulmask2[c][b] |= 1u << p;
+            prod = gf_mul_h(prod, 2u, e, f);
+        }
+    }
     FieldTab *d = nullptr;
     if (cudaMalloc(reinterpret_cast<void **>(&d), sizeof(FieldTab)) != cudaSuccess) return nullptr;
     // complete before any kernel (on any stream) can be enqueued with d: a pageable cudaMemcpy

@@ -204,6 +204,22 @@ def nj_mul_packed(A: PackedMatrix, B: PackedMatrix, C: PackedMatrix | None = Non
     return C
 
 
+def nj_mul_sliced(A: SlicedMatrix, B: SlicedMatrix, C: SlicedMatrix | None = None) -> SlicedMatrix:
+    """C = A*B (or C ^= A*B when C is given) on bit planes in one launch (gf2e_nj_slice_mul):
+    the Newton-John table product that PLE and TRSM use for their small updates."""
+    _check_operands(A, B)
+    ctx = A.ctx
+    m, k, n = A.nrows, A.ncols, B.ncols
+    acc = C is not None
+    if C is None:
+        C = SlicedMatrix(ctx, m, n)
+    lda, ldb, ldc = A.planes.shape[2], B.planes.shape[2], C.planes.shape[2]
+    _lib.call("gf2e_nj_slice_mul", ctx.e, ctx.f, _device.ptr(A.planes), lda, m * lda, _device.ptr(B.planes), ldb,
+              k * ldb, _device.ptr(C.planes), ldc, m * ldc, m, k, n, _lib.ACCUMULATE if acc else 0,
+              _device.stream_handle())
+    return C
+
+
 def _small(A: PackedMatrix, B: PackedMatrix, backend: str | None) -> bool:
     return (backend is None and max(A.nrows, A.ncols, B.ncols) <= NJ_CROSSOVER[A.ctx.e]
             and nj_fits(A.ctx.e, B.ncols))

@@ -496,6 +496,47 @@ def test_nj_small_products_golden(g, golden):
 
 
 @pytest.mark.parametrize("e", range(2, 11))
+def test_nj_sliced_oracle(g, e):
+    # the bit-plane Newton-John product (gf2e_nj_slice_mul: PLE / TRSM small updates) against
+    # the oracle, k across table chunks (32 rows of B) and words, n with a partial last word
+    from paper_1111_6900_b200 import poly_mul
+
+    ctx = g.field_new(e)
+    for (m, k, n) in [(1, 1, 1), (5, 7, 3), (64, 64, 64), (65, 100, 130), (200, 33, 63), (130, 257, 17),
+                      (300, 128, 200)]:
+        A = oracle.packed_random(e, m, k, 1)
+        B = oracle.packed_random(e, k, n, 2)
+        C0 = oracle.packed_random(e, m, n, 3)
+        SA = oracle.slice_words(e, m, k, A)
+        SB = oracle.slice_words(e, k, n, B)
+        SC = oracle.slice_words(e, m, n, C0)
+        ref, _ = oracle.karatsuba(e, ctx.f, SA, SB, m, k, n)
+        gA = g.SlicedMatrix.from_numpy(ctx, SA, k)
+        gB = g.SlicedMatrix.from_numpy(ctx, SB, n)
+        gC = g.SlicedMatrix.from_numpy(ctx, SC, n)
+        assert np.array_equal(poly_mul.nj_mul_sliced(gA, gB).to_numpy(), ref), (m, k, n)
+        assert g._lib.last_product_kernel() == "k_nj_sliced"
+        poly_mul.nj_mul_sliced(gA, gB, gC)
+        assert np.array_equal(gC.to_numpy(), ref ^ SC), (m, k, n, "acc")
+
+
+@pytest.mark.parametrize("e", [4, 8, 10])
+def test_nj_sliced_vs_tensor_cores(g, e):
+    # larger shapes (grids with several passes per row block) against the tensor-core product
+    from paper_1111_6900_b200 import poly_mul
+
+    ctx = g.field_new(e)
+    for (m, k, n) in [(8128, 64, 64), (128, 128, 8064), (3000, 96, 700), (40000, 64, 128)]:
+        A = g.SlicedMatrix.random(ctx, m, k, 1)
+        B = g.SlicedMatrix.random(ctx, k, n, 2)
+        C = g.SlicedMatrix.random(ctx, m, n, 3)
+        want = C.copy()
+        g.addmul(want, A, B, backend="tc")
+        poly_mul.nj_mul_sliced(A, B, C)
+        assert np.array_equal(C.to_numpy(), want.to_numpy()), (m, k, n)
+
+
+@pytest.mark.parametrize("e", range(2, 11))
 def test_nj_small_products_oracle(g, e):
     from paper_1111_6900_b200 import poly_mul
 

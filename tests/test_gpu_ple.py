@@ -200,7 +200,9 @@ def test_counters_through_the_api(g, golden):
                 c = g.MulCounters()
                 fn(T, B.copy(), crossover=cx, counters=c)
                 got.append([c.gf2_matmul_count, c.additions, c.peak_live_products])
-                assert c.device_products > 0 and c.device_products % g.count_products(e) == 0, tag
+                # (updates and leaves with k <= 128 take the CUDA-core Newton-John form, which runs
+                # no GF(2) products; the rest run whole Karatsuba schedules)
+                assert c.device_products % g.count_products(e) == 0, tag
         assert got == golden[f"{tag}/counters"].tolist(), tag
     for tag in (str(t) for t in golden["ple_tags"]):
         e, f, m, n = (int(x) for x in golden[f"{tag}/meta"])
