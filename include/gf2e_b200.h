@@ -176,6 +176,16 @@ int gf2e_slice_mul_parts(int e, uint32_t f, const uint64_t *A_dev, int64_t lda, 
                          int64_t workspace_bytes, void *stream);
 
 /*
+ * The running-sum form's drain grouping for field (e, f) (diagnostic; the kernel's schedule):
+ * product seq[i] is the i-th accumulated entry of a tile, group g = the next gsize[g] entries
+ * with one accumulator drain whose parity is folded into the output planes gmask[g];
+ * run_load = the most entries one accumulator takes per tile (exactness: run_load * k_pad <
+ * 65536, else the plain one-group-per-product order runs).  Arrays hold up to 128 entries.
+ */
+int gf2e_run_schedule(int e, uint32_t f, int *nseq, int *ngrp, int *run_load, int *seq, int *gsize,
+                      uint32_t *gmask);
+
+/*
  * Columns of C per product tile (CTA pair) of the form a product with inner dimension k and
  * these flags would use (256, or 192 for the short-k running-sum form) — the quantum for
  * gf2e_slice_mul_parts bounds that keep every tile inside one part.  -1 on bad arguments.

@@ -48,6 +48,7 @@ SIGNATURES = {
     "gf2e_slice_mul": (_INT, [_INT, _U32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64,
                               _U32, _P, _I64, _P]),
     "gf2e_nj_mul": (_INT, [_INT, _U32, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _U32, _P]),
+    "gf2e_run_schedule": (_INT, [_INT, _U32, _P, _P, _P, _P, _P, _P]),
     "gf2e_nj_slice_mul": (_INT, [_INT, _U32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64,
                                  _U32, _P]),
     "gf2e_slice_mul_parts": (_INT, [_INT, _U32, _P, _I64, _I64, _INT, ctypes.POINTER(_I64), ctypes.POINTER(_P),
@@ -199,6 +200,15 @@ def int_peak(iters: int = 2000) -> tuple[float, float]:
     check(load().gf2e_int_peak(iters, ctypes.byref(bps), ctypes.byref(tops),
                                torch.cuda.current_stream().cuda_stream), "gf2e_int_peak")
     return bps.value, tops.value
+
+
+def run_schedule(e: int, f: int) -> tuple[list[int], list[int], list[int], int]:
+    """The running-sum form's drain grouping: (seq, gsize, gmask, run_load)."""
+    n, g, load_ = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    seq, gsize, gmask = (ctypes.c_int * 128)(), (ctypes.c_int * 128)(), (ctypes.c_uint32 * 128)()
+    check(load().gf2e_run_schedule(e, f, ctypes.byref(n), ctypes.byref(g), ctypes.byref(load_), seq, gsize, gmask),
+          "gf2e_run_schedule")
+    return list(seq[:n.value]), list(gsize[:g.value]), list(gmask[:g.value]), load_.value
 
 
 def last_product_kernel() -> str:

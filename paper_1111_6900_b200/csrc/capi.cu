@@ -3,6 +3,7 @@
 // schedule, workspace carving, and the launch sequence of the hot path.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdarg>
 #include <cstddef>
@@ -107,7 +108,144 @@ struct Schedule {
     std::vector<uint64_t> subsets;  // per product: bitmask of input planes
     std::vector<uint64_t> outmap;   // per output plane: bitmask of products
     int64_t counters[3];            // gf2_matmul_count, additions, peak_live_products
+    // running-sum form grouping (Sched.seq / gsize / gmask, run_groups below)
+    std::vector<int> grp_seq, grp_size;
+    std::vector<uint32_t> grp_mask;
+    int grp_load = 0;
 };
+
+// ---- drain grouping of the running-sum form ----------------------------------------------
+// The running-sum kernel pays one accumulator drain (TMEM read + parity + fold) per group of
+// products, and every accumulated entry pays its operand staging and MMAs.  Output
+// plane b is the XOR of the parities of the products t with bit b of their column M_t (the
+// e-bit vector of output planes product t feeds).  Choose q drain vectors c_1..c_q in GF(2)^e
+// and write every column as a XOR of a few of them, M_t = sum_{j in R_t} c_j: product t is
+// accumulated into each group j of R_t, group j's drain parity is folded into the planes c_j,
+// and plane b receives sum_j c_j[b] sum_{t: j in R_t} P_t = sum_t M_t[b] P_t.  One group per
+// product (c = the columns) is the identity; fewer groups trade drains for repeated MMAs.
+// dist: fewest vectors of S summing to each element of GF(2)^e (BFS), par: last vector used.
+static void gf2_span_bfs(const std::vector<uint32_t> &S, int e, std::vector<int> &dist, std::vector<int> *par) {
+    const int n = 1 << e;
+    dist.assign(n, 1 << 20);
+    if (par) par->assign(n, -1);
+    std::vector<uint32_t> frontier{0}, next;
+    dist[0] = 0;
+    while (!frontier.empty()) {
+        next.clear();
+        for (uint32_t v : frontier)
+            for (size_t j = 0; j < S.size(); ++j) {
+                const uint32_t u = v ^ S[j];
+                if (dist[u] > dist[v] + 1) {
+                    dist[u] = dist[v] + 1;
+                    if (par) (*par)[u] = (int)j;
+                    next.push_back(u);
+                }
+            }
+        frontier.swap(next);
+    }
+}
+static int64_t grouping_cost(const std::vector<uint32_t> &S, const std::vector<uint32_t> &cols, int e) {
+    std::vector<int> d;
+    gf2_span_bfs(S, e, d, nullptr);
+    int64_t c = 0;
+    for (uint32_t x : cols) c += d[x];
+    return c;
+}
+
+// q: drains per tile (GF2E_RUN_DRAINS; default and >= K: identity)
+static void run_groups(Schedule &s, int e) {
+    const int K = (int)s.subsets.size();
+    std::vector<uint32_t> cols(K);
+    for (int t = 0; t < K; ++t) {
+        uint32_t m = 0;
+        for (int j = 0; j < e; ++j)
+            if ((s.outmap[j] >> t) & 1ULL) m |= 1u << j;
+        cols[t] = m;
+    }
+    std::vector<uint32_t> S = cols;
+    std::sort(S.begin(), S.end());
+    S.erase(std::unique(S.begin(), S.end()), S.end());
+    S.erase(std::remove(S.begin(), S.end(), 0u), S.end());
+    const char *env = getenv("GF2E_RUN_DRAINS");
+    const int want = env ? atoi(env) : 0;
+    // greedy removal down to e vectors, keeping the frontier (entries per number of drains)
+    std::vector<std::vector<uint32_t>> front(S.size() + 1);
+    std::vector<int64_t> fcost(S.size() + 1, -1);
+    front[S.size()] = S;
+    fcost[S.size()] = grouping_cost(S, cols, e);
+    for (std::vector<uint32_t> cur = S; (int)cur.size() > e;) {
+        int64_t best = -1;
+        size_t bi = 0;
+        for (size_t i = 0; i < cur.size(); ++i) {
+            std::vector<uint32_t> T = cur;
+            T.erase(T.begin() + i);
+            const int64_t c = grouping_cost(T, cols, e);
+            if (c < (int64_t)K * (1 << 20) && (best < 0 || c < best)) {
+                best = c;
+                bi = i;
+            }
+        }
+        if (best < 0) break;
+        cur.erase(cur.begin() + bi);
+        front[cur.size()] = cur;
+        fcost[cur.size()] = best;
+    }
+    // measured (profiles/r02/run_grouping.txt, e = 8, config 4): 27 drains 17.0 ms, 24: 17.4,
+    // 20: 18.5, 16: 19.3 -- an extra accumulated entry costs more than the drain it saves
+    // while the A operand is expanded into TMEM by the expander warps, so the default is the
+    // identity (one drain per product); GF2E_RUN_DRAINS=q selects a grouping
+    int q = (int)S.size();
+    if (want > 0) {
+        q = want < (int)S.size() ? want : (int)S.size();
+        while (q < (int)S.size() && fcost[q] < 0) ++q;
+    }
+    std::vector<uint32_t> G = front[q];
+    int64_t gc = fcost[q];
+    if (e <= 8 && q < (int)S.size()) {  // local search: replace one vector by any other
+        for (bool improved = true; improved;) {
+            improved = false;
+            for (size_t i = 0; i < G.size(); ++i)
+                for (uint32_t v = 1; v < (1u << e); ++v) {
+                    if (std::find(G.begin(), G.end(), v) != G.end()) continue;
+                    std::vector<uint32_t> U = G;
+                    U[i] = v;
+                    const int64_t c = grouping_cost(U, cols, e);
+                    if (c < gc) {
+                        gc = c;
+                        G = U;
+                        improved = true;
+                    }
+                }
+        }
+    }
+    // representations and groups (empty groups dropped)
+    std::vector<int> dist, par;
+    gf2_span_bfs(G, e, dist, &par);
+    std::vector<std::vector<int>> members(G.size());
+    for (int t = 0; t < K; ++t)
+        for (uint32_t x = cols[t]; x;) {
+            const int j = par[x];
+            members[j].push_back(t);
+            x ^= G[j];
+        }
+    s.grp_seq.clear();
+    s.grp_size.clear();
+    s.grp_mask.clear();
+    int64_t load[2] = {0, 0};
+    for (size_t j = 0; j < G.size(); ++j) {
+        if (members[j].empty()) continue;
+        load[s.grp_size.size() & 1] += (int64_t)members[j].size();
+        s.grp_size.push_back((int)members[j].size());
+        s.grp_mask.push_back(G[j]);
+        for (int t : members[j]) s.grp_seq.push_back(t);
+    }
+    s.grp_load = (int)std::max(load[0], load[1]);
+    if ((int)s.grp_seq.size() > kMaxSeq || (int)s.grp_size.size() > kMaxSeq) {  // cannot happen for e <= 10
+        s.grp_seq.clear();
+        s.grp_size.clear();
+        s.grp_mask.clear();
+    }
+}
 
 struct Replay {
     std::vector<uint64_t> subsets;
@@ -188,7 +326,19 @@ const Schedule &get_schedule(int e, uint32_t f) {
     for (int j = 0; j < e; ++j)
         for (int d = 0; d < 2 * e - 1; ++d)
             if ((work[j] >> d) & 1ULL) s.outmap[j] ^= gamma[d];
+    run_groups(s, e);
     return g_sched_cache.emplace(key, s).first->second;
+}
+
+// one group per product: the running-sum form's plain order (exact whenever run_ok holds)
+void run_identity(Sched &k) {
+    k.nseq = k.ngrp = k.nprod;
+    for (int t = 0; t < k.nprod; ++t) {
+        k.seq[t] = (uint8_t)t;
+        k.gsize[t] = 1;
+        k.gmask[t] = k.outmask[t];
+    }
+    k.run_load = (k.nprod + 1) / 2;
 }
 
 Sched to_kernel_sched(int e, const Schedule &S) {
@@ -204,6 +354,17 @@ Sched to_kernel_sched(int e, const Schedule &S) {
             if ((S.outmap[j] >> t) & 1ULL) m |= (uint16_t)(1u << j);
         k.outmask[t] = m;
     }
+    run_identity(k);
+    if (!S.grp_seq.empty()) {
+        k.nseq = (int)S.grp_seq.size();
+        k.ngrp = (int)S.grp_size.size();
+        for (int i = 0; i < k.nseq; ++i) k.seq[i] = (uint8_t)S.grp_seq[i];
+        for (int g = 0; g < k.ngrp; ++g) {
+            k.gsize[g] = (uint8_t)S.grp_size[g];
+            k.gmask[g] = (uint16_t)S.grp_mask[g];
+        }
+        k.run_load = S.grp_load;
+    }
     return k;
 }
 
@@ -215,6 +376,7 @@ Sched plane_sched() {
     k.nprod = 1;
     k.subset[0] = 1;
     k.outmask[0] = 1;
+    run_identity(k);
     return k;
 }
 
@@ -378,7 +540,18 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags, in
     return L;
 }
 
+// GF(2) plane products one launch_form call runs (the grouped running-sum sequence repeats some)
+int form_products(const Sched &ks, const TcArgs &a, int form) {
+    if (form != kFormFp4Run || (int64_t)ks.run_load * a.kwords * 64 >= kRunMaxSum) return ks.nprod;
+    return ks.nseq;
+}
+
 cudaError_t launch_form(const Sched &ks, const TcArgs &a, int form, cudaStream_t st) {
+    if (form == kFormFp4Run && (int64_t)ks.run_load * a.kwords * 64 >= kRunMaxSum) {
+        Sched plain = ks;  // the grouping's accumulators would overflow at this k: plain order
+        run_identity(plain);
+        return launch_product_run(plain, a, st);
+    }
     return form == kFormFp4Run ? launch_product_run(ks, a, st) : launch_product_tc2(ks, a, form, st);
 }
 
@@ -468,7 +641,7 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
         TcArgs a{Ac, Bx, L.a_pstride, L.b_pstride, L.kwords, m, n, L.m_pad, L.n_pad, C, ldc, pc, acc ? 1 : 0};
         ProfScope prof(st);
         CK(launch_form(ks, a, form, st), "product");
-        g_products += ks.nprod;
+        g_products += form_products(ks, a, form);
         g_kernel = form_name(form);
     }
     return GF2E_OK;
@@ -1280,6 +1453,23 @@ int gf2e_fp4_selfcheck(int rerun, int inject_fault, int *ok) {
     return GF2E_OK;
 }
 
+int gf2e_run_schedule(int e, uint32_t f, int *nseq, int *ngrp, int *run_load, int *seq, int *gsize,
+                      uint32_t *gmask) {
+    g_err.clear();
+    if (int rc = check_field(e, f)) return rc;
+    const Sched k = to_kernel_sched(e, get_schedule(e, f));
+    if (nseq) *nseq = k.nseq;
+    if (ngrp) *ngrp = k.ngrp;
+    if (run_load) *run_load = k.run_load;
+    for (int i = 0; i < k.nseq; ++i)
+        if (seq) seq[i] = k.seq[i];
+    for (int g = 0; g < k.ngrp; ++g) {
+        if (gsize) gsize[g] = k.gsize[g];
+        if (gmask) gmask[g] = k.gmask[g];
+    }
+    return GF2E_OK;
+}
+
 int64_t gf2e_tile_cols(int e, uint32_t f, int64_t k, uint32_t flags) {
     g_err.clear();
     if (check_field(e, f) || check_flags(flags)) return -1;
@@ -1579,7 +1769,7 @@ int gf2e_slice_mul_parts(int e, uint32_t f, const uint64_t *A, int64_t lda, int6
                      (avail - done) * tw, C + n0 / 64, ldc, pc, acc ? 1 : 0};
             ProfScope prof(st);
             CK(launch_form(ks, a, form, st), "product");
-            g_products += ks.nprod;
+            g_products += form_products(ks, a, form);
             done = avail;
         }
     }
@@ -1794,7 +1984,7 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
                       dCs[sl] + c0 / 64, nwn, rows * nwn, acc ? 1 : 0};
             ProfScope prof(P.sc);
             CK(launch_form(ks, ta, form, P.sc), "product");
-            g_products += ks.nprod;
+            g_products += form_products(ks, ta, form);
             tr.mark(P.sc, "product", i, p);
             if (last && p == 0 && cs < n) {  // first column part out while the second computes
                 const int64_t cw = cs * w / 64;

@@ -13,12 +13,23 @@ constexpr int kMaxE = 10;
 constexpr int kMaxProducts = 64;
 
 // Karatsuba schedule handed to kernels by value (kernel parameter space).
+constexpr int kMaxSeq = 128;
+
 struct Sched {
     int e;                          // input planes
     int nprod;                      // K(e)
     int nout;                       // output planes (e, or 1 for a plain GF(2) product)
     uint16_t subset[kMaxProducts];  // input planes XOR-ed into operand t
     uint16_t outmask[kMaxProducts]; // output planes product t is folded into (M = R_f.Gamma)
+    // running-sum form (product_run.cu): the products are accumulated in ngrp groups, one
+    // accumulator drain per group.  Entry i of the sequence is product seq[i]; group g is the
+    // next gsize[g] entries and its drain parity is folded into the output planes gmask[g].
+    // Identity: one group per product (gmask = outmask).  run_load = the most entries any one
+    // of the two accumulators takes per tile (exactness bound of the running sums).
+    int nseq, ngrp, run_load;
+    uint8_t seq[kMaxSeq];
+    uint8_t gsize[kMaxSeq];
+    uint16_t gmask[kMaxSeq];
 };
 
 __host__ __device__ __forceinline__ int64_t words_for(int64_t ncols) { return (ncols + 63) >> 6; }

@@ -85,7 +85,7 @@ __device__ unsigned long long g_instr_run[1024][32];
 struct __align__(8) Bars {
     uint64_t full[S], empty[S], bfullB[S], tfull[2], tempty[2], bfull[D], bempty[D];
     uint32_t tmem_base;
-    uint16_t outmask[kMaxProducts];
+    uint16_t gmask[kMaxSeq];  // output planes of each drain group
 };
 static_assert(sizeof(Bars) <= BARS_BYTES, "barrier block");
 
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
     const int64_t ntiles = tiles_m * tiles_n;
     const int64_t my_tiles = ntiles > cluster ? (ntiles - cluster + nclusters - 1) / nclusters : 0;
     const int nks = (int)(a.kwords / KW);
-    const int64_t total = my_tiles * (int64_t)s.nprod * nks;
+    const int64_t total = my_tiles * (int64_t)s.nseq * nks;  // operand stages (entries x k-stages)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         }
         mbar_fence_init();
     }
-    if (threadIdx.x < kMaxProducts) bars->outmask[threadIdx.x] = s.outmask[threadIdx.x];
+    if (threadIdx.x < kMaxSeq) bars->gmask[threadIdx.x] = s.gmask[threadIdx.x];
     if (warp == MMA_WARP) tmem_alloc2(&bars->tmem_base, 512);
     tc_fence_before();
     __syncthreads();
@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
             int64_t tm, tn;
             tile_coords(tile, tiles_m, tiles_n, tm, tn);
             const int64_t rbA = tm * 2 + rank, rbB = tn * 2 + rank;
-            for (int t = 0; t < s.nprod; ++t) {
+            for (int i = 0; i < s.nseq; ++i) {
+                const int t = s.seq[i];  // entry i of the grouped sequence is product t
                 const uint64_t *Ab = a.Ac + t * a.a_pstride + rbA * KS * tw_a;
                 const uint64_t *Bb = a.Bt + t * a.b_pstride + rbB * KS * tw_b;
                 for (int ks = 0; ks < nks; ++ks) {
@@ -402,16 +403,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
             for (int j = 0; j < E; ++j)
 #pragma unroll
                 for (int c = 0; c < CH; ++c) acc[j][c] = 0;
-            for (int t = 0; t < s.nprod; ++t, ++gp) {
+            for (int t = 0; t < s.ngrp; ++t, ++gp) {  // one drain per group
                 const int b = (int)(gp & 1);
-                const uint32_t mask = bars->outmask[t];
+                const uint32_t mask = bars->gmask[t];
                 TWR(i_tfull, mbar_wait(&bars->tfull[b], (uint32_t)((gp >> 1) & 1)));
 #if GF2E_INSTR
                 const long long i_d0 = clock64();
 #endif
                 tc_fence_after();
                 const uint32_t ta = tmem + lq + (b ? ACC1 : 0u) + (uint32_t)(h * (CH * 32));
-                const bool last = t + 2 >= s.nprod;  // this buffer's last product in the tile
+                const bool last = t + 2 >= s.ngrp;  // this buffer's last group in the tile
                 uint32_t sel[E];  // all-ones for the output planes this product folds into
 #pragma unroll
                 for (int j = 0; j < E; ++j) sel[j] = 0u - ((mask >> j) & 1u);
@@ -519,12 +520,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(i_g0));
 #endif
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
-            for (int t = 0; t < s.nprod; ++t, ++gp) {
+            for (int t = 0; t < s.ngrp; ++t, ++gp) {  // group t: its entries into one accumulator
                 const int b = (int)(gp & 1);
                 TWR(i_tempty, mbar_wait(&bars->tempty[b], (uint32_t)((gp >> 1) & 1) ^ 1));
                 tc_fence_after();
                 const uint32_t dt = tmem + (b ? ACC1 : 0u);
-                for (int ks = 0; ks < nks; ++ks) {
+                for (int ks = 0; ks < nks * s.gsize[t]; ++ks) {
                     TWR(i_full, mbar_wait(&bars->full[st], phase));
                     tc_fence_after();
                     const uint32_t sb = st0 + (uint32_t)(st * B_BYTES);

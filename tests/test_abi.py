@@ -51,6 +51,28 @@ def test_native_schedule_custom_f(e, f):
     assert list(s.outmap) == o.outmap and list(s.subsets) == o.subsets
 
 
+@pytest.mark.parametrize("e,f", [(e, None) for e in range(2, 11)] + [(4, 0b11001), (8, 0x11B), (10, 0b10000001111)])
+def test_run_grouping_reproduces_outmap(e, f):
+    # the running-sum form's drain groups: every output plane b must receive exactly the
+    # products of outmap[b], i.e. for each product t the XOR of the masks of the groups it is
+    # accumulated into is its column of M (oracle schedule, poly_mul.py:245-259)
+    o = oracle.schedule(e, f)
+    seq, gsize, gmask, load = g._lib.run_schedule(e, o.f)
+    K = len(o.subsets)
+    assert sum(gsize) == len(seq) and all(0 <= t < K for t in seq)
+    col = [0] * K
+    i = 0
+    buf = [0, 0]
+    for gi, (n, m) in enumerate(zip(gsize, gmask)):
+        for t in seq[i:i + n]:
+            col[t] ^= m
+        buf[gi & 1] += n
+        i += n
+    want = [sum(((o.outmap[b] >> t) & 1) << b for b in range(e)) for t in range(K)]
+    assert col == want
+    assert load == max(buf) and len(gsize) <= K
+
+
 def test_schedule_rejects_bad_fields():
     n = ctypes.c_int()
     L = _lib.load()

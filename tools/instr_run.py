@@ -40,8 +40,10 @@ names = {0: "exp wait empty", 1: "exp wait bfull", 2: "exp work (expand+wait_st)
 for i, nm in names.items():
     col = a[0::2, i] if 8 <= i <= 11 else a[:, i]
     print(f"{nm:28s} {col.mean():14.0f} cycles  {100 * col.mean() / tot:5.1f}%")
-K = g.count_products(e)
+K = len(_lib.run_schedule(e, ctx.f)[0])  # entries (MMA products) per tile of the grouped sequence
+if os.environ.get("GF2E_RUN_DRAINS") and int(os.environ["GF2E_RUN_DRAINS"]) >= g.count_products(e):
+    K = g.count_products(e)
 tiles = (-(-m // 256)) * (-(-n // 192))
 per_pair = tiles / (nb // 2) * K
-print(f"products per CTA pair {per_pair:.0f}; cycles per product (MMA thread): {a[0::2, 10].mean() / per_pair:.0f}; "
+print(f"entries per CTA pair {per_pair:.0f}; cycles per entry (MMA thread): {a[0::2, 10].mean() / per_pair:.0f}; "
       f"SM clock {a[0::2, 10].mean() / a[0::2, 11].mean():.3f} GHz over {a[0::2, 11].mean() / 1e6:.2f} ms")
