@@ -1047,7 +1047,7 @@ int ple_rec(PleCtx &c, int64_t r0, int64_t c0, int64_t m, int64_t n, int64_t *P,
     uint64_t *V = c.S + r0 * c.ld + c0 / 64;
     if (n <= kPlePanel) {  // base case nj_ple (newton_john.py:207-260) on one plane word
         CK(launch_ple_panel(c.e, c.tab, V, c.ld, c.ps, m, (int)n, c.pout, c.st), "ple_panel");
-        g_launches += m > ple_window() ? 2 : 1;
+        g_launches += m > ple_window(c.e) ? 2 : 1;
         ++c.panels;
         struct Head {  // the leading members of PanelOut (rank .. Q)
             int rank, ndisp, window, pad;
@@ -1161,7 +1161,7 @@ int ple_rec_spec(PleSpec &c, int64_t r0, int64_t c0, int64_t m, int64_t n) {
     uint64_t *V = c.S + r0 * c.ld + c0 / 64;
     if (n <= kPlePanel) {
         CK(launch_ple_panel(c.e, c.tab, V, c.ld, c.ps, m, (int)n, c.pout, c.st), "ple_panel");
-        g_launches += m > ple_window() ? 1 : 0;
+        g_launches += m > ple_window(c.e) ? 1 : 0;
         CK(launch_ple_commit(c.pout, c.Pg, c.Qg, r0, c0, (int)(m < n ? m : n), c.flag, c.st), "ple_commit");
         return GF2E_OK;
     }

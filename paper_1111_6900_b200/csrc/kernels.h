@@ -167,7 +167,7 @@ struct FieldTab {
     uint32_t f;                              // the field polynomial (bit e set)
 };
 const FieldTab *field_tab(int e, uint32_t f, uint32_t g);  // device pointer (synchronous fill)
-int ple_window();  // rows kept in shared memory by the panel kernel (launches = 1 + (m > window))
+int ple_window(int e);  // rows kept in shared memory by the panel kernel (launches = 1 + (m > window))
 cudaError_t launch_ple_panel(int e, const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb,
                              PanelOut *out, cudaStream_t st);
 // speculative PLE: swaps t <-> Pg[t] (t in [t0, t1)) read from device memory; a panel's pivots

@@ -41,10 +41,14 @@ __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * block
 
 // ---- per-field constant tables (static module memory, filled once per (e, f)) ----------------
 
-#ifndef GF2E_PLE_WIN
-#define GF2E_PLE_WIN 128
+// window rows of the panel kernel: 128, or 64 for e >= GF2E_PLE_WIN64_E (a window row is
+// nonzero at a pivot column with probability 1 - 2^-e, so 64 rows leave the lazy scan below
+// the window practically unused there while halving the panel kernel's threads)
+#ifndef GF2E_PLE_WIN64_E
+#define GF2E_PLE_WIN64_E 5
 #endif
-constexpr int PT = GF2E_PLE_WIN;  // phase-1 threads = window rows
+template <int E>
+constexpr int ple_win() { return E >= GF2E_PLE_WIN64_E ? 64 : 128; }
 constexpr int KP = 64;   // pivots per panel (one plane word)
 
 __device__ __forceinline__ uint64_t swap_bits(uint64_t w, int a, int b) {
@@ -74,8 +78,9 @@ __device__ __forceinline__ void stepE(uint64_t *v, uint32_t x, const uint64_t *b
 // one ballot); 1024 threads, RP rows per pass.
 template <int E>
 struct FindShape {
-    static constexpr int NT = 1024;
+    static constexpr int PT = ple_win<E>();      // window rows
     static constexpr int TPR = E <= 8 ? 8 : 16;
+    static constexpr int NT = PT * TPR < 1024 ? PT * TPR : 1024;
     static constexpr int RP = NT / TPR;           // window rows per pass
     static constexpr int PASSES = (PT + RP - 1) / RP;
     static constexpr uint32_t EMASK = (1u << E) - 1;
@@ -93,7 +98,7 @@ __global__ void __launch_bounds__(1024) k_ple_find(const FieldTab *__restrict__ 
                                                    PanelOut *__restrict__ out) {
     using F = FindShape<E>;
     using SP = PleSplit<E>;
-    constexpr int NT = F::NT, TPR = F::TPR;
+    constexpr int NT = F::NT, TPR = F::TPR, PT = F::PT;
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t *win = reinterpret_cast<uint64_t *>(smem);  // [PT][E]
     uint64_t *ptab = win + PT * E;                       // [Q][E]: multiples of the current T_r
@@ -601,6 +606,7 @@ inline int grid_for(int64_t total, int threads) {
 template <int E>
 cudaError_t launch_ple_e(const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb, PanelOut *out,
                          cudaStream_t st) {
+    constexpr int PT = FindShape<E>::PT;
     const int smem = (PT * E + PleSplit<E>::QE) * 8 + (1 << E) * E * 4 + (1 << E) * 2;
     const int smem2 = (int)ApplyShape<E>::SMEM;
     // launch attributes once per instantiation and device (idempotent)
@@ -623,7 +629,7 @@ cudaError_t launch_ple_e(const FieldTab *tab, uint64_t *S, int64_t ld, int64_t p
     return cudaGetLastError();
 }
 
-int ple_window() { return PT; }
+int ple_window(int e) { return e >= GF2E_PLE_WIN64_E ? 64 : 128; }
 
 cudaError_t launch_ple_panel(int e, const FieldTab *tab, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int nb,
                              PanelOut *out, cudaStream_t st) {
