@@ -186,6 +186,13 @@ __global__ void __launch_bounds__(512, 1) k_nj_sliced(const FieldTab *__restrict
     for (int q = 0; q < Sh::MAXPASS; ++q) v[q] = 0;
     for (int64_t i0 = 0; i0 < k; i0 += KC) {
         const int kc = (int)(k - i0 < KC ? k - i0 : KC);
+        // this chunk's A words, loaded before the tables are built (their latency overlaps)
+        uint64_t aw[Sh::MAXPASS];
+#pragma unroll
+        for (int q = 0; q < Sh::MAXPASS; ++q) {
+            const int64_t r = row0 + q * Sh::RPC + rl;
+            aw[q] = (q < npass && r < m && b < E) ? A[b * pa + r * lda + (i0 >> 6)] : 0;
+        }
         __syncthreads();  // the previous chunk's tables are consumed
         for (int i = tid; i < kc * E; i += Sh::THREADS) bs[i] = B[(i % E) * pb + (i0 + i / E) * ldb + w];
         __syncthreads();
@@ -223,18 +230,19 @@ __global__ void __launch_bounds__(512, 1) k_nj_sliced(const FieldTab *__restrict
 #pragma unroll
         for (int q = 0; q < Sh::MAXPASS; ++q) {
             if (q >= npass) break;
-            const int64_t r = row0 + q * Sh::RPC + rl;
-            const uint64_t aw = (r < m && b < E) ? A[b * pa + r * lda + (i0 >> 6)] : 0;
+            // entry 0 of every table is zero: no branch on x; lanes past the planes (TPR > E)
+            // read plane-0 words and drop them at the store
+            const uint64_t *tb = tab + (b < E ? b : 0);
+            const uint64_t arow = aw[q] >> sh;
+#pragma unroll 4
             for (int i = 0; i < kc; ++i) {
-                const unsigned bal = __ballot_sync(0xffffffffu, (aw >> (sh + i)) & 1ULL);
+                const unsigned bal = __ballot_sync(0xffffffffu, (arow >> i) & 1ULL);
                 const uint32_t x = (bal >> gl) & EMASK;
-                if (x && b < E) {
-                    const uint64_t *ti = tab + i * QE + b;
-                    if constexpr (SP::H2 > 0)
-                        v[q] ^= ti[(x & ((1u << SP::H1) - 1)) * E] ^ ti[((1u << SP::H1) + (x >> SP::H1)) * E];
-                    else
-                        v[q] ^= ti[x * E];
-                }
+                const uint64_t *ti = tb + i * QE;
+                if constexpr (SP::H2 > 0)
+                    v[q] ^= ti[(x & ((1u << SP::H1) - 1)) * E] ^ ti[((1u << SP::H1) + (x >> SP::H1)) * E];
+                else
+                    v[q] ^= ti[x * E];
             }
         }
     }
