@@ -135,6 +135,11 @@ __global__ void __launch_bounds__(TriShape<E, TB>::THREADS)
             tmask[q] = smk[c * E + b];
         }
     }
+    // one table word per thread (the common case): its plane selection as 64-bit AND masks
+    constexpr bool ONE = S::NB == 1;
+    uint64_t tsel[ONE ? E : 1];
+#pragma unroll
+    for (int p = 0; p < (ONE ? E : 1); ++p) tsel[p] = 0ULL - (uint64_t)((tmask[0] >> p) & 1u);
     __syncthreads();  // cU
     for (int step = 0; step < rows; ++step) {
         const int i = upper ? rows - 1 - step : step;
@@ -145,19 +150,29 @@ __global__ void __launch_bounds__(TriShape<E, TB>::THREADS)
         }
         const uint32_t c = cU[i * TB + k];
         __syncthreads();  // X_i published
-#pragma unroll
-        for (int q = 0; q < S::NB; ++q) {
-            const int idx = threadIdx.x + q * S::THREADS;
-            if (idx < S::TW) {
-                const uint64_t *pv = pub + (idx % NW) * E;
+        if constexpr (ONE) {
+            if (threadIdx.x < S::TW) {
+                const uint64_t *pv = pub + (threadIdx.x % NW) * E;
                 uint64_t acc = 0;
 #pragma unroll
-                for (int p = 0; p < E; ++p) acc ^= pv[p] & (0ULL - (uint64_t)((tmask[q] >> p) & 1u));
-                tab[idx] = acc;
+                for (int p = 0; p < E; ++p) acc ^= pv[p] & tsel[p];
+                tab[threadIdx.x] = acc;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < S::NB; ++q) {
+                const int idx = threadIdx.x + q * S::THREADS;
+                if (idx < S::TW) {
+                    const uint64_t *pv = pub + (idx % NW) * E;
+                    uint64_t acc = 0;
+#pragma unroll
+                    for (int p = 0; p < E; ++p) acc ^= pv[p] & (0ULL - (uint64_t)((tmask[q] >> p) & 1u));
+                    tab[idx] = acc;
+                }
             }
         }
         __syncthreads();  // table built
-        if (c) {
+        {  // entry 0 of both tables is zero: no branch on c
             const uint64_t *lo = tab + (size_t)(c & ((1u << H1) - 1)) * E * NW + w;
             if constexpr (S::H2 > 0) {
                 const uint64_t *hi = tab + (size_t)((1u << H1) + (c >> H1)) * E * NW + w;
