@@ -2171,13 +2171,49 @@ int gf2e_echelonize(int e, uint32_t f, uint64_t *S, int64_t ld, int64_t ps, int6
         CKH(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     }
     CKH(cudaMemcpyAsync(idx, Q.data(), r * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
-    CK(launch_echelon_marks(e, S, ld, ps, m, idx, (int)r, st), "echelon_marks");  // (:364-370)
+    // per column word: its pivots in increasing t and the prefix ORs of their bits
+    const int64_t nw = words_for(n);
+    std::vector<std::vector<int>> per(nw);
+    for (int64_t t = 0; t < r; ++t) per[Q[t] >> 6].push_back((int)t);
+    std::vector<int> wstart(nw + 1), tpos;
+    std::vector<uint64_t> pmask;
+    tpos.reserve(r);
+    pmask.reserve(r);
+    for (int64_t w = 0; w < nw; ++w) {
+        wstart[w] = (int)tpos.size();
+        uint64_t acc = 0;
+        for (int t : per[w]) {
+            acc |= 1ULL << (Q[t] & 63);
+            tpos.push_back(t);
+            pmask.push_back(acc);
+        }
+    }
+    wstart[nw] = (int)tpos.size();
+    const size_t mk_bytes = align256((nw + 1) * 4) + align256(r * 4) + (size_t)r * 8;
+    DevTmp mk(mk_bytes, st);
+    if (!mk.p) return fail(GF2E_ENOMEM, "out of device memory (echelonize marks)");
+    int *d_ws = static_cast<int *>(mk.p);
+    int *d_tp = reinterpret_cast<int *>(static_cast<char *>(mk.p) + align256((nw + 1) * 4));
+    uint64_t *d_pm = reinterpret_cast<uint64_t *>(static_cast<char *>(mk.p) + align256((nw + 1) * 4) + align256(r * 4));
+    CKH(cudaMemcpyAsync(d_ws, wstart.data(), (nw + 1) * 4, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    CKH(cudaMemcpyAsync(d_tp, tpos.data(), r * 4, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    CKH(cudaMemcpyAsync(d_pm, pmask.data(), r * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    CK(launch_echelon_marks(e, S, ld, ps, m, nw, idx, (int)r, d_ws, d_tp, d_pm, st), "echelon_marks");  // (:364-370)
     if (full) {  // rows[:r] = upper^-1 rows[:r], upper = pivot columns (:371-375)
         const int64_t lw = words_for(r);
         DevTmp ut((size_t)e * r * lw * 8, st);
         if (!ut.p) return fail(GF2E_ENOMEM, "out of device memory (echelonize corner)");
         uint64_t *U = static_cast<uint64_t *>(ut.p);
-        CK(launch_gather_cols(e, S, ld, ps, idx, r, U, lw, r * lw, st), "gather_cols");
+        bool ident = true;  // pivot columns 0 .. r-1 (a generic matrix): the gather is a copy
+        for (int64_t t = 0; t < r && ident; ++t) ident = Q[t] == t;
+        if (ident) {
+            for (int b = 0; b < e; ++b)
+                CKH(cudaMemcpy2DAsync(U + b * r * lw, lw * 8, S + b * ps, ld * 8, lw * 8, r, cudaMemcpyDeviceToDevice,
+                                      st),
+                    "cudaMemcpy2DAsync");
+        } else {
+            CK(launch_gather_cols(e, S, ld, ps, idx, r, U, lw, r * lw, st), "gather_cols");
+        }
         const int64_t tws = gf2e_trsm_workspace(e, f, r, n);
         DevTmp tw((size_t)(tws > 0 ? tws : 256), st);
         if (!tw.p) return fail(GF2E_ENOMEM, "out of device memory (echelonize trsm workspace)");

@@ -182,8 +182,10 @@ cudaError_t launch_col_swaps(int planes, int w, uint64_t *S, int64_t ld, int64_t
                              int n, cudaStream_t st);
 cudaError_t launch_tril_copy(int e, const uint64_t *S, int64_t ld, int64_t ps, int64_t r, uint64_t *out, int64_t ldo,
                              int64_t po, cudaStream_t st);
-cudaError_t launch_echelon_marks(int e, uint64_t *S, int64_t ld, int64_t ps, int64_t m, const int64_t *Q, int r,
-                                 cudaStream_t st);
+// (wstart: nw + 1 offsets; tpos / pmask: per column word, its pivots' t in increasing order and
+// the prefix ORs of their bits -- built on the host from Q)
+cudaError_t launch_echelon_marks(int e, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int64_t nw, const int64_t *Q,
+                                 int r, const int *wstart, const int *tpos, const uint64_t *pmask, cudaStream_t st);
 cudaError_t launch_gather_cols(int e, const uint64_t *S, int64_t ld, int64_t ps, const int64_t *Q, int64_t r,
                                uint64_t *out, int64_t ldo, int64_t po, cudaStream_t st);
 

@@ -566,16 +566,30 @@ __global__ void k_tril_copy(int e, const uint64_t *__restrict__ S, int64_t ld, i
 }
 
 // echelonize: rows >= t lose column Q[t]; row t < r gets the leading one at Q[t]
-__global__ void k_echelon_marks(int e, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t m,
-                                const int64_t *__restrict__ Q, int r) {
-    for (int64_t i = gtid(); i < m; i += gstride()) {
+// Row i clears the pivot columns Q[t], t <= min(i, r - 1), in every plane, and row i < r sets
+// its leading one.  Thread = (row, column word); the host lists, per column word, the pivots
+// it holds in increasing t (tpos) with prefix ORs of their bits (pmask), so a thread's mask is
+// one binary search away.
+__global__ void k_echelon_marks(int e, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t m, int64_t nw,
+                                const int64_t *__restrict__ Q, int r, const int *__restrict__ wstart,
+                                const int *__restrict__ tpos, const uint64_t *__restrict__ pmask) {
+    const int64_t total = m * nw;
+    for (int64_t idx = gtid(); idx < total; idx += gstride()) {
+        const int64_t i = idx / nw, w = idx - i * nw;
         const int tmax = (int)(i < r - 1 ? i : r - 1);
-        for (int t = 0; t <= tmax; ++t) {
-            const int64_t c = Q[t];
-            const uint64_t bit = 1ULL << (c & 63);
-            for (int b = 0; b < e; ++b) S[b * ps + i * ld + (c >> 6)] &= ~bit;
+        int lo = wstart[w], hi = wstart[w + 1];  // first entry with tpos > tmax
+        const int base = lo;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (tpos[mid] <= tmax)
+                lo = mid + 1;
+            else
+                hi = mid;
         }
-        if (i < r) S[i * ld + (Q[i] >> 6)] |= 1ULL << (Q[i] & 63);
+        const uint64_t mask = lo > base ? pmask[lo - 1] : 0ULL;
+        if (mask)
+            for (int b = 0; b < e; ++b) S[b * ps + i * ld + w] &= ~mask;
+        if (i < r && (Q[i] >> 6) == w) S[i * ld + w] |= 1ULL << (Q[i] & 63);
     }
 }
 
@@ -743,10 +757,10 @@ cudaError_t launch_tril_copy(int e, const uint64_t *S, int64_t ld, int64_t ps, i
     return cudaGetLastError();
 }
 
-cudaError_t launch_echelon_marks(int e, uint64_t *S, int64_t ld, int64_t ps, int64_t m, const int64_t *Q, int r,
-                                 cudaStream_t st) {
+cudaError_t launch_echelon_marks(int e, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int64_t nw, const int64_t *Q,
+                                 int r, const int *wstart, const int *tpos, const uint64_t *pmask, cudaStream_t st) {
     if (r == 0 || m == 0) return cudaSuccess;
-    k_echelon_marks<<<grid_for(m, 256), 256, 0, st>>>(e, S, ld, ps, m, Q, r);
+    k_echelon_marks<<<grid_for(m * nw, 256), 256, 0, st>>>(e, S, ld, ps, m, nw, Q, r, wstart, tpos, pmask);
     return cudaGetLastError();
 }
 

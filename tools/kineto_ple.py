@@ -1,5 +1,5 @@
-"""Dev: real (not ncu-serialised) kernel times and device idle of one PLE, from torch.profiler
-(CUPTI activity records).  python tools/kineto_ple.py e n"""
+"""Dev: real (not ncu-serialised) kernel times and device idle of one PLE (or echelonize with
+--ech), from torch.profiler (CUPTI activity records).  python tools/kineto_ple.py e n [--ech]"""
 import collections
 import os
 import sys
@@ -14,12 +14,13 @@ e, n = int(sys.argv[1]), int(sys.argv[2])
 ctx = g.field_new(e)
 S0 = g.slice_packed(g.PackedMatrix.random(ctx, n, n, 11))
 S = S0.copy()
-g.ple_sliced(S)
+op = (lambda X: g.echelonize_sliced(X, True)) if "--ech" in sys.argv else g.ple_sliced
+op(S)
 torch.cuda.synchronize()
 S.planes.copy_(S0.planes)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA], acc_events=True) as prof:
-    g.ple_sliced(S)
+    op(S)
     torch.cuda.synchronize()
 evs = [ev for ev in prof.events() if ev.device_type == torch.autograd.DeviceType.CUDA]
 kern = [(ev.time_range.start, ev.time_range.end, ev.name) for ev in evs]
