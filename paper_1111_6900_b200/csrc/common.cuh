@@ -206,6 +206,13 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
            | ((uint32_t)(N >> 3) << 17)   // N
            | ((uint32_t)(M >> 4) << 24);  // M
 }
+// Programmatic dependent launch for the consumers' chains of small kernels (PLE, TRSM): a
+// kernel launched with launch_pdl may start while its predecessor in the stream finishes; it
+// signals its own dependents at once (pdl_trigger) and waits for the predecessor's completion
+// and memory (pdl_wait) before its first access to data the chain produces -- only reads of
+// the constant field tables come before.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 #endif  // __CUDACC__
 
 }  // namespace gf2e

@@ -197,4 +197,23 @@ cudaError_t run_fp4_probe(int iters, int mode, const uint8_t *a_img, const uint8
                           cudaStream_t st, float *ms);
 cudaError_t run_mma_peak(int cta_group, int iters, int nsms, cudaStream_t st, float *ms);
 
+
+// launch with programmatic stream serialization (GF2E_PDL=0 turns it off): the kernel must
+// call pdl_wait() before touching data its predecessors produce (common.cuh)
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace gf2e

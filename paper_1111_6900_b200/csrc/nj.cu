@@ -178,6 +178,8 @@ __global__ void __launch_bounds__(512, 1) k_nj_sliced(const FieldTab *__restrict
     extern __shared__ __align__(16) uint64_t nsm[];
     uint64_t *tab = nsm;                   // [KC][Q][E]
     uint64_t *bs = tab + KC * QE;          // [KC][E]: the chunk's rows of B, word w
+    pdl_trigger();
+    pdl_wait();  // A, B, C come from the chain
     const int tid = threadIdx.x, lane = tid & 31, b = tid % TPR, gl = lane - b, rl = tid / TPR;
     const int64_t w = blockIdx.x;
     const int64_t row0 = (int64_t)blockIdx.y * Sh::RPC * npass;
@@ -289,9 +291,8 @@ cudaError_t launch_nj_sliced_e(const FieldTab *ftab, const uint64_t *A, int64_t 
     const int64_t rb = (m + (int64_t)Sh::RPC * npass - 1) / ((int64_t)Sh::RPC * npass);
     if (nw > 0x7fffffff || rb > 65535) return cudaErrorInvalidValue;
     dim3 grid((unsigned)nw, (unsigned)rb);
-    k_nj_sliced<E><<<grid, Sh::THREADS, Sh::SMEM, st>>>(ftab, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, acc ? 1 : 0,
-                                                         npass);
-    return cudaGetLastError();
+    return launch_pdl(k_nj_sliced<E>, grid, dim3(Sh::THREADS), Sh::SMEM, st, ftab, A, lda, pa, B, ldb, pb, C, ldc, pc, m,
+                      k, n, acc ? 1 : 0, npass);
 }
 
 }  // namespace

@@ -25,6 +25,7 @@
 //   k_echelon_marks: echelonize's "drop L, set the implicit leading ones" (ple_echelon.py:364-370).
 //   k_gather_cols: pivot columns of the leading rows as an r x r matrix (_gather_columns,
 //     ple_echelon.py:338-340).
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(1024) k_ple_find(const FieldTab *__restrict__ 
     __shared__ unsigned long long s_supp;
     __shared__ int64_t s_pmin;
 
+    pdl_trigger();
     const int tid = threadIdx.x;
     const int lane = tid & 31, b = tid % TPR, gl = lane - b, rl = tid / TPR;
     const int W = (int)(m < PT ? m : PT);
@@ -130,6 +132,7 @@ __global__ void __launch_bounds__(1024) k_ple_find(const FieldTab *__restrict__ 
         for (int q = 0; q < E; ++q) smm[i * E + q] = tab->mulmask2[i][q];
     }
     __syncthreads();
+    pdl_wait();  // the field tables above are constant; S and out come from the chain
     // window rows; candidates for column 0 (lowest row of each warp with a nonzero entry)
 #pragma unroll
     for (int pass = 0; pass < F::PASSES; ++pass) {
@@ -369,6 +372,8 @@ struct ApplyShape {
 template <int E>
 __global__ void __launch_bounds__(512) k_ple_apply(uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t m, int nb,
                                                    const PanelOut *__restrict__ in) {
+    pdl_trigger();
+    pdl_wait();
     using A = ApplyShape<E>;
     using SP = PleSplit<E>;
     extern __shared__ __align__(16) uint64_t ctab[];  // [CH][Q][E]
@@ -460,6 +465,8 @@ __global__ void k_row_swaps(int planes, uint64_t *__restrict__ S, int64_t ld, in
 // speculative PLE: the pivots stay in device memory, ple_commit)
 __global__ void k_row_swaps_vec(int planes, uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t nwords,
                                 const int64_t *__restrict__ Pg, int64_t t0, int64_t t1) {
+    pdl_trigger();
+    pdl_wait();
     // the pivots are staged in shared memory and compacted to the non-trivial swaps (a generic
     // matrix pivots on the diagonal almost everywhere), 1024 pivot positions at a time; 128
     // threads per block (the compaction's layout)
@@ -518,6 +525,8 @@ __global__ void k_row_swaps_vec(int planes, uint64_t *__restrict__ S, int64_t ld
 // the column offset); a rank other than the speculated one raises the flag
 __global__ void k_ple_commit(const PanelOut *__restrict__ po, int64_t *__restrict__ Pg, int64_t *__restrict__ Qg,
                              int64_t r0, int64_t c0, int expected, int *__restrict__ flag) {
+    pdl_trigger();
+    pdl_wait();
     const int r = po->rank;
     for (int t = threadIdx.x; t < expected; t += blockDim.x) {
         Pg[r0 + t] = t < r ? r0 + po->P[t] : r0 + t;
@@ -550,6 +559,8 @@ __global__ void k_col_swaps(int planes, int w, uint64_t *__restrict__ S, int64_t
 // out[i][c] = S[i][c] for c <= i < r, 0 above the diagonal
 __global__ void k_tril_copy(int e, const uint64_t *__restrict__ S, int64_t ld, int64_t ps, int64_t r,
                             uint64_t *__restrict__ out, int64_t ldo, int64_t po) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t nw = words_for(r);
     const int64_t total = (int64_t)e * r * nw;
     for (int64_t idx = gtid(); idx < total; idx += gstride()) {
@@ -635,12 +646,16 @@ cudaError_t launch_ple_e(const FieldTab *tab, uint64_t *S, int64_t ld, int64_t p
         if (err != cudaSuccess) return err;
         if (dev < kMaxDevices) attr_set[dev] = true;
     }
-    k_ple_find<E><<<1, FindShape<E>::NT, smem, st>>>(tab, S, ld, ps, m, nb, out);
-    err = cudaGetLastError();
+    err = launch_pdl(k_ple_find<E>, dim3(1), dim3(FindShape<E>::NT), smem, st, tab, S, ld, ps, m, nb, out);
     if (err != cudaSuccess || m <= PT) return err;
     using A = ApplyShape<E>;
-    k_ple_apply<E><<<(unsigned)((m - PT + A::RPC - 1) / A::RPC), A::THREADS, smem2, st>>>(S, ld, ps, m, nb, out);
-    return cudaGetLastError();
+    return launch_pdl(k_ple_apply<E>, dim3((unsigned)((m - PT + A::RPC - 1) / A::RPC)), dim3(A::THREADS), smem2, st, S,
+                      ld, ps, m, nb, (const PanelOut *)out);
+}
+
+bool pdl_enabled() {
+    static const bool on = !getenv("GF2E_PDL") || atoi(getenv("GF2E_PDL")) != 0;
+    return on;
 }
 
 int ple_window(int e) { return e >= GF2E_PLE_WIN64_E ? 64 : 128; }
@@ -732,15 +747,14 @@ cudaError_t launch_row_swaps_vec(int planes, uint64_t *S, int64_t ld, int64_t ps
                                  int64_t t0, int64_t t1, cudaStream_t st) {
     if (t1 <= t0 || nwords == 0) return cudaSuccess;
     const int64_t total = (int64_t)planes * nwords;
-    k_row_swaps_vec<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(planes, S, ld, ps, nwords, Pg, t0, t1);
-    return cudaGetLastError();
+    return launch_pdl(k_row_swaps_vec, dim3((unsigned)((total + 127) / 128)), dim3(128), 0, st, planes, S, ld, ps, nwords,
+                      Pg, t0, t1);
 }
 
 cudaError_t launch_ple_commit(const PanelOut *po, int64_t *Pg, int64_t *Qg, int64_t r0, int64_t c0, int expected,
                               int *flag, cudaStream_t st) {
     if (expected <= 0) return cudaSuccess;
-    k_ple_commit<<<1, 64, 0, st>>>(po, Pg, Qg, r0, c0, expected, flag);
-    return cudaGetLastError();
+    return launch_pdl(k_ple_commit, dim3(1), dim3(64), 0, st, po, Pg, Qg, r0, c0, expected, flag);
 }
 
 cudaError_t launch_col_swaps(int planes, int w, uint64_t *S, int64_t ld, int64_t ps, int64_t rows, const int64_t *trip,
@@ -753,8 +767,8 @@ cudaError_t launch_col_swaps(int planes, int w, uint64_t *S, int64_t ld, int64_t
 cudaError_t launch_tril_copy(int e, const uint64_t *S, int64_t ld, int64_t ps, int64_t r, uint64_t *out, int64_t ldo,
                              int64_t po, cudaStream_t st) {
     if (r == 0) return cudaSuccess;
-    k_tril_copy<<<grid_for((int64_t)e * r * words_for(r), 256), 256, 0, st>>>(e, S, ld, ps, r, out, ldo, po);
-    return cudaGetLastError();
+    return launch_pdl(k_tril_copy, dim3(grid_for((int64_t)e * r * words_for(r), 256)), dim3(256), 0, st, e, S, ld, ps,
+                      r, out, ldo, po);
 }
 
 cudaError_t launch_echelon_marks(int e, uint64_t *S, int64_t ld, int64_t ps, int64_t m, int64_t nw, const int64_t *Q,

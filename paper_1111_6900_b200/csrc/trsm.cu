@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(TriShape<E, TB>::THREADS)
     CT *cU = reinterpret_cast<CT *>(pub + NW * E);          // [TB (step)][TB (row)]
     __shared__ uint16_t sinv[1 << E], smk[(1 << E) * E], sex[1 << E], slg[1 << E], sdlog[TB];
     constexpr int ORD = (1 << E) - 1;  // multiplicative group order
+    pdl_trigger();
     for (int i = threadIdx.x; i < (1 << E); i += S::THREADS) {
         sinv[i] = ftab->inv[i];
         sex[i] = ftab->ex[i < ORD ? i : 0];
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(TriShape<E, TB>::THREADS)
 #pragma unroll
         for (int b = 0; b < E; ++b) smk[i * E + b] = ftab->mulmask[i][b];
     }
+    pdl_wait();  // T comes from the chain (the field tables above are constant)
     const int64_t r0 = (int64_t)blockIdx.x * TB;
     const int rows = (int)((m - r0) < TB ? (m - r0) : TB);
     const int k = threadIdx.x / TPR, sub = threadIdx.x % TPR;
@@ -278,9 +280,8 @@ cudaError_t launch_tri_e(const FieldTab *ftab, const uint64_t *T, int64_t ldt, i
         if (err != cudaSuccess) return err;
         if (dev < kMaxDevices) attr_set[dev] = true;
     }
-    k_tri_inverse<E, TB><<<(unsigned)nblk, S::THREADS, S::SMEM, st>>>(ftab, T, ldt, pt, m, upper ? 1 : 0,
-                                                                      unit ? 1 : 0, Tinv, bad_row);
-    return cudaGetLastError();
+    return launch_pdl(k_tri_inverse<E, TB>, dim3((unsigned)nblk), dim3(S::THREADS), S::SMEM, st, ftab, T, ldt, pt, m,
+                      upper ? 1 : 0, unit ? 1 : 0, Tinv, bad_row);
 }
 
 template <int TB>
