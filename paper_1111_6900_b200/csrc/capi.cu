@@ -466,7 +466,6 @@ int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 constexpr int64_t kFp4MinK = 2048;
 // short k: the running-sum fp4 form (double-buffered accumulators, no per-product
 // re-initialisation; config 4 e=8: 17.7 ms against 21.5 ms for int8, profiles/r02)
-constexpr int kSmallKForm = kFormFp4Run;
 constexpr int64_t kFp4LongK = 8192;  // 8 expander / 4 epilogue warps pay off for long accumulations
 // fp4 exactness self-check state per device: 0 not run, 1 passed, -1 failed (fp4 disabled)
 int g_fp4_state[kMaxDevices] = {};
@@ -482,23 +481,32 @@ int fp4_state() {
 // ceil(K/2) products of at most k_pad each per buffer and tile
 bool run_ok(int nprod, int64_t k) { return (int64_t)((nprod + 1) / 2) * round_up(k, kTcBKFp4) < kRunMaxSum; }
 
-int tc_form(uint32_t flags, int64_t k, int nprod = kMaxProducts) {
+// the running-sum form expands B^T in-kernel for products of at most this many rows: there
+// the 4x pre-expanded B^T would be written for one or a few row tiles (GF2E_RUNX_MAXM)
+int64_t runx_max_m() {
+    static const int64_t v = getenv("GF2E_RUNX_MAXM") ? atoll(getenv("GF2E_RUNX_MAXM")) : 2048;
+    return v;
+}
+bool is_run(int form) { return form == kFormFp4Run || form == kFormFp4RunX; }
+
+int tc_form(uint32_t flags, int64_t k, int nprod = kMaxProducts, int64_t m = INT64_MAX) {
     if (flags & GF2E_TC_INT8) return kFormI8;
     if (fp4_state() < 0) return kFormI8;  // the fp4 self-check failed on this device
-    if ((flags & GF2E_TC_RUN) && run_ok(nprod, k)) return kFormFp4Run;
+    const int run = m <= runx_max_m() ? kFormFp4RunX : kFormFp4Run;
+    if ((flags & GF2E_TC_RUN) && run_ok(nprod, k)) return run;
     if (k >= kFp4LongK) return kFormFp4Long;
     if (k >= kFp4MinK) return kFormFp4;
     if (flags & GF2E_TC_FP4) return kFormFp4Pair;
-    return run_ok(nprod, k) ? kSmallKForm : kFormI8;
+    return run_ok(nprod, k) ? run : kFormI8;
 }
 const char *form_name(int form) {
     return form == kFormFp4Pair                            ? "k_product_tc2<fp4x2>"
            : (form == kFormFp4 || form == kFormFp4Long) ? "k_product_tc2<fp4>"
-           : form == kFormFp4Run                          ? "k_product_run<fp4>"
+           : is_run(form)                                 ? "k_product_run<fp4>"
                                                           : "k_product_tc2<i8>";
 }
 // tile columns of a form (CTA-pair tile width; B^T is stage-tiled in half-width row blocks)
-int64_t form_bn(int form) { return form == kFormFp4Run ? kRunBN : kTcBN; }
+int64_t form_bn(int form) { return is_run(form) ? kRunBN : kTcBN; }
 int form_br(int form) { return (int)(form_bn(form) / 2); }
 // B^T words per row per bit word: 4 when the form's B operand is stored pre-expanded
 int64_t form_bx(int form) { return (form == kFormFp4Run && kRunBPre) ? 4 : 1; }
@@ -516,7 +524,7 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags, in
         L.a_pstride = L.m_pad * L.kwords;
         L.b_pstride = L.k_pad * (L.n_pad / 64);
     } else {
-        if (form == -1) form = tc_form(flags, k, nprod);
+        if (form == -1) form = tc_form(flags, k, nprod, m);
         L.m_pad = round_up(m, 2 * kTcBM);  // CTA-pair tiles are 256 rows
         int64_t bx = 1;
         if (form == kFormAny) {  // every form a call with these sizes may take
@@ -542,17 +550,17 @@ Layout layout_for(int nprod, int64_t m, int64_t k, int64_t n, uint32_t flags, in
 
 // GF(2) plane products one launch_form call runs (the grouped running-sum sequence repeats some)
 int form_products(const Sched &ks, const TcArgs &a, int form) {
-    if (form != kFormFp4Run || (int64_t)ks.run_load * a.kwords * 64 >= kRunMaxSum) return ks.nprod;
+    if (!is_run(form) || (int64_t)ks.run_load * a.kwords * 64 >= kRunMaxSum) return ks.nprod;
     return ks.nseq;
 }
 
 cudaError_t launch_form(const Sched &ks, const TcArgs &a, int form, cudaStream_t st) {
-    if (form == kFormFp4Run && (int64_t)ks.run_load * a.kwords * 64 >= kRunMaxSum) {
+    if (is_run(form) && (int64_t)ks.run_load * a.kwords * 64 >= kRunMaxSum) {
         Sched plain = ks;  // the grouping's accumulators would overflow at this k: plain order
         run_identity(plain);
-        return launch_product_run(plain, a, st);
+        return launch_product_run(plain, a, st, form == kFormFp4Run);
     }
-    return form == kFormFp4Run ? launch_product_run(ks, a, st) : launch_product_tc2(ks, a, form, st);
+    return is_run(form) ? launch_product_run(ks, a, st, form == kFormFp4Run) : launch_product_tc2(ks, a, form, st);
 }
 
 // Per host thread and device: a side stream and a fork / join event pair for running the
@@ -596,7 +604,7 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
     const bool tc = !(flags & GF2E_BACKEND_M4RM);
     if (tc && form_override < 0 && !(flags & GF2E_TC_INT8))
         if (int rc = ensure_fp4_checked()) return rc;
-    const int form = form_override >= 0 ? form_override : tc_form(flags, k, ks.nprod);
+    const int form = form_override >= 0 ? form_override : tc_form(flags, k, ks.nprod, m);
     const bool fp4 = tc && form != kFormI8;
     static const bool trace = getenv("GF2E_PROD_TRACE") != nullptr;
     if (trace) fprintf(stderr, "product m=%lld k=%lld n=%lld form=%d\n", (long long)m, (long long)k, (long long)n, form);
@@ -669,7 +677,8 @@ int fp4_probe_run(bool inject, int *ok) {
         int form;
         int64_t k;
         int e;
-    } cases[] = {{kFormFp4Long, 33024, 1}, {kFormFp4, 4096, 1}, {kFormFp4Pair, 1024, 1}, {kFormFp4Run, 1792, 4}};
+    } cases[] = {{kFormFp4Long, 33024, 1}, {kFormFp4, 4096, 1}, {kFormFp4Pair, 1024, 1}, {kFormFp4Run, 1792, 4},
+                 {kFormFp4RunX, 1792, 4}};
     cudaStream_t st = nullptr;
     CKH(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
     struct StreamGuard {

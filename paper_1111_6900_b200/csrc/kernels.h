@@ -83,6 +83,7 @@ constexpr int kFormI8 = 0, kFormFp4 = 1, kFormFp4Pair = 2, kFormFp4Long = 3;  //
 // fp4 running-sum form (product_run.cu): double-buffered accumulators, no per-product
 // re-initialisation; tiles 256 x kRunBN, B^T stage-tiled in kRunBN/2-row blocks
 constexpr int kFormFp4Run = 4;
+constexpr int kFormFp4RunX = 5;  // the running-sum form with B^T expanded in-kernel (few row tiles)
 constexpr int kRunBN = 192;  // tile columns (two 192-column accumulators, three A stages and the
                              // scale factors fill the 512 TMEM columns; 128-column tiles with three
                              // accumulators measured slower: 23.1 vs 17.7 ms at config 4, e = 8)
@@ -93,7 +94,8 @@ constexpr int64_t kRunMaxSum = 65536;  // ceil(K/2) * k_pad must stay below (exa
 // the running-sum form's B^T operand is stored pre-expanded (4 words per bit word, swizzled
 // stage tiles: launch_combos_bt(..., expand)) and bulk-copied straight into shared memory
 constexpr bool kRunBPre = GF2E_RUN_BPRE != 0;
-cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st);
+// bpre: B^T stages pre-expanded (launch_combos_bt(..., expand)); else bit tiles expanded in-kernel
+cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st, bool bpre);
 constexpr int64_t kFp4PairMaxK = 2047;
 cudaError_t launch_product_tc2(const Sched &s, const TcArgs &a, int form, cudaStream_t st);
 

@@ -46,8 +46,14 @@ constexpr int NTHREADS = (NEXP + NEPI + 2) * 32;
 constexpr int B_BYTES = BNH * 128;                     // expanded B^T stage (12 KiB)
 // B^T operand stages: pre-expanded by k_combos_bt and bulk-copied ready for the MMA (kRunBPre),
 // or expanded here from bit tiles
-constexpr bool BPRE = kRunBPre;
-constexpr int BITS_A = BM * KW * 8, BITS_B = BPRE ? 0 : BNH * KW * 8, BITS_BYTES = BITS_A + BITS_B;
+// B^T operand stages: pre-expanded by k_combos_bt and bulk-copied ready for the MMA (BP), or
+// expanded here from bit tiles by the expander warps (products with few row tiles, where the
+// 4x pre-expanded B^T would be written for one or two reads)
+constexpr int BITS_A = BM * KW * 8;
+template <bool BP>
+struct RunMem {
+    static constexpr int BITS_B = BP ? 0 : BNH * KW * 8, BITS_BYTES = BITS_A + BITS_B;
+};
 constexpr uint32_t ACC1 = BN;  // TMEM column of the second accumulator (the first starts at 0)
 constexpr uint32_t ATM0 = 2 * BN, SFA = 480, SFB = 496;
 static_assert(ATM0 + 32 * S <= SFA, "TMEM: A stages overlap the scale factors");
@@ -62,7 +68,8 @@ constexpr int BARS_BYTES = 1024;
 // epilogue staging (per CTA and tile): the E x 128 x 192-bit output words and their C0
 // epilogue staging (per CTA and tile): the E x 128 x 192-bit output words and their C0
 constexpr int STAGE_OUT_BYTES = kMaxE * BM * 24, STAGE_OLD_BYTES = kMaxE * BM * 24;
-constexpr int SMEM_BYTES = S * B_BYTES + D * BITS_BYTES + BARS_BYTES + STAGE_OUT_BYTES + STAGE_OLD_BYTES + 1024;
+constexpr int SMEM_BYTES = S * B_BYTES + D * RunMem<false>::BITS_BYTES + BARS_BYTES + STAGE_OUT_BYTES +
+                           STAGE_OLD_BYTES + 1024;  // (the larger of the two bit rings)
 static_assert(B_BYTES % 1024 == 0, "swizzle atoms need 1024-byte aligned stages");
 static_assert(SMEM_BYTES <= 232448, "shared memory");
 
@@ -171,8 +178,9 @@ __device__ __forceinline__ void mma2_mxf4_ts(uint32_t d, uint32_t at, uint64_t b
         : "memory");
 }
 
-template <int E>
+template <int E, bool BPRE>
 __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, const TcArgs a) {
+    constexpr int BITS_B = RunMem<BPRE>::BITS_B, BITS_BYTES = RunMem<BPRE>::BITS_BYTES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *stages = smem;
@@ -570,13 +578,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
 
 int g_num_sms_run = 0;
 
-template <int E>
+template <int E, bool BP>
 cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
     static bool attr_set[kMaxDevices] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= kMaxDevices || !attr_set[dev]) {
-        cudaError_t err = cudaFuncSetAttribute(k_product_run<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaError_t err =
+            cudaFuncSetAttribute(k_product_run<E, BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         if (err != cudaSuccess) return err;
         if (dev < kMaxDevices) attr_set[dev] = true;
     }
@@ -599,25 +608,19 @@ cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_product_run<E>, s, a);
+    return cudaLaunchKernelEx(&cfg, k_product_run<E, BP>, s, a);
 }
 
 }  // namespace
 
-cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st) {
+cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st, bool bpre) {
+#define RUN_E(EE) \
+    case EE: return bpre ? launch_e<EE, true>(s, a, st) : launch_e<EE, false>(s, a, st);
     switch (s.nout) {
-        case 1: return launch_e<1>(s, a, st);
-        case 2: return launch_e<2>(s, a, st);
-        case 3: return launch_e<3>(s, a, st);
-        case 4: return launch_e<4>(s, a, st);
-        case 5: return launch_e<5>(s, a, st);
-        case 6: return launch_e<6>(s, a, st);
-        case 7: return launch_e<7>(s, a, st);
-        case 8: return launch_e<8>(s, a, st);
-        case 9: return launch_e<9>(s, a, st);
-        case 10: return launch_e<10>(s, a, st);
+        RUN_E(1) RUN_E(2) RUN_E(3) RUN_E(4) RUN_E(5) RUN_E(6) RUN_E(7) RUN_E(8) RUN_E(9) RUN_E(10)
         default: return cudaErrorInvalidValue;
     }
+#undef RUN_E
 }
 
 }  // namespace gf2e
