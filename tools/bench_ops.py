@@ -107,7 +107,7 @@ def ple_lines(a, ctx):
         S.planes.copy_(S0.planes)
         g.ple_sliced(S)
 
-    ms = timed(run_ple, reps=2, warm=1)
+    ms = timed(run_ple, reps=5, warm=2)
     K = g.count_products(e)
     print(json.dumps({"op": "ple (sliced, in place)", "e": e, "m": n, "n": n, "ms": round(ms, 2),
                       "eff_Tbit-op/s": round(K * 2 * n ** 3 / 3 / (ms * 1e-3) / 1e12, 1),
@@ -119,7 +119,7 @@ def ple_lines(a, ctx):
         S.planes.copy_(S0.planes)
         g.echelonize_sliced(S, True)
 
-    ms = timed(run_ech, reps=2, warm=1)
+    ms = timed(run_ech, reps=5, warm=2)
     print(json.dumps({"op": "echelonize full (sliced)", "e": e, "m": n, "n": n, "ms": round(ms, 2)}), flush=True)
     nc = 1024
     arr = g.PackedMatrix.random(ctx, nc, nc, 11).to_array()
