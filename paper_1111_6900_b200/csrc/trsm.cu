@@ -38,13 +38,17 @@ __device__ __forceinline__ uint32_t gf_mul_slow(uint32_t a, uint32_t b, int e, u
 //     entries, FieldTab.mulmask: plane b of c*v = XOR of the planes in mulmask[c][b]); each
 //     row then adds two looked-up words per plane instead of an e x e plane product.
 // Two barriers per step: X_i published -> table built -> table consumed (and X_i+1 final).
+#ifndef GF2E_TRI_BS
+#define GF2E_TRI_BS 2
+#endif
 template <int E, int TB>
 struct TriShape {
     static constexpr int NW = TB / 64;            // plane words per block row
-    static constexpr int BS = TB == 128 ? 2 : 1;  // plane groups per row
+    static constexpr int BS = TB == 128 ? GF2E_TRI_BS : 1;  // plane groups per row
     static constexpr int TPR = NW * BS;           // threads per row
     static constexpr int THREADS = TB * TPR;
     static constexpr int PB = (E + BS - 1) / BS;  // planes per thread
+    static_assert(BS == 1 || BS == 2, "the final row scaling exchanges plane halves between two lanes");
     static constexpr int H1 = E <= 4 ? E : E / 2, H2 = E <= 4 ? 0 : E - E / 2;
     static constexpr int Q = (1 << H1) + (H2 ? (1 << H2) : 0);  // table entries
     static constexpr int TW = Q * E * NW;                        // table words
