@@ -263,6 +263,221 @@ __global__ void k_scalar_mul(int e, uint32_t f, uint32_t c, int w, const uint64_
     }
 }
 
+// Blocked inverse of a 128-row diagonal block (the PLE corners and TRSM at e = 9, 10 / small n):
+// instead of one 128-step substitution chain, four 32-row chains run at once (one warp each,
+// lane = row, the published row broadcast by shuffles, scalar * row by the multiplication
+// matrices) and the off-diagonal 32-row blocks follow from block products by diagonals,
+//   lower: X_IJ = X_II * sum_{K=J..I-1} U_IK X_KJ,  upper: X_IJ = X_II * sum_{K=I+1..J} U_IK X_KJ
+// (U = T D^-1 unit triangular as in k_tri_inverse; minus is plus in GF(2^e)).  A block product
+// C = A * B (32 x 32 elements times 32 bitsliced rows) tabulates the multiples of B's rows
+// (split by the scalar's low / high bits, PleSplit) and each row of C adds two words per plane
+// and row of B; A's entries come from the multipliers (U blocks) or, for X_II, one ballot over
+// the row's plane lanes.  X is kept as 32-bit words per (plane, row, 32-column block).
+template <int E>
+struct TriBlk {
+    static constexpr int TB = 128, BR = 32, NBK = TB / BR;
+    static constexpr int THREADS = 512;
+    static constexpr int TPR = E <= 8 ? 8 : 16;  // lanes per row in the products
+    using SP = PleSplit<E>;
+    static constexpr int QE = SP::QE;
+    using CT = typename std::conditional<(E <= 8), uint8_t, uint16_t>::type;
+    static constexpr size_t SMEM = (size_t)TB * TB * sizeof(CT)       // cU
+                                   + (size_t)E * TB * NBK * 4           // Xs
+                                   + (size_t)E * BR * 4                 // Ts
+                                   + (size_t)BR * QE * 4;               // tables of one product
+};
+
+template <int E>
+__global__ void __launch_bounds__(512) k_tri_inverse_blk(const FieldTab *__restrict__ ftab,
+                                                         const uint64_t *__restrict__ T, int64_t ldt, int64_t pt,
+                                                         int64_t m, int upper, int unit, uint64_t *__restrict__ Tinv,
+                                                         int *__restrict__ bad_row) {
+    using B = TriBlk<E>;
+    using SP = typename B::SP;
+    using CT = typename B::CT;
+    constexpr int TB = B::TB, BR = B::BR, NBK = B::NBK, TPR = B::TPR, QE = B::QE, H1 = SP::H1;
+    constexpr uint32_t EMASK = (1u << E) - 1;
+    extern __shared__ __align__(16) uint8_t bsm[];
+    CT *cU = reinterpret_cast<CT *>(bsm);                                           // [i][k]: U_ki
+    uint32_t *Xs = reinterpret_cast<uint32_t *>(bsm + (size_t)TB * TB * sizeof(CT));  // [E][TB][NBK]
+    uint32_t *Ts = Xs + E * TB * NBK;                                                 // [E][BR]
+    uint32_t *tab = Ts + E * BR;                                                      // [BR][Q][E]
+    __shared__ uint16_t sinv[1 << E], smk[(1 << E) * E], sex[1 << E], slg[1 << E], sdlog[TB], sdk[TB];
+    constexpr int ORD = (1 << E) - 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_trigger();
+    for (int i = tid; i < (1 << E); i += B::THREADS) {
+        sinv[i] = ftab->inv[i];
+        sex[i] = ftab->ex[i < ORD ? i : 0];
+        slg[i] = ftab->lg[i];
+#pragma unroll
+        for (int b = 0; b < E; ++b) smk[i * E + b] = ftab->mulmask[i][b];
+    }
+    for (int i = tid; i < E * TB * NBK; i += B::THREADS) Xs[i] = 0;
+    pdl_wait();  // T comes from the chain (the field tables above are constant)
+    const int64_t r0 = (int64_t)blockIdx.x * TB;
+    const int rows = (int)((m - r0) < TB ? (m - r0) : TB);
+    // multipliers: thread (row k, 32-column part c4): its row's plane words, entries by bit
+    const int k = tid >> 2, c4 = tid & 3;
+    uint64_t t[E];
+#pragma unroll
+    for (int b = 0; b < E; ++b) t[b] = 0;
+    if (k < rows && c4 * BR < rows) {
+        const uint64_t *src = T + (r0 + k) * ldt + (r0 >> 6) + (c4 >> 1);
+#pragma unroll
+        for (int b = 0; b < E; ++b) t[b] = src[b * pt];
+    }
+    auto entry = [&](int i) {  // T[k][i], i in this thread's 32 columns
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = 0; b < E; ++b) v |= (uint32_t)((t[b] >> (i & 63)) & 1ULL) << b;
+        return v;
+    };
+    __syncthreads();  // field tables, Xs zeroed
+    if (c4 == (k >> 5)) {
+        const uint32_t dk = k < rows ? entry(k) : 1u;
+        if (!unit && k < rows && dk == 0) atomicMin(bad_row, (int)(r0 + k));
+        sdlog[k] = (unit || dk == 0) ? 0 : slg[dk];
+        sdk[k] = (uint16_t)dk;
+    }
+    __syncthreads();  // sdlog
+    for (int cc = 0; cc < BR; ++cc) {
+        const int i = c4 * BR + cc;
+        uint32_t c = 0;
+        if (k < rows && i < rows && (upper ? (k < i) : (k > i))) {
+            c = entry(i);
+            if (c && !unit) {  // U_ki = T_ki / T_ii
+                int l = (int)slg[c] - (int)sdlog[i];
+                c = sex[l < 0 ? l + ORD : l];
+            }
+        }
+        cU[i * TB + k] = (CT)c;
+    }
+    __syncthreads();  // cU
+    const int nb = (rows + BR - 1) / BR;  // 32-row blocks in use
+    // ---- phase 1: the diagonal blocks, one warp each ----
+    if (warp < nb) {
+        const int I = warp, kk = I * BR + lane;
+        uint32_t x[E];
+#pragma unroll
+        for (int b = 0; b < E; ++b) x[b] = 0;
+        x[0] = 1u << lane;
+        for (int s = 0; s < BR; ++s) {
+            const int il = upper ? BR - 1 - s : s, i = I * BR + il;
+            uint32_t xi[E];
+#pragma unroll
+            for (int p = 0; p < E; ++p) xi[p] = __shfl_sync(0xffffffffu, x[p], il);
+            const uint32_t c = cU[i * TB + kk];  // zero unless row kk is below / above row i
+            if (c) {
+#pragma unroll
+                for (int b = 0; b < E; ++b) {
+                    const uint32_t mk = smk[c * E + b];
+                    uint32_t acc = 0;
+#pragma unroll
+                    for (int p = 0; p < E; ++p) acc ^= xi[p] & (0u - ((mk >> p) & 1u));
+                    x[b] ^= acc;
+                }
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < E; ++b) Xs[(b * TB + kk) * NBK + I] = x[b];
+    }
+    __syncthreads();
+    // ---- phase 2: block products by diagonals ----
+    // C[r] (+)= sum_q A(r, q) * Brow(q): tables of the 32 rows of B, then lane (r, b) adds two
+    // table words per q.  amode 0: A = U block (I, K) from the multipliers; 1: A = X_II.
+    const int pr = tid / TPR, pb = tid % TPR, gl = lane - (lane % TPR);
+    // B row q, plane p: bsrc[p * bps + q * brs]; C row r, plane p: dst[p * dps + r * drs]
+    auto product = [&](int amode, int I, int K, const uint32_t *bsrc, int bps, int brs, uint32_t *dst, int dps,
+                       int drs, bool accumulate) {
+        // tables: task (row q of B, half h, plane q2)
+        constexpr int NH = SP::H2 ? 2 : 1;
+        for (int tsk = tid; tsk < BR * NH * E; tsk += B::THREADS) {
+            const int q = tsk / (NH * E), rem = tsk - q * (NH * E), h = rem / E, q2 = rem - h * E;
+            const int s0 = h ? SP::H1 : 0, hb = h ? SP::H2 : SP::H1;
+            uint32_t br[E];
+#pragma unroll
+            for (int p = 0; p < E; ++p) br[p] = bsrc[p * bps + q * brs];
+            const uint32_t m1 = ftab->mulmask2[1][q2];
+            uint32_t basis[SP::H1 > SP::H2 ? SP::H1 : SP::H2];
+#pragma unroll
+            for (int u = 0; u < (SP::H1 > SP::H2 ? SP::H1 : SP::H2); ++u) {
+                const uint32_t mk = (m1 >> (s0 + u)) & EMASK;
+                uint32_t a = 0;
+#pragma unroll
+                for (int p = 0; p < E; ++p) a ^= br[p] & (0u - ((mk >> p) & 1u));
+                basis[u] = a;
+            }
+            uint32_t *d = tab + q * QE + (h ? (1 << SP::H1) : 0) * E + q2;
+            d[0] = 0;
+#pragma unroll
+            for (int u = 0; u < (SP::H1 > SP::H2 ? SP::H1 : SP::H2); ++u) {
+                if (u >= hb) break;
+                for (int t2 = 0; t2 < (1 << u); ++t2) d[((1 << u) + t2) * E] = d[t2 * E] ^ basis[u];
+            }
+        }
+        __syncthreads();
+        if (pr < BR) {  // every lane of the row's group takes part in the ballots
+            const int r = pr, bb = pb < E ? pb : 0;
+            const uint32_t xw = amode ? Xs[(bb * TB + I * BR + r) * NBK + I] : 0;
+            uint32_t acc = 0;
+            for (int q = 0; q < BR; ++q) {
+                uint32_t x;
+                if (amode) {
+                    const unsigned bal = __ballot_sync(0xffffffffu, pb < E && ((xw >> q) & 1u));
+                    x = (bal >> gl) & EMASK;
+                } else {
+                    x = cU[(K * BR + q) * TB + I * BR + r];
+                }
+                const uint32_t *tq = tab + q * QE + bb;
+                if constexpr (SP::H2 > 0)
+                    acc ^= tq[(x & ((1u << H1) - 1)) * E] ^ tq[((1u << H1) + (x >> H1)) * E];
+                else
+                    acc ^= tq[x * E];
+            }
+            if (pb < E) {
+                uint32_t *o = dst + pb * dps + r * drs;
+                *o = accumulate ? (*o ^ acc) : acc;
+            }
+        }
+        __syncthreads();
+    };
+    for (int d = 1; d < nb; ++d) {
+        for (int J0 = 0; J0 + d < nb; ++J0) {
+            const int I = upper ? J0 : J0 + d, J = upper ? J0 + d : J0;
+            // Ts = sum_K U_IK X_KJ, then X_IJ = X_II Ts
+            const int K0 = upper ? I + 1 : J, K1 = upper ? J : I - 1;
+            for (int K = K0; K <= K1; ++K)
+                product(0, I, K, Xs + (K * BR) * NBK + J, TB * NBK, NBK, Ts, BR, 1, K != K0);
+            product(1, I, I, Ts, BR, 1, Xs + (I * BR) * NBK + J, TB * NBK, NBK, false);
+        }
+    }
+    // ---- row scaling (T^-1 = D^-1 U^-1) and output: plane b, row k, two 64-bit words ----
+    uint64_t *out = Tinv + (int64_t)blockIdx.x * E * TB * 2;
+    for (int idx = tid; idx < E * TB; idx += B::THREADS) {
+        const int b = idx / TB, kr = idx - b * TB;
+        uint32_t v[NBK];
+        if (unit) {
+#pragma unroll
+            for (int cb = 0; cb < NBK; ++cb) v[cb] = Xs[(b * TB + kr) * NBK + cb];
+        } else {
+            uint32_t c = sinv[sdk[kr]];
+            if (c == 0) c = 1;  // singular block: reported above, result unused
+            const uint32_t mk = smk[c * E + b];
+#pragma unroll
+            for (int cb = 0; cb < NBK; ++cb) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int p = 0; p < E; ++p) acc ^= Xs[(p * TB + kr) * NBK + cb] & (0u - ((mk >> p) & 1u));
+                v[cb] = acc;
+            }
+        }
+        const bool live = kr < rows;
+        out[((int64_t)b * TB + kr) * 2] = live ? ((uint64_t)v[0] | ((uint64_t)v[1] << 32)) : 0;
+        out[((int64_t)b * TB + kr) * 2 + 1] = live ? ((uint64_t)v[2] | ((uint64_t)v[3] << 32)) : 0;
+    }
+}
+
 inline int grid_for(int64_t total, int threads) {
     int64_t g = (total + threads - 1) / threads;
     if (g > 148 * 32) g = 148 * 32;
@@ -271,9 +486,26 @@ inline int grid_for(int64_t total, int threads) {
 
 }  // namespace
 
+#ifndef GF2E_TRI_BLK
+#define GF2E_TRI_BLK 1
+#endif
 template <int E, int TB>
 cudaError_t launch_tri_e(const FieldTab *ftab, const uint64_t *T, int64_t ldt, int64_t pt, int64_t m, bool upper,
                          bool unit, uint64_t *Tinv, int *bad_row, int64_t nblk, cudaStream_t st) {
+    if constexpr (TB == 128 && GF2E_TRI_BLK) {  // the blocked form (32-row chains + block products)
+        using BK = TriBlk<E>;
+        static bool attr_blk[kMaxDevices] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= kMaxDevices || !attr_blk[dev]) {
+            cudaError_t err = cudaFuncSetAttribute(k_tri_inverse_blk<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)BK::SMEM);
+            if (err != cudaSuccess) return err;
+            if (dev < kMaxDevices) attr_blk[dev] = true;
+        }
+        return launch_pdl(k_tri_inverse_blk<E>, dim3((unsigned)nblk), dim3(BK::THREADS), BK::SMEM, st, ftab, T, ldt, pt,
+                          m, upper ? 1 : 0, unit ? 1 : 0, Tinv, bad_row);
+    }
     using S = TriShape<E, TB>;
     static bool attr_set[kMaxDevices] = {};
     int dev = 0;
