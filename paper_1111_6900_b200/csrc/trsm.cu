@@ -273,9 +273,9 @@ __global__ void k_scalar_mul(int e, uint32_t f, uint32_t c, int w, const uint64_
 // (split by the scalar's low / high bits, PleSplit) and each row of C adds two words per plane
 // and row of B; A's entries come from the multipliers (U blocks) or, for X_II, one ballot over
 // the row's plane lanes.  X is kept as 32-bit words per (plane, row, 32-column block).
-template <int E>
+template <int E, int TB_>
 struct TriBlk {
-    static constexpr int TB = 128, BR = 32, NBK = TB / BR;
+    static constexpr int TB = TB_, BR = 32, NBK = TB / BR, NW = TB / 64;
     static constexpr int THREADS = 512;
     static constexpr int TPR = E <= 8 ? 8 : 16;  // lanes per row in the products
     using SP = PleSplit<E>;
@@ -287,15 +287,15 @@ struct TriBlk {
                                    + (size_t)BR * QE * 4;               // tables of one product
 };
 
-template <int E>
+template <int E, int TB_>
 __global__ void __launch_bounds__(512) k_tri_inverse_blk(const FieldTab *__restrict__ ftab,
                                                          const uint64_t *__restrict__ T, int64_t ldt, int64_t pt,
                                                          int64_t m, int upper, int unit, uint64_t *__restrict__ Tinv,
                                                          int *__restrict__ bad_row) {
-    using B = TriBlk<E>;
+    using B = TriBlk<E, TB_>;
     using SP = typename B::SP;
     using CT = typename B::CT;
-    constexpr int TB = B::TB, BR = B::BR, NBK = B::NBK, TPR = B::TPR, QE = B::QE, H1 = SP::H1;
+    constexpr int TB = B::TB, BR = B::BR, NBK = B::NBK, NW = B::NW, TPR = B::TPR, QE = B::QE, H1 = SP::H1;
     constexpr uint32_t EMASK = (1u << E) - 1;
     extern __shared__ __align__(16) uint8_t bsm[];
     CT *cU = reinterpret_cast<CT *>(bsm);                                           // [i][k]: U_ki
@@ -317,41 +317,54 @@ __global__ void __launch_bounds__(512) k_tri_inverse_blk(const FieldTab *__restr
     pdl_wait();  // T comes from the chain (the field tables above are constant)
     const int64_t r0 = (int64_t)blockIdx.x * TB;
     const int rows = (int)((m - r0) < TB ? (m - r0) : TB);
-    // multipliers: thread (row k, 32-column part c4): its row's plane words, entries by bit
-    const int k = tid >> 2, c4 = tid & 3;
-    uint64_t t[E];
-#pragma unroll
-    for (int b = 0; b < E; ++b) t[b] = 0;
-    if (k < rows && c4 * BR < rows) {
-        const uint64_t *src = T + (r0 + k) * ldt + (r0 >> 6) + (c4 >> 1);
-#pragma unroll
-        for (int b = 0; b < E; ++b) t[b] = src[b * pt];
-    }
-    auto entry = [&](int i) {  // T[k][i], i in this thread's 32 columns
-        uint32_t v = 0;
-#pragma unroll
-        for (int b = 0; b < E; ++b) v |= (uint32_t)((t[b] >> (i & 63)) & 1ULL) << b;
-        return v;
-    };
     __syncthreads();  // field tables, Xs zeroed
-    if (c4 == (k >> 5)) {
-        const uint32_t dk = k < rows ? entry(k) : 1u;
-        if (!unit && k < rows && dk == 0) atomicMin(bad_row, (int)(r0 + k));
-        sdlog[k] = (unit || dk == 0) ? 0 : slg[dk];
-        sdk[k] = (uint16_t)dk;
+    // multipliers: task (row k, 32-column part c4): its row's plane words, entries by bit
+    for (int task = tid; task < TB * NBK; task += B::THREADS) {
+        const int k = task / NBK, c4 = task % NBK;
+        uint64_t t[E];
+#pragma unroll
+        for (int b = 0; b < E; ++b) t[b] = 0;
+        if (k < rows && c4 * BR < rows) {
+            const uint64_t *src = T + (r0 + k) * ldt + (r0 >> 6) + (c4 >> 1);
+#pragma unroll
+            for (int b = 0; b < E; ++b) t[b] = src[b * pt];
+        }
+        if (c4 == (k >> 5)) {
+            uint32_t dk = 1;
+            if (k < rows) {
+                dk = 0;
+#pragma unroll
+                for (int b = 0; b < E; ++b) dk |= (uint32_t)((t[b] >> (k & 63)) & 1ULL) << b;
+            }
+            if (!unit && k < rows && dk == 0) atomicMin(bad_row, (int)(r0 + k));
+            sdlog[k] = (unit || dk == 0) ? 0 : slg[dk];
+            sdk[k] = (uint16_t)dk;
+        }
     }
     __syncthreads();  // sdlog
-    for (int cc = 0; cc < BR; ++cc) {
-        const int i = c4 * BR + cc;
-        uint32_t c = 0;
-        if (k < rows && i < rows && (upper ? (k < i) : (k > i))) {
-            c = entry(i);
-            if (c && !unit) {  // U_ki = T_ki / T_ii
-                int l = (int)slg[c] - (int)sdlog[i];
-                c = sex[l < 0 ? l + ORD : l];
-            }
+    for (int task = tid; task < TB * NBK; task += B::THREADS) {
+        const int k = task / NBK, c4 = task % NBK;
+        uint64_t t[E];
+#pragma unroll
+        for (int b = 0; b < E; ++b) t[b] = 0;
+        if (k < rows && c4 * BR < rows) {
+            const uint64_t *src = T + (r0 + k) * ldt + (r0 >> 6) + (c4 >> 1);
+#pragma unroll
+            for (int b = 0; b < E; ++b) t[b] = src[b * pt];
         }
-        cU[i * TB + k] = (CT)c;
+        for (int cc = 0; cc < BR; ++cc) {
+            const int i = c4 * BR + cc;
+            uint32_t c = 0;
+            if (k < rows && i < rows && (upper ? (k < i) : (k > i))) {
+#pragma unroll
+                for (int b = 0; b < E; ++b) c |= (uint32_t)((t[b] >> (i & 63)) & 1ULL) << b;
+                if (c && !unit) {  // U_ki = T_ki / T_ii
+                    int l = (int)slg[c] - (int)sdlog[i];
+                    c = sex[l < 0 ? l + ORD : l];
+                }
+            }
+            cU[i * TB + k] = (CT)c;
+        }
     }
     __syncthreads();  // cU
     const int nb = (rows + BR - 1) / BR;  // 32-row blocks in use
@@ -453,7 +466,7 @@ __global__ void __launch_bounds__(512) k_tri_inverse_blk(const FieldTab *__restr
         }
     }
     // ---- row scaling (T^-1 = D^-1 U^-1) and output: plane b, row k, two 64-bit words ----
-    uint64_t *out = Tinv + (int64_t)blockIdx.x * E * TB * 2;
+    uint64_t *out = Tinv + (int64_t)blockIdx.x * E * TB * NW;
     for (int idx = tid; idx < E * TB; idx += B::THREADS) {
         const int b = idx / TB, kr = idx - b * TB;
         uint32_t v[NBK];
@@ -473,8 +486,9 @@ __global__ void __launch_bounds__(512) k_tri_inverse_blk(const FieldTab *__restr
             }
         }
         const bool live = kr < rows;
-        out[((int64_t)b * TB + kr) * 2] = live ? ((uint64_t)v[0] | ((uint64_t)v[1] << 32)) : 0;
-        out[((int64_t)b * TB + kr) * 2 + 1] = live ? ((uint64_t)v[2] | ((uint64_t)v[3] << 32)) : 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+            out[((int64_t)b * TB + kr) * NW + w] = live ? ((uint64_t)v[2 * w] | ((uint64_t)v[2 * w + 1] << 32)) : 0;
     }
 }
 
@@ -492,19 +506,19 @@ inline int grid_for(int64_t total, int threads) {
 template <int E, int TB>
 cudaError_t launch_tri_e(const FieldTab *ftab, const uint64_t *T, int64_t ldt, int64_t pt, int64_t m, bool upper,
                          bool unit, uint64_t *Tinv, int *bad_row, int64_t nblk, cudaStream_t st) {
-    if constexpr (TB == 128 && GF2E_TRI_BLK) {  // the blocked form (32-row chains + block products)
-        using BK = TriBlk<E>;
+    if constexpr (GF2E_TRI_BLK) {  // the blocked form (32-row chains + block products)
+        using BK = TriBlk<E, TB>;
         static bool attr_blk[kMaxDevices] = {};
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev >= kMaxDevices || !attr_blk[dev]) {
-            cudaError_t err = cudaFuncSetAttribute(k_tri_inverse_blk<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)BK::SMEM);
+            cudaError_t err = cudaFuncSetAttribute(k_tri_inverse_blk<E, TB>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BK::SMEM);
             if (err != cudaSuccess) return err;
             if (dev < kMaxDevices) attr_blk[dev] = true;
         }
-        return launch_pdl(k_tri_inverse_blk<E>, dim3((unsigned)nblk), dim3(BK::THREADS), BK::SMEM, st, ftab, T, ldt, pt,
-                          m, upper ? 1 : 0, unit ? 1 : 0, Tinv, bad_row);
+        return launch_pdl(k_tri_inverse_blk<E, TB>, dim3((unsigned)nblk), dim3(BK::THREADS), BK::SMEM, st, ftab, T, ldt,
+                          pt, m, upper ? 1 : 0, unit ? 1 : 0, Tinv, bad_row);
     }
     using S = TriShape<E, TB>;
     static bool attr_set[kMaxDevices] = {};
