@@ -77,10 +77,13 @@ __device__ __forceinline__ void stepE(uint64_t *v, uint32_t x, const uint64_t *b
 
 // Window threads: TPR lanes of one warp per window row, lane b holding plane b (an entry is
 // one ballot); 1024 threads, RP rows per pass.
+// lanes per window row (measured per e, PLE 8192^2: e = 4 20.9 ms at 4 lanes vs 23.5 at 8;
+// e = 8 28.7 ms at 8 vs 30.0 at 4 and 33.0 at 2; e = 10 46.7 at 16 vs 47.2 at 8)
 template <int E>
 struct FindShape {
     static constexpr int PT = ple_win<E>();      // window rows
-    static constexpr int TPR = E <= 8 ? 8 : 16;
+    static constexpr int TPR = E <= 4 ? 4 : E <= 8 ? 8 : 16;
+    static constexpr int PPL = (E + TPR - 1) / TPR;  // planes per lane: sub, sub + TPR, ...
     static constexpr int NT = PT * TPR < 1024 ? PT * TPR : 1024;
     static constexpr int RP = NT / TPR;           // window rows per pass
     static constexpr int PASSES = (PT + RP - 1) / RP;
@@ -94,12 +97,13 @@ __device__ __forceinline__ int first_row(unsigned bal, int row_of_lane0) {
 }
 
 template <int E>
-__global__ void __launch_bounds__(1024) k_ple_find(const FieldTab *__restrict__ tab, uint64_t *__restrict__ S,
+__global__ void __launch_bounds__(FindShape<E>::NT) k_ple_find(const FieldTab *__restrict__ tab, uint64_t *__restrict__ S,
                                                    int64_t ld, int64_t ps, int64_t m, int nb,
                                                    PanelOut *__restrict__ out) {
     using F = FindShape<E>;
     using SP = PleSplit<E>;
-    constexpr int NT = F::NT, TPR = F::TPR, PT = F::PT;
+    constexpr int NT = F::NT, TPR = F::TPR, PT = F::PT, PPL = F::PPL;
+    constexpr uint32_t GMASK = TPR >= 32 ? 0xffffffffu : ((1u << TPR) - 1);
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t *win = reinterpret_cast<uint64_t *>(smem);  // [PT][E]
     uint64_t *ptab = win + PT * E;                       // [Q][E]: multiples of the current T_r
@@ -137,12 +141,17 @@ __global__ void __launch_bounds__(1024) k_ple_find(const FieldTab *__restrict__ 
 #pragma unroll
     for (int pass = 0; pass < F::PASSES; ++pass) {
         const int s = pass * F::RP + rl;
-        uint64_t x = 0;
-        if (s < W && b < E) {
-            x = S[b * ps + s * ld] & cmask;
-            win[s * E + b] = x;
+        uint64_t any = 0;
+#pragma unroll
+        for (int sl = 0; sl < PPL; ++sl) {
+            const int bb = b + TPR * sl;
+            if (s < W && bb < E) {
+                const uint64_t x = S[bb * ps + s * ld] & cmask;
+                win[s * E + bb] = x;
+                any |= x;
+            }
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, x & 1ULL);
+        const unsigned bal = __ballot_sync(0xffffffffu, any & 1ULL);
         if (lane == 0 && bal) atomicMin(&s_mn[0], first_row<TPR>(bal, pass * F::RP + (tid - lane) / TPR));
     }
     __syncthreads();
@@ -229,8 +238,11 @@ __global__ void __launch_bounds__(1024) k_ple_find(const FieldTab *__restrict__ 
 #pragma unroll
                 for (int pass = 0; pass < F::PASSES; ++pass) {
                     const int s = pass * F::RP + rl;
-                    const bool act = s >= r && s < W && b < E;
-                    const unsigned bal = __ballot_sync(0xffffffffu, act && ((win[s * E + b] >> (j + 1)) & 1ULL));
+                    uint64_t any = 0;
+#pragma unroll
+                    for (int sl = 0; sl < PPL; ++sl)
+                        if (s >= r && s < W && b + TPR * sl < E) any |= win[s * E + b + TPR * sl];
+                    const unsigned bal = __ballot_sync(0xffffffffu, (any >> (j + 1)) & 1ULL);
                     if (lane == 0 && bal)
                         atomicMin(&s_mn[cb ^ 1], first_row<TPR>(bal, pass * F::RP + (tid - lane) / TPR));
                 }
@@ -300,22 +312,36 @@ __global__ void __launch_bounds__(1024) k_ple_find(const FieldTab *__restrict__ 
 #pragma unroll
         for (int pass = 0; pass < F::PASSES; ++pass) {
             const int s = pass * F::RP + rl;
-            const bool act = s > r && s < W && b < E;
-            uint64_t v = 0;
-            if (act) v = (s == ipos) ? oldr[b] : win[s * E + b];  // the old row r moved to ipos
-            const unsigned bal = __ballot_sync(0xffffffffu, (v >> j) & 1ULL);
-            const uint32_t x = (bal >> gl) & F::EMASK;
-            if (act && (x || s == ipos)) {
-                if (x) {
-                    if constexpr (SP::H2 > 0)
-                        v ^= ptab[(x & ((1u << SP::H1) - 1)) * E + b] ^ ptab[((1u << SP::H1) + (x >> SP::H1)) * E + b];
-                    else
-                        v ^= ptab[x * E + b];
+            const bool act = s > r && s < W;
+            uint64_t v[PPL];
+            uint32_t x = 0;
+#pragma unroll
+            for (int sl = 0; sl < PPL; ++sl) {  // lane b holds planes b, b + TPR, ...
+                const int bb = b + TPR * sl;
+                v[sl] = 0;
+                if (act && bb < E) v[sl] = (s == ipos) ? oldr[bb] : win[s * E + bb];  // old row r moved to ipos
+                const unsigned bal = __ballot_sync(0xffffffffu, (v[sl] >> j) & 1ULL);
+                x |= ((bal >> gl) & GMASK) << (TPR * sl);
+            }
+            x &= F::EMASK;
+            uint64_t any = 0;
+#pragma unroll
+            for (int sl = 0; sl < PPL; ++sl) {
+                const int bb = b + TPR * sl;
+                if (act && bb < E && (x || s == ipos)) {
+                    if (x) {
+                        if constexpr (SP::H2 > 0)
+                            v[sl] ^= ptab[(x & ((1u << SP::H1) - 1)) * E + bb] ^
+                                     ptab[((1u << SP::H1) + (x >> SP::H1)) * E + bb];
+                        else
+                            v[sl] ^= ptab[x * E + bb];
+                    }
+                    win[s * E + bb] = v[sl];
                 }
-                win[s * E + b] = v;
+                any |= v[sl];
             }
             if (next) {
-                const unsigned bal2 = __ballot_sync(0xffffffffu, act && ((v >> (j + 1)) & 1ULL));
+                const unsigned bal2 = __ballot_sync(0xffffffffu, act && ((any >> (j + 1)) & 1ULL));
                 if (lane == 0 && bal2)
                     atomicMin(&s_mn[cb ^ 1], first_row<TPR>(bal2, pass * F::RP + (tid - lane) / TPR));
             }
@@ -327,14 +353,18 @@ __global__ void __launch_bounds__(1024) k_ple_find(const FieldTab *__restrict__ 
 #pragma unroll
     for (int pass = 0; pass < F::PASSES; ++pass) {
         const int s = pass * F::RP + rl;
-        if (s < W && b < E) {
-            uint64_t v = win[s * E + b];
-            for (int t = 0; t < r && t <= s; ++t) {
-                const int q = (int)s_Q[t];
-                if (q != t) v = swap_bits(v, t, q);
+#pragma unroll
+        for (int sl = 0; sl < PPL; ++sl) {
+            const int bb = b + TPR * sl;
+            if (s < W && bb < E) {
+                uint64_t v = win[s * E + bb];
+                for (int t = 0; t < r && t <= s; ++t) {
+                    const int q = (int)s_Q[t];
+                    if (q != t) v = swap_bits(v, t, q);
+                }
+                uint64_t *d = S + bb * ps + s * ld;
+                *d = (*d & ~cmask) | v;
             }
-            uint64_t *d = S + b * ps + s * ld;
-            *d = (*d & ~cmask) | v;
         }
     }
     // outputs for phase 2 and the host
