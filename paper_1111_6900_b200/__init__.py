@@ -7,6 +7,7 @@ same names and semantics, computed by hand-written sm_100a CUDA in libgf2e_b200.
 """
 
 from . import _lib
+from ._device import release_workspace
 from .gf2e import DEFAULT_POLYS, FieldCtx, field_new, is_irreducible, is_primitive
 from .mat_gf2 import BitMatrix, RowOpCounters, addmul as gf2_addmul, mul, mzd_addmul, mzd_mul, words_for
 from .mat_packed import PackedMatrix, pack_width
@@ -50,6 +51,7 @@ from .poly_mul import (
 )
 
 __all__ = [
+    "release_workspace",
     "DEFAULT_POLYS", "FieldCtx", "field_new", "is_irreducible", "is_primitive",
     "BitMatrix", "RowOpCounters", "mul", "gf2_addmul", "mzd_mul", "mzd_addmul", "words_for",
     "PackedMatrix", "pack_width",

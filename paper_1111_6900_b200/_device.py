@@ -6,6 +6,7 @@ libgf2e_b200.so.  There is no CPU path: without an sm_100 GPU every call raises.
 
 from __future__ import annotations
 
+import os
 import threading
 
 import numpy as np
@@ -43,14 +44,22 @@ def to_host_words(t: torch.Tensor) -> np.ndarray:
     return t.detach().contiguous().cpu().numpy().view(np.uint64)
 
 
+# scratch requests above this size are not kept between calls (GF2E_WORKSPACE_KEEP bytes)
+WORKSPACE_KEEP = int(os.environ.get("GF2E_WORKSPACE_KEEP", str(4 << 30)))
+
+
 class _Workspace(threading.local):
-    """Per-thread, per-(device, stream) scratch buffer that only grows."""
+    """Per-thread, per-(device, stream) scratch buffer, reused across calls up to
+    WORKSPACE_KEEP bytes; a larger request gets a one-call tensor (back to PyTorch's caching
+    allocator when the call returns), so one huge product does not pin its scratch."""
 
     def __init__(self):
         self.bufs: dict[tuple[int, int], torch.Tensor] = {}
 
     def get(self, nbytes: int) -> torch.Tensor:
         dev = require_cuda()
+        if nbytes > WORKSPACE_KEEP:
+            return torch.empty(nbytes, dtype=torch.uint8, device=dev)
         key = (dev.index, stream_handle())
         buf = self.bufs.get(key)
         if buf is None or buf.numel() < nbytes:
@@ -60,6 +69,18 @@ class _Workspace(threading.local):
 
     def clear(self) -> None:
         self.bufs.clear()
+
+
+def release_workspace() -> None:
+    """Drop the kept scratch buffers of this thread, return PyTorch's cached blocks to the
+    driver and trim the library's own pool (gf2e_trim_pool)."""
+    workspace.clear()
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        from . import _lib
+
+        _lib.load().gf2e_trim_pool(0)
 
 
 workspace = _Workspace()

@@ -557,3 +557,14 @@ def test_nj_small_products_oracle(g, e):
         poly_mul.nj_mul_packed(PA, PB, PC)
         ref2 = ref ^ oracle.slice_words(e, m, n, C0)
         assert np.array_equal(PC.to_numpy(), oracle.cling_words(e, m, n, ref2)), (m, k, n, "acc")
+
+
+def test_release_workspace(g):
+    # scratch buffers can be dropped between calls (and the library pool trimmed); products
+    # computed before and after are identical
+    ctx = g.field_new(8)
+    A = g.SlicedMatrix.random(ctx, 300, 500, 1)
+    B = g.SlicedMatrix.random(ctx, 500, 400, 2)
+    C1 = g.karatsuba_mul(A, B).to_numpy()
+    g.release_workspace()
+    assert np.array_equal(g.karatsuba_mul(A, B).to_numpy(), C1)
