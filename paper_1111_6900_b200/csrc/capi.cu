@@ -924,7 +924,9 @@ int run_update(const Sched &ks, int e, const FieldTab *tab, const uint64_t *A, i
                const uint64_t *B, int64_t ldb, int64_t pb, uint64_t *C, int64_t ldc, int64_t pc, int64_t m,
                int64_t k, int64_t n, uint32_t flags, void *ws, int64_t ws_bytes, cudaStream_t st,
                bool c_aliases_b = false) {
-    if (tab && m > 0 && n > 0 && k > 0 && k <= nj_sliced_max_k() && (!c_aliases_b || m <= nj_sliced_alias_rows(e))) {
+    // (grid limits of the Newton-John launch: 65535 row blocks of at least 64 rows)
+    if (tab && m > 0 && n > 0 && k > 0 && k <= nj_sliced_max_k() && m <= 65535LL * 64 &&
+        (!c_aliases_b || m <= nj_sliced_alias_rows(e))) {
         CK(launch_nj_sliced(e, tab, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, (flags & GF2E_ACCUMULATE) != 0,
                             c_aliases_b, st),
            "nj_sliced");
