@@ -959,6 +959,19 @@ int trsm_rec(TrsmCtx &c, int64_t i0, int64_t i1) {
         // the product kernel starts (stream order), so C may alias B here
         const uint64_t *Ib = c.inv + (i0 / tb) * c.e * tb * (tb / 64);
         uint64_t *Bb = c.B + i0 * c.ldb;
+        const int64_t nwn = words_for(c.n);
+        if (rows <= nj_sliced_max_k() && rows > 64 && c.pb % c.ldb == 0) {
+            // the Newton-John form with the rows split over CTAs: B_blk copied to the scratch
+            // first (one 3-D copy of all planes), so C no longer aliases the operand
+            cudaMemcpy3DParms cp = {};
+            cp.srcPtr = make_cudaPitchedPtr(Bb, (size_t)c.ldb * 8, (size_t)nwn * 8, (size_t)(c.pb / c.ldb));
+            cp.dstPtr = make_cudaPitchedPtr(c.tmp, (size_t)nwn * 8, (size_t)nwn * 8, (size_t)tb);
+            cp.extent = make_cudaExtent((size_t)nwn * 8, (size_t)rows, (size_t)c.e);
+            cp.kind = cudaMemcpyDeviceToDevice;
+            CKH(cudaMemcpy3DAsync(&cp, c.st), "cudaMemcpy3DAsync");
+            return run_update(c.ks, c.e, c.tab, Ib, tb / 64, tb * (tb / 64), c.tmp, nwn, tb * nwn, Bb, c.ldb, c.pb,
+                              rows, rows, c.n, 0, c.mulws, c.mulws_bytes, c.st, false);
+        }
         return run_update(c.ks, c.e, c.tab, Ib, tb / 64, tb * (tb / 64), Bb, c.ldb, c.pb, Bb, c.ldb, c.pb, rows, rows,
                           c.n, 0, c.mulws, c.mulws_bytes, c.st, true);
     }
