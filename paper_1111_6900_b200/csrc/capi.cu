@@ -925,7 +925,10 @@ int run_update(const Sched &ks, int e, const FieldTab *tab, const uint64_t *A, i
                int64_t k, int64_t n, uint32_t flags, void *ws, int64_t ws_bytes, cudaStream_t st,
                bool c_aliases_b = false) {
     // (grid limits of the Newton-John launch: 65535 row blocks of at least 64 rows)
-    if (tab && m > 0 && n > 0 && k > 0 && k <= nj_sliced_max_k() && m <= 65535LL * 64 &&
+    // (at e >= 9 the split tables of 64 entries make a wide 128-deep product cheaper on the
+    // tensor cores: TRSM 8192 \ 8192 x 16384 at e = 10 18.7 against 22.5 ms, measured)
+    const bool small_k = k <= 64 || (k <= nj_sliced_max_k() && (e <= 8 || n <= 2048));
+    if (tab && m > 0 && n > 0 && k > 0 && small_k && m <= 65535LL * 64 &&
         (!c_aliases_b || m <= nj_sliced_alias_rows(e))) {
         CK(launch_nj_sliced(e, tab, A, lda, pa, B, ldb, pb, C, ldc, pc, m, k, n, (flags & GF2E_ACCUMULATE) != 0,
                             c_aliases_b, st),
@@ -960,7 +963,7 @@ int trsm_rec(TrsmCtx &c, int64_t i0, int64_t i1) {
         const uint64_t *Ib = c.inv + (i0 / tb) * c.e * tb * (tb / 64);
         uint64_t *Bb = c.B + i0 * c.ldb;
         const int64_t nwn = words_for(c.n);
-        if (rows <= nj_sliced_max_k() && rows > 64 && c.pb % c.ldb == 0) {
+        if (rows <= nj_sliced_max_k() && rows > 64 && (c.e <= 8 || c.n <= 2048) && c.pb % c.ldb == 0) {
             // the Newton-John form with the rows split over CTAs: B_blk copied to the scratch
             // first (one 3-D copy of all planes), so C no longer aliases the operand
             cudaMemcpy3DParms cp = {};
