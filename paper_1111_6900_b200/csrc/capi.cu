@@ -759,6 +759,11 @@ int pair_count() {
 // 72 of 74 at n = 16384), so the products that run while B is still arriving use the whole
 // GPU.  The rest go in `chunk`-row chunks, the remainder merged into the first of them (at
 // 16384 rows: 2304, 3840, 5 x 2048 — 97-99.8% wave fill each, against 86% for 1792 rows).
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
 std::vector<int64_t> host_row_plan(int64_t m, int64_t n, int64_t k, int64_t chunk, int nbp, bool fixed, int64_t tw) {
     std::vector<int64_t> rb{0};
     int64_t first = chunk;
@@ -766,8 +771,9 @@ std::vector<int64_t> host_row_plan(int64_t m, int64_t n, int64_t k, int64_t chun
     // C0/C copies dominate and uniform chunks pipeline them best)
     fixed = fixed || k < 4096;
     if (!fixed && nbp > 1) {
+        static const int reserve = env_int("GF2E_E2E_RESERVE", 0);
         const int64_t part_tiles = ((n + tw - 1) / tw + nbp - 1) / nbp;
-        const int64_t rt0 = pair_count() / part_tiles;
+        const int64_t rt0 = (pair_count() - reserve) / part_tiles;
         if (rt0 >= 1) first = rt0 * 256;
     }
     if (first >= m) return {0, m};
@@ -1834,14 +1840,12 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     const int64_t tw = form_bn(form);  // column tile width: B parts and column splits align to it
     int64_t chunk = chunk_rows > 0 ? round_up(chunk_rows, 2 * kTcBM) : 2048;
     if (chunk > round_up(m, 2 * kTcBM)) chunk = round_up(m, 2 * kTcBM);
-    constexpr int kMaxBParts = 8;
-#ifndef GF2E_BPARTS
-#define GF2E_BPARTS 8
-#endif
+    constexpr int kMaxBParts = 16;
     // B arrives in column parts (multiples of 256 columns) so the first row chunk's products
     // start after the first part's upload instead of all of B's
-    const int nbp = (n >= 8192 && m > chunk) ? GF2E_BPARTS : 1;
-    static_assert(GF2E_BPARTS >= 1 && GF2E_BPARTS <= kMaxBParts, "B parts");
+    static const int bparts = std::min(std::max(env_int("GF2E_E2E_BPARTS", 8), 1), kMaxBParts);
+    static const bool a_first = env_int("GF2E_E2E_AFIRST", 0) != 0;
+    const int nbp = (n >= 8192 && m > chunk) ? bparts : 1;
     const std::vector<int64_t> rb = host_row_plan(m, n, k, chunk, nbp, chunk_rows > 0, tw);
     for (size_t i = 1; i < rb.size(); ++i)
         if (rb[i] - rb[i - 1] > chunk) chunk = rb[i] - rb[i - 1];  // slot size
@@ -1970,8 +1974,11 @@ int gf2e_mzed_mul_host(int e, uint32_t f, const uint64_t *A_h, int64_t lda, cons
     };
     // enqueue order (each event recorded before any wait on it): B part 0, chunk 0, the other
     // B parts; A's preparation one chunk ahead of the products
-    if (int rc = h2d_bpart(0)) return rc;
+    if (!a_first)
+        if (int rc = h2d_bpart(0)) return rc;
     if (int rc = h2d_chunk(0)) return rc;
+    if (a_first)
+        if (int rc = h2d_bpart(0)) return rc;
     for (int p = 1; p < nbp; ++p)
         if (int rc = h2d_bpart(p)) return rc;
     if (side) {
