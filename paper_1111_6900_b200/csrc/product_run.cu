@@ -30,6 +30,22 @@
 #include "kernels.h"
 #include "tc_common.cuh"
 
+// Per-degree variants (build knobs, chosen by measurement, profiles/r02/run_variants.txt):
+//  STW: a store warp writes each finished tile out (double-buffered staging in shared memory,
+//       C0 read by that warp) while the epilogue warps drain the next tile; for E >= the knob
+//  DIET: differenced output masks (no previous parity words kept), the parity word packed with
+//       IMAD.HI on the FMA pipe, plane selectors read from a shared table; for E >= the knob
+#ifndef GF2E_RUN_STW_MIN_E
+#define GF2E_RUN_STW_MIN_E 7
+#endif
+#ifndef GF2E_RUN_DIET_MIN_E
+#define GF2E_RUN_DIET_MIN_E 11
+#endif
+template <int E>
+struct RunVar {
+    static constexpr bool STW = E >= GF2E_RUN_STW_MIN_E, DIET = E >= GF2E_RUN_DIET_MIN_E;
+};
+
 namespace gf2e {
 namespace {
 using namespace tc;
@@ -41,8 +57,8 @@ constexpr int KW = 4;                 // 64-bit words per row per stage (256 k-b
 constexpr int S = 3;                  // operand stages (A: 3 x 32 TMEM columns)
 constexpr int D = 8;                  // raw bit-tile ring
 constexpr int NEXP = 4, NEPI = 8;  // epilogue: lane quarter x column half (96 columns, one TMEM round trip)
-constexpr int EPI_W0 = NEXP, MMA_WARP = NEXP + NEPI, LOAD_WARP = MMA_WARP + 1;
-constexpr int NTHREADS = (NEXP + NEPI + 2) * 32;
+constexpr int EPI_W0 = NEXP, MMA_WARP = NEXP + NEPI, LOAD_WARP = MMA_WARP + 1, STORE_WARP = LOAD_WARP + 1;
+constexpr int NTHREADS = (NEXP + NEPI + 3) * 32;  // + the store warp (idle unless RunVar<E>::STW)
 constexpr int B_BYTES = BNH * 128;                     // expanded B^T stage (12 KiB)
 // B^T operand stages: pre-expanded by k_combos_bt and bulk-copied ready for the MMA (kRunBPre),
 // or expanded here from bit tiles
@@ -68,8 +84,13 @@ constexpr int BARS_BYTES = 1024;
 // epilogue staging (per CTA and tile): the E x 128 x 192-bit output words and their C0
 // epilogue staging (per CTA and tile): the E x 128 x 192-bit output words and their C0
 constexpr int STAGE_OUT_BYTES = kMaxE * BM * 24, STAGE_OLD_BYTES = kMaxE * BM * 24;
-constexpr int SMEM_BYTES = S * B_BYTES + D * RunMem<false>::BITS_BYTES + BARS_BYTES + STAGE_OUT_BYTES +
-                           STAGE_OLD_BYTES + 1024;  // (the larger of the two bit rings)
+// per drain group: the all-ones / zero selector word of every output plane (SEL_EP words per
+// group, 16-byte aligned rows, read with LDS.128 instead of being formed from the mask)
+constexpr int SEL_EP = 12, SEL_BYTES = kMaxSeq * SEL_EP * 4;
+// with the store warp: two staging buffers for the output words and two for the prefetched C0
+constexpr int SMEM_BYTES = S * B_BYTES + D * RunMem<false>::BITS_BYTES + BARS_BYTES +
+                           STAGE_OUT_BYTES + STAGE_OLD_BYTES + SEL_BYTES +
+                           1024;  // (the larger bit ring)
 static_assert(B_BYTES % 1024 == 0, "swizzle atoms need 1024-byte aligned stages");
 static_assert(SMEM_BYTES <= 232448, "shared memory");
 
@@ -90,7 +111,7 @@ __device__ unsigned long long g_instr_run[1024][32];
 #endif
 
 struct __align__(8) Bars {
-    uint64_t full[S], empty[S], bfullB[S], tfull[2], tempty[2], bfull[D], bempty[D];
+    uint64_t full[S], empty[S], bfullB[S], tfull[2], tempty[2], bfull[D], bempty[D], sfull[2], sempty[2];
     uint32_t tmem_base;
     uint16_t gmask[kMaxSeq];  // output planes of each drain group
 };
@@ -126,6 +147,22 @@ __device__ __forceinline__ uint32_t parity_word_tree(const uint32_t (&v)[16]) {
     }
     return ((w[0] | w[1]) | (w[2] | w[3])) | ((w[4] | w[5]) | (w[6] | w[7]));
 }
+
+// the same word with the merge on the FMA pipe: PRMT gathers bytes 0 and 2 of each cell pair
+// without sign replication (a byte is parity << 7: the running sum is an integer in mantissa
+// bits 7.., bits 0-6 are zero), then IMAD.HI shifts word g right by 7 - g and adds (disjoint
+// bits, so the sum is the OR): 8 PRMT + 7 IMAD.HI instead of 8 PRMT + 8 LOP3 on the ALU pipe.
+// The multipliers come from a register (ptxas would turn a constant power of two into SHF).
+__device__ __forceinline__ uint32_t parity_word_mad(const uint32_t (&v)[16], uint32_t m25) {
+    uint32_t w[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) asm("prmt.b32 %0, %1, %2, 0x6420;" : "=r"(w[g]) : "r"(v[2 * g]), "r"(v[2 * g + 1]));
+    uint32_t o = w[7];
+#pragma unroll
+    for (int g = 0; g < 7; ++g) asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(o) : "r"(w[g]), "r"(m25 << g), "r"(o));
+    return o;
+}
+#define PARITY_WORD(v) (DIET ? parity_word_mad(v, m25) : parity_word_tree(v))
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -181,6 +218,7 @@ __device__ __forceinline__ void mma2_mxf4_ts(uint32_t d, uint32_t at, uint64_t b
 template <int E, bool BPRE>
 __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, const TcArgs a) {
     constexpr int BITS_B = RunMem<BPRE>::BITS_B, BITS_BYTES = RunMem<BPRE>::BITS_BYTES;
+    constexpr bool STW = RunVar<E>::STW, DIET = RunVar<E>::DIET;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *stages = smem;
@@ -211,9 +249,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
             mbar_init(&bars->bfull[i], 1);
             mbar_init(&bars->bempty[i], NEXP);
         }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->sfull[i], NEPI);
+            mbar_init(&bars->sempty[i], 1);
+        }
         mbar_fence_init();
     }
     if (threadIdx.x < kMaxSeq) bars->gmask[threadIdx.x] = s.gmask[threadIdx.x];
+    // DIET: differenced output masks -- parity(count_t) = bit7(S_t) ^ bit7(S_{t-2}) (same
+    // buffer), so plane j = XOR over t of bit7(S_t) * (M_j[t] ^ M_j[t+2]): the bit-7 word of each
+    // drain is folded as it is, with no previous word kept (M_j[t+2] = 0 past the buffer's last
+    // group); the per-plane all-ones / zero selectors of each group in a table
+    uint32_t *selt = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(bars) + BARS_BYTES +
+                                                  STAGE_OUT_BYTES + STAGE_OLD_BYTES);
+    if constexpr (DIET)
+        for (int i = threadIdx.x; i < s.ngrp * SEL_EP; i += NTHREADS) {
+            const int t = i / SEL_EP, j = i - t * SEL_EP;
+            const uint32_t m = s.gmask[t] ^ (t + 2 < s.ngrp ? s.gmask[t + 2] : 0u);
+            selt[i] = j < E ? 0u - ((m >> j) & 1u) : 0u;
+        }
     if (warp == MMA_WARP) tmem_alloc2(&bars->tmem_base, 512);
     tc_fence_before();
     __syncthreads();
@@ -373,11 +427,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         const int64_t nw = words_for(a.n);
         const uint32_t tempty_leader = mapa(smem_u32(&bars->tempty[0]), 0);
         const uint32_t lq = (uint32_t)(q * 32) << 16;
+        // 2^25, opaque to ptxas (bars->tmem_base is a multiple of 2^16 with lane 0, column < 512)
+        const uint32_t m25 = (bars->tmem_base & 0x1000000u) | 0x2000000u;
+        (void)m25;
         uint32_t *stage_out = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(bars) + BARS_BYTES);
         uint64_t *stage_old = reinterpret_cast<uint64_t *>(stage_out + E * BM * 6);
         const uint64_t *stage_out64 = reinterpret_cast<const uint64_t *>(stage_out);
         constexpr int NOUT = E * BM * 3;  // 64-bit output words per CTA and tile
-        uint32_t pc[CH], po[CH];          // previous parity words: current buffer / the other buffer
+        uint32_t pc[CH], po[CH];  // !DIET: previous parity words: current buffer / the other buffer
 #pragma unroll
         for (int c = 0; c < CH; ++c) pc[c] = po[c] = 0;
         int64_t gp = 0;
@@ -396,7 +453,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
             int64_t tm, tn;
             tile_coords(tile, tiles_m, tiles_n, tm, tn);
             const int64_t m0 = tm * (2 * BM) + (int64_t)rank * BM, n0w = tn * (BN / 64);
-            if (a.accumulate) {  // C0 of the words this thread writes out, into shared memory
+            if (!STW && a.accumulate) {  // C0 of the words this thread writes out, into shared memory
                 for (int idx = et; idx < NOUT; idx += NEPI * 32) {
                     bool ok;
                     const uint64_t *src = out_ptr(idx, m0, n0w, ok);
@@ -422,12 +479,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                 const uint32_t ta = tmem + lq + (b ? ACC1 : 0u) + (uint32_t)(h * (CH * 32));
                 const bool last = t + 2 >= s.ngrp;  // this buffer's last group in the tile
                 uint32_t sel[E];  // all-ones for the output planes this product folds into
+                if constexpr (DIET) {
+                    const uint4 *sp = reinterpret_cast<const uint4 *>(selt + t * SEL_EP);
 #pragma unroll
-                for (int j = 0; j < E; ++j) sel[j] = 0u - ((mask >> j) & 1u);
+                    for (int j4 = 0; j4 < (E + 3) / 4; ++j4) {
+                        const uint4 q4 = sp[j4];
+                        const uint32_t qq[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (4 * j4 + u < E) sel[4 * j4 + u] = qq[u];
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < E; ++j) sel[j] = 0u - ((mask >> j) & 1u);
+                }
                 auto fold = [&](int c, uint32_t w) {
-                    const uint32_t pw = w ^ pc[c];
-                    pc[c] = po[c];
-                    po[c] = last ? 0u : w;
+                    uint32_t pw = w;  // DIET: differenced masks, the bit-7 word as it is
+                    if constexpr (!DIET) {
+                        pw = w ^ pc[c];
+                        pc[c] = po[c];
+                        po[c] = last ? 0u : w;
+                    }
 #pragma unroll
                     for (int j = 0; j < E; ++j) acc[j][c] ^= pw & sel[j];
                 };
@@ -443,9 +515,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                     st32_const(ta, RUN_INIT);
                     st32_const(ta + 32, RUN_INIT);
                 }
-                const uint32_t w0 = parity_word_tree(v[0]);  // bit 7 of each cell
+                const uint32_t w0 = PARITY_WORD(v[0]);  // bit 7 of each cell
                 tmem_ld32_pack16(ta + 64, v[0]);
-                const uint32_t w1 = parity_word_tree(v[1]);
+                const uint32_t w1 = PARITY_WORD(v[1]);
                 if constexpr (E > 4) {  // registers: fold before the hand-off
                     fold(0, w0);
                     fold(1, w1);
@@ -471,7 +543,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                     fold(0, w0);         // this accumulator meanwhile)
                     fold(1, w1);
                 }
-                fold(2, parity_word_tree(v[0]));
+                fold(2, PARITY_WORD(v[0]));
 #if GF2E_INSTR
                 i_e[0] += (unsigned long long)(i_e1 - i_d0);
                 i_e[1] += (unsigned long long)(i_e2 - i_e1);
@@ -486,6 +558,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
 #if GF2E_INSTR
             const long long i_s0 = clock64();
 #endif
+            if constexpr (STW) {  // stage buffer ti & 1 -> the store warp (it freed the buffer after tile ti - 2)
+                const int sb = (int)(ti & 1);
+                if (ti >= 2) mbar_wait(&bars->sempty[sb], (uint32_t)(((ti >> 1) - 1) & 1));
+                uint32_t *so = stage_out + sb * (kMaxE * BM * 6);
+#pragma unroll
+                for (int j = 0; j < E; ++j)
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) so[(j * BM + r_cta) * 6 + h * CH + c] = acc[j][c];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->sfull[sb]);
+            } else {
             // stage: row r_cta's 96 columns of each plane -> stage_out[j][r][h*3 .. h*3+2]
             named_bar_sync(1, NEPI * 32);  // the previous tile's copy-out has read stage_out
 #pragma unroll
@@ -498,6 +581,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                 bool ok;
                 uint64_t *dst = out_ptr(idx, m0, n0w, ok);
                 if (ok) *dst = stage_out64[idx] ^ (a.accumulate ? stage_old[idx] : 0ull);
+            }
             }
 #if GF2E_INSTR
             i_store += (unsigned long long)(clock64() - i_s0);
@@ -512,6 +596,49 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
             for (int i = 0; i < 5; ++i) g_instr_run[blockIdx.x][16 + i] = i_e[i];
         }
 #endif
+    } else if (warp == STORE_WARP) {
+        if constexpr (STW) {
+        // ===================== store warp =====================
+        // Per tile: wait for the 8 epilogue warps' staged words (buffer ti & 1), write them out
+        // as 64-bit row segments XORed with C0 (addmul; read here, 16 words in flight per lane),
+        // free the buffer.
+        const int64_t nw = words_for(a.n);
+        constexpr int NOUT = E * BM * 3, BUFW = kMaxE * BM * 3;  // words per tile / per buffer
+        const uint64_t *stage64 = reinterpret_cast<const uint64_t *>(reinterpret_cast<uint8_t *>(bars) + BARS_BYTES);
+        auto word_ptr = [&](int idx, int64_t m0, int64_t n0w, bool &ok) -> uint64_t * {
+            const int j = idx / (BM * 3), rem = idx - j * (BM * 3), r = rem / 3, w = rem - r * 3;
+            const int64_t row = m0 + r, gw = n0w + w;
+            ok = row < a.m && gw < nw;
+            return a.C + j * a.c_pstride + row * a.ldc + gw;
+        };
+        for (int64_t ti = 0; ti < my_tiles; ++ti) {
+            int64_t tm, tn;
+            tile_coords(cluster + ti * nclusters, tiles_m, tiles_n, tm, tn);
+            const int64_t m0 = tm * (2 * BM) + (int64_t)rank * BM, n0w = tn * (BN / 64);
+            const int sb = (int)(ti & 1);
+            mbar_wait_sleep(&bars->sfull[sb], (uint32_t)((ti >> 1) & 1), 64);
+            const uint64_t *so = stage64 + sb * BUFW;
+            constexpr int U = 16;
+            for (int i0 = lane; i0 < NOUT; i0 += 32 * U) {
+                uint64_t v[U];
+                uint64_t *dst[U];
+                bool ok[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int idx = i0 + 32 * u;
+                    dst[u] = word_ptr(idx, m0, n0w, ok[u]);
+                    ok[u] = ok[u] && idx < NOUT;
+                    v[u] = 0ull;
+                    if (a.accumulate && ok[u]) v[u] = *dst[u];
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (ok[u]) *dst[u] = v[u] ^ so[i0 + 32 * u];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->sempty[sb]);
+        }
+        }
     } else if (warp == MMA_WARP && rank == 0) {
         // ===================== MMA issuer (leader CTA) =====================
         const bool issuer = elect_one();
