@@ -78,6 +78,13 @@ static_assert(ATM0 + 32 * S <= SFA, "TMEM: A stages overlap the scale factors");
 // i.e. ceil(K/2) * k < 65536 (host: kRunMaxSum)
 constexpr uint32_t RUN_INIT = 0x47800000u;
 constexpr uint32_t SF_ONE = 0x7F7F7F7Fu;               // E8M0 1.0
+// Paired drains (PR, E <= 8 at k <= 256): two groups share one accumulator fill, the second one
+// scaled by 2^11 through its A scale factors (TMEM columns SFA2..SFA2+7, E8M0 2^11).  The
+// accumulators start at 2^23 (ulp 1), so a cell's running sum is F0 + 2^11 F1 with F0, F1 the
+// running sums of the two fields' counts, exact while F0 < 2^11 and the total < 2^23 (host:
+// run_pair_ok); the parities are bits 0 and 11 of the low 16 bits, i.e. one TMEM drain and one
+// hand-off serve two products
+constexpr uint32_t PAIR_INIT = 0x4B000000u, SF_2P11 = 0x8A8A8A8Au, SFA2 = 488;
 constexpr int CH = BN / (NEPI / 4) / 32;               // 32-column chunks per epilogue thread
 constexpr int GROUP_M = 8;
 constexpr int BARS_BYTES = 1024;
@@ -215,7 +222,7 @@ __device__ __forceinline__ void mma2_mxf4_ts(uint32_t d, uint32_t at, uint64_t b
         : "memory");
 }
 
-template <int E, bool BPRE>
+template <int E, bool BPRE, bool PR>
 __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, const TcArgs a) {
     constexpr int BITS_B = RunMem<BPRE>::BITS_B, BITS_BYTES = RunMem<BPRE>::BITS_BYTES;
     constexpr bool STW = RunVar<E>::STW, DIET = RunVar<E>::DIET;
@@ -262,7 +269,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
     // group); the per-plane all-ones / zero selectors of each group in a table
     uint32_t *selt = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(bars) + BARS_BYTES +
                                                   STAGE_OUT_BYTES + STAGE_OLD_BYTES);
-    if constexpr (DIET)
+    if constexpr (PR) {  // drain d: field 0 = group 2d, field 1 = group 2d + 1 (differenced per field)
+        const int nd = (s.ngrp + 1) / 2;
+        auto gm = [&](int g) -> uint32_t { return g < s.ngrp ? (uint32_t)s.gmask[g] : 0u; };
+        for (int i = threadIdx.x; i < nd * 2 * SEL_EP; i += NTHREADS) {
+            const int d = i / (2 * SEL_EP), r = i - d * (2 * SEL_EP), f = r / SEL_EP, j = r - f * SEL_EP;
+            const uint32_t m = gm(2 * d + f) ^ (d + 2 < nd ? gm(2 * d + 4 + f) : 0u);
+            selt[i] = j < E ? 0u - ((m >> j) & 1u) : 0u;
+        }
+    } else if constexpr (DIET)
         for (int i = threadIdx.x; i < s.ngrp * SEL_EP; i += NTHREADS) {
             const int t = i / SEL_EP, j = i - t * SEL_EP;
             const uint32_t m = s.gmask[t] ^ (t + 2 < s.ngrp ? s.gmask[t + 2] : 0u);
@@ -277,7 +292,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         // scale factors (every byte E8M0 1.0) and both running-sum accumulators at 65536
         const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
         st32_const(tmem + lb + SFA, SF_ONE);
-        for (int c = 0; c < 2 * BN; c += 32) st32_const(tmem + lb + c, RUN_INIT);
+        if constexpr (PR)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(tmem + lb + SFA2),
+                         "r"(SF_2P11)
+                         : "memory");
+        for (int c = 0; c < 2 * BN; c += 32) st32_const(tmem + lb + c, PR ? PAIR_INIT : RUN_INIT);
         wait_st();
     }
     tc_fence_before();
@@ -468,6 +487,66 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
             for (int j = 0; j < E; ++j)
 #pragma unroll
                 for (int c = 0; c < CH; ++c) acc[j][c] = 0;
+            if constexpr (PR) {
+                // paired drains: per 32-column chunk two parity words, bit 0 (field 0: group 2d)
+                // and bit 11 (field 1: group 2d + 1) of each cell's low 16 bits, folded with the
+                // differenced per-field masks of the selector table (no previous words kept)
+                const int nd = (s.ngrp + 1) / 2;
+                for (int d = 0; d < nd; ++d, ++gp) {
+                    const int b = (int)(gp & 1);
+                    TWR(i_tfull, mbar_wait(&bars->tfull[b], (uint32_t)((gp >> 1) & 1)));
+#if GF2E_INSTR
+                    const long long i_d0 = clock64();
+#endif
+                    tc_fence_after();
+                    const uint32_t ta = tmem + lq + (b ? ACC1 : 0u) + (uint32_t)(h * (CH * 32));
+                    const bool last = d + 2 >= nd;  // this buffer's last drain in the tile
+                    uint32_t sel0[E], sel1[E];
+                    {
+                        const uint4 *sp = reinterpret_cast<const uint4 *>(selt + d * 2 * SEL_EP);
+#pragma unroll
+                        for (int j4 = 0; j4 < (E + 3) / 4; ++j4) {
+                            const uint4 q0 = sp[j4], q1 = sp[SEL_EP / 4 + j4];
+                            const uint32_t a0[4] = {q0.x, q0.y, q0.z, q0.w}, a1[4] = {q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                if (4 * j4 + u < E) {
+                                    sel0[4 * j4 + u] = a0[u];
+                                    sel1[4 * j4 + u] = a1[u];
+                                }
+                        }
+                    }
+                    auto fold2 = [&](int c, const uint32_t (&vv)[16]) {
+                        const uint32_t w0 = parity_word_packed_shl<7, 0xECA8>(vv);
+                        const uint32_t w1 = parity_word_packed_shl<4, 0xFDB9>(vv);
+#pragma unroll
+                        for (int j = 0; j < E; ++j) acc[j][c] ^= (w0 & sel0[j]) ^ (w1 & sel1[j]);
+                    };
+                    uint32_t v[2][16];
+                    tmem_ld32_pack16(ta, v[0]);
+                    tmem_ld32_pack16(ta + 32, v[1]);
+                    tmem_wait_ld();
+                    if (last) {
+                        st32_const(ta, PAIR_INIT);
+                        st32_const(ta + 32, PAIR_INIT);
+                    }
+                    fold2(0, v[0]);
+                    tmem_ld32_pack16(ta + 64, v[0]);
+                    fold2(1, v[1]);
+                    tmem_wait_ld();
+                    if (last) {
+                        st32_const(ta + 64, PAIR_INIT);
+                        wait_st();
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(b * 8));
+                    fold2(2, v[0]);
+#if GF2E_INSTR
+                    i_drain += (unsigned long long)(clock64() - i_d0);
+#endif
+                }
+            } else
             for (int t = 0; t < s.ngrp; ++t, ++gp) {  // one drain per group
                 const int b = (int)(gp & 1);
                 const uint32_t mask = bars->gmask[t];
@@ -655,20 +734,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(i_g0));
 #endif
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
-            for (int t = 0; t < s.ngrp; ++t, ++gp) {  // group t: its entries into one accumulator
+            // drain unit: one group, or (PR) groups 2d and 2d + 1, the second one's entries with the
+            // 2^11 A scale factors
+            constexpr int GPD = PR ? 2 : 1;
+            for (int t0 = 0; t0 < s.ngrp; t0 += GPD, ++gp) {
                 const int b = (int)(gp & 1);
                 TWR(i_tempty, mbar_wait(&bars->tempty[b], (uint32_t)((gp >> 1) & 1) ^ 1));
                 tc_fence_after();
                 const uint32_t dt = tmem + (b ? ACC1 : 0u);
-                for (int ks = 0; ks < nks * s.gsize[t]; ++ks) {
+                const int n0 = nks * s.gsize[t0], nall = n0 + ((PR && t0 + 1 < s.ngrp) ? nks * s.gsize[t0 + 1] : 0);
+                for (int ks = 0; ks < nall; ++ks) {
                     TWR(i_full, mbar_wait(&bars->full[st], phase));
                     tc_fence_after();
                     const uint32_t sb = st0 + (uint32_t)(st * B_BYTES);
+                    const uint32_t sfa = tmem + ((PR && ks >= n0) ? SFA2 : SFA);
                     if (issuer) {
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
                             mma2_mxf4_ts(dt, tmem + ATM0 + (uint32_t)(st * 32 + kk * 8), umma_desc_sw128(sb + kk * 32),
-                                         idesc, tmem + SFA, tmem + SFB);
+                                         idesc, sfa, tmem + SFB);
                         mma2_commit_both(&bars->empty[st]);
                     }
                     __syncwarp();
@@ -676,6 +760,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
                         st = 0;
                         phase ^= 1;
                     }
+
                 }
                 if (issuer) mma2_commit_both(&bars->tfull[b]);
                 __syncwarp();
@@ -705,14 +790,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
 
 int g_num_sms_run = 0;
 
-template <int E, bool BP>
+template <int E, bool BP, bool PR>
 cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
     static bool attr_set[kMaxDevices] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= kMaxDevices || !attr_set[dev]) {
         cudaError_t err =
-            cudaFuncSetAttribute(k_product_run<E, BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+            cudaFuncSetAttribute(k_product_run<E, BP, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         if (err != cudaSuccess) return err;
         if (dev < kMaxDevices) attr_set[dev] = true;
     }
@@ -735,14 +820,39 @@ cudaError_t launch_e(const Sched &s, const TcArgs &a, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_product_run<E, BP>, s, a);
+    return cudaLaunchKernelEx(&cfg, k_product_run<E, BP, PR>, s, a);
 }
 
 }  // namespace
 
+// paired drains (PR): per accumulator buffer and tile, the field-0 counts must stay below 2^11
+// and F0 + 2^11 F1 below 2^23 (every count <= k_pad).  Used for the degrees in the bit mask
+// GF2E_RUN_PAIR_E (default e = 3..6, where it measured faster: config 4 e=3 4.70 -> 4.24 ms,
+// e=4 6.73 -> 6.61, e=6 11.81 -> 11.44; at e = 2, 7, 8 slower, profiles/r02/run_variants.txt)
+bool run_pair_ok(const Sched &s, int64_t kpad) {
+    static const unsigned emask = getenv("GF2E_RUN_PAIR_E") ? (unsigned)strtoul(getenv("GF2E_RUN_PAIR_E"), nullptr, 0)
+                                                            : 0x78u;
+    if (s.nout > 8 || !((emask >> s.nout) & 1u) || s.ngrp < 2) return false;
+    int64_t f0[2] = {0, 0}, f1[2] = {0, 0};
+    for (int d = 0; 2 * d < s.ngrp; ++d) {
+        f0[d & 1] += s.gsize[2 * d];
+        if (2 * d + 1 < s.ngrp) f1[d & 1] += s.gsize[2 * d + 1];
+    }
+    for (int b = 0; b < 2; ++b)
+        if (f0[b] * kpad >= 2048 || f1[b] * kpad * 2048 + f0[b] * kpad >= (int64_t(1) << 23)) return false;
+    return true;
+}
+
+template <int E, bool BP>
+cudaError_t launch_ep(const Sched &s, const TcArgs &a, cudaStream_t st) {
+    if constexpr (E <= 8)
+        if (run_pair_ok(s, a.kwords * 64)) return launch_e<E, BP, true>(s, a, st);
+    return launch_e<E, BP, false>(s, a, st);
+}
+
 cudaError_t launch_product_run(const Sched &s, const TcArgs &a, cudaStream_t st, bool bpre) {
 #define RUN_E(EE) \
-    case EE: return bpre ? launch_e<EE, true>(s, a, st) : launch_e<EE, false>(s, a, st);
+    case EE: return bpre ? launch_ep<EE, true>(s, a, st) : launch_ep<EE, false>(s, a, st);
     switch (s.nout) {
         RUN_E(1) RUN_E(2) RUN_E(3) RUN_E(4) RUN_E(5) RUN_E(6) RUN_E(7) RUN_E(8) RUN_E(9) RUN_E(10)
         default: return cudaErrorInvalidValue;

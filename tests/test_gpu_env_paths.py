@@ -1,7 +1,8 @@
 """Code paths that environment switches select at process start (read once per process, so
 each runs in a fresh interpreter): the running-sum form's drain grouping (GF2E_RUN_DRAINS),
 the consumers without programmatic dependent launch (GF2E_PDL=0), the small-product
-crossover of PLE / TRSM (GF2E_NJS_MAXK=0: every update on the tensor cores).  Each child
+crossover of PLE / TRSM (GF2E_NJS_MAXK=0: every update on the tensor cores), the paired drains
+of the running-sum form (GF2E_RUN_PAIR_E).  Each child
 compares its results with the oracle / with the default path computed here."""
 
 import json
@@ -92,3 +93,38 @@ def test_consumers_without_pdl_and_small_products_match(tmp_path):
         got = np.load(alt)
         for key in ref.files:
             assert np.array_equal(ref[key], got[key]), (env, key)
+
+
+CHILD_RUN_ALL_E = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1111_6900_b200 as g, oracle
+out = {}
+for e in range(2, 11):
+    ctx = g.field_new(e)
+    for (m, k, n, acc) in ((520, 256, 700, True), (300, 64, 260, False), (2100, 130, 450, True)):
+        A = oracle.sliced_random(e, m, k, 1)
+        B = oracle.sliced_random(e, k, n, 2)
+        C0 = oracle.sliced_random(e, m, n, 3)
+        ref, _ = oracle.karatsuba(e, ctx.f, A, B, m, k, n)
+        C = g.SlicedMatrix.from_numpy(ctx, C0.copy(), n)
+        if acc:
+            g.addmul(C, g.SlicedMatrix.from_numpy(ctx, A, k), g.SlicedMatrix.from_numpy(ctx, B, n), backend="tc_run")
+            ref = ref ^ C0
+        else:
+            C = g.karatsuba_mul(g.SlicedMatrix.from_numpy(ctx, A, k), g.SlicedMatrix.from_numpy(ctx, B, n),
+                                backend="tc_run")
+        out[f"{e}/{m}x{k}x{n}"] = bool(np.array_equal(C.to_numpy(), ref))
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("pair_e", ["0x1fc", "0"])
+def test_run_form_paired_drains_parity(pair_e):
+    # the paired-drain running-sum form (two groups per accumulator fill, the second scaled by
+    # 2^11) forced on for every e <= 8 where its sums stay exact, and forced off: bit-exact
+    # with the oracle for every e, mul and addmul, in-kernel and pre-expanded B (m > 2048)
+    out = json.loads(_run(CHILD_RUN_ALL_E, {"GF2E_RUN_PAIR_E": pair_e}).strip().splitlines()[-1])
+    bad = [key for key, ok in out.items() if not ok]
+    assert not bad, (pair_e, bad)

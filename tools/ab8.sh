@@ -1,0 +1,6 @@
+O=gpurun_out/ab8; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_env_paths.py -x -q -k paired 2>&1 | tail -2 > $O/pytest_pair.txt; cat $O/pytest_pair.txt
+timeout 900 python -m pytest tests -m gpu -x -q -k "run or config4 or fuzz or selfcheck or fp4" 2>&1 | tail -2 > $O/pytest.txt; cat $O/pytest.txt
+for e in 2 3 4 5 6 7 8 9 10; do
+ timeout 300 python bench.py --config 4 --e $e --no-e2e --steps 10 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('head', d['config']['workload'][:20], d['ms_per_step'], d['value'], d['roofline']['frac'], d.get('parity',{}).get('device'))"
+done 2>&1 | tee $O/ab.txt
