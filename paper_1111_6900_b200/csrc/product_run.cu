@@ -35,6 +35,9 @@
 //       C0 read by that warp) while the epilogue warps drain the next tile; for E >= the knob
 //  DIET: differenced output masks (no previous parity words kept), the parity word packed with
 //       IMAD.HI on the FMA pipe, plane selectors read from a shared table; for E >= the knob
+#ifndef GF2E_RUN_REINIT_EVERY_TILE  // 1: reset the running sums at every tile (the round-2 form)
+#define GF2E_RUN_REINIT_EVERY_TILE 0
+#endif
 #ifndef GF2E_RUN_STW_MIN_E
 #define GF2E_RUN_STW_MIN_E 7
 #endif
@@ -457,6 +460,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
 #pragma unroll
         for (int c = 0; c < CH; ++c) pc[c] = po[c] = 0;
         int64_t gp = 0;
+        const int64_t sum_tile = (int64_t)(s.run_load > 0 ? s.run_load : 1) * a.kwords * 64;
+        const int64_t reinit_tiles =
+            (DIET || PR || GF2E_RUN_REINIT_EVERY_TILE) ? 1 : ((kRunMaxSum - 1) / sum_tile > 0 ? (kRunMaxSum - 1) / sum_tile : 1);
         unsigned long long i_tfull = 0, i_drain = 0, i_store = 0, i_e[5] = {0, 0, 0, 0, 0};
         const long long i_t0 = clock64();
         (void)i_tfull, (void)i_drain, (void)i_store, (void)i_t0, (void)i_e;
@@ -487,6 +493,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
             for (int j = 0; j < E; ++j)
 #pragma unroll
                 for (int c = 0; c < CH; ++c) acc[j][c] = 0;
+            // The running sums continue across tiles (the previous parity words pc / po are kept
+            // per thread, which drains the same TMEM cells in every tile) and are re-initialised
+            // only every reinit_tiles tiles, as late as exactness allows: a buffer takes at most
+            // run_load entries of <= k_pad counts per tile.  (DIET's differenced masks and the
+            // paired drains assume a reset per tile.)
+            const bool reinit = (ti + 1) % reinit_tiles == 0 || ti + 1 == my_tiles;
             if constexpr (PR) {
                 // paired drains: per 32-column chunk two parity words, bit 0 (field 0: group 2d)
                 // and bit 11 (field 1: group 2d + 1) of each cell's low 16 bits, folded with the
@@ -556,7 +568,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
 #endif
                 tc_fence_after();
                 const uint32_t ta = tmem + lq + (b ? ACC1 : 0u) + (uint32_t)(h * (CH * 32));
-                const bool last = t + 2 >= s.ngrp;  // this buffer's last group in the tile
+                // this buffer's last group before a re-initialisation (every reinit_tiles tiles)
+                const bool last = t + 2 >= s.ngrp && reinit;
                 uint32_t sel[E];  // all-ones for the output planes this product folds into
                 if constexpr (DIET) {
                     const uint4 *sp = reinterpret_cast<const uint4 *>(selt + t * SEL_EP);
