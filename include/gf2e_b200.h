@@ -39,8 +39,11 @@ extern "C" {
 
 /* gf2e_slice_mul flags */
 #define GF2E_ACCUMULATE 1u   /* C ^= A*B (addmul) instead of C = A*B              */
-#define GF2E_BACKEND_TC 0u   /* K4 on tcgen05 tensor cores (default): kind::mxf4 (e2m1 0/1,
-                                exact fp32 accumulation) for k >= 2048, kind::i8 below      */
+#define GF2E_BACKEND_TC 0u   /* K4 on tcgen05 tensor cores (default), all kind::mxf4 (e2m1
+                                0/1, exact fp32 accumulation) unless the device's fp4 self-
+                                check failed: the long-k form for k >= 8192, the fp4 form for
+                                k >= 2048, the running-sum form below while its sums stay
+                                exact, kind::i8 past that bound                             */
 #define GF2E_BACKEND_M4RM 2u /* K4 as M4RM Gray tables in shared memory (INT pipe) */
 #define GF2E_TC_INT8 4u      /* tensor-core K4 forced to kind::i8 at every k                */
 #define GF2E_TC_FP4 8u       /* tensor-core K4 forced to kind::mxf4 at every k (paired form
