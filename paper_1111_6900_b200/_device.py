@@ -13,9 +13,15 @@ import numpy as np
 import torch
 
 
+_CUDA_CHECKED = False
+
+
 def require_cuda() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_1111_6900_b200 needs a CUDA (sm_100) device; there is no CPU fallback")
+    global _CUDA_CHECKED
+    if not _CUDA_CHECKED:  # once per process (the per-call check was a measurable host cost)
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1111_6900_b200 needs a CUDA (sm_100) device; there is no CPU fallback")
+        _CUDA_CHECKED = True
     return torch.device("cuda", torch.cuda.current_device())
 
 
@@ -56,11 +62,11 @@ class _Workspace(threading.local):
     def __init__(self):
         self.bufs: dict[tuple[int, int], torch.Tensor] = {}
 
-    def get(self, nbytes: int) -> torch.Tensor:
+    def get(self, nbytes: int, stream: int | None = None) -> torch.Tensor:
         dev = require_cuda()
         if nbytes > WORKSPACE_KEEP:
             return torch.empty(nbytes, dtype=torch.uint8, device=dev)
-        key = (dev.index, stream_handle())
+        key = (dev.index, stream_handle() if stream is None else stream)
         buf = self.bufs.get(key)
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)

@@ -617,9 +617,13 @@ int run_product(const Sched &ks, const uint64_t *A, int64_t lda, int64_t pa, con
     uint64_t *Bx = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + L.a_bytes);
     // tensor-core forms: the B^T combinations run beside the A combinations on a side stream
     // (fork / join by events): two small independent kernels, latency-bound at small sizes
+    // (below GF2E_FORK_MIN_BITS operand bits the fork's four event calls cost the host more
+    // than the overlap saves the device; default 0: always fork)
+    static const int64_t fork_min = getenv("GF2E_FORK_MIN_BITS") ? atoll(getenv("GF2E_FORK_MIN_BITS")) : 0;
     SideStream no_side;
-    SideStream &side = tc ? side_stream() : no_side;
-    const bool forked = tc && side.s;
+    const bool want_fork = tc && m * k + k * n >= fork_min;
+    SideStream &side = want_fork ? side_stream() : no_side;
+    const bool forked = want_fork && side.s;
     if (forked) {
         CKH(cudaEventRecord(side.fork, st), "cudaEventRecord");
         CKH(cudaStreamWaitEvent(side.s, side.fork, 0), "cudaStreamWaitEvent");

@@ -122,11 +122,11 @@ def _slice_mul(A: SlicedMatrix, B: SlicedMatrix, C: SlicedMatrix, accumulate: bo
     ws_bytes = int(L.gf2e_slice_mul_workspace(ctx.e, ctx.f, m, k, n, flags))
     if ws_bytes < 0:
         _lib.check(_lib.GF2E_EINVAL, "gf2e_slice_mul_workspace")
-    ws = _device.workspace.get(ws_bytes)
+    stream = _device.stream_handle()
+    ws = _device.workspace.get(ws_bytes, stream)
     lda, ldb, ldc = A.planes.shape[2], B.planes.shape[2], C.planes.shape[2]
     _lib.call("gf2e_slice_mul", ctx.e, ctx.f, _device.ptr(A.planes), lda, m * lda, _device.ptr(B.planes), ldb,
-              k * ldb, _device.ptr(C.planes), ldc, m * ldc, m, k, n, flags, ws.data_ptr(), ws.numel(),
-              _device.stream_handle())
+              k * ldb, _device.ptr(C.planes), ldc, m * ldc, m, k, n, flags, ws.data_ptr(), ws.numel(), stream)
 
 
 def karatsuba_mul(A: SlicedMatrix, B: SlicedMatrix, counters: MulCounters | None = None,
