@@ -1,0 +1,7 @@
+O=gpurun_out/ab13; mkdir -p $O
+timeout 1200 python -m pytest tests -m gpu -x -q -k "run or config4 or fuzz or plane or gf2 or paired or config1" 2>&1 | tail -2 > $O/pytest.txt; cat $O/pytest.txt
+for r in 1 2; do for V in pf0 default; do
+  L=paper_1111_6900_b200/libgf2e_b200.so; [ $V = pf0 ] && L=build/variants/lib_pf0.so
+  GF2E_LIB_PATH=$L timeout 300 python bench.py --config 4 --e 2 --no-e2e --steps 10 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('$V', d['config']['workload'][:20], d['ms_per_step'], d['value'], d['roofline']['frac'], d.get('parity',{}).get('device'))"
+  GF2E_LIB_PATH=$L timeout 300 python bench.py --config 1 --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('$V', d['config']['workload'][:20], d['ms_per_step'], d['value'], d['roofline']['kernel_ms'], d.get('parity',{}).get('device'))"
+done; done 2>&1 | tee $O/ab.txt
