@@ -44,9 +44,20 @@
 #ifndef GF2E_RUN_DIET_MIN_E
 #define GF2E_RUN_DIET_MIN_E 11
 #endif
+// Tile raster: groups of GROUP_M row tiles walk all column tiles.  The pre-expanded B^T of a
+// config-4 product (e = 8: 27 x 342 column tiles x 24 KiB = 221 MB) does not fit the L2, so it
+// streams from DRAM once per row group: wider groups re-read it less (e = 8: 8 -> 24 rows,
+// 15.93 -> 14.85 ms, profiles/r02/run_variants.txt); for small e the narrow raster measured best
+#ifndef GF2E_RUN_GROUP_M_SMALL
+#define GF2E_RUN_GROUP_M_SMALL 8
+#endif
+#ifndef GF2E_RUN_GROUP_M_LARGE
+#define GF2E_RUN_GROUP_M_LARGE 24
+#endif
 template <int E>
 struct RunVar {
     static constexpr bool STW = E >= GF2E_RUN_STW_MIN_E, DIET = E >= GF2E_RUN_DIET_MIN_E;
+    static constexpr int GM = E >= 7 ? GF2E_RUN_GROUP_M_LARGE : GF2E_RUN_GROUP_M_SMALL;  // raster rows
 };
 
 namespace gf2e {
@@ -89,7 +100,6 @@ constexpr uint32_t SF_ONE = 0x7F7F7F7Fu;               // E8M0 1.0
 // hand-off serve two products
 constexpr uint32_t PAIR_INIT = 0x4B000000u, SF_2P11 = 0x8A8A8A8Au, SFA2 = 488;
 constexpr int CH = BN / (NEPI / 4) / 32;               // 32-column chunks per epilogue thread
-constexpr int GROUP_M = 8;
 constexpr int BARS_BYTES = 1024;
 // epilogue staging (per CTA and tile): the E x 128 x 192-bit output words and their C0
 // epilogue staging (per CTA and tile): the E x 128 x 192-bit output words and their C0
@@ -127,6 +137,7 @@ struct __align__(8) Bars {
 };
 static_assert(sizeof(Bars) <= BARS_BYTES, "barrier block");
 
+template <int GROUP_M>
 __device__ __forceinline__ void tile_coords(int64_t tile, int64_t tiles_m, int64_t tiles_n, int64_t &tm,
                                             int64_t &tn) {
     const int64_t per_group = (int64_t)GROUP_M * tiles_n;
@@ -399,7 +410,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             const int64_t tile = cluster + ti * nclusters;
             int64_t tm, tn;
-            tile_coords(tile, tiles_m, tiles_n, tm, tn);
+            tile_coords<RunVar<E>::GM>(tile, tiles_m, tiles_n, tm, tn);
             const int64_t rbA = tm * 2 + rank, rbB = tn * 2 + rank;
             for (int i = 0; i < s.nseq; ++i) {
                 const int t = s.seq[i];  // entry i of the grouped sequence is product t
@@ -476,7 +487,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             const int64_t tile = cluster + ti * nclusters;
             int64_t tm, tn;
-            tile_coords(tile, tiles_m, tiles_n, tm, tn);
+            tile_coords<RunVar<E>::GM>(tile, tiles_m, tiles_n, tm, tn);
             const int64_t m0 = tm * (2 * BM) + (int64_t)rank * BM, n0w = tn * (BN / 64);
             if (!STW && a.accumulate) {  // C0 of the words this thread writes out, into shared memory
                 for (int idx = et; idx < NOUT; idx += NEPI * 32) {
@@ -705,7 +716,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_product_run(const Sched s, cons
         };
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             int64_t tm, tn;
-            tile_coords(cluster + ti * nclusters, tiles_m, tiles_n, tm, tn);
+            tile_coords<RunVar<E>::GM>(cluster + ti * nclusters, tiles_m, tiles_n, tm, tn);
             const int64_t m0 = tm * (2 * BM) + (int64_t)rank * BM, n0w = tn * (BN / 64);
             const int sb = (int)(ti & 1);
             mbar_wait_sleep(&bars->sfull[sb], (uint32_t)((ti >> 1) & 1), 64);
