@@ -47,9 +47,12 @@
 // Tile raster: groups of GROUP_M row tiles walk all column tiles.  The pre-expanded B^T of a
 // config-4 product (e = 8: 27 x 342 column tiles x 24 KiB = 221 MB) does not fit the L2, so it
 // streams from DRAM once per row group: wider groups re-read it less (e = 8: 8 -> 24 rows,
-// 15.93 -> 14.85 ms, profiles/r02/run_variants.txt); for small e the narrow raster measured best
+// 15.93 -> 14.85 ms, profiles/r02/run_variants.txt); 48 rows at e = 4..6, 8 below
 #ifndef GF2E_RUN_GROUP_M_SMALL
 #define GF2E_RUN_GROUP_M_SMALL 8
+#endif
+#ifndef GF2E_RUN_GROUP_M_MID  // e = 4..6 (e = 4: 6.59 -> 6.44 ms, e = 6: 11.33 -> 11.26)
+#define GF2E_RUN_GROUP_M_MID 48
 #endif
 #ifndef GF2E_RUN_GROUP_M_LARGE
 #define GF2E_RUN_GROUP_M_LARGE 24
@@ -57,7 +60,9 @@
 template <int E>
 struct RunVar {
     static constexpr bool STW = E >= GF2E_RUN_STW_MIN_E, DIET = E >= GF2E_RUN_DIET_MIN_E;
-    static constexpr int GM = E >= 7 ? GF2E_RUN_GROUP_M_LARGE : GF2E_RUN_GROUP_M_SMALL;  // raster rows
+    static constexpr int GM = E >= 7   ? GF2E_RUN_GROUP_M_LARGE
+                              : E >= 4 ? GF2E_RUN_GROUP_M_MID
+                                       : GF2E_RUN_GROUP_M_SMALL;  // raster rows
 };
 
 namespace gf2e {
