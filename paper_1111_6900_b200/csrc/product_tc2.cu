@@ -106,7 +106,10 @@ constexpr uint32_t IDLE_SLEEP_NS = GF2E_IDLE_SLEEP_NS;  // epilogue (long k only
 // (A and B^T rows) and 8 epilogue warps (lane quarter x column half).
 constexpr int NPW = 4;  // expander warps (non-split forms)
 constexpr int NEW = 8;  // epilogue warps (non-split forms)
-constexpr int GROUP_M = 8;  // tile rasterisation: row-tiles per column sweep (L2 reuse)
+#ifndef GF2E_TC2_GROUP_M
+#define GF2E_TC2_GROUP_M 8
+#endif
+constexpr int GROUP_M = GF2E_TC2_GROUP_M;  // tile rasterisation: row-tiles per column sweep (L2 reuse)
 constexpr int MMA_WARP = NPW + NEW;
 constexpr int LOAD_WARP = MMA_WARP + 1;
 constexpr int NTHREADS = (NPW + NEW + 2) * 32;
